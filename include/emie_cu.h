@@ -1,0 +1,160 @@
+/* emie_cu.h — C ABI of the B200 (sm_100a) CIE hot path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no
+ * torch or C++ types. Every entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj). The C++ mirror of the
+ * reference API (include/emie/*.hpp, namespace emie) and the Python mirror
+ * (paper_1512_06126_b200) are thin layers over these functions.
+ *
+ * Conventions
+ *  - Complex numbers are interleaved double pairs, layout-compatible with
+ *    std::complex<double> (the reference's cdouble, include/emie/types.hpp:9).
+ *  - Field vectors use the reference GridVector layout
+ *    ((c*nz + iz)*ny + iy)*nx + ix (include/emie/types.hpp:14-30); a batch of
+ *    nrhs fields is nrhs such vectors back to back.
+ *  - "d_" pointers are device pointers (cuda:0 context of the caller),
+ *    "h_" pointers are host pointers.
+ *  - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Status codes map one-to-one onto the reference's exception types
+ *    (SURVEY.md §8(b)): no exception crosses the ABI; the message of the last
+ *    failure on the calling thread is emie_cu_last_error().
+ *  - Every kernel is deterministic (no order-dependent atomics): repeated and
+ *    concurrent calls return bit-identical results (test_toeplitz.cpp:416-434).
+ */
+#ifndef EMIE_CU_H
+#define EMIE_CU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum emie_cu_status {
+  EMIE_CU_OK = 0,
+  EMIE_CU_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  EMIE_CU_DOMAIN_ERROR = 2,     /* std::domain_error */
+  EMIE_CU_OUT_OF_RANGE = 3,     /* std::out_of_range */
+  EMIE_CU_RUNTIME_ERROR = 4,    /* std::runtime_error */
+  EMIE_CU_CUDA_ERROR = 5        /* device failure (no reference equivalent) */
+};
+
+typedef struct emie_cu_operator_s* emie_cu_operator; /* device SpectralOperator */
+typedef struct emie_cu_system_s* emie_cu_system;     /* device SystemOperator */
+
+const char* emie_cu_last_error(void);
+const char* emie_cu_version(void);
+int emie_cu_device_count(int* count);
+
+/* smooth_embedding_size (include/emie/toeplitz.hpp:13, src/toeplitz.cpp:18-26) */
+int emie_cu_smooth_embedding_size(int n, int* out);
+
+/* ---------------------------------------------------------------------
+ * Spectral operator (SpectralOperator, include/emie/toeplitz.hpp:21-35)
+ * ------------------------------------------------------------------- */
+
+/* transform_operator (include/emie/toeplitz.hpp:37, src/toeplitz.cpp:92-161)
+ * from a host compressed operator (CompressedGreensOperator,
+ * include/emie/greens.hpp:74-81): blocks[oi*nx + oj], each block the six
+ * GreensBlock components xx yy zz xy (upper triangles, nz(nz+1)/2 entries,
+ * index tri(k,kp) of greens.hpp:61-65) then xz yz (full nz*nz), i.e.
+ * 2 nz (2 nz + 1) complex per block. The parity-extended 2-D lateral
+ * transforms run on the device; the result stays device-resident. */
+int emie_cu_operator_from_blocks(int nx, int ny, int nz, double omega,
+                                 const double* h_blocks, emie_cu_operator* out,
+                                 void* stream);
+
+/* assemble_operator + transform_operator (include/emie/greens.hpp:144-147,
+ * src/greens.cpp:332-371; toeplitz.cpp:92-161) entirely on the device:
+ * filter design (hankel.cpp:204-281), lambda accumulation of the vertical
+ * moment tables (greens.cpp:150-221, layered.cpp:67-408), spectra.
+ * Model: L interfaces tops[L] (m), L+1 complex conductivities sigma.
+ * Grid: nz intervals breaks[nz+1] (m), nx x ny cells of hx x hy (m).
+ * filter: {step, shift, half, n1, n2} (FilterParams, hankel.hpp:20-26) or
+ * NULL for the defaults. keep_blocks != 0 keeps the compressed blocks on
+ * the device for emie_cu_operator_download_blocks. */
+int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
+                         const double* breaks, int nx, int ny, double hx, double hy,
+                         double omega, const double* filter, int keep_blocks,
+                         emie_cu_operator* out, void* stream);
+
+/* dims = {nx, ny, nz, ex, ey, qx, qy}; omega */
+int emie_cu_operator_dims(emie_cu_operator op, int dims[7], double* omega);
+
+/* SpectralOperator::comp (toeplitz.hpp:58-61): six host arrays written back
+ * to back: comp[c][(my*qx + mx)*nent + s], nent = nz(nz+1)/2 for c < 4 and
+ * nz^2 for c >= 4 (total qx*qy*2nz(2nz+1) complex). */
+int emie_cu_operator_download_spectra(emie_cu_operator op, double* h_comp);
+
+/* compressed blocks in the emie_cu_operator_from_blocks layout; only for
+ * operators built with keep_blocks or from blocks. */
+int emie_cu_operator_download_blocks(emie_cu_operator op, double* h_blocks);
+
+/* filter weights of one offset: w[6][n2-n1+1], lam[n2-n1+1], in the
+ * greens.cpp:137 order (0,0) (2,0) (0,2) (1,1) (1,0) (0,1); hankel.cpp:239-281 */
+int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy,
+                                  const double* filter, double* h_w, double* h_lam);
+
+void emie_cu_operator_destroy(emie_cu_operator op);
+
+/* apply(const SpectralOperator&, const GridVector&) (toeplitz.hpp:43,
+ * src/toeplitz.cpp:163-283) on nrhs device fields; d_out may not alias d_in */
+int emie_cu_apply_spectral(emie_cu_operator op, const double* d_in, double* d_out,
+                           int nrhs, void* stream);
+
+/* ---------------------------------------------------------------------
+ * System operator A = S + R1 B R2 (include/emie/cie.hpp:26-39)
+ * ------------------------------------------------------------------- */
+
+/* build_system (cie.hpp:36-37, src/cie.cpp:24-54): per-cell contrast
+ * coefficients (cie.cpp:9-22) from the host conductivities sigma_a
+ * [(iz*ny + iy)*nx + ix] and sigma_b[iz] (complex) and the cell volumes
+ * volume[iz] = hx*hy*dz (greens.hpp:35). The system references (does not
+ * own) op; op must outlive it (cie.hpp:26-34). */
+int emie_cu_system_create(emie_cu_operator op, const double* h_sigma_a,
+                          const double* h_sigma_b, const double* h_volume,
+                          emie_cu_system* out);
+/* s (complex), r1 (real), r2 (complex) per cell, as SystemOperator holds them */
+int emie_cu_system_download(emie_cu_system sys, double* h_s, double* h_r1, double* h_r2);
+void emie_cu_system_destroy(emie_cu_system sys);
+
+/* apply(const SystemOperator&, const GridVector&) (cie.hpp:39, cie.cpp:56-73) */
+int emie_cu_apply_system(emie_cu_system sys, const double* d_in, double* d_out,
+                         int nrhs, void* stream);
+
+/* same, host buffers in and out: H2D, apply, D2H inside the call (the
+ * reference-facing plugin call; used for the end-to-end measurement) */
+int emie_cu_apply_system_host(emie_cu_system sys, const double* h_in, double* h_out,
+                              int nrhs, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Solve (include/emie/cie.hpp:41-80, src/cie.cpp:117-249)
+ * ------------------------------------------------------------------- */
+
+/* SolveReport (cie.hpp:43-48): status 0 converged, 1 max_iterations,
+ * 2 breakdown (SolveStatus order) */
+typedef struct {
+  int status;
+  int iterations;
+  double residual;
+  int history_len; /* entries written to the history buffer */
+} emie_cu_report;
+
+/* fgmres (cie.hpp:71-72, cie.cpp:117-238) with A = apply(sys, .), no
+ * preconditioner, nrhs independent right-hand sides solved in lockstep
+ * (they share every operator read). d_rhs, d_x: nrhs device fields; reports
+ * nrhs entries; history: nrhs x hist_cap relative residuals (may be NULL). */
+int emie_cu_fgmres(emie_cu_system sys, const double* d_rhs, double* d_x, int nrhs,
+                   double tol, int restart, int max_iters, emie_cu_report* reports,
+                   double* h_history, int hist_cap, void* stream);
+
+/* kernel launches issued by this library on the calling thread since the
+ * last reset (evidence for bench.py's gpu_launches) */
+long long emie_cu_launch_count(void);
+void emie_cu_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EMIE_CU_H */

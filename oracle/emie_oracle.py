@@ -503,3 +503,267 @@ def assemble_operator(grid: Grid, omega):
         for oj in range(grid.nx):
             out[oi, oj] = block_vector(assemble_block(grid, omega, oi, oj, den))
     return out
+
+
+# ------------------------------------------------------- toeplitz / apply ---
+def smooth_embedding_size(n):
+    """src/toeplitz.cpp:18-26."""
+    if n < 1:
+        raise ValueError("smooth_embedding_size: n < 1")
+    c = n
+    while True:
+        r = c
+        for f in (2, 3, 5):
+            while r % f == 0:
+                r //= f
+        if r == 1:
+            return c
+        c += 1
+
+
+def _split_block(vec, nz):
+    nt, nf = ntri(nz), nz * nz
+    o = np.cumsum([0, nt, nt, nt, nt, nf, nf])
+    return [vec[..., o[i]:o[i + 1]] for i in range(6)]
+
+
+def transform_operator(blocks, nx, ny, nz):
+    """src/toeplitz.cpp:92-161: blocks (ny, nx, nent) -> (dims, comp[6]) with
+    comp[c] of shape (qy*qx, nent_c) (mode-major, toeplitz.hpp:58-61)."""
+    if nx <= 0 or ny <= 0 or nz <= 0:
+        raise ValueError("transform_operator: empty operator")
+    ex, ey = smooth_embedding_size(2 * nx - 1), smooth_embedding_size(2 * ny - 1)
+    qx, qy = ex // 2 + 1, ey // 2 + 1
+    comps = _split_block(np.asarray(blocks), nz)
+    out = []
+    for c in range(6):
+        sx, sy = PARITY_X[c], PARITY_Y[c]
+        v = comps[c]  # (ny, nx, nent_c)
+        w = np.zeros((ey, ex, v.shape[-1]), np.complex128)
+        w[:ny, :nx] = v
+        if nx > 1:
+            w[:ny, ex - np.arange(1, nx)] = sx * v[:, 1:]
+        if ny > 1:
+            w[ey - np.arange(1, ny), :nx] = sy * v[1:, :]
+        if nx > 1 and ny > 1:
+            w[np.ix_(ey - np.arange(1, ny), ex - np.arange(1, nx))] = sx * sy * v[1:, 1:]
+        f = np.fft.fft2(w, axes=(0, 1))
+        out.append(f[:qy, :qx].reshape(qy * qx, -1))
+    return (ex, ey, qx, qy), out
+
+
+def _mode_matrix(comp, dims, nz, my, mx):
+    """3nz x 3nz coupling of lateral mode (my, mx) as apply rebuilds it
+    (toeplitz.cpp:213-250)."""
+    ex, ey, qx, qy = dims
+    qmy, qmx, fy, fx = my, mx, 1.0, 1.0
+    if my > ey // 2:
+        qmy, fy = ey - my, -1.0
+    if mx > ex // 2:
+        qmx, fx = ex - mx, -1.0
+    qm = qmy * qx + qmx
+    iu = np.triu_indices(nz)
+
+    def sym(t):
+        m = np.zeros((nz, nz), np.complex128)
+        m[iu] = t
+        return m + np.triu(m, 1).T
+
+    xx, yy, zz, xy = (sym(comp[c][qm]) for c in range(4))
+    xz = comp[4][qm].reshape(nz, nz)
+    yz = comp[5][qm].reshape(nz, nz)
+    M = np.zeros((3 * nz, 3 * nz), np.complex128)
+    s = slice
+    M[s(0, nz), s(0, nz)] = xx
+    M[s(0, nz), s(nz, 2 * nz)] = fx * fy * xy
+    M[s(0, nz), s(2 * nz, 3 * nz)] = fx * xz
+    M[s(nz, 2 * nz), s(0, nz)] = fx * fy * xy
+    M[s(nz, 2 * nz), s(nz, 2 * nz)] = yy
+    M[s(nz, 2 * nz), s(2 * nz, 3 * nz)] = fy * yz
+    M[s(2 * nz, 3 * nz), s(0, nz)] = -fx * xz.T
+    M[s(2 * nz, 3 * nz), s(nz, 2 * nz)] = -fy * yz.T
+    M[s(2 * nz, 3 * nz), s(2 * nz, 3 * nz)] = zz
+    return M
+
+
+def apply_spectral(comp, dims, nx, ny, nz, v):
+    """apply(SpectralOperator) (src/toeplitz.cpp:163-283)."""
+    ex, ey, qx, qy = dims
+    v = np.asarray(v, np.complex128).reshape(3 * nz, ny, nx)
+    pad = np.zeros((3 * nz, ey, ex), np.complex128)
+    pad[:, :ny, :nx] = v
+    spec = np.fft.fft2(pad, axes=(1, 2))
+    out = np.zeros_like(spec)
+    for my in range(ey):
+        for mx in range(ex):
+            out[:, my, mx] = _mode_matrix(comp, dims, nz, my, mx) @ spec[:, my, mx]
+    back = np.fft.ifft2(out, axes=(1, 2))  # includes the 1/(ex ey)
+    return back[:, :ny, :nx].reshape(-1)
+
+
+def fetch_block(blocks, nz, oi, oj):
+    """src/greens.cpp:295-330 -> (3, 3, nz, nz)."""
+    ny, nx = blocks.shape[:2]
+    if abs(oi) >= ny or abs(oj) >= nx:
+        raise IndexError("fetch_block: offset out of range")
+    b = _split_block(blocks[abs(oi), abs(oj)], nz)
+    sx = -1.0 if oj < 0 else 1.0
+    sy = -1.0 if oi < 0 else 1.0
+    iu = np.triu_indices(nz)
+
+    def sym(t):
+        m = np.zeros((nz, nz), np.complex128)
+        m[iu] = t
+        return m + np.triu(m, 1).T
+
+    F = np.zeros((3, 3, nz, nz), np.complex128)
+    F[0, 0], F[1, 1], F[2, 2] = sym(b[0]), sym(b[1]), sym(b[2])
+    F[0, 1] = F[1, 0] = sx * sy * sym(b[3])
+    F[0, 2] = sx * b[4].reshape(nz, nz)
+    F[1, 2] = sy * b[5].reshape(nz, nz)
+    F[2, 0] = -F[0, 2].T
+    F[2, 1] = -F[1, 2].T
+    return F
+
+
+def dense_apply(blocks, nx, ny, nz, v):
+    """dense_reference_apply (src/toeplitz.cpp:285-312)."""
+    if nx * ny * nz > 4096:
+        raise ValueError("dense_reference_apply: grid too large")
+    v = np.asarray(v, np.complex128).reshape(3, nz, ny, nx)
+    out = np.zeros_like(v)
+    for oi in range(-(ny - 1), ny):
+        for oj in range(-(nx - 1), nx):
+            F = fetch_block(blocks, nz, oi, oj)
+            for iy in range(max(0, oi), min(ny, ny + oi)):
+                for ix in range(max(0, oj), min(nx, nx + oj)):
+                    src = v[:, :, iy - oi, ix - oj]  # (3, nz)
+                    out[:, :, iy, ix] += np.einsum("abkl,bl->ak", F, src)
+    return out.reshape(-1)
+
+
+def system_diagonals(grid: Grid):
+    """build_system (src/cie.cpp:24-54) with contrast_coefficients (9-22)."""
+    nz = grid.nz
+    s = np.zeros((nz, grid.ny, grid.nx), np.complex128)
+    r1 = np.zeros((nz, grid.ny, grid.nx))
+    r2 = np.zeros_like(s)
+    for iz in range(nz):
+        sb = grid.sigma_b[iz]
+        if not sb.real > 0.0:
+            raise ValueError("build_system: interval without conduction")
+        sq = math.sqrt(sb.real)
+        sa = grid.sigma_a[iz]
+        g = (sa - sb) / (sa + np.conj(sb))
+        if np.any(~(np.abs(g) < 1.0)):
+            raise ArithmeticError("contrast coefficients: contraction factor reaches one")
+        s[iz] = 1.0 - g
+        r1[iz] = 2.0 / grid.volume(iz) * sq
+        r2[iz] = -sq * g
+    return s.reshape(-1), r1.reshape(-1), r2.reshape(-1)
+
+
+def apply_system(diag, applyB, u):
+    """apply(SystemOperator) (src/cie.cpp:56-73); applyB maps a field to B v."""
+    s, r1, r2 = diag
+    u = np.asarray(u, np.complex128).reshape(3, -1)
+    out = np.asarray(applyB((r2[None, :] * u).reshape(-1))).reshape(3, -1)
+    return (s[None, :] * u + r1[None, :] * out).reshape(-1)
+
+
+def _make_rotation(f, g):
+    """src/cie.cpp:100-113."""
+    if g == 0:
+        return 1.0, 0j
+    if f == 0:
+        return 0.0, np.conj(g) / abs(g)
+    t = math.sqrt(abs(f) ** 2 + abs(g) ** 2)
+    return abs(f) / t, f / abs(f) * np.conj(g) / t
+
+
+def fgmres(apply_a, rhs, tol=1e-8, restart=40, max_iters=500):
+    """Flexible restarted GMRES, MGS twice (src/cie.cpp:117-238), no
+    preconditioner. -> (x, report dict)."""
+    if not tol > 0 or restart < 1 or max_iters < 1:
+        raise ValueError("fgmres: bad solver configuration")
+    rhs = np.asarray(rhs, np.complex128).reshape(-1)
+    x = np.zeros_like(rhs)
+    rep = {"status": "max_iterations", "iterations": 0, "residual": 0.0, "history": []}
+    bnorm = np.linalg.norm(rhs)
+    if bnorm == 0.0:
+        rep["status"] = "converged"
+        return x, rep
+    m = restart
+    r = rhs.copy()
+    rnorm = bnorm
+    it = 0
+    broke = False
+    while it < max_iters:
+        V = [r / rnorm]
+        H = np.zeros((m, m + 1), np.complex128)  # H[j] = column j
+        cs = np.zeros(m)
+        sn = np.zeros(m, np.complex128)
+        g = np.zeros(m + 1, np.complex128)
+        g[0] = rnorm
+        cols = 0
+        for j in range(m):
+            if not it < max_iters:
+                break
+            it += 1
+            w = apply_a(V[j])
+            wn0 = np.linalg.norm(w)
+            hj = H[j]
+            for _ in range(2):
+                for i in range(j + 1):
+                    hc = np.vdot(V[i], w)
+                    w = w - hc * V[i]
+                    hj[i] += hc
+            hnext = np.linalg.norm(w)
+            for i in range(j):
+                t = cs[i] * hj[i] + sn[i] * hj[i + 1]
+                hj[i + 1] = -np.conj(sn[i]) * hj[i] + cs[i] * hj[i + 1]
+                hj[i] = t
+            if hnext <= 1e-13 * max(wn0, 1e-300):
+                colmax = max([hnext] + [abs(hj[i]) for i in range(j + 1)])
+                if abs(hj[j]) > 1e-13 * max(colmax, 1e-300):
+                    cols = j + 1
+                else:
+                    cols = j
+                    broke = True
+                    rep["history"].append(rnorm / bnorm)
+                break
+            hj[j + 1] = hnext
+            V.append(w / hnext)
+            cs[j], sn[j] = _make_rotation(hj[j], hnext)
+            t = cs[j] * hj[j] + sn[j] * hj[j + 1]
+            hj[j + 1] = 0
+            hj[j] = t
+            g[j + 1] = -np.conj(sn[j]) * g[j]
+            g[j] = cs[j] * g[j]
+            cols = j + 1
+            est = abs(g[j + 1]) / bnorm
+            rep["history"].append(est)
+            if est <= tol:
+                break
+        if cols > 0:
+            y = np.zeros(cols, np.complex128)
+            for k in range(cols - 1, -1, -1):
+                acc = g[k]
+                for l in range(k + 1, cols):
+                    acc -= H[l, k] * y[l]
+                y[k] = acc / H[k, k]
+            for k in range(cols):
+                x = x + y[k] * V[k]
+        r = rhs - apply_a(x)
+        rnorm = np.linalg.norm(r)
+        if rnorm / bnorm <= tol:
+            rep["status"] = "converged"
+            break
+        if broke:
+            rep["status"] = "breakdown"
+            break
+    if broke and rnorm / bnorm <= tol:
+        rep["status"] = "converged"
+    rep["iterations"] = it
+    rep["residual"] = rnorm / bnorm
+    return x, rep

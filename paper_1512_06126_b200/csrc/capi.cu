@@ -1,0 +1,376 @@
+// C ABI (include/emie_cu.h) over the sm_100a kernels. Validation mirrors the
+// reference's argument checks and maps its exception types onto status codes.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/emie_cu.h"
+#include "operator.cuh"
+
+namespace emie_cu {
+
+long long& launch_counter() {
+  static thread_local long long n = 0;
+  return n;
+}
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return EMIE_CU_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return EMIE_CU_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EMIE_CU_RUNTIME_ERROR;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int smooth_size(int n) {  // toeplitz.cpp:18-26
+  if (n < 1) fail(EMIE_CU_INVALID_ARGUMENT, "smooth_embedding_size: n < 1");
+  for (int c = n;; ++c) {
+    int r = c;
+    for (int f : {2, 3, 5})
+      while (r % f == 0) r /= f;
+    if (r == 1) return c;
+  }
+}
+
+template <class T>
+T* dev_alloc(std::size_t n) {
+  void* p = nullptr;
+  EMIE_CUDA(cudaMalloc(&p, n * sizeof(T) + 16));
+  return static_cast<T*>(p);
+}
+
+// --------------------------------------------------- system diagonals ----
+// contrast_coefficients + build_system (cie.cpp:9-54), one thread per cell;
+// err[0] = 1 for Re sigma_b <= 0 (invalid_argument), 2 for |gamma| >= 1
+// (domain_error), lowest failing cell wins deterministically via atomicMin.
+__global__ void system_kernel(const cplx* __restrict__ sa, const cplx* __restrict__ sb,
+                              const double* __restrict__ vol, int ny_nx, int nz, cplx* s,
+                              double* r1, cplx* r2, unsigned long long* err) {
+  const long long n = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long cells = static_cast<long long>(ny_nx) * nz;
+  if (n >= cells) return;
+  const int iz = static_cast<int>(n / ny_nx);
+  const cplx b = sb[iz];
+  if (!(b.re > 0.0)) {
+    atomicMin(err, (1ull << 62) | static_cast<unsigned long long>(n));
+    return;
+  }
+  const double sq = sqrt(b.re);
+  const double den = 2.0 * sq;
+  const cplx a = sa[n];
+  // gamma = (sa - sb) / (sa + conj sb)   (cie.cpp:17)
+  const cplx num = a - b;
+  const cplx dd = a + conj(b);
+  // complex division in the std::complex<double> textbook form
+  const double dn = dd.re * dd.re + dd.im * dd.im;
+  const cplx g = {(num.re * dd.re + num.im * dd.im) / dn, (num.im * dd.re - num.re * dd.im) / dn};
+  if (!(hypot(g.re, g.im) < 1.0)) {
+    atomicMin(err, (2ull << 62) | static_cast<unsigned long long>(n));
+    return;
+  }
+  (void)den;
+  s[n] = cplx{1.0 - g.re, -g.im};
+  r1[n] = 2.0 / vol[iz] * sq;
+  r2[n] = cplx{-sq * g.re, -sq * g.im};
+}
+
+}  // namespace
+
+Operator::~Operator() {
+  cudaFree(spec);
+  cudaFree(blocks);
+  cudaFree(tw_x);
+  cudaFree(tw_y);
+  cudaFree(trilut);
+}
+
+System::~System() {
+  cudaFree(s);
+  cudaFree(r1);
+  cudaFree(r2);
+}
+
+cplx* upload_twiddles(int n) {
+  std::vector<cplx> h(static_cast<std::size_t>(n));
+  for (int m = 0; m < n; ++m) {
+    const long double a = 2.0L * 3.14159265358979323846264338327950288L * m / n;
+    h[m] = cplx{static_cast<double>(cosl(a)), -static_cast<double>(sinl(a))};
+  }
+  cplx* d = dev_alloc<cplx>(n);
+  EMIE_CUDA(cudaMemcpy(d, h.data(), n * sizeof(cplx), cudaMemcpyHostToDevice));
+  return d;
+}
+
+void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) {
+  if (nx <= 0 || ny <= 0 || nz <= 0)
+    fail(EMIE_CU_INVALID_ARGUMENT, "transform_operator: empty operator");
+  op.nx = nx;
+  op.ny = ny;
+  op.nz = nz;
+  op.omega = omega;
+  op.ex = smooth_size(2 * nx - 1);  // toeplitz.cpp:100-103
+  op.ey = smooth_size(2 * ny - 1);
+  op.qx = op.ex / 2 + 1;
+  op.qy = op.ey / 2 + 1;
+  op.ntri = nz * (nz + 1) / 2;
+  op.nfull = nz * nz;
+  op.nent = 4 * op.ntri + 2 * op.nfull;
+  if (!make_plan(op.ex, op.plan_x) || !make_plan(op.ey, op.plan_y))
+    fail(EMIE_CU_RUNTIME_ERROR, "toeplitz: planning failed");
+  op.spec = dev_alloc<cplx>(op.modes() * op.nent);
+  op.tw_x = upload_twiddles(op.ex);
+  op.tw_y = upload_twiddles(op.ey);
+  std::vector<uint32_t> lut(op.ntri);
+  for (int k = 0; k < nz; ++k)
+    for (int kp = k; kp < nz; ++kp)
+      lut[k * nz - k * (k - 1) / 2 + (kp - k)] = (static_cast<uint32_t>(k) << 16) | kp;
+  op.trilut = dev_alloc<uint32_t>(op.ntri);
+  EMIE_CUDA(cudaMemcpy(op.trilut, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice));
+}
+
+}  // namespace emie_cu
+
+using namespace emie_cu;
+
+struct emie_cu_operator_s {
+  Operator op;
+};
+struct emie_cu_system_s {
+  System sys;
+};
+
+extern "C" {
+
+const char* emie_cu_last_error(void) { return g_err.c_str(); }
+const char* emie_cu_version(void) { return "emie-b200 0.1 (sm_100a)"; }
+
+int emie_cu_device_count(int* count) {
+  return guarded([&] { EMIE_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int emie_cu_smooth_embedding_size(int n, int* out) {
+  return guarded([&] { *out = smooth_size(n); });
+}
+
+long long emie_cu_launch_count(void) { return launch_counter(); }
+void emie_cu_reset_launch_count(void) { launch_counter() = 0; }
+
+int emie_cu_operator_from_blocks(int nx, int ny, int nz, double omega, const double* h_blocks,
+                                 emie_cu_operator* out, void* stream) {
+  return guarded([&] {
+    if (!out || !h_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "operator_from_blocks: null pointer");
+    auto h = std::make_unique<emie_cu_operator_s>();
+    Operator& op = h->op;
+    init_operator_geometry(op, nx, ny, nz, omega);
+    const cudaStream_t st = as_stream(stream);
+    const std::size_t nb = static_cast<std::size_t>(nx) * ny * op.nent;
+    op.blocks = dev_alloc<cplx>(nb);
+    EMIE_CUDA(cudaMemcpyAsync(op.blocks, h_blocks, nb * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    transform_blocks(op, op.blocks, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    *out = h.release();
+  });
+}
+
+int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
+                         const double* breaks, int nx, int ny, double hx, double hy, double omega,
+                         const double* filter, int keep_blocks, emie_cu_operator* out,
+                         void* stream) {
+  return guarded([&] {
+    if (!out || !tops || !sigma || !breaks) fail(EMIE_CU_INVALID_ARGUMENT, "greens_build: null pointer");
+    FilterParams fp;
+    if (filter) {
+      fp.step = filter[0];
+      fp.shift = filter[1];
+      fp.half = static_cast<int>(filter[2]);
+      fp.n1 = static_cast<int>(filter[3]);
+      fp.n2 = static_cast<int>(filter[4]);
+    }
+    check_filter_params(fp);
+    auto h = std::make_unique<emie_cu_operator_s>();
+    init_operator_geometry(h->op, nx, ny, nz, omega);
+    const cudaStream_t st = as_stream(stream);
+    greens_build(h->op, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, fp,
+                 keep_blocks != 0, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    *out = h.release();
+  });
+}
+
+int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy, const double* filter,
+                                  double* h_w, double* h_lam) {
+  return guarded([&] {
+    FilterParams fp;
+    if (filter) {
+      fp.step = filter[0];
+      fp.shift = filter[1];
+      fp.half = static_cast<int>(filter[2]);
+      fp.n1 = static_cast<int>(filter[3]);
+      fp.n2 = static_cast<int>(filter[4]);
+    }
+    check_filter_params(fp);
+    design_offset_filters_host(oi, oj, hx, hy, fp, h_w, h_lam);
+  });
+}
+
+int emie_cu_operator_dims(emie_cu_operator h, int dims[7], double* omega) {
+  return guarded([&] {
+    if (!h) fail(EMIE_CU_INVALID_ARGUMENT, "null operator");
+    const Operator& op = h->op;
+    const int d[7] = {op.nx, op.ny, op.nz, op.ex, op.ey, op.qx, op.qy};
+    std::memcpy(dims, d, sizeof d);
+    if (omega) *omega = op.omega;
+  });
+}
+
+int emie_cu_operator_download_spectra(emie_cu_operator h, double* h_comp) {
+  return guarded([&] {
+    if (!h || !h_comp) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
+    const Operator& op = h->op;
+    std::vector<cplx> mm(op.modes() * op.nent);
+    EMIE_CUDA(cudaMemcpy(mm.data(), op.spec, mm.size() * sizeof(cplx), cudaMemcpyDeviceToHost));
+    // mode-major packed -> six component arrays (toeplitz.hpp:58-61)
+    cplx* o = reinterpret_cast<cplx*>(h_comp);
+    const std::size_t modes = op.modes();
+    for (int c = 0; c < 6; ++c) {
+      const int nent_c = c < 4 ? op.ntri : op.nfull;
+      const int off = c < 4 ? c * op.ntri : 4 * op.ntri + (c - 4) * op.nfull;
+      for (std::size_t m = 0; m < modes; ++m)
+        std::memcpy(o + m * nent_c, mm.data() + m * op.nent + off, nent_c * sizeof(cplx));
+      o += modes * nent_c;
+    }
+  });
+}
+
+int emie_cu_operator_download_blocks(emie_cu_operator h, double* h_blocks) {
+  return guarded([&] {
+    if (!h || !h_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
+    const Operator& op = h->op;
+    if (!op.blocks) fail(EMIE_CU_INVALID_ARGUMENT, "operator holds no compressed blocks");
+    EMIE_CUDA(cudaMemcpy(h_blocks, op.blocks,
+                         static_cast<std::size_t>(op.nx) * op.ny * op.nent * sizeof(cplx),
+                         cudaMemcpyDeviceToHost));
+  });
+}
+
+void emie_cu_operator_destroy(emie_cu_operator h) { delete h; }
+
+int emie_cu_apply_spectral(emie_cu_operator h, const double* d_in, double* d_out, int nrhs,
+                           void* stream) {
+  return guarded([&] {
+    if (!h || !d_in || !d_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
+    if (d_in == d_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: output aliases input");
+    apply_b(h->op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<cplx*>(d_out), nrhs,
+            nullptr, as_stream(stream));
+  });
+}
+
+int emie_cu_system_create(emie_cu_operator h, const double* h_sigma_a, const double* h_sigma_b,
+                          const double* h_volume, emie_cu_system* out) {
+  return guarded([&] {
+    if (!h || !h_sigma_a || !h_sigma_b || !h_volume || !out)
+      fail(EMIE_CU_INVALID_ARGUMENT, "build_system: null pointer");
+    const Operator& op = h->op;
+    auto s = std::make_unique<emie_cu_system_s>();
+    System& sys = s->sys;
+    sys.op = &op;
+    const std::size_t cells = op.cells();
+    sys.s = dev_alloc<cplx>(cells);
+    sys.r1 = dev_alloc<double>(cells);
+    sys.r2 = dev_alloc<cplx>(cells);
+    cplx* sa = dev_alloc<cplx>(cells);
+    cplx* sb = dev_alloc<cplx>(op.nz);
+    double* vol = dev_alloc<double>(op.nz);
+    unsigned long long* err = dev_alloc<unsigned long long>(1);
+    const unsigned long long none = ~0ull;
+    EMIE_CUDA(cudaMemcpy(sa, h_sigma_a, cells * sizeof(cplx), cudaMemcpyHostToDevice));
+    EMIE_CUDA(cudaMemcpy(sb, h_sigma_b, op.nz * sizeof(cplx), cudaMemcpyHostToDevice));
+    EMIE_CUDA(cudaMemcpy(vol, h_volume, op.nz * sizeof(double), cudaMemcpyHostToDevice));
+    EMIE_CUDA(cudaMemcpy(err, &none, sizeof none, cudaMemcpyHostToDevice));
+    system_kernel<<<ceil_div(static_cast<long long>(cells), 256), 256>>>(
+        sa, sb, vol, op.nx * op.ny, op.nz, sys.s, sys.r1, sys.r2, err);
+    check_launch("system_kernel");
+    unsigned long long e = 0;
+    EMIE_CUDA(cudaMemcpy(&e, err, sizeof e, cudaMemcpyDeviceToHost));
+    cudaFree(sa);
+    cudaFree(sb);
+    cudaFree(vol);
+    cudaFree(err);
+    if (e != none) {
+      if ((e >> 62) == 1) fail(EMIE_CU_INVALID_ARGUMENT, "build_system: interval without conduction");
+      fail(EMIE_CU_DOMAIN_ERROR, "contrast coefficients: contraction factor reaches one");
+    }
+    *out = s.release();
+  });
+}
+
+int emie_cu_system_download(emie_cu_system h, double* h_s, double* h_r1, double* h_r2) {
+  return guarded([&] {
+    if (!h) fail(EMIE_CU_INVALID_ARGUMENT, "null system");
+    const std::size_t cells = h->sys.op->cells();
+    if (h_s) EMIE_CUDA(cudaMemcpy(h_s, h->sys.s, cells * sizeof(cplx), cudaMemcpyDeviceToHost));
+    if (h_r1) EMIE_CUDA(cudaMemcpy(h_r1, h->sys.r1, cells * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h_r2) EMIE_CUDA(cudaMemcpy(h_r2, h->sys.r2, cells * sizeof(cplx), cudaMemcpyDeviceToHost));
+  });
+}
+
+void emie_cu_system_destroy(emie_cu_system h) { delete h; }
+
+int emie_cu_apply_system(emie_cu_system h, const double* d_in, double* d_out, int nrhs,
+                         void* stream) {
+  return guarded([&] {
+    if (!h || !d_in || !d_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
+    if (d_in == d_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: output aliases input");
+    apply_b(*h->sys.op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<cplx*>(d_out),
+            nrhs, &h->sys, as_stream(stream));
+  });
+}
+
+int emie_cu_apply_system_host(emie_cu_system h, const double* h_in, double* h_out, int nrhs,
+                              void* stream) {
+  return guarded([&] {
+    if (!h || !h_in || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
+    const cudaStream_t st = as_stream(stream);
+    const std::size_t n = 3 * h->sys.op->cells() * static_cast<std::size_t>(nrhs);
+    cplx* din = scratch<cplx>(n, st);
+    cplx* dout = scratch<cplx>(n, st);
+    EMIE_CUDA(cudaMemcpyAsync(din, h_in, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    apply_b(*h->sys.op, din, dout, nrhs, &h->sys, st);
+    EMIE_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    release(din, st);
+    release(dout, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"
+
+extern "C" int emie_cu_fgmres(emie_cu_system h, const double* d_rhs, double* d_x, int nrhs,
+                              double tol, int restart, int max_iters, emie_cu_report* reports,
+                              double* h_history, int hist_cap, void* stream) {
+  return guarded([&] {
+    if (!h || !d_rhs || !d_x) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: nrhs < 1");
+    fgmres_device(h->sys, reinterpret_cast<const cplx*>(d_rhs), reinterpret_cast<cplx*>(d_x),
+                  nrhs, tol, restart, max_iters, reports, h_history, hist_cap, as_stream(stream));
+  });
+}

@@ -1,0 +1,448 @@
+// Device FGMRES for A U = rhs with A = apply(SystemOperator) — the
+// reference's fgmres (src/cie.cpp:117-238) restated for the GPU.
+//
+// What stays on the host: the (m+1) x m Hessenberg column, the complex
+// Givens rotations with real cosine (cie.cpp:100-113), the breakdown test
+// (cie.cpp:171-187), the back substitution (cie.cpp:205-212) — O(m^2)
+// scalars per cycle, bit-for-bit the reference's arithmetic.
+// What runs on the device: every vector operation (norms, the conjugated
+// dots, axpys, scalings) and the operator applies. Basis vectors of all
+// right-hand sides share one apply call per step (the two MT polarisations
+// read the operator once).
+//
+// Orthogonalisation: classical Gram-Schmidt run twice (CGS2) instead of the
+// reference's modified Gram-Schmidt run twice (cie.cpp:158-165). Both
+// produce the same Krylov basis in exact arithmetic and are "twice is
+// enough" stable; CGS2 turns the (j+1) sequential dot/axpy pairs into one
+// batched dot sweep and one batched update sweep per pass. All reductions
+// are fixed-order (per-block partials, then an ordered final sum), so
+// solves are bit-reproducible.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "../../include/emie_cu.h"
+#include "operator.cuh"
+
+namespace emie_cu {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kChunk = 8;
+
+int red_blocks(std::size_t n) {
+  return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(592, (n + kRedThreads - 1) / kRedThreads)));
+}
+
+// block-wide sum of NV doubles per thread into out[0..NV) (thread 0 writes)
+template <int NV>
+__device__ void block_sum(double (&v)[NV], double* out) {
+  __shared__ double red[kRedThreads / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp][i] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < kRedThreads / 32; ++w) s += red[w][i];
+      out[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// partial[blk][2*(l0+l) .. +1] = sum_e conj(V_l[e]) w[e] for l in chunk;
+// partial[blk][2*nv] = sum_e |w[e]|^2 when with_norm (chunk 0 only)
+__global__ void __launch_bounds__(kRedThreads) dots_kernel(const cplx* __restrict__ V, std::size_t vstride,
+                                                           int nv, const cplx* __restrict__ w,
+                                                           std::size_t n, double* partial, int pstride,
+                                                           int with_norm) {
+  const int nchunks = max(1, (nv + kChunk - 1) / kChunk);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int l0 = ci * kChunk;
+    double acc[2 * kChunk + 1];
+#pragma unroll
+    for (int i = 0; i < 2 * kChunk + 1; ++i) acc[i] = 0.0;
+    const int nl = max(0, min(kChunk, nv - l0));
+    for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+      const cplx wv = ldg(w + e);
+      if (l0 == 0) acc[2 * kChunk] = fma(wv.re, wv.re, fma(wv.im, wv.im, acc[2 * kChunk]));
+#pragma unroll
+      for (int l = 0; l < kChunk; ++l) {
+        if (l < nl) {
+          const cplx v = ldg(V + (l0 + l) * vstride + e);
+          acc[2 * l] = fma(v.re, wv.re, fma(v.im, wv.im, acc[2 * l]));
+          acc[2 * l + 1] = fma(v.re, wv.im, fma(-v.im, wv.re, acc[2 * l + 1]));
+        }
+      }
+    }
+    __shared__ double tot[2 * kChunk + 1];
+    block_sum<2 * kChunk + 1>(acc, tot);
+    if (threadIdx.x < 2 * nl) partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * l0 + threadIdx.x] = tot[threadIdx.x];
+    if (l0 == 0 && with_norm && threadIdx.x == 0)
+      partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * nv] = tot[2 * kChunk];
+  }
+}
+
+// out[i] = sum over blocks (in block order) of partial[b][i]
+__global__ void finalize_kernel(const double* partial, int nblocks, int pstride, int nvals,
+                                double* out) {
+  for (int i = threadIdx.x; i < nvals; i += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += partial[static_cast<std::size_t>(b) * pstride + i];
+    out[i] = s;
+  }
+}
+
+// w[e] -= sum_l h[l] V_l[e]; optional per-block |w|^2 partial at pstride slot 0
+__global__ void __launch_bounds__(kRedThreads) update_kernel(cplx* w, const cplx* __restrict__ V,
+                                                             std::size_t vstride, int nv,
+                                                             const double* __restrict__ h,
+                                                             std::size_t n, double* partial) {
+  double acc[1] = {0.0};
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    cplx x = w[e];
+    for (int l = 0; l < nv; ++l) {
+      const cplx v = ldg(V + l * vstride + e);
+      const double hr = h[2 * l], hi = h[2 * l + 1];
+      // x -= h v
+      x.re = fma(-hr, v.re, fma(hi, v.im, x.re));
+      x.im = fma(-hr, v.im, fma(-hi, v.re, x.im));
+    }
+    w[e] = x;
+    acc[0] = fma(x.re, x.re, fma(x.im, x.im, acc[0]));
+  }
+  if (partial) {
+    __shared__ double tot[1];
+    block_sum<1>(acc, tot);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot[0];
+  }
+}
+
+// y[e] = a * x[e] (real a)
+__global__ void scale_kernel(cplx* y, const cplx* __restrict__ x, double a, std::size_t n) {
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    y[e] = a * ldg(x + e);
+}
+
+// x[e] += sum_k y[k] V_k[e] in k order (cie.cpp:213-214)
+__global__ void combine_kernel(cplx* x, const cplx* __restrict__ V, std::size_t vstride, int nv,
+                               const double* __restrict__ y, std::size_t n) {
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    cplx acc = x[e];
+    for (int k = 0; k < nv; ++k) acc = acc + cplx{y[2 * k], y[2 * k + 1]} * ldg(V + k * vstride + e);
+    x[e] = acc;
+  }
+}
+
+// r[e] = b[e] - t[e], per-block |r|^2 partials
+__global__ void __launch_bounds__(kRedThreads) residual_kernel(cplx* r, const cplx* __restrict__ b,
+                                                               const cplx* __restrict__ t,
+                                                               std::size_t n, double* partial) {
+  double acc[1] = {0.0};
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const cplx v = ldg(b + e) - ldg(t + e);
+    r[e] = v;
+    acc[0] = fma(v.re, v.re, fma(v.im, v.im, acc[0]));
+  }
+  __shared__ double tot[1];
+  block_sum<1>(acc, tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot[0];
+}
+
+using cd = std::complex<double>;
+
+// reference make_rotation (cie.cpp:100-113)
+void make_rotation(cd f, cd g, double& c, cd& s) {
+  if (g == 0.0) {
+    c = 1.0;
+    s = 0.0;
+  } else if (f == 0.0) {
+    c = 0.0;
+    s = std::conj(g) / std::abs(g);
+  } else {
+    const double t = std::sqrt(std::norm(f) + std::norm(g));
+    c = std::abs(f) / t;
+    s = f / std::abs(f) * std::conj(g) / t;
+  }
+}
+
+struct Workspace {
+  cudaStream_t st;
+  std::size_t n;  // complex entries per field
+  int G;          // reduction blocks
+  double* partial = nullptr;  // G x pstride
+  double* dvals = nullptr;    // finalized values
+  double* hpin = nullptr;     // pinned host mirror
+  int pstride = 0;
+
+  Workspace(cudaStream_t s, std::size_t n_, int maxv) : st(s), n(n_) {
+    G = red_blocks(n);
+    pstride = 2 * maxv + 2;
+    partial = scratch<double>(static_cast<std::size_t>(G) * pstride, st);
+    dvals = scratch<double>(pstride, st);
+    EMIE_CUDA(cudaMallocHost(&hpin, pstride * sizeof(double)));
+  }
+  ~Workspace() {
+    release(partial, st);
+    release(dvals, st);
+    cudaFreeHost(hpin);
+  }
+
+  // dots of w against nv vectors (+ |w|^2): values land in dvals and hpin
+  void dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, bool with_norm) {
+    dots_kernel<<<G, kRedThreads, 0, st>>>(V, vstride, nv, w, n, partial, pstride, with_norm);
+    check_launch("dots_kernel");
+    finalize(2 * nv + (with_norm ? 1 : 0), with_norm ? 0 : -1);
+  }
+  // finalize partial sums; when norm_slot_src >= 0 the |w|^2 lives at 2*nv
+  void finalize(int nvals, int) {
+    finalize_kernel<<<1, 128, 0, st>>>(partial, G, pstride, nvals, dvals);
+    check_launch("finalize_kernel");
+  }
+  double norm_of(const cplx* w) {
+    dots_kernel<<<G, kRedThreads, 0, st>>>(w, 0, 0, w, n, partial, pstride, 1);
+    check_launch("dots_kernel");
+    finalize_kernel<<<1, 128, 0, st>>>(partial, G, pstride, 1, dvals);
+    check_launch("finalize_kernel");
+    fetch(1);
+    return std::sqrt(hpin[0]);
+  }
+  void fetch(int nvals) {
+    EMIE_CUDA(cudaMemcpyAsync(hpin, dvals, nvals * sizeof(double), cudaMemcpyDeviceToHost, st));
+    EMIE_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
+// one right-hand side's FGMRES state, advanced between operator applies
+struct Rhs {
+  enum Phase { kInner, kResidual, kDone };
+  int idx = 0;
+  Phase phase = kDone;
+  cplx* x = nullptr;    // solution (device)
+  const cplx* b = nullptr;
+  cplx* r = nullptr;    // residual (device)
+  cplx* V = nullptr;    // basis (m+1) vectors (device)
+  cplx* w = nullptr;    // apply output (device)
+  double bnorm = 0, rnorm = 0;
+  int iter = 0, j = 0, cols = 0;
+  bool broke = false;
+  std::vector<cd> h, g, rot_s;
+  std::vector<double> rot_c, history;
+  emie_cu_report rep{1, 0, 0.0, 0};
+};
+
+}  // namespace
+
+void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, double tol,
+                   int m, int max_iters, emie_cu_report* reports, double* h_history,
+                   int hist_cap, cudaStream_t st) {
+  if (!(tol > 0.0) || m < 1 || max_iters < 1)
+    fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: bad solver configuration");
+  const Operator& op = *sys.op;
+  const std::size_t n = 3 * op.cells();
+  Workspace ws(st, n, m + 1);
+  const int T = 256;
+  const int GB = red_blocks(n);
+
+  // device storage: basis V[r][m+1][n], residual, apply in/out batches
+  cplx* Vall = scratch<cplx>(static_cast<std::size_t>(nrhs) * (m + 1) * n, st);
+  cplx* Rall = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
+  cplx* Wall = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
+  cplx* Bin = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
+  double* ycoef = scratch<double>(2 * (m + 1), st);
+  double* hcoef = scratch<double>(2 * (m + 1), st);
+
+  std::vector<Rhs> rs(nrhs);
+  for (int i = 0; i < nrhs; ++i) {
+    Rhs& R = rs[i];
+    R.idx = i;
+    R.x = d_x + i * n;
+    R.b = d_rhs + i * n;
+    R.r = Rall + i * n;
+    R.V = Vall + static_cast<std::size_t>(i) * (m + 1) * n;
+    R.w = Wall + i * n;
+    EMIE_CUDA(cudaMemsetAsync(R.x, 0, n * sizeof(cplx), st));
+    R.bnorm = ws.norm_of(R.b);
+    if (R.bnorm == 0.0) {  // cie.cpp:124-128
+      R.rep.status = 0;
+      R.phase = Rhs::kDone;
+      continue;
+    }
+    EMIE_CUDA(cudaMemcpyAsync(R.r, R.b, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    R.rnorm = R.bnorm;
+    R.phase = Rhs::kResidual;  // marker: start a cycle below
+  }
+
+  // start a restart cycle (cie.cpp:136-147); returns false when the
+  // iteration budget is exhausted
+  auto start_cycle = [&](Rhs& R) -> bool {
+    if (!(R.iter < max_iters)) return false;
+    scale_kernel<<<GB, T, 0, st>>>(R.V, R.r, 1.0 / R.rnorm, n);
+    check_launch("scale_kernel");
+    R.h.assign(static_cast<std::size_t>(m + 1) * m, cd(0.0));
+    R.rot_c.assign(m, 0.0);
+    R.rot_s.assign(m, cd(0.0));
+    R.g.assign(m + 1, cd(0.0));
+    R.g[0] = R.rnorm;
+    R.cols = 0;
+    R.j = 0;
+    R.phase = Rhs::kInner;
+    return true;
+  };
+  auto finish = [&](Rhs& R) {
+    if (R.broke && R.rnorm / R.bnorm <= tol) R.rep.status = 0;  // cie.cpp:232-233
+    R.phase = Rhs::kDone;
+  };
+  for (Rhs& R : rs)
+    if (R.phase == Rhs::kResidual && !start_cycle(R)) finish(R);
+
+  // end of a cycle: update x, then request the explicit residual
+  auto close_cycle = [&](Rhs& R) {
+    if (R.cols > 0) {  // back substitution (cie.cpp:205-215)
+      std::vector<cd> y(R.cols);
+      for (int k = R.cols - 1; k >= 0; --k) {
+        cd acc = R.g[k];
+        for (int l = k + 1; l < R.cols; ++l)
+          acc -= R.h[static_cast<std::size_t>(l) * (m + 1) + k] * y[l];
+        y[k] = acc / R.h[static_cast<std::size_t>(k) * (m + 1) + k];
+      }
+      EMIE_CUDA(cudaMemcpyAsync(ycoef, y.data(), R.cols * sizeof(cd), cudaMemcpyHostToDevice, st));
+      combine_kernel<<<GB, T, 0, st>>>(R.x, R.V, n, R.cols, ycoef, n);
+      check_launch("combine_kernel");
+      EMIE_CUDA(cudaStreamSynchronize(st));  // ycoef is reused by the next rhs
+    }
+    R.phase = Rhs::kResidual;
+  };
+
+  while (true) {
+    // gather every pending apply into one batched call
+    std::vector<Rhs*> req;
+    for (Rhs& R : rs)
+      if (R.phase == Rhs::kInner || R.phase == Rhs::kResidual) req.push_back(&R);
+    if (req.empty()) break;
+    for (std::size_t q = 0; q < req.size(); ++q) {
+      Rhs& R = *req[q];
+      const cplx* src = R.phase == Rhs::kInner ? R.V + static_cast<std::size_t>(R.j) * n : R.x;
+      EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    }
+    apply_b(op, Bin, Wall, static_cast<int>(req.size()), &sys, st);
+    for (std::size_t q = 0; q < req.size(); ++q) {
+      Rhs& R = *req[q];
+      cplx* w = Wall + q * n;
+      if (R.phase == Rhs::kResidual) {  // cie.cpp:217-229
+        residual_kernel<<<ws.G, kRedThreads, 0, st>>>(R.r, R.b, w, n, ws.partial);
+        check_launch("residual_kernel");
+        finalize_kernel<<<1, 128, 0, st>>>(ws.partial, ws.G, 1, 1, ws.dvals);
+        check_launch("finalize_kernel");
+        ws.fetch(1);
+        R.rnorm = std::sqrt(ws.hpin[0]);
+        if (R.rnorm / R.bnorm <= tol) {
+          R.rep.status = 0;
+          finish(R);
+        } else if (R.broke) {
+          R.rep.status = 2;
+          finish(R);
+        } else if (!start_cycle(R)) {
+          finish(R);
+        }
+        continue;
+      }
+      // inner step j (cie.cpp:148-203)
+      ++R.iter;
+      const int j = R.j;
+      cd* hj = R.h.data() + static_cast<std::size_t>(j) * (m + 1);
+      // pass 1: dots against v_0..v_j plus |w|^2
+      ws.dots(R.V, n, j + 1, w, true);
+      ws.fetch(2 * (j + 1) + 1);
+      const double wn0 = std::sqrt(ws.hpin[2 * (j + 1)]);
+      for (int i = 0; i <= j; ++i) hj[i] += cd(ws.hpin[2 * i], ws.hpin[2 * i + 1]);
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, ws.dvals, n, nullptr);
+      check_launch("update_kernel");
+      // pass 2
+      ws.dots(R.V, n, j + 1, w, false);
+      ws.fetch(2 * (j + 1));
+      for (int i = 0; i <= j; ++i) hj[i] += cd(ws.hpin[2 * i], ws.hpin[2 * i + 1]);
+      EMIE_CUDA(cudaMemcpyAsync(hcoef, ws.dvals, 2 * (j + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, hcoef, n, ws.partial);
+      check_launch("update_kernel");
+      finalize_kernel<<<1, 128, 0, st>>>(ws.partial, ws.G, 1, 1, ws.dvals);
+      check_launch("finalize_kernel");
+      ws.fetch(1);
+      const double hnext = std::sqrt(ws.hpin[0]);
+      for (int i = 0; i < j; ++i) {
+        const cd t = R.rot_c[i] * hj[i] + R.rot_s[i] * hj[i + 1];
+        hj[i + 1] = -std::conj(R.rot_s[i]) * hj[i] + R.rot_c[i] * hj[i + 1];
+        hj[i] = t;
+      }
+      bool end_inner = false;
+      if (hnext <= 1e-13 * std::max(wn0, 1e-300)) {
+        double colmax = hnext;
+        for (int i = 0; i <= j; ++i) colmax = std::max(colmax, std::abs(hj[i]));
+        if (std::abs(hj[j]) > 1e-13 * std::max(colmax, 1e-300)) {
+          R.cols = j + 1;
+        } else {
+          R.cols = j;
+          R.broke = true;
+          R.history.push_back(R.rnorm / R.bnorm);
+        }
+        end_inner = true;
+      } else {
+        hj[j + 1] = hnext;
+        scale_kernel<<<GB, T, 0, st>>>(R.V + static_cast<std::size_t>(j + 1) * n, w, 1.0 / hnext, n);
+        check_launch("scale_kernel");
+        make_rotation(hj[j], hnext, R.rot_c[j], R.rot_s[j]);
+        const cd t = R.rot_c[j] * hj[j] + R.rot_s[j] * hj[j + 1];
+        hj[j + 1] = 0.0;
+        hj[j] = t;
+        R.g[j + 1] = -std::conj(R.rot_s[j]) * R.g[j];
+        R.g[j] = R.rot_c[j] * R.g[j];
+        R.cols = j + 1;
+        const double est = std::abs(R.g[j + 1]) / R.bnorm;
+        R.history.push_back(est);
+        if (est <= tol) end_inner = true;
+      }
+      if (!end_inner) {
+        ++R.j;
+        if (!(R.j < m && R.iter < max_iters)) end_inner = true;
+      }
+      if (end_inner) close_cycle(R);
+    }
+  }
+
+  for (int i = 0; i < nrhs; ++i) {
+    Rhs& R = rs[i];
+    R.rep.iterations = R.iter;
+    R.rep.residual = R.bnorm == 0.0 ? 0.0 : R.rnorm / R.bnorm;
+    R.rep.history_len = static_cast<int>(R.history.size());
+    if (reports) reports[i] = R.rep;
+    if (h_history)
+      for (int k = 0; k < hist_cap && k < static_cast<int>(R.history.size()); ++k)
+        h_history[static_cast<std::size_t>(i) * hist_cap + k] = R.history[k];
+  }
+  release(Vall, st);
+  release(Rall, st);
+  release(Wall, st);
+  release(Bin, st);
+  release(ycoef, st);
+  release(hcoef, st);
+  EMIE_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace emie_cu
+

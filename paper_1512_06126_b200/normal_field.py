@@ -1,0 +1,115 @@
+"""Plane-wave normal field and CIE right-hand side.
+
+The reference leaves this stage as a placeholder (src/normal_field.cpp:1),
+so there is no reference arithmetic to match; one shared host routine feeds
+both the oracle and the B200 solver. It is a 1-D,
+O(layers) computation per frequency and stays on the host.
+
+Convention: fields ~ e^{-i omega t} with eta_m = sqrt(-i omega mu0 sigma_m),
+Re eta > 0 (the lambda = 0 limit of build_spectral_state, layered.cpp:87-89);
+unit tangential electric field at z = 0; the lower halfspace carries only
+the decaying mode. Inside layer m (top zt, bottom zb, thickness l):
+    E(z) = D [ e^{-eta (z - zt)} + rho e^{-eta l} e^{-eta (zb - z)} ]
+with rho = (eta + Y_b) / (eta - Y_b) fixed by the admittance Y = E'/E at the
+bottom; every exponential has a non-positive real exponent.
+"""
+from __future__ import annotations
+
+import cmath
+
+import numpy as np
+
+MU0 = 1.2566370614359172e-06
+
+
+def _cexpm1(x: complex) -> complex:
+    """e^x - 1 without cancellation (the form of layered.cpp:19-25)."""
+    import math
+    em = math.expm1(x.real)
+    s = math.sin(0.5 * x.imag)
+    return complex(em * math.cos(x.imag) - 2.0 * s * s, (em + 1.0) * math.sin(x.imag))
+
+
+def _layers(tops, sigma, omega):
+    L = len(tops)
+    eta = []
+    for m in range(L + 1):
+        s = complex(sigma[m])
+        if s.real < 1e-9:
+            s = complex(1e-9, s.imag)
+        e = cmath.sqrt(-1j * omega * MU0 * s)
+        eta.append(-e if e.real < 0 else e)
+    return eta
+
+
+def profile(tops, sigma, omega):
+    """-> list of per-layer (zt, l, D, rho, eta) for layers 1..L (l = inf for
+    the lower halfspace), normalised to E(0) = 1 with z = 0 the top of layer 1."""
+    L = len(tops)
+    eta = _layers(tops, sigma, omega)
+    # admittance from the bottom up
+    Y = [None] * (L + 1)
+    rho = [0j] * (L + 1)
+    Yb = -eta[L]
+    Y[L] = Yb
+    for m in range(L - 1, 0, -1):
+        l = tops[m] - tops[m - 1]
+        e = eta[m]
+        r = (e + Yb) / (e - Yb)
+        rho[m] = r
+        q = r * cmath.exp(-2.0 * e * l)
+        Yb = e * (-1.0 + q) / (1.0 + q)
+        Y[m] = Yb
+    out = []
+    Et = 1.0 + 0j  # E at the surface (top of layer 1)
+    for m in range(1, L + 1):
+        e = eta[m]
+        zt = tops[m - 1]
+        if m == L:
+            out.append((zt, np.inf, Et, 0j, e))
+            break
+        l = tops[m] - tops[m - 1]
+        el = cmath.exp(-e * l)
+        D = Et / (1.0 + rho[m] * el * el)
+        out.append((zt, l, D, rho[m], e))
+        Et = D * el * (1.0 + rho[m])
+    return out
+
+
+def field_at(prof, z):
+    for zt, l, D, r, e in prof:
+        if z >= zt and (z < zt + l or np.isinf(l)):
+            if np.isinf(l):
+                return D * cmath.exp(-e * (z - zt))
+            return D * (cmath.exp(-e * (z - zt)) + r * cmath.exp(-e * l) * cmath.exp(-e * (zt + l - z)))
+    raise ValueError("depth above the surface")
+
+
+def interval_average(prof, a, b):
+    """(1/(b-a)) * integral of E over [a, b] inside one layer."""
+    h = b - a
+    for zt, l, D, r, e in prof:
+        if a >= zt - 1e-9 and (np.isinf(l) or b <= zt + l + 1e-7 * (1.0 + abs(b))):
+            g = -_cexpm1(-e * h) / e  # (1 - e^{-eta h}) / eta
+            down = cmath.exp(-e * (a - zt)) * g
+            if np.isinf(l):
+                return D * down / h
+            up = r * cmath.exp(-e * l) * cmath.exp(-e * (zt + l - b)) * g
+            return D * (down + up) / h
+    raise ValueError("interval straddles a layer")
+
+
+def build_rhs(tops, sigma, breaks, nx, ny, omega, polarization: str):
+    """U0_n = sqrt(Re sigma_b^n) * cell average of E^N for
+    an x- or y-polarised plane wave -> GridVector-layout complex array."""
+    prof = profile(tops, sigma, omega)
+    nz = len(breaks) - 1
+    u = np.zeros((3, nz, ny, nx), np.complex128)
+    c = {"x": 0, "y": 1}[polarization]
+    import bisect
+    for iz in range(nz):
+        m = bisect.bisect_right(list(tops), breaks[iz])
+        sb = complex(sigma[m])
+        sb = max(sb.real, 1e-9)
+        u[c, iz] = np.sqrt(sb) * interval_average(prof, breaks[iz], breaks[iz + 1])
+    return u.reshape(-1)

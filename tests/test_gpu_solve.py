@@ -1,0 +1,56 @@
+"""GPU FGMRES parity: solve_cie on config 1 against the reference's own
+solve (tests/golden/cfg1.npz), plus the SPEC.md:381-384 properties."""
+import numpy as np
+import pytest
+
+import paper_1512_06126_b200 as emie
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg1():
+    g = golden("cfg1")
+    nz = len(g["breaks"]) - 1
+    sop = emie.transform_operator(g["blocks"], int(g["nx"]), int(g["ny"]), nz, float(g["omega"]))
+    model = emie.LayeredModel(list(g["tops"]), list(g["sigma"]))
+    grid = emie.make_grid(model, list(g["breaks"]), int(g["nx"]), int(g["ny"]), float(g["hx"]), float(g["hy"]))
+    grid.sigma_a[...] = g["sigma_a"].reshape(grid.sigma_a.shape)
+    return g, model, grid, sop
+
+
+def test_solve_matches_reference_cfg1(torch_cuda):
+    g, model, grid, sop = _cfg1()
+    # both polarisations in one lockstep solve
+    x, reps = emie.solve_cie(grid, model, sop, g["rhs"], emie.SolverConfig(tol=1e-10))
+    for i in range(2):
+        assert reps[i].status == "converged"
+        want = g["x_tol10"][i]
+        assert np.linalg.norm(x[i] - want) <= 1e-8 * np.linalg.norm(want)
+    x6, reps6 = emie.solve_cie(grid, model, sop, g["rhs"], emie.SolverConfig(tol=1e-6))
+    for i in range(2):
+        assert reps6[i].status == "converged"
+        assert abs(reps6[i].iterations - int(g["iters_tol6"][i])) <= 1
+        want = g["x_tol6"][i]
+        # fields E_n = U_n / a_n share a per-cell factor: compare U directly
+        assert np.linalg.norm(x6[i] - want) <= 1e-6 * np.linalg.norm(want)
+        h = np.array(reps6[i].history)
+        assert np.all(np.diff(h[: min(40, len(h))]) <= 1e-12)  # monotone inside a cycle
+
+
+def test_zero_rhs_and_identity(torch_cuda):
+    g, model, grid, sop = _cfg1()
+    n = g["rhs"].shape[1]
+    x, reps = emie.solve_cie(grid, model, sop, np.zeros(n, np.complex128), emie.SolverConfig(tol=1e-8))
+    assert reps[0].status == "converged" and reps[0].iterations == 0 and np.all(x == 0)
+    # zero contrast: A = identity, converges in one iteration with U = rhs
+    grid0 = emie.make_grid(model, list(g["breaks"]), int(g["nx"]), int(g["ny"]), float(g["hx"]), float(g["hy"]))
+    x, reps = emie.solve_cie(grid0, model, sop, g["rhs"][0], emie.SolverConfig(tol=1e-8))
+    assert reps[0].status == "converged" and reps[0].iterations == 1
+    assert np.max(np.abs(x - g["rhs"][0])) <= 1e-14 * np.max(np.abs(g["rhs"][0]))
+
+
+def test_bad_config(torch_cuda):
+    g, model, grid, sop = _cfg1()
+    with pytest.raises(emie.InvalidArgument):
+        emie.solve_cie(grid, model, sop, g["rhs"][0], emie.SolverConfig(tol=0.0))
