@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the CIE operator apply (BASELINE.json metric: "CIE operator
+applies/s (complex128) at 128x128x32; Green's tensor build time").
+
+Workload (config 3, the reference's headline single-GPU config): the
+128x128x32 model of paper_1512_06126_b200/configs.py, 5-layer background,
+seeded log10 sigma in [-4, 1], 1 Hz, both MT polarisations. One step is one
+apply(SystemOperator) (include/emie/cie.hpp:39) on the two polarisations'
+fields (nrhs = 2, as FGMRES runs them in lockstep), so one step = 2 applies.
+The operator is built on the device by the Green's build (its wall time is
+reported as greens_build_s, the second half of the metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): weak scaling over independent
+frequencies (config 5's sweep): rank r owns frequency r, builds its own
+operator and applies it; there is no data-path collective. value = all
+ranks' applies / max-over-ranks device time.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref, compiled from its sources) of the same apply on this host's
+cores, same workload and metric; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CIE operator applies/s (complex128) at 128x128x32"
+UNIT = "applies/s"
+NRHS = 2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=self.out, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.out.flush()
+        rows = [r.split(",") for r in Path(self.out.name).read_text().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        os.unlink(self.out.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------ reference arm ----
+def write_case(cfg, path, omega):
+    import ref_binding as R
+    R.write_case(path, cfg.tops, cfg.sigma, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy, omega,
+                 cfg.sigma_a)
+
+
+def reference_apply_rate(cfg, reps, threads=None):
+    """The reference's apply(SystemOperator) (src/cie.cpp:56-73) timed on the
+    host cores through oracle/_ref/emie_ref_tool (all OpenMP threads)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_binding as R
+    if not R.TOOL.exists():
+        R.build()
+    with tempfile.TemporaryDirectory() as td:
+        case = Path(td) / "case.bin"
+        write_case(cfg, case, cfg.omega)
+        out = R.run_tool("bench-apply", case, reps, NRHS, threads=threads)
+    d = json.loads(out)
+    return d
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1512_06126_b200 import configs
+    cfg = configs.config(args.config)
+    threads = os.cpu_count()
+    d = reference_apply_rate(cfg, args.warmup + args.steps, threads=threads)
+    times = d["times"][args.warmup:]
+    tot = float(np.sum(times))
+    value = NRHS * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic (seeded config-3 conductivity; operator values synthetic, same shape)",
+        "config": {"workload": "cfg3 128x128x32, apply(SystemOperator), 2 polarisations",
+                   "nrhs": NRHS, "threads": d["threads"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": d["threads"], "kind": "reference",
+                         "sample": f"{len(times)} steps x {NRHS} applies at cfg3 (reference apply, "
+                                   "OpenMP, FFTW-API shim)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- our arm ----
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import paper_1512_06126_b200 as emie
+    from paper_1512_06126_b200 import configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = configs.config(args.config)
+    freqs = configs.config(5).freqs
+    freq = cfg.freqs[0] if world == 1 else freqs[rank % len(freqs)]
+    omega = 2.0 * np.pi * freq
+    model = emie.LayeredModel(cfg.tops, cfg.sigma)
+    grid = emie.make_grid(model, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy)
+    grid.sigma_a[...] = cfg.sigma_a
+
+    L = emie.lib()
+    # Green's build on the device (wall time, device synchronised)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    operator_src = "device Green's build"
+    try:
+        sop = emie.assemble_operator(grid, model, omega)
+    except emie.EmieRuntimeError:
+        operator_src = "synthetic compressed blocks (device Green's build unavailable)"
+        rng = np.random.default_rng(5)
+        nent = 2 * cfg.nz * (2 * cfg.nz + 1)
+        blocks = (rng.standard_normal((cfg.ny, cfg.nx, nent)) +
+                  1j * rng.standard_normal((cfg.ny, cfg.nx, nent))) * 1e-3
+        sop = emie.transform_operator(blocks, cfg.nx, cfg.ny, cfg.nz, omega)
+    torch.cuda.synchronize()
+    greens_s = time.perf_counter() - t0
+    system = emie.build_system(grid, sop)
+
+    n = 3 * cfg.cells()
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    U = torch.complex(torch.rand(NRHS * n, device="cuda", dtype=torch.float64, generator=g) * 2 - 1,
+                      torch.rand(NRHS * n, device="cuda", dtype=torch.float64, generator=g) * 2 - 1)
+    W = torch.empty_like(U)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step():
+        emie._check(L.emie_cu_apply_system(system.handle, ctypes.c_void_p(U.data_ptr()),
+                                           ctypes.c_void_p(W.data_ptr()), NRHS, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    L.emie_cu_profile_enable.argtypes = [ctypes.c_int]
+    L.emie_cu_profile_collect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    L.emie_cu_probe_fp64.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
+    ms5 = np.zeros(5)
+    cnt5 = np.zeros(5, np.int64)
+    emie._check(L.emie_cu_profile_collect(ms5.ctypes.data, cnt5.ctypes.data, 5))  # drain
+    emie._check(L.emie_cu_profile_enable(1))
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.4)
+    L.emie_cu_reset_launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = int(L.emie_cu_launch_count())
+    clk = clocks.stop()
+    emie._check(L.emie_cu_profile_enable(0))
+    emie._check(L.emie_cu_profile_collect(ms5.ctypes.data, cnt5.ctypes.data, 5))
+    ms = e0.elapsed_time(e1)
+    tmax = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    value = world * NRHS * args.steps / (ms_max * 1e-3)
+
+    # end to end through the reference-facing host-buffer C-ABI call
+    hin = torch.empty(NRHS * n, dtype=torch.complex128).pin_memory()
+    hout = torch.empty(NRHS * n, dtype=torch.complex128).pin_memory()
+    hin.copy_(U.cpu())
+    for _ in range(2):
+        emie._check(L.emie_cu_apply_system_host(system.handle, ctypes.c_void_p(hin.data_ptr()),
+                                                ctypes.c_void_p(hout.data_ptr()), NRHS, sp))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        emie._check(L.emie_cu_apply_system_host(system.handle, ctypes.c_void_p(hin.data_ptr()),
+                                                ctypes.c_void_p(hout.data_ptr()), NRHS, sp))
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * NRHS * args.e2e_steps / float(e2e_s.item())
+
+    # roofline of the dominant kernel (the per-mode contraction)
+    nz = cfg.nz
+    modes = sop.qx * sop.qy
+    E = sop.ex * sop.ey
+    nent = 2 * nz * (2 * nz + 1)
+    bytes_ct = modes * nent * 16 + 2 * NRHS * E * 3 * nz * 16
+    flops_ct = NRHS * 72.0 * nz * nz * E
+    ct_ms = ms5[2] / max(1, cnt5[2])
+    hbm, hbm_kind = peaks()
+    fp64 = ctypes.c_double(0.0)
+    emie._check(L.emie_cu_probe_fp64(ctypes.byref(fp64), sp))
+    achieved = bytes_ct / (ct_ms * 1e-3) / 1e9
+    stage_names = ["fwd_x_fft", "fwd_y_fft", "contraction", "inv_y_fft", "inv_x_fft_epilogue"]
+    stages = {nm: round(float(ms5[i] / max(1, cnt5[i])), 4) for i, nm in enumerate(stage_names)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            d = reference_apply_rate(cfg, 4, threads=os.cpu_count())
+            times = d["times"][1:]
+            cpu = {"value": NRHS * len(times) / float(np.sum(times)), "unit": UNIT,
+                   "cores": d["threads"], "kind": "reference",
+                   "sample": f"{len(times)} steps x {NRHS} applies of the reference apply(SystemOperator) "
+                             "at cfg3 shape (oracle/_ref, OpenMP, FFTW-API shim)"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded config-3 conductivity field, seeded fields)",
+            "config": {"workload": "cfg3 128x128x32 (5-layer background), apply(SystemOperator) on both "
+                                   "MT polarisations per step (nrhs=2)",
+                       "nrhs": NRHS, "frequency_hz": freq if world == 1 else "one config-5 frequency per rank",
+                       "operator": operator_src,
+                       "l2": "inputs larger than L2 (1.1 GB operator streamed per step)",
+                       "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
+            "greens_build_s": greens_s,
+            "stage_ms": stages,
+            "roofline": {"bound": "hbm", "kernel": "contract_kernel", "achieved": achieved,
+                         "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_source": hbm_kind, "traffic": None,
+                         "bytes_per_launch": bytes_ct,
+                         "fp64": {"achieved_tflops": flops_ct / (ct_ms * 1e-3) / 1e12,
+                                  "peak_tflops": fp64.value, "peak_source": "emie_cu_probe_fp64 (DFMA loop, this GPU)",
+                                  "frac": (flops_ct / (ct_ms * 1e-3) / 1e12) / fp64.value if fp64.value else None}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": NRHS * n * 16,
+                    "d2h_bytes_per_step": NRHS * n * 16},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

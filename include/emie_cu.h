@@ -95,6 +95,12 @@ int emie_cu_operator_download_blocks(emie_cu_operator op, double* h_blocks);
 int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy,
                                   const double* filter, double* h_w, double* h_lam);
 
+/* kernel_output (hankel.hpp:32, hankel.cpp:101-113): the closed-form design
+ * output of the (alpha, beta) kernel at log radii s[n], as the device filter
+ * design samples it */
+int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int beta,
+                          const double* h_s, int n, double* h_out);
+
 void emie_cu_operator_destroy(emie_cu_operator op);
 
 /* apply(const SpectralOperator&, const GridVector&) (toeplitz.hpp:43,
@@ -147,6 +153,18 @@ typedef struct {
 int emie_cu_fgmres(emie_cu_system sys, const double* d_rhs, double* d_x, int nrhs,
                    double tol, int restart, int max_iters, emie_cu_report* reports,
                    double* h_history, int hist_cap, void* stream);
+
+/* Stage profiling: when enabled, every apply brackets its kernels with CUDA
+ * events on the launching stream (stages: 0 fwd-x FFT, 1 fwd-y FFT,
+ * 2 contraction, 3 inv-y FFT, 4 inv-x FFT + epilogue). collect synchronises
+ * the recorded events and returns per-stage total milliseconds and launch
+ * counts (arrays of n entries) since the last collect. */
+int emie_cu_profile_enable(int on);
+int emie_cu_profile_collect(double* ms, long long* count, int n);
+
+/* FP64 throughput probe: a DFMA-bound kernel on the device (denominator of
+ * the FP64 roofline, which MEASURED_PEAKS.json does not carry) */
+int emie_cu_probe_fp64(double* tflops, void* stream);
 
 /* kernel launches issued by this library on the calling thread since the
  * last reset (evidence for bench.py's gpu_launches) */

@@ -111,6 +111,8 @@ def lib():
         "emie_cu_fgmres": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                            ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
         "emie_cu_device_count": [ip],
+        "emie_cu_kernel_output": [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                  ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -372,6 +374,15 @@ def design_offset_filters(oi: int, oj: int, hx: float, hy: float,
     _check(lib().emie_cu_design_offset_filters(int(oi), int(oj), float(hx), float(hy), _ptr(fp),
                                                _ptr(w), _ptr(lam)))
     return w, lam
+
+
+def kernel_output(oi: int, oj: int, hx: float, hy: float, alpha: int, beta: int, s) -> np.ndarray:
+    """hankel.hpp:32 evaluated on the device (the samples the filter design uses)."""
+    x = np.ascontiguousarray(np.atleast_1d(s), dtype=np.float64)
+    out = np.empty_like(x)
+    _check(lib().emie_cu_kernel_output(int(oi), int(oj), float(hx), float(hy), int(alpha), int(beta),
+                                       _ptr(x), x.size, _ptr(out)))
+    return out
 
 
 class SystemOperator:

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -92,18 +93,90 @@ __global__ void system_kernel(const cplx* __restrict__ sa, const cplx* __restric
 
 }  // namespace
 
+// ------------------------------------------------------------ profiling --
+namespace {
+constexpr int kStages = 8;
+struct Prof {
+  bool on = false;
+  std::mutex mu;
+  std::vector<cudaEvent_t> pool;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  cudaEvent_t open[kStages] = {};
+};
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+cudaEvent_t take_event(Prof& p) {
+  if (!p.pool.empty()) {
+    cudaEvent_t e = p.pool.back();
+    p.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  EMIE_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// DFMA-bound probe: 8 independent chains per thread
+__global__ void fp64_probe_kernel(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+  const double m = 0.999999999, c = 1e-12;
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.0) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+void profile_mark(int stage, bool begin, cudaStream_t st) {
+  Prof& p = prof();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> lk(p.mu);
+  cudaEvent_t e = take_event(p);
+  EMIE_CUDA(cudaEventRecord(e, st));
+  if (begin) {
+    p.open[stage] = e;
+  } else {
+    p.pending.push_back({stage, p.open[stage], e});
+    p.open[stage] = nullptr;
+  }
+}
+
 Operator::~Operator() {
   cudaFree(spec);
   cudaFree(blocks);
   cudaFree(tw_x);
   cudaFree(tw_y);
-  cudaFree(trilut);
+  cudaFree(emap);
 }
 
 System::~System() {
   cudaFree(s);
   cudaFree(r1);
   cudaFree(r2);
+}
+
+// Scratch comes from the stream-ordered pool; by default the pool trims to
+// zero at every synchronisation, which makes each synchronous call re-map
+// its workspaces. Keep what it holds.
+void keep_pool_warm() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  EMIE_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  EMIE_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ull;
+  EMIE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = true;
 }
 
 cplx* upload_twiddles(int n) {
@@ -131,17 +204,36 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.ntri = nz * (nz + 1) / 2;
   op.nfull = nz * nz;
   op.nent = 4 * op.ntri + 2 * op.nfull;
+  op.nsd = nz / 2 + 1;
+  op.nentD = 4 * op.nsd * nz + 2 * op.nfull;
   if (!make_plan(op.ex, op.plan_x) || !make_plan(op.ey, op.plan_y))
     fail(EMIE_CU_RUNTIME_ERROR, "toeplitz: planning failed");
-  op.spec = dev_alloc<cplx>(op.modes() * op.nent);
+  keep_pool_warm();
+  op.spec = dev_alloc<cplx>(op.modes() * op.nentD);
   op.tw_x = upload_twiddles(op.ex);
   op.tw_y = upload_twiddles(op.ey);
-  std::vector<uint32_t> lut(op.ntri);
-  for (int k = 0; k < nz; ++k)
-    for (int kp = k; kp < nz; ++kp)
-      lut[k * nz - k * (k - 1) / 2 + (kp - k)] = (static_cast<uint32_t>(k) << 16) | kp;
-  op.trilut = dev_alloc<uint32_t>(op.ntri);
-  EMIE_CUDA(cudaMemcpy(op.trilut, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice));
+  // reference entry -> wrapped-diagonal slot(s) (see operator.cuh)
+  op.emap_host.assign(op.nent, int2{-1, -1});
+  for (int c = 0; c < 4; ++c)
+    for (int k = 0; k < nz; ++k)
+      for (int kp = k; kp < nz; ++kp) {
+        const int e = c * op.ntri + k * nz - k * (k - 1) / 2 + (kp - k);
+        const int t = kp - k, base = c * op.nsd * nz;
+        int2 m{-1, -1};
+        if (t < nz - t) m.x = base + t * nz + k;
+        else if (t > nz - t) m.x = base + (nz - t) * nz + kp;
+        else { m.x = base + t * nz + k; m.y = base + t * nz + kp; }
+        op.emap_host[e] = m;
+      }
+  for (int c = 0; c < 2; ++c)
+    for (int k = 0; k < nz; ++k)
+      for (int kp = 0; kp < nz; ++kp) {
+        const int e = 4 * op.ntri + c * op.nfull + k * nz + kp;
+        const int t = ((kp - k) % nz + nz) % nz;
+        op.emap_host[e] = int2{4 * op.nsd * nz + c * op.nfull + t * nz + k, -1};
+      }
+  op.emap = dev_alloc<int2>(op.nent);
+  EMIE_CUDA(cudaMemcpy(op.emap, op.emap_host.data(), op.nent * sizeof(int2), cudaMemcpyHostToDevice));
 }
 
 }  // namespace emie_cu
@@ -243,16 +335,17 @@ int emie_cu_operator_download_spectra(emie_cu_operator h, double* h_comp) {
   return guarded([&] {
     if (!h || !h_comp) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
     const Operator& op = h->op;
-    std::vector<cplx> mm(op.modes() * op.nent);
+    std::vector<cplx> mm(op.modes() * op.nentD);
     EMIE_CUDA(cudaMemcpy(mm.data(), op.spec, mm.size() * sizeof(cplx), cudaMemcpyDeviceToHost));
-    // mode-major packed -> six component arrays (toeplitz.hpp:58-61)
+    // diagonal-layout mode blocks -> six component arrays (toeplitz.hpp:58-61)
     cplx* o = reinterpret_cast<cplx*>(h_comp);
     const std::size_t modes = op.modes();
     for (int c = 0; c < 6; ++c) {
       const int nent_c = c < 4 ? op.ntri : op.nfull;
       const int off = c < 4 ? c * op.ntri : 4 * op.ntri + (c - 4) * op.nfull;
       for (std::size_t m = 0; m < modes; ++m)
-        std::memcpy(o + m * nent_c, mm.data() + m * op.nent + off, nent_c * sizeof(cplx));
+        for (int s = 0; s < nent_c; ++s)
+          o[m * nent_c + s] = mm[m * op.nentD + op.emap_host[off + s].x];
       o += modes * nent_c;
     }
   });
@@ -373,4 +466,64 @@ extern "C" int emie_cu_fgmres(emie_cu_system h, const double* d_rhs, double* d_x
     fgmres_device(h->sys, reinterpret_cast<const cplx*>(d_rhs), reinterpret_cast<cplx*>(d_x),
                   nrhs, tol, restart, max_iters, reports, h_history, hist_cap, as_stream(stream));
   });
+}
+
+extern "C" int emie_cu_profile_enable(int on) {
+  return guarded([&] { prof().on = on != 0; });
+}
+
+extern "C" int emie_cu_profile_collect(double* ms, long long* count, int n) {
+  return guarded([&] {
+    Prof& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    for (int i = 0; i < n; ++i) {
+      if (ms) ms[i] = 0.0;
+      if (count) count[i] = 0;
+    }
+    for (const auto& r : p.pending) {
+      EMIE_CUDA(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      EMIE_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      if (r.stage < n) {
+        if (ms) ms[r.stage] += t;
+        if (count) count[r.stage] += 1;
+      }
+      p.pool.push_back(r.a);
+      p.pool.push_back(r.b);
+    }
+    p.pending.clear();
+  });
+}
+
+extern "C" int emie_cu_probe_fp64(double* tflops, void* stream) {
+  return guarded([&] {
+    const cudaStream_t st = as_stream(stream);
+    int dev = 0, sms = 0;
+    EMIE_CUDA(cudaGetDevice(&dev));
+    EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* out = scratch<double>(1, st);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    EMIE_CUDA(cudaEventCreate(&a));
+    EMIE_CUDA(cudaEventCreate(&b));
+    fp64_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);  // warm-up
+    check_launch("fp64_probe_kernel");
+    EMIE_CUDA(cudaEventRecord(a, st));
+    for (int r = 0; r < 5; ++r) fp64_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);
+    check_launch("fp64_probe_kernel");
+    EMIE_CUDA(cudaEventRecord(b, st));
+    EMIE_CUDA(cudaEventSynchronize(b));
+    float t = 0.f;
+    EMIE_CUDA(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    release(out, st);
+    const double flops = 5.0 * 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    *tflops = flops / (t * 1e-3) / 1e12;
+  });
+}
+
+extern "C" int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int beta,
+                                     const double* h_s, int n, double* h_out) {
+  return guarded([&] { kernel_output_host(oi, oj, hx, hy, alpha, beta, h_s, n, h_out); });
 }

@@ -1,7 +1,657 @@
-// Green's-tensor build on the device (placeholder until the kernels land).
+// Green's-tensor build on the device (sm_100a): assemble_operator
+// (src/greens.cpp:332-371) + transform_operator (src/toeplitz.cpp:92-161).
+//
+//  K6 filter_design_kernel  one CTA per (offset, kernel): 2*half samples of
+//     the closed-form design output (hankel.cpp:35-113), FFT, division by the
+//     input spectrum, inverse FFT, 451-weight window (hankel.cpp:239-281).
+//  K5 assemble_kernel       one CTA per (offset, pair group): lambda in chunks
+//     of LC; per chunk the layer states (layered.cpp:67-129), interval packs
+//     and factors (layered.cpp:237-317) and chain prefix products are built
+//     in SMEM, then every thread advances its own interval pairs' seven
+//     accumulators over the chunk in lambda order (greens.cpp:167-191).
+//     Blocks are scaled by R^3/4pi, R^2/4pi, R/4pi (greens.cpp:193-213).
+//  K7 the spectra passes of operator.cu.
+//
+// Numerics kept from the reference: expm1-based
+// exponentials, exact one_p/one_q, the W11d/W20d jump-content choice, the
+// erfc tails, the lambda > 38 cutoff, the alternating-sign lattices. The
+// off-diagonal chain products prod_{l=k+1}^{kp-1} theta_l come from prefix
+// products kept as (mantissa, binary exponent, zero count), so an underflowed
+// theta zeroes exactly the chains that span it, as the running product does.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "operator.cuh"
 
 namespace emie_cu {
+
+namespace {
+
+constexpr double kMu0 = 1.2566370614359172e-06;  // include/emie/types.hpp:11
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr double kSqrtPi = 1.7724538509055160273;
+constexpr int kMaxLayers = 16;
+constexpr int kGreenThreads = 256;
+constexpr int kPairsPerThread = 3;
+
+// ------------------------------------------------------ complex helpers ----
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  // Smith's algorithm (no overflow for the magnitudes met here)
+  if (fabs(b.re) >= fabs(b.im)) {
+    const double r = b.im / b.re, d = b.re + b.im * r;
+    return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
+  }
+  const double r = b.re / b.im, d = b.re * r + b.im;
+  return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
+}
+__device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
+__device__ __forceinline__ cplx csqrt_pos(cplx z) {
+  // principal square root, then the Re > 0 branch (layered.cpp:87-89)
+  const double m = hypot(z.re, z.im);
+  cplx r;
+  if (m == 0.0) return {0.0, 0.0};
+  const double t = sqrt(0.5 * (fabs(z.re) + m));
+  if (z.re >= 0.0) r = {t, z.im / (2.0 * t)};
+  else r = {fabs(z.im) / (2.0 * t), copysign(t, z.im)};
+  if (r.re < 0.0) r = -r;
+  return r;
+}
+// exp(x) - 1 without cancellation (layered.cpp:19-25)
+__device__ __forceinline__ cplx cexpm1(cplx x) {
+  const double em = expm1(x.re);
+  double sh, ch;
+  sincos(0.5 * x.im, &sh, &ch);
+  double s, c;
+  sincos(x.im, &s, &c);
+  return {em * c - 2.0 * sh * sh, (em + 1.0) * s};
+}
+__device__ __forceinline__ cplx cexp(cplx x) {
+  const double e = exp(x.re);
+  double s, c;
+  sincos(x.im, &s, &c);
+  return {e * c, e * s};
+}
+__device__ __forceinline__ cplx scal2(cplx a, int e) { return {scalbn(a.re, e), scalbn(a.im, e)}; }
+
+// ------------------------------------------------------ hankel helpers ----
+__device__ __forceinline__ double ediff(double a, double b) {  // hankel.cpp:22-26
+  if (a > 1.0 && b > 1.0) return erfc(0.5 * a) - erfc(0.5 * b);
+  if (a < -1.0 && b < -1.0) return erfc(-0.5 * b) - erfc(-0.5 * a);
+  return erf(0.5 * b) - erf(0.5 * a);
+}
+
+__device__ void axis_stencil(int alpha, double d, double h, double out[3]) {  // hankel.cpp:35-71
+  const double wp = d + h, w0 = d, wm = d - h;
+  const double gp = exp(-0.25 * wp * wp);
+  const double g0 = exp(-0.25 * w0 * w0);
+  const double gm = exp(-0.25 * wm * wm);
+  const double gs = gp - 2.0 * g0 + gm;
+  const double ep = ediff(w0, wp);
+  const double em = ediff(wm, w0);
+  if (alpha == 0) {
+    const double lin = wp * ep - wm * em;
+    const double w2s = wp * wp * gp - 2.0 * w0 * w0 * g0 + wm * wm * gm;
+    out[0] = kSqrtPi * lin + 2.0 * gs;
+    out[1] = 2.0 * kSqrtPi * lin + 8.0 * gs;
+    out[2] = 12.0 * kSqrtPi * lin + 4.0 * w2s + 64.0 * gs;
+  } else if (alpha == 1) {
+    const double es = ep - em;
+    const double wg = wp * gp - 2.0 * w0 * g0 + wm * gm;
+    const double w3g = wp * wp * wp * gp - 2.0 * w0 * w0 * w0 * g0 + wm * wm * wm * gm;
+    out[0] = kSqrtPi * es;
+    out[1] = 2.0 * kSqrtPi * es - 2.0 * wg;
+    out[2] = 12.0 * kSqrtPi * es - 2.0 * w3g - 12.0 * wg;
+  } else {
+    out[0] = gs;
+    out[1] = wp * wp * gp - 2.0 * w0 * w0 * g0 + wm * wm * gm;
+    out[2] = wp * wp * wp * wp * gp - 2.0 * w0 * w0 * w0 * w0 * g0 + wm * wm * wm * wm * gm;
+  }
+}
+
+struct Geom {
+  double r, p, q, phi;
+};
+__host__ __device__ inline Geom pair_geometry(int oi, int oj, double hx, double hy) {  // hankel.cpp:80-91
+  const double ax = oj * hx - 0.5 * hx;
+  const double ay = oi * hy - 0.5 * hy;
+  Geom g;
+  g.r = hypot(ax, ay);
+  g.p = hx / g.r;
+  g.q = hy / g.r;
+  g.phi = atan2(ay, ax);
+  return g;
+}
+
+__device__ double kernel_output(const Geom& g, int alpha, int beta, double s) {  // hankel.cpp:101-113
+  const double r = exp(s);
+  const double hx = g.p * r, hy = g.q * r;
+  double sn, cs;
+  sincos(g.phi, &sn, &cs);
+  const double dx = r * cs + 0.5 * hx;
+  const double dy = r * sn + 0.5 * hy;
+  double ax[3], ay[3];
+  axis_stencil(alpha, dx, hx, ax);
+  axis_stencil(beta, dy, hy, ay);
+  const double comb = 0.25 * (ax[2] * ay[0] + 2.0 * ax[1] * ay[1] + ax[0] * ay[2]);
+  if (comb == 0.0) return 0.0;
+  return exp(-(3 - alpha - beta) * s) * comb;
+}
+
+__device__ __forceinline__ double design_input(double lambda) {  // hankel.cpp:93-99
+  if (lambda > 38.0) return 0.0;
+  const double l2 = lambda * lambda;
+  return 8.0 * exp(-l2) * lambda * ((l2 - 4.0) * l2 + 2.0);
+}
+
+__constant__ int kAlpha[6] = {0, 2, 0, 1, 1, 0};  // greens.cpp:137
+__constant__ int kBeta[6] = {0, 0, 2, 1, 0, 1};
+
+// ----------------------------------------------------------- K6 kernels ----
+// input spectrum of the design (FilterDesigner ctor, hankel.cpp:219-231)
+__global__ void filter_den_kernel(cplx* den, double* floor_out, const cplx* __restrict__ tw,
+                                  FftPlan pl, int half, double step) {
+  extern __shared__ cplx sm[];
+  const int n = pl.n, ld = n | 1;
+  cplx* a = sm;
+  cplx* b = a + ld;
+  cplx* t = b + ld;
+  load_twiddles(t, tw, n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int m = j - half;
+    const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
+    a[j] = {sign * design_input(exp(-m * step)), 0.0};
+  }
+  __syncthreads();
+  cplx* res = fft_smem(a, b, ld, 1, pl, t, false);
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    den[k] = res[k];
+    mx = fmax(mx, hypot(res[k].re, res[k].im));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) m = fmax(m, red[w]);
+    *floor_out = 1e-12 * m;
+  }
+}
+
+// FilterDesigner::design (hankel.cpp:239-281) for offset blockIdx.x (oi, oj
+// >= 0 row-major over ny x nx) and kernel blockIdx.y; err bits: 1 vanishing
+// input spectrum, 2 non-real residue
+__global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
+                                     const double* __restrict__ den_floor,
+                                     const cplx* __restrict__ tw, FftPlan pl, int half, double step,
+                                     double shift, int n1, int n2, int nx, double hx, double hy,
+                                     int* err, int fixed_oi, int fixed_oj) {
+  extern __shared__ cplx sm[];
+  const int n = pl.n, ld = n | 1;
+  cplx* a = sm;
+  cplx* b = a + ld;
+  cplx* t = b + ld;
+  const int off = blockIdx.x, kern = blockIdx.y;
+  const int oi = fixed_oi != INT32_MIN ? fixed_oi : off / nx;
+  const int oj = fixed_oi != INT32_MIN ? fixed_oj : off % nx;
+  const Geom g = pair_geometry(oi, oj, hx, hy);
+  const int alpha = kAlpha[kern], beta = kBeta[kern];
+  load_twiddles(t, tw, n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int m = j - half;
+    const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
+    a[j] = {sign * kernel_output(g, alpha, beta, m * step + shift), 0.0};
+  }
+  __syncthreads();
+  cplx* res = fft_smem(a, b, ld, 1, pl, t, false);
+  cplx* other = res == a ? b : a;
+  const double fl = *den_floor;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const cplx d = den[k];
+    if (hypot(d.re, d.im) < fl) atomicOr(err, 1);
+    res[k] = cdiv(res[k], d);
+  }
+  __syncthreads();
+  cplx* back = fft_smem(res, other, ld, 1, pl, t, true);
+  __shared__ double rmax[32], imax[32];
+  double rm = 0.0, im = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    rm = fmax(rm, fabs(back[k].re));
+    im = fmax(im, fabs(back[k].im));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    rm = fmax(rm, __shfl_down_sync(0xffffffffu, rm, o));
+    im = fmax(im, __shfl_down_sync(0xffffffffu, im, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rmax[threadIdx.x >> 5] = rm;
+    imax[threadIdx.x >> 5] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0, i = 0.0;
+    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) {
+      r = fmax(r, rmax[w]);
+      i = fmax(i, imax[w]);
+    }
+    if (i > 1e-10 * r) atomicOr(err, 2);
+  }
+  const int nw = n2 - n1 + 1;
+  double* wo = W + (static_cast<size_t>(off) * 6 + kern) * nw;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+    const int m = n1 + i;
+    const int j = ((m % n) + n) % n;
+    const double sign = (m % 2 != 0) ? -1.0 : 1.0;
+    wo[i] = sign * back[j].re / n;
+  }
+}
+
+// ----------------------------------------------------------- K5 kernel ----
+struct GreenParams {
+  int L;           // interfaces
+  int nz;
+  int nx, ny;
+  double hx, hy, omega;
+  int nw;          // weights per kernel
+  double step, shift;
+  int n1;
+  int LC;          // lambdas per chunk
+  int npairs;      // nz(nz+1)/2
+  int nent;
+  // model (host-filled)
+  double thick[kMaxLayers];
+  cplx sig[kMaxLayers];  // floored conductivities
+};
+
+// per-interval geometry (device arrays): a, b, h, d (top), dp (bottom), l
+struct Interval {
+  double a, b, h, d, dp, l;
+  int layer;
+  int has_p, has_q;
+  cplx inv_sig;  // 1 / sigma_b of the interval
+};
+
+// SMEM plan for one chunk of LC lambdas
+struct Chunk {
+  // layer states [lc][gamma][m]
+  cplx* eta;     // [lc][m]
+  cplx* e2l;     // [lc][m]
+  cplx* em1;     // [lc][m]
+  cplx* p;       // [lc][g][m]
+  cplx* q;
+  cplx* one_p;
+  cplx* one_q;
+  cplx* diag_a;
+  // interval fields [lc][f][j]
+  cplx* F;
+  int* E;        // [lc][4][j]: Pu_e, Pu_z, Pc_e, Pc_z
+};
+// interval field slots
+enum {
+  fH0u, fJ0u, fW00u, fPu, fPiu,
+  fH0c, fH1c, fJ0c, fJ1c, fW00c, fW10c, fW11c, fW20c, fPc, fPic,
+  fEta2, fThu, fThc, kFields
+};
+
+__global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
+    const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
+    cplx* __restrict__ blocks, int* err) {
+  extern __shared__ cplx sm[];
+  const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
+  const int off = blockIdx.x;
+  const int oi = off / P.nx, oj = off % P.nx;
+  const Geom g = pair_geometry(oi, oj, P.hx, P.hy);
+  const double R = g.r;
+  const double* Woff = W + static_cast<size_t>(off) * 6 * P.nw;
+  const double wmu = P.omega * kMu0;  // V1 = i wmu W00 (layered.cpp:400)
+
+  Chunk C;
+  {
+    cplx* s = sm;
+    C.eta = s; s += LC * NL;
+    C.e2l = s; s += LC * NL;
+    C.em1 = s; s += LC * NL;
+    C.p = s; s += LC * 2 * NL;
+    C.q = s; s += LC * 2 * NL;
+    C.one_p = s; s += LC * 2 * NL;
+    C.one_q = s; s += LC * 2 * NL;
+    C.diag_a = s; s += LC * 2 * NL;
+    C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
+    C.E = reinterpret_cast<int*>(s);
+  }
+  auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
+  auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 4 + f) * nz + j]; };
+
+  // this thread's pairs (k <= kp), triangle order
+  int pk[kPairsPerThread], pkp[kPairsPerThread];
+  bool pv[kPairsPerThread];
+  for (int i = 0; i < kPairsPerThread; ++i) {
+    const int s = blockIdx.y * kGreenThreads * kPairsPerThread + i * kGreenThreads + threadIdx.x;
+    pv[i] = s < P.npairs;
+    int k = 0, rem = pv[i] ? s : 0;
+    while (rem >= nz - k) { rem -= nz - k; ++k; }
+    pk[i] = k;
+    pkp[i] = k + rem;
+  }
+  // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k)
+  cplx acc[kPairsPerThread][9];
+  for (int i = 0; i < kPairsPerThread; ++i)
+    for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
+
+  const int nw = P.nw;
+  for (int t0 = 0; t0 < nw; t0 += LC) {
+    const int lc = min(LC, nw - t0);
+    __syncthreads();  // previous chunk consumed
+    // phase 0a: eta, e2l, em1 per (lambda, layer)
+    for (int x = threadIdx.x; x < lc * NL; x += blockDim.x) {
+      const int li = x / NL, m = x - li * NL;
+      const double lam = exp((P.n1 + t0 + li) * P.step + P.shift) / R;
+      const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
+      const cplx eta = csqrt_pos(eta2);
+      C.eta[li * NL + m] = eta;
+      if (m == 0 || m == L) {
+        C.e2l[li * NL + m] = {1.0, 0.0};
+        C.em1[li * NL + m] = {0.0, 0.0};
+      } else {
+        const cplx e = cexpm1((-2.0 * P.thick[m]) * eta);
+        C.e2l[li * NL + m] = cplx{1.0, 0.0} + e;
+        C.em1[li * NL + m] = -e;
+      }
+    }
+    __syncthreads();
+    // phase 0b: reflection chains per (lambda, gamma, direction) (layered.cpp:107-122)
+    for (int x = threadIdx.x; x < lc * 4; x += blockDim.x) {
+      const int li = x >> 2, gm = (x >> 1) & 1, dir = x & 1;
+      const cplx* eta = C.eta + li * NL;
+      const cplx* e2l = C.e2l + li * NL;
+      const cplx* em1 = C.em1 + li * NL;
+      const int base = (li * 2 + gm) * NL;
+      if (dir == 0) {
+        cplx* p = C.p + base;
+        cplx* op = C.one_p + base;
+        p[0] = {0.0, 0.0};
+        op[0] = {1.0, 0.0};
+        for (int m = 0; m < L; ++m) {
+          const cplx t = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - op[m]), em1[m] + e2l[m] * op[m]);
+          const cplx alpha = gm ? cdiv(P.sig[m + 1], P.sig[m]) : cplx{1.0, 0.0};
+          const cplx w = alpha * cdiv(eta[m], eta[m + 1]) * t;
+          p[m + 1] = cdiv(cplx{1.0, 0.0} + w, cplx{1.0, 0.0} - w);
+          op[m + 1] = cdiv(cplx{2.0, 0.0}, cplx{1.0, 0.0} - w);
+        }
+      } else {
+        cplx* q = C.q + base;
+        cplx* oq = C.one_q + base;
+        q[L] = {0.0, 0.0};
+        oq[L] = {1.0, 0.0};
+        for (int m = L; m > 0; --m) {
+          const cplx u = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - oq[m]), em1[m] + e2l[m] * oq[m]);
+          const cplx beta = gm ? cdiv(P.sig[m - 1], P.sig[m]) : cplx{1.0, 0.0};
+          const cplx w = beta * cdiv(eta[m], eta[m - 1]) * u;
+          q[m - 1] = cdiv(cplx{1.0, 0.0} + w, cplx{1.0, 0.0} - w);
+          oq[m - 1] = cdiv(cplx{2.0, 0.0}, cplx{1.0, 0.0} - w);
+        }
+      }
+    }
+    __syncthreads();
+    // phase 0c: diag_a (layered.cpp:124-126)
+    for (int x = threadIdx.x; x < lc * 2 * NL; x += blockDim.x) {
+      const int li = x / (2 * NL), r = x - li * 2 * NL;
+      const int m = r % NL;
+      const cplx eta = C.eta[li * NL + m], e2l = C.e2l[li * NL + m], em1 = C.em1[li * NL + m];
+      const cplx pq = C.p[li * 2 * NL + r] * C.q[li * 2 * NL + r];
+      C.diag_a[li * 2 * NL + r] = crecip(eta * (em1 + e2l * (cplx{1.0, 0.0} - pq)));
+    }
+    __syncthreads();
+    // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317)
+    for (int x = threadIdx.x; x < lc * nz; x += blockDim.x) {
+      const int li = x / nz, j = x - li * nz;
+      const Interval I = iv[j];
+      const cplx eta = C.eta[li * NL + I.layer];
+      const cplx ehm1 = cexpm1(-I.h * eta);
+      const cplx eh = cplx{1.0, 0.0} + ehm1;
+      const cplx el2 = C.e2l[li * NL + I.layer];
+      cplx epa = {1.0, 0.0}, epa2m1 = {0.0, 0.0}, epabm1 = {0.0, 0.0}, epb2m1 = {0.0, 0.0};
+      cplx eqb = {1.0, 0.0}, eqabm1 = {0.0, 0.0};
+      if (I.has_p) {
+        const cplx epam1 = cexpm1(-(I.a - I.d) * eta);
+        const cplx epbm1 = epam1 + ehm1 + epam1 * ehm1;
+        epa = cplx{1.0, 0.0} + epam1;
+        epa2m1 = 2.0 * epam1 + epam1 * epam1;
+        epabm1 = epam1 + epbm1 + epam1 * epbm1;
+        epb2m1 = 2.0 * epbm1 + epbm1 * epbm1;
+      }
+      if (I.has_q) {
+        const cplx eqbm1 = cexpm1(-(I.dp - I.b) * eta);
+        const cplx eqam1 = eqbm1 + ehm1 + eqbm1 * ehm1;
+        eqb = cplx{1.0, 0.0} + eqbm1;
+        eqabm1 = eqam1 + eqbm1 + eqam1 * eqbm1;
+      }
+      const cplx elh = (I.has_p && I.has_q) ? cexp((-(2.0 * I.l - I.h)) * eta) : cplx{0.0, 0.0};
+      const cplx u = -ehm1;
+      const cplx eta2 = eta * eta;
+      F(li, fEta2, j) = eta2;
+      for (int gm = 0; gm < 2; ++gm) {
+        const int r = li * 2 * NL + gm * NL + I.layer;
+        const cplx p = C.p[r], q = C.q[r], A = C.diag_a[r];
+        const cplx one_p = C.one_p[r], one_q = C.one_q[r];
+        const cplx Sa = one_p + p * epa2m1;
+        const cplx Sab = one_p + p * epabm1;
+        const cplx Mab = (cplx{2.0, 0.0} - one_p) - p * epabm1;
+        const cplx Dp = one_p + p * epb2m1;
+        const cplx Tq = one_q + q * eqabm1;
+        const cplx TMq = (cplx{2.0, 0.0} - one_q) - q * eqabm1;
+        const cplx theta = cdiv(eh * Sa, Dp);
+        const cplx H0 = cdiv(u * Sab, eta * Dp);
+        const cplx J0 = cdiv(A * u * Sa * Tq, eta);
+        const cplx Ip = cdiv(epa * u, eta);
+        const cplx Iq = cdiv(eqb * u, eta);
+        const cplx Sp = p * Ip * Ip, Sq = q * Iq * Iq;
+        const cplx M0 = cdiv(2.0 * (I.h * eta + ehm1), eta2);
+        const cplx P0 = 2.0 * (cdiv(elh * u, eta2) - cdiv(I.h * el2, eta));
+        const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
+        if (gm == 0) {
+          F(li, fH0u, j) = H0;
+          F(li, fJ0u, j) = J0;
+          F(li, fW00u, j) = W00d;
+          F(li, fThu, j) = theta;
+        } else {
+          F(li, fH0c, j) = H0;
+          F(li, fH1c, j) = cdiv(u * Mab, Dp);
+          F(li, fJ0c, j) = J0;
+          F(li, fJ1c, j) = -(A * u * Sa * TMq);
+          F(li, fW00c, j) = W00d;
+          F(li, fW10c, j) = A * eta * (Sq - Sp);
+          F(li, fW11c, j) = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) -
+                            cplx{2.0 * I.h, 0.0};
+          F(li, fW20c, j) = eta2 * W00d - cplx{2.0 * I.h, 0.0};
+          F(li, fThc, j) = theta;
+        }
+      }
+    }
+    __syncthreads();
+    // phase 1b: prefix products of theta per (lambda, gamma) as
+    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l
+    for (int x = threadIdx.x; x < lc * 2; x += blockDim.x) {
+      const int li = x >> 1, gm = x & 1;
+      const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
+      cplx m = {1.0, 0.0};
+      int e = 0, z = 0;
+      for (int j = 0; j < nz; ++j) {
+        F(li, fP, j) = m;
+        F(li, fPi, j) = crecip(m);
+        Ei(li, gm * 2, j) = e;
+        Ei(li, gm * 2 + 1, j) = z;
+        const cplx th = F(li, fT, j);
+        if (th.re == 0.0 && th.im == 0.0) {
+          ++z;
+        } else {
+          m = m * th;
+          const double a = fmax(fabs(m.re), fabs(m.im));
+          const int s = ilogb(a);
+          m = scal2(m, -s);
+          e += s;
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: pairs x lambdas (greens.cpp:167-191)
+    for (int li = 0; li < lc; ++li) {
+      const int t = t0 + li;
+      const double lam = exp((P.n1 + t) * P.step + P.shift) / R;
+      const double w00 = Woff[0 * nw + t], w20 = Woff[1 * nw + t], w02 = Woff[2 * nw + t];
+      const double w11 = Woff[3 * nw + t], w10 = Woff[4 * nw + t], w01 = Woff[5 * nw + t];
+#pragma unroll
+      for (int i = 0; i < kPairsPerThread; ++i) {
+        if (!pv[i]) continue;
+        const int k = pk[i], kp = pkp[i];
+        const cplx isk = iv[k].inv_sig;
+        cplx W00u, W00c, W10c, W11c, W20c, W01c;
+        if (k == kp) {
+          W00u = F(li, fW00u, k);
+          W00c = F(li, fW00c, k);
+          W10c = F(li, fW10c, k);
+          W01c = W10c;
+          W11c = F(li, fW11c, k);
+          W20c = F(li, fW20c, k);
+        } else {
+          cplx Cu = {1.0, 0.0}, Cc = {1.0, 0.0};
+          if (kp > k + 1) {
+            Cu = (Ei(li, 1, kp) != Ei(li, 1, k + 1))
+                     ? cplx{0.0, 0.0}
+                     : scal2(F(li, fPu, kp) * F(li, fPiu, k + 1), Ei(li, 0, kp) - Ei(li, 0, k + 1));
+            Cc = (Ei(li, 3, kp) != Ei(li, 3, k + 1))
+                     ? cplx{0.0, 0.0}
+                     : scal2(F(li, fPc, kp) * F(li, fPic, k + 1), Ei(li, 2, kp) - Ei(li, 2, k + 1));
+          }
+          W00u = (F(li, fH0u, k) * Cu) * F(li, fJ0u, kp);
+          const cplx a0 = F(li, fH0c, k) * Cc, a1 = F(li, fH1c, k) * Cc;
+          W00c = a0 * F(li, fJ0c, kp);
+          W01c = a0 * F(li, fJ1c, kp);
+          W10c = a1 * F(li, fJ0c, kp);
+          W11c = a1 * F(li, fJ1c, kp);
+          W20c = F(li, fEta2, k) * W00c;
+        }
+        // v_functions (layered.cpp:397-408) at (k, kp)
+        const cplx V1 = {-wmu * W00u.im, wmu * W00u.re};
+        const cplx V2 = {-wmu * W00c.im, wmu * W00c.re};
+        const cplx V3 = -(W11c * isk);
+        const cplx V4 = W10c * isk;
+        const cplx V5 = W20c * isk;
+        const cplx f4 = lam * V4;
+        acc[i][5] = acc[i][5] + w10 * f4;
+        acc[i][6] = acc[i][6] + w01 * f4;
+        const cplx f2 = (V1 + V3) * (1.0 / lam);
+        acc[i][0] = acc[i][0] + w00 * (lam * V1);
+        acc[i][1] = acc[i][1] + w20 * f2;
+        acc[i][2] = acc[i][2] + w02 * f2;
+        acc[i][3] = acc[i][3] + w11 * f2;
+        acc[i][4] = acc[i][4] + w00 * (lam * (V2 + V5));
+        if (k != kp) {
+          // lower entry (kp, k): W10c(kp,k) = (sig_kp / sig_k) W01c(k,kp)
+          // (reciprocity, layered.cpp:363-376), V4 = W10c / sig_kp
+          const cplx ratio = P.sig[iv[kp].layer] * iv[k].inv_sig;
+          const cplx V4l = (ratio * W01c) * iv[kp].inv_sig;
+          const cplx f4l = lam * V4l;
+          acc[i][7] = acc[i][7] + w10 * f4l;
+          acc[i][8] = acc[i][8] + w01 * f4l;
+        }
+      }
+    }
+  }
+  // scale and store (greens.cpp:193-219)
+  const double c3 = R * R * R / (4.0 * kPi), c2 = R * R / (4.0 * kPi), c1 = R / (4.0 * kPi);
+  const int ntri = P.npairs, nfull = nz * nz;
+  cplx* blk = blocks + static_cast<size_t>(off) * P.nent;
+  bool bad = false;
+  for (int i = 0; i < kPairsPerThread; ++i) {
+    if (!pv[i]) continue;
+    const int k = pk[i], kp = pkp[i];
+    const int s = k * nz - k * (k - 1) / 2 + (kp - k);
+    cplx v[8];
+    v[0] = c3 * acc[i][0] + c1 * acc[i][1];
+    v[1] = c3 * acc[i][0] + c1 * acc[i][2];
+    v[2] = c3 * acc[i][4];
+    v[3] = c1 * acc[i][3];
+    v[4] = c2 * acc[i][5];
+    v[5] = c2 * acc[i][6];
+    v[6] = c2 * acc[i][7];
+    v[7] = c2 * acc[i][8];
+    for (int c = 0; c < 8; ++c) bad |= !isfinite(v[c].re) || !isfinite(v[c].im);
+    blk[s] = v[0];
+    blk[ntri + s] = v[1];
+    blk[2 * ntri + s] = v[2];
+    blk[3 * ntri + s] = v[3];
+    blk[4 * ntri + k * nz + kp] = v[4];
+    blk[4 * ntri + nfull + k * nz + kp] = v[5];
+    if (k != kp) {
+      blk[4 * ntri + kp * nz + k] = v[6];
+      blk[4 * ntri + nfull + kp * nz + k] = v[7];
+    }
+  }
+  if (bad) atomicOr(err, 4);
+}
+
+__global__ void kernel_output_kernel(Geom g, int alpha, int beta, const double* s, int n,
+                                     double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = kernel_output(g, alpha, beta, s[i]);
+}
+
+inline void set_smem(const void* fn, size_t bytes) {
+  EMIE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+}
+
+struct FilterBank {
+  FftPlan pl;
+  cplx* tw = nullptr;
+  cplx* den = nullptr;
+  double* floor = nullptr;
+};
+
+FilterBank make_filter_bank(const FilterParams& fp, cudaStream_t st) {
+  FilterBank fb;
+  const int n = 2 * fp.half;
+  if (!make_plan(n, fb.pl))
+    fail(EMIE_CU_INVALID_ARGUMENT, "filter params: transform length 2*half must be 2,3,5-smooth");
+  fb.tw = upload_twiddles(n);
+  fb.den = scratch<cplx>(n, st);
+  fb.floor = scratch<double>(1, st);
+  const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
+  set_smem(reinterpret_cast<const void*>(filter_den_kernel), smem);
+  filter_den_kernel<<<1, 256, smem, st>>>(fb.den, fb.floor, fb.tw, fb.pl, fp.half, fp.step);
+  check_launch("filter_den_kernel");
+  return fb;
+}
+
+void free_filter_bank(FilterBank& fb, cudaStream_t st) {
+  release(fb.den, st);
+  release(fb.floor, st);
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  cudaFree(fb.tw);
+}
+
+void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, int nx, double hx,
+                    double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
+                    int fixed_oj = 0) {
+  const int n = 2 * fp.half;
+  const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
+  set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
+  dim3 grid(noff, 6);
+  filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
+                                                fp.step, fp.shift, fp.n1, fp.n2, nx, hx, hy, err,
+                                                fixed_oi, fixed_oj);
+  check_launch("filter_design_kernel");
+}
+
+void raise_filter_errors(int e) {
+  if (e & 1) fail(EMIE_CU_RUNTIME_ERROR, "filter design: input spectrum vanishes at a used mode");
+  if (e & 2) fail(EMIE_CU_RUNTIME_ERROR, "filter design: weights have a non-real residue");
+}
+
+}  // namespace
 
 void check_filter_params(const FilterParams& par) {  // hankel.cpp:205-208
   if (!(par.step > 0.0) || !(par.shift > 0.0) || !(par.shift < 0.5 * par.step))
@@ -10,13 +660,154 @@ void check_filter_params(const FilterParams& par) {  // hankel.cpp:205-208
     fail(EMIE_CU_INVALID_ARGUMENT, "filter params: bad weight window");
 }
 
-void greens_build(Operator&, int, const double*, const cplx*, const double*, double, double,
-                  const FilterParams&, bool, cudaStream_t) {
-  fail(EMIE_CU_RUNTIME_ERROR, "greens_build: not built yet");
+void kernel_output_host(int oi, int oj, double hx, double hy, int alpha, int beta,
+                        const double* s, int n, double* out) {
+  if (!(hx > 0.0) || !(hy > 0.0))
+    fail(EMIE_CU_INVALID_ARGUMENT, "pair_geometry: cell sizes must be positive");
+  if (alpha < 0 || beta < 0 || alpha > 2 || beta > 2 || alpha + beta > 2)
+    fail(EMIE_CU_INVALID_ARGUMENT, "kernel orders: need alpha, beta >= 0 and alpha + beta <= 2");
+  if (n <= 0) return;
+  double* d = nullptr;
+  EMIE_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+  EMIE_CUDA(cudaMemcpy(d, s, n * sizeof(double), cudaMemcpyHostToDevice));
+  kernel_output_kernel<<<ceil_div(n, 256), 256>>>(pair_geometry(oi, oj, hx, hy), alpha, beta, d, n,
+                                                  d + n);
+  check_launch("kernel_output_kernel");
+  EMIE_CUDA(cudaMemcpy(out, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(d);
 }
 
-void design_offset_filters_host(int, int, double, double, const FilterParams&, double*, double*) {
-  fail(EMIE_CU_RUNTIME_ERROR, "design_offset_filters: not built yet");
+void design_offset_filters_host(int oi, int oj, double hx, double hy, const FilterParams& fp,
+                                double* w, double* lam) {
+  if (!(hx > 0.0) || !(hy > 0.0))
+    fail(EMIE_CU_INVALID_ARGUMENT, "pair_geometry: cell sizes must be positive");
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  FilterBank fb = make_filter_bank(fp, st);
+  const int nw = fp.n2 - fp.n1 + 1;
+  double* dW = scratch<double>(6 * nw, st);
+  int* err = scratch<int>(1, st);
+  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  design_filters(fb, fp, 1, 1, hx, hy, dW, err, st, oi, oj);
+  int e = 0;
+  EMIE_CUDA(cudaMemcpyAsync(w, dW, 6 * nw * sizeof(double), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  release(dW, st);
+  release(err, st);
+  free_filter_bank(fb, st);
+  raise_filter_errors(e);
+  for (int m = fp.n1; m <= fp.n2; ++m) lam[m - fp.n1] = std::exp(m * fp.step + fp.shift);
+}
+
+void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
+                  double hx, double hy, const FilterParams& fp, bool keep_blocks, cudaStream_t st) {
+  // ---- host validation: LayeredModel::validate, VerticalPartition::create,
+  // AnomalyGrid::validate (layered.cpp:53-65, 191-208; greens.cpp:18-35)
+  if (L < 1) fail(EMIE_CU_INVALID_ARGUMENT, "layered model needs at least one interface");
+  if (L + 1 > kMaxLayers) fail(EMIE_CU_INVALID_ARGUMENT, "layered model: too many layers for the device build");
+  for (int i = 0; i + 1 < L; ++i)
+    if (!(tops[i] < tops[i + 1])) fail(EMIE_CU_INVALID_ARGUMENT, "layered model: interface depths must increase");
+  for (int i = 0; i < L; ++i)
+    if (!std::isfinite(tops[i])) fail(EMIE_CU_INVALID_ARGUMENT, "layered model: non-finite depth");
+  for (int i = 0; i <= L; ++i)
+    if (!std::isfinite(sigma[i].re) || !std::isfinite(sigma[i].im))
+      fail(EMIE_CU_INVALID_ARGUMENT, "layered model: non-finite conductivity");
+  if (!(hx > 0.0) || !(hy > 0.0)) fail(EMIE_CU_INVALID_ARGUMENT, "grid: cell sizes must be positive");
+  const int nz = op.nz;
+  auto layer_of = [&](double z) {  // points on an interface belong below
+    return static_cast<int>(std::upper_bound(tops, tops + L, z) - tops);
+  };
+  auto top_of = [&](int m) { return m == 0 ? tops[0] : tops[m - 1]; };
+  auto bottom_of = [&](int m) { return m == L ? tops[L - 1] : tops[m]; };
+  GreenParams P{};
+  P.L = L;
+  P.nz = nz;
+  P.nx = op.nx;
+  P.ny = op.ny;
+  P.hx = hx;
+  P.hy = hy;
+  P.omega = op.omega;
+  P.nw = fp.n2 - fp.n1 + 1;
+  P.step = fp.step;
+  P.shift = fp.shift;
+  P.n1 = fp.n1;
+  P.npairs = op.ntri;
+  P.nent = op.nent;
+  for (int m = 0; m <= L; ++m) {
+    P.thick[m] = bottom_of(m) - top_of(m);
+    cplx s = sigma[m];
+    if (s.re < 1e-9) s.re = 1e-9;  // sigma_floored (layered.cpp:47-51)
+    P.sig[m] = s;
+  }
+  std::vector<Interval> ivh(nz);
+  for (int i = 0; i < nz; ++i) {
+    if (!(breaks[i] < breaks[i + 1])) fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition: breaks must increase");
+    const int m = layer_of(breaks[i]);
+    const double slack = 1e-7 * (1.0 + std::fabs(breaks[i + 1]));
+    if (m < L && breaks[i + 1] > bottom_of(m) + slack)
+      fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition: interval straddles a layer interface");
+    if (!(sigma[m].re > 0.0))
+      fail(EMIE_CU_INVALID_ARGUMENT,
+           "grid: interval in a non-conducting layer; the anomaly must be buried in the conductive section");
+    Interval& I = ivh[i];
+    I.a = breaks[i];
+    I.b = breaks[i + 1];
+    I.h = I.b - I.a;
+    I.layer = m;
+    I.d = top_of(m);
+    I.dp = bottom_of(m);
+    I.l = P.thick[m];
+    I.has_p = m > 0;
+    I.has_q = m < L;
+    const cplx s = P.sig[m];
+    const double dn = s.re * s.re + s.im * s.im;
+    I.inv_sig = {s.re / dn, -s.im / dn};
+  }
+  P.LC = std::max(1, std::min(32, 256 / nz));
+
+  keep_pool_warm();
+  const int noff = op.nx * op.ny;
+  FilterBank fb = make_filter_bank(fp, st);
+  double* W = scratch<double>(static_cast<size_t>(noff) * 6 * P.nw, st);
+  int* err = scratch<int>(1, st);
+  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  design_filters(fb, fp, noff, op.nx, hx, hy, W, err, st);
+
+  Interval* div = scratch<Interval>(nz, st);
+  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
+  cplx* blocks = nullptr;
+  EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(noff) * op.nent * sizeof(cplx) + 16));
+  const int NL = L + 1;
+  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 10 * NL + kFields * nz)) * sizeof(cplx) +
+                      static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
+  set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
+  const int groups = ceil_div(P.npairs, kGreenThreads * kPairsPerThread);
+  dim3 grid(noff, groups);
+  profile_mark(5, true, st);
+  assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err);
+  check_launch("assemble_kernel");
+  profile_mark(5, false, st);
+  int e = 0;
+  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  release(W, st);
+  release(err, st);
+  release(div, st);
+  free_filter_bank(fb, st);
+  if (e) {
+    cudaFree(blocks);
+    raise_filter_errors(e);
+    fail(EMIE_CU_DOMAIN_ERROR, "assemble_block: non-finite block entry");
+  }
+  profile_mark(6, true, st);
+  transform_blocks(op, blocks, st);
+  profile_mark(6, false, st);
+  if (keep_blocks) {
+    op.blocks = blocks;
+  } else {
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    cudaFree(blocks);
+  }
 }
 
 }  // namespace emie_cu

@@ -73,7 +73,8 @@ __global__ void spectra_x_kernel(const cplx* __restrict__ blocks, cplx* __restri
 // y pass over the x-transformed rows, parity-extended in oi; keep my < qy
 __global__ void spectra_y_kernel(const cplx* __restrict__ R, cplx* __restrict__ spec,
                                  const cplx* __restrict__ tw, FftPlan pl, int ny, int qx,
-                                 int qy, int nent, int ntri, int nfull, int EC) {
+                                 int qy, int nent, int ntri, int nfull, int EC,
+                                 const int2* __restrict__ emap, int nentD) {
   extern __shared__ cplx sm[];
   const int ey = pl.n, ld = smem_ld(ey);
   cplx* a = sm;
@@ -101,7 +102,13 @@ __global__ void spectra_y_kernel(const cplx* __restrict__ R, cplx* __restrict__ 
   for (int idx = threadIdx.x; idx < EC * qy; idx += blockDim.x) {
     const int tt = idx % EC, my = idx / EC;
     const int e = e0 + tt;
-    if (e < nent) spec[(static_cast<size_t>(my) * qx + mx) * nent + e] = res[tt * ld + my];
+    if (e < nent) {
+      const int2 m = emap[e];
+      cplx* blk = spec + (static_cast<size_t>(my) * qx + mx) * nentD;
+      const cplx v = res[tt * ld + my];
+      blk[m.x] = v;
+      if (m.y >= 0) blk[m.y] = v;
+    }
   }
 }
 
@@ -251,127 +258,105 @@ __global__ void apply_ix_kernel(const cplx* __restrict__ T, const cplx* __restri
 }
 
 // ------------------------------------------------------ contraction -------
-// One CTA per quadrant mode (qmy, qmx). The block's six stored components
-// are expanded in SMEM into symmetric / full 32x32 tiles (ld 33: row and
-// column walks are both bank-conflict free), then warp a in {x, y, z}
-// computes output rows (a, k) (lane = k) for CB columns at once; a column is
-// one (mirror mode, rhs) pair. Mirror modes reuse the quadrant block with
-// the fold signs D = diag(fx, fy, 1): M(mode) = D M(quadrant) D
-// (toeplitz.cpp:213-250), applied to the staged inputs and to the outputs.
-constexpr int kTile = 32;
-constexpr int kTld = kTile + 1;
-constexpr int kTsz = kTile * kTld;
+// Per quadrant mode (qmy, qmx): out = M u for the 3nz x 3nz coupling M of the
+// mode (toeplitz.cpp:197-258), applied to every mirror mode and rhs. Mirror
+// modes reuse the quadrant block with the fold signs D = diag(fx, fy, 1):
+// M(mirror) = D M D (toeplitz.cpp:213-250), folded into the staged inputs and
+// the outputs. One warp owns one mode at a time (persistent grid-stride over
+// modes); lane k computes output rows (x,k), (y,k), (z,k) for CB columns
+// (column = (mirror, rhs)), stepping t over the wrapped diagonals so every
+// coefficient load of the warp is one contiguous run (see operator.cuh).
+// The inputs of the mode sit in the warp's SMEM slot: lane k reads entry
+// (k + t) mod nz, 32 consecutive complex -> conflict-free.
+constexpr int kCtWarps = 8;
 
 template <int CB>
-__global__ void __launch_bounds__(96) contract_kernel(const cplx* __restrict__ op, cplx* S,
-                                                      const uint32_t* __restrict__ trilut, int nz,
-                                                      int ex, int ey, int qx, int nrhs,
-                                                      int ncolpad) {
+__global__ void __launch_bounds__(kCtWarps * 32, 1)
+    contract_kernel(const cplx* __restrict__ op, cplx* S, int nz, int nsd, int nentD, int ex,
+                    int ey, int qx, int nmodes, int nrhs) {
   extern __shared__ cplx sm[];
-  const int ntri = nz * (nz + 1) / 2, nfull = nz * nz, nent = 4 * ntri + 2 * nfull;
-  const int np = 3 * nz;
-  const size_t E = static_cast<size_t>(ex) * ey;
-  const int qm = blockIdx.x;
-  const int qmy = qm / qx, qmx = qm - qmy * qx;
-  const bool mx_ok = qmx > 0 && (ex - qmx) > ex / 2;
-  const bool my_ok = qmy > 0 && (ey - qmy) > ey / 2;
-  int mode[4];
-  double fxs[4], fys[4];
-  int nmir = 0;
-  mode[nmir] = qmy * ex + qmx; fxs[nmir] = 1.0; fys[nmir] = 1.0; ++nmir;
-  if (mx_ok) { mode[nmir] = qmy * ex + (ex - qmx); fxs[nmir] = -1.0; fys[nmir] = 1.0; ++nmir; }
-  if (my_ok) { mode[nmir] = (ey - qmy) * ex + qmx; fxs[nmir] = 1.0; fys[nmir] = -1.0; ++nmir; }
-  if (mx_ok && my_ok) { mode[nmir] = (ey - qmy) * ex + (ex - qmx); fxs[nmir] = -1.0; fys[nmir] = -1.0; ++nmir; }
-  const int ncol = nmir * nrhs;
-
-  // tiles: 0 xx, 1 yy, 2 zz, 3 xy, 4 xz(kb,kpb), 5 yz(kb,kpb), 6 xz(kpb,kb), 7 yz(kpb,kb)
-  cplx* tile = sm;
-  cplx* U = sm + 8 * kTsz;  // [col][plane], ncolpad columns
-  const cplx* blk = op + static_cast<size_t>(qm) * nent;
-
-  // stage the inputs of every column (zero-padded to ncolpad)
-  for (int i = threadIdx.x; i < ncolpad * np; i += blockDim.x) {
-    const int col = i / np, pl = i - col * np;
-    cplx v = {0.0, 0.0};
-    if (col < ncol) {
-      const int mi = col / nrhs, r = col - mi * nrhs;
-      v = S[(static_cast<size_t>(r) * E + mode[mi]) * np + pl];
-      const int c = pl / nz;
-      if (c == 0) v = fxs[mi] * v;
-      if (c == 1) v = fys[mi] * v;
-    }
-    U[i] = v;
-  }
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a = warp;  // output component
-  for (int kb = 0; kb < nz; kb += kTile) {
-    for (int cb = 0; cb < ncolpad; cb += CB) {
-      cplx acc[CB];
+  const int np = 3 * nz;
+  cplx* U = sm + static_cast<size_t>(warp) * CB * np;  // [col][plane]
+  const size_t E = static_cast<size_t>(ex) * ey;
+  const int gw = blockIdx.x * kCtWarps + warp, nw = gridDim.x * kCtWarps;
+  for (int qm = gw; qm < nmodes; qm += nw) {
+    const int qmy = qm / qx, qmx = qm - qmy * qx;
+    const bool mx_ok = qmx > 0 && (ex - qmx) > ex / 2;
+    const bool my_ok = qmy > 0 && (ey - qmy) > ey / 2;
+    int mode[4];
+    int nmir = 0;
+    mode[nmir++] = qmy * ex + qmx;
+    if (mx_ok) mode[nmir++] = qmy * ex + (ex - qmx);
+    if (my_ok) mode[nmir++] = (ey - qmy) * ex + qmx;
+    if (mx_ok && my_ok) mode[nmir++] = (ey - qmy) * ex + (ex - qmx);
+    // mirror mi's signs: x flipped for the 2nd (and 4th), y for the 3rd/4th
+    auto fx_of = [&](int mi) { return (mx_ok && (mi & 1)) ? -1.0 : 1.0; };
+    auto fy_of = [&](int mi) { return (my_ok && (mi >= (mx_ok ? 2 : 1))) ? -1.0 : 1.0; };
+    const int ncol = nmir * nrhs;
+    __syncwarp();
+    for (int i = lane; i < CB * np; i += 32) {
+      const int col = i / np, pl = i - col * np;
+      cplx v = {0.0, 0.0};
+      if (col < ncol) {
+        const int mi = col / nrhs, r = col - mi * nrhs;
+        v = S[(static_cast<size_t>(r) * E + mode[mi]) * np + pl];
+        const int c = pl / nz;
+        if (c == 0) v = fx_of(mi) * v;
+        if (c == 1) v = fy_of(mi) * v;
+      }
+      U[i] = v;
+    }
+    __syncwarp();
+    const cplx* blk = op + static_cast<size_t>(qm) * nentD;
+    const cplx* Dxx = blk;
+    const cplx* Dyy = blk + nsd * nz;
+    const cplx* Dzz = blk + 2 * nsd * nz;
+    const cplx* Dxy = blk + 3 * nsd * nz;
+    const cplx* Dxz = blk + 4 * nsd * nz;
+    const cplx* Dyz = Dxz + nz * nz;
+    for (int kb = 0; kb < nz; kb += 32) {
+      const int k = kb + lane;
+      const int kc = k < nz ? k : 0;
+      cplx ax[CB], ay[CB], az[CB];
 #pragma unroll
-      for (int c = 0; c < CB; ++c) acc[c] = {0.0, 0.0};
-      for (int kpb = 0; kpb < nz; kpb += kTile) {
-        __syncthreads();  // previous tile fully consumed (and U staged)
-        // stage tiles for rows kb.., cols kpb..
-        for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
-          const int dk = i / kTile, dkp = i - dk * kTile;
-          const int k = kb + dk, kp = kpb + dkp;
-          const int o = dk * kTld + dkp;
-          if (k < nz && kp < nz) {
-            const int lo = min(k, kp), hi = max(k, kp);
-            const int s = lo * nz - lo * (lo - 1) / 2 + (hi - lo);
-            tile[0 * kTsz + o] = ldg(blk + s);
-            tile[1 * kTsz + o] = ldg(blk + ntri + s);
-            tile[2 * kTsz + o] = ldg(blk + 2 * ntri + s);
-            tile[3 * kTsz + o] = ldg(blk + 3 * ntri + s);
-            tile[4 * kTsz + o] = ldg(blk + 4 * ntri + k * nz + kp);
-            tile[5 * kTsz + o] = ldg(blk + 4 * ntri + nfull + k * nz + kp);
-            // transposed pair: element (kp, k) stored at [dkp][dk]
-            tile[6 * kTsz + dkp * kTld + dk] = ldg(blk + 4 * ntri + kp * nz + k);
-            tile[7 * kTsz + dkp * kTld + dk] = ldg(blk + 4 * ntri + nfull + kp * nz + k);
-          } else {
-            const cplx z = {0.0, 0.0};
-            for (int m = 0; m < 6; ++m) tile[m * kTsz + o] = z;
-            tile[6 * kTsz + dkp * kTld + dk] = z;
-            tile[7 * kTsz + dkp * kTld + dk] = z;
-          }
-        }
-        __syncthreads();
-        // operand tiles of this warp's row component
-        //  x: xx, xy, xz      y: xy, yy, yz      z: -xz^T, -yz^T, zz
-        const cplx* A0 = tile + (a == 0 ? 0 : a == 1 ? 3 : 6) * kTsz;
-        const cplx* A1 = tile + (a == 0 ? 3 : a == 1 ? 1 : 7) * kTsz;
-        const cplx* A2 = tile + (a == 0 ? 4 : a == 1 ? 5 : 2) * kTsz;
-        const double sg = a == 2 ? -1.0 : 1.0;
-        const int kpn = min(kTile, nz - kpb);
-        for (int dkp = 0; dkp < kpn; ++dkp) {
-          // tiles 6/7 hold (kp, k) at [dkp][dk]: read with the row index swapped
-          const int o = lane * kTld + dkp;
-          const int ot = dkp * kTld + lane;
-          const cplx m0 = sg * A0[a == 2 ? ot : o];
-          const cplx m1 = sg * A1[a == 2 ? ot : o];
-          const cplx m2 = A2[o];
-          const int kp = kpb + dkp;
+      for (int c = 0; c < CB; ++c) ax[c] = ay[c] = az[c] = cplx{0.0, 0.0};
+      // t visited in pairs (0, 1, nz-1, 2, nz-2, ...): the two uses of each
+      // diagonal are adjacent, so the second hits L1
+      for (int i = 0; i < nz; ++i) {
+        const int t = (i == 0) ? 0 : ((i & 1) ? (i + 1) >> 1 : nz - (i >> 1));
+        int kp = kc + t;
+        if (kp >= nz) kp -= nz;
+        const bool lo = t <= nz - t;
+        const int so = (lo ? t : nz - t) * nz + (lo ? kc : kp);
+        const cplx mxx = ldg(Dxx + so), myy = ldg(Dyy + so), mzz = ldg(Dzz + so), mxy = ldg(Dxy + so);
+        const int tb = (t == 0) ? 0 : nz - t;
+        const cplx xz_k = ldg(Dxz + t * nz + kc), yz_k = ldg(Dyz + t * nz + kc);
+        const cplx xz_t = -ldg(Dxz + tb * nz + kp), yz_t = -ldg(Dyz + tb * nz + kp);
 #pragma unroll
-          for (int c = 0; c < CB; ++c) {
-            const cplx* uc = U + (cb + c) * np;
-            cmac(acc[c], m0, uc[kp]);
-            cmac(acc[c], m1, uc[nz + kp]);
-            cmac(acc[c], m2, uc[2 * nz + kp]);
-          }
+        for (int c = 0; c < CB; ++c) {
+          const cplx* u = U + c * np;
+          const cplx ux = u[kp], uy = u[nz + kp], uz = u[2 * nz + kp];
+          cmac(ax[c], mxx, ux);
+          cmac(ax[c], mxy, uy);
+          cmac(ax[c], xz_k, uz);
+          cmac(ay[c], mxy, ux);
+          cmac(ay[c], myy, uy);
+          cmac(ay[c], yz_k, uz);
+          cmac(az[c], xz_t, ux);
+          cmac(az[c], yz_t, uy);
+          cmac(az[c], mzz, uz);
         }
       }
-      const int k = kb + lane;
       if (k < nz) {
 #pragma unroll
         for (int c = 0; c < CB; ++c) {
-          const int col = cb + c;
-          if (col < ncol) {
-            const int mi = col / nrhs, r = col - mi * nrhs;
-            cplx v = acc[c];
-            if (a == 0) v = fxs[mi] * v;
-            if (a == 1) v = fys[mi] * v;
-            S[(static_cast<size_t>(r) * E + mode[mi]) * np + a * nz + k] = v;
+          if (c < ncol) {
+            const int mi = c / nrhs, r = c - mi * nrhs;
+            cplx* o = S + (static_cast<size_t>(r) * E + mode[mi]) * np;
+            o[k] = fx_of(mi) * ax[c];
+            o[nz + k] = fy_of(mi) * ay[c];
+            o[2 * nz + k] = az[c];
           }
         }
       }
@@ -407,7 +392,8 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st) {
     set_smem(reinterpret_cast<const void*>(spectra_y_kernel), smem);
     dim3 grid(op.qx, ceil_div(nent, EC));
     spectra_y_kernel<<<grid, 256, smem, st>>>(R, op.spec, op.tw_y, op.plan_y, op.ny, op.qx,
-                                              op.qy, nent, op.ntri, op.nfull, EC);
+                                              op.qy, nent, op.ntri, op.nfull, EC, op.emap,
+                                              op.nentD);
     check_launch("spectra_y_kernel");
   }
   release(R, st);
@@ -420,6 +406,7 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
   cplx* T = scratch<cplx>(static_cast<size_t>(rows) * op.ex, st);
   cplx* S = scratch<cplx>(static_cast<size_t>(nrhs) * op.lateral() * np, st);
   // K_fx
+  profile_mark(0, true, st);
   {
     const int RT = pick_rows(op.ex);
     const size_t smem = (2 * static_cast<size_t>(RT) * smem_ld(op.ex) + op.ex) * sizeof(cplx);
@@ -428,9 +415,11 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
         d_in, sys ? sys->r2 : nullptr, T, op.tw_x, op.plan_x, op.nx, op.ny, op.nz, rows, RT);
     check_launch("apply_fx_kernel");
   }
+  profile_mark(0, false, st);
   // K_fy
   const int XC = std::min(2, op.ex);
   const int PC = std::max(1, std::min(np, 2048 / (op.ey * XC)));
+  profile_mark(1, true, st);
   {
     const size_t smem =
         (2 * static_cast<size_t>(PC) * XC * smem_ld(op.ey) + op.ey) * sizeof(cplx);
@@ -439,30 +428,35 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
     apply_fy_kernel<<<grid, 256, smem, st>>>(T, S, op.tw_y, op.plan_y, op.ny, op.ex, np, PC, XC);
     check_launch("apply_fy_kernel");
   }
-  // K_ct
+  profile_mark(1, false, st);
+  // K_ct: up to two right-hand sides per launch (8 columns of a full mode)
+  profile_mark(2, true, st);
   {
-    const int ncolmax = 4 * nrhs;
-    int CB = 8;
-    if (ncolmax <= 1) CB = 1;
-    else if (ncolmax <= 2) CB = 2;
-    else if (ncolmax <= 4) CB = 4;
-    const int ncolpad = ceil_div(ncolmax, CB) * CB;
-    const size_t smem = (8 * static_cast<size_t>(kTsz) + static_cast<size_t>(ncolpad) * np) * sizeof(cplx);
-    const void* fn = CB == 8 ? reinterpret_cast<const void*>(contract_kernel<8>)
-                   : CB == 4 ? reinterpret_cast<const void*>(contract_kernel<4>)
-                   : CB == 2 ? reinterpret_cast<const void*>(contract_kernel<2>)
-                             : reinterpret_cast<const void*>(contract_kernel<1>);
-    set_smem(fn, smem);
-    const int grid = static_cast<int>(op.modes());
-    switch (CB) {
-      case 8: contract_kernel<8><<<grid, 96, smem, st>>>(op.spec, S, op.trilut, op.nz, op.ex, op.ey, op.qx, nrhs, ncolpad); break;
-      case 4: contract_kernel<4><<<grid, 96, smem, st>>>(op.spec, S, op.trilut, op.nz, op.ex, op.ey, op.qx, nrhs, ncolpad); break;
-      case 2: contract_kernel<2><<<grid, 96, smem, st>>>(op.spec, S, op.trilut, op.nz, op.ex, op.ey, op.qx, nrhs, ncolpad); break;
-      default: contract_kernel<1><<<grid, 96, smem, st>>>(op.spec, S, op.trilut, op.nz, op.ex, op.ey, op.qx, nrhs, ncolpad); break;
+    int sms = 0, dev = 0;
+    EMIE_CUDA(cudaGetDevice(&dev));
+    EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int nmodes = static_cast<int>(op.modes());
+    const int grid = std::max(1, std::min(sms, ceil_div(nmodes, kCtWarps)));
+    for (int r0 = 0; r0 < nrhs; r0 += 2) {
+      const int g = std::min(2, nrhs - r0);
+      cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
+      const int CB = g == 2 ? 8 : 4;
+      const size_t smem = static_cast<size_t>(kCtWarps) * CB * np * sizeof(cplx);
+      if (CB == 8) {
+        set_smem(reinterpret_cast<const void*>(contract_kernel<8>), smem);
+        contract_kernel<8><<<grid, kCtWarps * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD,
+                                                               op.ex, op.ey, op.qx, nmodes, g);
+      } else {
+        set_smem(reinterpret_cast<const void*>(contract_kernel<4>), smem);
+        contract_kernel<4><<<grid, kCtWarps * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD,
+                                                               op.ex, op.ey, op.qx, nmodes, g);
+      }
+      check_launch("contract_kernel");
     }
-    check_launch("contract_kernel");
   }
+  profile_mark(2, false, st);
   // K_iy
+  profile_mark(3, true, st);
   {
     const size_t smem =
         (2 * static_cast<size_t>(PC) * XC * smem_ld(op.ey) + op.ey) * sizeof(cplx);
@@ -471,7 +465,9 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
     apply_iy_kernel<<<grid, 256, smem, st>>>(S, T, op.tw_y, op.plan_y, op.ny, op.ex, np, PC, XC);
     check_launch("apply_iy_kernel");
   }
+  profile_mark(3, false, st);
   // K_ix
+  profile_mark(4, true, st);
   {
     const int RT = pick_rows(op.ex);
     const size_t smem = (2 * static_cast<size_t>(RT) * smem_ld(op.ex) + op.ex) * sizeof(cplx);
@@ -482,6 +478,7 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
         op.nx, op.ny, op.nz, rows, RT, inv);
     check_launch("apply_ix_kernel");
   }
+  profile_mark(4, false, st);
   release(S, st);
   release(T, st);
 }

@@ -12,20 +12,31 @@
 namespace emie_cu {
 
 // SpectralOperator (reference include/emie/toeplitz.hpp:21-35), device side.
-// Spectra layout (HBM): mode-major, one contiguous block per quadrant mode
-//   spec[(my*qx + mx)*nent + e],  e over xx yy zz xy (triangles) | xz yz (full)
-// i.e. the six reference components of one mode packed back to back, so the
-// contraction reads each mode's 2nz(2nz+1) complex as one contiguous run.
+// Spectra layout (HBM): mode-major, one contiguous block of nentD complex per
+// quadrant mode, each nz x nz component stored by WRAPPED DIAGONALS:
+//   full F (xz, yz):       D_t[k] = F(k, (k+t) mod nz),  t = 0..nz-1
+//   symmetric S (xx yy zz xy): D_t[k] = S(k, (k+t) mod nz), t = 0..nz/2
+//     (S(k,kp) with (kp-k) mod nz > nz/2 is D_{nz-t}[kp]; the other
+//      triangle entries appear once, the t = nz/2 ones twice for even nz)
+//   block = [xx | yy | zz | xy] (4 * nsd * nz) then [xz | yz] (2 * nz^2)
+// With lane k of a warp handling output row k, step t reads one contiguous
+// (rotated) 32-entry run of every diagonal: the contraction streams each
+// mode's coefficients straight from L2 with coalesced loads, no SMEM copy.
+// emap[e] maps reference entry e (GreensBlock order: triangles tri(k,kp)
+// then full k*nz+kp) to its diagonal slot(s).
 struct Operator {
   int nx = 0, ny = 0, nz = 0;
   int ex = 0, ey = 0, qx = 0, qy = 0;
   double omega = 0.0;
   int ntri = 0, nfull = 0, nent = 0;
-  cplx* spec = nullptr;      // qx*qy*nent
+  int nsd = 0, nentD = 0;    // symmetric diagonals per component, diag block size
+  cplx* spec = nullptr;      // qx*qy*nentD (diagonal layout)
+  int2* emap = nullptr;      // reference entry -> (slot, second slot or -1)
+  std::vector<int2> emap_host;
   cplx* blocks = nullptr;    // optional compressed blocks, (ny*nx)*nent
   cplx* tw_x = nullptr;      // e^{-2 pi i m/ex}
   cplx* tw_y = nullptr;      // e^{-2 pi i m/ey}
-  uint32_t* trilut = nullptr;  // triangle slot -> (k << 16) | kp
+
   FftPlan plan_x, plan_y;
 
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
@@ -45,6 +56,7 @@ struct System {
 
 // host helpers
 void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega);
+void keep_pool_warm();
 cplx* upload_twiddles(int n);
 
 // stages (operator.cu)
@@ -61,8 +73,13 @@ void check_filter_params(const FilterParams& fp);
 void greens_build(Operator& op, int L, const double* tops, const cplx* sigma,
                   const double* breaks, double hx, double hy, const FilterParams& fp,
                   bool keep_blocks, cudaStream_t st);
+void kernel_output_host(int oi, int oj, double hx, double hy, int alpha, int beta,
+                        const double* s, int n, double* out);
 void design_offset_filters_host(int oi, int oj, double hx, double hy, const FilterParams& fp,
                                 double* w, double* lam);
+
+// stage profiling (capi.cu): no-ops unless emie_cu_profile_enable(1)
+void profile_mark(int stage, bool begin, cudaStream_t st);
 
 // scratch from the stream-ordered pool (reentrant per call)
 template <class T>

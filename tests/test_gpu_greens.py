@@ -1,0 +1,104 @@
+"""GPU parity of the device Green's build (filter design + lambda
+accumulation + spectra) against the reference's own operators.
+
+Tolerance note: the reference's Green's tensor is only
+determined to ~1e-6 of the block maximum by its own arithmetic — a 1-ulp
+change of the cell size moves its blocks that much (the filter designs
+amplify sample rounding, and large-lambda terms cancel) — so block parity is
+asserted at 1e-5 of the block maximum, the level the reference's own tests
+use for independently designed filters (test_greens.cpp:222-228). The
+well-conditioned stages are held to 1e-12 elsewhere (test_gpu_apply.py)."""
+import math
+
+import numpy as np
+import pytest
+
+import emie_oracle as O
+import paper_1512_06126_b200 as emie
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+GREENS_TOL = 1e-5
+
+
+def _grid(g):
+    model = emie.LayeredModel(list(g["tops"]), list(g["sigma"]))
+    grid = emie.make_grid(model, list(g["breaks"]), int(g["nx"]), int(g["ny"]), float(g["hx"]),
+                          float(g["hy"]))
+    return model, grid
+
+
+def test_filter_weights_match_reference(torch_cuda):
+    g = golden("filters")
+    f = lambda lam: lam * np.exp(-lam * lam)
+    for i, (oi, oj, hx, hy) in enumerate(g["geoms"]):
+        w, lam = emie.design_offset_filters(int(oi), int(oj), hx, hy)
+        assert np.allclose(lam, g["lam"], rtol=1e-15, atol=0)
+        R = O.pair_geometry(int(oi), int(oj), hx, hy)[0]
+        ours = np.array([np.sum(w[k] * f(lam / R)) for k in range(6)])
+        ref = np.array([np.sum(g["W"][i, k] * f(g["lam"] / R)) for k in range(6)])
+        assert np.max(np.abs(ours - ref)) <= 1e-7 * np.max(np.abs(ref))
+
+
+def test_untruncated_weights_reproduce_design_pair(torch_cuda):
+    # test_hankel.cpp:118-135 on the device design
+    full = emie.FilterParams(0.2, 0.0964, 512, -512, 511)
+    w, _ = emie.design_offset_filters(0, 0, 1.0, 1.0, full)
+    geom = O.pair_geometry(0, 0, 1.0, 1.0)
+    vt = O.design_input(np.exp(-0.2 * np.arange(-1023, 1024)))
+    m = np.arange(-512, 512)
+    want = emie.kernel_output(0, 0, 1.0, 1.0, 0, 0, 0.2 * m + 0.0964)  # the device's own samples
+    got = np.array([np.dot(w[0], vt[mm - m + 1023]) for mm in m])
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+    # the device samples agree with the closed forms of the oracle up to the
+    # forms' own cancellation noise at extreme log radius
+    ora = O.kernel_output(geom, 0, 0, 0.2 * m + 0.0964)
+    assert np.max(np.abs(want - ora)) / np.max(np.abs(ora)) < 1e-9
+    # window layout and repeatability (:97-116)
+    w1, lam1 = emie.design_offset_filters(0, 0, 1.0, 1.0)
+    w2, _ = emie.design_offset_filters(0, 0, 1.0, 1.0)
+    assert w1.shape == (6, 451) and abs(lam1[250] - math.exp(0.0964)) < 1e-14 * lam1[250]
+    assert np.array_equal(w1, w2)
+    assert np.array_equal(w1[0], w[0][512 - 250:512 + 201])
+
+
+@pytest.mark.parametrize("name", ["toeplitz_single", "toeplitz_tiny", "toeplitz_small",
+                                  "toeplitz_large", "cfg1"])
+def test_blocks_match_reference(torch_cuda, name):
+    g = golden(name)
+    model, grid = _grid(g)
+    sop = emie.assemble_operator(grid, model, float(g["omega"]), keep_blocks=True)
+    blocks = sop.blocks()
+    ref = g["blocks"]
+    worst = 0.0
+    for oi in range(ref.shape[0]):
+        for oj in range(ref.shape[1]):
+            scale = np.max(np.abs(ref[oi, oj]))
+            worst = max(worst, np.max(np.abs(blocks[oi, oj] - ref[oi, oj])) / scale)
+    assert worst <= GREENS_TOL, worst
+    # spectra and apply of the device-built operator against the reference's
+    spec = np.concatenate(sop.comp)
+    assert np.max(np.abs(spec - g["spec"])) <= GREENS_TOL * np.max(np.abs(g["spec"]))
+    for v, want in zip(g["vecs"], g["applyB"]):
+        got = emie.apply(sop, v)
+        assert np.max(np.abs(got - want)) <= GREENS_TOL * np.max(np.abs(want))
+
+
+def test_device_blocks_transform_like_uploaded(torch_cuda):
+    # the device build's blocks, uploaded again, give bit-identical spectra
+    g = golden("toeplitz_large")
+    model, grid = _grid(g)
+    sop = emie.assemble_operator(grid, model, float(g["omega"]), keep_blocks=True)
+    nz = len(g["breaks"]) - 1
+    again = emie.transform_operator(sop.blocks(), int(g["nx"]), int(g["ny"]), nz, float(g["omega"]))
+    assert np.array_equal(np.concatenate(again.comp), np.concatenate(sop.comp))
+
+
+def test_greens_errors(torch_cuda):
+    m = emie.LayeredModel([0.0, 400.0], [0.0, 0.01, 0.1])
+    grid = emie.make_grid(m, [0.0, 200.0, 400.0], 2, 2, 200.0, 260.0)
+    with pytest.raises(emie.InvalidArgument):
+        emie.assemble_operator(grid, m, 1.0, emie.FilterParams(0.2, 0.11))
+    bad = emie.LayeredModel([0.0, 400.0], [0.0, 0.01, float("nan")])
+    with pytest.raises(emie.InvalidArgument):
+        emie.assemble_operator(grid, bad, 1.0)
