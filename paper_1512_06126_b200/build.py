@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libemie_cu.so"
-SOURCES = ["capi.cu", "operator.cu", "solver.cu", "greens.cu"]
+SOURCES = ["capi.cu", "operator.cu", "lateral.cu", "solver.cu", "greens.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

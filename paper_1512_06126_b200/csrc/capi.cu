@@ -208,6 +208,8 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.nentD = 4 * op.nsd * nz + 2 * op.nfull;
   if (!make_plan(op.ex, op.plan_x) || !make_plan(op.ey, op.plan_y))
     fail(EMIE_CU_RUNTIME_ERROR, "toeplitz: planning failed");
+  op.p2x = op.ex <= 2048 && make_pow2_plan(op.ex, op.plan_x2);
+  op.p2y = op.ey <= 2048 && make_pow2_plan(op.ey, op.plan_y2);
   keep_pool_warm();
   op.spec = dev_alloc<cplx>(op.modes() * op.nentD);
   op.tw_x = upload_twiddles(op.ex);

@@ -150,3 +150,147 @@ __device__ __forceinline__ void load_twiddles(cplx* dst, const cplx* __restrict_
 }
 
 }  // namespace emie_cu
+
+namespace emie_cu {
+
+// ===================================================================
+// Power-of-two fast path: in-place Stockham with radix-16/8/4/2 passes,
+// every thread holding EPT elements in registers across a pass (loads,
+// barrier, butterflies, stores, barrier), so one SMEM tile suffices and a
+// 256-point transform needs two passes. Tile element i of transform t
+// lives at phys(t*n + i) = idx + idx/16: the stride-R stores of a pass
+// then fall on distinct 16-byte banks.
+// ===================================================================
+constexpr int kFftEPT = 16;
+
+__host__ __device__ __forceinline__ int fft_phys(int idx) { return idx + (idx >> 4); }
+
+inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// e^{s 2 pi i m / 16}, m = 0..15 (s = -1 forward)
+__host__ __device__ constexpr double cos16(int m) {
+  return (m & 15) == 0 ? 1.0 : (m & 15) == 1 ? 0.92387953251128675613 : (m & 15) == 2 ? 0.70710678118654752440
+       : (m & 15) == 3 ? 0.38268343236508977173 : (m & 15) == 4 ? 0.0 : (m & 15) == 5 ? -0.38268343236508977173
+       : (m & 15) == 6 ? -0.70710678118654752440 : (m & 15) == 7 ? -0.92387953251128675613 : (m & 15) == 8 ? -1.0
+       : (m & 15) == 9 ? -0.92387953251128675613 : (m & 15) == 10 ? -0.70710678118654752440
+       : (m & 15) == 11 ? -0.38268343236508977173 : (m & 15) == 12 ? 0.0 : (m & 15) == 13 ? 0.38268343236508977173
+       : (m & 15) == 14 ? 0.70710678118654752440 : 0.92387953251128675613;
+}
+__device__ __forceinline__ cplx w16(int m, double s) {
+  return {cos16(m), s * cos16(m + 12)};  // sin(x) = cos(x - pi/2)
+}
+
+template <>
+__device__ __forceinline__ void butterfly<8>(cplx* v, double s) {
+  // 8 = 2 x 4: DFT4 over (a + 2c), twiddle W8^{ab}, DFT2 over a
+  cplx e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+  butterfly<4>(e, s);
+  butterfly<4>(o, s);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const cplx t = o[b] * w16(2 * b, s);
+    v[b] = e[b] + t;
+    v[b + 4] = e[b] - t;
+  }
+}
+
+template <>
+__device__ __forceinline__ void butterfly<16>(cplx* v, double s) {
+  // 16 = 4 x 4 (n = a + 4c, k = b + 4d), in place; the final 4x4 transpose
+  // is a register renaming once unrolled
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    cplx q[4] = {v[a], v[a + 4], v[a + 8], v[a + 12]};
+    butterfly<4>(q, s);
+    v[a] = q[0];
+#pragma unroll
+    for (int b = 1; b < 4; ++b) v[a + 4 * b] = (a == 0) ? q[b] : q[b] * w16(a * b, s);
+  }
+  // v[a + 4b] = y[a][b]
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    cplx q[4] = {v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]};
+    butterfly<4>(q, s);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) v[4 * b + d] = q[d];
+  }
+  // X[b + 4d] sits at v[4b + d]: transpose
+  cplx t[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) t[r] = v[4 * (r & 3) + (r >> 2)];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = t[r];
+}
+
+inline bool make_pow2_plan(int n, FftPlan& p) {
+  if (!is_pow2(n) || n > 4096) return false;
+  p = FftPlan{};
+  p.n = n;
+  int r = n;
+  while (r >= 16) { p.radix[p.npass++] = 16; r /= 16; }
+  if (r > 1) p.radix[p.npass++] = r;  // 8, 4 or 2
+  return true;
+}
+
+template <int R>
+__device__ __forceinline__ void pow2_pass(cplx* buf, int n, int ns, int work, const cplx* tw,
+                                          double s) {
+  constexpr int B = kFftEPT / R;  // butterflies per thread
+  const int m = n / R;
+  const int tstep = n / (ns * R);
+  cplx v[B][R];
+  int dst[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int w = threadIdx.x + b * blockDim.x;
+    dst[b] = -1;
+    if (w < work) {
+      const int t = w / m, j = w - t * m;
+      const int k = j & (ns - 1);
+      const int base = t * n;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        cplx x = buf[fft_phys(base + j + r * m)];
+        if (r > 0 && k > 0) {
+          cplx wv = tw[r * k * tstep];
+          if (s > 0) wv.im = -wv.im;
+          x = x * wv;
+        }
+        v[b][r] = x;
+      }
+      butterfly<R>(v[b], s);
+      dst[b] = base + (j / ns) * ns * R + k;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+    if (dst[b] >= 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[fft_phys(dst[b] + r * ns)] = v[b][r];
+    }
+  __syncthreads();
+}
+
+// In-place transform of ntr sequences of length n (pow2) in a padded tile;
+// ntr * n must be <= blockDim.x * kFftEPT. Caller synchronises after the
+// fill; returns synchronised.
+__device__ inline void fft_pow2(cplx* buf, int ntr, const FftPlan& pl, const cplx* tw,
+                                bool inverse) {
+  const double s = inverse ? 1.0 : -1.0;
+  const int n = pl.n;
+  const int lg = 31 - __clz(n);  // n = 2^lg: lg/4 radix-16 passes, then 2^(lg%4)
+  int ns = 1;
+  for (int p = 0; p < (lg >> 2); ++p) {
+    pow2_pass<16>(buf, n, ns, ntr * (n >> 4), tw, s);
+    ns <<= 4;
+  }
+  switch (lg & 3) {
+    case 3: pow2_pass<8>(buf, n, ns, ntr * (n >> 3), tw, s); break;
+    case 2: pow2_pass<4>(buf, n, ns, ntr * (n >> 2), tw, s); break;
+    case 1: pow2_pass<2>(buf, n, ns, ntr * (n >> 1), tw, s); break;
+    default: break;
+  }
+}
+
+}  // namespace emie_cu

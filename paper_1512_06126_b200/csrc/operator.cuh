@@ -37,7 +37,9 @@ struct Operator {
   cplx* tw_x = nullptr;      // e^{-2 pi i m/ex}
   cplx* tw_y = nullptr;      // e^{-2 pi i m/ey}
 
-  FftPlan plan_x, plan_y;
+  FftPlan plan_x, plan_y;    // mixed-radix plans (any 5-smooth length)
+  FftPlan plan_x2, plan_y2;  // radix-16 plans when the length is a power of two
+  bool p2x = false, p2y = false;
 
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
   std::size_t lateral() const { return static_cast<std::size_t>(ex) * ey; }
@@ -58,6 +60,13 @@ struct System {
 void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega);
 void keep_pool_warm();
 cplx* upload_twiddles(int n);
+
+// lateral FFT stages (lateral.cu)
+void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st);
+void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx* T, cplx* S,
+                     int nrhs, cudaStream_t st);
+void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_in, cplx* d_out,
+                     const cplx* s, const double* r1, int nrhs, cudaStream_t st);
 
 // stages (operator.cu)
 void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st);
