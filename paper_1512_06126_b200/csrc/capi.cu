@@ -205,7 +205,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.nfull = nz * nz;
   op.nent = 4 * op.ntri + 2 * op.nfull;
   op.nsd = nz / 2 + 1;
-  op.nentD = 4 * op.nsd * nz + 2 * op.nfull;
+  op.nentD = op.nent;  // compact wrapped-diagonal layout (operator.cuh)
   if (!make_plan(op.ex, op.plan_x) || !make_plan(op.ey, op.plan_y))
     fail(EMIE_CU_RUNTIME_ERROR, "toeplitz: planning failed");
   op.p2x = op.ex <= 2048 && make_pow2_plan(op.ex, op.plan_x2);
@@ -214,25 +214,25 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.spec = dev_alloc<cplx>(op.modes() * op.nentD);
   op.tw_x = upload_twiddles(op.ex);
   op.tw_y = upload_twiddles(op.ey);
-  // reference entry -> wrapped-diagonal slot(s) (see operator.cuh)
+  // reference entry -> wrapped-diagonal slot (see operator.cuh)
   op.emap_host.assign(op.nent, int2{-1, -1});
   for (int c = 0; c < 4; ++c)
     for (int k = 0; k < nz; ++k)
       for (int kp = k; kp < nz; ++kp) {
         const int e = c * op.ntri + k * nz - k * (k - 1) / 2 + (kp - k);
-        const int t = kp - k, base = c * op.nsd * nz;
-        int2 m{-1, -1};
-        if (t < nz - t) m.x = base + t * nz + k;
-        else if (t > nz - t) m.x = base + (nz - t) * nz + kp;
-        else { m.x = base + t * nz + k; m.y = base + t * nz + kp; }
-        op.emap_host[e] = m;
+        const int t = kp - k, base = c * op.ntri;
+        int slot;
+        if (2 * t < nz) slot = base + t * nz + k;
+        else if (2 * t > nz) slot = base + (nz - t) * nz + kp;
+        else slot = base + t * nz + k;  // half diagonal, k < nz/2
+        op.emap_host[e] = int2{slot, -1};
       }
   for (int c = 0; c < 2; ++c)
     for (int k = 0; k < nz; ++k)
       for (int kp = 0; kp < nz; ++kp) {
         const int e = 4 * op.ntri + c * op.nfull + k * nz + kp;
         const int t = ((kp - k) % nz + nz) % nz;
-        op.emap_host[e] = int2{4 * op.nsd * nz + c * op.nfull + t * nz + k, -1};
+        op.emap_host[e] = int2{4 * op.ntri + c * op.nfull + t * nz + k, -1};
       }
   op.emap = dev_alloc<int2>(op.nent);
   EMIE_CUDA(cudaMemcpy(op.emap, op.emap_host.data(), op.nent * sizeof(int2), cudaMemcpyHostToDevice));

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, 2) spectra_y_kernel(const cplx* __restric
 // Layouts (complex128):
 //   u   [r][plane][iy][ix]        GridVector, plane = c*nz + iz
 //   T   [r][mx][plane][iy]        after the x pass (and before the inverse x)
-//   S   [r][my][mx][plane]        spectrum, mode-major for the contraction
+//   S   [r][mx][my][plane]        spectrum, mode-major for the contraction
 // Every load and store below walks a contiguous run of >= 128 B.
 // The mirror-mode signs of the contraction (D = diag(fx, fy, 1), fx = -1 for
 // mx > ex/2 on x planes, fy = -1 for my > ey/2 on y planes) are applied when
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256, 2) apply_fy_kernel(const cplx* __restrict
   for (int idx = threadIdx.x; idx < PC * ey; idx += blockDim.x) {
     const int p = idx % PC, my = idx / PC;
     if (p < pc)
-      S[((static_cast<size_t>(r) * ey + my) * ex + mx) * np + p0 + p] =
+      S[((static_cast<size_t>(r) * ex + mx) * ey + my) * np + p0 + p] =
           mirror_sign(p0 + p, nz, my, mx, ey, ex) * res[T.at(p, my)];
   }
 }
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256, 2) apply_iy_kernel(const cplx* __restrict
     cplx v = {0.0, 0.0};
     if (p < pc)
       v = mirror_sign(p0 + p, nz, j, mx, ey, ex) *
-          ldg(S + ((static_cast<size_t>(r) * ey + j) * ex + mx) * np + p0 + p);
+          ldg(S + ((static_cast<size_t>(r) * ex + mx) * ey + j) * np + p0 + p);
     T.a[T.at(p, j)] = v;
   }
   __syncthreads();

@@ -7,7 +7,7 @@
 // The lateral FFT stages live in lateral.cu. Apply data flow for nrhs fields (all complex128):
 //   u [r][plane][iy][ix]            plane = c*nz + iz (GridVector layout)
 //   K_fx : r2-scale, zero-pad, x-FFT        -> T [r][plane][iy][mx]
-//   K_fy : zero-pad, y-FFT, transpose       -> S [r][my][mx][plane]  (mode-major)
+//   K_fy : zero-pad, y-FFT, transpose       -> S [r][mx][my][plane]  (mode-major)
 //   K_ct : per quadrant mode, 3nz x 3nz block times 4 mirror modes x nrhs
 //                                            -> S (in place)
 //   K_iy : inverse y-FFT, keep iy < ny       -> T
@@ -16,6 +16,7 @@
 // 3nz run per (mode, rhs); the transposes ride inside the FFT kernels' SMEM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "operator.cuh"
 
@@ -74,10 +75,11 @@ __device__ __forceinline__ ModeCols mode_cols(int qm, int qx, int ex, int ey) {
   const bool mx_ok = qmx > 0 && (ex - qmx) > ex / 2;
   const bool my_ok = qmy > 0 && (ey - qmy) > ey / 2;
   mc.nmir = 0;
-  mc.mode[mc.nmir++] = qmy * ex + qmx;
-  if (mx_ok) mc.mode[mc.nmir++] = qmy * ex + (ex - qmx);
-  if (my_ok) mc.mode[mc.nmir++] = (ey - qmy) * ex + qmx;
-  if (mx_ok && my_ok) mc.mode[mc.nmir++] = (ey - qmy) * ex + (ex - qmx);
+  // spectrum mode index mx*ey + my (S layout [r][mx][my][plane], lateral.cu)
+  mc.mode[mc.nmir++] = qmx * ey + qmy;
+  if (mx_ok) mc.mode[mc.nmir++] = (ex - qmx) * ey + qmy;
+  if (my_ok) mc.mode[mc.nmir++] = qmx * ey + (ey - qmy);
+  if (mx_ok && my_ok) mc.mode[mc.nmir++] = (ex - qmx) * ey + (ey - qmy);
   return mc;
 }
 
@@ -128,11 +130,12 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     const ModeCols mc = mode_cols(qm, qx, ex, ey);
     const int ncol = mc.nmir * nrhs;
     const cplx* blk = op + static_cast<size_t>(qm) * nentD;
+    const int ntri = nz * (nz + 1) / 2;
     const cplx* Dxx = blk;
-    const cplx* Dyy = blk + nsd * nz;
-    const cplx* Dzz = blk + 2 * nsd * nz;
-    const cplx* Dxy = blk + 3 * nsd * nz;
-    const cplx* Dxz = blk + 4 * nsd * nz;
+    const cplx* Dyy = blk + ntri;
+    const cplx* Dzz = blk + 2 * ntri;
+    const cplx* Dxy = blk + 3 * ntri;
+    const cplx* Dxz = blk + 4 * ntri;
     const cplx* Dyz = Dxz + nz * nz;
     for (int kb = 0; kb < nz; kb += 32) {
       const int k = kb + lane;
@@ -152,8 +155,10 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
         const int t = (i == 0) ? 0 : ((i & 1) ? (i + 1) >> 1 : nz - (i >> 1));
         int kp = kc + t;
         if (kp >= nz) kp -= nz;
-        const bool lo = t <= nz - t;
-        const int so = (lo ? t : nz - t) * nz + (lo ? kc : kp);
+        // symmetric slot (compact wrapped diagonals, operator.cuh)
+        const int so = (2 * t < nz)   ? t * nz + kc
+                       : (2 * t > nz) ? (nz - t) * nz + kp
+                                      : t * nz + min(kc, kp);
         const int tb = (t == 0) ? 0 : nz - t;
         m.xx = ldg(Dxx + so);
         m.yy = ldg(Dyy + so);
@@ -219,6 +224,197 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
   }
 }
 
+// ------------------------------------------- contraction on FP64 MMA -----
+// Same product as contract_kernel, on the FP64 tensor cores (DMMA.8x8x4 via
+// mma.sync.m8n8k4.f64): measured 37 TF/s at 4 warps/SM on B200, where DFMA
+// needs ~32 warps to approach it. Used when nz is a multiple of 8 and
+// nz <= 32 (the whole mode block fits in SMEM twice).
+// One CTA (4 warps) owns one quadrant mode at a time, persistent over modes.
+// An elected thread brings the next mode's coefficient block (nentD complex,
+// one TMA bulk copy) and its input columns (one bulk copy per (mirror, rhs),
+// column stride np + 4 for conflict-free fragment loads) into the second
+// buffer while the CTA computes the current one.
+// Output rows are 8-row tiles (component a, rows k0..k0+7): 3nz/8 tiles,
+// round-robin over 8 warps (two per SMSP, so one warp's operand loads and
+// adds overlap the other's MMAs; for nz = 32 every SMSP gets 3 tiles); the 8 columns are the MMA's N; K runs over
+// (component b, kp) in steps of 4. Complex products use three real MMAs
+// (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi); re = P1 - P2, im = P3 - P1 - P2).
+constexpr int kMmaWarps = 8;
+constexpr int kMmaTilesPerWarp = 3;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// offset of M_ab(k, kp) in the mode block (wrapped-diagonal layout,
+// operator.cuh); bit 31 set when the entry enters negated (zx = -xz^T,
+// zy = -yz^T). NZ is a power of two here, so the wraps are masks.
+template <int NZ>
+__device__ __forceinline__ uint32_t coef_offset(int a, int b, int k, int kp) {
+  constexpr int ntri = NZ * (NZ + 1) / 2;
+  auto sym = [&](int c) -> uint32_t {
+    const int t = (kp - k) & (NZ - 1);
+    const int o = (2 * t < NZ) ? t * NZ + k : (2 * t > NZ) ? (NZ - t) * NZ + kp : t * NZ + (k < kp ? k : kp);
+    return c * ntri + o;
+  };
+  auto full = [&](int c, int r, int s) -> uint32_t {
+    const int t = (s - r) & (NZ - 1);
+    return 4 * ntri + c * NZ * NZ + t * NZ + r;
+  };
+  if (a == 0) return b == 0 ? sym(0) : b == 1 ? sym(3) : full(0, k, kp);
+  if (a == 1) return b == 0 ? sym(3) : b == 1 ? sym(1) : full(1, k, kp);
+  if (b == 2) return sym(2);
+  return (b == 0 ? full(0, kp, k) : full(1, kp, k)) | 0x80000000u;
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(kMmaWarps * 32, 1)
+    contract_mma_kernel(const cplx* __restrict__ op, cplx* S, int ex, int ey, int qx, int nmodes,
+                        int nrhs, int dbg) {
+  constexpr int np = 3 * NZ, ldu = np + 4;
+  constexpr int nentD = 2 * NZ * (2 * NZ + 1);
+  constexpr int ntiles = np / 8, nk = np / 4;
+  constexpr int TPW = (ntiles + kMmaWarps - 1) / kMmaWarps;  // tiles per warp
+  constexpr int kBlkStages = 3, kUStages = 2;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bbar = reinterpret_cast<uint64_t*>(smraw);   // block stages
+  uint64_t* ubar = bbar + kBlkStages;                     // input stages
+  cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128);
+  cplx* ubuf = blkbuf + kBlkStages * nentD;
+  const size_t E = static_cast<size_t>(ex) * ey;
+  constexpr uint32_t colbytes = np * sizeof(cplx);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBlkStages; ++i) mbar_init(bbar + i, 1);
+    for (int i = 0; i < kUStages; ++i) mbar_init(ubar + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kUStages * 8 * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
+  __syncthreads();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const int G = gridDim.x;
+  // j-th mode of this CTA: blockIdx.x + j*G
+  auto issue_block = [&](int j) {
+    const int qm = blockIdx.x + j * G;
+    if (threadIdx.x == 0 && qm < nmodes) {
+      constexpr uint32_t blkbytes = nentD * sizeof(cplx);
+      const int st = j % kBlkStages;
+      mbar_expect_tx(bbar + st, blkbytes);
+      bulk_g2s(blkbuf + st * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bbar + st);
+    }
+  };
+  auto issue_cols = [&](int j) {
+    const int qm = blockIdx.x + j * G;
+    if (threadIdx.x == 0 && qm < nmodes) {
+      const ModeCols mc = mode_cols(qm, qx, ex, ey);
+      const int ncol = mc.nmir * nrhs;
+      const int st = j % kUStages;
+      mbar_expect_tx(ubar + st, ncol * colbytes);
+      cplx* dst = ubuf + st * 8 * ldu;
+      for (int col = 0; col < ncol; ++col) {
+        const int mi = col / nrhs, r = col - mi * nrhs;
+        bulk_g2s(dst + col * ldu, S + (static_cast<size_t>(r) * E + mc.mode[mi]) * np, colbytes, ubar + st);
+      }
+    }
+  };
+  // fragment coordinates: A row fr / k fc; B k fc / col fr; C row fr, cols 2fc..2fc+1
+  const int fr = lane >> 2, fc = lane & 3;
+  // per-lane coefficient offsets of every (own tile, k step): mode independent
+  uint32_t off[TPW][nk];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) {
+    const int rt = warp + i * kMmaWarps;
+    const int a = (8 * rt) / NZ, k0 = 8 * rt - a * NZ;
+#pragma unroll
+    for (int ks = 0; ks < nk; ++ks) {
+      const int b = (4 * ks) / NZ, kp0 = 4 * ks - b * NZ;
+      off[i][ks] = rt < ntiles ? coef_offset<NZ>(a, b, k0 + fr, kp0 + fc) : 0u;
+    }
+  }
+  // prologue: blocks of modes 0, 1; inputs of mode 0
+  issue_block(0);
+  issue_block(1);
+  issue_cols(0);
+  int j = 0;
+  for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
+    // stages freed by mode j-1 (all warps passed the barrier at its end)
+    if (!(dbg & 2)) {
+      issue_cols(j + 1);
+      issue_block(j + 2);
+    }
+    const int bs_ = j % kBlkStages, us_ = j % kUStages;
+    if (!(dbg & 2) || j == 0) {
+      mbar_wait(bbar + bs_, static_cast<uint32_t>((j / kBlkStages) & 1));
+      mbar_wait(ubar + us_, static_cast<uint32_t>((j / kUStages) & 1));
+    }
+    const cplx* blk = blkbuf + bs_ * nentD;
+    const cplx* U = ubuf + us_ * 8 * ldu + fr * ldu + fc;
+    double p1[TPW][2], p2[TPW][2], p3[TPW][2];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) p1[i][0] = p1[i][1] = p2[i][0] = p2[i][1] = p3[i][0] = p3[i][1] = 0.0;
+    if (!(dbg & 1)) {
+#pragma unroll
+      for (int ks = 0; ks < nk; ++ks) {
+        const cplx bu = (dbg & 8) ? cplx{0.25 * ks, 1.0} : U[4 * ks];  // B[k = fc][col = fr]
+        const double bs = bu.re + bu.im;
+        // Branch-free: tiles past ntiles compute on offset 0 and are never
+        // stored; the zx / zy negation flips the sign bit of the (shared) B
+        // fragment (with NZ == 32 and 8 warps, tile i = 1 is the z component,
+        // so the flag folds at compile time).
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+          const uint32_t o = off[i][ks];
+          const cplx m = (dbg & 4) ? cplx{1.0 + ks, 0.5 * i} : blk[o & 0x7fffffffu];
+          unsigned long long sg;
+          if (NZ == 32 && kMmaWarps == 8)  // tiles w, w+8: only i == 1 is a z tile
+            sg = (i == 1 && (4 * ks) / NZ < 2) ? 0x8000000000000000ull : 0ull;
+          else
+            sg = static_cast<unsigned long long>(o >> 31) << 63;
+          const double br = __longlong_as_double(__double_as_longlong(bu.re) ^ sg);
+          const double bi = __longlong_as_double(__double_as_longlong(bu.im) ^ sg);
+          const double bss = __longlong_as_double(__double_as_longlong(bs) ^ sg);
+          dmma(p1[i][0], p1[i][1], m.re, br);
+          dmma(p2[i][0], p2[i][1], m.im, bi);
+          dmma(p3[i][0], p3[i][1], m.re + m.im, bss);
+        }
+      }
+    }
+    const ModeCols mc = mode_cols(qm, qx, ex, ey);
+    const int ncol = mc.nmir * nrhs;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int rt = warp + i * kMmaWarps;
+      if (rt >= ntiles) continue;
+      const int plane = 8 * rt + fr;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 2 * fc + h;
+        if (col < ncol) {
+          const int mi = nrhs == 2 ? col >> 1 : col, r = nrhs == 2 ? col & 1 : 0;
+          const cplx v = {p1[i][h] - p2[i][h], p3[i][h] - p1[i][h] - p2[i][h]};
+          S[(static_cast<size_t>(r) * E + mc.mode[mi]) * np + plane] = v;
+        }
+      }
+    }
+    // stages of mode j fully consumed (their reads are done: values are in
+    // registers) before the next iterations refill them. The buffers are only
+    // ever read through the generic proxy, so no proxy fence is needed here
+    // (one after the initial zero fill suffices).
+    __syncthreads();
+  }
+}
+
+// experiment switch (EMIE_CT_DEBUG: 1 = skip the MMAs, 2 = skip the copies)
+int ct_debug() {
+  static const int v = [] {
+    const char* e = std::getenv("EMIE_CT_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 void set_smem(const void* fn, size_t bytes) {
   EMIE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes)));
@@ -248,6 +444,24 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
     for (int r0 = 0; r0 < nrhs; r0 += 2) {
       const int g = std::min(2, nrhs - r0);
       cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
+      const bool mma = op.nz == 8 || op.nz == 16 || op.nz == 32;
+      if (mma) {
+        const size_t smem = 128 + 3 * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                            2 * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
+        const int grid = std::max(1, std::min(sms, nmodes));
+        const void* fn = op.nz == 8 ? reinterpret_cast<const void*>(contract_mma_kernel<8>)
+                       : op.nz == 16 ? reinterpret_cast<const void*>(contract_mma_kernel<16>)
+                                     : reinterpret_cast<const void*>(contract_mma_kernel<32>);
+        set_smem(fn, smem);
+        if (op.nz == 8)
+          contract_mma_kernel<8><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+        else if (op.nz == 16)
+          contract_mma_kernel<16><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+        else
+          contract_mma_kernel<32><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+        check_launch("contract_mma_kernel");
+        continue;
+      }
       const int CB = g == 2 ? 8 : 4;
       // two input buffers per warp; as many warps as 220 KB of SMEM holds
       const size_t per_warp = 16 + 2 * static_cast<size_t>(CB) * np * sizeof(cplx);

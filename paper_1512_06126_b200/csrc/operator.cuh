@@ -12,13 +12,15 @@
 namespace emie_cu {
 
 // SpectralOperator (reference include/emie/toeplitz.hpp:21-35), device side.
-// Spectra layout (HBM): mode-major, one contiguous block of nentD complex per
-// quadrant mode, each nz x nz component stored by WRAPPED DIAGONALS:
+// Spectra layout (HBM): mode-major, one contiguous block of nentD = nent =
+// 2nz(2nz+1) complex per quadrant mode (a permutation of the reference's
+// entries), each nz x nz component stored by WRAPPED DIAGONALS:
 //   full F (xz, yz):       D_t[k] = F(k, (k+t) mod nz),  t = 0..nz-1
-//   symmetric S (xx yy zz xy): D_t[k] = S(k, (k+t) mod nz), t = 0..nz/2
-//     (S(k,kp) with (kp-k) mod nz > nz/2 is D_{nz-t}[kp]; the other
-//      triangle entries appear once, the t = nz/2 ones twice for even nz)
-//   block = [xx | yy | zz | xy] (4 * nsd * nz) then [xz | yz] (2 * nz^2)
+//   symmetric S (xx yy zz xy): D_t[k] = S(k, (k+t) mod nz) for 2t < nz;
+//     S(k,kp) with t = (kp-k) mod nz, 2t > nz, is D_{nz-t}[kp]; for even nz
+//     the half diagonal t = nz/2 keeps only k < nz/2 (S(k,kp) at
+//     D_{nz/2}[min(k,kp)]), so each component is exactly nz(nz+1)/2 long
+//   block = [xx | yy | zz | xy] (4 * ntri) then [xz | yz] (2 * nz^2)
 // With lane k of a warp handling output row k, step t reads one contiguous
 // (rotated) 32-entry run of every diagonal: the contraction streams each
 // mode's coefficients straight from L2 with coalesced loads, no SMEM copy.

@@ -1,0 +1,38 @@
+"""Summarise an ncu report: per kernel time, DRAM bytes, pipe utilisation and
+top stall reasons. usage: python tools/ncu_summary.py report.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed.sum", "launch__occupancy_limit_registers",
+        "launch__occupancy_limit_shared_mem", "sm__maximum_warps_per_active_cycle_pct"]
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    u = dict(zip(hdr, units))
+    name = d.get("Kernel Name", "?")[:70]
+    print("==", name)
+    for k in keys:
+        if k in d:
+            print(f"   {k:70s} {d[k]} {u.get(k, '')}")
+    st = []
+    for h, v in d.items():
+        if "average_warps_issue_stalled" in h and "per_issue_active" in h:
+            try:
+                st.append((h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""), float(v)))
+            except ValueError:
+                pass
+    st.sort(key=lambda x: -x[1])
+    print("   stalls/issue:", ", ".join(f"{h} {v:.2f}" for h, v in st[:7]))
