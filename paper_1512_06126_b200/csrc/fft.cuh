@@ -164,6 +164,10 @@ namespace emie_cu {
 constexpr int kFftEPT = 16;
 
 __host__ __device__ __forceinline__ int fft_phys(int idx) { return idx + (idx >> 4); }
+// 2-D form: transform t starts at t*ldp with ldp = n + n/16 + 1 (odd), so
+// element j of consecutive transforms also falls on distinct banks
+__host__ __device__ __forceinline__ int fft_ldp(int n) { return n + (n >> 4) + 1; }
+__host__ __device__ __forceinline__ int fft_phys2(int t, int j, int ldp) { return t * ldp + j + (j >> 4); }
 
 inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
@@ -233,24 +237,23 @@ inline bool make_pow2_plan(int n, FftPlan& p) {
 }
 
 template <int R>
-__device__ __forceinline__ void pow2_pass(cplx* buf, int n, int ns, int work, const cplx* tw,
+__device__ __forceinline__ void pow2_pass(cplx* buf, int n, int ldp, int ns, int work, const cplx* tw,
                                           double s) {
   constexpr int B = kFftEPT / R;  // butterflies per thread
   const int m = n / R;
   const int tstep = n / (ns * R);
   cplx v[B][R];
-  int dst[B];
+  int dt[B], dj[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const int w = threadIdx.x + b * blockDim.x;
-    dst[b] = -1;
+    dt[b] = -1;
     if (w < work) {
       const int t = w / m, j = w - t * m;
       const int k = j & (ns - 1);
-      const int base = t * n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        cplx x = buf[fft_phys(base + j + r * m)];
+        cplx x = buf[fft_phys2(t, j + r * m, ldp)];
         if (r > 0 && k > 0) {
           cplx wv = tw[r * k * tstep];
           if (s > 0) wv.im = -wv.im;
@@ -259,15 +262,16 @@ __device__ __forceinline__ void pow2_pass(cplx* buf, int n, int ns, int work, co
         v[b][r] = x;
       }
       butterfly<R>(v[b], s);
-      dst[b] = base + (j / ns) * ns * R + k;
+      dt[b] = t;
+      dj[b] = (j / ns) * ns * R + k;
     }
   }
   __syncthreads();
 #pragma unroll
   for (int b = 0; b < B; ++b)
-    if (dst[b] >= 0) {
+    if (dt[b] >= 0) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[fft_phys(dst[b] + r * ns)] = v[b][r];
+      for (int r = 0; r < R; ++r) buf[fft_phys2(dt[b], dj[b] + r * ns, ldp)] = v[b][r];
     }
   __syncthreads();
 }
@@ -278,17 +282,17 @@ __device__ __forceinline__ void pow2_pass(cplx* buf, int n, int ns, int work, co
 __device__ inline void fft_pow2(cplx* buf, int ntr, const FftPlan& pl, const cplx* tw,
                                 bool inverse) {
   const double s = inverse ? 1.0 : -1.0;
-  const int n = pl.n;
+  const int n = pl.n, ldp = fft_ldp(n);
   const int lg = 31 - __clz(n);  // n = 2^lg: lg/4 radix-16 passes, then 2^(lg%4)
   int ns = 1;
   for (int p = 0; p < (lg >> 2); ++p) {
-    pow2_pass<16>(buf, n, ns, ntr * (n >> 4), tw, s);
+    pow2_pass<16>(buf, n, ldp, ns, ntr * (n >> 4), tw, s);
     ns <<= 4;
   }
   switch (lg & 3) {
-    case 3: pow2_pass<8>(buf, n, ns, ntr * (n >> 3), tw, s); break;
-    case 2: pow2_pass<4>(buf, n, ns, ntr * (n >> 2), tw, s); break;
-    case 1: pow2_pass<2>(buf, n, ns, ntr * (n >> 1), tw, s); break;
+    case 3: pow2_pass<8>(buf, n, ldp, ns, ntr * (n >> 3), tw, s); break;
+    case 2: pow2_pass<4>(buf, n, ldp, ns, ntr * (n >> 2), tw, s); break;
+    case 1: pow2_pass<2>(buf, n, ldp, ns, ntr * (n >> 1), tw, s); break;
     default: break;
   }
 }

@@ -33,10 +33,10 @@ struct Tile {
   int n, ld;
   __device__ Tile(cplx* sm, int ntr, int n_) : n(n_) {
     if (P2) {
-      ld = n;
+      ld = fft_ldp(n);
       a = sm;
       b = nullptr;
-      tw = sm + fft_phys(ntr * n);
+      tw = sm + ntr * ld;
     } else {
       ld = n | 1;  // odd: column walks hit distinct banks
       a = sm;
@@ -44,7 +44,7 @@ struct Tile {
       tw = b + ntr * ld;
     }
   }
-  __device__ __forceinline__ int at(int t, int j) const { return P2 ? fft_phys(t * n + j) : t * ld + j; }
+  __device__ __forceinline__ int at(int t, int j) const { return P2 ? fft_phys2(t, j, ld) : t * ld + j; }
   __device__ cplx* run(int ntr, const FftPlan& pl, bool inverse) {
     if (P2) {
       fft_pow2(a, ntr, pl, tw, inverse);
@@ -54,8 +54,34 @@ struct Tile {
   }
 };
 
+// Fill a tile through fetch(idx, pos) -> value. On the power-of-two path
+// every thread issues all of its kFftEPT global loads before the first SMEM
+// store, so each thread keeps 16 independent loads in flight.
+template <bool P2, class F>
+__device__ __forceinline__ void fill_tile(Tile<P2>& T, int total, F&& fetch) {
+  if constexpr (P2) {
+    cplx v[kFftEPT];
+    int pos[kFftEPT];
+#pragma unroll
+    for (int e = 0; e < kFftEPT; ++e) {
+      const int idx = threadIdx.x + e * blockDim.x;
+      v[e] = idx < total ? fetch(idx, pos[e]) : cplx{0.0, 0.0};
+      if (idx >= total) pos[e] = -1;
+    }
+#pragma unroll
+    for (int e = 0; e < kFftEPT; ++e)
+      if (pos[e] >= 0) T.a[pos[e]] = v[e];
+  } else {
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      int pos;
+      const cplx v = fetch(idx, pos);
+      T.a[pos] = v;
+    }
+  }
+}
+
 size_t tile_bytes(bool p2, int ntr, int n) {
-  const size_t e = p2 ? static_cast<size_t>(fft_phys(ntr * n)) + n
+  const size_t e = p2 ? static_cast<size_t>(ntr) * fft_ldp(n) + n
                       : 2 * static_cast<size_t>(ntr) * (n | 1) + n;
   return e * sizeof(cplx);
 }
@@ -165,16 +191,18 @@ __global__ void __launch_bounds__(256, 2) apply_fx_kernel(const cplx* __restrict
   const int pr = blockIdx.x, iy0 = blockIdx.y * RT;
   const int r = pr / np, plane = pr - r * np, iz = plane % nz;
   load_twiddles(T.tw, tw, ex);
-  for (int idx = threadIdx.x; idx < RT * ex; idx += blockDim.x) {
+  auto fetch = [&](int idx, int& pos) {
     const int tt = idx / ex, j = idx - tt * ex;
     const int iy = iy0 + tt;
+    pos = T.at(tt, j);
     cplx v = {0.0, 0.0};
-    if (iy < ny && j < nx) {
+    if (tt < RT && iy < ny && j < nx) {
       v = ldg(u + (static_cast<size_t>(pr) * ny + iy) * nx + j);
       if (r2) v = ldg(r2 + (static_cast<size_t>(iz) * ny + iy) * nx + j) * v;
     }
-    T.a[T.at(tt, j)] = v;
-  }
+    return v;
+  };
+  fill_tile<P2>(T, RT * ex, fetch);
   __syncthreads();
   const cplx* res = T.run(RT, pl, false);
   for (int idx = threadIdx.x; idx < RT * ex; idx += blockDim.x) {
@@ -196,10 +224,12 @@ __global__ void __launch_bounds__(256, 2) apply_fy_kernel(const cplx* __restrict
   const int pc = min(PC, np - p0);
   load_twiddles(T.tw, tw, ey);
   const cplx* src = Tin + ((static_cast<size_t>(r) * ex + mx) * np + p0) * ny;
-  for (int idx = threadIdx.x; idx < PC * ey; idx += blockDim.x) {
+  auto fetch = [&](int idx, int& pos) {
     const int p = idx / ey, j = idx - p * ey;
-    T.a[T.at(p, j)] = (j < ny && p < pc) ? ldg(src + p * ny + j) : cplx{0.0, 0.0};
-  }
+    pos = T.at(p, j);
+    return (j < ny && p < pc) ? ldg(src + p * ny + j) : cplx{0.0, 0.0};
+  };
+  fill_tile<P2>(T, PC * ey, fetch);
   __syncthreads();
   const cplx* res = T.run(PC, pl, false);
   for (int idx = threadIdx.x; idx < PC * ey; idx += blockDim.x) {
@@ -222,14 +252,16 @@ __global__ void __launch_bounds__(256, 2) apply_iy_kernel(const cplx* __restrict
   const int mx = blockIdx.x, p0 = blockIdx.y * PC, r = blockIdx.z;
   const int pc = min(PC, np - p0);
   load_twiddles(T.tw, tw, ey);
-  for (int idx = threadIdx.x; idx < PC * ey; idx += blockDim.x) {
+  auto fetch = [&](int idx, int& pos) {
     const int p = idx % PC, j = idx / PC;
+    pos = T.at(p, j);
     cplx v = {0.0, 0.0};
-    if (p < pc)
+    if (p < pc && j < ey)
       v = mirror_sign(p0 + p, nz, j, mx, ey, ex) *
           ldg(S + ((static_cast<size_t>(r) * ex + mx) * ey + j) * np + p0 + p);
-    T.a[T.at(p, j)] = v;
-  }
+    return v;
+  };
+  fill_tile<P2>(T, PC * ey, fetch);
   __syncthreads();
   const cplx* res = T.run(PC, pl, true);
   cplx* dst = Tout + ((static_cast<size_t>(r) * ex + mx) * np + p0) * ny;
@@ -253,12 +285,14 @@ __global__ void __launch_bounds__(256, 2) apply_ix_kernel(const cplx* __restrict
   const int pr = blockIdx.x, iy0 = blockIdx.y * RT;
   const int r = pr / np, plane = pr - r * np, iz = plane % nz;
   load_twiddles(T.tw, tw, ex);
-  for (int idx = threadIdx.x; idx < RT * ex; idx += blockDim.x) {
+  auto fetch = [&](int idx, int& pos) {
     const int tt = idx % RT, mx = idx / RT;
     const int iy = iy0 + tt;
-    T.a[T.at(tt, mx)] =
-        iy < ny ? ldg(Tin + ((static_cast<size_t>(r) * ex + mx) * np + plane) * ny + iy) : cplx{0.0, 0.0};
-  }
+    pos = T.at(tt, mx);
+    return (iy < ny && mx < ex) ? ldg(Tin + ((static_cast<size_t>(r) * ex + mx) * np + plane) * ny + iy)
+                                : cplx{0.0, 0.0};
+  };
+  fill_tile<P2>(T, RT * ex, fetch);
   __syncthreads();
   const cplx* res = T.run(RT, pl, true);
   for (int idx = threadIdx.x; idx < RT * nx; idx += blockDim.x) {
