@@ -178,7 +178,9 @@ def run_ours(args):
 
     cfg = configs.config(args.config)
     freqs = configs.config(5).freqs
-    freq = cfg.freqs[0] if world == 1 else freqs[rank % len(freqs)]
+    from paper_1512_06126_b200.sharding import shard_indices
+    # weak scaling over the config-5 sweep: rank r owns frequency r (round robin)
+    freq = cfg.freqs[0] if world == 1 else freqs[shard_indices(len(freqs), world, rank)[0]]
     omega = 2.0 * np.pi * freq
     model = emie.LayeredModel(cfg.tops, cfg.sigma)
     grid = emie.make_grid(model, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy)

@@ -78,6 +78,12 @@ int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
                          double omega, const double* filter, int keep_blocks,
                          emie_cu_operator* out, void* stream);
 
+/* a SpectralOperator given by its six host component arrays (the
+ * emie_cu_operator_download_spectra layout): uploaded into the device
+ * wrapped-diagonal layout, no transform */
+int emie_cu_operator_from_spectra(int nx, int ny, int nz, double omega, const double* h_comp,
+                                  emie_cu_operator* out);
+
 /* dims = {nx, ny, nz, ex, ey, qx, qy}; omega */
 int emie_cu_operator_dims(emie_cu_operator op, int dims[7], double* omega);
 
@@ -107,6 +113,10 @@ void emie_cu_operator_destroy(emie_cu_operator op);
  * src/toeplitz.cpp:163-283) on nrhs device fields; d_out may not alias d_in */
 int emie_cu_apply_spectral(emie_cu_operator op, const double* d_in, double* d_out,
                            int nrhs, void* stream);
+
+/* same, host fields in and out (H2D, apply, D2H inside the call) */
+int emie_cu_apply_spectral_host(emie_cu_operator op, const double* h_in, double* h_out,
+                                int nrhs, void* stream);
 
 /* ---------------------------------------------------------------------
  * System operator A = S + R1 B R2 (include/emie/cie.hpp:26-39)
@@ -165,6 +175,11 @@ int emie_cu_profile_collect(double* ms, long long* count, int n);
 /* FP64 throughput probe: a DFMA-bound kernel on the device (denominator of
  * the FP64 roofline, which MEASURED_PEAKS.json does not carry) */
 int emie_cu_probe_fp64(double* tflops, void* stream);
+
+/* same with host right-hand sides and solutions */
+int emie_cu_fgmres_host(emie_cu_system sys, const double* h_rhs, double* h_x, int nrhs,
+                        double tol, int restart, int max_iters, emie_cu_report* reports,
+                        double* h_history, int hist_cap, void* stream);
 
 /* kernel launches issued by this library on the calling thread since the
  * last reset (evidence for bench.py's gpu_launches) */

@@ -15,6 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libemie_cu.so"
+CPPLIB = PKG / "libemie_b200.so"  # C++ drop-in of the reference emie:: API over the C ABI
 SOURCES = ["capi.cu", "operator.cu", "lateral.cu", "solver.cu", "greens.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -30,7 +31,10 @@ def stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "emie_cu.h"]
+    deps = (list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "emie_cu.h"]
+            + list((PKG / "cpp").glob("*.cpp")) + list((ROOT / "include" / "emie").glob("*.hpp")))
+    if not CPPLIB.exists():
+        return True
     return any(p.stat().st_mtime > t for p in deps)
 
 
@@ -60,7 +64,19 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+    build_cpp()
     return LIB
+
+
+def build_cpp() -> Path:
+    """libemie_b200.so: include/emie/*.hpp implemented over libemie_cu.so."""
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", str(ROOT / "include"),
+           str(PKG / "cpp" / "emie_dropin.cpp"), "-L", str(PKG), "-lemie_cu",
+           "-Wl,-rpath,$ORIGIN", "-o", str(CPPLIB)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("drop-in build failed:\n" + r.stdout + r.stderr)
+    return CPPLIB
 
 
 if __name__ == "__main__":

@@ -1,0 +1,568 @@
+// emie-b200 C++ drop-in: the reference's public emie:: API (include/emie/*.hpp)
+// implemented over the C ABI of libemie_cu.so (include/emie_cu.h). Code written
+// against the reference library builds unchanged against these headers and
+// runs its hot path on the B200: assemble_operator -> device Green's build,
+// transform_operator -> device spectra, apply / solve_cie -> device kernels.
+//
+// Host-side code here is the API glue the reference also does on the host:
+// argument validation with the reference's exception types, layout
+// conversions, the EMG1 snapshot I/O (greens.cpp:373-446), and two test
+// helpers the reference itself ships as oracles (dense_reference_apply,
+// toeplitz.cpp:285-312; fetch_block, greens.cpp:295-330).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "emie/cie.hpp"
+#include "emie/greens.hpp"
+#include "emie/layered.hpp"
+#include "emie/toeplitz.hpp"
+#include "emie_cu.h"
+
+namespace emie {
+
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string msg = emie_cu_last_error();
+  switch (rc) {
+    case EMIE_CU_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case EMIE_CU_DOMAIN_ERROR: throw std::domain_error(msg);
+    case EMIE_CU_OUT_OF_RANGE: throw std::out_of_range(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+void check(int rc) {
+  if (rc != EMIE_CU_OK) rethrow(rc);
+}
+const double* dbl(const cdouble* p) { return reinterpret_cast<const double*>(p); }
+double* dbl(cdouble* p) { return reinterpret_cast<double*>(p); }
+
+}  // namespace
+
+struct DeviceOperator {
+  emie_cu_operator h = nullptr;
+  explicit DeviceOperator(emie_cu_operator x) : h(x) {}
+  DeviceOperator(const DeviceOperator&) = delete;
+  DeviceOperator& operator=(const DeviceOperator&) = delete;
+  ~DeviceOperator() { emie_cu_operator_destroy(h); }
+};
+struct DeviceSystem {
+  emie_cu_system h = nullptr;
+  explicit DeviceSystem(emie_cu_system x) : h(x) {}
+  DeviceSystem(const DeviceSystem&) = delete;
+  DeviceSystem& operator=(const DeviceSystem&) = delete;
+  ~DeviceSystem() { emie_cu_system_destroy(h); }
+};
+
+// ------------------------------------------------------------- layered ----
+int LayeredModel::layer_of(double z) const {
+  return static_cast<int>(std::upper_bound(tops.begin(), tops.end(), z) - tops.begin());
+}
+double LayeredModel::top_of(int m) const { return m == 0 ? tops.front() : tops[m - 1]; }
+double LayeredModel::bottom_of(int m) const {
+  return m == static_cast<int>(tops.size()) ? tops.back() : tops[m];
+}
+double LayeredModel::thickness(int m) const { return bottom_of(m) - top_of(m); }
+cdouble LayeredModel::sigma_floored(int m) const {
+  const cdouble s = sigma[m];
+  return s.real() < sigma_floor ? cdouble(sigma_floor, s.imag()) : s;
+}
+void LayeredModel::validate() const {
+  if (tops.empty()) throw std::invalid_argument("layered model needs at least one interface");
+  if (sigma.size() != tops.size() + 1)
+    throw std::invalid_argument("layered model: sigma count must be tops count + 1");
+  for (std::size_t i = 1; i < tops.size(); ++i)
+    if (!(tops[i - 1] < tops[i])) throw std::invalid_argument("layered model: interface depths must increase");
+  for (double d : tops)
+    if (!std::isfinite(d)) throw std::invalid_argument("layered model: non-finite depth");
+  for (const cdouble& s : sigma)
+    if (!std::isfinite(s.real()) || !std::isfinite(s.imag()))
+      throw std::invalid_argument("layered model: non-finite conductivity");
+}
+
+VerticalPartition VerticalPartition::create(const LayeredModel& model, const std::vector<double>& breaks) {
+  if (breaks.size() < 2) throw std::invalid_argument("vertical partition needs at least one interval");
+  VerticalPartition p;
+  p.breaks = breaks;
+  const int L = static_cast<int>(model.tops.size());
+  for (std::size_t i = 0; i + 1 < breaks.size(); ++i) {
+    if (!(breaks[i] < breaks[i + 1])) throw std::invalid_argument("vertical partition: breaks must increase");
+    const int m = model.layer_of(breaks[i]);
+    const double slack = 1e-7 * (1.0 + std::fabs(breaks[i + 1]));
+    if (m < L && breaks[i + 1] > model.bottom_of(m) + slack)
+      throw std::invalid_argument("vertical partition: interval straddles a layer interface");
+    p.layer.push_back(m);
+  }
+  return p;
+}
+
+// --------------------------------------------------------------- grid ----
+void AnomalyGrid::validate(const LayeredModel& model) const {
+  if (nx <= 0 || ny <= 0 || part.count() <= 0) throw std::invalid_argument("grid: empty dimensions");
+  if (!(hx > 0.0) || !(hy > 0.0)) throw std::invalid_argument("grid: cell sizes must be positive");
+  if (sigma_a.size() != std::size_t(nx) * ny * part.count() || sigma_b.size() != std::size_t(part.count()))
+    throw std::invalid_argument("grid: conductivity array sizes");
+  for (const cdouble& s : sigma_a)
+    if (!(s.real() >= 0.0)) throw std::invalid_argument("grid: cell conductivity with negative real part");
+  for (int m : part.layer)
+    if (!(model.sigma[m].real() > 0.0))
+      throw std::invalid_argument("grid: interval in a non-conducting layer");
+}
+
+AnomalyGrid make_grid(const LayeredModel& model, const std::vector<double>& breaks, int nx, int ny,
+                      double hx, double hy, double x0, double y0) {
+  AnomalyGrid g;
+  g.nx = nx;
+  g.ny = ny;
+  g.hx = hx;
+  g.hy = hy;
+  g.x0 = x0;
+  g.y0 = y0;
+  g.part = VerticalPartition::create(model, breaks);
+  for (int m : g.part.layer) g.sigma_b.push_back(model.sigma_floored(m));
+  g.sigma_a.resize(std::size_t(std::max(nx, 0)) * std::max(ny, 0) * g.part.count());
+  for (int iz = 0; iz < g.part.count(); ++iz)
+    std::fill_n(g.sigma_a.begin() + std::size_t(iz) * std::max(nx, 0) * std::max(ny, 0),
+                std::size_t(std::max(nx, 0)) * std::max(ny, 0), g.sigma_b[iz]);
+  g.validate(model);
+  return g;
+}
+
+void fill_box(AnomalyGrid& g, int ix0, int ix1, int iy0, int iy1, int iz0, int iz1, cdouble sigma) {
+  if (ix0 < 0 || iy0 < 0 || iz0 < 0 || ix1 >= g.nx || iy1 >= g.ny || iz1 >= g.nz() || ix0 > ix1 ||
+      iy0 > iy1 || iz0 > iz1)
+    throw std::invalid_argument("fill_box: index box out of range");
+  for (int iz = iz0; iz <= iz1; ++iz)
+    for (int iy = iy0; iy <= iy1; ++iy)
+      for (int ix = ix0; ix <= ix1; ++ix) g.sigma_a[g.cell(iz, iy, ix)] = sigma;
+}
+
+// --------------------------------------------------- compressed operator ----
+const GreensBlock& CompressedGreensOperator::stored(int oi, int oj) const {
+  if (oi < 0 || oj < 0 || oi >= ny || oj >= nx) throw std::out_of_range("stored: offset outside the stored sector");
+  return blocks[std::size_t(oi) * nx + oj];
+}
+
+std::size_t CompressedGreensOperator::stored_complex_count() const {
+  std::size_t n = 0;
+  for (const auto& b : blocks) n += b.stored_count();
+  return n;
+}
+
+CompressedGreensOperator compress(int nx, int ny, std::vector<GreensBlock> blocks, double omega) {
+  if (blocks.size() != std::size_t(nx) * ny)
+    throw std::invalid_argument("compress: need one block per non-negative offset");
+  CompressedGreensOperator op;
+  op.nx = nx;
+  op.ny = ny;
+  op.nz = blocks.empty() ? 0 : blocks.front().nz;
+  op.omega = omega;
+  const std::size_t nt = std::size_t(op.nz) * (op.nz + 1) / 2, nf = std::size_t(op.nz) * op.nz;
+  for (const auto& b : blocks)
+    if (b.nz != op.nz || b.xx.size() != nt || b.yy.size() != nt || b.zz.size() != nt || b.xy.size() != nt ||
+        b.xz.size() != nf || b.yz.size() != nf)
+      throw std::invalid_argument("compress: block missing or malformed");
+  op.blocks = std::move(blocks);
+  return op;
+}
+
+FullBlock fetch_block(const CompressedGreensOperator& op, int oi, int oj) {
+  if (std::abs(oi) >= op.ny || std::abs(oj) >= op.nx) throw std::out_of_range("fetch_block: offset out of range");
+  const GreensBlock& b = op.stored(std::abs(oi), std::abs(oj));
+  const int nz = op.nz;
+  const double sx = oj < 0 ? -1.0 : 1.0, sy = oi < 0 ? -1.0 : 1.0;
+  FullBlock f;
+  f.nz = nz;
+  for (auto& q : f.q) q.assign(std::size_t(nz) * nz, cdouble(0.0));
+  for (int k = 0; k < nz; ++k)
+    for (int kp = 0; kp < nz; ++kp) {
+      const std::size_t i = std::size_t(k) * nz + kp, t = GreensBlock::tri(std::min(k, kp), std::max(k, kp), nz);
+      f.q[0][i] = b.xx[t];
+      f.q[4][i] = b.yy[t];
+      f.q[8][i] = b.zz[t];
+      f.q[1][i] = f.q[3][i] = sx * sy * b.xy[t];
+      f.q[2][i] = sx * b.xz[i];
+      f.q[5][i] = sy * b.yz[i];
+    }
+  for (int k = 0; k < nz; ++k)
+    for (int kp = 0; kp < nz; ++kp) {
+      f.q[6][std::size_t(k) * nz + kp] = -f.q[2][std::size_t(kp) * nz + k];
+      f.q[7][std::size_t(k) * nz + kp] = -f.q[5][std::size_t(kp) * nz + k];
+    }
+  return f;
+}
+
+namespace {
+// reference block layout <-> the ABI's packed block vectors
+std::vector<cdouble> pack_blocks(const CompressedGreensOperator& op) {
+  const std::size_t per = 2 * std::size_t(op.nz) * (2 * op.nz + 1);
+  std::vector<cdouble> v(per * op.blocks.size());
+  cdouble* o = v.data();
+  for (const auto& b : op.blocks)
+    for (const auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz}) o = std::copy(c->begin(), c->end(), o);
+  return v;
+}
+std::vector<GreensBlock> unpack_blocks(const std::vector<cdouble>& v, int nblocks, int nz) {
+  const std::size_t nt = std::size_t(nz) * (nz + 1) / 2, nf = std::size_t(nz) * nz;
+  std::vector<GreensBlock> out(nblocks);
+  const cdouble* p = v.data();
+  for (auto& b : out) {
+    b.nz = nz;
+    for (auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz}) {
+      const std::size_t n = (c == &b.xz || c == &b.yz) ? nf : nt;
+      c->assign(p, p + n);
+      p += n;
+    }
+  }
+  return out;
+}
+}  // namespace
+
+CompressedGreensOperator assemble_operator(const AnomalyGrid& grid, const LayeredModel& model, double omega,
+                                           const FilterParams& params) {
+  grid.validate(model);
+  model.validate();
+  const int nz = grid.nz();
+  const double fp[5] = {params.step, params.shift, double(params.half), double(params.n1), double(params.n2)};
+  emie_cu_operator h = nullptr;
+  check(emie_cu_greens_build(static_cast<int>(model.tops.size()), model.tops.data(), dbl(model.sigma.data()), nz,
+                             grid.part.breaks.data(), grid.nx, grid.ny, grid.hx, grid.hy, omega, fp, 1, &h,
+                             nullptr));
+  DeviceOperator guard(h);
+  std::vector<cdouble> v(std::size_t(grid.nx) * grid.ny * 2 * nz * (2 * nz + 1));
+  check(emie_cu_operator_download_blocks(h, dbl(v.data())));
+  return compress(grid.nx, grid.ny, unpack_blocks(v, grid.nx * grid.ny, nz), omega);
+}
+
+// EMG1 snapshot (greens.cpp:373-446)
+void save_operator(const std::string& path, const CompressedGreensOperator& op) {
+  std::ofstream os(path, std::ios::binary | std::ios::trunc);
+  if (!os) throw std::runtime_error("save_operator: cannot open " + path);
+  const std::uint32_t magic = 0x454d4731;
+  const std::int32_t dims[3] = {op.nx, op.ny, op.nz};
+  os.write(reinterpret_cast<const char*>(&magic), 4);
+  os.write(reinterpret_cast<const char*>(dims), 12);
+  os.write(reinterpret_cast<const char*>(&op.omega), 8);
+  for (const auto& b : op.blocks)
+    for (const auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz}) {
+      const std::uint64_t n = c->size();
+      os.write(reinterpret_cast<const char*>(&n), 8);
+      os.write(reinterpret_cast<const char*>(c->data()), std::streamsize(n * sizeof(cdouble)));
+    }
+  if (!os) throw std::runtime_error("save_operator: write failed on " + path);
+}
+
+std::optional<CompressedGreensOperator> load_operator(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) return std::nullopt;
+  std::uint32_t magic = 0;
+  std::int32_t d[3] = {0, 0, 0};
+  double omega = 0;
+  is.read(reinterpret_cast<char*>(&magic), 4);
+  is.read(reinterpret_cast<char*>(d), 12);
+  is.read(reinterpret_cast<char*>(&omega), 8);
+  if (!is || magic != 0x454d4731 || d[0] <= 0 || d[1] <= 0 || d[2] <= 0) return std::nullopt;
+  const std::size_t nt = std::size_t(d[2]) * (d[2] + 1) / 2, nf = std::size_t(d[2]) * d[2];
+  std::vector<GreensBlock> blocks(std::size_t(d[0]) * d[1]);
+  for (auto& b : blocks) {
+    b.nz = d[2];
+    for (auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz}) {
+      std::uint64_t n = 0;
+      is.read(reinterpret_cast<char*>(&n), 8);
+      if (!is || n != ((c == &b.xz || c == &b.yz) ? nf : nt)) return std::nullopt;
+      c->resize(n);
+      is.read(reinterpret_cast<char*>(c->data()), std::streamsize(n * sizeof(cdouble)));
+      if (!is) return std::nullopt;
+    }
+  }
+  return compress(d[0], d[1], std::move(blocks), omega);
+}
+
+// ------------------------------------------------------------- spectra ----
+int smooth_embedding_size(int n) {
+  int out = 0;
+  check(emie_cu_smooth_embedding_size(n, &out));
+  return out;
+}
+
+std::size_t SpectralOperator::stored_complex_count() const {
+  std::size_t n = 0;
+  for (const auto& c : comp) n += c.size();
+  return n;
+}
+
+namespace {
+void fill_host_view(SpectralOperator& s, emie_cu_operator h) {
+  int dims[7];
+  double omega = 0;
+  check(emie_cu_operator_dims(h, dims, &omega));
+  s.nx = dims[0];
+  s.ny = dims[1];
+  s.nz = dims[2];
+  s.ex = dims[3];
+  s.ey = dims[4];
+  s.qx = dims[5];
+  s.qy = dims[6];
+  s.omega = omega;
+  const std::size_t nt = std::size_t(s.nz) * (s.nz + 1) / 2, nf = std::size_t(s.nz) * s.nz;
+  std::vector<cdouble> all(s.mode_count() * 2 * s.nz * (2 * s.nz + 1));
+  check(emie_cu_operator_download_spectra(h, dbl(all.data())));
+  const cdouble* p = all.data();
+  for (int c = 0; c < 6; ++c) {
+    const std::size_t n = s.mode_count() * (c < 4 ? nt : nf);
+    s.comp[c].assign(p, p + n);
+    p += n;
+  }
+}
+
+std::mutex g_lazy;
+emie_cu_operator device_of(const SpectralOperator& s) {
+  std::lock_guard<std::mutex> lk(g_lazy);
+  if (!s.device) {  // a SpectralOperator assembled by hand: upload its comp
+    std::vector<cdouble> all;
+    for (const auto& c : s.comp) all.insert(all.end(), c.begin(), c.end());
+    emie_cu_operator h = nullptr;
+    check(emie_cu_operator_from_spectra(s.nx, s.ny, s.nz, s.omega, dbl(all.data()), &h));
+    const_cast<SpectralOperator&>(s).device = std::make_shared<DeviceOperator>(h);
+  }
+  return s.device->h;
+}
+}  // namespace
+
+SpectralOperator transform_operator(const CompressedGreensOperator& op) {
+  if (op.nx <= 0 || op.ny <= 0 || op.nz <= 0) throw std::invalid_argument("transform_operator: empty operator");
+  const std::vector<cdouble> packed = pack_blocks(op);
+  emie_cu_operator h = nullptr;
+  check(emie_cu_operator_from_blocks(op.nx, op.ny, op.nz, op.omega, dbl(packed.data()), &h, nullptr));
+  SpectralOperator s;
+  s.device = std::make_shared<DeviceOperator>(h);
+  fill_host_view(s, h);
+  return s;
+}
+
+GridVector apply(const SpectralOperator& sop, const GridVector& v) {
+  if (v.nx != sop.nx || v.ny != sop.ny || v.nz != sop.nz || v.size() != 3 * std::size_t(sop.nx) * sop.ny * sop.nz)
+    throw std::invalid_argument("apply: field shape does not match operator");
+  GridVector out(sop.nx, sop.ny, sop.nz);
+  check(emie_cu_apply_spectral_host(device_of(sop), dbl(v.a.data()), dbl(out.a.data()), 1, nullptr));
+  return out;
+}
+
+GridVector dense_reference_apply(const CompressedGreensOperator& op, const GridVector& v) {
+  // O(N^2) oracle, guarded to 4096 cells as in the reference
+  const int nx = op.nx, ny = op.ny, nz = op.nz;
+  const std::size_t cells = std::size_t(nx) * ny * nz;
+  if (cells > 4096) throw std::invalid_argument("dense_reference_apply: grid too large");
+  if (v.nx != nx || v.ny != ny || v.nz != nz || v.size() != 3 * cells)
+    throw std::invalid_argument("dense_reference_apply: field shape");
+  GridVector out(nx, ny, nz);
+  for (int oi = -(ny - 1); oi < ny; ++oi)
+    for (int oj = -(nx - 1); oj < nx; ++oj) {
+      const FullBlock f = fetch_block(op, oi, oj);
+      for (int iy = std::max(0, oi); iy < std::min(ny, ny + oi); ++iy)
+        for (int ix = std::max(0, oj); ix < std::min(nx, nx + oj); ++ix)
+          for (int a = 0; a < 3; ++a)
+            for (int k = 0; k < nz; ++k) {
+              cdouble acc = 0.0;
+              for (int b = 0; b < 3; ++b)
+                for (int kp = 0; kp < nz; ++kp) acc += f.at(a, b, k, kp) * v.at(b, kp, iy - oi, ix - oj);
+              out.at(a, k, iy, ix) += acc;
+            }
+    }
+  return out;
+}
+
+// ------------------------------------------------------------------ cie ----
+ContrastCoefficients contrast_coefficients(cdouble sa, cdouble sb) {
+  if (!(sb.real() > 0.0)) throw std::invalid_argument("contrast coefficients: background needs Re sigma > 0");
+  const double den = 2.0 * std::sqrt(sb.real());
+  ContrastCoefficients c{(sa + std::conj(sb)) / den, (sa - sb) / den, (sa - sb) / (sa + std::conj(sb))};
+  if (!(std::abs(c.gamma) < 1.0)) throw std::domain_error("contrast coefficients: contraction factor reaches one");
+  return c;
+}
+
+SystemOperator build_system(const AnomalyGrid& grid, const SpectralOperator& op) {
+  if (grid.nx != op.nx || grid.ny != op.ny || grid.nz() != op.nz)
+    throw std::invalid_argument("build_system: grid and operator disagree");
+  std::vector<double> vol(grid.nz());
+  for (int iz = 0; iz < grid.nz(); ++iz) vol[iz] = grid.volume(iz);
+  emie_cu_system h = nullptr;
+  check(emie_cu_system_create(device_of(op), dbl(grid.sigma_a.data()), dbl(grid.sigma_b.data()), vol.data(), &h));
+  SystemOperator sys;
+  sys.b = &op;
+  sys.device = std::make_shared<DeviceSystem>(h);
+  const std::size_t cells = grid.sigma_a.size();
+  sys.s.resize(cells);
+  sys.r1.resize(cells);
+  sys.r2.resize(cells);
+  check(emie_cu_system_download(h, dbl(sys.s.data()), sys.r1.data(), dbl(sys.r2.data())));
+  return sys;
+}
+
+GridVector apply(const SystemOperator& sys, const GridVector& u) {
+  const SpectralOperator& b = *sys.b;
+  if (u.nx != b.nx || u.ny != b.ny || u.nz != b.nz) throw std::invalid_argument("apply: field shape does not match system");
+  if (!sys.device) throw std::invalid_argument("apply: system not built by build_system");
+  GridVector out(u.nx, u.ny, u.nz);
+  check(emie_cu_apply_system_host(sys.device->h, dbl(u.a.data()), dbl(out.a.data()), 1, nullptr));
+  return out;
+}
+
+// Flexible restarted GMRES for a caller-supplied host map (cie.cpp:117-238
+// interface). The operator work happens in the map; for the CIE system use
+// solve_cie, which runs the whole iteration on the device.
+FgmresResult fgmres(const LinearMap& A, const GridVector& rhs, const SolverConfig& cfg) {
+  if (!(cfg.tol > 0.0) || cfg.restart < 1 || cfg.max_iters < 1)
+    throw std::invalid_argument("fgmres: bad solver configuration");
+  auto dot = [](const GridVector& u, const GridVector& v) {
+    cdouble s = 0.0;
+    for (std::size_t i = 0; i < u.a.size(); ++i) s += std::conj(u.a[i]) * v.a[i];
+    return s;
+  };
+  auto nrm = [](const GridVector& u) {
+    double s = 0.0;
+    for (const auto& c : u.a) s += std::norm(c);
+    return std::sqrt(s);
+  };
+  FgmresResult res;
+  res.x = GridVector(rhs.nx, rhs.ny, rhs.nz);
+  const double bnorm = nrm(rhs);
+  if (bnorm == 0.0) {
+    res.report.status = SolveStatus::converged;
+    return res;
+  }
+  const int m = cfg.restart;
+  GridVector r = rhs;
+  double rnorm = bnorm;
+  int iter = 0;
+  bool broke = false;
+  while (iter < cfg.max_iters) {
+    std::vector<GridVector> V, Z;
+    V.push_back(r);
+    for (auto& c : V[0].a) c *= 1.0 / rnorm;
+    std::vector<cdouble> h(std::size_t(m + 1) * m), g(m + 1), sn(m);
+    std::vector<double> cs(m);
+    g[0] = rnorm;
+    int cols = 0;
+    for (int j = 0; j < m && iter < cfg.max_iters; ++j) {
+      ++iter;
+      cdouble* hj = h.data() + std::size_t(j) * (m + 1);
+      GridVector w;
+      if (cfg.right_precond) {
+        Z.push_back(cfg.right_precond(V[j]));
+        w = A(Z.back());
+      } else {
+        w = A(V[j]);
+      }
+      const double wn0 = nrm(w);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i <= j; ++i) {
+          const cdouble hc = dot(V[i], w);
+          for (std::size_t e = 0; e < w.a.size(); ++e) w.a[e] -= hc * V[i].a[e];
+          hj[i] += hc;
+        }
+      const double hnext = nrm(w);
+      for (int i = 0; i < j; ++i) {
+        const cdouble t = cs[i] * hj[i] + sn[i] * hj[i + 1];
+        hj[i + 1] = -std::conj(sn[i]) * hj[i] + cs[i] * hj[i + 1];
+        hj[i] = t;
+      }
+      if (hnext <= 1e-13 * std::max(wn0, 1e-300)) {
+        double colmax = hnext;
+        for (int i = 0; i <= j; ++i) colmax = std::max(colmax, std::abs(hj[i]));
+        if (std::abs(hj[j]) > 1e-13 * std::max(colmax, 1e-300)) {
+          cols = j + 1;
+        } else {
+          cols = j;
+          broke = true;
+          res.report.history.push_back(rnorm / bnorm);
+          if (cfg.on_iteration) cfg.on_iteration(iter, rnorm / bnorm);
+        }
+        break;
+      }
+      hj[j + 1] = hnext;
+      V.push_back(w);
+      for (auto& c : V.back().a) c *= 1.0 / hnext;
+      const cdouble f = hj[j];
+      if (f == 0.0) {
+        cs[j] = 0.0;
+        sn[j] = 1.0;
+      } else {
+        const double t = std::sqrt(std::norm(f) + hnext * hnext);
+        cs[j] = std::abs(f) / t;
+        sn[j] = f / std::abs(f) * hnext / t;
+      }
+      hj[j] = cs[j] * hj[j] + sn[j] * hj[j + 1];
+      hj[j + 1] = 0.0;
+      g[j + 1] = -std::conj(sn[j]) * g[j];
+      g[j] = cs[j] * g[j];
+      cols = j + 1;
+      const double est = std::abs(g[j + 1]) / bnorm;
+      res.report.history.push_back(est);
+      if (cfg.on_iteration) cfg.on_iteration(iter, est);
+      if (est <= cfg.tol) break;
+    }
+    std::vector<cdouble> y(cols);
+    for (int k = cols - 1; k >= 0; --k) {
+      cdouble acc = g[k];
+      for (int l = k + 1; l < cols; ++l) acc -= h[std::size_t(l) * (m + 1) + k] * y[l];
+      y[k] = acc / h[std::size_t(k) * (m + 1) + k];
+    }
+    for (int k = 0; k < cols; ++k) {
+      const GridVector& d = cfg.right_precond ? Z[k] : V[k];
+      for (std::size_t e = 0; e < d.a.size(); ++e) res.x.a[e] += y[k] * d.a[e];
+    }
+    GridVector rt = A(res.x);
+    for (std::size_t e = 0; e < rt.a.size(); ++e) rt.a[e] = rhs.a[e] - rt.a[e];
+    rnorm = nrm(rt);
+    r = std::move(rt);
+    if (rnorm / bnorm <= cfg.tol) {
+      res.report.status = SolveStatus::converged;
+      break;
+    }
+    if (broke) {
+      res.report.status = SolveStatus::breakdown;
+      break;
+    }
+  }
+  if (broke && rnorm / bnorm <= cfg.tol) res.report.status = SolveStatus::converged;
+  res.report.iterations = iter;
+  res.report.residual = rnorm / bnorm;
+  return res;
+}
+
+GridVector solve_cie(const AnomalyGrid& grid, const LayeredModel& model, const SpectralOperator& op,
+                     const GridVector& rhs, const SolverConfig& cfg, SolveReport* report) {
+  grid.validate(model);
+  if (cfg.right_precond) {  // flexible preconditioning needs the host-callback solver
+    const SystemOperator sys = build_system(grid, op);
+    FgmresResult r = fgmres([&](const GridVector& u) { return apply(sys, u); }, rhs, cfg);
+    if (report) *report = std::move(r.report);
+    return std::move(r.x);
+  }
+  if (!(cfg.tol > 0.0) || cfg.restart < 1 || cfg.max_iters < 1)
+    throw std::invalid_argument("fgmres: bad solver configuration");
+  const SystemOperator sys = build_system(grid, op);
+  GridVector x(rhs.nx, rhs.ny, rhs.nz);
+  emie_cu_report rep{};
+  std::vector<double> hist(std::size_t(cfg.max_iters) + 1);
+  check(emie_cu_fgmres_host(sys.device->h, dbl(rhs.a.data()), dbl(x.a.data()), 1, cfg.tol, cfg.restart,
+                            cfg.max_iters, &rep, hist.data(), static_cast<int>(hist.size()), nullptr));
+  if (report) {
+    report->status = static_cast<SolveStatus>(rep.status);
+    report->iterations = rep.iterations;
+    report->residual = rep.residual;
+    report->history.assign(hist.begin(), hist.begin() + std::min<int>(rep.history_len, int(hist.size())));
+    if (cfg.on_iteration)
+      for (std::size_t i = 0; i < report->history.size(); ++i) cfg.on_iteration(int(i) + 1, report->history[i]);
+  }
+  return x;
+}
+
+}  // namespace emie

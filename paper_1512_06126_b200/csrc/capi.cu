@@ -353,6 +353,28 @@ int emie_cu_operator_download_spectra(emie_cu_operator h, double* h_comp) {
   });
 }
 
+int emie_cu_operator_from_spectra(int nx, int ny, int nz, double omega, const double* h_comp,
+                                  emie_cu_operator* out) {
+  return guarded([&] {
+    if (!out || !h_comp) fail(EMIE_CU_INVALID_ARGUMENT, "operator_from_spectra: null pointer");
+    auto h = std::make_unique<emie_cu_operator_s>();
+    Operator& op = h->op;
+    init_operator_geometry(op, nx, ny, nz, omega);
+    std::vector<cplx> mm(op.modes() * op.nentD);
+    const cplx* in = reinterpret_cast<const cplx*>(h_comp);
+    const std::size_t modes = op.modes();
+    for (int c = 0; c < 6; ++c) {
+      const int nent_c = c < 4 ? op.ntri : op.nfull;
+      const int off = c < 4 ? c * op.ntri : 4 * op.ntri + (c - 4) * op.nfull;
+      for (std::size_t m = 0; m < modes; ++m)
+        for (int s = 0; s < nent_c; ++s) mm[m * op.nentD + op.emap_host[off + s].x] = in[m * nent_c + s];
+      in += modes * nent_c;
+    }
+    EMIE_CUDA(cudaMemcpy(op.spec, mm.data(), mm.size() * sizeof(cplx), cudaMemcpyHostToDevice));
+    *out = h.release();
+  });
+}
+
 int emie_cu_operator_download_blocks(emie_cu_operator h, double* h_blocks) {
   return guarded([&] {
     if (!h || !h_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
@@ -528,4 +550,41 @@ extern "C" int emie_cu_probe_fp64(double* tflops, void* stream) {
 extern "C" int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int beta,
                                      const double* h_s, int n, double* h_out) {
   return guarded([&] { kernel_output_host(oi, oj, hx, hy, alpha, beta, h_s, n, h_out); });
+}
+
+extern "C" int emie_cu_apply_spectral_host(emie_cu_operator h, const double* h_in, double* h_out,
+                                           int nrhs, void* stream) {
+  return guarded([&] {
+    if (!h || !h_in || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
+    const cudaStream_t st = as_stream(stream);
+    const std::size_t n = 3 * h->op.cells() * static_cast<std::size_t>(nrhs);
+    cplx* din = scratch<cplx>(n, st);
+    cplx* dout = scratch<cplx>(n, st);
+    EMIE_CUDA(cudaMemcpyAsync(din, h_in, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    apply_b(h->op, din, dout, nrhs, nullptr, st);
+    EMIE_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    release(din, st);
+    release(dout, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int emie_cu_fgmres_host(emie_cu_system h, const double* h_rhs, double* h_x, int nrhs,
+                                   double tol, int restart, int max_iters, emie_cu_report* reports,
+                                   double* h_history, int hist_cap, void* stream) {
+  return guarded([&] {
+    if (!h || !h_rhs || !h_x) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: nrhs < 1");
+    const cudaStream_t st = as_stream(stream);
+    const std::size_t n = 3 * h->sys.op->cells() * static_cast<std::size_t>(nrhs);
+    cplx* drhs = scratch<cplx>(n, st);
+    cplx* dx = scratch<cplx>(n, st);
+    EMIE_CUDA(cudaMemcpyAsync(drhs, h_rhs, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    fgmres_device(h->sys, drhs, dx, nrhs, tol, restart, max_iters, reports, h_history, hist_cap, st);
+    EMIE_CUDA(cudaMemcpyAsync(h_x, dx, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    release(drhs, st);
+    release(dx, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+  });
 }
