@@ -72,7 +72,30 @@ __device__ __forceinline__ cplx cexp(cplx x) {
   sincos(x.im, &s, &c);
   return {e * c, e * s};
 }
-__device__ __forceinline__ cplx scal2(cplx a, int e) { return {scalbn(a.re, e), scalbn(a.im, e)}; }
+// 2^e as a double for e in [-1022, 1023] (exponent bits built directly)
+__device__ __forceinline__ double pow2i(int e) {
+  return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+// a * 2^e without the software scalbn: one multiply in the normal range, two
+// half-steps outside it (exact unless the result itself under/overflows)
+__device__ __forceinline__ cplx scal2(cplx a, int e) {
+  if (e >= -1022 && e <= 1023) {
+    const double f = pow2i(e);
+    return {a.re * f, a.im * f};
+  }
+  e = max(-2200, min(2200, e));
+  const int e1 = e / 2, e2 = e - e1;
+  const double f1 = (e1 < -1022) ? 0.0 : pow2i(min(e1, 1023));
+  const double f2 = (e2 < -1022) ? 0.0 : pow2i(min(e2, 1023));
+  return {a.re * f1 * f2, a.im * f1 * f2};
+}
+// floor(log2 |x|) for finite x != 0 (ilogb without the library call)
+__device__ __forceinline__ int ilog2(double x) {
+  const long long b = __double_as_longlong(x);
+  const int ex = static_cast<int>((b >> 52) & 0x7ff);
+  if (ex != 0) return ex - 1023;
+  return ilogb(x);  // subnormal: rare
+}
 
 // ------------------------------------------------------ hankel helpers ----
 __device__ __forceinline__ double ediff(double a, double b) {  // hankel.cpp:22-26
@@ -286,6 +309,7 @@ struct Chunk {
   cplx* diag_a;
   // interval fields [lc][f][j]
   cplx* F;
+  double* lam;   // [8][lc]: lambda, 1/lambda, w00 w20 w02 w11 w10 w01
   int* E;        // [lc][4][j]: Pu_e, Pu_z, Pc_e, Pc_z
 };
 // interval field slots
@@ -319,7 +343,8 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
     C.one_q = s; s += LC * 2 * NL;
     C.diag_a = s; s += LC * 2 * NL;
     C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
-    C.E = reinterpret_cast<int*>(s);
+    C.lam = reinterpret_cast<double*>(s);  // [lc]: lambda, 1/lambda, 6 weights
+    C.E = reinterpret_cast<int*>(C.lam + 8 * LC);
   }
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
   auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 4 + f) * nz + j]; };
@@ -344,6 +369,14 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
   for (int t0 = 0; t0 < nw; t0 += LC) {
     const int lc = min(LC, nw - t0);
     __syncthreads();  // previous chunk consumed
+    // per-lambda scalars of the chunk
+    for (int li = threadIdx.x; li < lc; li += blockDim.x) {
+      const int t = t0 + li;
+      const double lam = exp((P.n1 + t) * P.step + P.shift) / R;
+      C.lam[li] = lam;
+      C.lam[LC + li] = 1.0 / lam;
+      for (int q = 0; q < 6; ++q) C.lam[(2 + q) * LC + li] = Woff[q * nw + t];
+    }
     // phase 0a: eta, e2l, em1 per (lambda, layer)
     for (int x = threadIdx.x; x < lc * NL; x += blockDim.x) {
       const int li = x / NL, m = x - li * NL;
@@ -472,36 +505,85 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
     }
     __syncthreads();
     // phase 1b: prefix products of theta per (lambda, gamma) as
-    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l
-    for (int x = threadIdx.x; x < lc * 2; x += blockDim.x) {
-      const int li = x >> 1, gm = x & 1;
-      const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
-      cplx m = {1.0, 0.0};
-      int e = 0, z = 0;
-      for (int j = 0; j < nz; ++j) {
-        F(li, fP, j) = m;
-        F(li, fPi, j) = crecip(m);
-        Ei(li, gm * 2, j) = e;
-        Ei(li, gm * 2 + 1, j) = z;
-        const cplx th = F(li, fT, j);
-        if (th.re == 0.0 && th.im == 0.0) {
-          ++z;
-        } else {
-          m = m * th;
-          const double a = fmax(fabs(m.re), fabs(m.im));
-          const int s = ilogb(a);
-          m = scal2(m, -s);
-          e += s;
+    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l. One warp
+    // per (lambda, gamma): a shuffle scan over 32-interval segments, the
+    // segment carry multiplied in, so the serial depth is log2(32) + nz/32.
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      const int nwarps = blockDim.x >> 5;
+      for (int task = warp; task < lc * 2; task += nwarps) {
+        const int li = task >> 1, gm = task & 1;
+        const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
+        cplx cm = {1.0, 0.0};  // carry: product of the previous segments
+        int ce = 0, cz = 0;
+        for (int j0 = 0; j0 < nz; j0 += 32) {
+          const int j = j0 + lane;
+          // this lane's factor, normalised
+          cplx m = {1.0, 0.0};
+          int e = 0, z = 0;
+          if (j < nz) {
+            const cplx th = F(li, fT, j);
+            if (th.re == 0.0 && th.im == 0.0) {
+              z = 1;
+            } else {
+              const int s = ilog2(fmax(fabs(th.re), fabs(th.im)));
+              m = scal2(th, -s);
+              e = s;
+            }
+          }
+          // inclusive scan (lane order = interval order)
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double mr = __shfl_up_sync(0xffffffffu, m.re, off);
+            const double mi = __shfl_up_sync(0xffffffffu, m.im, off);
+            const int oe = __shfl_up_sync(0xffffffffu, e, off);
+            const int oz = __shfl_up_sync(0xffffffffu, z, off);
+            if (lane >= off) {
+              m = cplx{mr, mi} * m;
+              const int s = ilog2(fmax(fabs(m.re), fabs(m.im)));
+              m = scal2(m, -s);
+              e += oe + s;
+              z += oz;
+            }
+          }
+          // exclusive prefix = carry x inclusive of the previous lane
+          cplx pm = {__shfl_up_sync(0xffffffffu, m.re, 1), __shfl_up_sync(0xffffffffu, m.im, 1)};
+          int pe = __shfl_up_sync(0xffffffffu, e, 1), pz = __shfl_up_sync(0xffffffffu, z, 1);
+          if (lane == 0) {
+            pm = {1.0, 0.0};
+            pe = 0;
+            pz = 0;
+          }
+          pm = cm * pm;
+          {
+            const int s = ilog2(fmax(fabs(pm.re), fabs(pm.im)));
+            pm = scal2(pm, -s);
+            pe += ce + s;
+          }
+          pz += cz;
+          if (j < nz) {
+            F(li, fP, j) = pm;
+            F(li, fPi, j) = crecip(pm);
+            Ei(li, gm * 2, j) = pe;
+            Ei(li, gm * 2 + 1, j) = pz;
+          }
+          // new carry: carry x inclusive of lane 31
+          const cplx lm = {__shfl_sync(0xffffffffu, m.re, 31), __shfl_sync(0xffffffffu, m.im, 31)};
+          const int le = __shfl_sync(0xffffffffu, e, 31), lz = __shfl_sync(0xffffffffu, z, 31);
+          cm = cm * lm;
+          const int s = ilog2(fmax(fabs(cm.re), fabs(cm.im)));
+          cm = scal2(cm, -s);
+          ce += le + s;
+          cz += lz;
         }
       }
     }
     __syncthreads();
     // phase 2: pairs x lambdas (greens.cpp:167-191)
     for (int li = 0; li < lc; ++li) {
-      const int t = t0 + li;
-      const double lam = exp((P.n1 + t) * P.step + P.shift) / R;
-      const double w00 = Woff[0 * nw + t], w20 = Woff[1 * nw + t], w02 = Woff[2 * nw + t];
-      const double w11 = Woff[3 * nw + t], w10 = Woff[4 * nw + t], w01 = Woff[5 * nw + t];
+      const double lam = C.lam[li], ilam = C.lam[LC + li];
+      const double w00 = C.lam[2 * LC + li], w20 = C.lam[3 * LC + li], w02 = C.lam[4 * LC + li];
+      const double w11 = C.lam[5 * LC + li], w10 = C.lam[6 * LC + li], w01 = C.lam[7 * LC + li];
 #pragma unroll
       for (int i = 0; i < kPairsPerThread; ++i) {
         if (!pv[i]) continue;
@@ -542,7 +624,7 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
         const cplx f4 = lam * V4;
         acc[i][5] = acc[i][5] + w10 * f4;
         acc[i][6] = acc[i][6] + w01 * f4;
-        const cplx f2 = (V1 + V3) * (1.0 / lam);
+        const cplx f2 = (V1 + V3) * ilam;
         acc[i][0] = acc[i][0] + w00 * (lam * V1);
         acc[i][1] = acc[i][1] + w20 * f2;
         acc[i][2] = acc[i][2] + w02 * f2;
@@ -763,7 +845,13 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
     const double dn = s.re * s.re + s.im * s.im;
     I.inv_sig = {s.re / dn, -s.im / dn};
   }
-  P.LC = std::max(1, std::min(32, 256 / nz));
+  // lambdas per chunk: as many as ~200 KB of SMEM holds (the serial per-chunk
+  // phases then run on more threads and there are fewer chunks), at most 32
+  {
+    const size_t per_lambda = (13 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
+                              8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
+    P.LC = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (200u << 10) / per_lambda)));
+  }
 
   keep_pool_warm();
   const int noff = op.nx * op.ny;
@@ -779,6 +867,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(noff) * op.nent * sizeof(cplx) + 16));
   const int NL = L + 1;
   const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 10 * NL + kFields * nz)) * sizeof(cplx) +
+                      8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
   const int groups = ceil_div(P.npairs, kGreenThreads * kPairsPerThread);
