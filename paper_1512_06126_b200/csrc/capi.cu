@@ -1,5 +1,6 @@
 // C ABI (include/emie_cu.h) over the sm_100a kernels. Validation mirrors the
 // reference's argument checks and maps its exception types onto status codes.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -156,6 +157,7 @@ Operator::~Operator() {
   cudaFree(tw_x);
   cudaFree(tw_y);
   cudaFree(emap);
+  cudaFree(ctab);
 }
 
 System::~System() {
@@ -205,17 +207,67 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.nfull = nz * nz;
   op.nent = 4 * op.ntri + 2 * op.nfull;
   op.nsd = nz / 2 + 1;
-  op.nentD = op.nent;  // compact wrapped-diagonal layout (operator.cuh)
+  op.mma = nz == 8 || nz == 16 || nz == 32;
+  // MMA layout (operator.cuh): bank of each element, bank-sorted triangles
+  std::vector<int> tri_pos;
+  const int H = nz / 2;
+  auto bank = [&](int k, int kp) { return (k + kp + ((H >= 8 && ((k ^ kp) & H)) ? 4 : 0)) & 7; };
+  if (op.mma) {
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    tri_pos.assign(static_cast<std::size_t>(nz) * nz, -1);
+    for (int k = 0; k < nz; ++k)
+      for (int kp = k; kp < nz; ++kp) {
+        const int b = bank(k, kp);
+        tri_pos[k * nz + kp] = tri_pos[kp * nz + k] = cnt[b]++ * 8 + b;
+      }
+    op.ntriP = 8 * *std::max_element(cnt, cnt + 8);
+    op.nentD = 4 * op.ntriP + 2 * op.nfull;
+  } else {
+    op.ntriP = op.ntri;
+    op.nentD = op.nent;  // compact wrapped-diagonal layout (operator.cuh)
+  }
   if (!make_plan(op.ex, op.plan_x) || !make_plan(op.ey, op.plan_y))
     fail(EMIE_CU_RUNTIME_ERROR, "toeplitz: planning failed");
   op.p2x = op.ex <= 2048 && make_pow2_plan(op.ex, op.plan_x2);
   op.p2y = op.ey <= 2048 && make_pow2_plan(op.ey, op.plan_y2);
   keep_pool_warm();
   op.spec = dev_alloc<cplx>(op.modes() * op.nentD);
+  if (op.nentD != op.nent)  // padding slots of the MMA layout are read, never written
+    EMIE_CUDA(cudaMemset(op.spec, 0, op.modes() * op.nentD * sizeof(cplx)));
   op.tw_x = upload_twiddles(op.ex);
   op.tw_y = upload_twiddles(op.ey);
-  // reference entry -> wrapped-diagonal slot (see operator.cuh)
   op.emap_host.assign(op.nent, int2{-1, -1});
+  if (op.mma) {
+    // reference entry -> MMA-layout slot, and the contraction's offset table
+    auto sym = [&](int c, int k, int kp) { return static_cast<uint32_t>(c * op.ntriP + tri_pos[k * nz + kp]); };
+    auto full = [&](int c, int r, int s) {
+      return static_cast<uint32_t>(4 * op.ntriP + c * op.nfull + r * nz + (s & ~7) + bank(r, s));
+    };
+    for (int c = 0; c < 4; ++c)
+      for (int k = 0; k < nz; ++k)
+        for (int kp = k; kp < nz; ++kp)
+          op.emap_host[c * op.ntri + k * nz - k * (k - 1) / 2 + (kp - k)] = int2{static_cast<int>(sym(c, k, kp)), -1};
+    for (int c = 0; c < 2; ++c)
+      for (int k = 0; k < nz; ++k)
+        for (int kp = 0; kp < nz; ++kp)
+          op.emap_host[4 * op.ntri + c * op.nfull + k * nz + kp] = int2{static_cast<int>(full(c, k, kp)), -1};
+    // M = [[xx xy xz] [xy yy yz] [-xz^T -yz^T zz]] (toeplitz.cpp:214-252)
+    std::vector<uint32_t> tab(9 * static_cast<std::size_t>(nz) * nz);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        for (int k = 0; k < nz; ++k)
+          for (int kp = 0; kp < nz; ++kp) {
+            uint32_t o;
+            if (a < 2 && b < 2) o = sym(a == b ? a : 3, k, kp);
+            else if (a == 2 && b == 2) o = sym(2, k, kp);
+            else if (b == 2) o = full(a, k, kp);
+            else o = full(b, kp, k) | 0x80000000u;
+            tab[((a * 3 + b) * nz + k) * nz + kp] = o;
+          }
+    op.ctab = dev_alloc<uint32_t>(tab.size());
+    EMIE_CUDA(cudaMemcpy(op.ctab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  } else {
+  // reference entry -> wrapped-diagonal slot (see operator.cuh)
   for (int c = 0; c < 4; ++c)
     for (int k = 0; k < nz; ++k)
       for (int kp = k; kp < nz; ++kp) {
@@ -234,6 +286,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
         const int t = ((kp - k) % nz + nz) % nz;
         op.emap_host[e] = int2{4 * op.ntri + c * op.nfull + t * nz + k, -1};
       }
+  }
   op.emap = dev_alloc<int2>(op.nent);
   EMIE_CUDA(cudaMemcpy(op.emap, op.emap_host.data(), op.nent * sizeof(int2), cudaMemcpyHostToDevice));
 }

@@ -248,33 +248,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// offset of M_ab(k, kp) in the mode block (wrapped-diagonal layout,
-// operator.cuh); bit 31 set when the entry enters negated (zx = -xz^T,
-// zy = -yz^T). NZ is a power of two here, so the wraps are masks.
-template <int NZ>
-__device__ __forceinline__ uint32_t coef_offset(int a, int b, int k, int kp) {
-  constexpr int ntri = NZ * (NZ + 1) / 2;
-  auto sym = [&](int c) -> uint32_t {
-    const int t = (kp - k) & (NZ - 1);
-    const int o = (2 * t < NZ) ? t * NZ + k : (2 * t > NZ) ? (NZ - t) * NZ + kp : t * NZ + (k < kp ? k : kp);
-    return c * ntri + o;
-  };
-  auto full = [&](int c, int r, int s) -> uint32_t {
-    const int t = (s - r) & (NZ - 1);
-    return 4 * ntri + c * NZ * NZ + t * NZ + r;
-  };
-  if (a == 0) return b == 0 ? sym(0) : b == 1 ? sym(3) : full(0, k, kp);
-  if (a == 1) return b == 0 ? sym(3) : b == 1 ? sym(1) : full(1, k, kp);
-  if (b == 2) return sym(2);
-  return (b == 0 ? full(0, kp, k) : full(1, kp, k)) | 0x80000000u;
-}
-
 template <int NZ>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1)
-    contract_mma_kernel(const cplx* __restrict__ op, cplx* S, int ex, int ey, int qx, int nmodes,
-                        int nrhs, int dbg) {
+    contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
+                        int ex, int ey, int qx, int nmodes, int nrhs, int nentD) {
   constexpr int np = 3 * NZ, ldu = np + 4;
-  constexpr int nentD = 2 * NZ * (2 * NZ + 1);
   constexpr int ntiles = np / 8, nk = np / 4;
   constexpr int TPW = (ntiles + kMmaWarps - 1) / kMmaWarps;  // tiles per warp
   constexpr int kBlkStages = 3, kUStages = 2;
@@ -299,7 +277,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
   auto issue_block = [&](int j) {
     const int qm = blockIdx.x + j * G;
     if (threadIdx.x == 0 && qm < nmodes) {
-      constexpr uint32_t blkbytes = nentD * sizeof(cplx);
+      const uint32_t blkbytes = nentD * sizeof(cplx);
       const int st = j % kBlkStages;
       mbar_expect_tx(bbar + st, blkbytes);
       bulk_g2s(blkbuf + st * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bbar + st);
@@ -319,18 +297,25 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
       }
     }
   };
-  // fragment coordinates: A row fr / k fc; B k fc / col fr; C row fr, cols 2fc..2fc+1
+  // fragment coordinates: A row fr / k fc; B k fc / col fr; C row fr, cols 2fc..2fc+1.
+  // Tile m of component a holds rows {4m..4m+3} u {4m+nz/2..4m+nz/2+3}
+  // (row fr -> 4m + fr/2 + (fr&1) nz/2): each quarter-warp reads rows r and
+  // r + nz/2, which the MMA layout puts in disjoint banks (operator.cuh).
   const int fr = lane >> 2, fc = lane & 3;
+  auto tile_row = [&](int rt) {
+    const int a = (8 * rt) / NZ, m = rt - a * (NZ / 8);
+    return a * NZ + 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
+  };
   // per-lane coefficient offsets of every (own tile, k step): mode independent
   uint32_t off[TPW][nk];
 #pragma unroll
   for (int i = 0; i < TPW; ++i) {
     const int rt = warp + i * kMmaWarps;
-    const int a = (8 * rt) / NZ, k0 = 8 * rt - a * NZ;
+    const int row = tile_row(rt), a = row / NZ, k = row - a * NZ;
 #pragma unroll
     for (int ks = 0; ks < nk; ++ks) {
-      const int b = (4 * ks) / NZ, kp0 = 4 * ks - b * NZ;
-      off[i][ks] = rt < ntiles ? coef_offset<NZ>(a, b, k0 + fr, kp0 + fc) : 0u;
+      const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
+      off[i][ks] = rt < ntiles ? __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) : 0u;
     }
   }
   // prologue: blocks of modes 0, 1; inputs of mode 0
@@ -340,24 +325,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
   int j = 0;
   for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
     // stages freed by mode j-1 (all warps passed the barrier at its end)
-    if (!(dbg & 2)) {
-      issue_cols(j + 1);
-      issue_block(j + 2);
-    }
+    issue_cols(j + 1);
+    issue_block(j + 2);
     const int bs_ = j % kBlkStages, us_ = j % kUStages;
-    if (!(dbg & 2) || j == 0) {
-      mbar_wait(bbar + bs_, static_cast<uint32_t>((j / kBlkStages) & 1));
-      mbar_wait(ubar + us_, static_cast<uint32_t>((j / kUStages) & 1));
-    }
+    mbar_wait(bbar + bs_, static_cast<uint32_t>((j / kBlkStages) & 1));
+    mbar_wait(ubar + us_, static_cast<uint32_t>((j / kUStages) & 1));
     const cplx* blk = blkbuf + bs_ * nentD;
     const cplx* U = ubuf + us_ * 8 * ldu + fr * ldu + fc;
     double p1[TPW][2], p2[TPW][2], p3[TPW][2];
 #pragma unroll
     for (int i = 0; i < TPW; ++i) p1[i][0] = p1[i][1] = p2[i][0] = p2[i][1] = p3[i][0] = p3[i][1] = 0.0;
-    if (!(dbg & 1)) {
+    {
 #pragma unroll
       for (int ks = 0; ks < nk; ++ks) {
-        const cplx bu = (dbg & 8) ? cplx{0.25 * ks, 1.0} : U[4 * ks];  // B[k = fc][col = fr]
+        const cplx bu = U[4 * ks];  // B[k = fc][col = fr]
         const double bs = bu.re + bu.im;
         // Branch-free: tiles past ntiles compute on offset 0 and are never
         // stored; the zx / zy negation flips the sign bit of the (shared) B
@@ -366,7 +347,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
 #pragma unroll
         for (int i = 0; i < TPW; ++i) {
           const uint32_t o = off[i][ks];
-          const cplx m = (dbg & 4) ? cplx{1.0 + ks, 0.5 * i} : blk[o & 0x7fffffffu];
+          const cplx m = blk[o & 0x7fffffffu];
           unsigned long long sg;
           if (NZ == 32 && kMmaWarps == 8)  // tiles w, w+8: only i == 1 is a z tile
             sg = (i == 1 && (4 * ks) / NZ < 2) ? 0x8000000000000000ull : 0ull;
@@ -387,7 +368,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
     for (int i = 0; i < TPW; ++i) {
       const int rt = warp + i * kMmaWarps;
       if (rt >= ntiles) continue;
-      const int plane = 8 * rt + fr;
+      const int plane = tile_row(rt);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = 2 * fc + h;
@@ -404,15 +385,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
     // (one after the initial zero fill suffices).
     __syncthreads();
   }
-}
-
-// experiment switch (EMIE_CT_DEBUG: 1 = skip the MMAs, 2 = skip the copies)
-int ct_debug() {
-  static const int v = [] {
-    const char* e = std::getenv("EMIE_CT_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
 }
 
 void set_smem(const void* fn, size_t bytes) {
@@ -444,7 +416,7 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
     for (int r0 = 0; r0 < nrhs; r0 += 2) {
       const int g = std::min(2, nrhs - r0);
       cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
-      const bool mma = op.nz == 8 || op.nz == 16 || op.nz == 32;
+      const bool mma = op.mma;
       if (mma) {
         const size_t smem = 128 + 3 * static_cast<size_t>(op.nentD) * sizeof(cplx) +
                             2 * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
@@ -454,11 +426,11 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
                                      : reinterpret_cast<const void*>(contract_mma_kernel<32>);
         set_smem(fn, smem);
         if (op.nz == 8)
-          contract_mma_kernel<8><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+          contract_mma_kernel<8><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
         else if (op.nz == 16)
-          contract_mma_kernel<16><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+          contract_mma_kernel<16><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
         else
-          contract_mma_kernel<32><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, Sg, op.ex, op.ey, op.qx, nmodes, g, ct_debug());
+          contract_mma_kernel<32><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
         check_launch("contract_mma_kernel");
         continue;
       }

@@ -32,9 +32,20 @@ struct Operator {
   double omega = 0.0;
   int ntri = 0, nfull = 0, nent = 0;
   int nsd = 0, nentD = 0;    // symmetric diagonals per component, diag block size
-  cplx* spec = nullptr;      // qx*qy*nentD (diagonal layout)
+  cplx* spec = nullptr;      // qx*qy*nentD (diagonal or MMA layout)
   int2* emap = nullptr;      // reference entry -> (slot, second slot or -1)
   std::vector<int2> emap_host;
+  // MMA layout (nz in {8, 16, 32}, contraction on the FP64 tensor cores):
+  // every nz x nz component is stored so that the element read by fragment
+  // lane (row k, col kp) lies in 16-byte bank f(k,kp) = k + kp + 4[(k^kp)&nz/2]
+  // (mod 8; the 4-term only for nz >= 16). Symmetric components (xx yy zz xy)
+  // hold their upper triangle bank-sorted, padded to ntriP = 8 * (largest bank
+  // count); full components (xz yz) are row-major with each aligned 8-run of
+  // kp rotated to bank f. With the tile rows {4m..4m+3} u {4m+nz/2..} every
+  // quarter-warp of a fragment load touches 8 distinct banks.
+  bool mma = false;
+  int ntriP = 0;
+  uint32_t* ctab = nullptr;  // [a][b][k][kp] -> slot of M_ab(k,kp), bit 31: negated
   cplx* blocks = nullptr;    // optional compressed blocks, (ny*nx)*nent
   cplx* tw_x = nullptr;      // e^{-2 pi i m/ex}
   cplx* tw_y = nullptr;      // e^{-2 pi i m/ey}
