@@ -227,163 +227,158 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
 // ------------------------------------------- contraction on FP64 MMA -----
 // Same product as contract_kernel, on the FP64 tensor cores (DMMA.8x8x4 via
 // mma.sync.m8n8k4.f64): measured 37 TF/s at 4 warps/SM on B200, where DFMA
-// needs ~32 warps to approach it. Used when nz is a multiple of 8 and
-// nz <= 32 (the whole mode block fits in SMEM twice).
-// One CTA (4 warps) owns one quadrant mode at a time, persistent over modes.
-// An elected thread brings the next mode's coefficient block (nentD complex,
-// one TMA bulk copy) and its input columns (one bulk copy per (mirror, rhs),
-// column stride np + 4 for conflict-free fragment loads) into the second
-// buffer while the CTA computes the current one.
-// Output rows are 8-row tiles (component a, rows k0..k0+7): 3nz/8 tiles,
-// round-robin over 8 warps (two per SMSP, so one warp's operand loads and
-// adds overlap the other's MMAs; for nz = 32 every SMSP gets 3 tiles); the 8 columns are the MMA's N; K runs over
+// needs ~32 warps to approach it. Used for nz in {8, 16, 32} with the MMA
+// operator layout (operator.cuh).
+// One CTA per SM, persistent over quadrant modes, warp-specialised:
+//  - 3nz/8 consumer warps, one 8-row output tile each (component a, rows
+//    {4m..4m+3} u {4m+nz/2..4m+nz/2+3}); for nz = 32 that is 12 warps, three
+//    per SMSP, so every SMSP's DMMA pipe has three independent tiles;
+//  - one producer warp whose elected lane brings each mode's coefficient
+//    block (one TMA bulk copy of nentD complex) and its input columns (one
+//    bulk copy per (mirror, rhs), column stride np + 4) into stage buffers
+//    guarded by full (tx-count) and empty (one arrive per consumer warp)
+//    mbarriers, so no CTA-wide barrier sits between modes.
+// The 8 columns (<= 4 mirrors x 2 rhs) are the MMA's N; K runs over
 // (component b, kp) in steps of 4. Complex products use three real MMAs
 // (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi); re = P1 - P2, im = P3 - P1 - P2).
-constexpr int kMmaWarps = 8;
-constexpr int kMmaTilesPerWarp = 3;
-
+// The zx / zy blocks (-xz^T, -yz^T) flip the sign bit of the B fragment.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+
+// mirror mi (0 .. nmir-1) of quadrant mode qm, in mode_cols order
+__device__ __forceinline__ int mirror_mode(int qm, int mi, int qx, int ex, int ey) {
+  const int qmy = qm / qx, qmx = qm - qmy * qx;
+  const bool mx_ok = qmx > 0 && (ex - qmx) > ex / 2;
+  const int mx = (mi == 3 || (mi == 1 && mx_ok)) ? ex - qmx : qmx;
+  const int my = (mi >= 2 || (mi == 1 && !mx_ok)) ? ey - qmy : qmy;
+  return mx * ey + my;
+}
+__device__ __forceinline__ int mirror_count(int qm, int qx, int ex, int ey) {
+  const int qmy = qm / qx, qmx = qm - qmy * qx;
+  const int a = (qmx > 0 && (ex - qmx) > ex / 2) ? 1 : 0;
+  const int b = (qmy > 0 && (ey - qmy) > ey / 2) ? 1 : 0;
+  return (1 + a) * (1 + b);
+}
 
 template <int NZ>
-__global__ void __launch_bounds__(kMmaWarps * 32, 1)
+constexpr int mma_warps() { return 3 * NZ / 8; }
+constexpr int kBlkStages = 3, kUStages = 2;
+
+template <int NZ>
+__global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
                         int ex, int ey, int qx, int nmodes, int nrhs, int nentD) {
   constexpr int np = 3 * NZ, ldu = np + 4;
-  constexpr int ntiles = np / 8, nk = np / 4;
-  constexpr int TPW = (ntiles + kMmaWarps - 1) / kMmaWarps;  // tiles per warp
-  constexpr int kBlkStages = 3, kUStages = 2;
+  constexpr int nk = np / 4;
+  constexpr int W = mma_warps<NZ>();
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bbar = reinterpret_cast<uint64_t*>(smraw);   // block stages
-  uint64_t* ubar = bbar + kBlkStages;                     // input stages
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* bempty = bfull + kBlkStages;
+  uint64_t* ufull = bempty + kBlkStages;
+  uint64_t* uempty = ufull + kUStages;
   cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128);
   cplx* ubuf = blkbuf + kBlkStages * nentD;
   const size_t E = static_cast<size_t>(ex) * ey;
   constexpr uint32_t colbytes = np * sizeof(cplx);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kBlkStages; ++i) mbar_init(bbar + i, 1);
-    for (int i = 0; i < kUStages; ++i) mbar_init(ubar + i, 1);
+    for (int i = 0; i < kBlkStages; ++i) {
+      mbar_init(bfull + i, 1);
+      mbar_init(bempty + i, W);
+    }
+    for (int i = 0; i < kUStages; ++i) {
+      mbar_init(ufull + i, 1);
+      mbar_init(uempty + i, W);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // columns past a mode's ncol are multiplied but never stored: keep them finite
   for (int i = threadIdx.x; i < kUStages * 8 * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
   __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const int G = gridDim.x;
-  // j-th mode of this CTA: blockIdx.x + j*G
-  auto issue_block = [&](int j) {
-    const int qm = blockIdx.x + j * G;
-    if (threadIdx.x == 0 && qm < nmodes) {
-      const uint32_t blkbytes = nentD * sizeof(cplx);
-      const int st = j % kBlkStages;
-      mbar_expect_tx(bbar + st, blkbytes);
-      bulk_g2s(blkbuf + st * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bbar + st);
-    }
-  };
-  auto issue_cols = [&](int j) {
-    const int qm = blockIdx.x + j * G;
-    if (threadIdx.x == 0 && qm < nmodes) {
-      const ModeCols mc = mode_cols(qm, qx, ex, ey);
-      const int ncol = mc.nmir * nrhs;
-      const int st = j % kUStages;
-      mbar_expect_tx(ubar + st, ncol * colbytes);
-      cplx* dst = ubuf + st * 8 * ldu;
-      for (int col = 0; col < ncol; ++col) {
-        const int mi = col / nrhs, r = col - mi * nrhs;
-        bulk_g2s(dst + col * ldu, S + (static_cast<size_t>(r) * E + mc.mode[mi]) * np, colbytes, ubar + st);
+
+  if (warp == W) {  // ---- producer
+    if (lane == 0) {
+      int j = 0;
+      for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
+        const int bs = j % kBlkStages, us = j % kUStages;
+        if (j >= kBlkStages) mbar_wait(bempty + bs, static_cast<uint32_t>((j / kBlkStages - 1) & 1));
+        const uint32_t blkbytes = nentD * sizeof(cplx);
+        mbar_expect_tx(bfull + bs, blkbytes);
+        bulk_g2s(blkbuf + bs * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bfull + bs);
+        if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
+        const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
+        mbar_expect_tx(ufull + us, ncol * colbytes);
+        cplx* dst = ubuf + us * 8 * ldu;
+        for (int col = 0; col < ncol; ++col) {
+          const int mi = col / nrhs, r = col - mi * nrhs;
+          bulk_g2s(dst + col * ldu, S + (static_cast<size_t>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np,
+                   colbytes, ufull + us);
+        }
       }
     }
-  };
-  // fragment coordinates: A row fr / k fc; B k fc / col fr; C row fr, cols 2fc..2fc+1.
-  // Tile m of component a holds rows {4m..4m+3} u {4m+nz/2..4m+nz/2+3}
-  // (row fr -> 4m + fr/2 + (fr&1) nz/2): each quarter-warp reads rows r and
-  // r + nz/2, which the MMA layout puts in disjoint banks (operator.cuh).
-  const int fr = lane >> 2, fc = lane & 3;
-  auto tile_row = [&](int rt) {
-    const int a = (8 * rt) / NZ, m = rt - a * (NZ / 8);
-    return a * NZ + 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
-  };
-  // per-lane coefficient offsets of every (own tile, k step): mode independent
-  uint32_t off[TPW][nk];
-#pragma unroll
-  for (int i = 0; i < TPW; ++i) {
-    const int rt = warp + i * kMmaWarps;
-    const int row = tile_row(rt), a = row / NZ, k = row - a * NZ;
-#pragma unroll
-    for (int ks = 0; ks < nk; ++ks) {
-      const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
-      off[i][ks] = rt < ntiles ? __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) : 0u;
-    }
+    return;
   }
-  // prologue: blocks of modes 0, 1; inputs of mode 0
-  issue_block(0);
-  issue_block(1);
-  issue_cols(0);
+
+  // ---- consumers. Fragment coordinates: A row fr / k fc; B k fc / col fr;
+  // C row fr, cols 2fc..2fc+1. Row fr of the tile -> 4m + fr/2 + (fr&1) nz/2:
+  // each quarter-warp reads rows r and r + nz/2, which the MMA layout puts in
+  // disjoint banks (operator.cuh).
+  const int fr = lane >> 2, fc = lane & 3;
+  const int a = warp / (NZ / 8), m = warp - a * (NZ / 8);
+  const int k = 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
+  const int plane = a * NZ + k;
+  const unsigned long long zsg = a == 2 ? 0x8000000000000000ull : 0ull;
+  // per-lane coefficient offsets of every k step: mode independent
+  uint32_t off[nk];
+#pragma unroll
+  for (int ks = 0; ks < nk; ++ks) {
+    const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
+    off[ks] = __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) & 0x7fffffffu;
+  }
   int j = 0;
   for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
-    // stages freed by mode j-1 (all warps passed the barrier at its end)
-    issue_cols(j + 1);
-    issue_block(j + 2);
-    const int bs_ = j % kBlkStages, us_ = j % kUStages;
-    mbar_wait(bbar + bs_, static_cast<uint32_t>((j / kBlkStages) & 1));
-    mbar_wait(ubar + us_, static_cast<uint32_t>((j / kUStages) & 1));
-    const cplx* blk = blkbuf + bs_ * nentD;
-    const cplx* U = ubuf + us_ * 8 * ldu + fr * ldu + fc;
-    double p1[TPW][2], p2[TPW][2], p3[TPW][2];
+    const int bs = j % kBlkStages, us = j % kUStages;
+    mbar_wait(bfull + bs, static_cast<uint32_t>((j / kBlkStages) & 1));
+    mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
+    const cplx* blk = blkbuf + bs * nentD;
+    const cplx* U = ubuf + us * 8 * ldu + fr * ldu + fc;
+    double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < TPW; ++i) p1[i][0] = p1[i][1] = p2[i][0] = p2[i][1] = p3[i][0] = p3[i][1] = 0.0;
-    {
+    for (int ks = 0; ks < nk; ++ks) {
+      const cplx bu = U[4 * ks];  // B[k = fc][col = fr]
+      const cplx mv = blk[off[ks]];
+      const unsigned long long sg = (4 * ks) / NZ < 2 ? zsg : 0ull;
+      const double br = __longlong_as_double(__double_as_longlong(bu.re) ^ sg);
+      const double bi = __longlong_as_double(__double_as_longlong(bu.im) ^ sg);
+      const double bss = __longlong_as_double(__double_as_longlong(bu.re + bu.im) ^ sg);
+      dmma(p1[0], p1[1], mv.re, br);
+      dmma(p2[0], p2[1], mv.im, bi);
+      dmma(p3[0], p3[1], mv.re + mv.im, bss);
+    }
+    // stage reads are complete (the DMMAs consumed them): release both stages
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(bempty + bs);
+      mbar_arrive(uempty + us);
+    }
+    const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
 #pragma unroll
-      for (int ks = 0; ks < nk; ++ks) {
-        const cplx bu = U[4 * ks];  // B[k = fc][col = fr]
-        const double bs = bu.re + bu.im;
-        // Branch-free: tiles past ntiles compute on offset 0 and are never
-        // stored; the zx / zy negation flips the sign bit of the (shared) B
-        // fragment (with NZ == 32 and 8 warps, tile i = 1 is the z component,
-        // so the flag folds at compile time).
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-          const uint32_t o = off[i][ks];
-          const cplx m = blk[o & 0x7fffffffu];
-          unsigned long long sg;
-          if (NZ == 32 && kMmaWarps == 8)  // tiles w, w+8: only i == 1 is a z tile
-            sg = (i == 1 && (4 * ks) / NZ < 2) ? 0x8000000000000000ull : 0ull;
-          else
-            sg = static_cast<unsigned long long>(o >> 31) << 63;
-          const double br = __longlong_as_double(__double_as_longlong(bu.re) ^ sg);
-          const double bi = __longlong_as_double(__double_as_longlong(bu.im) ^ sg);
-          const double bss = __longlong_as_double(__double_as_longlong(bs) ^ sg);
-          dmma(p1[i][0], p1[i][1], m.re, br);
-          dmma(p2[i][0], p2[i][1], m.im, bi);
-          dmma(p3[i][0], p3[i][1], m.re + m.im, bss);
-        }
+    for (int h = 0; h < 2; ++h) {
+      const int col = 2 * fc + h;
+      if (col < ncol) {
+        const int mi = nrhs == 2 ? col >> 1 : col, r = nrhs == 2 ? col & 1 : 0;
+        const cplx v = {p1[h] - p2[h], p3[h] - p1[h] - p2[h]};
+        S[(static_cast<size_t>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np + plane] = v;
       }
     }
-    const ModeCols mc = mode_cols(qm, qx, ex, ey);
-    const int ncol = mc.nmir * nrhs;
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-      const int rt = warp + i * kMmaWarps;
-      if (rt >= ntiles) continue;
-      const int plane = tile_row(rt);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = 2 * fc + h;
-        if (col < ncol) {
-          const int mi = nrhs == 2 ? col >> 1 : col, r = nrhs == 2 ? col & 1 : 0;
-          const cplx v = {p1[i][h] - p2[i][h], p3[i][h] - p1[i][h] - p2[i][h]};
-          S[(static_cast<size_t>(r) * E + mc.mode[mi]) * np + plane] = v;
-        }
-      }
-    }
-    // stages of mode j fully consumed (their reads are done: values are in
-    // registers) before the next iterations refill them. The buffers are only
-    // ever read through the generic proxy, so no proxy fence is needed here
-    // (one after the initial zero fill suffices).
-    __syncthreads();
   }
 }
 
@@ -418,19 +413,17 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
       cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
       const bool mma = op.mma;
       if (mma) {
-        const size_t smem = 128 + 3 * static_cast<size_t>(op.nentD) * sizeof(cplx) +
-                            2 * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
+        const size_t smem = 128 + kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                            kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
         const int grid = std::max(1, std::min(sms, nmodes));
-        const void* fn = op.nz == 8 ? reinterpret_cast<const void*>(contract_mma_kernel<8>)
-                       : op.nz == 16 ? reinterpret_cast<const void*>(contract_mma_kernel<16>)
-                                     : reinterpret_cast<const void*>(contract_mma_kernel<32>);
-        set_smem(fn, smem);
-        if (op.nz == 8)
-          contract_mma_kernel<8><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
-        else if (op.nz == 16)
-          contract_mma_kernel<16><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
-        else
-          contract_mma_kernel<32><<<grid, kMmaWarps * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g, op.nentD);
+        auto launch = [&](auto kern, int warps) {
+          set_smem(reinterpret_cast<const void*>(kern), smem);
+          kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g,
+                                                     op.nentD);
+        };
+        if (op.nz == 8) launch(contract_mma_kernel<8>, mma_warps<8>());
+        else if (op.nz == 16) launch(contract_mma_kernel<16>, mma_warps<16>());
+        else launch(contract_mma_kernel<32>, mma_warps<32>());
         check_launch("contract_mma_kernel");
         continue;
       }
