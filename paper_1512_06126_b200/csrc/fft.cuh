@@ -12,6 +12,8 @@
 // 2*half). Twiddles come from a host table computed in long double.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace emie_cu {
@@ -184,17 +186,43 @@ __device__ __forceinline__ cplx w16(int m, double s) {
   return {cos16(m), s * cos16(m + 12)};  // sin(x) = cos(x - pi/2)
 }
 
+// x * e^{s 2 pi i m / 16} for a compile-time m, without the multiplications
+// by 0 and 1 that IEEE semantics keep in a general product
+template <int m>
+__device__ __forceinline__ cplx mulw16(cplx x, double s) {
+  constexpr int q = m & 15;
+  constexpr double h = 0.70710678118654752440;
+  if constexpr (q == 0) {
+    return x;
+  } else if constexpr (q == 4) {  // s i
+    return {-s * x.im, s * x.re};
+  } else if constexpr (q == 8) {
+    return {-x.re, -x.im};
+  } else if constexpr (q == 12) {  // -s i
+    return {s * x.im, -s * x.re};
+  } else if constexpr (q == 2 || q == 6 || q == 10 || q == 14) {
+    // (c + i s sn) with |c| = |sn| = h
+    constexpr double c = (q == 2 || q == 14) ? h : -h;
+    constexpr double sn = (q == 2 || q == 6) ? h : -h;
+    const double si = s * sn;
+    return {c * x.re - si * x.im, c * x.im + si * x.re};
+  } else {
+    const cplx w = w16(q, s);
+    return x * w;
+  }
+}
+
 template <>
 __device__ __forceinline__ void butterfly<8>(cplx* v, double s) {
   // 8 = 2 x 4: DFT4 over (a + 2c), twiddle W8^{ab}, DFT2 over a
   cplx e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
   butterfly<4>(e, s);
   butterfly<4>(o, s);
+  const cplx t[4] = {o[0], mulw16<2>(o[1], s), mulw16<4>(o[2], s), mulw16<6>(o[3], s)};
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const cplx t = o[b] * w16(2 * b, s);
-    v[b] = e[b] + t;
-    v[b + 4] = e[b] - t;
+    v[b] = e[b] + t[b];
+    v[b + 4] = e[b] - t[b];
   }
 }
 
@@ -202,14 +230,19 @@ template <>
 __device__ __forceinline__ void butterfly<16>(cplx* v, double s) {
   // 16 = 4 x 4 (n = a + 4c, k = b + 4d), in place; the final 4x4 transpose
   // is a register renaming once unrolled
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
+  auto col = [&](auto A) {
+    constexpr int a = decltype(A)::value;
     cplx q[4] = {v[a], v[a + 4], v[a + 8], v[a + 12]};
     butterfly<4>(q, s);
     v[a] = q[0];
-#pragma unroll
-    for (int b = 1; b < 4; ++b) v[a + 4 * b] = (a == 0) ? q[b] : q[b] * w16(a * b, s);
-  }
+    v[a + 4] = mulw16<a * 1>(q[1], s);
+    v[a + 8] = mulw16<a * 2>(q[2], s);
+    v[a + 12] = mulw16<a * 3>(q[3], s);
+  };
+  col(std::integral_constant<int, 0>{});
+  col(std::integral_constant<int, 1>{});
+  col(std::integral_constant<int, 2>{});
+  col(std::integral_constant<int, 3>{});
   // v[a + 4b] = y[a][b]
 #pragma unroll
   for (int b = 0; b < 4; ++b) {

@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(256, 2) spectra_y_kernel(const cplx* __restric
 // the spectrum is stored and again when it is read back, so the per-mode
 // contraction is sign-free: out = D M D u.
 __device__ __forceinline__ double mirror_sign(int plane, int nz, int my, int mx, int ey, int ex) {
-  const int c = plane / nz;
-  return ((c == 0 && mx > ex / 2) || (c == 1 && my > ey / 2)) ? -1.0 : 1.0;
+  // component c = plane / nz without the division: x planes [0, nz), y planes [nz, 2nz)
+  return ((plane < nz && 2 * mx > ex) || (plane >= nz && plane < 2 * nz && 2 * my > ey)) ? -1.0 : 1.0;
 }
 
 // forward x of rows iy0.. of plane pr = r*np + plane; r2 (cie.cpp:63-65) on load
