@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import bisect
 import ctypes
+import os as _os
 import math
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -44,6 +45,8 @@ __all__ = [
 
 _PKG = Path(__file__).resolve().parent
 _LIB_PATH = _PKG / "libemie_cu.so"
+if _os.environ.get("EMIE_CU_LIBRARY"):  # developer override (kernel experiments)
+    _LIB_PATH = Path(_os.environ["EMIE_CU_LIBRARY"]).resolve()
 SIGMA_FLOOR = 1e-9  # include/emie/layered.hpp:32
 MU0 = 1.2566370614359172e-06
 

@@ -340,8 +340,6 @@ struct Geo {
   static constexpr int ntr = kStreamElems / N;  // transforms per tile
   static constexpr int ldp = N + N / 16 + 1;    // = fft_ldp(N)
   static constexpr int tile = ntr * ldp;        // padded tile, elements
-  static constexpr int lgN = N >= 2048 ? 11 : N >= 1024 ? 10 : N >= 512 ? 9 : N >= 256 ? 8 : N >= 128 ? 7
-                           : N >= 64 ? 6 : N >= 32 ? 5 : 4;
   __device__ static __forceinline__ int at(int t, int j) { return t * ldp + j + (j >> 4); }
 };
 

@@ -20,6 +20,10 @@
 
 #include "operator.cuh"
 
+#ifndef EMIE_CT_EXPERIMENT
+#define EMIE_CT_EXPERIMENT 0  // 1: no MMAs, 2: no copies (timing experiments only)
+#endif
+
 namespace emie_cu {
 
 namespace {
@@ -56,6 +60,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
   asm volatile(
@@ -269,6 +276,14 @@ __device__ __forceinline__ int mirror_count(int qm, int qx, int ex, int ey) {
 template <int NZ>
 constexpr int mma_warps() { return 3 * NZ / 8; }
 constexpr int kBlkStages = 3, kUStages = 2;
+#ifndef EMIE_CT_L2AHEAD
+#define EMIE_CT_L2AHEAD 0
+#endif
+#ifndef EMIE_CT_ACC
+#define EMIE_CT_ACC 1
+#endif
+constexpr int kL2Ahead = EMIE_CT_L2AHEAD;  // modes past the SMEM stages prefetched to L2
+constexpr int kAcc = EMIE_CT_ACC;          // accumulator sets per DMMA chain
 
 template <int NZ>
 __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
@@ -283,7 +298,9 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   uint64_t* bempty = bfull + kBlkStages;
   uint64_t* ufull = bempty + kBlkStages;
   uint64_t* uempty = ufull + kUStages;
-  cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128);
+  // per input stage: output offsets (r*E + mode)*np of its 8 columns (-1: none)
+  long long* colbase = reinterpret_cast<long long*>(smraw + 128);
+  cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128 + kUStages * 8 * sizeof(long long));
   cplx* ubuf = blkbuf + kBlkStages * nentD;
   const size_t E = static_cast<size_t>(ex) * ey;
   constexpr uint32_t colbytes = np * sizeof(cplx);
@@ -311,17 +328,33 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         const int bs = j % kBlkStages, us = j % kUStages;
         if (j >= kBlkStages) mbar_wait(bempty + bs, static_cast<uint32_t>((j / kBlkStages - 1) & 1));
         const uint32_t blkbytes = nentD * sizeof(cplx);
+        // blocks of the modes after the SMEM stages go to L2 ahead of their copy
+        for (int d = (j == 0 ? kBlkStages : kL2Ahead); d <= kL2Ahead; ++d) {
+          const int qp = qm + d * G;
+          if (qp < nmodes) bulk_prefetch_l2(op + static_cast<size_t>(qp) * nentD, blkbytes);
+        }
+#if EMIE_CT_EXPERIMENT == 2
+        mbar_expect_tx(bfull + bs, 0);
+#else
         mbar_expect_tx(bfull + bs, blkbytes);
         bulk_g2s(blkbuf + bs * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bfull + bs);
+#endif
         if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
         const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
+        long long base[8];
+        for (int col = 0; col < 8; ++col) {
+          const int mi = col / nrhs, r = col - mi * nrhs;
+          base[col] = col < ncol ? (static_cast<long long>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np : -1LL;
+          colbase[us * 8 + col] = base[col];
+        }
+        // the column table is published by the arrive (release) below
+#if EMIE_CT_EXPERIMENT == 2
+        mbar_expect_tx(ufull + us, 0);
+#else
         mbar_expect_tx(ufull + us, ncol * colbytes);
         cplx* dst = ubuf + us * 8 * ldu;
-        for (int col = 0; col < ncol; ++col) {
-          const int mi = col / nrhs, r = col - mi * nrhs;
-          bulk_g2s(dst + col * ldu, S + (static_cast<size_t>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np,
-                   colbytes, ufull + us);
-        }
+        for (int col = 0; col < ncol; ++col) bulk_g2s(dst + col * ldu, S + base[col], colbytes, ufull + us);
+#endif
       }
     }
     return;
@@ -350,35 +383,54 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
     const cplx* blk = blkbuf + bs * nentD;
     const cplx* U = ubuf + us * 8 * ldu + fr * ldu + fc;
-    double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+    double p1[kAcc][2] = {}, p2[kAcc][2] = {}, p3[kAcc][2] = {};
+    // operands PD k-steps ahead of their MMAs (SMEM latency off the DMMA chain)
+    constexpr int PD = 6;
+    cplx av[PD], bv[PD];
 #pragma unroll
-    for (int ks = 0; ks < nk; ++ks) {
-      const cplx bu = U[4 * ks];  // B[k = fc][col = fr]
-      const cplx mv = blk[off[ks]];
+    for (int ks = 0; ks < PD; ++ks) {
+      av[ks] = blk[off[ks]];
+      bv[ks] = U[4 * ks];
+    }
+#pragma unroll
+    for (int ks = 0; ks < (EMIE_CT_EXPERIMENT == 1 ? 0 : nk); ++ks) {
+      const cplx bu = bv[ks % PD];  // B[k = fc][col = fr]
+      const cplx mv = av[ks % PD];
+      if (ks + PD < nk) {
+        av[ks % PD] = blk[off[ks + PD]];
+        bv[ks % PD] = U[4 * (ks + PD)];
+      }
+      // zx / zy (-xz^T, -yz^T): the z tile flips the sign of the B fragment for b < 2
       const unsigned long long sg = (4 * ks) / NZ < 2 ? zsg : 0ull;
       const double br = __longlong_as_double(__double_as_longlong(bu.re) ^ sg);
       const double bi = __longlong_as_double(__double_as_longlong(bu.im) ^ sg);
       const double bss = __longlong_as_double(__double_as_longlong(bu.re + bu.im) ^ sg);
-      dmma(p1[0], p1[1], mv.re, br);
-      dmma(p2[0], p2[1], mv.im, bi);
-      dmma(p3[0], p3[1], mv.re + mv.im, bss);
+      const int h = kAcc == 1 ? 0 : (ks & 1);
+      dmma(p1[h][0], p1[h][1], mv.re, br);
+      dmma(p2[h][0], p2[h][1], mv.im, bi);
+      dmma(p3[h][0], p3[h][1], mv.re + mv.im, bss);
     }
-    // stage reads are complete (the DMMAs consumed them): release both stages
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(bempty + bs);
-      mbar_arrive(uempty + us);
-    }
-    const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
+    double q1[2], q2[2], q3[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int col = 2 * fc + h;
-      if (col < ncol) {
-        const int mi = nrhs == 2 ? col >> 1 : col, r = nrhs == 2 ? col & 1 : 0;
-        const cplx v = {p1[h] - p2[h], p3[h] - p1[h] - p2[h]};
-        S[(static_cast<size_t>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np + plane] = v;
+      q1[h] = p1[0][h];
+      q2[h] = p2[0][h];
+      q3[h] = p3[0][h];
+#pragma unroll
+      for (int c = 1; c < kAcc; ++c) {
+        q1[h] += p1[c][h];
+        q2[h] += p2[c][h];
+        q3[h] += p3[c][h];
       }
     }
+    // block stage reads are complete (the DMMAs consumed them): release it
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bempty + bs);
+    const long long cb0 = colbase[us * 8 + 2 * fc], cb1 = colbase[us * 8 + 2 * fc + 1];
+    if (cb0 >= 0) S[cb0 + plane] = cplx{q1[0] - q2[0], q3[0] - q1[0] - q2[0]};
+    if (cb1 >= 0) S[cb1 + plane] = cplx{q1[1] - q2[1], q3[1] - q1[1] - q2[1]};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(uempty + us);  // input columns and their table
   }
 }
 
@@ -413,11 +465,14 @@ void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const 
       cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
       const bool mma = op.mma;
       if (mma) {
-        const size_t smem = 128 + kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+        const size_t smem = 128 + kUStages * 8 * sizeof(long long) +
+                            kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
                             kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
-        const int grid = std::max(1, std::min(sms, nmodes));
         auto launch = [&](auto kern, int warps) {
           set_smem(reinterpret_cast<const void*>(kern), smem);
+          int per_sm = 1;
+          EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (warps + 1) * 32, smem));
+          const int grid = std::max(1, std::min(sms * std::max(1, per_sm), nmodes));
           kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g,
                                                      op.nentD);
         };
