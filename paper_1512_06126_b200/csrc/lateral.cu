@@ -321,11 +321,17 @@ __global__ void __launch_bounds__(256, 2) apply_ix_kernel(const cplx* __restrict
 // each transform (the zero half of the embedding is never loaded) and applies
 // the per-element prescaling (r2, mirror signs); the operands of the prescale
 // and of the system epilogue are fetched into registers when the tile starts.
+#ifndef EMIE_STREAM_EXPERIMENT
+// timing experiments only: 1 no FFT passes, 2 no loads, 3 no loads or stores, 4 loads only
+#define EMIE_STREAM_EXPERIMENT 0
+#endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+#if EMIE_STREAM_EXPERIMENT != 2 && EMIE_STREAM_EXPERIMENT != 3
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int K>
@@ -378,13 +384,64 @@ __device__ __forceinline__ void spass(cplx* buf, const cplx* tw) {
   __syncthreads();
 }
 
+// radix of the last pass: 16 when N is a power of 16, else the remainder
+template <int N>
+constexpr int last_radix() {
+  int n = N;
+  while (n > 16) n /= 16;
+  return n;
+}
+
+// passes at strides NS .. < N / last_radix (the middle passes)
 template <int N, int NS, bool INV>
-__device__ __forceinline__ void spasses(cplx* buf, const cplx* tw) {
-  if constexpr (NS * 16 <= N) {
+__device__ __forceinline__ void smid(cplx* buf, const cplx* tw) {
+  constexpr int NSL = N / last_radix<N>();
+  if constexpr (NS < NSL) {
     spass<N, 16, NS, INV>(buf, tw);
-    spasses<N, NS * 16, INV>(buf, tw);
-  } else if constexpr (NS < N) {
-    spass<N, N / NS, NS, INV>(buf, tw);
+    smid<N, NS * 16, INV>(buf, tw);
+  }
+}
+
+// Last pass (stride NS = N/R): thread b-th butterfly w -> (transform t, j);
+// output r of it is element jo = j + r*NS of transform t, handed to
+// p.emit(ops, t, jo, b, r, value) straight from registers. TF: transform
+// index fastest across lanes (fx, fy: their global rows run along t), else
+// element index fastest (iy, ix).
+template <int N, bool TF>
+__device__ __forceinline__ void last_coord(int b, int& t, int& j) {
+  constexpr int R = last_radix<N>(), NS = N / R, NT = Geo<N>::ntr;
+  const int w = threadIdx.x + b * kStreamThreads;
+  if (TF) {
+    t = w % NT;
+    j = w / NT;
+  } else {
+    t = w / NS;
+    j = w % NS;
+  }
+}
+template <int N, bool INV, class P>
+__device__ __forceinline__ void slast(const cplx* buf, const cplx* tw, const P& p, const typename P::Ops& ops) {
+  using G = Geo<N>;
+  constexpr int R = last_radix<N>(), NS = N / R, B = kFftEPT / R;
+  constexpr double s = INV ? 1.0 : -1.0;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    int t, j;
+    last_coord<N, P::kTFast>(b, t, j);
+    cplx v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      cplx x = buf[G::at(t, j + r * NS)];
+      if (r > 0) {
+        cplx wv = tw[r * j];  // e^{-2 pi i r j / N}: TSTEP = 1 in the last pass
+        if (INV) wv.im = -wv.im;
+        x = x * wv;
+      }
+      v[r] = x;
+    }
+    butterfly<R>(v, s);
+#pragma unroll
+    for (int r = 0; r < R; ++r) p.template emit<N>(ops, t, j + r * NS, b, r, v[r]);
   }
 }
 
@@ -411,44 +468,79 @@ __device__ __forceinline__ void spass_first(cplx* buf, const P& p, const typenam
 
 // The persistent driver. P supplies ntiles(), load<N>(tile, buf) (cp.async),
 // prefetch<N>(tile, ops), pre(ops, t, r, jj, x), nin and store<N>(tile, buf, ops).
+#ifndef EMIE_STREAM_NBUF
+#define EMIE_STREAM_NBUF 2
+#endif
+constexpr int kStreamBufs = EMIE_STREAM_NBUF;  // tile buffers per CTA (prefetch depth + 1)
+
 template <int N, class P>
-__global__ void __launch_bounds__(kStreamThreads, 3) stream_fft_kernel(P p, const cplx* __restrict__ tw) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamBufs == 2 ? 3 : 2)
+    stream_fft_kernel(P p, const cplx* __restrict__ tw) {
   using G = Geo<N>;
+  constexpr int NB = kStreamBufs;
   extern __shared__ cplx sm[];
-  cplx* tws = sm + 2 * G::tile;
+  cplx* tws = sm + NB * G::tile;
   load_twiddles(tws, tw, N);
   const int ntiles = p.ntiles();
   int tile = blockIdx.x;
-  if (tile < ntiles) p.template load<N>(tile, sm);
-  cp_async_commit();
+#pragma unroll
+  for (int b = 0; b < NB - 1; ++b) {
+    const int t = tile + b * gridDim.x;
+    if (t < ntiles) p.template load<N>(t, sm + b * G::tile);
+    cp_async_commit();
+  }
 #pragma unroll 1
   for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
-    cplx* cur = (i & 1) ? sm + G::tile : sm;
-    cplx* nxt = (i & 1) ? sm : sm + G::tile;
-    const int next = tile + gridDim.x;
-    if (next < ntiles) p.template load<N>(next, nxt);
+    cplx* cur = sm + (i % NB) * G::tile;
+    const int next = tile + (NB - 1) * gridDim.x;
+    if (next < ntiles) p.template load<N>(next, sm + ((i + NB - 1) % NB) * G::tile);
     cp_async_commit();
     typename P::Ops ops;
     p.template prefetch<N>(tile, ops);
-    cp_async_wait<1>();
+    cp_async_wait<NB - 1>();
     __syncthreads();
+#if EMIE_STREAM_EXPERIMENT != 1 && EMIE_STREAM_EXPERIMENT != 4
     spass_first<N, P::kInverse>(cur, p, ops);
-    spasses<N, 16, P::kInverse>(cur, tws);
-    p.template store<N>(tile, cur, ops);
+    smid<N, 16, P::kInverse>(cur, tws);
+#endif
+    slast<N, P::kInverse>(cur, tws, p, ops);
     __syncthreads();  // cur is refilled by the next iteration's load
   }
   cp_async_wait<0>();
 }
 
+// global store of the streaming passes
+__device__ __forceinline__ void gst(cplx* p, cplx v) {
+#if EMIE_STREAM_EXPERIMENT != 3 && EMIE_STREAM_EXPERIMENT != 4
+  *p = v;
+#endif
+}
+
+// Loops over a tile run a compile-time count: a power-of-two embedding of
+// 2n-1 points has n in (N/4, N/2], so rows are walked as N/2-wide with a
+// predicate. Thread-constant parts of the mirror signs are hoisted per tile.
+template <int N>
+struct Half {
+  static constexpr int H = N / 2;                                   // row width walked
+  static constexpr int per = (Geo<N>::ntr * H) / kStreamThreads;    // elements per thread
+  __device__ static __forceinline__ void rc(int e, int& t, int& j) {  // element e of the thread
+    const int idx = threadIdx.x + e * kStreamThreads;
+    t = idx / H;
+    j = idx % H;
+  }
+};
+
 // x forward: tile = RT rows iy0.. of plane pr (nrhs*np planes); r2 on load
 struct FxStream {
-  static constexpr bool kInverse = false;
+  static constexpr bool kInverse = false, kTFast = true;
   const cplx* u;
   const cplx* r2;
   cplx* T;
   int nx, ny, nz, np, ex, tpp, nplanes, nin;
   struct Ops {
     cplx r2v[kStreamPre];
+    cplx* dst;  // T at (r, mx = 0, plane, iy0)
+    int rows;
   };
   __device__ int ntiles() const { return nplanes * tpp; }
   template <int N>
@@ -457,137 +549,148 @@ struct FxStream {
     const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
     const cplx* src = u + (static_cast<size_t>(pr) * ny + iy0) * nx;
     const int rows = min(RT, ny - iy0);
-    for (int t = 0; t < rows; ++t)
-      for (int j = threadIdx.x; j < nx; j += kStreamThreads) cp_async16(buf + Geo<N>::at(t, j), src + t * nx + j);
+#pragma unroll
+    for (int e = 0; e < Half<N>::per; ++e) {
+      int t, j;
+      Half<N>::rc(e, t, j);
+      if (t < rows && j < nx) cp_async16(buf + Geo<N>::at(t, j), src + t * nx + j);
+    }
   }
   template <int N>
   __device__ void prefetch(int tile, Ops& o) const {
-    if (!r2) return;
     constexpr int RT = Geo<N>::ntr, M = N / 16;
     const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
-    const int iz = (pr % np) % nz;
+    const int r = pr / np, plane = pr - r * np;
+    o.rows = min(RT, ny - iy0);
+    o.dst = T + ((static_cast<size_t>(r) * ex) * np + plane) * ny + iy0;
+    if (!r2) return;
+    const int iz = plane % nz;
     const int t = threadIdx.x / M, j = threadIdx.x % M;
     const int iy = min(iy0 + t, ny - 1);
     const cplx* row = r2 + (static_cast<size_t>(iz) * ny + iy) * nx;
 #pragma unroll
-    for (int r = 0; r < kStreamPre; ++r) {
-      const int jj = j + r * M;
-      o.r2v[r] = jj < nx ? ldg(row + jj) : cplx{0.0, 0.0};
+    for (int q = 0; q < kStreamPre; ++q) {
+      const int jj = j + q * M;
+      o.r2v[q] = jj < nx ? ldg(row + jj) : cplx{0.0, 0.0};
     }
   }
   __device__ cplx pre(const Ops& o, int, int r, int, cplx x) const {
     return (r2 && r < kStreamPre) ? o.r2v[r] * x : x;
   }
+  // T[r][mx][plane][iy]: lanes t (= iy) fastest, 128 B runs per mx
   template <int N>
-  __device__ void store(int tile, const cplx* buf, const Ops&) const {
-    constexpr int RT = Geo<N>::ntr;
-    const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
-    const int r = pr / np, plane = pr - r * np;
-    const int rows = min(RT, ny - iy0);
-    cplx* dst = T + ((static_cast<size_t>(r) * ex) * np + plane) * ny + iy0;
-    const size_t mstride = static_cast<size_t>(np) * ny;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < RT * N; idx += kStreamThreads) {
-      const int tt = idx % RT, mx = idx / RT;
-      if (tt < rows) dst[mx * mstride + tt] = buf[Geo<N>::at(tt, mx)];
-    }
+  __device__ void emit(const Ops& o, int t, int mx, int, int, cplx v) const {
+    if (t < o.rows) gst(o.dst + static_cast<size_t>(mx) * np * ny + t, v);
   }
 };
 
 // y forward: tile = PC planes p0.. at column mx of rhs r; mirror signs on store
 struct FyStream {
-  static constexpr bool kInverse = false;
+  static constexpr bool kInverse = false, kTFast = true;
   const cplx* T;
   cplx* S;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
-  struct Ops {};
+  struct Ops {
+    cplx* dst;  // S at (r, mx, my = 0, p0)
+    int p0;
+    bool mxflip;
+  };
   __device__ int ntiles() const { return nrhs * ex * gpc; }
-  __device__ void coords(int tile, int PC, int& r, int& mx, int& p0) const {
+  template <int N>
+  __device__ void coords(int tile, int& r, int& mx, int& p0) const {
     const int g = tile % gpc, rm = tile / gpc;
     mx = rm % ex;
     r = rm / ex;
-    p0 = g * PC;
+    p0 = g * Geo<N>::ntr;
   }
   template <int N>
   __device__ void load(int tile, cplx* buf) const {
-    constexpr int PC = Geo<N>::ntr;
     int r, mx, p0;
-    coords(tile, PC, r, mx, p0);
-    const int pc = min(PC, np - p0);
+    coords<N>(tile, r, mx, p0);
+    const int pc = min(Geo<N>::ntr, np - p0);
     const cplx* src = T + ((static_cast<size_t>(r) * ex + mx) * np + p0) * ny;
-    for (int t = 0; t < pc; ++t)
-      for (int j = threadIdx.x; j < ny; j += kStreamThreads) cp_async16(buf + Geo<N>::at(t, j), src + t * ny + j);
+#pragma unroll
+    for (int e = 0; e < Half<N>::per; ++e) {
+      int t, j;
+      Half<N>::rc(e, t, j);
+      if (t < pc && j < ny) cp_async16(buf + Geo<N>::at(t, j), src + t * ny + j);
+    }
   }
   template <int N>
-  __device__ void prefetch(int, Ops&) const {}
+  __device__ void prefetch(int tile, Ops& o) const {
+    int r, mx;
+    coords<N>(tile, r, mx, o.p0);
+    o.dst = S + (static_cast<size_t>(r) * ex + mx) * N * np + o.p0;
+    o.mxflip = 2 * mx > ex;
+  }
   __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
+  // S[r][mx][my][plane] with the mirror signs: lanes t (= plane) fastest
   template <int N>
-  __device__ void store(int tile, const cplx* buf, const Ops&) const {
-    constexpr int PC = Geo<N>::ntr;
-    int r, mx, p0;
-    coords(tile, PC, r, mx, p0);
-    const int pc = min(PC, np - p0);
-    cplx* dst = S + (static_cast<size_t>(r) * ex + mx) * N * np + p0;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < PC * N; idx += kStreamThreads) {
-      const int p = idx % PC, my = idx / PC;
-      if (p < pc) dst[my * np + p] = mirror_sign(p0 + p, nz, my, mx, N, ex) * buf[Geo<N>::at(p, my)];
-    }
+  __device__ void emit(const Ops& o, int t, int my, int, int, cplx v) const {
+    const int plane = o.p0 + t;
+    if (plane >= np) return;
+    const bool flip = (plane < nz && o.mxflip) || (plane >= nz && plane < 2 * nz && 2 * my > N);
+    gst(o.dst + static_cast<size_t>(my) * np + t, flip ? -v : v);
   }
 };
 
 // y inverse: tile = PC planes p0.. at column mx; mirror signs undone on load
 struct IyStream {
-  static constexpr bool kInverse = true;
+  static constexpr bool kInverse = true, kTFast = false;
   const cplx* S;
   cplx* T;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
   struct Ops {
-    int mx, p0;
+    cplx* dst;  // T at (r, mx, p0, iy = 0)
+    int p0;
+    bool fx, yp;  // sign flags of the thread's first-pass transform
   };
   __device__ int ntiles() const { return nrhs * ex * gpc; }
-  __device__ void coords(int tile, int PC, int& r, int& mx, int& p0) const {
+  template <int N>
+  __device__ void coords(int tile, int& r, int& mx, int& p0) const {
     const int g = tile % gpc, rm = tile / gpc;
     mx = rm % ex;
     r = rm / ex;
-    p0 = g * PC;
+    p0 = g * Geo<N>::ntr;
   }
   template <int N>
   __device__ void load(int tile, cplx* buf) const {
     constexpr int PC = Geo<N>::ntr;
     int r, mx, p0;
-    coords(tile, PC, r, mx, p0);
-    const int pc = min(PC, np - p0);
-    const cplx* src = S + (static_cast<size_t>(r) * ex + mx) * N * np + p0;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < PC * N; idx += kStreamThreads) {
-      const int p = idx % PC, j = idx / PC;
-      if (p < pc) cp_async16(buf + Geo<N>::at(p, j), src + j * np + p);
+    coords<N>(tile, r, mx, p0);
+    const int p = threadIdx.x % PC;  // same for every e (PC divides 128)
+    if (p0 + p >= np) return;
+    const cplx* src = S + (static_cast<size_t>(r) * ex + mx) * N * np + p0 + p;
+#pragma unroll
+    for (int e = 0; e < PC * N / kStreamThreads; ++e) {
+      const int j = (threadIdx.x + e * kStreamThreads) / PC;
+      cp_async16(buf + Geo<N>::at(p, j), src + j * np);
     }
   }
   template <int N>
   __device__ void prefetch(int tile, Ops& o) const {
-    int r;
-    coords(tile, Geo<N>::ntr, r, o.mx, o.p0);
+    int r, mx;
+    coords<N>(tile, r, mx, o.p0);
+    o.dst = T + ((static_cast<size_t>(r) * ex + mx) * np + o.p0) * ny;
+    const int plane = o.p0 + threadIdx.x / (N / 16);  // first-pass transform of the thread
+    o.fx = plane < nz && 2 * mx > ex;
+    o.yp = plane >= nz && plane < 2 * nz;
   }
-  __device__ cplx pre(const Ops& o, int t, int, int jj, cplx x) const {
-    return mirror_sign(o.p0 + t, nz, jj, o.mx, ey, ex) * x;
+  __device__ cplx pre(const Ops& o, int, int, int jj, cplx x) const {
+    return (o.fx || (o.yp && 2 * jj > ey)) ? -x : x;
   }
+  // T[r][mx][plane][iy], iy < ny: lanes j (= iy) fastest
   template <int N>
-  __device__ void store(int tile, const cplx* buf, const Ops& o) const {
-    constexpr int PC = Geo<N>::ntr;
-    int r = tile / gpc / ex;
-    const int pc = min(PC, np - o.p0);
-    cplx* dst = T + ((static_cast<size_t>(r) * ex + o.mx) * np + o.p0) * ny;
-    for (int p = 0; p < pc; ++p)
-      for (int iy = threadIdx.x; iy < ny; iy += kStreamThreads) dst[p * ny + iy] = buf[Geo<N>::at(p, iy)];
+  __device__ void emit(const Ops& o, int t, int iy, int, int, cplx v) const {
+    if (iy < ny && o.p0 + t < np) gst(o.dst + t * ny + iy, v);
   }
 };
 
 // x inverse: tile = RT rows iy0.. of plane pr; truncation, 1/(ex ey) and the
-// system epilogue s*u + r1*(.) (cie.cpp:67-72), its operands prefetched
+// system epilogue s*u + r1*(.) (cie.cpp:67-72), its operands prefetched for
+// the thread's kept outputs (slot b*R/2 + r, r < R/2: ix < N/2)
 struct IxStream {
-  static constexpr bool kInverse = true;
+  static constexpr bool kInverse = true, kTFast = false;
   const cplx* T;
   const cplx* u;
   cplx* out;
@@ -598,6 +701,7 @@ struct IxStream {
   struct Ops {
     cplx uv[kStreamPre], sv[kStreamPre];
     double rv[kStreamPre];
+    int pr, iy0;
   };
   __device__ int ntiles() const { return nplanes * tpp; }
   template <int N>
@@ -608,55 +712,51 @@ struct IxStream {
     const int rows = min(RT, ny - iy0);
     const cplx* src = T + ((static_cast<size_t>(r) * ex) * np + plane) * ny + iy0;
     const size_t mstride = static_cast<size_t>(np) * ny;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < RT * N; idx += kStreamThreads) {
-      const int tt = idx % RT, mx = idx / RT;
-      if (tt < rows) cp_async16(buf + Geo<N>::at(tt, mx), src + mx * mstride + tt);
+    const int tt = threadIdx.x % RT;  // same for every e (RT divides 128)
+    if (tt >= rows) return;
+#pragma unroll
+    for (int e = 0; e < RT * N / kStreamThreads; ++e) {
+      const int mx = (threadIdx.x + e * kStreamThreads) / RT;
+      cp_async16(buf + Geo<N>::at(tt, mx), src + mx * mstride + tt);
     }
   }
-  // output e of the thread: row tt = e / CH, column ix = (e % CH) * 128 + tid
-  template <int N>
-  static constexpr int chunks() { return N / 2 > kStreamThreads ? N / 2 / kStreamThreads : 1; }
   template <int N>
   __device__ void prefetch(int tile, Ops& o) const {
+    constexpr int RT = Geo<N>::ntr, R = last_radix<N>(), NS = N / R, B = kFftEPT / R;
+    o.pr = tile / tpp;
+    o.iy0 = (tile - o.pr * tpp) * RT;
     if (!s) return;
-    constexpr int RT = Geo<N>::ntr, CH = chunks<N>();
-    const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
-    const int iz = (pr % np) % nz;
+    const int iz = (o.pr % np) % nz;
 #pragma unroll
-    for (int e = 0; e < kStreamPre && e < RT * CH; ++e) {
-      const int tt = e / CH, ix = (e % CH) * kStreamThreads + threadIdx.x, iy = iy0 + tt;
-      if (iy < ny && ix < nx) {
-        const size_t cell = (static_cast<size_t>(iz) * ny + iy) * nx + ix;
-        o.uv[e] = ldg(u + (static_cast<size_t>(pr) * ny + iy) * nx + ix);
-        o.sv[e] = ldg(s + cell);
-        o.rv[e] = __ldg(r1 + cell);
+    for (int b = 0; b < B; ++b) {
+      int t, j;
+      last_coord<N, false>(b, t, j);
+#pragma unroll
+      for (int r = 0; r < R / 2; ++r) {
+        const int q = b * (R / 2) + r, ix = j + r * NS, iy = o.iy0 + t;
+        if (iy < ny && ix < nx) {
+          const size_t cell = (static_cast<size_t>(iz) * ny + iy) * nx + ix;
+          o.uv[q] = ldg(u + (static_cast<size_t>(o.pr) * ny + iy) * nx + ix);
+          o.sv[q] = ldg(s + cell);
+          o.rv[q] = __ldg(r1 + cell);
+        }
       }
     }
   }
   __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
+  // out[pr][iy][ix], ix < nx: lanes j (= ix) fastest
   template <int N>
-  __device__ void store(int tile, const cplx* buf, const Ops& o) const {
-    constexpr int RT = Geo<N>::ntr, CH = chunks<N>();
-    const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
-    const int iz = (pr % np) % nz;
-#pragma unroll
-    for (int e = 0; e < RT * CH; ++e) {
-      const int tt = e / CH, ix = (e % CH) * kStreamThreads + threadIdx.x, iy = iy0 + tt;
-      if (iy < ny && ix < nx) {
-        const size_t q = (static_cast<size_t>(pr) * ny + iy) * nx + ix;
-        cplx v = inv * buf[Geo<N>::at(tt, ix)];
-        if (s) {
-          if (e < kStreamPre) {
-            v = o.sv[e] * o.uv[e] + o.rv[e] * v;
-          } else {
-            const size_t cell = (static_cast<size_t>(iz) * ny + iy) * nx + ix;
-            v = ldg(s + cell) * ldg(u + q) + __ldg(r1 + cell) * v;
-          }
-        }
-        out[q] = v;
-      }
+  __device__ void emit(const Ops& o, int t, int ix, int b, int r, cplx v) const {
+    constexpr int R = last_radix<N>();
+    const int iy = o.iy0 + t;
+    if (r >= R / 2 || ix >= nx || iy >= ny) return;
+    const size_t q = (static_cast<size_t>(o.pr) * ny + iy) * nx + ix;
+    v = inv * v;
+    if (s) {
+      const int k = b * (R / 2) + r;
+      v = o.sv[k] * o.uv[k] + o.rv[k] * v;
     }
+    gst(out + q, v);
   }
 };
 
@@ -673,11 +773,11 @@ int per_tile(int n) { return std::max(1, kTileElems / std::max(1, n)); }
 
 // the streaming path takes power-of-two n in [16, 2048] whose nonzero input
 // run is at most half the transform (always true of a circulant embedding)
-bool stream_ok(bool p2, int n, int nin) { return p2 && n >= 16 && n <= kStreamElems && 2 * nin <= n; }
+bool stream_ok(bool p2, int n, int nin) { return p2 && n >= 32 && n <= kStreamElems && 2 * nin <= n; }
 
 template <int N, class P>
 void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
-  const size_t smem = (2 * static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx);
+  const size_t smem = (kStreamBufs * static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx);
   const void* fn = reinterpret_cast<const void*>(stream_fft_kernel<N, P>);
   set_smem(fn, smem);
   int dev = 0, sms = 0, per_sm = 0;
@@ -691,7 +791,6 @@ void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
 template <class P>
 void launch_stream(const P& p, int ntiles, const cplx* tw, int n, cudaStream_t st, const char* what) {
   switch (n) {
-    case 16: launch_stream_n<16>(p, ntiles, tw, st); break;
     case 32: launch_stream_n<32>(p, ntiles, tw, st); break;
     case 64: launch_stream_n<64>(p, ntiles, tw, st); break;
     case 128: launch_stream_n<128>(p, ntiles, tw, st); break;
