@@ -286,6 +286,13 @@ def run_ours(args):
     fp64 = ctypes.c_double(0.0)
     emie._check(L.emie_cu_probe_fp64(ctypes.byref(fp64), sp))
     achieved = bytes_ct / (ct_ms * 1e-3) / 1e9
+    ct_kernel = "contract_mma_kernel<%d>" % nz if nz in (8, 16, 32) else "contract_kernel"
+    traffic = None  # dram read + write per launch, from the committed ncu --set full capture
+    tpath = ROOT / "profiles" / "traffic.json"
+    if tpath.exists():
+        t = json.loads(tpath.read_text()).get(ct_kernel)
+        if t and t.get("config") == f"cfg{args.config} nrhs={NRHS}":
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     stage_names = ["fwd_x_fft", "fwd_y_fft", "contraction", "inv_y_fft", "inv_x_fft_epilogue"]
     stages = {nm: round(float(ms5[i] / max(1, cnt5[i])), 4) for i, nm in enumerate(stage_names)}
 
@@ -316,11 +323,14 @@ def run_ours(args):
                        "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
             "greens_build_s": greens_s,
             "stage_ms": stages,
-            "roofline": {"bound": "hbm", "kernel": "contract_kernel", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": ct_kernel, "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_source": hbm_kind, "traffic": None,
+                         "peak_source": hbm_kind, "traffic": traffic,
+                         "traffic_source": "profiles/traffic.json (ncu --set full, dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum, one launch)",
                          "bytes_per_launch": bytes_ct,
-                         "fp64": {"achieved_tflops": flops_ct / (ct_ms * 1e-3) / 1e12,
+                         "fp64": {"flops": "8 per complex multiply-add of the (3nz)^2 mode matrices, all ex*ey modes",
+                                  "achieved_tflops": flops_ct / (ct_ms * 1e-3) / 1e12,
                                   "peak_tflops": fp64.value, "peak_source": "emie_cu_probe_fp64 (DFMA loop, this GPU)",
                                   "frac": (flops_ct / (ct_ms * 1e-3) / 1e12) / fp64.value if fp64.value else None}},
             "cpu_baseline": cpu,
