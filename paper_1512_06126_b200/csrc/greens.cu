@@ -19,7 +19,9 @@
 // products kept as (mantissa, binary exponent, zero count), so an underflowed
 // theta zeroes exactly the chains that span it, as the running product does.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
+#include <complex>
 #include <vector>
 
 #include "operator.cuh"
@@ -32,12 +34,18 @@ constexpr double kMu0 = 1.2566370614359172e-06;  // include/emie/types.hpp:11
 constexpr double kPi = 3.141592653589793238462643383279502884;
 constexpr double kSqrtPi = 1.7724538509055160273;
 constexpr int kMaxLayers = 16;
-constexpr int kGreenThreads = 256;
-constexpr int kPairsPerThread = 3;
+#ifndef EMIE_GREEN_THREADS
+#define EMIE_GREEN_THREADS 256
+#endif
+#ifndef EMIE_GREEN_PPT
+#define EMIE_GREEN_PPT 3
+#endif
+constexpr int kGreenThreads = EMIE_GREEN_THREADS;  // threads per assemble CTA
+constexpr int kPairsPerThread = EMIE_GREEN_PPT;    // interval pairs per thread
 
 // ------------------------------------------------------ complex helpers ----
-__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
-  // Smith's algorithm (no overflow for the magnitudes met here)
+// Smith's algorithm: the exact-path fallback of cdiv (zero or non-finite divisor)
+__device__ __noinline__ cplx cdiv_smith(cplx a, cplx b) {
   if (fabs(b.re) >= fabs(b.im)) {
     const double r = b.im / b.re, d = b.re + b.im * r;
     return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
@@ -45,7 +53,7 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   const double r = b.re / b.im, d = b.re * r + b.im;
   return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
 }
-__device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
+
 __device__ __forceinline__ cplx csqrt_pos(cplx z) {
   // principal square root, then the Re > 0 branch (layered.cpp:87-89)
   const double m = hypot(z.re, z.im);
@@ -96,6 +104,30 @@ __device__ __forceinline__ int ilog2(double x) {
   if (ex != 0) return ex - 1023;
   return ilogb(x);  // subnormal: rare
 }
+
+// 1/d for d in [1, 8) to ~1 ulp: hardware reciprocal estimate + two Newton steps
+__device__ __forceinline__ double rcp_unit(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+// a / b without FP64 divisions (nvcc emits each as an out-of-line call): b is
+// scaled by the power of two of its larger component, so |b'|^2 is in [1, 2]
+// and neither overflows nor underflows; a / b = a conj(b') / |b'|^2 * 2^-e.
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  const double m = fmax(fabs(b.re), fabs(b.im));
+  if (!(m > 0.0) || !(m <= 1.0e300) || m < 1.0e-300) return cdiv_smith(a, b);
+  const int e = ilog2(m);
+  const double sc = pow2i(-e);
+  const double br = b.re * sc, bi = b.im * sc;
+  const double r = rcp_unit(br * br + bi * bi);
+  const cplx q = {(a.re * br + a.im * bi) * r, (a.im * br - a.re * bi) * r};
+  return scal2(q, -e);
+}
+__device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
 
 // ------------------------------------------------------ hankel helpers ----
 __device__ __forceinline__ double ediff(double a, double b) {  // hankel.cpp:22-26
@@ -286,6 +318,8 @@ struct GreenParams {
   // model (host-filled)
   double thick[kMaxLayers];
   cplx sig[kMaxLayers];  // floored conductivities
+  cplx sig_up[kMaxLayers];  // sig[m+1] / sig[m] (TM reflection chain, layered.cpp:113)
+  cplx sig_dn[kMaxLayers];  // sig[m-1] / sig[m]
 };
 
 // per-interval geometry (device arrays): a, b, h, d (top), dp (bottom), l
@@ -307,6 +341,8 @@ struct Chunk {
   cplx* one_p;
   cplx* one_q;
   cplx* diag_a;
+  cplx* rup;     // [lc][m]: eta[m] / eta[m+1]
+  cplx* rdn;     // [lc][m]: eta[m] / eta[m-1]
   // interval fields [lc][f][j]
   cplx* F;
   double* lam;   // [8][lc]: lambda, 1/lambda, w00 w20 w02 w11 w10 w01
@@ -319,7 +355,23 @@ enum {
   fEta2, fThu, fThc, kFields
 };
 
-__global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
+#ifdef EMIE_GREENS_PHASE_CLOCKS  // timing experiment: cycles per phase summed over CTAs
+__device__ unsigned long long g_phase_clk[8];
+#define PHASE_MARK(i)                                                        \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      const long long now = clock64();                                       \
+      atomicAdd(&g_phase_clk[i], static_cast<unsigned long long>(now - clk)); \
+      clk = now;                                                             \
+    }                                                                        \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
     cplx* __restrict__ blocks, int* err) {
   extern __shared__ cplx sm[];
@@ -342,6 +394,8 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
     C.one_p = s; s += LC * 2 * NL;
     C.one_q = s; s += LC * 2 * NL;
     C.diag_a = s; s += LC * 2 * NL;
+    C.rup = s; s += LC * NL;
+    C.rdn = s; s += LC * NL;
     C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
     C.lam = reinterpret_cast<double*>(s);  // [lc]: lambda, 1/lambda, 6 weights
     C.E = reinterpret_cast<int*>(C.lam + 8 * LC);
@@ -366,9 +420,13 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
     for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
 
   const int nw = P.nw;
+#ifdef EMIE_GREENS_PHASE_CLOCKS
+  long long clk = clock64();
+#endif
   for (int t0 = 0; t0 < nw; t0 += LC) {
     const int lc = min(LC, nw - t0);
     __syncthreads();  // previous chunk consumed
+    PHASE_MARK(0);
     // per-lambda scalars of the chunk
     for (int li = threadIdx.x; li < lc; li += blockDim.x) {
       const int t = t0 + li;
@@ -384,6 +442,12 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
       const cplx eta = csqrt_pos(eta2);
       C.eta[li * NL + m] = eta;
+      if (m < L) {  // neighbour ratios for the reflection chains, off their critical path
+        const cplx eta2n = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m + 1];
+        const cplx etan = csqrt_pos(eta2n);
+        C.rup[li * NL + m] = cdiv(eta, etan);
+        C.rdn[li * NL + m + 1] = cdiv(etan, eta);
+      }
       if (m == 0 || m == L) {
         C.e2l[li * NL + m] = {1.0, 0.0};
         C.em1[li * NL + m] = {0.0, 0.0};
@@ -394,40 +458,52 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       }
     }
     __syncthreads();
-    // phase 0b: reflection chains per (lambda, gamma, direction) (layered.cpp:107-122)
+    PHASE_MARK(1);
+    // phase 0b: reflection chains per (lambda, gamma, direction) (layered.cpp:107-122).
+    // Tasks are direction-major so a warp runs one kind of chain (no divergence);
+    // one complex reciprocal per step gives both p = (1+w)/(1-w) and 1+p = 2/(1-w).
     for (int x = threadIdx.x; x < lc * 4; x += blockDim.x) {
-      const int li = x >> 2, gm = (x >> 1) & 1, dir = x & 1;
-      const cplx* eta = C.eta + li * NL;
+      const int dir = x / (2 * lc), rem = x - dir * 2 * lc;
+      const int li = rem >> 1, gm = rem & 1;
       const cplx* e2l = C.e2l + li * NL;
       const cplx* em1 = C.em1 + li * NL;
       const int base = (li * 2 + gm) * NL;
       if (dir == 0) {
         cplx* p = C.p + base;
         cplx* op = C.one_p + base;
+        const cplx* rup = C.rup + li * NL;
+        cplx opm = {1.0, 0.0};
         p[0] = {0.0, 0.0};
-        op[0] = {1.0, 0.0};
+        op[0] = opm;
         for (int m = 0; m < L; ++m) {
-          const cplx t = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - op[m]), em1[m] + e2l[m] * op[m]);
-          const cplx alpha = gm ? cdiv(P.sig[m + 1], P.sig[m]) : cplx{1.0, 0.0};
-          const cplx w = alpha * cdiv(eta[m], eta[m + 1]) * t;
-          p[m + 1] = cdiv(cplx{1.0, 0.0} + w, cplx{1.0, 0.0} - w);
-          op[m + 1] = cdiv(cplx{2.0, 0.0}, cplx{1.0, 0.0} - w);
+          const cplx t = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - opm), em1[m] + e2l[m] * opm);
+          const cplx alpha = gm ? P.sig_up[m] : cplx{1.0, 0.0};
+          const cplx w = alpha * rup[m] * t;
+          const cplx r = crecip(cplx{1.0, 0.0} - w);
+          p[m + 1] = (cplx{1.0, 0.0} + w) * r;
+          opm = 2.0 * r;
+          op[m + 1] = opm;
         }
       } else {
         cplx* q = C.q + base;
         cplx* oq = C.one_q + base;
+        const cplx* rdn = C.rdn + li * NL;
+        cplx oqm = {1.0, 0.0};
         q[L] = {0.0, 0.0};
-        oq[L] = {1.0, 0.0};
+        oq[L] = oqm;
         for (int m = L; m > 0; --m) {
-          const cplx u = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - oq[m]), em1[m] + e2l[m] * oq[m]);
-          const cplx beta = gm ? cdiv(P.sig[m - 1], P.sig[m]) : cplx{1.0, 0.0};
-          const cplx w = beta * cdiv(eta[m], eta[m - 1]) * u;
-          q[m - 1] = cdiv(cplx{1.0, 0.0} + w, cplx{1.0, 0.0} - w);
-          oq[m - 1] = cdiv(cplx{2.0, 0.0}, cplx{1.0, 0.0} - w);
+          const cplx u = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - oqm), em1[m] + e2l[m] * oqm);
+          const cplx beta = gm ? P.sig_dn[m] : cplx{1.0, 0.0};
+          const cplx w = beta * rdn[m] * u;
+          const cplx r = crecip(cplx{1.0, 0.0} - w);
+          q[m - 1] = (cplx{1.0, 0.0} + w) * r;
+          oqm = 2.0 * r;
+          oq[m - 1] = oqm;
         }
       }
     }
     __syncthreads();
+    PHASE_MARK(2);
     // phase 0c: diag_a (layered.cpp:124-126)
     for (int x = threadIdx.x; x < lc * 2 * NL; x += blockDim.x) {
       const int li = x / (2 * NL), r = x - li * 2 * NL;
@@ -437,6 +513,7 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       C.diag_a[li * 2 * NL + r] = crecip(eta * (em1 + e2l * (cplx{1.0, 0.0} - pq)));
     }
     __syncthreads();
+    PHASE_MARK(3);
     // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317)
     for (int x = threadIdx.x; x < lc * nz; x += blockDim.x) {
       const int li = x / nz, j = x - li * nz;
@@ -504,6 +581,7 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       }
     }
     __syncthreads();
+    PHASE_MARK(4);
     // phase 1b: prefix products of theta per (lambda, gamma) as
     // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l. One warp
     // per (lambda, gamma): a shuffle scan over 32-interval segments, the
@@ -579,6 +657,7 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       }
     }
     __syncthreads();
+    PHASE_MARK(5);
     // phase 2: pairs x lambdas (greens.cpp:167-191)
     for (int li = 0; li < lc; ++li) {
       const double lam = C.lam[li], ilam = C.lam[LC + li];
@@ -642,6 +721,8 @@ __global__ void __launch_bounds__(kGreenThreads) assemble_kernel(
       }
     }
   }
+  __syncthreads();
+  PHASE_MARK(6);
   // scale and store (greens.cpp:193-219)
   const double c3 = R * R * R / (4.0 * kPi), c2 = R * R / (4.0 * kPi), c1 = R / (4.0 * kPi);
   const int ntri = P.npairs, nfull = nz * nz;
@@ -821,6 +902,13 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
     if (s.re < 1e-9) s.re = 1e-9;  // sigma_floored (layered.cpp:47-51)
     P.sig[m] = s;
   }
+  for (int m = 0; m <= L; ++m) {
+    const std::complex<double> sm(P.sig[m].re, P.sig[m].im);
+    const std::complex<double> up = m < L ? std::complex<double>(P.sig[m + 1].re, P.sig[m + 1].im) / sm : 1.0;
+    const std::complex<double> dn = m > 0 ? std::complex<double>(P.sig[m - 1].re, P.sig[m - 1].im) / sm : 1.0;
+    P.sig_up[m] = {up.real(), up.imag()};
+    P.sig_dn[m] = {dn.real(), dn.imag()};
+  }
   std::vector<Interval> ivh(nz);
   for (int i = 0; i < nz; ++i) {
     if (!(breaks[i] < breaks[i + 1])) fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition: breaks must increase");
@@ -848,9 +936,11 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   // lambdas per chunk: as many as ~200 KB of SMEM holds (the serial per-chunk
   // phases then run on more threads and there are fewer chunks), at most 32
   {
-    const size_t per_lambda = (13 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
+    const size_t per_lambda = (15 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
                               8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
-    P.LC = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (200u << 10) / per_lambda)));
+    int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (200u << 10) / per_lambda)));
+    if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
+    P.LC = lcm;
   }
 
   keep_pool_warm();
@@ -866,15 +956,34 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   cplx* blocks = nullptr;
   EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(noff) * op.nent * sizeof(cplx) + 16));
   const int NL = L + 1;
-  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 10 * NL + kFields * nz)) * sizeof(cplx) +
+  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 12 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
   const int groups = ceil_div(P.npairs, kGreenThreads * kPairsPerThread);
   dim3 grid(noff, groups);
   profile_mark(5, true, st);
+#ifdef EMIE_GREENS_PHASE_CLOCKS
+  {
+    unsigned long long z[8] = {};
+    EMIE_CUDA(cudaMemcpyToSymbolAsync(g_phase_clk, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+  }
+#endif
   assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err);
   check_launch("assemble_kernel");
+#ifdef EMIE_GREENS_PHASE_CLOCKS
+  {
+    unsigned long long h[8];
+    EMIE_CUDA(cudaMemcpyFromSymbolAsync(h, g_phase_clk, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    const char* nm[7] = {"chunk-start", "0a", "0b", "0c", "1", "1b", "2"};
+    unsigned long long tot = 0;
+    for (int i = 0; i < 7; ++i) tot += h[i];
+    for (int i = 0; i < 7; ++i)
+      std::fprintf(stderr, "assemble phase %-12s %6.2f%%  %.3e cycles/CTA\n", nm[i], 100.0 * h[i] / tot,
+                   static_cast<double>(h[i]) / (static_cast<double>(grid.x) * grid.y));
+  }
+#endif
   profile_mark(5, false, st);
   int e = 0;
   EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
