@@ -37,11 +37,7 @@ constexpr int kMaxLayers = 16;
 #ifndef EMIE_GREEN_THREADS
 #define EMIE_GREEN_THREADS 256
 #endif
-#ifndef EMIE_GREEN_PPT
-#define EMIE_GREEN_PPT 3
-#endif
 constexpr int kGreenThreads = EMIE_GREEN_THREADS;  // threads per assemble CTA
-constexpr int kPairsPerThread = EMIE_GREEN_PPT;    // interval pairs per thread
 
 // ------------------------------------------------------ complex helpers ----
 // Smith's algorithm: the exact-path fallback of cdiv (zero or non-finite divisor)
@@ -355,6 +351,92 @@ enum {
   fEta2, fThu, fThc, kFields
 };
 
+// Pair order inside a group: diagonals (k, k) for s < nz, then neighbours
+// (k, k+1), then kp >= k + 2 row by row -- so a warp mostly holds one kind of
+// pair and the kind branches of the pair evaluation stay warp-uniform.
+__device__ __forceinline__ void pair_of(int s, int nz, int& k, int& kp) {
+  if (s < nz) {
+    k = kp = s;
+    return;
+  }
+  s -= nz;
+  if (s < nz - 1) {
+    k = s;
+    kp = s + 1;
+    return;
+  }
+  s -= nz - 1;
+  k = 0;
+  while (s >= nz - 2 - k) {
+    s -= nz - 2 - k;
+    ++k;
+  }
+  kp = k + 2 + s;
+}
+
+struct PairC {
+  int k, kp, kn;  // kn = min(k + 1, nz - 1)
+  int kind;       // 0 diagonal, 1 neighbour, 2 general
+  cplx isk;       // 1 / sigma of interval k
+};
+
+// one lambda of one interval pair into its nine accumulators (greens.cpp:167-191,
+// v_functions layered.cpp:397-408); wl = lambda, 1/lambda, w00 w20 w02 w11 w10 w01
+__device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const int* __restrict__ El, int nz,
+                                            const PairC& c, const double* wl, double wmu, cplx* a) {
+  const int k = c.k, kp = c.kp;
+  cplx W00u, W00c, W01c, W10c, W11c, W20c;
+  if (c.kind == 0) {
+    W00u = Fl[fW00u * nz + k];
+    W00c = Fl[fW00c * nz + k];
+    W10c = Fl[fW10c * nz + k];
+    W01c = W10c;
+    W11c = Fl[fW11c * nz + k];
+    W20c = Fl[fW20c * nz + k];
+  } else {
+    cplx Cu = {1.0, 0.0}, Cc = {1.0, 0.0};
+    if (c.kind == 2) {  // chain prod_{l=k+1}^{kp-1} theta_l from the prefix products
+      const int kn = c.kn;
+      Cu = (El[1 * nz + kp] != El[1 * nz + kn])
+               ? cplx{0.0, 0.0}
+               : scal2(Fl[fPu * nz + kp] * Fl[fPiu * nz + kn], El[0 * nz + kp] - El[0 * nz + kn]);
+      Cc = (El[3 * nz + kp] != El[3 * nz + kn])
+               ? cplx{0.0, 0.0}
+               : scal2(Fl[fPc * nz + kp] * Fl[fPic * nz + kn], El[2 * nz + kp] - El[2 * nz + kn]);
+    }
+    W00u = (Fl[fH0u * nz + k] * Cu) * Fl[fJ0u * nz + kp];
+    const cplx a0 = Fl[fH0c * nz + k] * Cc, a1 = Fl[fH1c * nz + k] * Cc;
+    const cplx j0 = Fl[fJ0c * nz + kp], j1 = Fl[fJ1c * nz + kp];
+    W00c = a0 * j0;
+    W01c = a0 * j1;
+    W10c = a1 * j0;
+    W11c = a1 * j1;
+    W20c = Fl[fEta2 * nz + k] * W00c;
+  }
+  const double lam = wl[0], ilam = wl[1];
+  const cplx V1 = {-wmu * W00u.im, wmu * W00u.re};
+  const cplx V2 = {-wmu * W00c.im, wmu * W00c.re};
+  const cplx V3 = -(W11c * c.isk);
+  const cplx V4 = W10c * c.isk;
+  const cplx V5 = W20c * c.isk;
+  const cplx f4 = lam * V4;
+  a[5] = a[5] + wl[6] * f4;
+  a[6] = a[6] + wl[7] * f4;
+  const cplx f2 = (V1 + V3) * ilam;
+  a[0] = a[0] + wl[2] * (lam * V1);
+  a[1] = a[1] + wl[3] * f2;
+  a[2] = a[2] + wl[4] * f2;
+  a[3] = a[3] + wl[5] * f2;
+  a[4] = a[4] + wl[2] * (lam * (V2 + V5));
+  if (c.kind != 0) {
+    // lower entry (kp, k): W10c(kp,k) = (sig_kp / sig_k) W01c(k,kp) (reciprocity,
+    // layered.cpp:363-376) and V4 = W10c / sig_kp, i.e. W01c / sig_k
+    const cplx f4l = lam * (W01c * c.isk);
+    a[7] = a[7] + wl[6] * f4l;
+    a[8] = a[8] + wl[7] * f4l;
+  }
+}
+
 #ifdef EMIE_GREENS_PHASE_CLOCKS  // timing experiment: cycles per phase summed over CTAs
 __device__ unsigned long long g_phase_clk[8];
 #define PHASE_MARK(i)                                                        \
@@ -403,20 +485,36 @@ __global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
   auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 4 + f) * nz + j]; };
 
-  // this thread's pairs (k <= kp), triangle order
-  int pk[kPairsPerThread], pkp[kPairsPerThread];
-  bool pv[kPairsPerThread];
-  for (int i = 0; i < kPairsPerThread; ++i) {
-    const int s = blockIdx.y * kGreenThreads * kPairsPerThread + i * kGreenThreads + threadIdx.x;
-    pv[i] = s < P.npairs;
-    int k = 0, rem = pv[i] ? s : 0;
-    while (rem >= nz - k) { rem -= nz - k; ++k; }
-    pk[i] = k;
-    pkp[i] = k + rem;
+  // Pair assignment (balanced): group pairs [g0, g0 + cnt), cnt <= 3T. Slots
+  // 0, 1: pair g0 + i T + tid over the full lambda range. The ntail = cnt - 2T
+  // remaining pairs are split over lambda: thread tid < Teff = (T / ntail) ntail
+  // keeps tail pair tid % ntail for every Teff-th (pair, lambda) item of a
+  // chunk; the T / ntail partial sums per tail pair are added in a fixed order
+  // at the end, so every thread evaluates ~2.06 pairs per lambda, not 3.
+  constexpr int T = kGreenThreads;
+  const int g0 = blockIdx.y * 3 * T;
+  const int cnt = min(3 * T, P.npairs - g0);
+  const int ntail = max(0, cnt - 2 * T);
+  const int teff = ntail > 0 ? (T / ntail) * ntail : 0;
+  PairC pc[3];
+  bool pv[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int sl = i < 2 ? i * T + threadIdx.x : 2 * T + (ntail > 0 ? threadIdx.x % ntail : 0);
+    pv[i] = i < 2 ? sl < cnt : static_cast<int>(threadIdx.x) < teff;
+    int k = 0, kp = 0;
+    if (pv[i]) pair_of(g0 + sl, nz, k, kp);
+    pc[i].k = k;
+    pc[i].kp = kp;
+    pc[i].kn = min(k + 1, nz - 1);
+    pc[i].kind = kp == k ? 0 : kp == k + 1 ? 1 : 2;
+    pc[i].isk = iv[k].inv_sig;
   }
   // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k)
-  cplx acc[kPairsPerThread][9];
-  for (int i = 0; i < kPairsPerThread; ++i)
+  cplx acc[3][9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
     for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
 
   const int nw = P.nw;
@@ -658,79 +756,54 @@ __global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
     }
     __syncthreads();
     PHASE_MARK(5);
-    // phase 2: pairs x lambdas (greens.cpp:167-191)
+    // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
     for (int li = 0; li < lc; ++li) {
-      const double lam = C.lam[li], ilam = C.lam[LC + li];
-      const double w00 = C.lam[2 * LC + li], w20 = C.lam[3 * LC + li], w02 = C.lam[4 * LC + li];
-      const double w11 = C.lam[5 * LC + li], w10 = C.lam[6 * LC + li], w01 = C.lam[7 * LC + li];
+      double wl[8];
 #pragma unroll
-      for (int i = 0; i < kPairsPerThread; ++i) {
-        if (!pv[i]) continue;
-        const int k = pk[i], kp = pkp[i];
-        const cplx isk = iv[k].inv_sig;
-        cplx W00u, W00c, W10c, W11c, W20c, W01c;
-        if (k == kp) {
-          W00u = F(li, fW00u, k);
-          W00c = F(li, fW00c, k);
-          W10c = F(li, fW10c, k);
-          W01c = W10c;
-          W11c = F(li, fW11c, k);
-          W20c = F(li, fW20c, k);
-        } else {
-          cplx Cu = {1.0, 0.0}, Cc = {1.0, 0.0};
-          if (kp > k + 1) {
-            Cu = (Ei(li, 1, kp) != Ei(li, 1, k + 1))
-                     ? cplx{0.0, 0.0}
-                     : scal2(F(li, fPu, kp) * F(li, fPiu, k + 1), Ei(li, 0, kp) - Ei(li, 0, k + 1));
-            Cc = (Ei(li, 3, kp) != Ei(li, 3, k + 1))
-                     ? cplx{0.0, 0.0}
-                     : scal2(F(li, fPc, kp) * F(li, fPic, k + 1), Ei(li, 2, kp) - Ei(li, 2, k + 1));
-          }
-          W00u = (F(li, fH0u, k) * Cu) * F(li, fJ0u, kp);
-          const cplx a0 = F(li, fH0c, k) * Cc, a1 = F(li, fH1c, k) * Cc;
-          W00c = a0 * F(li, fJ0c, kp);
-          W01c = a0 * F(li, fJ1c, kp);
-          W10c = a1 * F(li, fJ0c, kp);
-          W11c = a1 * F(li, fJ1c, kp);
-          W20c = F(li, fEta2, k) * W00c;
-        }
-        // v_functions (layered.cpp:397-408) at (k, kp)
-        const cplx V1 = {-wmu * W00u.im, wmu * W00u.re};
-        const cplx V2 = {-wmu * W00c.im, wmu * W00c.re};
-        const cplx V3 = -(W11c * isk);
-        const cplx V4 = W10c * isk;
-        const cplx V5 = W20c * isk;
-        const cplx f4 = lam * V4;
-        acc[i][5] = acc[i][5] + w10 * f4;
-        acc[i][6] = acc[i][6] + w01 * f4;
-        const cplx f2 = (V1 + V3) * ilam;
-        acc[i][0] = acc[i][0] + w00 * (lam * V1);
-        acc[i][1] = acc[i][1] + w20 * f2;
-        acc[i][2] = acc[i][2] + w02 * f2;
-        acc[i][3] = acc[i][3] + w11 * f2;
-        acc[i][4] = acc[i][4] + w00 * (lam * (V2 + V5));
-        if (k != kp) {
-          // lower entry (kp, k): W10c(kp,k) = (sig_kp / sig_k) W01c(k,kp)
-          // (reciprocity, layered.cpp:363-376), V4 = W10c / sig_kp
-          const cplx ratio = P.sig[iv[kp].layer] * iv[k].inv_sig;
-          const cplx V4l = (ratio * W01c) * iv[kp].inv_sig;
-          const cplx f4l = lam * V4l;
-          acc[i][7] = acc[i][7] + w10 * f4l;
-          acc[i][8] = acc[i][8] + w01 * f4l;
-        }
+      for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
+      const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
+      const int* El = C.E + li * 4 * nz;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, wmu, acc[i]);
+    }
+    if (pv[2]) {
+      for (int u = threadIdx.x; u < ntail * lc; u += teff) {
+        const int li = u / ntail;
+        double wl[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
+        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[2], wl, wmu, acc[2]);
       }
     }
   }
   __syncthreads();
   PHASE_MARK(6);
+  // tail pairs: partial sums of the lambda-split threads, added in order
+  if (ntail > 0) {
+    cplx* part = sm;  // the chunk buffers are free now: [9][T]
+#pragma unroll
+    for (int f = 0; f < 9; ++f) part[f * T + threadIdx.x] = acc[2][f];
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < ntail) {
+#pragma unroll
+      for (int f = 0; f < 9; ++f) {
+        cplx sum = part[f * T + threadIdx.x];
+        for (int r = threadIdx.x + ntail; r < teff; r += ntail) sum = sum + part[f * T + r];
+        acc[2][f] = sum;
+      }
+    }
+  }
   // scale and store (greens.cpp:193-219)
   const double c3 = R * R * R / (4.0 * kPi), c2 = R * R / (4.0 * kPi), c1 = R / (4.0 * kPi);
   const int ntri = P.npairs, nfull = nz * nz;
   cplx* blk = blocks + static_cast<size_t>(off) * P.nent;
   bool bad = false;
-  for (int i = 0; i < kPairsPerThread; ++i) {
-    if (!pv[i]) continue;
-    const int k = pk[i], kp = pkp[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const bool own = i < 2 ? pv[i] : static_cast<int>(threadIdx.x) < ntail;
+    if (!own) continue;
+    const int k = pc[i].k, kp = pc[i].kp;
     const int s = k * nz - k * (k - 1) / 2 + (kp - k);
     cplx v[8];
     v[0] = c3 * acc[i][0] + c1 * acc[i][1];
@@ -960,7 +1033,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
-  const int groups = ceil_div(P.npairs, kGreenThreads * kPairsPerThread);
+  const int groups = ceil_div(P.npairs, 3 * kGreenThreads);
   dim3 grid(noff, groups);
   profile_mark(5, true, st);
 #ifdef EMIE_GREENS_PHASE_CLOCKS
