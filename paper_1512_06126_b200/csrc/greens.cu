@@ -66,9 +66,9 @@ __device__ __forceinline__ cplx cexpm1(cplx x) {
   const double em = expm1(x.re);
   double sh, ch;
   sincos(0.5 * x.im, &sh, &ch);
-  double s, c;
-  sincos(x.im, &s, &c);
-  return {em * c - 2.0 * sh * sh, (em + 1.0) * s};
+  // one sincos: cos x = 1 - 2 sin^2(x/2), sin x = 2 sin(x/2) cos(x/2)
+  const double s = 2.0 * sh * ch, cm1 = -2.0 * sh * sh;
+  return {em * (1.0 + cm1) + cm1, (em + 1.0) * s};
 }
 __device__ __forceinline__ cplx cexp(cplx x) {
   const double e = exp(x.re);
