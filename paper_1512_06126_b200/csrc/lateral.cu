@@ -11,7 +11,10 @@
 // Reference: src/toeplitz.cpp:92-161 (spectra), 163-283 (apply), cie.cpp:56-73.
 #include <algorithm>
 
+#include <cudaTypedefs.h>
+
 #include "operator.cuh"
+#include "tma.cuh"
 
 namespace emie_cu {
 
@@ -325,9 +328,6 @@ __global__ void __launch_bounds__(256, 2) apply_ix_kernel(const cplx* __restrict
 // timing experiments only: 1 no FFT passes, 2 no loads, 3 no loads or stores, 4 loads only
 #define EMIE_STREAM_EXPERIMENT 0
 #endif
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 #if EMIE_STREAM_EXPERIMENT != 2 && EMIE_STREAM_EXPERIMENT != 3
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -509,6 +509,71 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamBufs == 2 ? 3 : 2)
   cp_async_wait<0>();
 }
 
+// TMA-staged variant (N = 256, the benchmark grids): a tile arrives by one
+// bulk copy (contiguous rows: fx, fy) or one tensor-map box with 128-byte
+// swizzle (strided rows: iy, ix) into a dense staging buffer; the first radix
+// pass reads it (p.staged) and writes the padded work buffer, after which the
+// staging buffer takes the next tile. Bulk copies keep far more bytes in
+// flight per SM than per-thread cp.async (no L1 miss-queue limit).
+#ifndef EMIE_TMA_MINB_SMALL
+#define EMIE_TMA_MINB_SMALL 3  // CTAs per SM the register budget targets for 16 KB stages
+#endif
+template <int N, class P, int NST>
+__global__ void __launch_bounds__(kStreamThreads, P::kStageBytes <= 16384 ? (NST == 1 ? EMIE_TMA_MINB_SMALL : 3)
+                                                                           : (NST == 1 ? 3 : 2))
+    stream_tma_kernel(const __grid_constant__ P p, const cplx* __restrict__ tw) {
+  using G = Geo<N>;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  cplx* stage[NST];
+#pragma unroll
+  for (int b = 0; b < NST; ++b) stage[b] = reinterpret_cast<cplx*>(smraw + b * P::kStageBytes);
+  cplx* work = reinterpret_cast<cplx*>(smraw + NST * P::kStageBytes);
+  cplx* tws = work + G::tile;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + N);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NST; ++b) mbar_init(bar + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  load_twiddles(tws, tw, N);
+  __syncthreads();
+  const int ntiles = p.ntiles();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NST; ++b)
+      if (tile + b * static_cast<int>(gridDim.x) < ntiles)
+        p.template issue<N>(tile + b * gridDim.x, stage[b], bar + b);
+  }
+#pragma unroll 1
+  for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
+    const int st = i % NST;
+    typename P::Ops ops;
+    p.template prefetch<N>(tile, ops);
+    mbar_wait(bar + st, static_cast<uint32_t>((i / NST) & 1));
+    {  // first radix-16 pass: staging -> work (NS = 1, no twiddles)
+      constexpr int M = N / 16;
+      constexpr double s = P::kInverse ? 1.0 : -1.0;
+      const int t = threadIdx.x / M, j = threadIdx.x % M;
+      cplx v[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int jj = j + r * M;
+        v[r] = jj < p.nin ? p.pre(ops, t, r, jj, p.staged(stage[st], t, jj)) : cplx{0.0, 0.0};
+      }
+      butterfly<16>(v, s);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) work[G::at(t, 16 * j + r)] = v[r];
+      __syncthreads();  // staging[st] consumed, work filled
+    }
+    const int next = tile + NST * gridDim.x;
+    if (threadIdx.x == 0 && next < ntiles) p.template issue<N>(next, stage[st], bar + st);
+    smid<N, 16, P::kInverse>(work, tws);
+    slast<N, P::kInverse>(work, tws, p, ops);
+    __syncthreads();  // work is rewritten by the next tile's first pass
+  }
+}
+
 // global store of the streaming passes
 __device__ __forceinline__ void gst(cplx* p, cplx v) {
 #if EMIE_STREAM_EXPERIMENT != 3 && EMIE_STREAM_EXPERIMENT != 4
@@ -533,6 +598,7 @@ struct Half {
 // x forward: tile = RT rows iy0.. of plane pr (nrhs*np planes); r2 on load
 struct FxStream {
   static constexpr bool kInverse = false, kTFast = true;
+  static constexpr int kStageBytes = 8 * 128 * 16;  // N = 256: 8 rows of <= 128 points
   const cplx* u;
   const cplx* r2;
   cplx* T;
@@ -577,6 +643,16 @@ struct FxStream {
   __device__ cplx pre(const Ops& o, int, int r, int, cplx x) const {
     return (r2 && r < kStreamPre) ? o.r2v[r] * x : x;
   }
+  // TMA staging: the tile's rows are one contiguous run of u
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    constexpr int RT = Geo<N>::ntr;
+    const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
+    const uint32_t bytes = static_cast<uint32_t>(min(RT, ny - iy0) * nx) * sizeof(cplx);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(stg, u + (static_cast<size_t>(pr) * ny + iy0) * nx, bytes, bar);
+  }
+  __device__ cplx staged(const cplx* stg, int t, int jj) const { return stg[t * nx + jj]; }
   // T[r][mx][plane][iy]: lanes t (= iy) fastest, 128 B runs per mx
   template <int N>
   __device__ void emit(const Ops& o, int t, int mx, int, int, cplx v) const {
@@ -587,6 +663,7 @@ struct FxStream {
 // y forward: tile = PC planes p0.. at column mx of rhs r; mirror signs on store
 struct FyStream {
   static constexpr bool kInverse = false, kTFast = true;
+  static constexpr int kStageBytes = 8 * 128 * 16;  // N = 256: 8 planes of <= 128 points
   const cplx* T;
   cplx* S;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
@@ -624,6 +701,16 @@ struct FyStream {
     o.mxflip = 2 * mx > ex;
   }
   __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
+  // TMA staging: the tile's planes are one contiguous run of T
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    int r, mx, p0;
+    coords<N>(tile, r, mx, p0);
+    const uint32_t bytes = static_cast<uint32_t>(min(Geo<N>::ntr, np - p0) * ny) * sizeof(cplx);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(stg, T + ((static_cast<size_t>(r) * ex + mx) * np + p0) * ny, bytes, bar);
+  }
+  __device__ cplx staged(const cplx* stg, int t, int jj) const { return stg[t * ny + jj]; }
   // S[r][mx][my][plane] with the mirror signs: lanes t (= plane) fastest
   template <int N>
   __device__ void emit(const Ops& o, int t, int my, int, int, cplx v) const {
@@ -637,6 +724,8 @@ struct FyStream {
 // y inverse: tile = PC planes p0.. at column mx; mirror signs undone on load
 struct IyStream {
   static constexpr bool kInverse = true, kTFast = false;
+  static constexpr int kStageBytes = 256 * 128;  // N = 256: [my][8 planes], 128-byte swizzle
+  CUtensorMap tm;  // S as {2 np doubles, ey, nrhs ex}, box {16, 256, 1}
   const cplx* S;
   cplx* T;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
@@ -679,6 +768,18 @@ struct IyStream {
   __device__ cplx pre(const Ops& o, int, int, int jj, cplx x) const {
     return (o.fx || (o.yp && 2 * jj > ey)) ? -x : x;
   }
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    int r, mx, p0;
+    coords<N>(tile, r, mx, p0);
+    mbar_expect_tx(bar, kStageBytes);
+    tma_load_3d(stg, &tm, 2 * p0, 0, r * ex + mx, bar);
+  }
+  // element jj (my) of transform t (plane): 16-byte chunk t of row jj, swizzled
+  __device__ cplx staged(const cplx* stg, int t, int jj) const {
+    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + jj * 128 +
+                                          ((t ^ (jj & 7)) << 4));
+  }
   // T[r][mx][plane][iy], iy < ny: lanes j (= iy) fastest
   template <int N>
   __device__ void emit(const Ops& o, int t, int iy, int, int, cplx v) const {
@@ -691,6 +792,8 @@ struct IyStream {
 // the thread's kept outputs (slot b*R/2 + r, r < R/2: ix < N/2)
 struct IxStream {
   static constexpr bool kInverse = true, kTFast = false;
+  static constexpr int kStageBytes = 256 * 128;  // N = 256: [mx][8 rows], 128-byte swizzle
+  CUtensorMap tm;  // T as {2 ny doubles, np, ex, nrhs}, box {16, 1, 256, 1}
   const cplx* T;
   const cplx* u;
   cplx* out;
@@ -744,6 +847,18 @@ struct IxStream {
     }
   }
   __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    constexpr int RT = Geo<N>::ntr;
+    const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
+    const int r = pr / np, plane = pr - r * np;
+    mbar_expect_tx(bar, kStageBytes);
+    tma_load_4d(stg, &tm, 2 * iy0, plane, 0, r, bar);
+  }
+  __device__ cplx staged(const cplx* stg, int t, int jj) const {
+    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + jj * 128 +
+                                          ((t ^ (jj & 7)) << 4));
+  }
   // out[pr][iy][ix], ix < nx: lanes j (= ix) fastest
   template <int N>
   __device__ void emit(const Ops& o, int t, int ix, int b, int r, cplx v) const {
@@ -788,6 +903,28 @@ void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
   stream_fft_kernel<N, P><<<grid, kStreamThreads, smem, st>>>(p, tw);
 }
 
+#ifndef EMIE_TMA_NST_INV
+#define EMIE_TMA_NST_INV 1  // staging buffers of the inverse passes (1: three CTAs per SM)
+#endif
+#ifndef EMIE_TMA_NST_FWD
+#define EMIE_TMA_NST_FWD 1
+#endif
+template <class P, int NST>
+void launch_tma(const P& p, int ntiles, const cplx* tw, cudaStream_t st, const char* what) {
+  constexpr int N = 256;
+  const size_t smem = NST * static_cast<size_t>(P::kStageBytes) +
+                      (static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx) + NST * sizeof(uint64_t);
+  const void* fn = reinterpret_cast<const void*>(stream_tma_kernel<N, P, NST>);
+  set_smem(fn, smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  EMIE_CUDA(cudaGetDevice(&dev));
+  EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_tma_kernel<N, P, NST>, kStreamThreads, smem));
+  const int grid = std::max(1, std::min(ntiles, sms * std::max(1, per_sm)));
+  stream_tma_kernel<N, P, NST><<<grid, kStreamThreads, smem, st>>>(p, tw);
+  check_launch(what);
+}
+
 template <class P>
 void launch_stream(const P& p, int ntiles, const cplx* tw, int n, cudaStream_t st, const char* what) {
   switch (n) {
@@ -806,6 +943,29 @@ void launch_stream(const P& p, int ntiles, const cplx* tw, int n, cudaStream_t s
 }  // namespace
 
 // ------------------------------------------------------------------ host --
+void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
+                           const uint64_t* strides_bytes, const uint32_t* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    EMIE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(EMIE_CU_RUNTIME_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  cuuint64_t d[5], sb[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) sb[i] = strides_bytes[i];
+  }
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), d, sb, b, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(EMIE_CU_RUNTIME_ERROR, "cuTensorMapEncodeTiled failed");
+}
+
 void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) {
   const int nent = op.nent;
   cplx* R = scratch<cplx>(static_cast<size_t>(op.ny) * op.qx * nent, st);
@@ -857,7 +1017,8 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.u = d_in; p.r2 = r2; p.T = T;
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
-    launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_fx");
+    if (op.ex == 256) launch_tma<FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    else launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_fx");
   } else {
     const bool p2 = op.p2x;
     const FftPlan& pl = p2 ? op.plan_x2 : op.plan_x;
@@ -880,7 +1041,8 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.T = T; p.S = S;
     p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
     p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ny;
-    launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_fy");
+    if (op.ey == 256) launch_tma<FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
+    else launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_fy");
   } else {
     const bool p2 = op.p2y;
     const FftPlan& pl = p2 ? op.plan_y2 : op.plan_y;
@@ -908,7 +1070,15 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
     p.S = S; p.T = T;
     p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
     p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ey;
-    launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_iy");
+    if (op.ey == 256) {
+      const uint64_t dims[3] = {2ull * np, 256ull, static_cast<uint64_t>(nrhs) * op.ex};
+      const uint64_t strides[2] = {static_cast<uint64_t>(np) * 16, 256ull * np * 16};
+      const uint32_t box[3] = {16, 256, 1};
+      encode_tensor_map_f64(&p.tm, S, 3, dims, strides, box);
+      launch_tma<IyStream, EMIE_TMA_NST_INV>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_iy");
+    } else {
+      launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_iy");
+    }
   } else {
     const bool p2 = op.p2y;
     const FftPlan& pl = p2 ? op.plan_y2 : op.plan_y;
@@ -932,7 +1102,16 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.ex;
     p.inv = 1.0 / static_cast<double>(op.lateral());
-    launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_ix");
+    if (op.ex == 256) {
+      const uint64_t dims[4] = {2ull * op.ny, static_cast<uint64_t>(np), 256ull, static_cast<uint64_t>(nrhs)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(op.ny) * 16, static_cast<uint64_t>(np) * op.ny * 16,
+                                   256ull * np * op.ny * 16};
+      const uint32_t box[4] = {16, 1, 256, 1};
+      encode_tensor_map_f64(&p.tm, T, 4, dims, strides, box);
+      launch_tma<IxStream, EMIE_TMA_NST_INV>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_ix");
+    } else {
+      launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_ix");
+    }
   } else {
     const bool p2 = op.p2x;
     const FftPlan& pl = p2 ? op.plan_x2 : op.plan_x;

@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "operator.cuh"
+#include "tma.cuh"
 
 #ifndef EMIE_CT_EXPERIMENT
 #define EMIE_CT_EXPERIMENT 0  // 1: no MMAs, 2: no copies (timing experiments only)
@@ -43,34 +44,6 @@ namespace {
 // mode computes; lane k reads entry (k + t) mod nz -> conflict-free.
 constexpr int kCtWarps = 8;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
-}
 
 struct ModeCols {
   int mode[4];
@@ -253,9 +226,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
 }
 
 // mirror mi (0 .. nmir-1) of quadrant mode qm, in mode_cols order
