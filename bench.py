@@ -132,6 +132,24 @@ def reference_apply_rate(cfg, reps, threads=None):
     return d
 
 
+def reference_greens_seconds(cfg, stride=16, threads=None):
+    """The reference's Green's build (assemble_block over the offsets with its
+    per-thread designers and shared moment memo, greens.cpp:332-371) timed on
+    every stride-th offset through oracle/_ref/emie_ref_tool and extrapolated
+    linearly to all nx*ny offsets."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_binding as R
+    if not R.TOOL.exists():
+        R.build()
+    with tempfile.TemporaryDirectory() as td:
+        case = Path(td) / "case.bin"
+        write_case(cfg, case, cfg.omega)
+        d = json.loads(R.run_tool("bench-greens", case, stride, threads=threads))
+    d["extrapolated_s"] = d["seconds"] * d["total_offsets"] / d["offsets"]
+    d["stride"] = stride
+    return d
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -155,6 +173,15 @@ def run_reference(args):
                                    "OpenMP, FFTW-API shim)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        g = reference_greens_seconds(cfg, 16, threads=threads)
+        line["greens_build_s"] = g["extrapolated_s"]
+        line["greens_sample"] = (f"assemble_block over every {g['stride']}th offset ({g['offsets']} of "
+                                 f"{g['total_offsets']}, {g['seconds']:.2f} s on {g['threads']} threads), "
+                                 "extrapolated linearly")
+    except Exception as ex:  # noqa: BLE001
+        line["greens_build_s"] = None
+        line["greens_sample"] = f"unavailable: {ex}"
     print(json.dumps(line), flush=True)
     return 0
 
@@ -202,6 +229,24 @@ def run_ours(args):
         sop = emie.transform_operator(blocks, cfg.nx, cfg.ny, cfg.nz, omega)
     torch.cuda.synchronize()
     greens_s = time.perf_counter() - t0
+    # second build in the same process (allocator and modules warm), with the
+    # library's own CUDA-event stage timers: 5 = assemble kernel, 6 = spectra
+    greens_warm_s, greens_stage = None, None
+    if operator_src == "device Green's build":
+        L.emie_cu_profile_enable.argtypes = [ctypes.c_int]
+        L.emie_cu_profile_collect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        ms8, cnt8 = np.zeros(8), np.zeros(8, np.int64)
+        L.emie_cu_profile_collect(ms8.ctypes.data, cnt8.ctypes.data, 8)
+        L.emie_cu_profile_enable(1)
+        t0 = time.perf_counter()
+        sop2 = emie.assemble_operator(grid, model, omega)
+        torch.cuda.synchronize()
+        greens_warm_s = time.perf_counter() - t0
+        L.emie_cu_profile_enable(0)
+        L.emie_cu_profile_collect(ms8.ctypes.data, cnt8.ctypes.data, 8)
+        greens_stage = {"assemble_kernel_ms": round(float(ms8[5]), 3), "spectra_ms": round(float(ms8[6]), 3)}
+        del sop2
+        torch.cuda.synchronize()
     system = emie.build_system(grid, sop)
 
     n = 3 * cfg.cells()
@@ -308,6 +353,15 @@ def run_ours(args):
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+    greens_cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            g = reference_greens_seconds(cfg, 16, threads=os.cpu_count())
+            greens_cpu = {"value_s": g["extrapolated_s"], "cores": g["threads"], "kind": "reference",
+                          "sample": f"assemble_block over every {g['stride']}th offset ({g['offsets']} of "
+                                    f"{g['total_offsets']}, {g['seconds']:.2f} s), extrapolated linearly"}
+        except Exception as ex:  # noqa: BLE001
+            greens_cpu = {"value_s": None, "sample": f"unavailable: {ex}"}
 
     if rank == 0:
         line = {
@@ -322,6 +376,9 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (1.1 GB operator streamed per step)",
                        "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
             "greens_build_s": greens_s,
+            "greens_build_warm_s": greens_warm_s,
+            "greens_stage_ms": greens_stage,
+            "greens_cpu_baseline": greens_cpu,
             "stage_ms": stages,
             "roofline": {"bound": "hbm", "kernel": ct_kernel, "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
