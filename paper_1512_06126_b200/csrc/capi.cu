@@ -291,6 +291,63 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   EMIE_CUDA(cudaMemcpy(op.emap, op.emap_host.data(), op.nent * sizeof(int2), cudaMemcpyHostToDevice));
 }
 
+// Host-buffer apply (the reference-facing GridVector call): the right-hand
+// sides go through one at a time so PCIe runs full duplex -- rhs r+1 uploads
+// on one copy stream while rhs r computes and rhs r-1 downloads on another.
+// Each output column depends only on its own input column, so the result is
+// bit-identical to the batched device call.
+namespace {
+struct CopyStreams {
+  cudaStream_t up = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> ev;
+  CopyStreams() {
+    EMIE_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    EMIE_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+  }
+  cudaEvent_t event(std::size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      EMIE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+};
+CopyStreams& copy_streams() {
+  static thread_local CopyStreams cs;  // per host thread: concurrent callers stay independent
+  return cs;
+}
+}  // namespace
+
+void host_pipelined_apply(const Operator& op, const System* sys, const double* h_in, double* h_out,
+                          int nrhs, cudaStream_t st) {
+  CopyStreams& cs = copy_streams();
+  const std::size_t n1 = 3 * op.cells();
+  cplx* din = scratch<cplx>(n1 * nrhs, st);
+  cplx* dout = scratch<cplx>(n1 * nrhs, st);
+  cudaEvent_t ready = cs.event(0);  // scratch allocated on st
+  EMIE_CUDA(cudaEventRecord(ready, st));
+  EMIE_CUDA(cudaStreamWaitEvent(cs.up, ready, 0));
+  for (int r = 0; r < nrhs; ++r) {
+    const cudaEvent_t in = cs.event(1 + 2 * r), out = cs.event(2 + 2 * r);
+    EMIE_CUDA(cudaMemcpyAsync(din + r * n1, reinterpret_cast<const cplx*>(h_in) + r * n1, n1 * sizeof(cplx),
+                              cudaMemcpyHostToDevice, cs.up));
+    EMIE_CUDA(cudaEventRecord(in, cs.up));
+    EMIE_CUDA(cudaStreamWaitEvent(st, in, 0));
+    apply_b(op, din + r * n1, dout + r * n1, 1, sys, st);
+    EMIE_CUDA(cudaEventRecord(out, st));
+    EMIE_CUDA(cudaStreamWaitEvent(cs.down, out, 0));
+    EMIE_CUDA(cudaMemcpyAsync(reinterpret_cast<cplx*>(h_out) + r * n1, dout + r * n1, n1 * sizeof(cplx),
+                              cudaMemcpyDeviceToHost, cs.down));
+  }
+  const cudaEvent_t done = cs.event(1 + 2 * nrhs);
+  EMIE_CUDA(cudaEventRecord(done, cs.down));
+  EMIE_CUDA(cudaStreamWaitEvent(st, done, 0));  // buffers go back to the pool after the last copy
+  release(din, st);
+  release(dout, st);
+  EMIE_CUDA(cudaStreamSynchronize(st));
+}
+
 }  // namespace emie_cu
 
 using namespace emie_cu;
@@ -519,16 +576,7 @@ int emie_cu_apply_system_host(emie_cu_system h, const double* h_in, double* h_ou
   return guarded([&] {
     if (!h || !h_in || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
     if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
-    const cudaStream_t st = as_stream(stream);
-    const std::size_t n = 3 * h->sys.op->cells() * static_cast<std::size_t>(nrhs);
-    cplx* din = scratch<cplx>(n, st);
-    cplx* dout = scratch<cplx>(n, st);
-    EMIE_CUDA(cudaMemcpyAsync(din, h_in, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
-    apply_b(*h->sys.op, din, dout, nrhs, &h->sys, st);
-    EMIE_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
-    release(din, st);
-    release(dout, st);
-    EMIE_CUDA(cudaStreamSynchronize(st));
+    host_pipelined_apply(*h->sys.op, &h->sys, h_in, h_out, nrhs, as_stream(stream));
   });
 }
 
@@ -610,16 +658,7 @@ extern "C" int emie_cu_apply_spectral_host(emie_cu_operator h, const double* h_i
   return guarded([&] {
     if (!h || !h_in || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "apply: null pointer");
     if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "apply: nrhs < 1");
-    const cudaStream_t st = as_stream(stream);
-    const std::size_t n = 3 * h->op.cells() * static_cast<std::size_t>(nrhs);
-    cplx* din = scratch<cplx>(n, st);
-    cplx* dout = scratch<cplx>(n, st);
-    EMIE_CUDA(cudaMemcpyAsync(din, h_in, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
-    apply_b(h->op, din, dout, nrhs, nullptr, st);
-    EMIE_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
-    release(din, st);
-    release(dout, st);
-    EMIE_CUDA(cudaStreamSynchronize(st));
+    host_pipelined_apply(h->op, nullptr, h_in, h_out, nrhs, as_stream(stream));
   });
 }
 
