@@ -13,6 +13,10 @@
 //   emie_ref_tool bench-apply <case.bin> <reps> <nrhs>
 //       times apply(SystemOperator) on a synthetic spectral operator of the
 //       case's shape (operator values do not change the cost), all OMP threads
+//   emie_ref_tool snapshot-check <file> [<resave>]
+//       loads an EMG1 snapshot with the reference's load_operator, prints its
+//       dimensions and a checksum of every stored entry, and optionally writes
+//       it back with the reference's save_operator
 //   emie_ref_tool bench-greens <case.bin> <stride>
 //       times assemble_block over every stride-th offset with the same
 //       per-thread designers / shared memo / dynamic schedule as
@@ -257,6 +261,27 @@ int bench_greens(const char* case_path, int stride) {
   return 0;
 }
 
+// load an EMG1 snapshot with the reference's load_operator (greens.cpp:425-446)
+// and print the same checksum as tests/cpp/dropin_snapshot.cpp
+int snapshot_check(const char* path, const char* resave) {
+  const auto op = load_operator(path);
+  if (!op) {
+    std::printf("{\"loaded\": false}\n");
+    return 3;
+  }
+  double s = 0.0, w = 1.0;
+  for (const auto& b : op->blocks)
+    for (const auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz})
+      for (const auto& v : *c) {
+        s += w * (v.real() + 0.5 * v.imag());
+        w = w * 1.000001 + 1e-3;
+      }
+  std::printf("{\"loaded\": true, \"nx\": %d, \"ny\": %d, \"nz\": %d, \"omega\": %.17g, \"checksum\": %.17g}\n",
+              op->nx, op->ny, op->nz, op->omega, s);
+  if (resave) save_operator(resave, *op);  // the reference's own writer, for a byte comparison
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -266,6 +291,8 @@ int main(int argc, char** argv) {
       return bench_apply(argv[2], std::atoi(argv[3]), std::atoi(argv[4]));
     if (argc >= 4 && std::string(argv[1]) == "bench-greens")
       return bench_greens(argv[2], std::atoi(argv[3]));
+    if (argc >= 3 && std::string(argv[1]) == "snapshot-check")
+      return snapshot_check(argv[2], argc >= 4 ? argv[3] : nullptr);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "emie_ref_tool: %s\n", e.what());
     return 2;
