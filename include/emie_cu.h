@@ -181,6 +181,48 @@ int emie_cu_fgmres_host(emie_cu_system sys, const double* h_rhs, double* h_x, in
                         double tol, int restart, int max_iters, emie_cu_report* reports,
                         double* h_history, int hist_cap, void* stream);
 
+/* ---- sharded apply (one grid over G GPUs) -------------
+ * apply(SystemOperator) (src/cie.cpp:56-73 over src/toeplitz.cpp:163-283)
+ * split at its contraction: each rank transforms its depth slab (all three
+ * components of intervals [z0, z1)), two all-to-alls (the caller's NCCL
+ * plumbing, paper_1512_06126_b200/distributed.py) move spectrum columns
+ * between the slab layout and the rank's quadrant-mode shard, and the rank
+ * contracts only its modes. Spectrum layout S[r][m][plane], mode m =
+ * mx*ey + my, plane = c*nz + iz (nz of the slab for slab spectra). */
+
+/* lateral geometry (plans, twiddles) of an nx x ny x nz field, no spectra */
+int emie_cu_geometry_create(int nx, int ny, int nz, emie_cu_operator* out);
+
+/* a copy of op holding only quadrant modes [q0, q1) (a mode shard) */
+int emie_cu_operator_restrict_modes(emie_cu_operator op, int q0, int q1, emie_cu_operator* out);
+
+/* the full modes m = mx*ey + my of quadrant modes [q0, q1) in contraction
+ * order (each quadrant mode's 1-4 mirrors); *count = total, at most cap written */
+int emie_cu_mode_list(emie_cu_operator op, int q0, int q1, int* h_modes, int cap, int* count);
+
+/* stage 1 (toeplitz.cpp:169-195, r2 scaling cie.cpp:63-65 if d_r2 != NULL):
+ * zero-padded forward 2-D DFT of every plane into mode-major d_S */
+int emie_cu_lateral_forward(emie_cu_operator geom, const double* d_in, const double* d_r2, double* d_S,
+                            int nrhs, void* stream);
+
+/* stage 3 (toeplitz.cpp:260-282; with d_s, d_r1: the system epilogue
+ * s*u + r1*(.) of cie.cpp:67-72 on d_u): inverse 2-D DFT, truncation, 1/(ex ey) */
+int emie_cu_lateral_inverse(emie_cu_operator geom, const double* d_S, const double* d_u, double* d_out,
+                            const double* d_s, const double* d_r1, int nrhs, void* stream);
+
+/* stage 2 (toeplitz.cpp:197-258) for quadrant modes [q0, q1), in place on the
+ * full-depth spectrum d_S (all modes' storage, only these modes touched) */
+int emie_cu_contract_modes(emie_cu_operator op, double* d_S, int nrhs, int q0, int q1, void* stream);
+
+/* column moves between slab spectra, full-depth spectra and packed exchange
+ * buffers: element (r, i, c, z), i < nidx, c < 3, z < nzh, goes from
+ * src[(mode_s)*desc[1] + c*desc[2] + desc[3] + z] to the same form in dst,
+ * with mode = r*modes_total + d_idx[i] when desc[0] != 0 ("mapped") and
+ * r*nidx + i otherwise ("packed") */
+int emie_cu_move_planes(const double* d_src, double* d_dst, int nrhs, int nidx, const int* d_idx,
+                        long long modes_total, const int src_desc[4], const int dst_desc[4], int nzh,
+                        void* stream);
+
 /* kernel launches issued by this library on the calling thread since the
  * last reset (evidence for bench.py's gpu_launches) */
 long long emie_cu_launch_count(void);

@@ -116,6 +116,15 @@ def lib():
         "emie_cu_device_count": [ip],
         "emie_cu_kernel_output": [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp],
+        # sharded apply (distributed.py)
+        "emie_cu_geometry_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+        "emie_cu_operator_restrict_modes": [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+        "emie_cu_mode_list": [vp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_int, ip],
+        "emie_cu_lateral_forward": [vp, vp, vp, vp, ctypes.c_int, vp],
+        "emie_cu_lateral_inverse": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp],
+        "emie_cu_contract_modes": [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
+        "emie_cu_move_planes": [vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_longlong, ip, ip,
+                                ctypes.c_int, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -364,6 +373,25 @@ def assemble_operator(grid: AnomalyGrid, model: LayeredModel, omega: float,
                                       grid.ny, grid.hx, grid.hy, float(omega), _ptr(fp),
                                       int(keep_blocks), ctypes.byref(h), None))
     return SpectralOperator(h)
+
+
+def restrict_modes(op: SpectralOperator, q0: int, q1: int) -> SpectralOperator:
+    """A device copy of op holding only quadrant modes [q0, q1) (the mode
+    shard of a sharded apply, distributed.py)."""
+    h = ctypes.c_void_p()
+    _check(lib().emie_cu_operator_restrict_modes(op.handle, int(q0), int(q1), ctypes.byref(h)))
+    return SpectralOperator(h)
+
+
+def mode_list(op: SpectralOperator, q0: int, q1: int) -> np.ndarray:
+    """Full modes (mx*ey + my) of quadrant modes [q0, q1) in contraction order."""
+    L = lib()
+    n = ctypes.c_int()
+    _check(L.emie_cu_mode_list(op.handle, int(q0), int(q1), None, 0, ctypes.byref(n)))
+    out = np.zeros(max(1, n.value), np.int32)
+    _check(L.emie_cu_mode_list(op.handle, int(q0), int(q1),
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), n.value, ctypes.byref(n)))
+    return out[:n.value]
 
 
 def design_offset_filters(oi: int, oj: int, hx: float, hy: float,

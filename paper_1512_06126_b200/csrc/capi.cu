@@ -192,7 +192,7 @@ cplx* upload_twiddles(int n) {
   return d;
 }
 
-void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) {
+void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, int q0, int q1) {
   if (nx <= 0 || ny <= 0 || nz <= 0)
     fail(EMIE_CU_INVALID_ARGUMENT, "transform_operator: empty operator");
   op.nx = nx;
@@ -231,9 +231,16 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega) 
   op.p2x = op.ex <= 2048 && make_pow2_plan(op.ex, op.plan_x2);
   op.p2y = op.ey <= 2048 && make_pow2_plan(op.ey, op.plan_y2);
   keep_pool_warm();
-  op.spec = dev_alloc<cplx>(op.modes() * op.nentD);
-  if (op.nentD != op.nent)  // padding slots of the MMA layout are read, never written
-    EMIE_CUDA(cudaMemset(op.spec, 0, op.modes() * op.nentD * sizeof(cplx)));
+  if (q1 < 0) q1 = static_cast<int>(op.modes());
+  if (q0 < 0 || q0 > q1 || q1 > static_cast<int>(op.modes()))
+    fail(EMIE_CU_OUT_OF_RANGE, "operator: quadrant-mode range outside the embedding");
+  op.qbase = q0;
+  op.qcount = q1 - q0;
+  if (op.qcount > 0) {
+    op.spec = dev_alloc<cplx>(static_cast<std::size_t>(op.qcount) * op.nentD);
+    if (op.nentD != op.nent)  // padding slots of the MMA layout are read, never written
+      EMIE_CUDA(cudaMemset(op.spec, 0, static_cast<std::size_t>(op.qcount) * op.nentD * sizeof(cplx)));
+  }
   op.tw_x = upload_twiddles(op.ex);
   op.tw_y = upload_twiddles(op.ey);
   op.emap_host.assign(op.nent, int2{-1, -1});
@@ -447,6 +454,8 @@ int emie_cu_operator_download_spectra(emie_cu_operator h, double* h_comp) {
   return guarded([&] {
     if (!h || !h_comp) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
     const Operator& op = h->op;
+    if (op.qbase != 0 || op.qcount != static_cast<int>(op.modes()))
+      fail(EMIE_CU_INVALID_ARGUMENT, "download_spectra: operator holds a mode shard");
     std::vector<cplx> mm(op.modes() * op.nentD);
     EMIE_CUDA(cudaMemcpy(mm.data(), op.spec, mm.size() * sizeof(cplx), cudaMemcpyDeviceToHost));
     // diagonal-layout mode blocks -> six component arrays (toeplitz.hpp:58-61)
@@ -497,6 +506,105 @@ int emie_cu_operator_download_blocks(emie_cu_operator h, double* h_blocks) {
 }
 
 void emie_cu_operator_destroy(emie_cu_operator h) { delete h; }
+
+// ------------------------------------------------------- sharded apply --
+int emie_cu_geometry_create(int nx, int ny, int nz, emie_cu_operator* out) {
+  return guarded([&] {
+    if (!out) fail(EMIE_CU_INVALID_ARGUMENT, "geometry: null pointer");
+    auto h = std::make_unique<emie_cu_operator_s>();
+    init_operator_geometry(h->op, nx, ny, nz, 0.0, 0, 0);
+    *out = h.release();
+  });
+}
+
+int emie_cu_operator_restrict_modes(emie_cu_operator h, int q0, int q1, emie_cu_operator* out) {
+  return guarded([&] {
+    if (!h || !out) fail(EMIE_CU_INVALID_ARGUMENT, "restrict_modes: null pointer");
+    const Operator& src = h->op;
+    if (q0 < src.qbase || q1 > src.qbase + src.qcount || q0 > q1)
+      fail(EMIE_CU_OUT_OF_RANGE, "restrict_modes: range not stored in the operator");
+    auto r = std::make_unique<emie_cu_operator_s>();
+    init_operator_geometry(r->op, src.nx, src.ny, src.nz, src.omega, q0, q1);
+    if (q1 > q0)
+      EMIE_CUDA(cudaMemcpy(r->op.spec, src.spec + static_cast<std::size_t>(q0 - src.qbase) * src.nentD,
+                           static_cast<std::size_t>(q1 - q0) * src.nentD * sizeof(cplx), cudaMemcpyDeviceToDevice));
+    *out = r.release();
+  });
+}
+
+int emie_cu_mode_list(emie_cu_operator h, int q0, int q1, int* modes, int cap, int* count) {
+  return guarded([&] {
+    if (!h || !count) fail(EMIE_CU_INVALID_ARGUMENT, "mode_list: null pointer");
+    const Operator& op = h->op;
+    if (q0 < 0 || q0 > q1 || q1 > static_cast<int>(op.modes()))
+      fail(EMIE_CU_OUT_OF_RANGE, "mode_list: quadrant-mode range outside the embedding");
+    int n = 0;
+    for (int qm = q0; qm < q1; ++qm) {  // mirrors in contraction order (operator.cu mirror_mode)
+      const int qmy = qm / op.qx, qmx = qm - qmy * op.qx;
+      const bool mx_ok = qmx > 0 && (op.ex - qmx) > op.ex / 2;
+      const bool my_ok = qmy > 0 && (op.ey - qmy) > op.ey / 2;
+      const int list[4] = {qmx * op.ey + qmy, (op.ex - qmx) * op.ey + qmy, qmx * op.ey + (op.ey - qmy),
+                           (op.ex - qmx) * op.ey + (op.ey - qmy)};
+      const bool use[4] = {true, mx_ok, my_ok, mx_ok && my_ok};
+      for (int i = 0; i < 4; ++i)
+        if (use[i]) {
+          if (modes && n < cap) modes[n] = list[i];
+          ++n;
+        }
+    }
+    *count = n;
+  });
+}
+
+int emie_cu_lateral_forward(emie_cu_operator geom, const double* d_in, const double* d_r2, double* d_S,
+                            int nrhs, void* stream) {
+  return guarded([&] {
+    if (!geom || !d_in || !d_S) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward: nrhs < 1");
+    const Operator& op = geom->op;
+    const cudaStream_t st = as_stream(stream);
+    cplx* T = scratch<cplx>(static_cast<std::size_t>(nrhs) * 3 * op.nz * op.ny * op.ex, st);
+    lateral_forward(op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<const cplx*>(d_r2), T,
+                    reinterpret_cast<cplx*>(d_S), nrhs, st);
+    release(T, st);
+  });
+}
+
+int emie_cu_lateral_inverse(emie_cu_operator geom, const double* d_S, const double* d_u, double* d_out,
+                            const double* d_s, const double* d_r1, int nrhs, void* stream) {
+  return guarded([&] {
+    if (!geom || !d_S || !d_out) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_inverse: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_inverse: nrhs < 1");
+    if ((d_s == nullptr) != (d_r1 == nullptr) || (d_s && !d_u))
+      fail(EMIE_CU_INVALID_ARGUMENT, "lateral_inverse: the system epilogue needs s, r1 and u");
+    const Operator& op = geom->op;
+    const cudaStream_t st = as_stream(stream);
+    cplx* T = scratch<cplx>(static_cast<std::size_t>(nrhs) * 3 * op.nz * op.ny * op.ex, st);
+    lateral_inverse(op, reinterpret_cast<const cplx*>(d_S), T, reinterpret_cast<const cplx*>(d_u),
+                    reinterpret_cast<cplx*>(d_out), reinterpret_cast<const cplx*>(d_s), d_r1, nrhs, st);
+    release(T, st);
+  });
+}
+
+int emie_cu_contract_modes(emie_cu_operator h, double* d_S, int nrhs, int q0, int q1, void* stream) {
+  return guarded([&] {
+    if (!h || !d_S) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes: nrhs < 1");
+    contract_modes(h->op, reinterpret_cast<cplx*>(d_S), nrhs, q0, q1, as_stream(stream));
+  });
+}
+
+int emie_cu_move_planes(const double* d_src, double* d_dst, int nrhs, int nidx, const int* d_idx,
+                        long long modes_total, const int src_desc[4], const int dst_desc[4], int nzh,
+                        void* stream) {
+  return guarded([&] {
+    if (!d_src || !d_dst || !src_desc || !dst_desc) fail(EMIE_CU_INVALID_ARGUMENT, "move_planes: null pointer");
+    if ((src_desc[0] || dst_desc[0]) && !d_idx) fail(EMIE_CU_INVALID_ARGUMENT, "move_planes: mode list missing");
+    if (nrhs < 0 || nidx < 0 || nzh < 0) fail(EMIE_CU_INVALID_ARGUMENT, "move_planes: negative size");
+    move_planes(reinterpret_cast<const cplx*>(d_src), reinterpret_cast<cplx*>(d_dst), nrhs, nidx, d_idx,
+                modes_total, src_desc, dst_desc, nzh, as_stream(stream));
+  });
+}
 
 int emie_cu_apply_spectral(emie_cu_operator h, const double* d_in, double* d_out, int nrhs,
                            void* stream) {

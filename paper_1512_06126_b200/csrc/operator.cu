@@ -66,7 +66,7 @@ __device__ __forceinline__ ModeCols mode_cols(int qm, int qx, int ex, int ey) {
 template <int CB>
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     contract_kernel(const cplx* __restrict__ op, cplx* S, int nz, int nsd, int nentD, int ex,
-                    int ey, int qx, int nmodes, int nrhs) {
+                    int ey, int qx, int q0, int q1, int qbase, int nrhs) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = 3 * nz;
@@ -99,17 +99,17 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     }
   };
   uint32_t phase[2] = {0u, 0u};
-  if (gw < nmodes) issue(gw, 0);
+  if (q0 + gw < q1) issue(q0 + gw, 0);
   int it = 0;
-  for (int qm = gw; qm < nmodes; qm += nw, ++it) {
+  for (int qm = q0 + gw; qm < q1; qm += nw, ++it) {
     const int buf = it & 1;
-    if (qm + nw < nmodes) issue(qm + nw, buf ^ 1);
+    if (qm + nw < q1) issue(qm + nw, buf ^ 1);
     mbar_wait(mbar + buf, phase[buf]);
     phase[buf] ^= 1u;
     const cplx* U = ubase + static_cast<size_t>(buf) * CB * np;
     const ModeCols mc = mode_cols(qm, qx, ex, ey);
     const int ncol = mc.nmir * nrhs;
-    const cplx* blk = op + static_cast<size_t>(qm) * nentD;
+    const cplx* blk = op + static_cast<size_t>(qm - qbase) * nentD;
     const int ntri = nz * (nz + 1) / 2;
     const cplx* Dxx = blk;
     const cplx* Dyy = blk + ntri;
@@ -258,7 +258,7 @@ constexpr int kAcc = EMIE_CT_ACC;          // accumulator sets per DMMA chain
 template <int NZ>
 __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
-                        int ex, int ey, int qx, int nmodes, int nrhs, int nentD) {
+                        int ex, int ey, int qx, int q0, int q1, int qbase, int nrhs, int nentD) {
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int nk = np / 4;
   constexpr int W = mma_warps<NZ>();
@@ -294,20 +294,20 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   if (warp == W) {  // ---- producer
     if (lane == 0) {
       int j = 0;
-      for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
+      for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
         const int bs = j % kBlkStages, us = j % kUStages;
         if (j >= kBlkStages) mbar_wait(bempty + bs, static_cast<uint32_t>((j / kBlkStages - 1) & 1));
         const uint32_t blkbytes = nentD * sizeof(cplx);
         // blocks of the modes after the SMEM stages go to L2 ahead of their copy
         for (int d = (j == 0 ? kBlkStages : kL2Ahead); d <= kL2Ahead; ++d) {
           const int qp = qm + d * G;
-          if (qp < nmodes) bulk_prefetch_l2(op + static_cast<size_t>(qp) * nentD, blkbytes);
+          if (qp < q1) bulk_prefetch_l2(op + static_cast<size_t>(qp - qbase) * nentD, blkbytes);
         }
 #if EMIE_CT_EXPERIMENT == 2
         mbar_expect_tx(bfull + bs, 0);
 #else
         mbar_expect_tx(bfull + bs, blkbytes);
-        bulk_g2s(blkbuf + bs * nentD, op + static_cast<size_t>(qm) * nentD, blkbytes, bfull + bs);
+        bulk_g2s(blkbuf + bs * nentD, op + static_cast<size_t>(qm - qbase) * nentD, blkbytes, bfull + bs);
 #endif
         if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
         const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     off[ks] = __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) & 0x7fffffffu;
   }
   int j = 0;
-  for (int qm = blockIdx.x; qm < nmodes; qm += G, ++j) {
+  for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
     const int bs = j % kBlkStages, us = j % kUStages;
     mbar_wait(bfull + bs, static_cast<uint32_t>((j / kBlkStages) & 1));
     mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
@@ -416,60 +416,68 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st) {
   lateral_spectra(op, d_blocks, st);
 }
 
+// K_ct over quadrant modes [q0, q1) (all stored in op: qbase <= q0, q1 <= qbase + qcount):
+// up to two right-hand sides per launch (8 columns of a full mode)
+void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaStream_t st) {
+  if (q0 < op.qbase || q1 > op.qbase + op.qcount || q0 > q1)
+    fail(EMIE_CU_OUT_OF_RANGE, "contraction: quadrant modes outside the stored range");
+  if (q0 == q1) return;
+  const int np = 3 * op.nz;
+  int sms = 0, dev = 0;
+  EMIE_CUDA(cudaGetDevice(&dev));
+  EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int nmodes = q1 - q0;
+  for (int r0 = 0; r0 < nrhs; r0 += 2) {
+    const int g = std::min(2, nrhs - r0);
+    cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
+    if (op.mma) {
+      const size_t smem = 128 + kUStages * 8 * sizeof(long long) +
+                          kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                          kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
+      auto launch = [&](auto kern, int warps) {
+        set_smem(reinterpret_cast<const void*>(kern), smem);
+        int per_sm = 1;
+        EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (warps + 1) * 32, smem));
+        const int grid = std::max(1, std::min(sms * std::max(1, per_sm), nmodes));
+        kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
+                                                   g, op.nentD);
+      };
+      if (op.nz == 8) launch(contract_mma_kernel<8>, mma_warps<8>());
+      else if (op.nz == 16) launch(contract_mma_kernel<16>, mma_warps<16>());
+      else launch(contract_mma_kernel<32>, mma_warps<32>());
+      check_launch("contract_mma_kernel");
+      continue;
+    }
+    const int CB = g == 2 ? 8 : 4;
+    // two input buffers per warp; as many warps as 220 KB of SMEM holds
+    const size_t per_warp = 16 + 2 * static_cast<size_t>(CB) * np * sizeof(cplx);
+    const int wpb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(kCtWarps, (220u << 10) / per_warp)));
+    const size_t smem = per_warp * wpb;
+    const int grid = std::max(1, std::min(sms, ceil_div(nmodes, wpb)));
+    if (CB == 8) {
+      set_smem(reinterpret_cast<const void*>(contract_kernel<8>), smem);
+      contract_kernel<8><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
+                                                       q0, q1, op.qbase, g);
+    } else {
+      set_smem(reinterpret_cast<const void*>(contract_kernel<4>), smem);
+      contract_kernel<4><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
+                                                       q0, q1, op.qbase, g);
+    }
+    check_launch("contract_kernel");
+  }
+}
+
 void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs, const System* sys,
              cudaStream_t st) {
+  if (op.qbase != 0 || op.qcount != static_cast<int>(op.modes()))
+    fail(EMIE_CU_INVALID_ARGUMENT, "apply: operator holds a mode shard (use the sharded apply)");
   const int np = 3 * op.nz;
   const long long rows = static_cast<long long>(nrhs) * np * op.ny;
   cplx* T = scratch<cplx>(static_cast<size_t>(rows) * op.ex, st);
   cplx* S = scratch<cplx>(static_cast<size_t>(nrhs) * op.lateral() * np, st);
   lateral_forward(op, d_in, sys ? sys->r2 : nullptr, T, S, nrhs, st);
-  // K_ct: up to two right-hand sides per launch (8 columns of a full mode)
   profile_mark(2, true, st);
-  {
-    int sms = 0, dev = 0;
-    EMIE_CUDA(cudaGetDevice(&dev));
-    EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int nmodes = static_cast<int>(op.modes());
-    for (int r0 = 0; r0 < nrhs; r0 += 2) {
-      const int g = std::min(2, nrhs - r0);
-      cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
-      const bool mma = op.mma;
-      if (mma) {
-        const size_t smem = 128 + kUStages * 8 * sizeof(long long) +
-                            kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
-                            kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
-        auto launch = [&](auto kern, int warps) {
-          set_smem(reinterpret_cast<const void*>(kern), smem);
-          int per_sm = 1;
-          EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (warps + 1) * 32, smem));
-          const int grid = std::max(1, std::min(sms * std::max(1, per_sm), nmodes));
-          kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, nmodes, g,
-                                                     op.nentD);
-        };
-        if (op.nz == 8) launch(contract_mma_kernel<8>, mma_warps<8>());
-        else if (op.nz == 16) launch(contract_mma_kernel<16>, mma_warps<16>());
-        else launch(contract_mma_kernel<32>, mma_warps<32>());
-        check_launch("contract_mma_kernel");
-        continue;
-      }
-      const int CB = g == 2 ? 8 : 4;
-      // two input buffers per warp; as many warps as 220 KB of SMEM holds
-      const size_t per_warp = 16 + 2 * static_cast<size_t>(CB) * np * sizeof(cplx);
-      const int wpb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(kCtWarps, (220u << 10) / per_warp)));
-      const size_t smem = per_warp * wpb;
-      const int grid = std::max(1, std::min(sms, ceil_div(nmodes, wpb)));
-      if (CB == 8) {
-        set_smem(reinterpret_cast<const void*>(contract_kernel<8>), smem);
-        contract_kernel<8><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex,
-                                                         op.ey, op.qx, nmodes, g);
-      } else {
-        set_smem(reinterpret_cast<const void*>(contract_kernel<4>), smem);
-        contract_kernel<4><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex,
-                                                         op.ey, op.qx, nmodes, g);
-      }
-      check_launch("contract_kernel");
-    }
-  }
+  contract_modes(op, S, nrhs, op.qbase, op.qbase + op.qcount, st);
   profile_mark(2, false, st);
   lateral_inverse(op, S, T, d_in, d_out, sys ? sys->s : nullptr, sys ? sys->r1 : nullptr, nrhs,
                   st);

@@ -1,6 +1,7 @@
 // Device-resident operator objects behind the C ABI (include/emie_cu.h).
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <vector>
@@ -54,6 +55,10 @@ struct Operator {
   FftPlan plan_x2, plan_y2;  // radix-16 plans when the length is a power of two
   bool p2x = false, p2y = false;
 
+  // stored quadrant modes [qbase, qbase + qcount): all of them unless the
+  // operator is a mode shard of a sharded apply (or a lateral-only geometry, qcount = 0)
+  int qbase = 0, qcount = 0;
+
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
   std::size_t lateral() const { return static_cast<std::size_t>(ex) * ey; }
   std::size_t cells() const { return static_cast<std::size_t>(nx) * ny * nz; }
@@ -70,7 +75,8 @@ struct System {
 };
 
 // host helpers
-void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega);
+// allocates spectra for quadrant modes [q0, q1) (q1 < 0: all; q0 == q1: lateral geometry only)
+void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, int q0 = 0, int q1 = -1);
 void keep_pool_warm();
 cplx* upload_twiddles(int n);
 
@@ -85,6 +91,11 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
 void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st);
 void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs,
              const System* sys, cudaStream_t st);
+void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaStream_t st);
+
+// sharded apply column moves (shard.cu); desc = {mapped, planes per column, component stride, depth offset}
+void move_planes(const cplx* src, cplx* dst, int nrhs, int nidx, const int* idx, long long modes_total,
+                 const int src_desc[4], const int dst_desc[4], int nzh, cudaStream_t st);
 
 // Green's build (greens.cu)
 struct FilterParams {

@@ -1,0 +1,355 @@
+"""Strong scaling of one grid over G GPUs.
+
+apply(SystemOperator) (reference src/cie.cpp:56-73 over src/toeplitz.cpp:163-283)
+split at its contraction:
+
+  1. every rank owns a depth slab -- all three components of the intervals
+     [z0, z1) -- and transforms it laterally (r2 scaling, zero-padded 2-D
+     DFTs): S_loc[r][m][c*nzl + z], mode m = mx*ey + my;
+  2. all-to-all #1: rank h sends rank g the columns of g's modes (the 1-4
+     mirrors of g's quadrant modes, in contraction order) for its planes; g
+     scatters them into the full-depth spectrum S[r][m][c*nz + z];
+  3. rank g contracts its quadrant modes [q0, q1) with its shard of the
+     spectra (1/G of the operator in HBM);
+  4. all-to-all #2 returns the columns to the slab owners;
+  5. every rank inverse-transforms its slab with the system epilogue.
+
+The per-rank stages are separate methods so the same code runs under NCCL
+(one process per GPU), gloo on CPU (tests, NumPy backend) or a loopback that
+runs G virtual ranks in one process (one-GPU parity tests). Backends: CUDA
+(the C ABI of libemie_cu.so on torch tensors) and NumPy (the restatement of
+oracle/emie_oracle.py, test infrastructure only).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Sequence
+
+import numpy as np
+
+
+# ------------------------------------------------------------------ plan ----
+def _splits(n: int, g: int) -> List[int]:
+    return [(i * n) // g for i in range(g + 1)]
+
+
+def mirror_modes(qm: int, qx: int, ex: int, ey: int) -> List[int]:
+    """Full modes m = mx*ey + my of quadrant mode qm in contraction order
+    (operator.cu mirror_mode; emie_cu_mode_list)."""
+    qmy, qmx = divmod(qm, qx)
+    mx_ok = qmx > 0 and (ex - qmx) > ex // 2
+    my_ok = qmy > 0 and (ey - qmy) > ey // 2
+    out = [qmx * ey + qmy]
+    if mx_ok:
+        out.append((ex - qmx) * ey + qmy)
+    if my_ok:
+        out.append(qmx * ey + (ey - qmy))
+    if mx_ok and my_ok:
+        out.append((ex - qmx) * ey + (ey - qmy))
+    return out
+
+
+@dataclass
+class ShardPlan:
+    """Depth slabs and quadrant-mode shards of G ranks for one grid."""
+    nx: int
+    ny: int
+    nz: int
+    ex: int
+    ey: int
+    G: int
+
+    def __post_init__(self):
+        if not 1 <= self.G <= self.nz:
+            raise ValueError("shard plan: need 1 <= G <= nz (every rank owns at least one interval)")
+        self.qx, self.qy = self.ex // 2 + 1, self.ey // 2 + 1
+        self.E = self.ex * self.ey
+        self.z = _splits(self.nz, self.G)
+        self.q = _splits(self.qx * self.qy, self.G)
+        self.modes = [np.array([m for qm in range(self.q[g], self.q[g + 1])
+                                for m in mirror_modes(qm, self.qx, self.ex, self.ey)], dtype=np.int32)
+                      for g in range(self.G)]
+
+    def nzl(self, g: int) -> int:
+        return self.z[g + 1] - self.z[g]
+
+    def slab_cells(self, g: int) -> int:
+        return self.nzl(g) * self.ny * self.nx
+
+
+def slab_of(u: np.ndarray, plan: ShardPlan, g: int, nrhs: int) -> np.ndarray:
+    """Rank g's part [nrhs][3][nzl][ny][nx] of nrhs GridVectors (flat)."""
+    v = np.asarray(u).reshape(nrhs, 3, plan.nz, plan.ny, plan.nx)
+    return np.ascontiguousarray(v[:, :, plan.z[g]:plan.z[g + 1]])
+
+
+def join_slabs(parts: Sequence[np.ndarray], plan: ShardPlan, nrhs: int) -> np.ndarray:
+    """Inverse of slab_of over all ranks: nrhs flat GridVectors."""
+    v = np.concatenate([np.asarray(p).reshape(nrhs, 3, plan.nzl(g), plan.ny, plan.nx)
+                        for g, p in enumerate(parts)], axis=2)
+    return v.reshape(nrhs, -1)
+
+
+# -------------------------------------------------------- orchestration ----
+class ShardedApply:
+    """One rank's share of the sharded apply(SystemOperator)."""
+
+    def __init__(self, plan: ShardPlan, rank: int, backend, nrhs: int):
+        self.plan, self.rank, self.be, self.nrhs = plan, rank, backend, nrhs
+        self.nzl = plan.nzl(rank)
+        self.q0, self.q1 = plan.q[rank], plan.q[rank + 1]
+
+    # column descriptors {mapped, planes per column, component stride, depth offset}
+    def _slab_desc(self, mapped: bool):
+        return (1 if mapped else 0, 3 * self.nzl, self.nzl, 0)
+
+    def stage_forward(self, U):
+        """Slab transform and the packed columns for every destination rank."""
+        P, be = self.plan, self.be
+        S_loc = be.lateral_forward(U, self.nrhs)
+        self._U, self._S_loc = U, S_loc
+        sends = []
+        for g in range(P.G):
+            buf = be.empty((self.nrhs, len(P.modes[g]), 3 * self.nzl))
+            be.move(S_loc, buf, self.nrhs, g, P.E, self._slab_desc(True), self._slab_desc(False), self.nzl)
+            sends.append(buf)
+        return sends
+
+    def stage_contract(self, recvs):
+        """Scatter the slabs' columns into the full-depth spectrum of this
+        rank's modes, contract them, pack the results per slab owner."""
+        P, be, me = self.plan, self.be, self.rank
+        S = be.zeros((self.nrhs, P.E, 3 * P.nz))
+        for h, buf in enumerate(recvs):
+            nzh = P.nzl(h)
+            be.move(buf, S, self.nrhs, me, P.E, (0, 3 * nzh, nzh, 0), (1, 3 * P.nz, P.nz, P.z[h]), nzh)
+        be.contract(S, self.nrhs, self.q0, self.q1)
+        sends = []
+        for h in range(P.G):
+            nzh = P.nzl(h)
+            buf = be.empty((self.nrhs, len(P.modes[me]), 3 * nzh))
+            be.move(S, buf, self.nrhs, me, P.E, (1, 3 * P.nz, P.nz, P.z[h]), (0, 3 * nzh, nzh, 0), nzh)
+            sends.append(buf)
+        return sends
+
+    def stage_inverse(self, recvs):
+        """Columns back into the slab spectrum, inverse transform + epilogue."""
+        P, be = self.plan, self.be
+        for g, buf in enumerate(recvs):
+            be.move(buf, self._S_loc, self.nrhs, g, P.E, self._slab_desc(False), self._slab_desc(True), self.nzl)
+        out = be.lateral_inverse(self._S_loc, self._U, self.nrhs)
+        self._S_loc = self._U = None
+        return out
+
+
+def loopback_apply(shards: Sequence[ShardedApply], slabs):
+    """G virtual ranks in one process: the all-to-alls are list transposes."""
+    s1 = [sh.stage_forward(u) for sh, u in zip(shards, slabs)]
+    s2 = [sh.stage_contract([s1[h][g] for h in range(len(shards))]) for g, sh in enumerate(shards)]
+    return [sh.stage_inverse([s2[g][h] for g in range(len(shards))]) for h, sh in enumerate(shards)]
+
+
+def torch_all_to_all(group=None):
+    """all_to_all over torch.distributed (NCCL on GPUs, gloo on CPU) on
+    complex128 tensors of per-peer shapes known to both sides."""
+    import torch
+    import torch.distributed as dist
+
+    use_p2p = dist.get_backend(group) != "nccl"  # gloo has no alltoall: pairwise send/recv
+
+    def a2a(sends, recv_shapes):
+        ins = [torch.view_as_real(s.contiguous()).reshape(-1) for s in sends]
+        outs = [torch.empty(int(np.prod(sh)) * 2, dtype=torch.float64, device=ins[0].device) for sh in recv_shapes]
+        if use_p2p:
+            me = dist.get_rank(group)
+            reqs = []
+            for h in range(len(ins)):
+                if h == me:
+                    outs[h].copy_(ins[h])
+                else:
+                    reqs.append(dist.isend(ins[h], h, group=group))
+                    reqs.append(dist.irecv(outs[h], h, group=group))
+            for r in reqs:
+                r.wait()
+        else:
+            dist.all_to_all(outs, ins, group=group)
+        return [torch.view_as_complex(o.view(-1, 2)).view(sh) for o, sh in zip(outs, recv_shapes)]
+    return a2a
+
+
+class DistributedSystem:
+    """The sharded apply of one grid on this rank (NCCL / gloo plumbing).
+    recv shapes of both exchanges follow from the plan."""
+
+    def __init__(self, shard: ShardedApply, group=None):
+        self.sh, self.a2a = shard, torch_all_to_all(group)
+
+    def apply(self, U):
+        sh, P = self.sh, self.sh.plan
+        me = sh.rank
+        s1 = sh.stage_forward(U)
+        r1 = self.a2a(s1, [(sh.nrhs, len(P.modes[me]), 3 * P.nzl(h)) for h in range(P.G)])
+        s2 = sh.stage_contract(r1)
+        r2 = self.a2a(s2, [(sh.nrhs, len(P.modes[g]), 3 * sh.nzl) for g in range(P.G)])
+        return sh.stage_inverse(r2)
+
+
+# -------------------------------------------------------------- backends ----
+class CudaBackend:
+    """Stages on the device through the C ABI; tensors are torch complex128
+    CUDA tensors (no host fallback: the library raises if it is missing)."""
+
+    def __init__(self, plan: ShardPlan, rank: int, op_shard, sigma_slab, sigma_b_slab, volume_slab):
+        import torch
+        from . import lib, _check
+        self.torch, self.L, self._check = torch, lib(), _check
+        self.plan, self.rank = plan, rank
+        L = self.L
+        nzl = plan.nzl(rank)
+        g = ctypes.c_void_p()
+        _check(L.emie_cu_geometry_create(plan.nx, plan.ny, nzl, ctypes.byref(g)))
+        self.geom = g
+        self.op = op_shard  # SpectralOperator holding quadrant modes [q0, q1)
+        # local system diagonals (cie.cpp:24-54) of the slab's cells
+        sysh = ctypes.c_void_p()
+        sa = np.ascontiguousarray(sigma_slab, dtype=np.complex128)
+        sb = np.ascontiguousarray(sigma_b_slab, dtype=np.complex128)
+        vol = np.ascontiguousarray(volume_slab, dtype=np.float64)
+        _check(L.emie_cu_system_create(g, sa.ctypes.data, sb.ctypes.data, vol.ctypes.data, ctypes.byref(sysh)))
+        n = plan.slab_cells(rank)
+        s = np.zeros(n, np.complex128)
+        r1 = np.zeros(n)
+        r2 = np.zeros(n, np.complex128)
+        _check(L.emie_cu_system_download(sysh, s.ctypes.data, r1.ctypes.data, r2.ctypes.data))
+        L.emie_cu_system_destroy(sysh)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.s = torch.from_numpy(s).to(dev)
+        self.r1 = torch.from_numpy(r1).to(dev)
+        self.r2 = torch.from_numpy(r2).to(dev)
+        self.idx = [torch.from_numpy(m).to(dev) for m in plan.modes]
+        self.dev = dev
+
+    def _st(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+
+    def empty(self, shape):
+        return self.torch.empty(shape, dtype=self.torch.complex128, device=self.dev)
+
+    def zeros(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.complex128, device=self.dev)
+
+    def lateral_forward(self, U, nrhs):
+        P = self.plan
+        S = self.empty((nrhs, P.E, 3 * P.nzl(self.rank)))
+        self._check(self.L.emie_cu_lateral_forward(self.geom, ctypes.c_void_p(U.data_ptr()),
+                                                   ctypes.c_void_p(self.r2.data_ptr()),
+                                                   ctypes.c_void_p(S.data_ptr()), nrhs, self._st()))
+        return S
+
+    def contract(self, S, nrhs, q0, q1):
+        self._check(self.L.emie_cu_contract_modes(self.op.handle, ctypes.c_void_p(S.data_ptr()), nrhs, q0, q1,
+                                                  self._st()))
+
+    def lateral_inverse(self, S, U, nrhs):
+        out = self.torch.empty_like(U)
+        self._check(self.L.emie_cu_lateral_inverse(self.geom, ctypes.c_void_p(S.data_ptr()),
+                                                   ctypes.c_void_p(U.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                                   ctypes.c_void_p(self.s.data_ptr()),
+                                                   ctypes.c_void_p(self.r1.data_ptr()), nrhs, self._st()))
+        return out
+
+    def move(self, src, dst, nrhs, g, E, sdesc, ddesc, nzh):
+        sd = (ctypes.c_int * 4)(*sdesc)
+        dd = (ctypes.c_int * 4)(*ddesc)
+        idx = self.idx[g]
+        self._check(self.L.emie_cu_move_planes(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                               nrhs, int(idx.numel()), ctypes.c_void_p(idx.data_ptr()),
+                                               ctypes.c_longlong(E), sd, dd, nzh, self._st()))
+
+    def __del__(self):
+        try:
+            self.L.emie_cu_operator_destroy(self.geom)
+        except Exception:  # noqa: BLE001 -- interpreter teardown
+            pass
+
+
+class NumpyBackend:
+    """The same stages restated with numpy (oracle/emie_oracle.py): test
+    infrastructure for the gloo CPU tests of the exchange logic."""
+
+    def __init__(self, plan: ShardPlan, rank: int, comp, dims, diag_slab, xp=None):
+        import torch
+        self.torch = torch
+        self.plan, self.rank, self.comp, self.dims = plan, rank, comp, dims
+        self.s, self.r1, self.r2 = (np.asarray(d) for d in diag_slab)
+        self._orc = None
+
+    def _oracle(self):
+        if self._orc is None:
+            import emie_oracle  # tests put oracle/ on sys.path
+            self._orc = emie_oracle
+        return self._orc
+
+    def empty(self, shape):
+        return self.torch.empty(shape, dtype=self.torch.complex128)
+
+    def zeros(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.complex128)
+
+    def lateral_forward(self, U, nrhs):
+        P = self.plan
+        nzl = P.nzl(self.rank)
+        u = U.numpy().reshape(nrhs, 3, nzl * P.ny * P.nx) * self.r2[None, None, :]
+        u = u.reshape(nrhs, 3 * nzl, P.ny, P.nx)
+        pad = np.zeros((nrhs, 3 * nzl, P.ey, P.ex), np.complex128)
+        pad[:, :, :P.ny, :P.nx] = u
+        F = np.fft.fft2(pad, axes=(2, 3))  # [r][plane][my][mx]
+        S = np.ascontiguousarray(F.transpose(0, 3, 2, 1)).reshape(nrhs, P.E, 3 * nzl)  # m = mx*ey + my
+        return self.torch.from_numpy(S)
+
+    def contract(self, S, nrhs, q0, q1):
+        P = self.plan
+        O = self._oracle()
+        Sn = S.numpy()
+        for qm in range(q0, q1):
+            for m in mirror_modes(qm, P.qx, P.ex, P.ey):
+                mx, my = divmod(m, P.ey)
+                M = O._mode_matrix(self.comp, self.dims, P.nz, my, mx)
+                for r in range(nrhs):
+                    Sn[r, m] = M @ Sn[r, m]
+
+    def lateral_inverse(self, S, U, nrhs):
+        P = self.plan
+        nzl = P.nzl(self.rank)
+        F = S.numpy().reshape(nrhs, P.ex, P.ey, 3 * nzl).transpose(0, 3, 2, 1)
+        b = np.fft.ifft2(F, axes=(2, 3))[:, :, :P.ny, :P.nx].reshape(nrhs, 3, -1)
+        u = U.numpy().reshape(nrhs, 3, -1)
+        out = self.s[None, None, :] * u + self.r1[None, None, :] * b
+        return self.torch.from_numpy(np.ascontiguousarray(out).reshape(U.shape))
+
+    def move(self, src, dst, nrhs, g, E, sdesc, ddesc, nzh):
+        idx = self.plan.modes[g]
+        s_arr, d_arr = src.numpy().reshape(-1), dst.numpy().reshape(-1)
+        ni = len(idx)
+        r = np.arange(nrhs)[:, None, None, None]
+        i = np.arange(ni)[None, :, None, None]
+        c = np.arange(3)[None, None, :, None]
+        z = np.arange(nzh)[None, None, None, :]
+        ms = r * E + idx[i] if sdesc[0] else r * ni + i
+        md = r * E + idx[i] if ddesc[0] else r * ni + i
+        d_arr[md * ddesc[1] + c * ddesc[2] + ddesc[3] + z] = s_arr[ms * sdesc[1] + c * sdesc[2] + sdesc[3] + z]
+
+
+def cuda_shard(grid, sop_full, plan: ShardPlan, rank: int, nrhs: int) -> ShardedApply:
+    """Rank `rank`'s sharded apply on the current CUDA device: the mode shard
+    of sop_full's spectra, the lateral geometry and system diagonals of the
+    depth slab (build_system, cie.cpp:24-54, restricted to its cells)."""
+    from . import restrict_modes
+    z0, z1 = plan.z[rank], plan.z[rank + 1]
+    op_shard = restrict_modes(sop_full, plan.q[rank], plan.q[rank + 1])
+    sa = np.asarray(grid.sigma_a)[z0:z1]
+    sb = np.asarray(grid.sigma_b)[z0:z1]
+    vol = np.array([grid.volume(iz) for iz in range(z0, z1)], dtype=np.float64)
+    be = CudaBackend(plan, rank, op_shard, sa, sb, vol)
+    return ShardedApply(plan, rank, be, nrhs)

@@ -75,3 +75,83 @@ def test_sweep_gathers_every_frequency_gloo():
         f = np.logspace(-3, 2, 5)[i]
         m = O.LayeredModel([0.0, 400.0], [0.0, 0.01, 0.1])
         assert v == complex(O.spectral_state(m, 2 * np.pi * f, [1e-3], True).p[0, 1])
+
+
+# ---- strong scaling of one grid: sharded apply -------
+def _sharded_case(nx=6, ny=5, nz=4, nrhs=2, seed=11):
+    import emie_oracle as O
+    rng = np.random.default_rng(seed)
+    nent = 2 * nz * (2 * nz + 1)
+    blocks = rng.standard_normal((ny, nx, nent)) + 1j * rng.standard_normal((ny, nx, nent))
+    dims, comp = O.transform_operator(blocks, nx, ny, nz)
+    m = O.LayeredModel([0.0, 5000.0], [0.0, 0.01, 0.1])
+    breaks = list(np.linspace(10.0, 10.0 + 50.0 * nz, nz + 1))
+    sa = 10.0 ** rng.uniform(-3, 0, (nz, ny, nx))
+    grid = O.make_grid(m, breaks, nx, ny, 100.0, 120.0, sa)
+    diag = O.system_diagonals(grid)
+    U = rng.standard_normal((nrhs, 3 * nx * ny * nz)) + 1j * rng.standard_normal((nrhs, 3 * nx * ny * nz))
+    want = np.stack([O.apply_system(diag, lambda x: O.apply_spectral(comp, dims, nx, ny, nz, x), u) for u in U])
+    return dims, comp, diag, U, want
+
+
+def _sharded_worker(rank, world, port, q):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1512_06126_b200 import distributed as D
+    nx, ny, nz, nrhs = 6, 5, 4, 2
+    dims, comp, diag, U, _ = _sharded_case(nx, ny, nz, nrhs)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], world)
+    z0, z1 = plan.z[rank], plan.z[rank + 1]
+    dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
+    be = D.NumpyBackend(plan, rank, comp, dims, dslab)
+    sysd = D.DistributedSystem(D.ShardedApply(plan, rank, be, nrhs))
+    out = sysd.apply(torch.from_numpy(D.slab_of(U, plan, rank, nrhs)))
+    parts = [None] * world
+    dist.all_gather_object(parts, out.numpy())
+    if rank == 0:
+        q.put(D.join_slabs(parts, plan, nrhs))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_apply_gloo_matches_full_apply():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    *_, want = _sharded_case()
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_sharded_apply_loopback_numpy(G):
+    """G virtual ranks in one process (the list-transpose all-to-all)."""
+    import sys
+    from pathlib import Path
+    import torch
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    from paper_1512_06126_b200 import distributed as D
+    nx, ny, nz, nrhs = 6, 5, 4, 2
+    dims, comp, diag, U, want = _sharded_case(nx, ny, nz, nrhs)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G)
+    # every full mode belongs to exactly one rank's list
+    allm = np.sort(np.concatenate(plan.modes))
+    assert np.array_equal(allm, np.arange(plan.E))
+    shards = []
+    for g in range(G):
+        z0, z1 = plan.z[g], plan.z[g + 1]
+        dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
+        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+    outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)) for g in range(G)])
+    got = D.join_slabs([o.numpy() for o in outs], plan, nrhs)
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
