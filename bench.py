@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--config", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--strong", action="store_true",
+                   help="strong scaling of one grid: depth-slab / mode-shard apply over the N ranks")
     return p.parse_args()
 
 
@@ -402,10 +404,104 @@ def run_ours(args):
     return 0
 
 
+# ------------------------------------------------- strong-scaling arm ----
+def run_strong(args):
+    """One grid sharded over the N ranks: each rank owns a
+    depth slab and a quadrant-mode shard of the spectra; two all-to-alls per
+    apply (NCCL; N = 1 runs the same stages through the loopback)."""
+    import torch
+    import paper_1512_06126_b200 as emie
+    from paper_1512_06126_b200 import configs
+    from paper_1512_06126_b200 import distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.config(args.config)
+    model = emie.LayeredModel(cfg.tops, cfg.sigma)
+    grid = emie.make_grid(model, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy)
+    grid.sigma_a[...] = cfg.sigma_a
+    sop = emie.assemble_operator(grid, model, cfg.omega)  # every rank; each keeps its mode shard
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, world)
+    shard = D.cuda_shard(grid, sop, plan, rank, NRHS)
+    del sop
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1234)
+    n = 3 * cfg.cells()
+    U = rng.uniform(-1, 1, (NRHS, n)) + 1j * rng.uniform(-1, 1, (NRHS, n))
+    slab = torch.from_numpy(D.slab_of(U, plan, rank, NRHS)).cuda()
+    if world > 1:
+        sysd = D.DistributedSystem(shard)
+        step = lambda: sysd.apply(slab)  # noqa: E731
+    else:
+        step = lambda: D.loopback_apply([shard], [slab])[0]  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.4)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    tmax = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    # end to end: the rank's slab from pinned host memory and back, each step
+    hin = torch.from_numpy(D.slab_of(U, plan, rank, NRHS)).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        out = (sysd.apply(hin.cuda(non_blocking=True)) if world > 1
+               else D.loopback_apply([shard], [hin.cuda(non_blocking=True)])[0])
+        hout.copy_(out)
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        slab_bytes = hin.numel() * 16
+        line = {
+            "metric": METRIC, "value": NRHS * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded config conductivity field, seeded fields)",
+            "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} sharded over {world} rank(s): "
+                                   "depth slabs + quadrant-mode shards, 2 all-to-alls per apply",
+                       "nrhs": NRHS, "slabs": plan.z, "mode_shards": plan.q},
+            "e2e": {"value": NRHS * args.e2e_steps / float(e2e_s.item()), "unit": UNIT,
+                    "h2d_bytes_per_step": slab_bytes * world, "d2h_bytes_per_step": slab_bytes * world},
+            "gpu_launches": None,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.strong:
+        return run_strong(args)
     return run_ours(args)
 
 

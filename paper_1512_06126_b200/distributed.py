@@ -120,7 +120,9 @@ class ShardedApply:
         """Scatter the slabs' columns into the full-depth spectrum of this
         rank's modes, contract them, pack the results per slab owner."""
         P, be, me = self.plan, self.be, self.rank
-        S = be.zeros((self.nrhs, P.E, 3 * P.nz))
+        # only this rank's mode columns are written (all planes, by the scatters
+        # below) and read (contraction, packs): no zero fill needed
+        S = be.empty((self.nrhs, P.E, 3 * P.nz))
         for h, buf in enumerate(recvs):
             nzh = P.nzl(h)
             be.move(buf, S, self.nrhs, me, P.E, (0, 3 * nzh, nzh, 0), (1, 3 * P.nz, P.nz, P.z[h]), nzh)
