@@ -38,7 +38,11 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "CIE operator applies/s (complex128) at 128x128x32"
+METRIC = "CIE operator applies/s (complex128) at 128x128x32"  # config 3 (the default)
+
+
+def metric_for(cfg):
+    return f"CIE operator applies/s (complex128) at {cfg.nx}x{cfg.ny}x{cfg.nz}"
 UNIT = "applies/s"
 NRHS = 2
 
@@ -164,11 +168,11 @@ def run_reference(args):
     tot = float(np.sum(times))
     value = NRHS * len(times) / tot
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_for(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
         "data": "synthetic (seeded config-3 conductivity; operator values synthetic, same shape)",
-        "config": {"workload": "cfg3 128x128x32, apply(SystemOperator), 2 polarisations",
+        "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz}, apply(SystemOperator), 2 polarisations",
                    "nrhs": NRHS, "threads": d["threads"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": d["threads"], "kind": "reference",
                          "sample": f"{len(times)} steps x {NRHS} applies at cfg3 (reference apply, "
@@ -367,15 +371,17 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_for(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded config-3 conductivity field, seeded fields)",
-            "config": {"workload": "cfg3 128x128x32 (5-layer background), apply(SystemOperator) on both "
+            "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} (5-layer background), "
+                                   "apply(SystemOperator) on both "
                                    "MT polarisations per step (nrhs=2)",
                        "nrhs": NRHS, "frequency_hz": freq if world == 1 else "one config-5 frequency per rank",
                        "operator": operator_src,
-                       "l2": "inputs larger than L2 (1.1 GB operator streamed per step)",
+                       "l2": f"inputs larger than L2 ({modes * 2 * nz * (2 * nz + 1) * 16 / 1e9:.2f} GB operator "
+                             "streamed per step)",
                        "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
             "greens_build_s": greens_s,
             "greens_build_warm_s": greens_warm_s,
@@ -478,7 +484,7 @@ def run_strong(args):
     if rank == 0:
         slab_bytes = hin.numel() * 16
         line = {
-            "metric": METRIC, "value": NRHS * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "metric": metric_for(cfg), "value": NRHS * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded config conductivity field, seeded fields)",
