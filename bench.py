@@ -306,10 +306,11 @@ def run_ours(args):
     value = world * NRHS * args.steps / (ms_max * 1e-3)
 
     # end to end through the reference-facing host-buffer C-ABI call
+    # (--e2e-steps 0 skips it, e.g. for a launch-list capture of the device steps)
     hin = torch.empty(NRHS * n, dtype=torch.complex128).pin_memory()
     hout = torch.empty(NRHS * n, dtype=torch.complex128).pin_memory()
     hin.copy_(U.cpu())
-    for _ in range(2):
+    for _ in range(2 if args.e2e_steps > 0 else 0):
         emie._check(L.emie_cu_apply_system_host(system.handle, ctypes.c_void_p(hin.data_ptr()),
                                                 ctypes.c_void_p(hout.data_ptr()), NRHS, sp))
     if dist:
@@ -323,7 +324,8 @@ def run_ours(args):
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
     if dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * NRHS * args.e2e_steps / float(e2e_s.item())
+    e2e_value = world * NRHS * args.e2e_steps / float(e2e_s.item()) if args.e2e_steps > 0 else None
+    pcie = pcie_bandwidth(hin, hout, U, W) if args.e2e_steps > 0 else None
 
     # roofline of the dominant kernel (the per-mode contraction)
     nz = cfg.nz
@@ -400,7 +402,7 @@ def run_ours(args):
                                   "frac": (flops_ct / (ct_ms * 1e-3) / 1e12) / fp64.value if fp64.value else None}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": NRHS * n * 16,
-                    "d2h_bytes_per_step": NRHS * n * 16},
+                    "d2h_bytes_per_step": NRHS * n * 16, "pcie_gbs": pcie},
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -408,6 +410,32 @@ def run_ours(args):
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def pcie_bandwidth(hin, hout, din, dout):
+    """Pinned-memory copy rates of this box (context for e2e, which moves
+    the same bytes): H2D alone, D2H alone, both at once on two streams."""
+    import torch
+    nbytes = hin.numel() * hin.element_size()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    res = {}
+    for name, fns in (("h2d", [(s1, lambda: din.copy_(hin, non_blocking=True))]),
+                      ("d2h", [(s2, lambda: hout.copy_(dout, non_blocking=True))]),
+                      ("duplex", [(s1, lambda: din.copy_(hin, non_blocking=True)),
+                                  (s2, lambda: hout.copy_(dout, non_blocking=True))])):
+        for _ in range(2):
+            for st, f in fns:
+                with torch.cuda.stream(st):
+                    f()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            for st, f in fns:
+                with torch.cuda.stream(st):
+                    f()
+        torch.cuda.synchronize()
+        res[name] = round(3 * len(fns) * nbytes / (time.perf_counter() - t0) / 1e9, 1)
+    return res
 
 
 # ------------------------------------------------- strong-scaling arm ----
