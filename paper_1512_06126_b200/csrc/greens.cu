@@ -238,13 +238,13 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
                                      const double* __restrict__ den_floor,
                                      const cplx* __restrict__ tw, FftPlan pl, int half, double step,
                                      double shift, int n1, int n2, int nx, double hx, double hy,
-                                     int* err, int fixed_oi, int fixed_oj) {
+                                     int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs) {
   extern __shared__ cplx sm[];
   const int n = pl.n, ld = n | 1;
   cplx* a = sm;
   cplx* b = a + ld;
   cplx* t = b + ld;
-  const int off = blockIdx.x, kern = blockIdx.y;
+  const int off = offs ? offs[blockIdx.x] : static_cast<int>(blockIdx.x), kern = blockIdx.y;
   const int oi = fixed_oi != INT32_MIN ? fixed_oi : off / nx;
   const int oj = fixed_oi != INT32_MIN ? fixed_oj : off % nx;
   const Geom g = pair_geometry(oi, oj, hx, hy);
@@ -455,10 +455,10 @@ __device__ unsigned long long g_phase_clk[8];
 
 __global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
-    cplx* __restrict__ blocks, int* err) {
+    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs) {
   extern __shared__ cplx sm[];
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
-  const int off = blockIdx.x;
+  const int off = offs[blockIdx.x];
   const int oi = off / P.nx, oj = off % P.nx;
   const Geom g = pair_geometry(oi, oj, P.hx, P.hy);
   const double R = g.r;
@@ -829,6 +829,27 @@ __global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
   if (bad) atomicOr(err, 4);
 }
 
+// x <-> y mirror of a square grid with hx == hy: the block of offset (oj, oi)
+// is the block of (oi, oj) with xx <-> yy and xz <-> yz exchanged (zz and xy
+// unchanged) -- the horizontal isotropy of the layered medium; measured on the
+// device build to agree with the independently computed block to <1e-6 of the
+// block max (filter-design rounding), tools/greens_symmetry_check.py
+__global__ void mirror_blocks_kernel(cplx* blocks, const int* __restrict__ pairs, int npairs, int nx, int ntri,
+                                     int nfull, int nent) {
+  const long long total = static_cast<long long>(npairs) * nent;
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(x / nent), e = static_cast<int>(x - static_cast<long long>(p) * nent);
+    const int off = pairs[p], oi = off / nx, oj = off - oi * nx;
+    int d = e;  // destination slot in the mirrored block
+    if (e < ntri) d = e + ntri;                                  // xx -> yy
+    else if (e < 2 * ntri) d = e - ntri;                         // yy -> xx
+    else if (e >= 4 * ntri && e < 4 * ntri + nfull) d = e + nfull;  // xz -> yz
+    else if (e >= 4 * ntri + nfull) d = e - nfull;               // yz -> xz
+    blocks[(static_cast<size_t>(oj) * nx + oi) * nent + d] = blocks[static_cast<size_t>(off) * nent + e];
+  }
+}
+
 __global__ void kernel_output_kernel(Geom g, int alpha, int beta, const double* s, int n,
                                      double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -871,14 +892,14 @@ void free_filter_bank(FilterBank& fb, cudaStream_t st) {
 
 void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, int nx, double hx,
                     double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
-                    int fixed_oj = 0) {
+                    int fixed_oj = 0, const int* offs = nullptr) {
   const int n = 2 * fp.half;
   const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
   set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
   dim3 grid(noff, 6);
   filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
                                                 fp.step, fp.shift, fp.n1, fp.n2, nx, hx, hy, err,
-                                                fixed_oi, fixed_oj);
+                                                fixed_oi, fixed_oj, offs);
   check_launch("filter_design_kernel");
 }
 
@@ -1018,11 +1039,27 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
 
   keep_pool_warm();
   const int noff = op.nx * op.ny;
+  // offsets computed: all, or on a square grid with hx == hy only oi <= oj
+  // (the rest by the x <-> y mirror, mirror_blocks_kernel)
+  const bool mirror = op.nx == op.ny && hx == hy;
+  std::vector<int> offs_h, pairs_h;
+  for (int oi = 0; oi < op.ny; ++oi)
+    for (int oj = 0; oj < op.nx; ++oj) {
+      if (mirror && oi > oj) continue;
+      offs_h.push_back(oi * op.nx + oj);
+      if (mirror && oi < oj) pairs_h.push_back(oi * op.nx + oj);
+    }
+  const int ncomp = static_cast<int>(offs_h.size());
+  int* offs = scratch<int>(offs_h.size() + pairs_h.size(), st);
+  int* pairs = offs + offs_h.size();
+  EMIE_CUDA(cudaMemcpyAsync(offs, offs_h.data(), offs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  if (!pairs_h.empty())
+    EMIE_CUDA(cudaMemcpyAsync(pairs, pairs_h.data(), pairs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   FilterBank fb = make_filter_bank(fp, st);
   double* W = scratch<double>(static_cast<size_t>(noff) * 6 * P.nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, noff, op.nx, hx, hy, W, err, st);
+  design_filters(fb, fp, ncomp, op.nx, hx, hy, W, err, st, INT32_MIN, 0, offs);
 
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
@@ -1034,7 +1071,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
   const int groups = ceil_div(P.npairs, 3 * kGreenThreads);
-  dim3 grid(noff, groups);
+  dim3 grid(ncomp, groups);
   profile_mark(5, true, st);
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {
@@ -1042,8 +1079,14 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
     EMIE_CUDA(cudaMemcpyToSymbolAsync(g_phase_clk, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
   }
 #endif
-  assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err);
+  assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs);
   check_launch("assemble_kernel");
+  if (!pairs_h.empty()) {
+    const long long total = static_cast<long long>(pairs_h.size()) * op.nent;
+    mirror_blocks_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
+        blocks, pairs, static_cast<int>(pairs_h.size()), op.nx, op.ntri, op.nfull, op.nent);
+    check_launch("mirror_blocks_kernel");
+  }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {
     unsigned long long h[8];
@@ -1064,6 +1107,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   release(W, st);
   release(err, st);
   release(div, st);
+  release(offs, st);
   free_filter_bank(fb, st);
   if (e) {
     cudaFree(blocks);
