@@ -299,7 +299,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         if (j >= kBlkStages) mbar_wait(bempty + bs, static_cast<uint32_t>((j / kBlkStages - 1) & 1));
         const uint32_t blkbytes = nentD * sizeof(cplx);
         // blocks of the modes after the SMEM stages go to L2 ahead of their copy
-        for (int d = (j == 0 ? kBlkStages : kL2Ahead); d <= kL2Ahead; ++d) {
+        for (int d = (j == 0 ? kBlkStages : kL2Ahead); kL2Ahead > 0 && d <= kL2Ahead; ++d) {
           const int qp = qm + d * G;
           if (qp < q1) bulk_prefetch_l2(op + static_cast<size_t>(qp - qbase) * nentD, blkbytes);
         }
