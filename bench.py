@@ -287,11 +287,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    marks[0].record(stream)
+    for i in range(args.steps):
         step()
+        marks[i + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    per_step = np.array([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)])
     if dist:
         dist.barrier()
     launches = int(L.emie_cu_launch_count())
@@ -385,6 +389,9 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 ({modes * 2 * nz * (2 * nz + 1) * 16 / 1e9:.2f} GB operator "
                              "streamed per step)",
                        "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
+            "step_ms_percentiles": {"p10": round(float(np.percentile(per_step, 10)), 4),
+                                    "p50": round(float(np.percentile(per_step, 50)), 4),
+                                    "p90": round(float(np.percentile(per_step, 90)), 4)},
             "greens_build_s": greens_s,
             "greens_build_warm_s": greens_warm_s,
             "greens_stage_ms": greens_stage,
