@@ -95,14 +95,19 @@ __global__ void __launch_bounds__(kRedThreads) dots_kernel(const cplx* __restric
   }
 }
 
-// out[i] = sum over blocks (in block order) of partial[b][i]
-__global__ void finalize_kernel(const double* partial, int nblocks, int pstride, int nvals,
-                                double* out) {
-  for (int i = threadIdx.x; i < nvals; i += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partial[static_cast<std::size_t>(b) * pstride + i];
-    out[i] = s;
-  }
+// out[i] = sum over blocks of partial[b][i]: block i, thread t sums blocks
+// b = t, t + 256, ... in order, then a fixed shuffle / warp tree (deterministic)
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* partial, int nblocks, int pstride,
+                                                               int nvals, double* out) {
+  const int i = blockIdx.x;
+  if (i >= nvals) return;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += kFinThreads) s += partial[static_cast<std::size_t>(b) * pstride + i];
+  double v[1] = {s};
+  __shared__ double tot[1];
+  block_sum<1>(v, tot);
+  if (threadIdx.x == 0) out[i] = tot[0];
 }
 
 // w[e] -= sum_l h[l] V_l[e]; optional per-block |w|^2 partial at pstride slot 0
@@ -212,13 +217,13 @@ struct Workspace {
   }
   // finalize partial sums; when norm_slot_src >= 0 the |w|^2 lives at 2*nv
   void finalize(int nvals, int) {
-    finalize_kernel<<<1, 128, 0, st>>>(partial, G, pstride, nvals, dvals);
+    finalize_kernel<<<nvals, kFinThreads, 0, st>>>(partial, G, pstride, nvals, dvals);
     check_launch("finalize_kernel");
   }
   double norm_of(const cplx* w) {
     dots_kernel<<<G, kRedThreads, 0, st>>>(w, 0, 0, w, n, partial, pstride, 1);
     check_launch("dots_kernel");
-    finalize_kernel<<<1, 128, 0, st>>>(partial, G, pstride, 1, dvals);
+    finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, G, pstride, 1, dvals);
     check_launch("finalize_kernel");
     fetch(1);
     return std::sqrt(hpin[0]);
@@ -245,6 +250,10 @@ struct Rhs {
   std::vector<cd> h, g, rot_s;
   std::vector<double> rot_c, history;
   emie_cu_report rep{1, 0, 0.0, 0};
+  // finalized reductions of the current step (device) and their pinned host
+  // mirror: [0] pass-1 dots + |w|^2, [1] pass-2 dots, [2] the new norm
+  double* dv = nullptr;
+  double* hp = nullptr;
 };
 
 }  // namespace
@@ -266,12 +275,21 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
   cplx* Wall = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
   cplx* Bin = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
   double* ycoef = scratch<double>(2 * (m + 1), st);
-  double* hcoef = scratch<double>(2 * (m + 1), st);
 
   std::vector<Rhs> rs(nrhs);
+  const int ps = ws.pstride;
+  double* dv_all = scratch<double>(static_cast<std::size_t>(nrhs) * 3 * ps, st);
+  struct Pinned {  // freed on every exit path
+    double* p = nullptr;
+    ~Pinned() { cudaFreeHost(p); }
+  } pinned;
+  EMIE_CUDA(cudaMallocHost(&pinned.p, static_cast<std::size_t>(nrhs) * 3 * ps * sizeof(double)));
+  double* hp_all = pinned.p;
   for (int i = 0; i < nrhs; ++i) {
     Rhs& R = rs[i];
     R.idx = i;
+    R.dv = dv_all + static_cast<std::size_t>(i) * 3 * ps;
+    R.hp = hp_all + static_cast<std::size_t>(i) * 3 * ps;
     R.x = d_x + i * n;
     R.b = d_rhs + i * n;
     R.r = Rall + i * n;
@@ -342,16 +360,50 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     }
     apply_b(op, Bin, Wall, static_cast<int>(req.size()), &sys, st);
+    // enqueue every right-hand side's reductions (stream ordered, results
+    // copied to pinned memory without waiting), then one synchronisation
+    auto to_host = [&](Rhs& R, int slot, int nvals) {
+      EMIE_CUDA(cudaMemcpyAsync(R.hp + slot * ps, R.dv + slot * ps, nvals * sizeof(double), cudaMemcpyDeviceToHost,
+                                st));
+    };
     for (std::size_t q = 0; q < req.size(); ++q) {
       Rhs& R = *req[q];
       cplx* w = Wall + q * n;
       if (R.phase == Rhs::kResidual) {  // cie.cpp:217-229
         residual_kernel<<<ws.G, kRedThreads, 0, st>>>(R.r, R.b, w, n, ws.partial);
         check_launch("residual_kernel");
-        finalize_kernel<<<1, 128, 0, st>>>(ws.partial, ws.G, 1, 1, ws.dvals);
+        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, R.dv + 2 * ps);
         check_launch("finalize_kernel");
-        ws.fetch(1);
-        R.rnorm = std::sqrt(ws.hpin[0]);
+        to_host(R, 2, 1);
+        continue;
+      }
+      const int j = R.j;
+      // CGS2 pass 1: dots against v_0..v_j plus |w|^2, then w -= V h
+      dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 1);
+      check_launch("dots_kernel");
+      finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, R.dv);
+      check_launch("finalize_kernel");
+      to_host(R, 0, 2 * (j + 1) + 1);
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, R.dv, n, nullptr);
+      check_launch("update_kernel");
+      // pass 2, with the new |w|^2
+      dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
+      check_launch("dots_kernel");
+      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), R.dv + ps);
+      check_launch("finalize_kernel");
+      to_host(R, 1, 2 * (j + 1));
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, R.dv + ps, n, ws.partial);
+      check_launch("update_kernel");
+      finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, R.dv + 2 * ps);
+      check_launch("finalize_kernel");
+      to_host(R, 2, 1);
+    }
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    for (std::size_t q = 0; q < req.size(); ++q) {
+      Rhs& R = *req[q];
+      cplx* w = Wall + q * n;
+      if (R.phase == Rhs::kResidual) {
+        R.rnorm = std::sqrt(R.hp[2 * ps]);
         if (R.rnorm / R.bnorm <= tol) {
           R.rep.status = 0;
           finish(R);
@@ -367,24 +419,10 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       ++R.iter;
       const int j = R.j;
       cd* hj = R.h.data() + static_cast<std::size_t>(j) * (m + 1);
-      // pass 1: dots against v_0..v_j plus |w|^2
-      ws.dots(R.V, n, j + 1, w, true);
-      ws.fetch(2 * (j + 1) + 1);
-      const double wn0 = std::sqrt(ws.hpin[2 * (j + 1)]);
-      for (int i = 0; i <= j; ++i) hj[i] += cd(ws.hpin[2 * i], ws.hpin[2 * i + 1]);
-      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, ws.dvals, n, nullptr);
-      check_launch("update_kernel");
-      // pass 2
-      ws.dots(R.V, n, j + 1, w, false);
-      ws.fetch(2 * (j + 1));
-      for (int i = 0; i <= j; ++i) hj[i] += cd(ws.hpin[2 * i], ws.hpin[2 * i + 1]);
-      EMIE_CUDA(cudaMemcpyAsync(hcoef, ws.dvals, 2 * (j + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, hcoef, n, ws.partial);
-      check_launch("update_kernel");
-      finalize_kernel<<<1, 128, 0, st>>>(ws.partial, ws.G, 1, 1, ws.dvals);
-      check_launch("finalize_kernel");
-      ws.fetch(1);
-      const double hnext = std::sqrt(ws.hpin[0]);
+      const double wn0 = std::sqrt(R.hp[2 * (j + 1)]);
+      for (int i = 0; i <= j; ++i) hj[i] += cd(R.hp[2 * i], R.hp[2 * i + 1]);
+      for (int i = 0; i <= j; ++i) hj[i] += cd(R.hp[ps + 2 * i], R.hp[ps + 2 * i + 1]);
+      const double hnext = std::sqrt(R.hp[2 * ps]);
       for (int i = 0; i < j; ++i) {
         const cd t = R.rot_c[i] * hj[i] + R.rot_s[i] * hj[i + 1];
         hj[i + 1] = -std::conj(R.rot_s[i]) * hj[i] + R.rot_c[i] * hj[i + 1];
@@ -440,7 +478,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
   release(Wall, st);
   release(Bin, st);
   release(ycoef, st);
-  release(hcoef, st);
+  release(dv_all, st);
   EMIE_CUDA(cudaStreamSynchronize(st));
 }
 
