@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "operator.cuh"
 #include "tma.cuh"
 
@@ -335,73 +337,65 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   // each quarter-warp reads rows r and r + nz/2, which the MMA layout puts in
   // disjoint banks (operator.cuh).
   const int fr = lane >> 2, fc = lane & 3;
-  const int a = warp / (NZ / 8), m = warp - a * (NZ / 8);
+  const int a_rt = warp / (NZ / 8), m = warp - a_rt * (NZ / 8);
   const int k = 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
-  const int plane = a * NZ + k;
-  const unsigned long long zsg = a == 2 ? 0x8000000000000000ull : 0ull;
-  // per-lane coefficient offsets of every k step: mode independent
-  uint32_t off[nk];
+  // The warp's component a is a template constant inside consume(): the
+  // zx / zy negation (-xz^T, -yz^T: the z tile, b < 2) is then a compile-time
+  // operand sign that the DMMA applies for free.
+  auto consume = [&](auto AC) {
+    constexpr int a = decltype(AC)::value;
+    const int plane = a * NZ + k;
+    // per-lane coefficient offsets of every k step: mode independent
+    uint32_t off[nk];
 #pragma unroll
-  for (int ks = 0; ks < nk; ++ks) {
-    const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
-    off[ks] = __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) & 0x7fffffffu;
-  }
-  int j = 0;
-  for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
-    const int bs = j % kBlkStages, us = j % kUStages;
-    mbar_wait(bfull + bs, static_cast<uint32_t>((j / kBlkStages) & 1));
-    mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
-    const cplx* blk = blkbuf + bs * nentD;
-    const cplx* U = ubuf + us * 8 * ldu + fr * ldu + fc;
-    double p1[kAcc][2] = {}, p2[kAcc][2] = {}, p3[kAcc][2] = {};
-    // operands PD k-steps ahead of their MMAs (SMEM latency off the DMMA chain)
-    constexpr int PD = 6;
-    cplx av[PD], bv[PD];
-#pragma unroll
-    for (int ks = 0; ks < PD; ++ks) {
-      av[ks] = blk[off[ks]];
-      bv[ks] = U[4 * ks];
+    for (int ks = 0; ks < nk; ++ks) {
+      const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
+      off[ks] = __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) & 0x7fffffffu;
     }
+    int j = 0;
+    for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
+      const int bs = j % kBlkStages, us = j % kUStages;
+      mbar_wait(bfull + bs, static_cast<uint32_t>((j / kBlkStages) & 1));
+      mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
+      const cplx* blk = blkbuf + bs * nentD;
+      const cplx* U = ubuf + us * 8 * ldu + fr * ldu + fc;
+      double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+      // operands PD k-steps ahead of their MMAs (SMEM latency off the DMMA chain)
+      constexpr int PD = 6;
+      cplx av[PD], bv[PD];
 #pragma unroll
-    for (int ks = 0; ks < (EMIE_CT_EXPERIMENT == 1 ? 0 : nk); ++ks) {
-      const cplx bu = bv[ks % PD];  // B[k = fc][col = fr]
-      const cplx mv = av[ks % PD];
-      if (ks + PD < nk) {
-        av[ks % PD] = blk[off[ks + PD]];
-        bv[ks % PD] = U[4 * (ks + PD)];
+      for (int ks = 0; ks < PD; ++ks) {
+        av[ks] = blk[off[ks]];
+        bv[ks] = U[4 * ks];
       }
-      // zx / zy (-xz^T, -yz^T): the z tile flips the sign of the B fragment for b < 2
-      const unsigned long long sg = (4 * ks) / NZ < 2 ? zsg : 0ull;
-      const double br = __longlong_as_double(__double_as_longlong(bu.re) ^ sg);
-      const double bi = __longlong_as_double(__double_as_longlong(bu.im) ^ sg);
-      const double bss = __longlong_as_double(__double_as_longlong(bu.re + bu.im) ^ sg);
-      const int h = kAcc == 1 ? 0 : (ks & 1);
-      dmma(p1[h][0], p1[h][1], mv.re, br);
-      dmma(p2[h][0], p2[h][1], mv.im, bi);
-      dmma(p3[h][0], p3[h][1], mv.re + mv.im, bss);
-    }
-    double q1[2], q2[2], q3[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      q1[h] = p1[0][h];
-      q2[h] = p2[0][h];
-      q3[h] = p3[0][h];
-#pragma unroll
-      for (int c = 1; c < kAcc; ++c) {
-        q1[h] += p1[c][h];
-        q2[h] += p2[c][h];
-        q3[h] += p3[c][h];
+      for (int ks = 0; ks < (EMIE_CT_EXPERIMENT == 1 ? 0 : nk); ++ks) {
+        const cplx bu = bv[ks % PD];  // B[k = fc][col = fr]
+        const cplx mv = av[ks % PD];
+        if (ks + PD < nk) {
+          av[ks % PD] = blk[off[ks + PD]];
+          bv[ks % PD] = U[4 * (ks + PD)];
+        }
+        constexpr bool kz = a == 2;
+        const bool neg = kz && (4 * ks) / NZ < 2;  // compile time after unrolling
+        const double bs_ = bu.re + bu.im;
+        dmma(p1[0], p1[1], mv.re, neg ? -bu.re : bu.re);
+        dmma(p2[0], p2[1], mv.im, neg ? -bu.im : bu.im);
+        dmma(p3[0], p3[1], mv.re + mv.im, neg ? -bs_ : bs_);
       }
+      // block stage reads are complete (the DMMAs consumed them): release it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bempty + bs);
+      const long long cb0 = colbase[us * 8 + 2 * fc], cb1 = colbase[us * 8 + 2 * fc + 1];
+      if (cb0 >= 0) S[cb0 + plane] = cplx{p1[0] - p2[0], p3[0] - p1[0] - p2[0]};
+      if (cb1 >= 0) S[cb1 + plane] = cplx{p1[1] - p2[1], p3[1] - p1[1] - p2[1]};
+      __syncwarp();
+      if (lane == 0) mbar_arrive(uempty + us);  // input columns and their table
     }
-    // block stage reads are complete (the DMMAs consumed them): release it
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bempty + bs);
-    const long long cb0 = colbase[us * 8 + 2 * fc], cb1 = colbase[us * 8 + 2 * fc + 1];
-    if (cb0 >= 0) S[cb0 + plane] = cplx{q1[0] - q2[0], q3[0] - q1[0] - q2[0]};
-    if (cb1 >= 0) S[cb1 + plane] = cplx{q1[1] - q2[1], q3[1] - q1[1] - q2[1]};
-    __syncwarp();
-    if (lane == 0) mbar_arrive(uempty + us);  // input columns and their table
-  }
+  };
+  if (a_rt == 0) consume(std::integral_constant<int, 0>{});
+  else if (a_rt == 1) consume(std::integral_constant<int, 1>{});
+  else consume(std::integral_constant<int, 2>{});
 }
 
 void set_smem(const void* fn, size_t bytes) {
