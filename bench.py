@@ -278,7 +278,7 @@ def run_ours(args):
     ms5 = np.zeros(5)
     cnt5 = np.zeros(5, np.int64)
     emie._check(L.emie_cu_profile_collect(ms5.ctypes.data, cnt5.ctypes.data, 5))  # drain
-    emie._check(L.emie_cu_profile_enable(1))
+    emie._check(L.emie_cu_profile_enable(0))  # the timed loop runs uninstrumented
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.4)
@@ -301,6 +301,13 @@ def run_ours(args):
         dist.barrier()
     launches = int(L.emie_cu_launch_count())
     clk = clocks.stop()
+    # stage breakdown (and the contraction time of the roofline) from a
+    # separate instrumented pass: the library's per-stage CUDA events cost ~5 %
+    # of the step, so they stay out of the timed loop
+    emie._check(L.emie_cu_profile_enable(1))
+    for _ in range(max(3, min(args.steps, 10))):
+        step()
+    torch.cuda.synchronize()
     emie._check(L.emie_cu_profile_enable(0))
     emie._check(L.emie_cu_profile_collect(ms5.ctypes.data, cnt5.ctypes.data, 5))
     ms = e0.elapsed_time(e1)
@@ -340,6 +347,8 @@ def run_ours(args):
         rhs = np.stack([NF.build_rhs(cfg.tops, cfg.sigma, cfg.breaks, cfg.nx, cfg.ny, omega, p).reshape(-1)
                         for p in ("x", "y")])
         d_rhs = torch.from_numpy(rhs.reshape(-1)).cuda()
+        # warm the stream-ordered pool for the (restart + 1)-vector bases first
+        emie.fgmres_system(system, d_rhs, emie.SolverConfig(tol=1e-6, restart=40, max_iters=1))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         _, reps = emie.fgmres_system(system, d_rhs, emie.SolverConfig(tol=1e-6, restart=40, max_iters=500))
