@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -164,6 +166,46 @@ System::~System() {
   cudaFree(s);
   cudaFree(r1);
   cudaFree(r2);
+}
+
+int sm_count() {
+  static thread_local int dev_cached = -1, sms = 0;
+  int dev = 0;
+  EMIE_CUDA(cudaGetDevice(&dev));
+  if (dev != dev_cached) {
+    EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+int resident_ctas(const void* fn, int threads, std::size_t smem) {
+  struct Key {
+    int dev;
+    const void* fn;
+    int threads;
+    std::size_t smem;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, fn, threads, smem) < std::tie(o.dev, o.fn, o.threads, o.smem);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  int dev = 0;
+  EMIE_CUDA(cudaGetDevice(&dev));
+  const Key key{dev, fn, threads, smem};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  EMIE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  per_sm = std::max(1, per_sm);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = per_sm;
+  return per_sm;
 }
 
 // Scratch comes from the stream-ordered pool; by default the pool trims to

@@ -893,13 +893,8 @@ bool stream_ok(bool p2, int n, int nin) { return p2 && n >= 32 && n <= kStreamEl
 template <int N, class P>
 void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
   const size_t smem = (kStreamBufs * static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx);
-  const void* fn = reinterpret_cast<const void*>(stream_fft_kernel<N, P>);
-  set_smem(fn, smem);
-  int dev = 0, sms = 0, per_sm = 0;
-  EMIE_CUDA(cudaGetDevice(&dev));
-  EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_fft_kernel<N, P>, kStreamThreads, smem));
-  const int grid = std::max(1, std::min(ntiles, sms * std::max(1, per_sm)));
+  const int per_sm = resident_ctas(reinterpret_cast<const void*>(stream_fft_kernel<N, P>), kStreamThreads, smem);
+  const int grid = std::max(1, std::min(ntiles, sm_count() * per_sm));
   stream_fft_kernel<N, P><<<grid, kStreamThreads, smem, st>>>(p, tw);
 }
 
@@ -914,13 +909,9 @@ void launch_tma(const P& p, int ntiles, const cplx* tw, cudaStream_t st, const c
   constexpr int N = 256;
   const size_t smem = NST * static_cast<size_t>(P::kStageBytes) +
                       (static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx) + NST * sizeof(uint64_t);
-  const void* fn = reinterpret_cast<const void*>(stream_tma_kernel<N, P, NST>);
-  set_smem(fn, smem);
-  int dev = 0, sms = 0, per_sm = 0;
-  EMIE_CUDA(cudaGetDevice(&dev));
-  EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_tma_kernel<N, P, NST>, kStreamThreads, smem));
-  const int grid = std::max(1, std::min(ntiles, sms * std::max(1, per_sm)));
+  const int per_sm =
+      resident_ctas(reinterpret_cast<const void*>(stream_tma_kernel<N, P, NST>), kStreamThreads, smem);
+  const int grid = std::max(1, std::min(ntiles, sm_count() * per_sm));
   stream_tma_kernel<N, P, NST><<<grid, kStreamThreads, smem, st>>>(p, tw);
   check_launch(what);
 }

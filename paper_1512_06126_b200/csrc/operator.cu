@@ -417,9 +417,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
     fail(EMIE_CU_OUT_OF_RANGE, "contraction: quadrant modes outside the stored range");
   if (q0 == q1) return;
   const int np = 3 * op.nz;
-  int sms = 0, dev = 0;
-  EMIE_CUDA(cudaGetDevice(&dev));
-  EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int sms = sm_count();
   const int nmodes = q1 - q0;
   for (int r0 = 0; r0 < nrhs; r0 += 2) {
     const int g = std::min(2, nrhs - r0);
@@ -429,10 +427,8 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
                           kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
                           kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
       auto launch = [&](auto kern, int warps) {
-        set_smem(reinterpret_cast<const void*>(kern), smem);
-        int per_sm = 1;
-        EMIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (warps + 1) * 32, smem));
-        const int grid = std::max(1, std::min(sms * std::max(1, per_sm), nmodes));
+        const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
+        const int grid = std::max(1, std::min(sms * per_sm, nmodes));
         kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
                                                    g, op.nentD);
       };

@@ -111,6 +111,13 @@ void kernel_output_host(int oi, int oj, double hx, double hy, int alpha, int bet
 void design_offset_filters_host(int oi, int oj, double hx, double hy, const FilterParams& fp,
                                 double* w, double* lam);
 
+// launch configuration cached per (device, kernel, threads, dynamic SMEM)
+// (capi.cu): sets the SMEM opt-in once and returns the resident CTAs per SM;
+// the hot paths launch the same kernels every apply, so these host queries
+// stay out of the per-apply cost
+int resident_ctas(const void* fn, int threads, std::size_t smem);
+int sm_count();
+
 // stage profiling (capi.cu): no-ops unless emie_cu_profile_enable(1)
 void profile_mark(int stage, bool begin, cudaStream_t st);
 
