@@ -598,11 +598,13 @@ struct Half {
 // x forward: tile = RT rows iy0.. of plane pr (nrhs*np planes); r2 on load
 struct FxStream {
   static constexpr bool kInverse = false, kTFast = true;
-  static constexpr int kStageBytes = 8 * 128 * 16;  // N = 256: 8 rows of <= 128 points
+  static constexpr int kRowBytes = 8 * 128 * 16;     // N = 256: 8 rows of <= 128 points
+  static constexpr int kStageBytes = 2 * kRowBytes;  // u rows, then the matching r2 rows
   const cplx* u;
   const cplx* r2;
   cplx* T;
   int nx, ny, nz, np, ex, tpp, nplanes, nin;
+  bool r2_staged;  // TMA path: r2 arrives with the tile (no per-thread loads)
   struct Ops {
     cplx r2v[kStreamPre];
     cplx* dst;  // T at (r, mx = 0, plane, iy0)
@@ -629,7 +631,7 @@ struct FxStream {
     const int r = pr / np, plane = pr - r * np;
     o.rows = min(RT, ny - iy0);
     o.dst = T + ((static_cast<size_t>(r) * ex) * np + plane) * ny + iy0;
-    if (!r2) return;
+    if (!r2 || r2_staged) return;
     const int iz = plane % nz;
     const int t = threadIdx.x / M, j = threadIdx.x % M;
     const int iy = min(iy0 + t, ny - 1);
@@ -641,18 +643,26 @@ struct FxStream {
     }
   }
   __device__ cplx pre(const Ops& o, int, int r, int, cplx x) const {
-    return (r2 && r < kStreamPre) ? o.r2v[r] * x : x;
+    return (r2 && !r2_staged && r < kStreamPre) ? o.r2v[r] * x : x;
   }
-  // TMA staging: the tile's rows are one contiguous run of u
+  // TMA staging: the tile's rows are one contiguous run of u, the matching
+  // rows of r2 (cells of plane iz) another
   template <int N>
   __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
     constexpr int RT = Geo<N>::ntr;
     const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
     const uint32_t bytes = static_cast<uint32_t>(min(RT, ny - iy0) * nx) * sizeof(cplx);
-    mbar_expect_tx(bar, bytes);
+    mbar_expect_tx(bar, r2 ? 2 * bytes : bytes);
     bulk_g2s(stg, u + (static_cast<size_t>(pr) * ny + iy0) * nx, bytes, bar);
+    if (r2) {
+      const int iz = (pr % np) % nz;
+      bulk_g2s(stg + kRowBytes / sizeof(cplx), r2 + (static_cast<size_t>(iz) * ny + iy0) * nx, bytes, bar);
+    }
   }
-  __device__ cplx staged(const cplx* stg, int t, int jj) const { return stg[t * nx + jj]; }
+  __device__ cplx staged(const cplx* stg, int t, int jj) const {
+    const cplx x = stg[t * nx + jj];
+    return r2 ? stg[kRowBytes / sizeof(cplx) + t * nx + jj] * x : x;
+  }
   // T[r][mx][plane][iy]: lanes t (= iy) fastest, 128 B runs per mx
   template <int N>
   __device__ void emit(const Ops& o, int t, int mx, int, int, cplx v) const {
@@ -1008,6 +1018,7 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.u = d_in; p.r2 = r2; p.T = T;
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
+    p.r2_staged = op.ex == 256;
     if (op.ex == 256) launch_tma<FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
     else launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_fx");
   } else {
