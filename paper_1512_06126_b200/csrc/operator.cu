@@ -68,27 +68,37 @@ __device__ __forceinline__ ModeCols mode_cols(int qm, int qx, int ex, int ey) {
 template <int CB>
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     contract_kernel(const cplx* __restrict__ op, cplx* S, int nz, int nsd, int nentD, int ex,
-                    int ey, int qx, int q0, int q1, int qbase, int nrhs) {
+                    int ey, int qx, int q0, int q1, int qbase, int nrhs, int pair) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = 3 * nz;
   const size_t colbytes = static_cast<size_t>(np) * sizeof(cplx);
-  // per warp: mbarriers[2] then two buffers of CB columns
-  const int wpb = blockDim.x >> 5;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw) + 2 * warp;
-  cplx* ubase = reinterpret_cast<cplx*>(smraw + 16 * wpb) + static_cast<size_t>(warp) * 2 * CB * np;
+  // pair = 1 (nz > 32): a warp pair shares a mode and its input buffers, each
+  // warp one 32-row half; the pair walks the diagonals in the same order, so
+  // the transposed reads of a diagonal (t and nz - t, adjacent in the walk)
+  // hit L1 instead of coming back from L2/HBM a whole pass later.
+  const int group = pair ? warp >> 1 : warp, role = pair ? warp & 1 : 0;
+  const int ngroups = (blockDim.x >> 5) >> pair;
+  // per group: mbarriers[2] then two buffers of CB columns
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw) + 2 * group;
+  cplx* ubase = reinterpret_cast<cplx*>(smraw + 16 * ngroups) + static_cast<size_t>(group) * 2 * CB * np;
   const size_t E = static_cast<size_t>(ex) * ey;
-  const int gw = blockIdx.x * wpb + warp, nw = gridDim.x * wpb;
-  if (lane == 0) {
+  const int gw = blockIdx.x * ngroups + group, nw = gridDim.x * ngroups;
+  if (lane == 0 && role == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = lane; i < 2 * CB * np; i += 32) ubase[i] = cplx{0.0, 0.0};
-  __syncwarp();
+  if (role == 0)
+    for (int i = lane; i < 2 * CB * np; i += 32) ubase[i] = cplx{0.0, 0.0};
+  __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  auto group_sync = [&]() {
+    if (pair) asm volatile("bar.sync %0, 64;" ::"r"(1 + group) : "memory");
+    else __syncwarp();
+  };
   auto issue = [&](int qm, int buf) {
-    if (lane == 0) {
+    if (lane == 0 && role == 0) {
       const ModeCols mc = mode_cols(qm, qx, ex, ey);
       const int ncol = mc.nmir * nrhs;
       mbar_expect_tx(mbar + buf, static_cast<uint32_t>(ncol * colbytes));
@@ -119,7 +129,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     const cplx* Dxy = blk + 3 * ntri;
     const cplx* Dxz = blk + 4 * ntri;
     const cplx* Dyz = Dxz + nz * nz;
-    for (int kb = 0; kb < nz; kb += 32) {
+    for (int kb = pair ? 32 * role : 0; kb < nz; kb += pair ? nz : 32) {
       const int k = kb + lane;
       const int kc = k < nz ? k : 0;
       cplx ax[CB], ay[CB], az[CB];
@@ -201,7 +211,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
       }
     }
     // this buffer is refilled (async proxy) after the next iteration's wait
-    __syncwarp();
+    group_sync();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
 }
@@ -439,19 +449,23 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
       continue;
     }
     const int CB = g == 2 ? 8 : 4;
-    // two input buffers per warp; as many warps as 220 KB of SMEM holds
-    const size_t per_warp = 16 + 2 * static_cast<size_t>(CB) * np * sizeof(cplx);
-    const int wpb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(kCtWarps, (220u << 10) / per_warp)));
-    const size_t smem = per_warp * wpb;
-    const int grid = std::max(1, std::min(sms, ceil_div(nmodes, wpb)));
+    // nz in (32, 64]: warp pairs, one 32-row half each
+    const int pair = (op.nz > 32 && op.nz <= 64) ? 1 : 0;
+    // two input buffers per warp group; as many groups as 220 KB of SMEM holds
+    const size_t per_group = 16 + 2 * static_cast<size_t>(CB) * np * sizeof(cplx);
+    const int groups = static_cast<int>(
+        std::max<size_t>(1, std::min<size_t>(kCtWarps >> pair, (220u << 10) / per_group)));
+    const int wpb = groups << pair;
+    const size_t smem = per_group * groups;
+    const int grid = std::max(1, std::min(sms, ceil_div(nmodes, groups)));
     if (CB == 8) {
       set_smem(reinterpret_cast<const void*>(contract_kernel<8>), smem);
       contract_kernel<8><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
-                                                       q0, q1, op.qbase, g);
+                                                       q0, q1, op.qbase, g, pair);
     } else {
       set_smem(reinterpret_cast<const void*>(contract_kernel<4>), smem);
       contract_kernel<4><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
-                                                       q0, q1, op.qbase, g);
+                                                       q0, q1, op.qbase, g, pair);
     }
     check_launch("contract_kernel");
   }
