@@ -453,7 +453,13 @@ __device__ unsigned long long g_phase_clk[8];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kGreenThreads, 1) assemble_kernel(
+#ifndef EMIE_GREEN_MINB
+#define EMIE_GREEN_MINB 1  // CTAs per SM the register budget targets
+#endif
+#ifndef EMIE_GREEN_SMEM_KB
+#define EMIE_GREEN_SMEM_KB 200  // SMEM budget of the lambda chunk buffers
+#endif
+__global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
     cplx* __restrict__ blocks, int* err, const int* __restrict__ offs) {
   extern __shared__ cplx sm[];
@@ -1032,7 +1038,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   {
     const size_t per_lambda = (15 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
                               8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
-    int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (200u << 10) / per_lambda)));
+    int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (size_t{EMIE_GREEN_SMEM_KB} << 10) / per_lambda)));
     if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
     P.LC = lcm;
   }
