@@ -370,7 +370,11 @@ def run_ours(args):
     modes = sop.qx * sop.qy
     E = sop.ex * sop.ey
     nent = 2 * nz * (2 * nz + 1)
-    bytes_ct = modes * nent * 16 + 2 * NRHS * E * 3 * nz * 16
+    # blocks read per launch: every quadrant mode, or with the x <-> y symmetry
+    # of a square grid (hx == hy) only the octant qmx <= qmy (operator.cu)
+    octant = emie.xy_symmetric(sop)
+    blocks_read = sop.qx * (sop.qx + 1) // 2 if octant else modes
+    bytes_ct = blocks_read * nent * 16 + 2 * NRHS * E * 3 * nz * 16
     flops_ct = NRHS * 72.0 * nz * nz * E
     ct_ms = ms5[2] / max(1, cnt5[2])
     hbm, hbm_kind = peaks()
@@ -420,9 +424,10 @@ def run_ours(args):
                                    "MT polarisations per step (nrhs=2)",
                        "nrhs": NRHS, "frequency_hz": freq if world == 1 else "one config-5 frequency per rank",
                        "operator": operator_src,
-                       "l2": f"inputs larger than L2 ({modes * 2 * nz * (2 * nz + 1) * 16 / 1e9:.2f} GB operator "
+                       "l2": f"inputs larger than L2 ({blocks_read * nent * 16 / 1e9:.2f} GB operator "
                              "streamed per step)",
-                       "embedding": [sop.ex, sop.ey], "quadrant_modes": modes},
+                       "embedding": [sop.ex, sop.ey], "quadrant_modes": modes,
+                       "contraction_blocks_read": blocks_read, "octant": octant},
             "solve": solve,
             "step_ms_percentiles": {"p10": round(float(np.percentile(per_step, 10)), 4),
                                     "p50": round(float(np.percentile(per_step, 50)), 4),

@@ -87,6 +87,15 @@ int emie_cu_operator_from_spectra(int nx, int ny, int nz, double omega, const do
 /* dims = {nx, ny, nz, ex, ey, qx, qy}; omega */
 int emie_cu_operator_dims(emie_cu_operator op, int dims[7], double* omega);
 
+/* x <-> y transposition symmetry of the operator (no reference counterpart:
+ * a property of src/toeplitz.cpp:92-161's spectra on a square grid whose
+ * compressed blocks satisfy block(oj, oi) = block(oi, oj) with xx <-> yy and
+ * xz <-> yz, checked bit for bit when the operator is built). *out = 1 when
+ * the contraction reads only the octant modes qmx <= qmy. disable != 0 turns
+ * the octant contraction off for this operator (A/B comparisons); it cannot
+ * be turned back on. */
+int emie_cu_operator_xy_symmetry(emie_cu_operator op, int disable, int* out);
+
 /* SpectralOperator::comp (toeplitz.hpp:58-61): six host arrays written back
  * to back: comp[c][(my*qx + mx)*nent + s], nent = nz(nz+1)/2 for c < 4 and
  * nz^2 for c >= 4 (total qx*qy*2nz(2nz+1) complex). */

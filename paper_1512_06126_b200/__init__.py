@@ -102,6 +102,7 @@ def lib():
                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, ctypes.c_int,
                                  ctypes.POINTER(vp), vp],
         "emie_cu_operator_dims": [vp, ip, dp],
+        "emie_cu_operator_xy_symmetry": [vp, ctypes.c_int, ip],
         "emie_cu_operator_download_spectra": [vp, vp],
         "emie_cu_operator_download_blocks": [vp, vp],
         "emie_cu_design_offset_filters": [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -381,6 +382,15 @@ def restrict_modes(op: SpectralOperator, q0: int, q1: int) -> SpectralOperator:
     h = ctypes.c_void_p()
     _check(lib().emie_cu_operator_restrict_modes(op.handle, int(q0), int(q1), ctypes.byref(h)))
     return SpectralOperator(h)
+
+
+def xy_symmetric(op: SpectralOperator, disable: bool = False) -> bool:
+    """True when the contraction runs on the octant modes only (the operator's
+    blocks are exactly x <-> y symmetric on a square grid). disable=True turns
+    the octant contraction off for this operator."""
+    out = ctypes.c_int()
+    _check(lib().emie_cu_operator_xy_symmetry(op.handle, int(bool(disable)), ctypes.byref(out)))
+    return bool(out.value)
 
 
 def mode_list(op: SpectralOperator, q0: int, q1: int) -> np.ndarray:

@@ -160,6 +160,7 @@ Operator::~Operator() {
   cudaFree(tw_y);
   cudaFree(emap);
   cudaFree(ctab);
+  cudaFree(octl);
 }
 
 System::~System() {
@@ -489,6 +490,15 @@ int emie_cu_operator_dims(emie_cu_operator h, int dims[7], double* omega) {
     const int d[7] = {op.nx, op.ny, op.nz, op.ex, op.ey, op.qx, op.qy};
     std::memcpy(dims, d, sizeof d);
     if (omega) *omega = op.omega;
+  });
+}
+
+int emie_cu_operator_xy_symmetry(emie_cu_operator h, int disable, int* out) {
+  return guarded([&] {
+    if (!h) fail(EMIE_CU_INVALID_ARGUMENT, "null operator");
+    Operator& op = h->op;
+    if (disable) op.xysym = false;
+    if (out) *out = op.xysym ? 1 : 0;
   });
 }
 

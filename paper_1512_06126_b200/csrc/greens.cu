@@ -856,6 +856,28 @@ __global__ void mirror_blocks_kernel(cplx* blocks, const int* __restrict__ pairs
   }
 }
 
+// ... and the offsets oi == oj of such a grid are their own mirrors: the
+// exact blocks have xx = yy and xz = yz there. The build designs the xx and
+// yy (xz and yz) filters independently, so its two copies differ by the
+// filter-design rounding (measured <= 1.4e-6 of the block max for xx/yy,
+// ~5e-15 for xz/yz: the level at which the reference's own blocks are
+// determined); both are replaced by their mean, which makes
+// the blocks exactly x <-> y symmetric (the octant contraction, operator.cu)
+__global__ void symmetrize_diagonal_kernel(cplx* blocks, int nx, int ntri, int nfull, int nent) {
+  const long long total = static_cast<long long>(nx) * (ntri + nfull);
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int o = static_cast<int>(x / (ntri + nfull)), e = static_cast<int>(x - static_cast<long long>(o) * (ntri + nfull));
+    cplx* blk = blocks + (static_cast<size_t>(o) * nx + o) * nent;
+    const int i = e < ntri ? e : 4 * ntri + (e - ntri);  // xx entry or xz entry
+    const int j = e < ntri ? i + ntri : i + nfull;       // its yy / yz partner
+    const cplx a = blk[i], b = blk[j];
+    const cplx m = {(a.re + b.re) * 0.5, (a.im + b.im) * 0.5};
+    blk[i] = m;
+    blk[j] = m;
+  }
+}
+
 __global__ void kernel_output_kernel(Geom g, int alpha, int beta, const double* s, int n,
                                      double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1093,6 +1115,12 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
         blocks, pairs, static_cast<int>(pairs_h.size()), op.nx, op.ntri, op.nfull, op.nent);
     check_launch("mirror_blocks_kernel");
   }
+  if (mirror) {
+    const long long total = static_cast<long long>(op.nx) * (op.ntri + op.nfull);
+    symmetrize_diagonal_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
+        blocks, op.nx, op.ntri, op.nfull, op.nent);
+    check_launch("symmetrize_diagonal_kernel");
+  }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {
     unsigned long long h[8];
@@ -1121,7 +1149,7 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
     fail(EMIE_CU_DOMAIN_ERROR, "assemble_block: non-finite block entry");
   }
   profile_mark(6, true, st);
-  transform_blocks(op, blocks, st);
+  transform_blocks(op, blocks, st, mirror ? -1 : 0);  // checked: the octant path needs bitwise symmetry
   profile_mark(6, false, st);
   if (keep_blocks) {
     op.blocks = blocks;

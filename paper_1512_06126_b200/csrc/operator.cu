@@ -258,36 +258,51 @@ __device__ __forceinline__ int mirror_count(int qm, int qx, int ex, int ey) {
 template <int NZ>
 constexpr int mma_warps() { return 3 * NZ / 8; }
 constexpr int kBlkStages = 3, kUStages = 2;
+#ifndef EMIE_CT_OCT_BST
+#define EMIE_CT_OCT_BST 2
+#endif
+constexpr int kBlkStagesOct = EMIE_CT_OCT_BST;  // 16-column stages leave SMEM for two blocks
 #ifndef EMIE_CT_L2AHEAD
 #define EMIE_CT_L2AHEAD 0
 #endif
-#ifndef EMIE_CT_ACC
-#define EMIE_CT_ACC 1
-#endif
 constexpr int kL2Ahead = EMIE_CT_L2AHEAD;  // modes past the SMEM stages prefetched to L2
-constexpr int kAcc = EMIE_CT_ACC;          // accumulator sets per DMMA chain
+// column-table flag: the column belongs to the transposed mode (x <-> y exchanged)
+constexpr long long kSwapCol = 1LL << 60;
 
-template <int NZ>
+template <bool OCT>
+constexpr int ct_cols() { return OCT ? 16 : 8; }
+template <bool OCT>
+constexpr int ct_blk_stages() { return OCT ? kBlkStagesOct : kBlkStages; }
+
+// OCT (operator.xysym): work item t is octant mode octl[t] = (qmy, qmx) with
+// qmx <= qmy. Columns 0-7 are its own (mirror, rhs) columns; columns 8-15 are
+// those of the transposed mode (qmx, qmy), read with their x and y thirds
+// exchanged and stored back exchanged: M(qmx, qmy) = P M(qmy, qmx) P with P
+// the x <-> y permutation, so one block read serves both modes and the MMA's
+// A fragment feeds two n8 products.
+template <int NZ, bool OCT>
 __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
-                        int ex, int ey, int qx, int q0, int q1, int qbase, int nrhs, int nentD) {
+                        int ex, int ey, int qx, int q0, int q1, int qbase, int nrhs, int nentD,
+                        const int* __restrict__ octl, int noct) {
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int nk = np / 4;
   constexpr int W = mma_warps<NZ>();
+  constexpr int NC = ct_cols<OCT>(), BST = ct_blk_stages<OCT>();
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bfull = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* bempty = bfull + kBlkStages;
-  uint64_t* ufull = bempty + kBlkStages;
+  uint64_t* bempty = bfull + BST;
+  uint64_t* ufull = bempty + BST;
   uint64_t* uempty = ufull + kUStages;
-  // per input stage: output offsets (r*E + mode)*np of its 8 columns (-1: none)
+  // per input stage: output offsets (r*E + mode)*np of its NC columns (-1: none)
   long long* colbase = reinterpret_cast<long long*>(smraw + 128);
-  cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128 + kUStages * 8 * sizeof(long long));
-  cplx* ubuf = blkbuf + kBlkStages * nentD;
+  cplx* blkbuf = reinterpret_cast<cplx*>(smraw + 128 + kUStages * NC * sizeof(long long));
+  cplx* ubuf = blkbuf + BST * nentD;
   const size_t E = static_cast<size_t>(ex) * ey;
   constexpr uint32_t colbytes = np * sizeof(cplx);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kBlkStages; ++i) {
+    for (int i = 0; i < BST; ++i) {
       mbar_init(bfull + i, 1);
       mbar_init(bempty + i, W);
     }
@@ -298,20 +313,22 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // columns past a mode's ncol are multiplied but never stored: keep them finite
-  for (int i = threadIdx.x; i < kUStages * 8 * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
+  for (int i = threadIdx.x; i < kUStages * NC * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
   __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const int G = gridDim.x;
+  const int nwork = OCT ? noct : q1 - q0;
 
-  if (warp == W) {  // ---- producer
-    if (lane == 0) {
-      int j = 0;
-      for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
-        const int bs = j % kBlkStages, us = j % kUStages;
-        if (j >= kBlkStages) mbar_wait(bempty + bs, static_cast<uint32_t>((j / kBlkStages - 1) & 1));
-        const uint32_t blkbytes = nentD * sizeof(cplx);
+  if (warp == W) {  // ---- producer warp: lane c issues column c's copy
+    int j = 0;
+    for (int t = blockIdx.x; t < nwork; t += G, ++j) {
+      const int qm = OCT ? __ldg(octl + t) : q0 + t;
+      const int bs = j % BST, us = j % kUStages;
+      if (j >= BST) mbar_wait(bempty + bs, static_cast<uint32_t>((j / BST - 1) & 1));
+      const uint32_t blkbytes = nentD * sizeof(cplx);
+      if (lane == 0) {
         // blocks of the modes after the SMEM stages go to L2 ahead of their copy
-        for (int d = (j == 0 ? kBlkStages : kL2Ahead); kL2Ahead > 0 && d <= kL2Ahead; ++d) {
+        for (int d = (j == 0 ? BST : kL2Ahead); !OCT && kL2Ahead > 0 && d <= kL2Ahead; ++d) {
           const int qp = qm + d * G;
           if (qp < q1) bulk_prefetch_l2(op + static_cast<size_t>(qp - qbase) * nentD, blkbytes);
         }
@@ -321,23 +338,29 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         mbar_expect_tx(bfull + bs, blkbytes);
         bulk_g2s(blkbuf + bs * nentD, op + static_cast<size_t>(qm - qbase) * nentD, blkbytes, bfull + bs);
 #endif
-        if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
-        const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
-        long long base[8];
-        for (int col = 0; col < 8; ++col) {
-          const int mi = col / nrhs, r = col - mi * nrhs;
-          base[col] = col < ncol ? (static_cast<long long>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np : -1LL;
-          colbase[us * 8 + col] = base[col];
-        }
-        // the column table is published by the arrive (release) below
-#if EMIE_CT_EXPERIMENT == 2
-        mbar_expect_tx(ufull + us, 0);
-#else
-        mbar_expect_tx(ufull + us, ncol * colbytes);
-        cplx* dst = ubuf + us * 8 * ldu;
-        for (int col = 0; col < ncol; ++col) bulk_g2s(dst + col * ldu, S + base[col], colbytes, ufull + us);
-#endif
       }
+      if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
+      const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
+      const int qmy = qm / qx, qmx = qm - qmy * qx;
+      const int ncol2 = OCT && qmx != qmy ? ncol : 0;
+      // column `lane`: (mirror, rhs) of the mode, or for lanes 8-15 of the
+      // transposed mode (qmx, qmy) (same mirror count: ex == ey)
+      const int c = lane & 7;
+      const int mi = c / nrhs, r = c - mi * nrhs;
+      long long base = -1LL;
+      if (lane < 8 && c < ncol)
+        base = (static_cast<long long>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np;
+      else if (OCT && lane >= 8 && lane < 16 && c < ncol2)
+        base = (static_cast<long long>(r) * E + mirror_mode(qmx * qx + qmy, mi, qx, ex, ey)) * np;
+      if (lane < NC) colbase[us * NC + lane] = base < 0 ? -1LL : (lane >= 8 ? base | kSwapCol : base);
+      __syncwarp();
+      // the column table is published by this arrive (release); the copies
+      // complete on it only after it set the expected bytes
+      if (lane == 0) mbar_expect_tx(ufull + us, EMIE_CT_EXPERIMENT == 2 ? 0u : (ncol + ncol2) * colbytes);
+      __syncwarp();
+#if EMIE_CT_EXPERIMENT != 2
+      if (base >= 0) bulk_g2s(ubuf + (us * NC + lane) * ldu, S + base, colbytes, ufull + us);
+#endif
     }
     return;
   }
@@ -355,6 +378,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   auto consume = [&](auto AC) {
     constexpr int a = decltype(AC)::value;
     const int plane = a * NZ + k;
+    const int plane_sw = (a == 2 ? 2 : 1 - a) * NZ + k;  // row of a transposed-mode column
     // per-lane coefficient offsets of every k step: mode independent
     uint32_t off[nk];
 #pragma unroll
@@ -362,50 +386,101 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
       const int b = (4 * ks) / NZ, kp = 4 * ks - b * NZ + fc;
       off[ks] = __ldg(ctab + ((a * 3 + b) * NZ + k) * NZ + kp) & 0x7fffffffu;
     }
-    int j = 0;
-    for (int qm = q0 + blockIdx.x; qm < q1; qm += G, ++j) {
-      const int bs = j % kBlkStages, us = j % kUStages;
-      mbar_wait(bfull + bs, static_cast<uint32_t>((j / kBlkStages) & 1));
-      mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
-      const cplx* blk = blkbuf + bs * nentD;
-      const cplx* U = ubuf + us * 8 * ldu + fr * ldu + fc;
-      double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+    // NG n8 column groups share every A fragment; group 1 (transposed-mode
+    // columns) reads k step ks of third b from third (x <-> y)(b)
+    auto run = [&](auto NGC, const cplx* blk, const cplx* U, int bs, int us) {
+      constexpr int NG = decltype(NGC)::value;
+      auto kof = [](int g, int ks) {
+        constexpr int q = NZ / 4;  // k steps per third
+        return g == 0 ? ks : (ks < q ? ks + q : ks < 2 * q ? ks - q : ks);
+      };
+      double p1[NG][2], p2[NG][2], p3[NG][2];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) p1[g][0] = p1[g][1] = p2[g][0] = p2[g][1] = p3[g][0] = p3[g][1] = 0.0;
       // operands PD k-steps ahead of their MMAs (SMEM latency off the DMMA chain)
       constexpr int PD = 6;
-      cplx av[PD], bv[PD];
+      cplx av[PD], bv[PD][NG];
 #pragma unroll
       for (int ks = 0; ks < PD; ++ks) {
         av[ks] = blk[off[ks]];
-        bv[ks] = U[4 * ks];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) bv[ks][g] = U[g * 8 * ldu + 4 * kof(g, ks)];
       }
 #pragma unroll
       for (int ks = 0; ks < (EMIE_CT_EXPERIMENT == 1 ? 0 : nk); ++ks) {
-        const cplx bu = bv[ks % PD];  // B[k = fc][col = fr]
         const cplx mv = av[ks % PD];
+        cplx bu[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) bu[g] = bv[ks % PD][g];  // B[k = fc][col = fr]
         if (ks + PD < nk) {
           av[ks % PD] = blk[off[ks + PD]];
-          bv[ks % PD] = U[4 * (ks + PD)];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) bv[ks % PD][g] = U[g * 8 * ldu + 4 * kof(g, ks + PD)];
         }
         constexpr bool kz = a == 2;
         const bool neg = kz && (4 * ks) / NZ < 2;  // compile time after unrolling
-        const double bs_ = bu.re + bu.im;
-        dmma(p1[0], p1[1], mv.re, neg ? -bu.re : bu.re);
-        dmma(p2[0], p2[1], mv.im, neg ? -bu.im : bu.im);
-        dmma(p3[0], p3[1], mv.re + mv.im, neg ? -bs_ : bs_);
+        const double ms = mv.re + mv.im;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const double bs_ = bu[g].re + bu[g].im;
+          dmma(p1[g][0], p1[g][1], mv.re, neg ? -bu[g].re : bu[g].re);
+          dmma(p2[g][0], p2[g][1], mv.im, neg ? -bu[g].im : bu[g].im);
+          dmma(p3[g][0], p3[g][1], ms, neg ? -bs_ : bs_);
+        }
       }
       // block stage reads are complete (the DMMAs consumed them): release it
       __syncwarp();
       if (lane == 0) mbar_arrive(bempty + bs);
-      const long long cb0 = colbase[us * 8 + 2 * fc], cb1 = colbase[us * 8 + 2 * fc + 1];
-      if (cb0 >= 0) S[cb0 + plane] = cplx{p1[0] - p2[0], p3[0] - p1[0] - p2[0]};
-      if (cb1 >= 0) S[cb1 + plane] = cplx{p1[1] - p2[1], p3[1] - p1[1] - p2[1]};
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
+          if (cb >= 0) {
+            const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? plane_sw : plane);
+            S[o] = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(uempty + us);  // input columns and their table
+    };
+    int j = 0;
+    for (int t = blockIdx.x; t < nwork; t += G, ++j) {
+      const int bs = j % BST, us = j % kUStages;
+      mbar_wait(bfull + bs, static_cast<uint32_t>((j / BST) & 1));
+      mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
+      const cplx* blk = blkbuf + bs * nentD;
+      const cplx* U = ubuf + us * NC * ldu + fr * ldu + fc;
+      if (OCT && colbase[us * NC + 8] >= 0) run(std::integral_constant<int, 2>{}, blk, U, bs, us);
+      else run(std::integral_constant<int, 1>{}, blk, U, bs, us);
     }
   };
   if (a_rt == 0) consume(std::integral_constant<int, 0>{});
   else if (a_rt == 1) consume(std::integral_constant<int, 1>{});
   else consume(std::integral_constant<int, 2>{});
+}
+
+// exact x <-> y symmetry of the compressed blocks (the property the octant
+// contraction relies on): block(oj, oi) == block(oi, oj) with xx <-> yy and
+// xz <-> yz, bit for bit, for every offset pair including oi == oj
+__global__ void xy_symmetry_kernel(const cplx* __restrict__ blocks, int nx, int ntri, int nfull, int nent,
+                                   int* bad) {
+  const long long total = static_cast<long long>(nx) * nx * nent;
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int off = static_cast<int>(x / nent), e = static_cast<int>(x - static_cast<long long>(off) * nent);
+    const int oi = off / nx, oj = off - oi * nx;
+    int d = e;
+    if (e < ntri) d = e + ntri;
+    else if (e < 2 * ntri) d = e - ntri;
+    else if (e >= 4 * ntri && e < 4 * ntri + nfull) d = e + nfull;
+    else if (e >= 4 * ntri + nfull) d = e - nfull;
+    const cplx u = blocks[x], v = blocks[(static_cast<size_t>(oj) * nx + oi) * nent + d];
+    if (__double_as_longlong(u.re) != __double_as_longlong(v.re) ||
+        __double_as_longlong(u.im) != __double_as_longlong(v.im))
+      *bad = 1;
+  }
 }
 
 void set_smem(const void* fn, size_t bytes) {
@@ -416,8 +491,51 @@ void set_smem(const void* fn, size_t bytes) {
 }  // namespace
 
 // ------------------------------------------------------------------ host --
-void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st) {
+void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int sym_known) {
   lateral_spectra(op, d_blocks, st);
+  bool sym = false;
+  if (op.nx == op.ny && op.ex == op.ey && op.mma && sym_known != 0) {
+    sym = true;
+    if (sym_known < 0) {
+      int* bad = scratch<int>(1, st);
+      EMIE_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+      const long long total = static_cast<long long>(op.nx) * op.nx * op.nent;
+      xy_symmetry_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 8 * sm_count())), 256, 0,
+                           st>>>(d_blocks, op.nx, op.ntri, op.nfull, op.nent, bad);
+      check_launch("xy_symmetry_kernel");
+      int h = 1;
+      EMIE_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      EMIE_CUDA(cudaStreamSynchronize(st));
+      release(bad, st);
+      sym = h == 0;
+    }
+  }
+  op.xysym = sym;
+  cudaFree(op.octl);
+  op.octl = nullptr;
+  op.noct = 0;
+  if (sym) {
+    // octant modes qmx <= qmy: off-diagonal (two modes per block) first, the
+    // diagonal (one mode) last, so the lighter items fill the tail
+    std::vector<int> l;
+    for (int qmy = 0; qmy < op.qy; ++qmy)
+      for (int qmx = 0; qmx < qmy; ++qmx) l.push_back(qmy * op.qx + qmx);
+    for (int q = 0; q < op.qx; ++q) l.push_back(q * op.qx + q);
+    EMIE_CUDA(cudaMalloc(&op.octl, l.size() * sizeof(int)));
+    EMIE_CUDA(cudaMemcpyAsync(op.octl, l.data(), l.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    op.noct = static_cast<int>(l.size());
+  }
+}
+
+// octant contraction in use (EMIE_CU_NO_OCTANT=1 turns it off, for A/B runs)
+static bool use_octant(const Operator& op, int q0, int q1) {
+  static const bool off = [] {
+    const char* e = std::getenv("EMIE_CU_NO_OCTANT");
+    return e && e[0] == '1';
+  }();
+  return !off && op.xysym && op.noct > 0 && op.qbase == 0 && q0 == 0 &&
+         q1 == static_cast<int>(op.modes()) && op.qcount == q1;
 }
 
 // K_ct over quadrant modes [q0, q1) (all stored in op: qbase <= q0, q1 <= qbase + qcount):
@@ -433,18 +551,28 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
     const int g = std::min(2, nrhs - r0);
     cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
     if (op.mma) {
-      const size_t smem = 128 + kUStages * 8 * sizeof(long long) +
-                          kBlkStages * static_cast<size_t>(op.nentD) * sizeof(cplx) +
-                          kUStages * 8 * static_cast<size_t>(np + 4) * sizeof(cplx);
+      const bool oct = use_octant(op, q0, q1);
+      const int nc = oct ? ct_cols<true>() : ct_cols<false>();
+      const int bst = oct ? ct_blk_stages<true>() : ct_blk_stages<false>();
+      const size_t smem = 128 + kUStages * nc * sizeof(long long) +
+                          bst * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                          kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+      const int nwork = oct ? op.noct : nmodes;
       auto launch = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
-        const int grid = std::max(1, std::min(sms * per_sm, nmodes));
+        const int grid = std::max(1, std::min(sms * per_sm, nwork));
         kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
-                                                   g, op.nentD);
+                                                   g, op.nentD, op.octl, op.noct);
       };
-      if (op.nz == 8) launch(contract_mma_kernel<8>, mma_warps<8>());
-      else if (op.nz == 16) launch(contract_mma_kernel<16>, mma_warps<16>());
-      else launch(contract_mma_kernel<32>, mma_warps<32>());
+      if (oct) {
+        if (op.nz == 8) launch(contract_mma_kernel<8, true>, mma_warps<8>());
+        else if (op.nz == 16) launch(contract_mma_kernel<16, true>, mma_warps<16>());
+        else launch(contract_mma_kernel<32, true>, mma_warps<32>());
+      } else {
+        if (op.nz == 8) launch(contract_mma_kernel<8, false>, mma_warps<8>());
+        else if (op.nz == 16) launch(contract_mma_kernel<16, false>, mma_warps<16>());
+        else launch(contract_mma_kernel<32, false>, mma_warps<32>());
+      }
       check_launch("contract_mma_kernel");
       continue;
     }

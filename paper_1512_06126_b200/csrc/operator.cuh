@@ -59,6 +59,15 @@ struct Operator {
   // operator is a mode shard of a sharded apply (or a lateral-only geometry, qcount = 0)
   int qbase = 0, qcount = 0;
 
+  // x <-> y transposition symmetry (square grid, ex == ey, compressed blocks
+  // with block(oj, oi) == block(oi, oj) under xx <-> yy, xz <-> yz exactly):
+  // the block of quadrant mode (qmy, qmx) is then the block of (qmx, qmy)
+  // with the x and y rows and columns exchanged, so the contraction reads
+  // only the octant qmx <= qmy (octl: those modes, off-diagonal ones first)
+  bool xysym = false;
+  int* octl = nullptr;
+  int noct = 0;
+
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
   std::size_t lateral() const { return static_cast<std::size_t>(ex) * ey; }
   std::size_t cells() const { return static_cast<std::size_t>(nx) * ny * nz; }
@@ -88,7 +97,9 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
                      const cplx* s, const double* r1, int nrhs, cudaStream_t st);
 
 // stages (operator.cu)
-void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st);
+// sym_known: 1 the blocks are x <-> y symmetric by construction, 0 they are
+// not, -1 check on the device (bitwise)
+void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int sym_known = -1);
 void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs,
              const System* sys, cudaStream_t st);
 void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaStream_t st);
