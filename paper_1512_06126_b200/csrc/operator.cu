@@ -420,13 +420,16 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         constexpr bool kz = a == 2;
         const bool neg = kz && (4 * ks) / NZ < 2;  // compile time after unrolling
         const double ms = mv.re + mv.im;
+        double bs[NG];
 #pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          const double bs_ = bu[g].re + bu[g].im;
-          dmma(p1[g][0], p1[g][1], mv.re, neg ? -bu[g].re : bu[g].re);
-          dmma(p2[g][0], p2[g][1], mv.im, neg ? -bu[g].im : bu[g].im);
-          dmma(p3[g][0], p3[g][1], ms, neg ? -bs_ : bs_);
-        }
+        for (int g = 0; g < NG; ++g) bs[g] = bu[g].re + bu[g].im;
+        // products sharing an A operand back to back
+#pragma unroll
+        for (int g = 0; g < NG; ++g) dmma(p1[g][0], p1[g][1], mv.re, neg ? -bu[g].re : bu[g].re);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) dmma(p2[g][0], p2[g][1], mv.im, neg ? -bu[g].im : bu[g].im);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) dmma(p3[g][0], p3[g][1], ms, neg ? -bs[g] : bs[g]);
       }
       // block stage reads are complete (the DMMAs consumed them): release it
       __syncwarp();

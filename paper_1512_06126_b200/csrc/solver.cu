@@ -143,6 +143,16 @@ __global__ void scale_kernel(cplx* y, const cplx* __restrict__ x, double a, std:
     y[e] = a * ldg(x + e);
 }
 
+// y[e] = x[e] / sqrt(*nrm2): the next basis vector normalised on the device
+// (same IEEE sqrt and division as the host path, so bit-identical to it)
+__global__ void scale_by_norm_kernel(cplx* y, const cplx* __restrict__ x, const double* nrm2, std::size_t n) {
+  const double s = *nrm2;
+  const double a = s > 0.0 ? 1.0 / std::sqrt(s) : 0.0;
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    y[e] = a * ldg(x + e);
+}
+
 // x[e] += sum_k y[k] V_k[e] in k order (cie.cpp:213-214)
 __global__ void combine_kernel(cplx* x, const cplx* __restrict__ V, std::size_t vstride, int nv,
                                const double* __restrict__ y, std::size_t n) {
@@ -278,18 +288,25 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
 
   std::vector<Rhs> rs(nrhs);
   const int ps = ws.pstride;
-  double* dv_all = scratch<double>(static_cast<std::size_t>(nrhs) * 3 * ps, st);
+  // finalized reductions per rhs, two rounds deep (parity): [par][3][ps]
+  double* dv_all = scratch<double>(static_cast<std::size_t>(nrhs) * 6 * ps, st);
   struct Pinned {  // freed on every exit path
     double* p = nullptr;
-    ~Pinned() { cudaFreeHost(p); }
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Pinned() {
+      cudaFreeHost(p);
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    }
   } pinned;
-  EMIE_CUDA(cudaMallocHost(&pinned.p, static_cast<std::size_t>(nrhs) * 3 * ps * sizeof(double)));
+  EMIE_CUDA(cudaMallocHost(&pinned.p, static_cast<std::size_t>(nrhs) * 6 * ps * sizeof(double)));
+  for (cudaEvent_t& e : pinned.ev) EMIE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   double* hp_all = pinned.p;
   for (int i = 0; i < nrhs; ++i) {
     Rhs& R = rs[i];
     R.idx = i;
-    R.dv = dv_all + static_cast<std::size_t>(i) * 3 * ps;
-    R.hp = hp_all + static_cast<std::size_t>(i) * 3 * ps;
+    R.dv = dv_all + static_cast<std::size_t>(i) * 6 * ps;
+    R.hp = hp_all + static_cast<std::size_t>(i) * 6 * ps;
     R.x = d_x + i * n;
     R.b = d_rhs + i * n;
     R.r = Rall + i * n;
@@ -348,120 +365,189 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
     R.phase = Rhs::kResidual;
   };
 
-  while (true) {
-    // gather every pending apply into one batched call
-    std::vector<Rhs*> req;
-    for (Rhs& R : rs)
-      if (R.phase == Rhs::kInner || R.phase == Rhs::kResidual) req.push_back(&R);
-    if (req.empty()) break;
-    for (std::size_t q = 0; q < req.size(); ++q) {
-      Rhs& R = *req[q];
-      const cplx* src = R.phase == Rhs::kInner ? R.V + static_cast<std::size_t>(R.j) * n : R.x;
+  // One round = one batched apply of every listed right-hand side plus each
+  // one's reductions (CGS2 for a basis vector, the residual norm for x), all
+  // stream ordered; the finalized values land in the pinned mirror of round
+  // parity `par`, and ev[par] marks their arrival. The reductions' update
+  // coefficients are read on the device, so a round never waits for the host.
+  struct Entry {
+    Rhs* R;
+    bool inner;
+    int j;
+    int slot;  // position in its round's batch (Bin / Wall slot)
+  };
+  auto enqueue_round = [&](const std::vector<Entry>& es, int par) {
+    for (std::size_t q = 0; q < es.size(); ++q) {
+      const Rhs& R = *es[q].R;  // es[q].slot == q
+      const cplx* src = es[q].inner ? R.V + static_cast<std::size_t>(es[q].j) * n : R.x;
       EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     }
-    apply_b(op, Bin, Wall, static_cast<int>(req.size()), &sys, st);
-    // enqueue every right-hand side's reductions (stream ordered, results
-    // copied to pinned memory without waiting), then one synchronisation
-    auto to_host = [&](Rhs& R, int slot, int nvals) {
-      EMIE_CUDA(cudaMemcpyAsync(R.hp + slot * ps, R.dv + slot * ps, nvals * sizeof(double), cudaMemcpyDeviceToHost,
-                                st));
-    };
-    for (std::size_t q = 0; q < req.size(); ++q) {
-      Rhs& R = *req[q];
+    apply_b(op, Bin, Wall, static_cast<int>(es.size()), &sys, st);
+    for (std::size_t q = 0; q < es.size(); ++q) {
+      Rhs& R = *es[q].R;
       cplx* w = Wall + q * n;
-      if (R.phase == Rhs::kResidual) {  // cie.cpp:217-229
+      double* dv = R.dv + par * 3 * ps;
+      double* hp = R.hp + par * 3 * ps;
+      auto to_host = [&](int slot, int nvals) {
+        EMIE_CUDA(cudaMemcpyAsync(hp + slot * ps, dv + slot * ps, nvals * sizeof(double), cudaMemcpyDeviceToHost,
+                                  st));
+      };
+      if (!es[q].inner) {  // cie.cpp:217-229
         residual_kernel<<<ws.G, kRedThreads, 0, st>>>(R.r, R.b, w, n, ws.partial);
         check_launch("residual_kernel");
-        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, R.dv + 2 * ps);
+        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, dv + 2 * ps);
         check_launch("finalize_kernel");
-        to_host(R, 2, 1);
+        to_host(2, 1);
         continue;
       }
-      const int j = R.j;
+      const int j = es[q].j;
       // CGS2 pass 1: dots against v_0..v_j plus |w|^2, then w -= V h
       dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 1);
       check_launch("dots_kernel");
-      finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, R.dv);
+      finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, dv);
       check_launch("finalize_kernel");
-      to_host(R, 0, 2 * (j + 1) + 1);
-      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, R.dv, n, nullptr);
+      to_host(0, 2 * (j + 1) + 1);
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
       check_launch("update_kernel");
       // pass 2, with the new |w|^2
       dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
       check_launch("dots_kernel");
-      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), R.dv + ps);
+      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
       check_launch("finalize_kernel");
-      to_host(R, 1, 2 * (j + 1));
-      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, R.dv + ps, n, ws.partial);
+      to_host(1, 2 * (j + 1));
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv + ps, n, ws.partial);
       check_launch("update_kernel");
-      finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, R.dv + 2 * ps);
+      finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, dv + 2 * ps);
       check_launch("finalize_kernel");
-      to_host(R, 2, 1);
+      to_host(2, 1);
     }
-    EMIE_CUDA(cudaStreamSynchronize(st));
-    for (std::size_t q = 0; q < req.size(); ++q) {
-      Rhs& R = *req[q];
-      cplx* w = Wall + q * n;
-      if (R.phase == Rhs::kResidual) {
-        R.rnorm = std::sqrt(R.hp[2 * ps]);
-        if (R.rnorm / R.bnorm <= tol) {
-          R.rep.status = 0;
-          finish(R);
-        } else if (R.broke) {
-          R.rep.status = 2;
-          finish(R);
-        } else if (!start_cycle(R)) {
-          finish(R);
-        }
-        continue;
+    EMIE_CUDA(cudaEventRecord(pinned.ev[par], st));
+  };
+
+  // host side of a processed round entry (cie.cpp:148-203 / 217-229);
+  // `scaled`: the next basis vector was already normalised on the device.
+  // Returns true when the rhs goes on with inner step j + 1.
+  auto process = [&](const Entry& e, int par, bool scaled) -> bool {
+    Rhs& R = *e.R;
+    const double* hp = R.hp + par * 3 * ps;
+    cplx* w = Wall + static_cast<std::size_t>(e.slot) * n;
+    if (!e.inner) {
+      R.rnorm = std::sqrt(hp[2 * ps]);
+      if (R.rnorm / R.bnorm <= tol) {
+        R.rep.status = 0;
+        finish(R);
+      } else if (R.broke) {
+        R.rep.status = 2;
+        finish(R);
+      } else if (!start_cycle(R)) {
+        finish(R);
       }
-      // inner step j (cie.cpp:148-203)
-      ++R.iter;
-      const int j = R.j;
-      cd* hj = R.h.data() + static_cast<std::size_t>(j) * (m + 1);
-      const double wn0 = std::sqrt(R.hp[2 * (j + 1)]);
-      for (int i = 0; i <= j; ++i) hj[i] += cd(R.hp[2 * i], R.hp[2 * i + 1]);
-      for (int i = 0; i <= j; ++i) hj[i] += cd(R.hp[ps + 2 * i], R.hp[ps + 2 * i + 1]);
-      const double hnext = std::sqrt(R.hp[2 * ps]);
-      for (int i = 0; i < j; ++i) {
-        const cd t = R.rot_c[i] * hj[i] + R.rot_s[i] * hj[i + 1];
-        hj[i + 1] = -std::conj(R.rot_s[i]) * hj[i] + R.rot_c[i] * hj[i + 1];
-        hj[i] = t;
-      }
-      bool end_inner = false;
-      if (hnext <= 1e-13 * std::max(wn0, 1e-300)) {
-        double colmax = hnext;
-        for (int i = 0; i <= j; ++i) colmax = std::max(colmax, std::abs(hj[i]));
-        if (std::abs(hj[j]) > 1e-13 * std::max(colmax, 1e-300)) {
-          R.cols = j + 1;
-        } else {
-          R.cols = j;
-          R.broke = true;
-          R.history.push_back(R.rnorm / R.bnorm);
-        }
-        end_inner = true;
+      return false;
+    }
+    ++R.iter;
+    const int j = R.j;
+    cd* hj = R.h.data() + static_cast<std::size_t>(j) * (m + 1);
+    const double wn0 = std::sqrt(hp[2 * (j + 1)]);
+    for (int i = 0; i <= j; ++i) hj[i] += cd(hp[2 * i], hp[2 * i + 1]);
+    for (int i = 0; i <= j; ++i) hj[i] += cd(hp[ps + 2 * i], hp[ps + 2 * i + 1]);
+    const double hnext = std::sqrt(hp[2 * ps]);
+    for (int i = 0; i < j; ++i) {
+      const cd t = R.rot_c[i] * hj[i] + R.rot_s[i] * hj[i + 1];
+      hj[i + 1] = -std::conj(R.rot_s[i]) * hj[i] + R.rot_c[i] * hj[i + 1];
+      hj[i] = t;
+    }
+    bool end_inner = false;
+    if (hnext <= 1e-13 * std::max(wn0, 1e-300)) {
+      double colmax = hnext;
+      for (int i = 0; i <= j; ++i) colmax = std::max(colmax, std::abs(hj[i]));
+      if (std::abs(hj[j]) > 1e-13 * std::max(colmax, 1e-300)) {
+        R.cols = j + 1;
       } else {
-        hj[j + 1] = hnext;
+        R.cols = j;
+        R.broke = true;
+        R.history.push_back(R.rnorm / R.bnorm);
+      }
+      end_inner = true;
+    } else {
+      hj[j + 1] = hnext;
+      if (!scaled) {
         scale_kernel<<<GB, T, 0, st>>>(R.V + static_cast<std::size_t>(j + 1) * n, w, 1.0 / hnext, n);
         check_launch("scale_kernel");
-        make_rotation(hj[j], hnext, R.rot_c[j], R.rot_s[j]);
-        const cd t = R.rot_c[j] * hj[j] + R.rot_s[j] * hj[j + 1];
-        hj[j + 1] = 0.0;
-        hj[j] = t;
-        R.g[j + 1] = -std::conj(R.rot_s[j]) * R.g[j];
-        R.g[j] = R.rot_c[j] * R.g[j];
-        R.cols = j + 1;
-        const double est = std::abs(R.g[j + 1]) / R.bnorm;
-        R.history.push_back(est);
-        if (est <= tol) end_inner = true;
       }
-      if (!end_inner) {
-        ++R.j;
-        if (!(R.j < m && R.iter < max_iters)) end_inner = true;
+      make_rotation(hj[j], hnext, R.rot_c[j], R.rot_s[j]);
+      const cd t = R.rot_c[j] * hj[j] + R.rot_s[j] * hj[j + 1];
+      hj[j + 1] = 0.0;
+      hj[j] = t;
+      R.g[j + 1] = -std::conj(R.rot_s[j]) * R.g[j];
+      R.g[j] = R.rot_c[j] * R.g[j];
+      R.cols = j + 1;
+      const double est = std::abs(R.g[j + 1]) / R.bnorm;
+      R.history.push_back(est);
+      if (est <= tol) end_inner = true;
+    }
+    if (!end_inner) {
+      ++R.j;
+      if (!(R.j < m && R.iter < max_iters)) end_inner = true;
+    }
+    if (end_inner) {
+      close_cycle(R);
+      return false;
+    }
+    return true;
+  };
+
+  // Pipeline: while the host reads round k's reductions, the device already
+  // runs round k + 1 for every rhs that can only go on with its next inner
+  // step (speculation: the next basis vector is normalised on the device,
+  // then applied and orthogonalised). A rhs that instead converges or breaks
+  // down at round k discards its speculative work (never read: it only
+  // touches the unused next basis slot and scratch) and the pipeline drains
+  // once so its residual apply batches with the others again.
+  std::vector<Entry> pending;
+  int par = 0;
+  bool drain = false;
+  while (true) {
+    if (pending.empty()) {
+      for (Rhs& R : rs)
+        if (R.phase == Rhs::kInner || R.phase == Rhs::kResidual)
+          pending.push_back({&R, R.phase == Rhs::kInner, R.j, static_cast<int>(pending.size())});
+      if (pending.empty()) break;
+      enqueue_round(pending, par);
+    }
+    bool spec = !drain;
+    for (const Entry& e : pending)
+      if (!e.inner || !(e.j + 1 < m && e.R->iter + 1 < max_iters)) spec = false;
+    std::vector<Entry> next;
+    if (spec) {
+      for (std::size_t q = 0; q < pending.size(); ++q) {
+        const Entry& e = pending[q];
+        const Rhs& R = *e.R;
+        scale_by_norm_kernel<<<GB, T, 0, st>>>(R.V + static_cast<std::size_t>(e.j + 1) * n,
+                                               Wall + static_cast<std::size_t>(e.slot) * n,
+                                               R.dv + par * 3 * ps + 2 * ps, n);
+        check_launch("scale_by_norm_kernel");
+        next.push_back({e.R, true, e.j + 1, static_cast<int>(q)});
       }
-      if (end_inner) close_cycle(R);
+      enqueue_round(next, par ^ 1);
+    }
+    EMIE_CUDA(cudaEventSynchronize(pinned.ev[par]));
+    std::vector<Entry> keep;
+    bool all = true;
+    for (std::size_t q = 0; q < pending.size(); ++q) {
+      const bool goes_on = process(pending[q], par, spec);
+      if (spec && goes_on) keep.push_back(next[q]);
+      all = all && goes_on;
+    }
+    drain = spec && !all;
+    if (spec) {
+      pending = keep;  // their speculative round is exactly their next step
+      par ^= 1;
+    } else {
+      pending.clear();
     }
   }
+  // the speculative rounds of finished rhs may still run: wait before releasing
+  EMIE_CUDA(cudaStreamSynchronize(st));
 
   for (int i = 0; i < nrhs; ++i) {
     Rhs& R = rs[i];
