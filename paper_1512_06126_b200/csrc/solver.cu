@@ -136,6 +136,65 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(cplx* w, const cplx
   }
 }
 
+// CGS2's middle: w' = w - V h1 (update_kernel's arithmetic, bit for bit),
+// then the pass-2 dots conj(V_l) . w' from the same loads: every V_l element
+// is read from HBM once for both, saving one full sweep over the basis per
+// step. Each thread keeps its element's nv basis entries in registers and
+// accumulates its per-l partials in its own SMEM column (conflict-free);
+// one CTA per SM, a fixed grid (kFuseBlocks) so the summation order does not
+// depend on the GPU. partial[blk][2l .. 2l+1] as dots_kernel writes them.
+constexpr int kFuseMax = 41;  // basis vectors per fused sweep (restart <= 40)
+constexpr int kFuseThreads = 256;
+constexpr int kFuseBlocks = 148;
+__global__ void __launch_bounds__(kFuseThreads, 1)
+    update_dots_kernel(cplx* w, const cplx* __restrict__ V, std::size_t vstride, int nv,
+                       const double* __restrict__ h, std::size_t n, double* partial, int pstride) {
+  extern __shared__ double acc[];  // [2 * kFuseMax][kFuseThreads], then the coefficients
+  double* hs = acc + 2 * kFuseMax * kFuseThreads;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int l = 0; l < 2 * kFuseMax; ++l) acc[l * kFuseThreads + t] = 0.0;
+  if (t < 2 * nv) hs[t] = h[t];
+  __syncthreads();
+  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * kFuseThreads + t; e < n;
+       e += static_cast<std::size_t>(gridDim.x) * kFuseThreads) {
+    cplx v[kFuseMax];
+#pragma unroll
+    for (int l = 0; l < kFuseMax; ++l)
+      if (l < nv) v[l] = ldg(V + l * vstride + e);
+    cplx x = w[e];
+#pragma unroll
+    for (int l = 0; l < kFuseMax; ++l) {
+      if (l < nv) {
+        const double hr = hs[2 * l], hi = hs[2 * l + 1];
+        x.re = fma(-hr, v[l].re, fma(hi, v[l].im, x.re));
+        x.im = fma(-hr, v[l].im, fma(-hi, v[l].re, x.im));
+      }
+    }
+    w[e] = x;
+#pragma unroll
+    for (int l = 0; l < kFuseMax; ++l) {
+      if (l < nv) {
+        double& ar = acc[(2 * l) * kFuseThreads + t];
+        double& ai = acc[(2 * l + 1) * kFuseThreads + t];
+        ar = fma(v[l].re, x.re, fma(v[l].im, x.im, ar));
+        ai = fma(v[l].re, x.im, fma(-v[l].im, x.re, ai));
+      }
+    }
+  }
+  __syncthreads();
+  // per (l, part): sum the 256 thread columns in a fixed tree, one warp per value
+  const int warp = t >> 5, lane = t & 31;
+  for (int i = warp; i < 2 * nv; i += kFuseThreads / 32) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kFuseThreads / 32; ++k) s += acc[i * kFuseThreads + k * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) partial[static_cast<std::size_t>(blockIdx.x) * pstride + i] = s;
+  }
+}
+
 // y[e] = a * x[e] (real a)
 __global__ void scale_kernel(cplx* y, const cplx* __restrict__ x, double a, std::size_t n) {
   for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
@@ -195,6 +254,14 @@ void make_rotation(cd f, cd g, double& c, cd& s) {
     c = std::abs(f) / t;
     s = f / std::abs(f) * std::conj(g) / t;
   }
+}
+
+constexpr std::size_t kFuseSmem = (2 * kFuseMax * kFuseThreads + 2 * kFuseMax) * sizeof(double);
+int fuse_blocks(std::size_t n) {
+  // sets the SMEM opt-in (once per device)
+  (void)resident_ctas(reinterpret_cast<const void*>(update_dots_kernel), kFuseThreads, kFuseSmem);
+  return static_cast<int>(std::max<std::size_t>(
+      1, std::min<std::size_t>(kFuseBlocks, (n + kFuseThreads - 1) / kFuseThreads)));
 }
 
 struct Workspace {
@@ -407,13 +474,22 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, dv);
       check_launch("finalize_kernel");
       to_host(0, 2 * (j + 1) + 1);
-      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
-      check_launch("update_kernel");
-      // pass 2, with the new |w|^2
-      dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
-      check_launch("dots_kernel");
-      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
-      check_launch("finalize_kernel");
+      if (j + 1 <= kFuseMax) {
+        // w -= V h1 and the pass-2 dots in one sweep over the basis
+        const int fb = fuse_blocks(n);
+        update_dots_kernel<<<fb, kFuseThreads, kFuseSmem, st>>>(w, R.V, n, j + 1, dv, n, ws.partial, ps);
+        check_launch("update_dots_kernel");
+        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, fb, ps, 2 * (j + 1), dv + ps);
+        check_launch("finalize_kernel");
+      } else {
+        update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
+        check_launch("update_kernel");
+        // pass 2, with the new |w|^2
+        dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
+        check_launch("dots_kernel");
+        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
+        check_launch("finalize_kernel");
+      }
       to_host(1, 2 * (j + 1));
       update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv + ps, n, ws.partial);
       check_launch("update_kernel");
