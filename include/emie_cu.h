@@ -181,8 +181,9 @@ int emie_cu_fgmres(emie_cu_system sys, const double* d_rhs, double* d_x, int nrh
 int emie_cu_profile_enable(int on);
 int emie_cu_profile_collect(double* ms, long long* count, int n);
 
-/* FP64 throughput probe: a DFMA-bound kernel on the device (denominator of
- * the FP64 roofline, which MEASURED_PEAKS.json does not carry) */
+/* FP64 throughput probe: the larger of a DFMA-bound and a DMMA-bound
+ * (mma.sync m8n8k4 f64) kernel on the device, TFLOP/s (denominator of the
+ * FP64 roofline, which MEASURED_PEAKS.json does not carry) */
 int emie_cu_probe_fp64(double* tflops, void* stream);
 
 /* same with host right-hand sides and solutions */

@@ -137,6 +137,30 @@ __global__ void fp64_probe_kernel(double* out, int iters) {
   for (int i = 0; i < 8; ++i) s += a[i];
   if (s == 12345.0) out[0] = s;  // keep the chains alive
 }
+
+// DMMA-bound probe (the contraction's instruction, mma.sync m8n8k4 f64):
+// 8 independent accumulator chains per warp, distinct operand registers
+__global__ void dmma_probe_kernel(double* out, int iters) {
+  double a[4], b[4], c[8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    a[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+    b[i] = 0.5 + 1e-9 * i;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a[i & 3]), "d"(b[(i >> 1) & 3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[0] = s;
+}
 }  // namespace
 
 void profile_mark(int stage, bool begin, cudaStream_t st) {
@@ -787,24 +811,37 @@ extern "C" int emie_cu_probe_fp64(double* tflops, void* stream) {
     EMIE_CUDA(cudaGetDevice(&dev));
     EMIE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     double* out = scratch<double>(1, st);
-    const int blocks = sms * 8, threads = 256, iters = 4096;
     cudaEvent_t a, b;
     EMIE_CUDA(cudaEventCreate(&a));
     EMIE_CUDA(cudaEventCreate(&b));
-    fp64_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);  // warm-up
-    check_launch("fp64_probe_kernel");
-    EMIE_CUDA(cudaEventRecord(a, st));
-    for (int r = 0; r < 5; ++r) fp64_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);
-    check_launch("fp64_probe_kernel");
-    EMIE_CUDA(cudaEventRecord(b, st));
-    EMIE_CUDA(cudaEventSynchronize(b));
-    float t = 0.f;
-    EMIE_CUDA(cudaEventElapsedTime(&t, a, b));
+    auto time_ms = [&](auto launch) {
+      launch();  // warm-up
+      EMIE_CUDA(cudaEventRecord(a, st));
+      for (int r = 0; r < 5; ++r) launch();
+      EMIE_CUDA(cudaEventRecord(b, st));
+      EMIE_CUDA(cudaEventSynchronize(b));
+      float t = 0.f;
+      EMIE_CUDA(cudaEventElapsedTime(&t, a, b));
+      return static_cast<double>(t);
+    };
+    // DFMA: 5 launches x 8 chains x iters x 2 flops per thread
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    const double t1 = time_ms([&] {
+      fp64_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);
+      check_launch("fp64_probe_kernel");
+    });
+    const double f1 = 5.0 * 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    // DMMA: 5 launches x 8 MMAs x iters x 512 flops per warp, 8 warps per SM
+    const int dit = 2048;
+    const double t2 = time_ms([&] {
+      dmma_probe_kernel<<<sms, 256, 0, st>>>(out, dit);
+      check_launch("dmma_probe_kernel");
+    });
+    const double f2 = 5.0 * 8.0 * dit * 512.0 * static_cast<double>(sms) * 8;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     release(out, st);
-    const double flops = 5.0 * 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
-    *tflops = flops / (t * 1e-3) / 1e12;
+    tflops[0] = std::max(f1 / (t1 * 1e-3), f2 / (t2 * 1e-3)) / 1e12;
   });
 }
 
