@@ -355,10 +355,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         iters = max(r.iterations for r in reps)
-        # CGS2 traffic per iteration and rhs: 4 sweeps over the
-        # j+1 basis vectors (+ w), 16 B x 3N each; j averages (restart-1)/2 over full cycles
+        # CGS2 traffic per iteration, 16 B x 3N per vector: three
+        # tiled sweeps over the j+1 basis vectors (dots; update + dots; update +
+        # norm: solver.cu) reading w each and writing it in the last two;
+        # j averages (restart-1)/2 over full cycles
         jbar = (min(40, iters) - 1) / 2.0
-        cgs2_bytes = NRHS * 4 * (jbar + 2) * 16 * n
+        cgs2_bytes = NRHS * (3 * (jbar + 1) + 5) * 16 * n
         solve = {"seconds": secs, "iterations": [r.iterations for r in reps],
                  "status": [r.status for r in reps], "tol": 1e-6, "restart": 40,
                  "ms_per_iteration": 1e3 * secs / max(1, iters),

@@ -25,6 +25,7 @@
 
 #include "../../include/emie_cu.h"
 #include "operator.cuh"
+#include "tma.cuh"
 
 namespace emie_cu {
 
@@ -136,63 +137,167 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(cplx* w, const cplx
   }
 }
 
-// CGS2's middle: w' = w - V h1 (update_kernel's arithmetic, bit for bit),
-// then the pass-2 dots conj(V_l) . w' from the same loads: every V_l element
-// is read from HBM once for both, saving one full sweep over the basis per
-// step. Each thread keeps its element's nv basis entries in registers and
-// accumulates its per-l partials in its own SMEM column (conflict-free);
-// one CTA per SM, a fixed grid (kFuseBlocks) so the summation order does not
-// depend on the GPU. partial[blk][2l .. 2l+1] as dots_kernel writes them.
-constexpr int kFuseMax = 41;  // basis vectors per fused sweep (restart <= 40)
-constexpr int kFuseThreads = 256;
-constexpr int kFuseBlocks = 148;
-__global__ void __launch_bounds__(kFuseThreads, 1)
-    update_dots_kernel(cplx* w, const cplx* __restrict__ V, std::size_t vstride, int nv,
-                       const double* __restrict__ h, std::size_t n, double* partial, int pstride) {
-  extern __shared__ double acc[];  // [2 * kFuseMax][kFuseThreads], then the coefficients
-  double* hs = acc + 2 * kFuseMax * kFuseThreads;
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int l = 0; l < 2 * kFuseMax; ++l) acc[l * kFuseThreads + t] = 0.0;
-  if (t < 2 * nv) hs[t] = h[t];
+// ---- tiled CGS2 sweeps (TMA-staged) ---------------------------------------
+// The basis vectors and w are cut into tiles of kTE elements; a producer warp
+// brings tile t of every V_l and of w into a SMEM stage with one bulk copy
+// per vector (lane l issues V_l's), two stages deep behind full/empty
+// mbarriers, so each sweep reads the basis from HBM once at full rate.
+//   MODE 0: dots conj(V_l) . w (+ |w|^2)                      (CGS2 pass 1)
+//   MODE 1: w' = w - V h, then conj(V_l) . w'                  (pass-1 update + pass-2 dots)
+//   MODE 2: w'' = w' - V h and |w''|^2                          (pass-2 update + norm)
+// The update keeps update_kernel's arithmetic (sequential in l, same FMAs),
+// so w', w'' are bit-identical to it. Dots: compute warp k owns vectors
+// l = k, k + 8, ..., lanes own elements; per-lane partials live in registers
+// across tiles and are reduced in a fixed order at the end (one CTA per SM,
+// fixed grid: the summation order does not depend on the GPU).
+constexpr int kTE = 128;        // elements per tile
+constexpr int kTileMaxV = 41;   // basis vectors per staged tile (restart <= 40)
+constexpr int kCgsWarps = 8;    // compute warps
+constexpr int kCgsThreads = (kCgsWarps + 1) * 32;
+constexpr int kCgsBlocks = 148;
+constexpr int kLPerWarp = (kTileMaxV + kCgsWarps - 1) / kCgsWarps;
+
+__device__ __forceinline__ void compute_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCgsWarps * 32) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCgsThreads, 1)
+    cgs_tile_kernel(cplx* w, const cplx* __restrict__ V, std::size_t vstride, int nv,
+                    const double* __restrict__ h, std::size_t n, double* partial, int pstride, int with_norm) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 2;
+  const std::size_t stage_elems = static_cast<std::size_t>(nv + 1) * kTE;
+  cplx* stage0 = reinterpret_cast<cplx*>(sm + 128);
+  cplx* xs = stage0 + 2 * stage_elems;
+  double* hs = reinterpret_cast<double*>(xs + kTE);
+  double* red = hs + 2 * kTileMaxV;  // kCgsWarps
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kCgsWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (MODE != 0)
+    for (int i = tid; i < 2 * nv; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
-  for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * kFuseThreads + t; e < n;
-       e += static_cast<std::size_t>(gridDim.x) * kFuseThreads) {
-    cplx v[kFuseMax];
+  const std::size_t ntiles = (n + kTE - 1) / kTE;
+
+  if (warp == kCgsWarps) {  // ---- producer
+    int j = 0;
+    for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      const int s = j & 1;
+      if (j >= 2) mbar_wait(empty + s, static_cast<uint32_t>(((j >> 1) - 1) & 1));
+      const std::size_t e0 = t * kTE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<std::size_t>(kTE), n - e0) * sizeof(cplx));
+      if (lane == 0) mbar_expect_tx(full + s, (nv + 1) * bytes);
+      __syncwarp();
+      cplx* st = stage0 + s * stage_elems;
+      for (int l = lane; l <= nv; l += 32)
+        bulk_g2s(st + static_cast<std::size_t>(l) * kTE, l < nv ? V + l * vstride + e0 : w + e0, bytes, full + s);
+    }
+    return;
+  }
+
+  // ---- compute warps
+  double acc[kLPerWarp][2];
 #pragma unroll
-    for (int l = 0; l < kFuseMax; ++l)
-      if (l < nv) v[l] = ldg(V + l * vstride + e);
-    cplx x = w[e];
+  for (int i = 0; i < kLPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
+  double nacc = 0.0;
+  int j = 0;
+  for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    const int s = j & 1;
+    mbar_wait(full + s, static_cast<uint32_t>((j >> 1) & 1));
+    const cplx* Vt = stage0 + s * stage_elems;
+    const cplx* wt = Vt + static_cast<std::size_t>(nv) * kTE;
+    const std::size_t e0 = t * kTE;
+    const int cnt = static_cast<int>(min(static_cast<std::size_t>(kTE), n - e0));
+    const cplx* x_src = wt;
+    if (MODE != 0) {
+      // update: thread e < kTE owns element e (update_kernel's arithmetic)
+      if (tid < cnt) {
+        cplx x = wt[tid];
+        for (int l = 0; l < nv; ++l) {
+          const cplx v = Vt[l * kTE + tid];
+          const double hr = hs[2 * l], hi = hs[2 * l + 1];
+          x.re = fma(-hr, v.re, fma(hi, v.im, x.re));
+          x.im = fma(-hr, v.im, fma(-hi, v.re, x.im));
+        }
+        w[e0 + tid] = x;
+        if (MODE == 1) xs[tid] = x;
+        if (MODE == 2) nacc = fma(x.re, x.re, fma(x.im, x.im, nacc));
+      }
+      if (MODE == 1) compute_bar();
+      x_src = xs;
+    }
+    if (MODE != 2) {
+      cplx wv[kTE / 32];
 #pragma unroll
-    for (int l = 0; l < kFuseMax; ++l) {
-      if (l < nv) {
-        const double hr = hs[2 * l], hi = hs[2 * l + 1];
-        x.re = fma(-hr, v[l].re, fma(hi, v[l].im, x.re));
-        x.im = fma(-hr, v[l].im, fma(-hi, v[l].re, x.im));
+      for (int k = 0; k < kTE / 32; ++k) {
+        const int e = lane + 32 * k;
+        wv[k] = e < cnt ? x_src[e] : cplx{0.0, 0.0};
+      }
+      if (MODE == 0 && with_norm && warp == 0) {
+#pragma unroll
+        for (int k = 0; k < kTE / 32; ++k) nacc = fma(wv[k].re, wv[k].re, fma(wv[k].im, wv[k].im, nacc));
+      }
+#pragma unroll
+      for (int i = 0; i < kLPerWarp; ++i) {
+        const int l = warp + kCgsWarps * i;
+        if (l < nv) {
+#pragma unroll
+          for (int k = 0; k < kTE / 32; ++k) {
+            const int e = lane + 32 * k;
+            if (e < cnt) {
+              const cplx v = Vt[l * kTE + e];
+              acc[i][0] = fma(v.re, wv[k].re, fma(v.im, wv[k].im, acc[i][0]));
+              acc[i][1] = fma(v.re, wv[k].im, fma(-v.im, wv[k].re, acc[i][1]));
+            }
+          }
+        }
       }
     }
-    w[e] = x;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
+    if (MODE == 1) compute_bar();  // xs is rewritten by the next tile
+  }
+  // ---- fixed-order reductions
+  if (MODE != 2) {
 #pragma unroll
-    for (int l = 0; l < kFuseMax; ++l) {
-      if (l < nv) {
-        double& ar = acc[(2 * l) * kFuseThreads + t];
-        double& ai = acc[(2 * l + 1) * kFuseThreads + t];
-        ar = fma(v[l].re, x.re, fma(v[l].im, x.im, ar));
-        ai = fma(v[l].re, x.im, fma(-v[l].im, x.re, ai));
+    for (int i = 0; i < kLPerWarp; ++i) {
+      const int l = warp + kCgsWarps * i;
+      double r = acc[i][0], im = acc[i][1];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_down_sync(0xffffffffu, r, o);
+        im += __shfl_down_sync(0xffffffffu, im, o);
+      }
+      if (lane == 0 && l < nv) {
+        partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * l] = r;
+        partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * l + 1] = im;
       }
     }
   }
-  __syncthreads();
-  // per (l, part): sum the 256 thread columns in a fixed tree, one warp per value
-  const int warp = t >> 5, lane = t & 31;
-  for (int i = warp; i < 2 * nv; i += kFuseThreads / 32) {
-    double s = 0.0;
+  if (MODE == 2 || (MODE == 0 && with_norm)) {
 #pragma unroll
-    for (int k = 0; k < kFuseThreads / 32; ++k) s += acc[i * kFuseThreads + k * 32 + lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (lane == 0) partial[static_cast<std::size_t>(blockIdx.x) * pstride + i] = s;
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+    if (lane == 0) red[warp] = nacc;
+    compute_bar();
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int k = 0; k < kCgsWarps; ++k) sum += red[k];
+      if (MODE == 2) partial[blockIdx.x] = sum;
+      else partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * nv] = sum;
+    }
   }
+}
+
+std::size_t cgs_smem(int nv) {
+  return 128 + 2 * static_cast<std::size_t>(nv + 1) * kTE * sizeof(cplx) + kTE * sizeof(cplx) +
+         (2 * kTileMaxV + kCgsWarps) * sizeof(double);
 }
 
 // y[e] = a * x[e] (real a)
@@ -256,12 +361,18 @@ void make_rotation(cd f, cd g, double& c, cd& s) {
   }
 }
 
-constexpr std::size_t kFuseSmem = (2 * kFuseMax * kFuseThreads + 2 * kFuseMax) * sizeof(double);
-int fuse_blocks(std::size_t n) {
-  // sets the SMEM opt-in (once per device)
-  (void)resident_ctas(reinterpret_cast<const void*>(update_dots_kernel), kFuseThreads, kFuseSmem);
-  return static_cast<int>(std::max<std::size_t>(
-      1, std::min<std::size_t>(kFuseBlocks, (n + kFuseThreads - 1) / kFuseThreads)));
+// tiled sweep launch: grid = kCgsBlocks (or fewer tiles), one CTA per SM
+template <int MODE>
+int cgs_launch(cplx* w, const cplx* V, std::size_t vstride, int nv, const double* h, std::size_t n,
+               double* partial, int pstride, int with_norm, cudaStream_t st) {
+  const std::size_t smem = cgs_smem(kTileMaxV);
+  (void)resident_ctas(reinterpret_cast<const void*>(cgs_tile_kernel<MODE>), kCgsThreads, smem);
+  const int G = static_cast<int>(std::max<std::size_t>(
+      1, std::min<std::size_t>(kCgsBlocks, (n + kTE - 1) / kTE)));
+  cgs_tile_kernel<MODE><<<G, kCgsThreads, cgs_smem(nv), st>>>(w, V, vstride, nv, h, n, partial, pstride,
+                                                              with_norm);
+  check_launch("cgs_tile_kernel");
+  return G;
 }
 
 struct Workspace {
@@ -276,7 +387,8 @@ struct Workspace {
   Workspace(cudaStream_t s, std::size_t n_, int maxv) : st(s), n(n_) {
     G = red_blocks(n);
     pstride = 2 * maxv + 2;
-    partial = scratch<double>(static_cast<std::size_t>(G) * pstride, st);
+    // rows for the reduction kernels' blocks and the tiled sweeps' (cgs_launch)
+    partial = scratch<double>(static_cast<std::size_t>(std::max(G, kCgsBlocks)) * pstride, st);
     dvals = scratch<double>(pstride, st);
     EMIE_CUDA(cudaMallocHost(&hpin, pstride * sizeof(double)));
   }
@@ -469,27 +581,34 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       }
       const int j = es[q].j;
       // CGS2 pass 1: dots against v_0..v_j plus |w|^2, then w -= V h
+      if (j + 1 <= kTileMaxV) {
+        int g = cgs_launch<0>(w, R.V, n, j + 1, nullptr, n, ws.partial, ps, 1, st);
+        finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, g, ps, 2 * (j + 1) + 1, dv);
+        check_launch("finalize_kernel");
+        to_host(0, 2 * (j + 1) + 1);
+        // w -= V h1 fused with the pass-2 dots, then w -= V h2 with the new norm
+        g = cgs_launch<1>(w, R.V, n, j + 1, dv, n, ws.partial, ps, 0, st);
+        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, g, ps, 2 * (j + 1), dv + ps);
+        check_launch("finalize_kernel");
+        to_host(1, 2 * (j + 1));
+        g = cgs_launch<2>(w, R.V, n, j + 1, dv + ps, n, ws.partial, 1, 0, st);
+        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, g, 1, 1, dv + 2 * ps);
+        check_launch("finalize_kernel");
+        to_host(2, 1);
+        continue;
+      }
       dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 1);
       check_launch("dots_kernel");
       finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, dv);
       check_launch("finalize_kernel");
       to_host(0, 2 * (j + 1) + 1);
-      if (j + 1 <= kFuseMax) {
-        // w -= V h1 and the pass-2 dots in one sweep over the basis
-        const int fb = fuse_blocks(n);
-        update_dots_kernel<<<fb, kFuseThreads, kFuseSmem, st>>>(w, R.V, n, j + 1, dv, n, ws.partial, ps);
-        check_launch("update_dots_kernel");
-        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, fb, ps, 2 * (j + 1), dv + ps);
-        check_launch("finalize_kernel");
-      } else {
-        update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
-        check_launch("update_kernel");
-        // pass 2, with the new |w|^2
-        dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
-        check_launch("dots_kernel");
-        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
-        check_launch("finalize_kernel");
-      }
+      update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
+      check_launch("update_kernel");
+      // pass 2, with the new |w|^2
+      dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
+      check_launch("dots_kernel");
+      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
+      check_launch("finalize_kernel");
       to_host(1, 2 * (j + 1));
       update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv + ps, n, ws.partial);
       check_launch("update_kernel");

@@ -54,3 +54,43 @@ def test_bad_config(torch_cuda):
     g, model, grid, sop = _cfg1()
     with pytest.raises(emie.InvalidArgument):
         emie.solve_cie(grid, model, sop, g["rhs"][0], emie.SolverConfig(tol=0.0))
+
+
+def _odd_system(nx, ny, nz, scale, seed):
+    rng = np.random.default_rng(seed)
+    nent = 2 * nz * (2 * nz + 1)
+    blocks = scale * (rng.standard_normal((ny, nx, nent)) + 1j * rng.standard_normal((ny, nx, nent)))
+    sop = emie.transform_operator(blocks, nx, ny, nz)
+    model = emie.LayeredModel([0.0, 5000.0], [0.0, 0.01, 0.1])
+    breaks = list(np.linspace(10.0, 10.0 + 50.0 * nz, nz + 1))
+    grid = emie.make_grid(model, breaks, nx, ny, 100.0, 120.0)
+    grid.sigma_a[...] = 10.0 ** rng.uniform(-3, 0, grid.sigma_a.shape)
+    n = 3 * nx * ny * nz
+    b = rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))
+    return sop, emie.build_system(grid, sop), b
+
+
+@pytest.mark.parametrize("nx,ny,nz,restart", [(5, 3, 3, 40), (7, 4, 8, 12), (16, 3, 8, 40)])
+def test_solve_residual_odd_sizes(torch_cuda, nx, ny, nz, restart):
+    """field lengths that are not a multiple of the CGS2 tile (128 entries):
+    the returned solution's true residual, through the independently checked
+    apply, meets the tolerance"""
+    sop, sys, b = _odd_system(nx, ny, nz, 1e-3, nx * 100 + restart)
+    x, reps = emie.fgmres_system(sys, b, emie.SolverConfig(tol=1e-9, restart=restart, max_iters=400))
+    for i in range(2):
+        assert reps[i].status == "converged"
+        r = emie.apply(sys, x[i]) - b[i]
+        assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b[i])
+
+
+def test_long_cycle_untiled_fallback(torch_cuda):
+    """a 60-vector cycle: steps past the tiled sweeps' 41 staged vectors run
+    the untiled CGS2 kernels; the Givens residual estimate still tracks the
+    true residual (orthogonality kept across the switch)"""
+    sop, sys, b = _odd_system(6, 5, 4, 0.2, 77)
+    x, reps = emie.fgmres_system(sys, b, emie.SolverConfig(tol=1e-15, restart=60, max_iters=55))
+    for i in range(2):
+        assert reps[i].iterations == 55
+        true = np.linalg.norm(emie.apply(sys, x[i]) - b[i]) / np.linalg.norm(b[i])
+        assert abs(true - reps[i].residual) <= 1e-9 + 1e-6 * true
+        assert abs(reps[i].history[54] - true) <= 1e-8 + 1e-4 * true
