@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 run() {
   python bench.py --steps 20 --warmup 5 --no-solve --e2e-steps 0 --no-cpu-baseline 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['value']), d['stage_ms']['contraction'])"
+import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['value']), d['stage_ms'])"
 }
 run default
 EMIE_CU_NO_OCTANT=1 run quadrant
