@@ -343,16 +343,19 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
       const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
       const int qmy = qm / qx, qmx = qm - qmy * qx;
       const int ncol2 = OCT && qmx != qmy ? ncol : 0;
-      // column `lane`: (mirror, rhs) of the mode, or for lanes 8-15 of the
-      // transposed mode (qmx, qmy) (same mirror count: ex == ey)
-      const int c = lane & 7;
+      // slot `lane`: column (mirror, rhs) of the mode, then those of the
+      // transposed mode (qmx, qmy) (same mirror count: ex == ey) -- packed
+      // behind them when both fit one n8 group (nrhs = 1), else in slots 8-15
+      const int t0 = ncol + ncol2 <= 8 ? ncol : 8;
+      const bool tr = OCT && lane >= t0 && lane < t0 + ncol2;
+      const int c = tr ? lane - t0 : lane;
       const int mi = c / nrhs, r = c - mi * nrhs;
       long long base = -1LL;
-      if (lane < 8 && c < ncol)
+      if (lane < ncol)
         base = (static_cast<long long>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np;
-      else if (OCT && lane >= 8 && lane < 16 && c < ncol2)
+      else if (tr)
         base = (static_cast<long long>(r) * E + mirror_mode(qmx * qx + qmy, mi, qx, ex, ey)) * np;
-      if (lane < NC) colbase[us * NC + lane] = base < 0 ? -1LL : (lane >= 8 ? base | kSwapCol : base);
+      if (lane < NC) colbase[us * NC + lane] = base < 0 ? -1LL : (tr ? base | kSwapCol : base);
       __syncwarp();
       // the column table is published by this arrive (release); the copies
       // complete on it only after it set the expected bytes
@@ -390,10 +393,15 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     // columns) reads k step ks of third b from third (x <-> y)(b)
     auto run = [&](auto NGC, const cplx* blk, const cplx* U, int bs, int us) {
       constexpr int NG = decltype(NGC)::value;
-      auto kof = [](int g, int ks) {
+      auto kswap = [](int ks) {
         constexpr int q = NZ / 4;  // k steps per third
-        return g == 0 ? ks : (ks < q ? ks + q : ks < 2 * q ? ks - q : ks);
+        return ks < q ? ks + q : ks < 2 * q ? ks - q : ks;
       };
+      // one group: this lane's B column may be a packed transposed-mode column
+      long long cbl = 0;
+      if (OCT && NG == 1) cbl = colbase[us * NC + fr];
+      const bool swp = OCT && NG == 1 && cbl >= 0 && (cbl & kSwapCol);
+      auto kof = [&](int g, int ks) { return (g == 1 || swp) ? kswap(ks) : ks; };
       double p1[NG][2], p2[NG][2], p3[NG][2];
 #pragma unroll
       for (int g = 0; g < NG; ++g) p1[g][0] = p1[g][1] = p2[g][0] = p2[g][1] = p3[g][0] = p3[g][1] = 0.0;
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
       const cplx* blk = blkbuf + bs * nentD;
       const cplx* U = ubuf + us * NC * ldu + fr * ldu + fc;
       if (OCT && colbase[us * NC + 8] >= 0) run(std::integral_constant<int, 2>{}, blk, U, bs, us);
-      else run(std::integral_constant<int, 1>{}, blk, U, bs, us);
+      else run(std::integral_constant<int, 1>{}, blk, U, bs, us);  // (packed transposed columns: swp)
     }
   };
   if (a_rt == 0) consume(std::integral_constant<int, 0>{});
