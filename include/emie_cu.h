@@ -224,6 +224,33 @@ int emie_cu_lateral_inverse(emie_cu_operator geom, const double* d_S, const doub
  * full-depth spectrum d_S (all modes' storage, only these modes touched) */
 int emie_cu_contract_modes(emie_cu_operator op, double* d_S, int nrhs, int q0, int q1, void* stream);
 
+/* ---- sharded FGMRES vector operations ("FGMRES on
+ * depth-sharded vectors: local partial dots, then an all-reduce"). The
+ * vector kernels of src/cie.cpp:77-98 (dot, norm, axpy, scaled) as batched
+ * CGS2 sweeps over this rank's slab; every reduction is the rank's local sum,
+ * finalized on the device (fixed order) for the caller to all-reduce. Vectors
+ * are complex128 of n entries, basis vector l at d_V + 2*l*vstride doubles. */
+
+/* d_out[2l], d_out[2l+1] = sum conj(V_l) . w (l < nv); d_out[2nv] = |w|^2 if with_norm */
+int emie_cu_vec_dots(const double* d_V, long long vstride, int nv, const double* d_w, long long n,
+                     int with_norm, double* d_out, void* stream);
+
+/* w -= sum_l h_l V_l (d_h: nv complex); then optionally (at most one of)
+ * d_dots_out = conj(V_l) . w_new (2nv doubles) or d_norm_out = |w_new|^2 */
+int emie_cu_vec_update(double* d_w, const double* d_V, long long vstride, int nv, const double* d_h,
+                       long long n, double* d_dots_out, double* d_norm_out, void* stream);
+
+/* x += sum_l y_l V_l in l order (cie.cpp:213-214), d_y: nv complex */
+int emie_cu_vec_combine(double* d_x, const double* d_V, long long vstride, int nv, const double* d_y,
+                        long long n, void* stream);
+
+/* y = a x (real a) */
+int emie_cu_vec_scale(double* d_y, const double* d_x, double a, long long n, void* stream);
+
+/* r = b - t; d_norm_out[0] = |r|^2 (cie.cpp:217-229) */
+int emie_cu_vec_residual(double* d_r, const double* d_b, const double* d_t, long long n,
+                         double* d_norm_out, void* stream);
+
 /* column moves between slab spectra, full-depth spectra and packed exchange
  * buffers: element (r, i, c, z), i < nidx, c < 3, z < nzh, goes from
  * src[(mode_s)*desc[1] + c*desc[2] + desc[3] + z] to the same form in dst,

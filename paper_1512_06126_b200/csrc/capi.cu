@@ -777,6 +777,54 @@ extern "C" int emie_cu_fgmres(emie_cu_system h, const double* d_rhs, double* d_x
   });
 }
 
+// ---- slab vector operations (sharded FGMRES) ----
+extern "C" int emie_cu_vec_dots(const double* d_V, long long vstride, int nv, const double* d_w, long long n,
+                                int with_norm, double* d_out, void* stream) {
+  return guarded([&] {
+    if (!d_w || !d_out || (nv > 0 && !d_V) || nv < 0 || n < 1 || vstride < 0)
+      fail(EMIE_CU_INVALID_ARGUMENT, "vec_dots: bad arguments");
+    vec_dots(reinterpret_cast<const cplx*>(d_V), static_cast<std::size_t>(vstride), nv,
+             reinterpret_cast<const cplx*>(d_w), static_cast<std::size_t>(n), with_norm != 0, d_out,
+             as_stream(stream));
+  });
+}
+
+extern "C" int emie_cu_vec_update(double* d_w, const double* d_V, long long vstride, int nv, const double* d_h,
+                                  long long n, double* d_dots_out, double* d_norm_out, void* stream) {
+  return guarded([&] {
+    if (!d_w || nv < 0 || n < 1 || (nv > 0 && (!d_V || !d_h)) || (d_dots_out && d_norm_out))
+      fail(EMIE_CU_INVALID_ARGUMENT, "vec_update: bad arguments");
+    vec_update(reinterpret_cast<cplx*>(d_w), reinterpret_cast<const cplx*>(d_V), static_cast<std::size_t>(vstride),
+               nv, d_h, static_cast<std::size_t>(n), d_dots_out, d_norm_out, as_stream(stream));
+  });
+}
+
+extern "C" int emie_cu_vec_combine(double* d_x, const double* d_V, long long vstride, int nv, const double* d_y,
+                                   long long n, void* stream) {
+  return guarded([&] {
+    if (!d_x || nv < 0 || n < 1 || (nv > 0 && (!d_V || !d_y))) fail(EMIE_CU_INVALID_ARGUMENT, "vec_combine: bad arguments");
+    vec_combine(reinterpret_cast<cplx*>(d_x), reinterpret_cast<const cplx*>(d_V), static_cast<std::size_t>(vstride),
+                nv, d_y, static_cast<std::size_t>(n), as_stream(stream));
+  });
+}
+
+extern "C" int emie_cu_vec_scale(double* d_y, const double* d_x, double a, long long n, void* stream) {
+  return guarded([&] {
+    if (!d_y || !d_x || n < 1) fail(EMIE_CU_INVALID_ARGUMENT, "vec_scale: bad arguments");
+    vec_scale(reinterpret_cast<cplx*>(d_y), reinterpret_cast<const cplx*>(d_x), a, static_cast<std::size_t>(n),
+              as_stream(stream));
+  });
+}
+
+extern "C" int emie_cu_vec_residual(double* d_r, const double* d_b, const double* d_t, long long n,
+                                    double* d_norm_out, void* stream) {
+  return guarded([&] {
+    if (!d_r || !d_b || !d_t || !d_norm_out || n < 1) fail(EMIE_CU_INVALID_ARGUMENT, "vec_residual: bad arguments");
+    vec_residual(reinterpret_cast<cplx*>(d_r), reinterpret_cast<const cplx*>(d_b), reinterpret_cast<const cplx*>(d_t),
+                 static_cast<std::size_t>(n), d_norm_out, as_stream(stream));
+  });
+}
+
 extern "C" int emie_cu_profile_enable(int on) {
   return guarded([&] { prof().on = on != 0; });
 }

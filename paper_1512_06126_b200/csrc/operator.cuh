@@ -144,6 +144,17 @@ inline void release(void* p, cudaStream_t st) noexcept {
   if (p) (void)cudaFreeAsync(p, st);
 }
 
+// slab vector operations of the sharded FGMRES (solver.cu): local sums,
+// finalized on the device; the caller all-reduces them
+void vec_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::size_t n, bool with_norm,
+              double* out, cudaStream_t st);
+void vec_update(cplx* w, const cplx* V, std::size_t vstride, int nv, const double* h, std::size_t n,
+                double* dots_out, double* norm_out, cudaStream_t st);
+void vec_combine(cplx* x, const cplx* V, std::size_t vstride, int nv, const double* y, std::size_t n,
+                 cudaStream_t st);
+void vec_scale(cplx* y, const cplx* x, double a, std::size_t n, cudaStream_t st);
+void vec_residual(cplx* r, const cplx* b, const cplx* t, std::size_t n, double* norm_out, cudaStream_t st);
+
 void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, double tol,
                    int m, int max_iters, emie_cu_report* reports, double* h_history,
                    int hist_cap, cudaStream_t st);

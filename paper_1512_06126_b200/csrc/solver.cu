@@ -763,5 +763,88 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
   EMIE_CUDA(cudaStreamSynchronize(st));
 }
 
-}  // namespace emie_cu
+// ---- slab vector operations of the sharded FGMRES (distributed.py) --------
+// Local sums over this rank's slab, finalized on the device into `out`; the
+// caller all-reduces them across ranks. Same kernels as fgmres_device.
+void vec_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::size_t n, bool with_norm,
+              double* out, cudaStream_t st) {
+  const int ps = 2 * nv + 2;
+  const int nvals = 2 * nv + (with_norm ? 1 : 0);
+  double* partial = scratch<double>(static_cast<std::size_t>(std::max(red_blocks(n), kCgsBlocks)) * ps, st);
+  int g;
+  if (nv >= 1 && nv <= kTileMaxV) {
+    g = cgs_launch<0>(const_cast<cplx*>(w), V, vstride, nv, nullptr, n, partial, ps, with_norm ? 1 : 0, st);
+  } else {
+    g = red_blocks(n);
+    dots_kernel<<<g, kRedThreads, 0, st>>>(V, vstride, nv, w, n, partial, ps, with_norm ? 1 : 0);
+    check_launch("dots_kernel");
+  }
+  if (nvals > 0) {
+    finalize_kernel<<<nvals, kFinThreads, 0, st>>>(partial, g, ps, nvals, out);
+    check_launch("finalize_kernel");
+  }
+  release(partial, st);
+}
 
+void vec_update(cplx* w, const cplx* V, std::size_t vstride, int nv, const double* h, std::size_t n,
+                double* dots_out, double* norm_out, cudaStream_t st) {
+  const int ps = 2 * nv + 2;
+  double* partial = scratch<double>(static_cast<std::size_t>(std::max(red_blocks(n), kCgsBlocks)) * ps, st);
+  const bool tiled = nv >= 1 && nv <= kTileMaxV;
+  if (tiled && dots_out && !norm_out) {
+    const int g = cgs_launch<1>(w, V, vstride, nv, h, n, partial, ps, 0, st);
+    finalize_kernel<<<2 * nv, kFinThreads, 0, st>>>(partial, g, ps, 2 * nv, dots_out);
+    check_launch("finalize_kernel");
+  } else if (tiled && !dots_out) {
+    const int g = cgs_launch<2>(w, V, vstride, nv, h, n, partial, 1, 0, st);
+    if (norm_out) {
+      finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+      check_launch("finalize_kernel");
+    }
+  } else {
+    const int g = red_blocks(n);
+    if (nv > 0) {
+      update_kernel<<<g, kRedThreads, 0, st>>>(w, V, vstride, nv, h, n, norm_out ? partial : nullptr);
+      check_launch("update_kernel");
+    }
+    if (norm_out) {
+      if (nv == 0) {
+        dots_kernel<<<g, kRedThreads, 0, st>>>(w, 0, 0, w, n, partial, 1, 1);
+        check_launch("dots_kernel");
+      }
+      finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+      check_launch("finalize_kernel");
+    }
+    if (dots_out && nv > 0) {
+      dots_kernel<<<g, kRedThreads, 0, st>>>(V, vstride, nv, w, n, partial, ps, 0);
+      check_launch("dots_kernel");
+      finalize_kernel<<<2 * nv, kFinThreads, 0, st>>>(partial, g, ps, 2 * nv, dots_out);
+      check_launch("finalize_kernel");
+    }
+  }
+  release(partial, st);
+}
+
+void vec_combine(cplx* x, const cplx* V, std::size_t vstride, int nv, const double* y, std::size_t n,
+                 cudaStream_t st) {
+  if (nv < 1) return;
+  combine_kernel<<<red_blocks(n), 256, 0, st>>>(x, V, vstride, nv, y, n);
+  check_launch("combine_kernel");
+}
+
+void vec_scale(cplx* y, const cplx* x, double a, std::size_t n, cudaStream_t st) {
+  scale_kernel<<<red_blocks(n), 256, 0, st>>>(y, x, a, n);
+  check_launch("scale_kernel");
+}
+
+void vec_residual(cplx* r, const cplx* b, const cplx* t, std::size_t n, double* norm_out, cudaStream_t st) {
+  const int g = red_blocks(n);
+  double* partial = scratch<double>(static_cast<std::size_t>(g), st);
+  residual_kernel<<<g, kRedThreads, 0, st>>>(r, b, t, n, partial);
+  check_launch("residual_kernel");
+  finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+  check_launch("finalize_kernel");
+  release(partial, st);
+}
+
+}  // namespace emie_cu

@@ -58,3 +58,36 @@ def test_mode_shard_rejects_foreign_modes(torch_cuda):
         emie.apply(shard, np.zeros(3 * cfg.cells(), np.complex128))
     with pytest.raises(emie.OutOfRange):
         emie.restrict_modes(shard, 0, 5)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_sharded_solve_loopback_matches_single_gpu(torch_cuda, G):
+    """FGMRES on depth-sharded vectors (distributed_solve.py: the slab vector
+    kernels emie_cu_vec_*, local sums summed over the ranks) against the
+    single-GPU device solve on the same system: same iteration counts, same
+    solution to the rounding of the rank-partitioned sums."""
+    torch = torch_cuda
+    from paper_1512_06126_b200 import normal_field as NF
+    from paper_1512_06126_b200 import distributed_solve as DS
+    cfg, grid, sop, sysop = _system(1)
+    rhs = np.stack([NF.build_rhs(cfg.tops, cfg.sigma, cfg.breaks, cfg.nx, cfg.ny, cfg.omega, p).reshape(-1)
+                    for p in ("x", "y")])
+    nrhs = 2
+    x1, reps1 = emie.fgmres_system(sysop, rhs, emie.SolverConfig(tol=1e-8, restart=40, max_iters=300))
+    emie.xy_symmetric(sop, disable=True)  # the shards contract quadrant modes (same as the reference order)
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    ops = [DS.CudaSlabOps() for _ in range(G)]
+    slabs = [torch.from_numpy(D.slab_of(rhs, plan, g, nrhs).reshape(nrhs, -1)).cuda() for g in range(G)]
+
+    def apply(U):
+        outs = D.loopback_apply(shards, [u.reshape(-1) for u in U])
+        return [o.reshape(nrhs, -1) for o in outs]
+
+    xs, reps = DS.fgmres_sharded(apply, ops, DS.LoopbackReducer(), slabs, tol=1e-8, restart=40, max_iters=300)
+    x = D.join_slabs([t.cpu().numpy() for t in xs], plan, nrhs)
+    for i in range(nrhs):
+        assert reps[i].status == reps1[i].status == "converged"
+        assert reps[i].iterations == reps1[i].iterations
+        assert np.linalg.norm(x[i] - x1[i]) <= 1e-10 * np.linalg.norm(x1[i])
+        assert abs(reps[i].residual - reps1[i].residual) <= 1e-6 * reps1[i].residual

@@ -155,3 +155,102 @@ def test_sharded_apply_loopback_numpy(G):
     outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)) for g in range(G)])
     got = D.join_slabs([o.numpy() for o in outs], plan, nrhs)
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+
+
+# ---- FGMRES on depth-sharded vectors -------------------
+def _solve_case(nx=6, ny=5, nz=4, nrhs=2, seed=21):
+    import emie_oracle as O
+    rng = np.random.default_rng(seed)
+    nent = 2 * nz * (2 * nz + 1)
+    blocks = 2e-3 * (rng.standard_normal((ny, nx, nent)) + 1j * rng.standard_normal((ny, nx, nent)))
+    dims, comp = O.transform_operator(blocks, nx, ny, nz)
+    m = O.LayeredModel([0.0, 5000.0], [0.0, 0.01, 0.1])
+    breaks = list(np.linspace(10.0, 10.0 + 50.0 * nz, nz + 1))
+    sa = 10.0 ** rng.uniform(-3, 0, (nz, ny, nx))
+    grid = O.make_grid(m, breaks, nx, ny, 100.0, 120.0, sa)
+    diag = O.system_diagonals(grid)
+    B = rng.standard_normal((nrhs, 3 * nx * ny * nz)) + 1j * rng.standard_normal((nrhs, 3 * nx * ny * nz))
+    A = lambda x: O.apply_system(diag, lambda v: O.apply_spectral(comp, dims, nx, ny, nz, v), x)  # noqa: E731
+    want = [O.fgmres(A, b, tol=1e-10, restart=8, max_iters=200) for b in B]
+    return dims, comp, diag, B, want
+
+
+def _numpy_sharded_solve(G, ranks, dims, comp, diag, B, reduce, dist_apply=None):
+    import torch
+    from paper_1512_06126_b200 import distributed as D
+    from paper_1512_06126_b200 import distributed_solve as DS
+    nx, ny, nz, nrhs = 6, 5, 4, B.shape[0]
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G)
+    shards, ops, rhs = [], [], []
+    for g in ranks:
+        z0, z1 = plan.z[g], plan.z[g + 1]
+        dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
+        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+        ops.append(DS.NumpySlabOps())
+        rhs.append(torch.from_numpy(D.slab_of(B, plan, g, nrhs).reshape(nrhs, -1)))
+    if dist_apply is None:
+        def apply(U):
+            outs = D.loopback_apply(shards, [u.reshape(-1) for u in U])
+            return [o.reshape(nrhs, -1) for o in outs]
+    else:
+        sysd = D.DistributedSystem(shards[0])
+
+        def apply(U):
+            return [sysd.apply(U[0].reshape(-1)).reshape(nrhs, -1)]
+    x, reps = DS.fgmres_sharded(apply, ops, reduce, rhs, tol=1e-10, restart=8, max_iters=200)
+    return plan, x, reps
+
+
+def _check_solve(x_full, reps, want):
+    for i, (wx, wrep) in enumerate(want):
+        assert reps[i].status == "converged" and wrep["status"] == "converged"
+        assert abs(reps[i].iterations - wrep["iterations"]) <= 1
+        assert np.linalg.norm(x_full[i] - wx) <= 1e-8 * np.linalg.norm(wx)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_sharded_solve_loopback_numpy(G):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    from paper_1512_06126_b200 import distributed as D
+    from paper_1512_06126_b200 import distributed_solve as DS
+    dims, comp, diag, B, want = _solve_case()
+    plan, x, reps = _numpy_sharded_solve(G, list(range(G)), dims, comp, diag, B, DS.LoopbackReducer())
+    _check_solve(D.join_slabs([t.numpy() for t in x], plan, B.shape[0]), reps, want)
+
+
+def _solve_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1512_06126_b200 import distributed_solve as DS
+    dims, comp, diag, B, _ = _solve_case()
+    plan, x, reps = _numpy_sharded_solve(world, [rank], dims, comp, diag, B, DS.TorchReducer(), dist_apply=True)
+    parts = [None] * world
+    dist.all_gather_object(parts, x[0].numpy())
+    if rank == 0:
+        q.put((parts, [(r.status, r.iterations) for r in reps]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_solve_gloo_matches_oracle():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    from paper_1512_06126_b200 import distributed as D
+    from paper_1512_06126_b200 import SolveReport
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts, reps = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dims, comp, diag, B, want = _solve_case()
+    plan = D.ShardPlan(6, 5, 4, dims[0], dims[1], 2)
+    x = D.join_slabs(parts, plan, B.shape[0])
+    _check_solve(x, [SolveReport(s, it) for s, it in reps], want)
