@@ -224,6 +224,32 @@ int emie_cu_lateral_inverse(emie_cu_operator geom, const double* d_S, const doub
  * full-depth spectrum d_S (all modes' storage, only these modes touched) */
 int emie_cu_contract_modes(emie_cu_operator op, double* d_S, int nrhs, int q0, int q1, void* stream);
 
+/* ---- sharded Green's build (SURVEY.md §8(e).3 "Green's build sharding:
+ * offsets are independent"): assemble_operator (greens.cpp:332-371) split
+ * over ranks by offset, the per-offset work (filter design, lambda
+ * accumulation: greens.cpp:133-221) being the dominant cost. Each rank
+ * computes its range of the build's computed offsets into a zeroed
+ * full-size block array; the caller sums the arrays across ranks (every
+ * offset is written by exactly one rank, so the sum is exact); every rank
+ * then runs the mirror and transform_operator (toeplitz.cpp:92-161) for its
+ * own quadrant-mode shard only. */
+
+/* the offsets oi*nx + oj a build computes (all, or oi <= oj on a square
+ * grid with hx == hy, the rest being mirrors); *count = their number */
+int emie_cu_greens_offsets(int nx, int ny, double hx, double hy, int* h_offs, int cap, int* count);
+
+/* blocks of computed offsets [c0, c1) into d_blocks (nx*ny*2nz(2nz+1)
+ * complex, offset-major GreensBlock order; other offsets untouched) */
+int emie_cu_greens_blocks(int L, const double* tops, const double* sigma, int nz, const double* breaks, int nx,
+                          int ny, double hx, double hy, double omega, const double* filter, int c0, int c1,
+                          double* d_blocks, void* stream);
+
+/* the operator of quadrant modes [q0, q1) (q1 < 0: all) from the summed
+ * blocks of every computed offset (d_blocks is completed in place by the
+ * mirror) */
+int emie_cu_operator_from_greens_blocks(int nx, int ny, int nz, double omega, double hx, double hy,
+                                        double* d_blocks, int q0, int q1, emie_cu_operator* out, void* stream);
+
 /* ---- sharded FGMRES vector operations ("FGMRES on
  * depth-sharded vectors: local partial dots, then an all-reduce"). The
  * vector kernels of src/cie.cpp:77-98 (dot, norm, axpy, scaled) as batched

@@ -102,6 +102,19 @@ def lib():
                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, ctypes.c_int,
                                  ctypes.POINTER(vp), vp],
         "emie_cu_operator_dims": [vp, ip, dp],
+        "emie_cu_greens_offsets": [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ip, ctypes.c_int,
+                                   ip],
+        "emie_cu_greens_blocks": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, ctypes.c_int,
+                                  ctypes.c_int, vp, vp],
+        "emie_cu_operator_from_greens_blocks": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                ctypes.c_double, ctypes.c_double, vp, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(vp), vp],
+        "emie_cu_vec_dots": [vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, ctypes.c_int, vp, vp],
+        "emie_cu_vec_update": [vp, vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp, vp, vp],
+        "emie_cu_vec_combine": [vp, vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp],
+        "emie_cu_vec_scale": [vp, vp, ctypes.c_double, ctypes.c_longlong, vp],
+        "emie_cu_vec_residual": [vp, vp, vp, ctypes.c_longlong, vp, vp],
         "emie_cu_operator_xy_symmetry": [vp, ctypes.c_int, ip],
         "emie_cu_operator_download_spectra": [vp, vp],
         "emie_cu_operator_download_blocks": [vp, vp],
@@ -373,6 +386,44 @@ def assemble_operator(grid: AnomalyGrid, model: LayeredModel, omega: float,
     _check(lib().emie_cu_greens_build(len(tops), _ptr(tops), _ptr(sig), grid.nz, _ptr(br), grid.nx,
                                       grid.ny, grid.hx, grid.hy, float(omega), _ptr(fp),
                                       int(keep_blocks), ctypes.byref(h), None))
+    return SpectralOperator(h)
+
+
+def greens_offsets(nx: int, ny: int, hx: float, hy: float) -> np.ndarray:
+    """Offsets oi*nx + oj the Green's build computes (the rest are x <-> y
+    mirrors on square grids with hx == hy); the sharded build splits these."""
+    L = lib()
+    n = ctypes.c_int()
+    _check(L.emie_cu_greens_offsets(int(nx), int(ny), float(hx), float(hy), None, 0, ctypes.byref(n)))
+    out = np.zeros(max(1, n.value), np.int32)
+    _check(L.emie_cu_greens_offsets(int(nx), int(ny), float(hx), float(hy),
+                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), n.value, ctypes.byref(n)))
+    return out[:n.value]
+
+
+def greens_blocks(grid: AnomalyGrid, model: LayeredModel, omega: float, c0: int, c1: int, d_blocks,
+                  params: Optional[FilterParams] = None) -> None:
+    """Blocks of computed offsets [c0, c1) (greens_offsets order) into the
+    complex128 CUDA tensor d_blocks (ny, nx, 2nz(2nz+1)); other offsets untouched."""
+    model.validate()
+    grid.validate(model)
+    tops = np.ascontiguousarray(model.tops, dtype=np.float64)
+    sig = _c128(model.sigma)
+    br = np.ascontiguousarray(grid.breaks, dtype=np.float64)
+    fp = (params or FilterParams()).as_array()
+    _check(lib().emie_cu_greens_blocks(len(tops), _ptr(tops), _ptr(sig), grid.nz, _ptr(br), grid.nx, grid.ny,
+                                       grid.hx, grid.hy, float(omega), _ptr(fp), int(c0), int(c1),
+                                       ctypes.c_void_p(d_blocks.data_ptr()), _stream_of(d_blocks)))
+
+
+def operator_from_greens_blocks(grid: AnomalyGrid, omega: float, d_blocks, q0: int = 0,
+                                q1: int = -1) -> SpectralOperator:
+    """Mirror + transform_operator of quadrant modes [q0, q1) from the summed
+    computed blocks (d_blocks is completed in place)."""
+    h = ctypes.c_void_p()
+    _check(lib().emie_cu_operator_from_greens_blocks(grid.nx, grid.ny, grid.nz, float(omega), grid.hx, grid.hy,
+                                                     ctypes.c_void_p(d_blocks.data_ptr()), int(q0), int(q1),
+                                                     ctypes.byref(h), _stream_of(d_blocks)))
     return SpectralOperator(h)
 
 

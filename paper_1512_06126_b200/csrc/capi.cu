@@ -491,6 +491,54 @@ int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
   });
 }
 
+int emie_cu_greens_offsets(int nx, int ny, double hx, double hy, int* h_offs, int cap, int* count) {
+  return guarded([&] {
+    if (nx < 1 || ny < 1 || !count) fail(EMIE_CU_INVALID_ARGUMENT, "greens_offsets: bad arguments");
+    const std::vector<int> offs = computed_offsets(nx, ny, hx, hy);
+    *count = static_cast<int>(offs.size());
+    if (h_offs)
+      for (int i = 0; i < cap && i < static_cast<int>(offs.size()); ++i) h_offs[i] = offs[i];
+  });
+}
+
+int emie_cu_greens_blocks(int L, const double* tops, const double* sigma, int nz, const double* breaks, int nx,
+                          int ny, double hx, double hy, double omega, const double* filter, int c0, int c1,
+                          double* d_blocks, void* stream) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || !d_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "greens_blocks: null pointer");
+    FilterParams fp;
+    if (filter) {
+      fp.step = filter[0];
+      fp.shift = filter[1];
+      fp.half = static_cast<int>(filter[2]);
+      fp.n1 = static_cast<int>(filter[3]);
+      fp.n2 = static_cast<int>(filter[4]);
+    }
+    check_filter_params(fp);
+    Operator geom;
+    init_operator_geometry(geom, nx, ny, nz, omega, 0, 0);
+    greens_blocks(geom, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, fp, c0, c1,
+                  reinterpret_cast<cplx*>(d_blocks), as_stream(stream));
+  });
+}
+
+int emie_cu_operator_from_greens_blocks(int nx, int ny, int nz, double omega, double hx, double hy,
+                                        double* d_blocks, int q0, int q1, emie_cu_operator* out, void* stream) {
+  return guarded([&] {
+    if (!out || !d_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "operator_from_greens_blocks: null pointer");
+    auto h = std::make_unique<emie_cu_operator_s>();
+    Operator& op = h->op;
+    const int nq = ((smooth_size(2 * nx - 1) / 2) + 1) * ((smooth_size(2 * ny - 1) / 2) + 1);
+    if (q1 < 0) q1 = nq;
+    if (q0 < 0 || q1 > nq || q0 >= q1) fail(EMIE_CU_OUT_OF_RANGE, "operator_from_greens_blocks: mode range");
+    init_operator_geometry(op, nx, ny, nz, omega, q0, q1);
+    const cudaStream_t st = as_stream(stream);
+    greens_finish(op, reinterpret_cast<cplx*>(d_blocks), hx, hy, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+    *out = h.release();
+  });
+}
+
 int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy, const double* filter,
                                   double* h_w, double* h_lam) {
   return guarded([&] {

@@ -984,8 +984,22 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
   for (int m = fp.n1; m <= fp.n2; ++m) lam[m - fp.n1] = std::exp(m * fp.step + fp.shift);
 }
 
-void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
-                  double hx, double hy, const FilterParams& fp, bool keep_blocks, cudaStream_t st) {
+// The computed offsets of a build: all, or on a square grid with hx == hy only
+// oi <= oj (the rest by the x <-> y mirror, mirror_blocks_kernel)
+std::vector<int> computed_offsets(int nx, int ny, double hx, double hy) {
+  const bool mirror = nx == ny && hx == hy;
+  std::vector<int> offs;
+  for (int oi = 0; oi < ny; ++oi)
+    for (int oj = 0; oj < nx; ++oj)
+      if (!(mirror && oi > oj)) offs.push_back(oi * nx + oj);
+  return offs;
+}
+
+// Blocks of computed offsets [c0, c1) (positions in computed_offsets) into
+// `blocks` (nx*ny*nent complex, offset-major; other offsets untouched):
+// filter design (K6) and the lambda accumulation (K5).
+void greens_blocks(const Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
+                   double hx, double hy, const FilterParams& fp, int c0, int c1, cplx* blocks, cudaStream_t st) {
   // ---- host validation: LayeredModel::validate, VerticalPartition::create,
   // AnomalyGrid::validate (layered.cpp:53-65, 191-208; greens.cpp:18-35)
   if (L < 1) fail(EMIE_CU_INVALID_ARGUMENT, "layered model needs at least one interface");
@@ -1067,22 +1081,14 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
 
   keep_pool_warm();
   const int noff = op.nx * op.ny;
-  // offsets computed: all, or on a square grid with hx == hy only oi <= oj
-  // (the rest by the x <-> y mirror, mirror_blocks_kernel)
-  const bool mirror = op.nx == op.ny && hx == hy;
-  std::vector<int> offs_h, pairs_h;
-  for (int oi = 0; oi < op.ny; ++oi)
-    for (int oj = 0; oj < op.nx; ++oj) {
-      if (mirror && oi > oj) continue;
-      offs_h.push_back(oi * op.nx + oj);
-      if (mirror && oi < oj) pairs_h.push_back(oi * op.nx + oj);
-    }
+  const std::vector<int> all = computed_offsets(op.nx, op.ny, hx, hy);
+  const int cb = std::max(0, std::min(c0, static_cast<int>(all.size())));
+  const int ce = c1 < 0 ? static_cast<int>(all.size()) : std::max(cb, std::min(c1, static_cast<int>(all.size())));
+  if (ce == cb) return;
+  const std::vector<int> offs_h(all.begin() + cb, all.begin() + ce);
   const int ncomp = static_cast<int>(offs_h.size());
-  int* offs = scratch<int>(offs_h.size() + pairs_h.size(), st);
-  int* pairs = offs + offs_h.size();
+  int* offs = scratch<int>(offs_h.size(), st);
   EMIE_CUDA(cudaMemcpyAsync(offs, offs_h.data(), offs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  if (!pairs_h.empty())
-    EMIE_CUDA(cudaMemcpyAsync(pairs, pairs_h.data(), pairs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   FilterBank fb = make_filter_bank(fp, st);
   double* W = scratch<double>(static_cast<size_t>(noff) * 6 * P.nw, st);
   int* err = scratch<int>(1, st);
@@ -1091,8 +1097,6 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
 
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
-  cplx* blocks = nullptr;
-  EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(noff) * op.nent * sizeof(cplx) + 16));
   const int NL = L + 1;
   const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 12 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
@@ -1109,18 +1113,6 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
 #endif
   assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs);
   check_launch("assemble_kernel");
-  if (!pairs_h.empty()) {
-    const long long total = static_cast<long long>(pairs_h.size()) * op.nent;
-    mirror_blocks_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
-        blocks, pairs, static_cast<int>(pairs_h.size()), op.nx, op.ntri, op.nfull, op.nent);
-    check_launch("mirror_blocks_kernel");
-  }
-  if (mirror) {
-    const long long total = static_cast<long long>(op.nx) * (op.ntri + op.nfull);
-    symmetrize_diagonal_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
-        blocks, op.nx, op.ntri, op.nfull, op.nent);
-    check_launch("symmetrize_diagonal_kernel");
-  }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {
     unsigned long long h[8];
@@ -1144,13 +1136,52 @@ void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, co
   release(offs, st);
   free_filter_bank(fb, st);
   if (e) {
-    cudaFree(blocks);
     raise_filter_errors(e);
     fail(EMIE_CU_DOMAIN_ERROR, "assemble_block: non-finite block entry");
+  }
+}
+
+// The rest of the build once every computed offset's block is in `blocks`:
+// the x <-> y mirror of the other offsets and the symmetrised diagonal
+// offsets (square grids with hx == hy), then the spectra (K7) of the modes
+// op stores.
+void greens_finish(Operator& op, cplx* blocks, double hx, double hy, cudaStream_t st) {
+  const bool mirror = op.nx == op.ny && hx == hy;
+  if (mirror) {
+    std::vector<int> pairs_h;
+    for (int oi = 0; oi < op.ny; ++oi)
+      for (int oj = oi + 1; oj < op.nx; ++oj) pairs_h.push_back(oi * op.nx + oj);
+    if (!pairs_h.empty()) {
+      int* pairs = scratch<int>(pairs_h.size(), st);
+      EMIE_CUDA(cudaMemcpyAsync(pairs, pairs_h.data(), pairs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      const long long total = static_cast<long long>(pairs_h.size()) * op.nent;
+      mirror_blocks_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
+          blocks, pairs, static_cast<int>(pairs_h.size()), op.nx, op.ntri, op.nfull, op.nent);
+      check_launch("mirror_blocks_kernel");
+      release(pairs, st);
+    }
+    const long long total = static_cast<long long>(op.nx) * (op.ntri + op.nfull);
+    symmetrize_diagonal_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 4096)), 256, 0, st>>>(
+        blocks, op.nx, op.ntri, op.nfull, op.nent);
+    check_launch("symmetrize_diagonal_kernel");
   }
   profile_mark(6, true, st);
   transform_blocks(op, blocks, st, mirror ? -1 : 0);  // checked: the octant path needs bitwise symmetry
   profile_mark(6, false, st);
+}
+
+void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
+                  double hx, double hy, const FilterParams& fp, bool keep_blocks, cudaStream_t st) {
+  cplx* blocks = nullptr;
+  EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(op.nx) * op.ny * op.nent * sizeof(cplx) + 16));
+  try {
+    greens_blocks(op, L, tops, sigma, breaks, hx, hy, fp, 0, -1, blocks, st);
+    greens_finish(op, blocks, hx, hy, st);
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    cudaFree(blocks);
+    throw;
+  }
   if (keep_blocks) {
     op.blocks = blocks;
   } else {

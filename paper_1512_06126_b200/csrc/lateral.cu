@@ -132,7 +132,7 @@ template <bool P2>
 __global__ void __launch_bounds__(256, 2) spectra_y_kernel(const cplx* __restrict__ R, cplx* __restrict__ spec,
                                  const cplx* __restrict__ tw, FftPlan pl, int ny, int qx, int qy,
                                  int nent, int ntri, int nfull, int EC, const int2* __restrict__ emap,
-                                 int nentD) {
+                                 int nentD, int qbase, int qcount) {
   extern __shared__ cplx sm[];
   const int ey = pl.n;
   Tile<P2> T(sm, EC, ey);
@@ -158,9 +158,10 @@ __global__ void __launch_bounds__(256, 2) spectra_y_kernel(const cplx* __restric
   for (int idx = threadIdx.x; idx < EC * qy; idx += blockDim.x) {
     const int tt = idx % EC, my = idx / EC;
     const int e = e0 + tt;
-    if (e < nent) {
+    const int qm = my * qx + mx;  // stored: quadrant modes [qbase, qbase + qcount)
+    if (e < nent && qm >= qbase && qm < qbase + qcount) {
       const int2 m = emap[e];
-      cplx* blk = spec + (static_cast<size_t>(my) * qx + mx) * nentD;
+      cplx* blk = spec + static_cast<size_t>(qm - qbase) * nentD;
       const cplx v = res[T.at(tt, my)];
       blk[m.x] = v;
       if (m.y >= 0) blk[m.y] = v;
@@ -997,12 +998,12 @@ void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) 
       set_smem(reinterpret_cast<const void*>(spectra_y_kernel<true>), smem);
       spectra_y_kernel<true><<<grid, kFftThreads, smem, st>>>(R, op.spec, op.tw_y, pl, op.ny, op.qx, op.qy,
                                                               nent, op.ntri, op.nfull, EC, op.emap,
-                                                              op.nentD);
+                                                              op.nentD, op.qbase, op.qcount);
     } else {
       set_smem(reinterpret_cast<const void*>(spectra_y_kernel<false>), smem);
       spectra_y_kernel<false><<<grid, 256, smem, st>>>(R, op.spec, op.tw_y, pl, op.ny, op.qx, op.qy,
                                                        nent, op.ntri, op.nfull, EC, op.emap,
-                                                       op.nentD);
+                                                       op.nentD, op.qbase, op.qcount);
     }
     check_launch("spectra_y_kernel");
   }

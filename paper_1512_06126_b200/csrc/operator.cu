@@ -505,7 +505,8 @@ void set_smem(const void* fn, size_t bytes) {
 void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int sym_known) {
   lateral_spectra(op, d_blocks, st);
   bool sym = false;
-  if (op.nx == op.ny && op.ex == op.ey && op.mma && sym_known != 0) {
+  const bool full = op.qbase == 0 && op.qcount == static_cast<int>(op.modes());
+  if (full && op.nx == op.ny && op.ex == op.ey && op.mma && sym_known != 0) {
     sym = true;
     if (sym_known < 0) {
       int* bad = scratch<int>(1, st);

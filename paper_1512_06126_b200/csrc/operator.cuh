@@ -117,6 +117,12 @@ void check_filter_params(const FilterParams& fp);
 void greens_build(Operator& op, int L, const double* tops, const cplx* sigma,
                   const double* breaks, double hx, double hy, const FilterParams& fp,
                   bool keep_blocks, cudaStream_t st);
+// the build in two parts (sharded build): the blocks of computed offsets
+// [c0, c1) of computed_offsets(), then mirror + spectra of op's stored modes
+std::vector<int> computed_offsets(int nx, int ny, double hx, double hy);
+void greens_blocks(const Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
+                   double hx, double hy, const FilterParams& fp, int c0, int c1, cplx* blocks, cudaStream_t st);
+void greens_finish(Operator& op, cplx* blocks, double hx, double hy, cudaStream_t st);
 void kernel_output_host(int oi, int oj, double hx, double hy, int alpha, int beta,
                         const double* s, int n, double* out);
 void design_offset_filters_host(int oi, int oj, double hx, double hy, const FilterParams& fp,

@@ -343,13 +343,64 @@ class NumpyBackend:
         d_arr[md * ddesc[1] + c * ddesc[2] + ddesc[3] + z] = s_arr[ms * sdesc[1] + c * sdesc[2] + sdesc[3] + z]
 
 
-def cuda_shard(grid, sop_full, plan: ShardPlan, rank: int, nrhs: int) -> ShardedApply:
+def greens_offset_ranges(n_offsets: int, G: int) -> List[tuple]:
+    """Contiguous ranges of the build's computed offsets per rank (every
+    offset costs the same: all nz(nz+1)/2 pairs over the same 451 lambdas)."""
+    s = _splits(n_offsets, G)
+    return [(s[g], s[g + 1]) for g in range(G)]
+
+
+def sharded_greens_build(grid, model, omega: float, plan: ShardPlan, ranks: Sequence[int], reduce_blocks,
+                         params=None):
+    """The Green's build sharded by offset: each listed
+    rank computes its range of the computed offsets into a zeroed block array,
+    reduce_blocks sums the arrays over all ranks (every offset is written by
+    one rank, so the sum is exact) and returns each listed rank's copy; each
+    rank then builds the spectra of its own quadrant-mode shard.
+    Returns the per-rank mode-shard operators (SpectralOperator)."""
+    import torch
+    from . import greens_offsets, greens_blocks, operator_from_greens_blocks
+    offs = greens_offsets(grid.nx, grid.ny, grid.hx, grid.hy)
+    rng = greens_offset_ranges(len(offs), plan.G)
+    nent = 2 * grid.nz * (2 * grid.nz + 1)
+    bufs = []
+    for g in ranks:
+        b = torch.zeros((grid.ny, grid.nx, nent), dtype=torch.complex128, device="cuda")
+        greens_blocks(grid, model, omega, rng[g][0], rng[g][1], b, params)
+        bufs.append(b)
+    full = reduce_blocks(bufs)
+    return [operator_from_greens_blocks(grid, omega, full[i], plan.q[g], plan.q[g + 1])
+            for i, g in enumerate(ranks)]
+
+
+def loopback_block_sum(bufs):
+    """Virtual ranks in one process: the all-reduce of the block arrays (rank
+    order); every rank gets its own copy (the mirror completes it in place)."""
+    tot = bufs[0].clone()
+    for b in bufs[1:]:
+        tot += b
+    return [tot.clone() for _ in bufs]
+
+
+def torch_block_sum(group=None):
+    """One rank per process: all-reduce (sum) of the rank's block array."""
+    import torch.distributed as dist
+
+    def red(bufs):
+        (b,) = bufs
+        dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+        return [b]
+    return red
+
+
+def cuda_shard(grid, sop_full, plan: ShardPlan, rank: int, nrhs: int, op_shard=None) -> ShardedApply:
     """Rank `rank`'s sharded apply on the current CUDA device: the mode shard
-    of sop_full's spectra, the lateral geometry and system diagonals of the
+    of sop_full's spectra (or the given op_shard), the lateral geometry and system diagonals of the
     depth slab (build_system, cie.cpp:24-54, restricted to its cells)."""
     from . import restrict_modes
     z0, z1 = plan.z[rank], plan.z[rank + 1]
-    op_shard = restrict_modes(sop_full, plan.q[rank], plan.q[rank + 1])
+    if op_shard is None:  # cut from a full operator (or built sharded: sharded_greens_build)
+        op_shard = restrict_modes(sop_full, plan.q[rank], plan.q[rank + 1])
     sa = np.asarray(grid.sigma_a)[z0:z1]
     sb = np.asarray(grid.sigma_b)[z0:z1]
     vol = np.array([grid.volume(iz) for iz in range(z0, z1)], dtype=np.float64)

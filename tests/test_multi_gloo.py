@@ -254,3 +254,19 @@ def test_sharded_solve_gloo_matches_oracle():
     plan = D.ShardPlan(6, 5, 4, dims[0], dims[1], 2)
     x = D.join_slabs(parts, plan, B.shape[0])
     _check_solve(x, [SolveReport(s, it) for s, it in reps], want)
+
+
+def test_greens_offset_ranges_partition():
+    """the sharded Green's build's split: every computed offset (all, or oi <= oj
+    on square grids with hx == hy) belongs to exactly one rank's range"""
+    import paper_1512_06126_b200 as emie
+    from paper_1512_06126_b200 import distributed as D
+    for nx, ny, hx, hy in [(16, 16, 500.0, 500.0), (12, 10, 100.0, 120.0), (8, 8, 100.0, 120.0), (1, 1, 1.0, 1.0)]:
+        offs = emie.greens_offsets(nx, ny, hx, hy)
+        mirror = nx == ny and hx == hy
+        want = [oi * nx + oj for oi in range(ny) for oj in range(nx) if not (mirror and oi > oj)]
+        assert list(offs) == want
+        for G in (1, 2, 3, 8):
+            rng = D.greens_offset_ranges(len(offs), G)
+            assert rng[0][0] == 0 and rng[-1][1] == len(offs)
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
