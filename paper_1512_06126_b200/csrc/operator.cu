@@ -65,10 +65,16 @@ __device__ __forceinline__ ModeCols mode_cols(int qm, int qx, int ex, int ey) {
   return mc;
 }
 
+// octv != nullptr (operator.xysym): work items are the codes 2 qm + sw of the
+// octant modes qm; sw = 1 applies qm's block to the transposed mode's columns
+// with their x and y thirds exchanged (the two halves of an item are adjacent
+// in the list, so they run on neighbouring warp groups of one CTA and share
+// the block through L1/L2: HBM reads the octant blocks once)
 template <int CB>
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     contract_kernel(const cplx* __restrict__ op, cplx* S, int nz, int nsd, int nentD, int ex,
-                    int ey, int qx, int q0, int q1, int qbase, int nrhs, int pair) {
+                    int ey, int qx, int q0, int q1, int qbase, int nrhs, int pair,
+                    const int* __restrict__ octv, int noctv) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = 3 * nz;
@@ -97,8 +103,25 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     if (pair) asm volatile("bar.sync %0, 64;" ::"r"(1 + group) : "memory");
     else __syncwarp();
   };
-  auto issue = [&](int qm, int buf) {
+  // work item v -> (block mode, column mode, swap)
+  auto item = [&](int v, int& qb, int& qc, bool& sw) {
+    if (octv) {
+      const int code = __ldg(octv + v);
+      qb = code >> 1;
+      sw = code & 1;
+      const int qy_ = qb / qx, qx_ = qb - qy_ * qx;
+      qc = sw ? qx_ * qx + qy_ : qb;
+    } else {
+      qb = qc = q0 + v;
+      sw = false;
+    }
+  };
+  const int nwork = octv ? noctv : q1 - q0;
+  auto issue = [&](int v, int buf) {
     if (lane == 0 && role == 0) {
+      int qb, qm;
+      bool sw;
+      item(v, qb, qm, sw);
       const ModeCols mc = mode_cols(qm, qx, ex, ey);
       const int ncol = mc.nmir * nrhs;
       mbar_expect_tx(mbar + buf, static_cast<uint32_t>(ncol * colbytes));
@@ -111,17 +134,22 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     }
   };
   uint32_t phase[2] = {0u, 0u};
-  if (q0 + gw < q1) issue(q0 + gw, 0);
+  if (gw < nwork) issue(gw, 0);
   int it = 0;
-  for (int qm = q0 + gw; qm < q1; qm += nw, ++it) {
+  for (int v = gw; v < nwork; v += nw, ++it) {
     const int buf = it & 1;
-    if (qm + nw < q1) issue(qm + nw, buf ^ 1);
+    if (v + nw < nwork) issue(v + nw, buf ^ 1);
     mbar_wait(mbar + buf, phase[buf]);
     phase[buf] ^= 1u;
     const cplx* U = ubase + static_cast<size_t>(buf) * CB * np;
+    int qb, qm;
+    bool sw;
+    item(v, qb, qm, sw);
+    // transposed-mode columns: x and y thirds exchanged on load and store
+    const int ox = sw ? nz : 0, oy = sw ? 0 : nz;
     const ModeCols mc = mode_cols(qm, qx, ex, ey);
     const int ncol = mc.nmir * nrhs;
-    const cplx* blk = op + static_cast<size_t>(qm - qbase) * nentD;
+    const cplx* blk = op + static_cast<size_t>(qb - qbase) * nentD;
     const int ntri = nz * (nz + 1) / 2;
     const cplx* Dxx = blk;
     const cplx* Dyy = blk + ntri;
@@ -172,7 +200,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
         // term-major: consecutive MACs hit different columns (independent)
         cplx u[CB];
 #pragma unroll
-        for (int c = 0; c < CB; ++c) u[c] = U[c * np + kp];
+        for (int c = 0; c < CB; ++c) u[c] = U[c * np + ox + kp];
 #pragma unroll
         for (int c = 0; c < CB; ++c) cmac(ax[c], cur.xx, u[c]);
 #pragma unroll
@@ -180,7 +208,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
 #pragma unroll
         for (int c = 0; c < CB; ++c) cmac(az[c], mxzt, u[c]);
 #pragma unroll
-        for (int c = 0; c < CB; ++c) u[c] = U[c * np + nz + kp];
+        for (int c = 0; c < CB; ++c) u[c] = U[c * np + oy + kp];
 #pragma unroll
         for (int c = 0; c < CB; ++c) cmac(ax[c], cur.xy, u[c]);
 #pragma unroll
@@ -203,8 +231,8 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
           if (c < ncol) {
             const int mi = c / nrhs, r = c - mi * nrhs;
             cplx* o = S + (static_cast<size_t>(r) * E + mc.mode[mi]) * np;
-            o[k] = ax[c];
-            o[nz + k] = ay[c];
+            o[ox + k] = ax[c];
+            o[oy + k] = ay[c];
             o[2 * nz + k] = az[c];
           }
         }
@@ -506,7 +534,7 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int s
   lateral_spectra(op, d_blocks, st);
   bool sym = false;
   const bool full = op.qbase == 0 && op.qcount == static_cast<int>(op.modes());
-  if (full && op.nx == op.ny && op.ex == op.ey && op.mma && sym_known != 0) {
+  if (full && op.nx == op.ny && op.ex == op.ey && sym_known != 0) {
     sym = true;
     if (sym_known < 0) {
       int* bad = scratch<int>(1, st);
@@ -525,7 +553,7 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int s
   op.xysym = sym;
   cudaFree(op.octl);
   op.octl = nullptr;
-  op.noct = 0;
+  op.noct = op.noctv = 0;
   if (sym) {
     // octant modes qmx <= qmy: off-diagonal (two modes per block) first, the
     // diagonal (one mode) last, so the lighter items fill the tail
@@ -533,10 +561,18 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int s
     for (int qmy = 0; qmy < op.qy; ++qmy)
       for (int qmx = 0; qmx < qmy; ++qmx) l.push_back(qmy * op.qx + qmx);
     for (int q = 0; q < op.qx; ++q) l.push_back(q * op.qx + q);
-    EMIE_CUDA(cudaMalloc(&op.octl, l.size() * sizeof(int)));
+    // the DFMA contraction's items: 2 qm (+ 2 qm + 1 for the transposed mode)
+    std::vector<int> v;
+    for (int qm : l) {
+      v.push_back(2 * qm);
+      if (qm / op.qx != qm % op.qx) v.push_back(2 * qm + 1);
+    }
+    EMIE_CUDA(cudaMalloc(&op.octl, (l.size() + v.size()) * sizeof(int)));
     EMIE_CUDA(cudaMemcpyAsync(op.octl, l.data(), l.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    EMIE_CUDA(cudaMemcpyAsync(op.octl + l.size(), v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     EMIE_CUDA(cudaStreamSynchronize(st));
     op.noct = static_cast<int>(l.size());
+    op.noctv = static_cast<int>(v.size());
   }
 }
 
@@ -597,15 +633,19 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
         std::max<size_t>(1, std::min<size_t>(kCtWarps >> pair, (220u << 10) / per_group)));
     const int wpb = groups << pair;
     const size_t smem = per_group * groups;
-    const int grid = std::max(1, std::min(sms, ceil_div(nmodes, groups)));
+    const int nitems = use_octant(op, q0, q1) ? op.noctv : nmodes;
+    const int grid = std::max(1, std::min(sms, ceil_div(nitems, groups)));
+    const bool oct = use_octant(op, q0, q1);
+    const int* octv = oct ? op.octl + op.noct : nullptr;
+    const int noctv = oct ? op.noctv : 0;
     if (CB == 8) {
       set_smem(reinterpret_cast<const void*>(contract_kernel<8>), smem);
       contract_kernel<8><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
-                                                       q0, q1, op.qbase, g, pair);
+                                                       q0, q1, op.qbase, g, pair, octv, noctv);
     } else {
       set_smem(reinterpret_cast<const void*>(contract_kernel<4>), smem);
       contract_kernel<4><<<grid, wpb * 32, smem, st>>>(op.spec, Sg, op.nz, op.nsd, op.nentD, op.ex, op.ey, op.qx,
-                                                       q0, q1, op.qbase, g, pair);
+                                                       q0, q1, op.qbase, g, pair, octv, noctv);
     }
     check_launch("contract_kernel");
   }

@@ -65,8 +65,8 @@ struct Operator {
   // with the x and y rows and columns exchanged, so the contraction reads
   // only the octant qmx <= qmy (octl: those modes, off-diagonal ones first)
   bool xysym = false;
-  int* octl = nullptr;
-  int noct = 0;
+  int* octl = nullptr;  // noct octant modes, then the DFMA kernel's noctv item codes
+  int noct = 0, noctv = 0;
 
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
   std::size_t lateral() const { return static_cast<std::size_t>(ex) * ey; }
