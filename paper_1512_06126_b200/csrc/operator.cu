@@ -434,7 +434,10 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
 #pragma unroll
       for (int g = 0; g < NG; ++g) p1[g][0] = p1[g][1] = p2[g][0] = p2[g][1] = p3[g][0] = p3[g][1] = 0.0;
       // operands PD k-steps ahead of their MMAs (SMEM latency off the DMMA chain)
-      constexpr int PD = 6;
+#ifndef EMIE_CT_PD
+#define EMIE_CT_PD 6
+#endif
+      constexpr int PD = EMIE_CT_PD;
       cplx av[PD], bv[PD][NG];
 #pragma unroll
       for (int ks = 0; ks < PD; ++ks) {
