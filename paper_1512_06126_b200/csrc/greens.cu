@@ -38,6 +38,10 @@ constexpr int kMaxLayers = 16;
 #define EMIE_GREEN_THREADS 256
 #endif
 constexpr int kGreenThreads = EMIE_GREEN_THREADS;  // threads per assemble CTA
+#ifndef EMIE_GREEN_SLOTS
+#define EMIE_GREEN_SLOTS 2
+#endif
+constexpr int kGreenSlots = EMIE_GREEN_SLOTS;  // full-lambda-range pairs per thread (+ a lambda-split tail)
 
 // ------------------------------------------------------ complex helpers ----
 // Smith's algorithm: the exact-path fallback of cdiv (zero or non-finite divisor)
@@ -497,17 +501,17 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   // keeps tail pair tid % ntail for every Teff-th (pair, lambda) item of a
   // chunk; the T / ntail partial sums per tail pair are added in a fixed order
   // at the end, so every thread evaluates ~2.06 pairs per lambda, not 3.
-  constexpr int T = kGreenThreads;
-  const int g0 = blockIdx.y * 3 * T;
-  const int cnt = min(3 * T, P.npairs - g0);
-  const int ntail = max(0, cnt - 2 * T);
+  constexpr int T = kGreenThreads, NS = kGreenSlots;
+  const int g0 = blockIdx.y * (NS + 1) * T;
+  const int cnt = min((NS + 1) * T, P.npairs - g0);
+  const int ntail = max(0, cnt - NS * T);
   const int teff = ntail > 0 ? (T / ntail) * ntail : 0;
-  PairC pc[3];
-  bool pv[3];
+  PairC pc[NS + 1];
+  bool pv[NS + 1];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const int sl = i < 2 ? i * T + threadIdx.x : 2 * T + (ntail > 0 ? threadIdx.x % ntail : 0);
-    pv[i] = i < 2 ? sl < cnt : static_cast<int>(threadIdx.x) < teff;
+  for (int i = 0; i <= NS; ++i) {
+    const int sl = i < NS ? i * T + threadIdx.x : NS * T + (ntail > 0 ? threadIdx.x % ntail : 0);
+    pv[i] = i < NS ? sl < cnt : static_cast<int>(threadIdx.x) < teff;
     int k = 0, kp = 0;
     if (pv[i]) pair_of(g0 + sl, nz, k, kp);
     pc[i].k = k;
@@ -517,9 +521,9 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     pc[i].isk = iv[k].inv_sig;
   }
   // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k)
-  cplx acc[3][9];
+  cplx acc[NS + 1][9];
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i <= NS; ++i)
 #pragma unroll
     for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
 
@@ -770,16 +774,16 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
       const int* El = C.E + li * 4 * nz;
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < NS; ++i)
         if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, wmu, acc[i]);
     }
-    if (pv[2]) {
+    if (pv[NS]) {
       for (int u = threadIdx.x; u < ntail * lc; u += teff) {
         const int li = u / ntail;
         double wl[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[2], wl, wmu, acc[2]);
+        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[NS], wl, wmu, acc[NS]);
       }
     }
   }
@@ -789,14 +793,14 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   if (ntail > 0) {
     cplx* part = sm;  // the chunk buffers are free now: [9][T]
 #pragma unroll
-    for (int f = 0; f < 9; ++f) part[f * T + threadIdx.x] = acc[2][f];
+    for (int f = 0; f < 9; ++f) part[f * T + threadIdx.x] = acc[NS][f];
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < ntail) {
 #pragma unroll
       for (int f = 0; f < 9; ++f) {
         cplx sum = part[f * T + threadIdx.x];
         for (int r = threadIdx.x + ntail; r < teff; r += ntail) sum = sum + part[f * T + r];
-        acc[2][f] = sum;
+        acc[NS][f] = sum;
       }
     }
   }
@@ -806,8 +810,8 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   cplx* blk = blocks + static_cast<size_t>(off) * P.nent;
   bool bad = false;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const bool own = i < 2 ? pv[i] : static_cast<int>(threadIdx.x) < ntail;
+  for (int i = 0; i <= NS; ++i) {
+    const bool own = i < NS ? pv[i] : static_cast<int>(threadIdx.x) < ntail;
     if (!own) continue;
     const int k = pc[i].k, kp = pc[i].kp;
     const int s = k * nz - k * (k - 1) / 2 + (kp - k);
@@ -1102,7 +1106,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
-  const int groups = ceil_div(P.npairs, 3 * kGreenThreads);
+  const int groups = ceil_div(P.npairs, (kGreenSlots + 1) * kGreenThreads);
   dim3 grid(ncomp, groups);
   profile_mark(5, true, st);
 #ifdef EMIE_GREENS_PHASE_CLOCKS
