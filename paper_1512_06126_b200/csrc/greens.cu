@@ -386,11 +386,15 @@ struct PairC {
 
 // one lambda of one interval pair into its nine accumulators (greens.cpp:167-191,
 // v_functions layered.cpp:397-408); wl = lambda, 1/lambda, w00 w20 w02 w11 w10 w01
+// KIND < 0: the pair's kind at run time; 0 / 1 / 2: known at compile time
+// (branch-free body, so two general pairs of a thread interleave: phase 2)
+template <int KIND = -1>
 __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const int* __restrict__ El, int nz,
                                             const PairC& c, const double* wl, double wmu, cplx* a) {
   const int k = c.k, kp = c.kp;
+  const int kind = KIND < 0 ? c.kind : KIND;
   cplx W00u, W00c, W01c, W10c, W11c, W20c;
-  if (c.kind == 0) {
+  if (kind == 0) {
     W00u = Fl[fW00u * nz + k];
     W00c = Fl[fW00c * nz + k];
     W10c = Fl[fW10c * nz + k];
@@ -399,7 +403,7 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
     W20c = Fl[fW20c * nz + k];
   } else {
     cplx Cu = {1.0, 0.0}, Cc = {1.0, 0.0};
-    if (c.kind == 2) {  // chain prod_{l=k+1}^{kp-1} theta_l from the prefix products
+    if (kind == 2) {  // chain prod_{l=k+1}^{kp-1} theta_l from the prefix products
       const int kn = c.kn;
       Cu = (El[1 * nz + kp] != El[1 * nz + kn])
                ? cplx{0.0, 0.0}
@@ -432,7 +436,7 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
   a[2] = a[2] + wl[4] * f2;
   a[3] = a[3] + wl[5] * f2;
   a[4] = a[4] + wl[2] * (lam * (V2 + V5));
-  if (c.kind != 0) {
+  if (kind != 0) {
     // lower entry (kp, k): W10c(kp,k) = (sig_kp / sig_k) W01c(k,kp) (reciprocity,
     // layered.cpp:363-376) and V4 = W10c / sig_kp, i.e. W01c / sig_k
     const cplx f4l = lam * (W01c * c.isk);
@@ -528,6 +532,8 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
 
   const int nw = P.nw;
+  const bool general2 =
+      NS == 2 && __all_sync(0xffffffffu, pv[0] && pv[1] && pc[0].kind == 2 && pc[NS > 1 ? 1 : 0].kind == 2);
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   long long clk = clock64();
 #endif
@@ -773,9 +779,14 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
       const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
       const int* El = C.E + li * 4 * nz;
+      if (general2) {  // warp-uniform: both slots general pairs, one branch-free block
+        pair_lambda<2>(Fl, El, nz, pc[0], wl, wmu, acc[0]);
+        pair_lambda<2>(Fl, El, nz, pc[1], wl, wmu, acc[1]);
+      } else {
 #pragma unroll
-      for (int i = 0; i < NS; ++i)
-        if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, wmu, acc[i]);
+        for (int i = 0; i < NS; ++i)
+          if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, wmu, acc[i]);
+      }
     }
     if (pv[NS]) {
       for (int u = threadIdx.x; u < ntail * lc; u += teff) {
