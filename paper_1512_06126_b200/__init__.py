@@ -427,6 +427,17 @@ def operator_from_greens_blocks(grid: AnomalyGrid, omega: float, d_blocks, q0: i
     return SpectralOperator(h)
 
 
+def warmup() -> None:
+    """Library initialisation: one tiny Green's build (16 x 16 x 2) and system
+    apply, so the device code of the build and the first allocations of the
+    stream-ordered pool are in place before a timed build (CUDA loads kernels
+    lazily, on first launch)."""
+    model = LayeredModel([0.0, 1000.0], [0.0, 0.01, 0.1])
+    grid = make_grid(model, [1100.0, 1200.0, 1300.0], 16, 16, 100.0, 100.0)
+    op = assemble_operator(grid, model, 2.0 * np.pi)
+    apply(build_system(grid, op), np.ones(3 * 16 * 16 * 2, np.complex128))
+
+
 def restrict_modes(op: SpectralOperator, q0: int, q1: int) -> SpectralOperator:
     """A device copy of op holding only quadrant modes [q0, q1) (the mode
     shard of a sharded apply, distributed.py)."""
