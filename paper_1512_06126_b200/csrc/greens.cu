@@ -343,6 +343,7 @@ struct Chunk {
   cplx* diag_a;
   cplx* rup;     // [lc][m]: eta[m] / eta[m+1]
   cplx* rdn;     // [lc][m]: eta[m] / eta[m-1]
+  cplx* ieta;    // [lc][m]: 1 / eta[m]
   // interval fields [lc][f][j]
   cplx* F;
   double* lam;   // [8][lc]: lambda, 1/lambda, w00 w20 w02 w11 w10 w01
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     C.diag_a = s; s += LC * 2 * NL;
     C.rup = s; s += LC * NL;
     C.rdn = s; s += LC * NL;
+    C.ieta = s; s += LC * NL;
     C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
     C.lam = reinterpret_cast<double*>(s);  // [lc]: lambda, 1/lambda, 6 weights
     C.E = reinterpret_cast<int*>(C.lam + 8 * LC);
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
       const cplx eta = csqrt_pos(eta2);
       C.eta[li * NL + m] = eta;
+      C.ieta[li * NL + m] = crecip(eta);
       if (m < L) {  // neighbour ratios for the reflection chains, off their critical path
         const cplx eta2n = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m + 1];
         const cplx etan = csqrt_pos(eta2n);
@@ -633,6 +636,8 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const int li = x / nz, j = x - li * nz;
       const Interval I = iv[j];
       const cplx eta = C.eta[li * NL + I.layer];
+      const cplx ie = C.ieta[li * NL + I.layer];  // 1/eta, 1/eta^2: the divisions below become products
+      const cplx ie2 = ie * ie;
       const cplx ehm1 = cexpm1(-I.h * eta);
       const cplx eh = cplx{1.0, 0.0} + ehm1;
       const cplx el2 = C.e2l[li * NL + I.layer];
@@ -666,14 +671,15 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         const cplx Dp = one_p + p * epb2m1;
         const cplx Tq = one_q + q * eqabm1;
         const cplx TMq = (cplx{2.0, 0.0} - one_q) - q * eqabm1;
-        const cplx theta = cdiv(eh * Sa, Dp);
-        const cplx H0 = cdiv(u * Sab, eta * Dp);
-        const cplx J0 = cdiv(A * u * Sa * Tq, eta);
-        const cplx Ip = cdiv(epa * u, eta);
-        const cplx Iq = cdiv(eqb * u, eta);
+        const cplx iDp = crecip(Dp);
+        const cplx theta = (eh * Sa) * iDp;
+        const cplx H0 = ((u * Sab) * ie) * iDp;
+        const cplx J0 = (A * u * Sa * Tq) * ie;
+        const cplx Ip = (epa * u) * ie;
+        const cplx Iq = (eqb * u) * ie;
         const cplx Sp = p * Ip * Ip, Sq = q * Iq * Iq;
-        const cplx M0 = cdiv(2.0 * (I.h * eta + ehm1), eta2);
-        const cplx P0 = 2.0 * (cdiv(elh * u, eta2) - cdiv(I.h * el2, eta));
+        const cplx M0 = (2.0 * (I.h * eta + ehm1)) * ie2;
+        const cplx P0 = 2.0 * ((elh * u) * ie2 - (I.h * el2) * ie);
         const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
         if (gm == 0) {
           F(li, fH0u, j) = H0;
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
           F(li, fThu, j) = theta;
         } else {
           F(li, fH0c, j) = H0;
-          F(li, fH1c, j) = cdiv(u * Mab, Dp);
+          F(li, fH1c, j) = (u * Mab) * iDp;
           F(li, fJ0c, j) = J0;
           F(li, fJ1c, j) = -(A * u * Sa * TMq);
           F(li, fW00c, j) = W00d;
@@ -723,7 +729,11 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
               e = s;
             }
           }
-          // inclusive scan (lane order = interval order)
+          // inclusive scan (lane order = interval order). Mantissas with max
+          // component in [1, 2) have modulus in [1, 2^1.5), so a product of
+          // <= 32 stays in [1, 2^48]: no renormalisation inside the scan, and
+          // since power-of-two scalings are exact, the final normalised
+          // mantissas equal a step-by-step renormalised scan bit for bit
 #pragma unroll
           for (int off = 1; off < 32; off <<= 1) {
             const double mr = __shfl_up_sync(0xffffffffu, m.re, off);
@@ -732,9 +742,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
             const int oz = __shfl_up_sync(0xffffffffu, z, off);
             if (lane >= off) {
               m = cplx{mr, mi} * m;
-              const int s = ilog2(fmax(fabs(m.re), fabs(m.im)));
-              m = scal2(m, -s);
-              e += oe + s;
+              e += oe;
               z += oz;
             }
           }
@@ -1087,7 +1095,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   // lambdas per chunk: as many as ~200 KB of SMEM holds (the serial per-chunk
   // phases then run on more threads and there are fewer chunks), at most 32
   {
-    const size_t per_lambda = (15 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
+    const size_t per_lambda = (16 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
                               8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
     int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (size_t{EMIE_GREEN_SMEM_KB} << 10) / per_lambda)));
     if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
@@ -1113,7 +1121,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
   const int NL = L + 1;
-  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 12 * NL + kFields * nz)) * sizeof(cplx) +
+  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 13 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
