@@ -341,8 +341,6 @@ struct Chunk {
   cplx* one_p;
   cplx* one_q;
   cplx* diag_a;
-  cplx* rup;     // [lc][m]: eta[m] / eta[m+1]
-  cplx* rdn;     // [lc][m]: eta[m] / eta[m-1]
   cplx* ieta;    // [lc][m]: 1 / eta[m]
   // interval fields [lc][f][j]
   cplx* F;
@@ -491,8 +489,6 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     C.one_p = s; s += LC * 2 * NL;
     C.one_q = s; s += LC * 2 * NL;
     C.diag_a = s; s += LC * 2 * NL;
-    C.rup = s; s += LC * NL;
-    C.rdn = s; s += LC * NL;
     C.ieta = s; s += LC * NL;
     C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
     C.lam = reinterpret_cast<double*>(s);  // [lc]: lambda, 1/lambda, 6 weights
@@ -559,12 +555,6 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const cplx eta = csqrt_pos(eta2);
       C.eta[li * NL + m] = eta;
       C.ieta[li * NL + m] = crecip(eta);
-      if (m < L) {  // neighbour ratios for the reflection chains, off their critical path
-        const cplx eta2n = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m + 1];
-        const cplx etan = csqrt_pos(eta2n);
-        C.rup[li * NL + m] = cdiv(eta, etan);
-        C.rdn[li * NL + m + 1] = cdiv(etan, eta);
-      }
       if (m == 0 || m == L) {
         C.e2l[li * NL + m] = {1.0, 0.0};
         C.em1[li * NL + m] = {0.0, 0.0};
@@ -584,37 +574,40 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const int li = rem >> 1, gm = rem & 1;
       const cplx* e2l = C.e2l + li * NL;
       const cplx* em1 = C.em1 + li * NL;
+      const cplx* eta = C.eta + li * NL;
+      const cplx* ie = C.ieta + li * NL;
       const int base = (li * 2 + gm) * NL;
+      // w = -g N / D with g = alpha eta_m / eta_{m+1} (layered.cpp:113-116), so
+      // p = (1 + w) / (1 - w) = (D - g N) / (D + g N) and 1 + p = 2 D / (D + g N):
+      // one complex reciprocal per step
       if (dir == 0) {
         cplx* p = C.p + base;
         cplx* op = C.one_p + base;
-        const cplx* rup = C.rup + li * NL;
         cplx opm = {1.0, 0.0};
         p[0] = {0.0, 0.0};
         op[0] = opm;
         for (int m = 0; m < L; ++m) {
-          const cplx t = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - opm), em1[m] + e2l[m] * opm);
-          const cplx alpha = gm ? P.sig_up[m] : cplx{1.0, 0.0};
-          const cplx w = alpha * rup[m] * t;
-          const cplx r = crecip(cplx{1.0, 0.0} - w);
-          p[m + 1] = (cplx{1.0, 0.0} + w) * r;
-          opm = 2.0 * r;
+          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - opm), D = em1[m] + e2l[m] * opm;
+          const cplx rat = eta[m] * ie[m + 1];
+          const cplx gN = (gm ? P.sig_up[m] * rat : rat) * N;
+          const cplx r = crecip(D + gN);
+          p[m + 1] = (D - gN) * r;
+          opm = 2.0 * (D * r);
           op[m + 1] = opm;
         }
       } else {
         cplx* q = C.q + base;
         cplx* oq = C.one_q + base;
-        const cplx* rdn = C.rdn + li * NL;
         cplx oqm = {1.0, 0.0};
         q[L] = {0.0, 0.0};
         oq[L] = oqm;
         for (int m = L; m > 0; --m) {
-          const cplx u = -cdiv(em1[m] + e2l[m] * (cplx{2.0, 0.0} - oqm), em1[m] + e2l[m] * oqm);
-          const cplx beta = gm ? P.sig_dn[m] : cplx{1.0, 0.0};
-          const cplx w = beta * rdn[m] * u;
-          const cplx r = crecip(cplx{1.0, 0.0} - w);
-          q[m - 1] = (cplx{1.0, 0.0} + w) * r;
-          oqm = 2.0 * r;
+          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - oqm), D = em1[m] + e2l[m] * oqm;
+          const cplx rat = eta[m] * ie[m - 1];
+          const cplx gN = (gm ? P.sig_dn[m] * rat : rat) * N;
+          const cplx r = crecip(D + gN);
+          q[m - 1] = (D - gN) * r;
+          oqm = 2.0 * (D * r);
           oq[m - 1] = oqm;
         }
       }
@@ -703,10 +696,86 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     __syncthreads();
     PHASE_MARK(4);
     // phase 1b: prefix products of theta per (lambda, gamma) as
-    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l. One warp
-    // per (lambda, gamma): a shuffle scan over 32-interval segments, the
-    // segment carry multiplied in, so the serial depth is log2(32) + nz/32.
-    {
+    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l.
+    // nz <= 64: eight lanes per (lambda, gamma), four tasks per warp at once;
+    // a lane owns ceil(nz/8) consecutive intervals: local products, a 3-step
+    // shuffle scan over the eight lanes, the lane's exclusive prefix
+    // multiplied in. Mantissas (max component in [1, 2), modulus < 2^1.5) are
+    // not renormalised inside: a product of <= 64 stays below 2^96.
+    if (nz <= 64) {
+      const int lane = threadIdx.x & 31, sub = lane & 7;
+      const int per = (nz + 7) >> 3;
+      const int ntask = lc * 2;
+      for (int task0 = (threadIdx.x >> 5) * 4; task0 < ntask; task0 += (blockDim.x >> 5) * 4) {
+        const int task = task0 + (lane >> 3);
+        const bool live = task < ntask;
+        const int li = live ? task >> 1 : 0, gm = task & 1;
+        const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
+        cplx m[8];
+        int e[8], z[8];
+        cplx lm = {1.0, 0.0};  // running local product (inclusive)
+        int le = 0, lz = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = sub * per + q;
+          cplx mq = {1.0, 0.0};
+          int eq = 0, zq = 0;
+          if (q < per && j < nz && live) {
+            const cplx th = F(li, fT, j);
+            if (th.re == 0.0 && th.im == 0.0) {
+              zq = 1;
+            } else {
+              const int sh = ilog2(fmax(fabs(th.re), fabs(th.im)));
+              mq = scal2(th, -sh);
+              eq = sh;
+            }
+          }
+          // exclusive local prefix of element q, then include it
+          m[q] = lm;
+          e[q] = le;
+          z[q] = lz;
+          lm = lm * mq;
+          le += eq;
+          lz += zq;
+        }
+        // inclusive scan of the lane totals over the eight lanes of the task
+        cplx sm_ = lm;
+        int se = le, sz = lz;
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {
+          const double mr = __shfl_up_sync(0xffffffffu, sm_.re, off, 8);
+          const double mi = __shfl_up_sync(0xffffffffu, sm_.im, off, 8);
+          const int oe = __shfl_up_sync(0xffffffffu, se, off, 8);
+          const int oz = __shfl_up_sync(0xffffffffu, sz, off, 8);
+          if (sub >= off) {
+            sm_ = cplx{mr, mi} * sm_;
+            se += oe;
+            sz += oz;
+          }
+        }
+        // exclusive lane prefix
+        cplx pm = {__shfl_up_sync(0xffffffffu, sm_.re, 1, 8), __shfl_up_sync(0xffffffffu, sm_.im, 1, 8)};
+        int pe = __shfl_up_sync(0xffffffffu, se, 1, 8), pz = __shfl_up_sync(0xffffffffu, sz, 1, 8);
+        if (sub == 0) {
+          pm = {1.0, 0.0};
+          pe = 0;
+          pz = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = sub * per + q;
+          if (q < per && j < nz && live) {
+            cplx v = pm * m[q];
+            const int sh = ilog2(fmax(fabs(v.re), fabs(v.im)));
+            v = scal2(v, -sh);
+            F(li, fP, j) = v;
+            F(li, fPi, j) = crecip(v);
+            Ei(li, gm * 2, j) = pe + e[q] + sh;
+            Ei(li, gm * 2 + 1, j) = pz + z[q];
+          }
+        }
+      }
+    } else {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       const int nwarps = blockDim.x >> 5;
       for (int task = warp; task < lc * 2; task += nwarps) {
@@ -1095,7 +1164,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   // lambdas per chunk: as many as ~200 KB of SMEM holds (the serial per-chunk
   // phases then run on more threads and there are fewer chunks), at most 32
   {
-    const size_t per_lambda = (16 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
+    const size_t per_lambda = (14 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
                               8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
     int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (size_t{EMIE_GREEN_SMEM_KB} << 10) / per_lambda)));
     if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
@@ -1121,7 +1190,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
   const int NL = L + 1;
-  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 13 * NL + kFields * nz)) * sizeof(cplx) +
+  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 11 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
