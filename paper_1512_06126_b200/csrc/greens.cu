@@ -347,11 +347,23 @@ struct Chunk {
   double* lam;   // [8][lc]: lambda, 1/lambda, w00 w20 w02 w11 w10 w01
   int* E;        // [lc][4][j]: Pu_e, Pu_z, Pc_e, Pc_z
 };
-// interval field slots
+// interval field slots. An off-diagonal pair (k < kp) needs, per medium, the
+// chain prod_{l=k+1}^{kp-1} theta_l = P(kp) / P(k+1) (prefix products P), so
+// every product W = H(k) chain J(kp) of layered.cpp:340-376 factors into a
+// left factor of row k, H(k) / P(k+1), and a right factor of column kp,
+// P(kp) J(kp), times 2^(E(kp) - E(k+1)) (the prefix exponents), zero unless
+// the two prefix zero counts agree. The V-function coefficients of
+// layered.cpp:397-408 (i omega mu0, 1/sigma(k), eta(k)^2) are folded into
+// the left factors, so a pair-lambda costs five complex products:
+//   fLU  = i wmu H0u(k) / Pu(k+1)                     -> V1
+//   fL0v = (i wmu + eta(k)^2 / sigma(k)) H0c(k) / Pc(k+1) -> V2 + V5
+//   fL1s = H1c(k) / sigma(k) / Pc(k+1)                -> V4 (with fR0), -V3 (with fR1)
+//   fL0s = H0c(k) / sigma(k) / Pc(k+1)                -> W01c / sigma(k) (lower entries)
+//   fRU = Pu J0u, fR0 = Pc J0c, fR1 = Pc J1c           (column kp)
+//   fD1, fD3, fD4, fD25: V1, V3, V4, V2 + V5 of the diagonal pair (k, k)
+//   fPiu, fPic: theta (phase 1), then 1 / P (phase 1b)
 enum {
-  fH0u, fJ0u, fW00u, fPu, fPiu,
-  fH0c, fH1c, fJ0c, fJ1c, fW00c, fW10c, fW11c, fW20c, fPc, fPic,
-  fEta2, fThu, fThc, kFields
+  fLU, fL0v, fL1s, fL0s, fRU, fR0, fR1, fD1, fD3, fD4, fD25, fPiu, fPic, kFields
 };
 
 // Pair order inside a group: diagonals (k, k) for s < nz, then neighbours
@@ -379,69 +391,51 @@ __device__ __forceinline__ void pair_of(int s, int nz, int& k, int& kp) {
 
 struct PairC {
   int k, kp, kn;  // kn = min(k + 1, nz - 1)
-  int kind;       // 0 diagonal, 1 neighbour, 2 general
-  cplx isk;       // 1 / sigma of interval k
+  int kind;       // 0 diagonal, 1 off-diagonal
 };
 
 // one lambda of one interval pair into its nine accumulators (greens.cpp:167-191,
-// v_functions layered.cpp:397-408); wl = lambda, 1/lambda, w00 w20 w02 w11 w10 w01
-// KIND < 0: the pair's kind at run time; 0 / 1 / 2: known at compile time
-// (branch-free body, so two general pairs of a thread interleave: phase 2)
+// v_functions layered.cpp:397-408); wl = w00 lambda, w20 / lambda, w02 / lambda,
+// w11 / lambda, w10 lambda, w01 lambda. KIND < 0: the pair's kind at run time;
+// 0 / 1: known at compile time (branch-free body, so two off-diagonal pairs of
+// a thread interleave: phase 2)
 template <int KIND = -1>
 __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const int* __restrict__ El, int nz,
-                                            const PairC& c, const double* wl, double wmu, cplx* a) {
+                                            const PairC& c, const double* wl, cplx* a) {
   const int k = c.k, kp = c.kp;
   const int kind = KIND < 0 ? c.kind : KIND;
-  cplx W00u, W00c, W01c, W10c, W11c, W20c;
+  cplx V1, V13, X25, V4;
   if (kind == 0) {
-    W00u = Fl[fW00u * nz + k];
-    W00c = Fl[fW00c * nz + k];
-    W10c = Fl[fW10c * nz + k];
-    W01c = W10c;
-    W11c = Fl[fW11c * nz + k];
-    W20c = Fl[fW20c * nz + k];
+    V1 = Fl[fD1 * nz + k];
+    V13 = V1 + Fl[fD3 * nz + k];
+    X25 = Fl[fD25 * nz + k];
+    V4 = Fl[fD4 * nz + k];
   } else {
-    cplx Cu = {1.0, 0.0}, Cc = {1.0, 0.0};
-    if (kind == 2) {  // chain prod_{l=k+1}^{kp-1} theta_l from the prefix products
-      const int kn = c.kn;
-      Cu = (El[1 * nz + kp] != El[1 * nz + kn])
-               ? cplx{0.0, 0.0}
-               : scal2(Fl[fPu * nz + kp] * Fl[fPiu * nz + kn], El[0 * nz + kp] - El[0 * nz + kn]);
-      Cc = (El[3 * nz + kp] != El[3 * nz + kn])
-               ? cplx{0.0, 0.0}
-               : scal2(Fl[fPc * nz + kp] * Fl[fPic * nz + kn], El[2 * nz + kp] - El[2 * nz + kn]);
-    }
-    W00u = (Fl[fH0u * nz + k] * Cu) * Fl[fJ0u * nz + kp];
-    const cplx a0 = Fl[fH0c * nz + k] * Cc, a1 = Fl[fH1c * nz + k] * Cc;
-    const cplx j0 = Fl[fJ0c * nz + kp], j1 = Fl[fJ1c * nz + kp];
-    W00c = a0 * j0;
-    W01c = a0 * j1;
-    W10c = a1 * j0;
-    W11c = a1 * j1;
-    W20c = Fl[fEta2 * nz + k] * W00c;
-  }
-  const double lam = wl[0], ilam = wl[1];
-  const cplx V1 = {-wmu * W00u.im, wmu * W00u.re};
-  const cplx V2 = {-wmu * W00c.im, wmu * W00c.re};
-  const cplx V3 = -(W11c * c.isk);
-  const cplx V4 = W10c * c.isk;
-  const cplx V5 = W20c * c.isk;
-  const cplx f4 = lam * V4;
-  a[5] = a[5] + wl[6] * f4;
-  a[6] = a[6] + wl[7] * f4;
-  const cplx f2 = (V1 + V3) * ilam;
-  a[0] = a[0] + wl[2] * (lam * V1);
-  a[1] = a[1] + wl[3] * f2;
-  a[2] = a[2] + wl[4] * f2;
-  a[3] = a[3] + wl[5] * f2;
-  a[4] = a[4] + wl[2] * (lam * (V2 + V5));
-  if (kind != 0) {
+    const int kn = c.kn;
+    V1 = (El[1 * nz + kp] != El[1 * nz + kn])
+             ? cplx{0.0, 0.0}
+             : scal2(Fl[fLU * nz + k] * Fl[fRU * nz + kp], El[0 * nz + kp] - El[0 * nz + kn]);
+    const bool zc = El[3 * nz + kp] != El[3 * nz + kn];
+    const int ec = El[2 * nz + kp] - El[2 * nz + kn];
+    const cplx r0 = zc ? cplx{0.0, 0.0} : scal2(Fl[fR0 * nz + kp], ec);
+    const cplx r1 = zc ? cplx{0.0, 0.0} : scal2(Fl[fR1 * nz + kp], ec);
+    const cplx l1 = Fl[fL1s * nz + k];
+    X25 = Fl[fL0v * nz + k] * r0;
+    V4 = l1 * r0;
+    V13 = V1 - l1 * r1;
     // lower entry (kp, k): W10c(kp,k) = (sig_kp / sig_k) W01c(k,kp) (reciprocity,
     // layered.cpp:363-376) and V4 = W10c / sig_kp, i.e. W01c / sig_k
-    const cplx f4l = lam * (W01c * c.isk);
-    a[7] = a[7] + wl[6] * f4l;
-    a[8] = a[8] + wl[7] * f4l;
+    const cplx lo = Fl[fL0s * nz + k] * r1;
+    a[7] = a[7] + wl[4] * lo;
+    a[8] = a[8] + wl[5] * lo;
   }
+  a[0] = a[0] + wl[0] * V1;
+  a[1] = a[1] + wl[1] * V13;
+  a[2] = a[2] + wl[2] * V13;
+  a[3] = a[3] + wl[3] * V13;
+  a[4] = a[4] + wl[0] * X25;
+  a[5] = a[5] + wl[4] * V4;
+  a[6] = a[6] + wl[5] * V4;
 }
 
 #ifdef EMIE_GREENS_PHASE_CLOCKS  // timing experiment: cycles per phase summed over CTAs
@@ -519,8 +513,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     pc[i].k = k;
     pc[i].kp = kp;
     pc[i].kn = min(k + 1, nz - 1);
-    pc[i].kind = kp == k ? 0 : kp == k + 1 ? 1 : 2;
-    pc[i].isk = iv[k].inv_sig;
+    pc[i].kind = kp == k ? 0 : 1;
   }
   // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k)
   cplx acc[NS + 1][9];
@@ -531,7 +524,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
 
   const int nw = P.nw;
   const bool general2 =
-      NS == 2 && __all_sync(0xffffffffu, pv[0] && pv[1] && pc[0].kind == 2 && pc[NS > 1 ? 1 : 0].kind == 2);
+      NS == 2 && __all_sync(0xffffffffu, pv[0] && pv[1] && pc[0].kind == 1 && pc[NS > 1 ? 1 : 0].kind == 1);
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   long long clk = clock64();
 #endif
@@ -542,10 +535,14 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     // per-lambda scalars of the chunk
     for (int li = threadIdx.x; li < lc; li += blockDim.x) {
       const int t = t0 + li;
-      const double lam = exp((P.n1 + t) * P.step + P.shift) / R;
-      C.lam[li] = lam;
-      C.lam[LC + li] = 1.0 / lam;
-      for (int q = 0; q < 6; ++q) C.lam[(2 + q) * LC + li] = Woff[q * nw + t];
+      const double lam = exp((P.n1 + t) * P.step + P.shift) / R, ilam = 1.0 / lam;
+      // weights w00 w20 w02 w11 w10 w01 (greens.cpp:137) times lambda or 1/lambda
+      C.lam[li] = Woff[t] * lam;
+      C.lam[LC + li] = Woff[nw + t] * ilam;
+      C.lam[2 * LC + li] = Woff[2 * nw + t] * ilam;
+      C.lam[3 * LC + li] = Woff[3 * nw + t] * ilam;
+      C.lam[4 * LC + li] = Woff[4 * nw + t] * lam;
+      C.lam[5 * LC + li] = Woff[5 * nw + t] * lam;
     }
     // phase 0a: eta, e2l, em1 per (lambda, layer)
     for (int x = threadIdx.x; x < lc * NL; x += blockDim.x) {
@@ -653,7 +650,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const cplx elh = (I.has_p && I.has_q) ? cexp((-(2.0 * I.l - I.h)) * eta) : cplx{0.0, 0.0};
       const cplx u = -ehm1;
       const cplx eta2 = eta * eta;
-      F(li, fEta2, j) = eta2;
+      const cplx isk = I.inv_sig;
       for (int gm = 0; gm < 2; ++gm) {
         const int r = li * 2 * NL + gm * NL + I.layer;
         const cplx p = C.p[r], q = C.q[r], A = C.diag_a[r];
@@ -675,21 +672,23 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         const cplx P0 = 2.0 * ((elh * u) * ie2 - (I.h * el2) * ie);
         const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
         if (gm == 0) {
-          F(li, fH0u, j) = H0;
-          F(li, fJ0u, j) = J0;
-          F(li, fW00u, j) = W00d;
-          F(li, fThu, j) = theta;
+          F(li, fLU, j) = cplx{-wmu * H0.im, wmu * H0.re};
+          F(li, fRU, j) = J0;
+          F(li, fD1, j) = cplx{-wmu * W00d.im, wmu * W00d.re};
+          F(li, fPiu, j) = theta;
         } else {
-          F(li, fH0c, j) = H0;
-          F(li, fH1c, j) = (u * Mab) * iDp;
-          F(li, fJ0c, j) = J0;
-          F(li, fJ1c, j) = -(A * u * Sa * TMq);
-          F(li, fW00c, j) = W00d;
-          F(li, fW10c, j) = A * eta * (Sq - Sp);
-          F(li, fW11c, j) = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) -
-                            cplx{2.0 * I.h, 0.0};
-          F(li, fW20c, j) = eta2 * W00d - cplx{2.0 * I.h, 0.0};
-          F(li, fThc, j) = theta;
+          const cplx H1 = (u * Mab) * iDp;
+          F(li, fL0v, j) = (cplx{0.0, wmu} + eta2 * isk) * H0;
+          F(li, fL0s, j) = H0 * isk;
+          F(li, fL1s, j) = H1 * isk;
+          F(li, fR0, j) = J0;
+          F(li, fR1, j) = -(A * u * Sa * TMq);
+          const cplx W11d = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) - cplx{2.0 * I.h, 0.0};
+          const cplx W20d = eta2 * W00d - cplx{2.0 * I.h, 0.0};
+          F(li, fD25, j) = cplx{-wmu * W00d.im, wmu * W00d.re} + W20d * isk;
+          F(li, fD3, j) = -(W11d * isk);
+          F(li, fD4, j) = (A * eta * (Sq - Sp)) * isk;
+          F(li, fPic, j) = theta;
         }
       }
     }
@@ -710,7 +709,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         const int task = task0 + (lane >> 3);
         const bool live = task < ntask;
         const int li = live ? task >> 1 : 0, gm = task & 1;
-        const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
+        const int fT = gm ? fPic : fPiu;
         cplx m[8];
         int e[8], z[8];
         cplx lm = {1.0, 0.0};  // running local product (inclusive)
@@ -768,8 +767,14 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
             cplx v = pm * m[q];
             const int sh = ilog2(fmax(fabs(v.re), fabs(v.im)));
             v = scal2(v, -sh);
-            F(li, fP, j) = v;
-            F(li, fPi, j) = crecip(v);
+            // right factors P(j) J(j); theta(j) (read above by this lane only) -> 1/P(j)
+            if (gm) {
+              F(li, fR0, j) = v * F(li, fR0, j);
+              F(li, fR1, j) = v * F(li, fR1, j);
+            } else {
+              F(li, fRU, j) = v * F(li, fRU, j);
+            }
+            F(li, fT, j) = crecip(v);
             Ei(li, gm * 2, j) = pe + e[q] + sh;
             Ei(li, gm * 2 + 1, j) = pz + z[q];
           }
@@ -780,7 +785,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       const int nwarps = blockDim.x >> 5;
       for (int task = warp; task < lc * 2; task += nwarps) {
         const int li = task >> 1, gm = task & 1;
-        const int fT = gm ? fThc : fThu, fP = gm ? fPc : fPu, fPi = gm ? fPic : fPiu;
+        const int fT = gm ? fPic : fPiu;
         cplx cm = {1.0, 0.0};  // carry: product of the previous segments
         int ce = 0, cz = 0;
         for (int j0 = 0; j0 < nz; j0 += 32) {
@@ -831,8 +836,13 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
           }
           pz += cz;
           if (j < nz) {
-            F(li, fP, j) = pm;
-            F(li, fPi, j) = crecip(pm);
+            if (gm) {
+              F(li, fR0, j) = pm * F(li, fR0, j);
+              F(li, fR1, j) = pm * F(li, fR1, j);
+            } else {
+              F(li, fRU, j) = pm * F(li, fRU, j);
+            }
+            F(li, fT, j) = crecip(pm);
             Ei(li, gm * 2, j) = pe;
             Ei(li, gm * 2 + 1, j) = pz;
           }
@@ -848,30 +858,40 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       }
     }
     __syncthreads();
+    // phase 1c: left factors of rows k < nz - 1 divided by P(k+1) of their medium
+    for (int x = threadIdx.x; x < lc * (nz - 1); x += blockDim.x) {
+      const int li = x / (nz - 1), j = x - li * (nz - 1);
+      const cplx pu = F(li, fPiu, j + 1), pcn = F(li, fPic, j + 1);
+      F(li, fLU, j) = F(li, fLU, j) * pu;
+      F(li, fL0v, j) = F(li, fL0v, j) * pcn;
+      F(li, fL1s, j) = F(li, fL1s, j) * pcn;
+      F(li, fL0s, j) = F(li, fL0s, j) * pcn;
+    }
+    __syncthreads();
     PHASE_MARK(5);
     // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
     for (int li = 0; li < lc; ++li) {
-      double wl[8];
+      double wl[6];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
+      for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
       const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
       const int* El = C.E + li * 4 * nz;
-      if (general2) {  // warp-uniform: both slots general pairs, one branch-free block
-        pair_lambda<2>(Fl, El, nz, pc[0], wl, wmu, acc[0]);
-        pair_lambda<2>(Fl, El, nz, pc[1], wl, wmu, acc[1]);
+      if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
+        pair_lambda<1>(Fl, El, nz, pc[0], wl, acc[0]);
+        pair_lambda<1>(Fl, El, nz, pc[1], wl, acc[1]);
       } else {
 #pragma unroll
         for (int i = 0; i < NS; ++i)
-          if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, wmu, acc[i]);
+          if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, acc[i]);
       }
     }
     if (pv[NS]) {
       for (int u = threadIdx.x; u < ntail * lc; u += teff) {
         const int li = u / ntail;
-        double wl[8];
+        double wl[6];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[NS], wl, wmu, acc[NS]);
+        for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
+        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[NS], wl, acc[NS]);
       }
     }
   }
