@@ -345,7 +345,7 @@ struct Chunk {
   // interval fields [lc][f][j]
   cplx* F;
   double* lam;   // [8][lc]: lambda, 1/lambda, w00 w20 w02 w11 w10 w01
-  int* E;        // [lc][4][j]: Pu_e, Pu_z, Pc_e, Pc_z
+  int* E;        // [lc][2][j]: packed prefix exponent / zero count (ez_pack), unit and conductive
 };
 // interval field slots. An off-diagonal pair (k < kp) needs, per medium, the
 // chain prod_{l=k+1}^{kp-1} theta_l = P(kp) / P(k+1) (prefix products P), so
@@ -389,6 +389,19 @@ __device__ __forceinline__ void pair_of(int s, int nz, int& k, int& kp) {
   kp = k + 2 + s;
 }
 
+// Prefix exponent e and zero count z of a chain packed as e - z 2^24: the
+// difference of two packed values is the exponent difference when the zero
+// counts agree and below -2^23 when they do not (|e| < 2^22: nz * 1100 at most)
+__device__ __forceinline__ int ez_pack(int e, int z) { return e - (z << 24); }
+// 2^e, or 0 below the normal range: a chain product under 2^-1022 contributes
+// nothing at any precision the block entries are defined to (the reference's
+// running product underflows to the same zero, layered.cpp:340-360)
+__device__ __forceinline__ double pow2_or_zero(int e) { return e < -1022 ? 0.0 : pow2i(min(e, 1023)); }
+__device__ __forceinline__ cplx scale_or_flush(cplx v, int e) {
+  if (e > 1023) return scal2(v, e);
+  return pow2_or_zero(e) * v;
+}
+
 struct PairC {
   int k, kp, kn;  // kn = min(k + 1, nz - 1)
   int kind;       // 0 diagonal, 1 off-diagonal
@@ -412,13 +425,17 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
     V4 = Fl[fD4 * nz + k];
   } else {
     const int kn = c.kn;
-    V1 = (El[1 * nz + kp] != El[1 * nz + kn])
-             ? cplx{0.0, 0.0}
-             : scal2(Fl[fLU * nz + k] * Fl[fRU * nz + kp], El[0 * nz + kp] - El[0 * nz + kn]);
-    const bool zc = El[3 * nz + kp] != El[3 * nz + kn];
-    const int ec = El[2 * nz + kp] - El[2 * nz + kn];
-    const cplx r0 = zc ? cplx{0.0, 0.0} : scal2(Fl[fR0 * nz + kp], ec);
-    const cplx r1 = zc ? cplx{0.0, 0.0} : scal2(Fl[fR1 * nz + kp], ec);
+    V1 = scale_or_flush(Fl[fLU * nz + k] * Fl[fRU * nz + kp], El[kp] - El[kn]);
+    const int ec = El[nz + kp] - El[nz + kn];
+    cplx r0 = Fl[fR0 * nz + kp], r1 = Fl[fR1 * nz + kp];
+    if (ec > 1023) {  // a chain product above 2^1023: never in practice, kept exact
+      r0 = scal2(r0, ec);
+      r1 = scal2(r1, ec);
+    } else {
+      const double f = pow2_or_zero(ec);
+      r0 = f * r0;
+      r1 = f * r1;
+    }
     const cplx l1 = Fl[fL1s * nz + k];
     X25 = Fl[fL0v * nz + k] * r0;
     V4 = l1 * r0;
@@ -489,7 +506,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     C.E = reinterpret_cast<int*>(C.lam + 8 * LC);
   }
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
-  auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 4 + f) * nz + j]; };
+  auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 2 + f) * nz + j]; };
 
   // Pair assignment (balanced): group pairs [g0, g0 + cnt), cnt <= 3T. Slots
   // 0, 1: pair g0 + i T + tid over the full lambda range. The ntail = cnt - 2T
@@ -775,8 +792,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
               F(li, fRU, j) = v * F(li, fRU, j);
             }
             F(li, fT, j) = crecip(v);
-            Ei(li, gm * 2, j) = pe + e[q] + sh;
-            Ei(li, gm * 2 + 1, j) = pz + z[q];
+            Ei(li, gm, j) = ez_pack(pe + e[q] + sh, pz + z[q]);
           }
         }
       }
@@ -843,8 +859,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
               F(li, fRU, j) = pm * F(li, fRU, j);
             }
             F(li, fT, j) = crecip(pm);
-            Ei(li, gm * 2, j) = pe;
-            Ei(li, gm * 2 + 1, j) = pz;
+            Ei(li, gm, j) = ez_pack(pe, pz);
           }
           // new carry: carry x inclusive of lane 31
           const cplx lm = {__shfl_sync(0xffffffffu, m.re, 31), __shfl_sync(0xffffffffu, m.im, 31)};
@@ -875,7 +890,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
 #pragma unroll
       for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
       const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
-      const int* El = C.E + li * 4 * nz;
+      const int* El = C.E + li * 2 * nz;
       if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
         pair_lambda<1>(Fl, El, nz, pc[0], wl, acc[0]);
         pair_lambda<1>(Fl, El, nz, pc[1], wl, acc[1]);
@@ -891,7 +906,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         double wl[6];
 #pragma unroll
         for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 4 * nz, nz, pc[NS], wl, acc[NS]);
+        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 2 * nz, nz, pc[NS], wl, acc[NS]);
       }
     }
   }
@@ -1185,7 +1200,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   // phases then run on more threads and there are fewer chunks), at most 32
   {
     const size_t per_lambda = (14 * static_cast<size_t>(L + 1) + kFields * static_cast<size_t>(nz)) * sizeof(cplx) +
-                              8 * sizeof(double) + 4 * static_cast<size_t>(nz) * sizeof(int);
+                              8 * sizeof(double) + 2 * static_cast<size_t>(nz) * sizeof(int);
     int lcm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(32, (size_t{EMIE_GREEN_SMEM_KB} << 10) / per_lambda)));
     if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
     P.LC = lcm;
@@ -1212,7 +1227,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   const int NL = L + 1;
   const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 11 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
-                      static_cast<size_t>(P.LC) * 4 * nz * sizeof(int);
+                      static_cast<size_t>(P.LC) * 2 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
   const int groups = ceil_div(P.npairs, (kGreenSlots + 1) * kGreenThreads);
   dim3 grid(ncomp, groups);
