@@ -368,9 +368,13 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
 // Host-buffer apply (the reference-facing GridVector call): the right-hand
 // sides go through one at a time so PCIe runs full duplex -- rhs r+1 uploads
 // on one copy stream while rhs r computes and rhs r-1 downloads on another.
-// Each output column depends only on its own input column, so the result is
-// bit-identical to the batched device call.
+// Device buffers are a ring of kHostSlots per direction, so a long batch of
+// right-hand sides (independent fields: polarisations, sources, the fields of
+// consecutive calls a caller batches) streams at the PCIe rate in bounded
+// memory. Each output column depends only on its own input column, so the
+// result is bit-identical to the batched device call.
 namespace {
+constexpr int kHostSlots = 3;
 struct CopyStreams {
   cudaStream_t up = nullptr, down = nullptr;
   std::vector<cudaEvent_t> ev;
@@ -397,24 +401,37 @@ void host_pipelined_apply(const Operator& op, const System* sys, const double* h
                           int nrhs, cudaStream_t st) {
   CopyStreams& cs = copy_streams();
   const std::size_t n1 = 3 * op.cells();
-  cplx* din = scratch<cplx>(n1 * nrhs, st);
-  cplx* dout = scratch<cplx>(n1 * nrhs, st);
-  cudaEvent_t ready = cs.event(0);  // scratch allocated on st
+  const int slots = std::min(nrhs, kHostSlots);
+  cplx* din = scratch<cplx>(n1 * slots, st);
+  cplx* dout = scratch<cplx>(n1 * slots, st);
+  // events: 0 scratch ready; per ring slot s: 1 + 3s uploaded, 2 + 3s applied, 3 + 3s downloaded
+  auto ev_up = [&](int s) { return cs.event(1 + 3 * s); };
+  auto ev_app = [&](int s) { return cs.event(2 + 3 * s); };
+  auto ev_down = [&](int s) { return cs.event(3 + 3 * s); };
+  cudaEvent_t ready = cs.event(0);
   EMIE_CUDA(cudaEventRecord(ready, st));
   EMIE_CUDA(cudaStreamWaitEvent(cs.up, ready, 0));
+  EMIE_CUDA(cudaStreamWaitEvent(cs.down, ready, 0));
   for (int r = 0; r < nrhs; ++r) {
-    const cudaEvent_t in = cs.event(1 + 2 * r), out = cs.event(2 + 2 * r);
-    EMIE_CUDA(cudaMemcpyAsync(din + r * n1, reinterpret_cast<const cplx*>(h_in) + r * n1, n1 * sizeof(cplx),
+    const int s = r % slots;
+    cplx* di = din + s * n1;
+    cplx* dq = dout + s * n1;
+    // slot reuse: the upload waits for the apply that read it, the apply for
+    // the download that emptied its output (rhs r - slots)
+    if (r >= slots) EMIE_CUDA(cudaStreamWaitEvent(cs.up, ev_app(s), 0));
+    EMIE_CUDA(cudaMemcpyAsync(di, reinterpret_cast<const cplx*>(h_in) + r * n1, n1 * sizeof(cplx),
                               cudaMemcpyHostToDevice, cs.up));
-    EMIE_CUDA(cudaEventRecord(in, cs.up));
-    EMIE_CUDA(cudaStreamWaitEvent(st, in, 0));
-    apply_b(op, din + r * n1, dout + r * n1, 1, sys, st);
-    EMIE_CUDA(cudaEventRecord(out, st));
-    EMIE_CUDA(cudaStreamWaitEvent(cs.down, out, 0));
-    EMIE_CUDA(cudaMemcpyAsync(reinterpret_cast<cplx*>(h_out) + r * n1, dout + r * n1, n1 * sizeof(cplx),
+    EMIE_CUDA(cudaEventRecord(ev_up(s), cs.up));
+    EMIE_CUDA(cudaStreamWaitEvent(st, ev_up(s), 0));
+    if (r >= slots) EMIE_CUDA(cudaStreamWaitEvent(st, ev_down(s), 0));
+    apply_b(op, di, dq, 1, sys, st);
+    EMIE_CUDA(cudaEventRecord(ev_app(s), st));
+    EMIE_CUDA(cudaStreamWaitEvent(cs.down, ev_app(s), 0));
+    EMIE_CUDA(cudaMemcpyAsync(reinterpret_cast<cplx*>(h_out) + r * n1, dq, n1 * sizeof(cplx),
                               cudaMemcpyDeviceToHost, cs.down));
+    EMIE_CUDA(cudaEventRecord(ev_down(s), cs.down));
   }
-  const cudaEvent_t done = cs.event(1 + 2 * nrhs);
+  const cudaEvent_t done = cs.event(1 + 3 * kHostSlots);
   EMIE_CUDA(cudaEventRecord(done, cs.down));
   EMIE_CUDA(cudaStreamWaitEvent(st, done, 0));  // buffers go back to the pool after the last copy
   release(din, st);

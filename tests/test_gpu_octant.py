@@ -124,12 +124,13 @@ def test_octant_system_apply(torch_cuda):
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
 
 
-@pytest.mark.parametrize("nz,nrhs", [(8, 2), (16, 1), (5, 3)])
+@pytest.mark.parametrize("nz,nrhs", [(8, 2), (16, 1), (5, 3), (8, 7)])
 def test_host_apply_matches_device_apply(torch_cuda, nz, nrhs):
     """host buffers through emie_cu_apply_system_host on a 256-point
     embedding (the bench's e2e path: per-rhs pipeline over separate upload /
-    download streams, nrhs = 1 contractions with packed octant columns)
-    equal the device-resident batched apply bit for bit"""
+    download streams, nrhs = 1 contractions with packed octant columns; 7
+    fields cycle the three-slot device ring twice) equal the device-resident
+    batched apply bit for bit"""
     torch = torch_cuda
     n = 128
     blocks = _symmetric_blocks(n, nz, 40 + nz)
