@@ -41,7 +41,11 @@ constexpr int kGreenThreads = EMIE_GREEN_THREADS;  // threads per assemble CTA
 #ifndef EMIE_GREEN_SLOTS
 #define EMIE_GREEN_SLOTS 2
 #endif
-constexpr int kGreenSlots = EMIE_GREEN_SLOTS;  // full-lambda-range pairs per thread (+ a lambda-split tail)
+constexpr int kGreenSlots = EMIE_GREEN_SLOTS;
+#ifndef EMIE_GREEN_PAIR_UNROLL
+#define EMIE_GREEN_PAIR_UNROLL 2
+#endif
+constexpr int kPairUnroll = EMIE_GREEN_PAIR_UNROLL;  // lambdas per pair-phase loop body  // full-lambda-range pairs per thread (+ a lambda-split tail)
 
 // ------------------------------------------------------ complex helpers ----
 // Smith's algorithm: the exact-path fallback of cdiv (zero or non-finite divisor)
@@ -885,6 +889,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     __syncthreads();
     PHASE_MARK(5);
     // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
+#pragma unroll kPairUnroll
     for (int li = 0; li < lc; ++li) {
       double wl[6];
 #pragma unroll
