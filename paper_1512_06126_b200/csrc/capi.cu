@@ -275,6 +275,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
   op.nent = 4 * op.ntri + 2 * op.nfull;
   op.nsd = nz / 2 + 1;
   op.mma = nz == 8 || nz == 16 || nz == 32;
+  op.rows = nz == 48 || nz == 64;
   // MMA layout (operator.cuh): bank of each element, bank-sorted triangles
   std::vector<int> tri_pos;
   const int H = nz / 2;
@@ -289,6 +290,9 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
       }
     op.ntriP = 8 * *std::max_element(cnt, cnt + 8);
     op.nentD = 4 * op.ntriP + 2 * op.nfull;
+  } else if (op.rows) {
+    op.ntriP = op.ntri;
+    op.nentD = 8 * op.nfull;  // eight dense blocks (operator.cuh)
   } else {
     op.ntriP = op.ntri;
     op.nentD = op.nent;  // compact wrapped-diagonal layout (operator.cuh)
@@ -340,6 +344,19 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
           }
     op.ctab = dev_alloc<uint32_t>(tab.size());
     EMIE_CUDA(cudaMemcpy(op.ctab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  } else if (op.rows) {
+    // symmetric entry (k, kp) -> both triangles of its dense block; xz / yz
+    // (k, kp) -> (k, kp) of the block and (kp, k) of its transpose
+    const int f = op.nfull;
+    for (int c = 0; c < 4; ++c)
+      for (int k = 0; k < nz; ++k)
+        for (int kp = k; kp < nz; ++kp)
+          op.emap_host[c * op.ntri + k * nz - k * (k - 1) / 2 + (kp - k)] =
+              int2{c * f + k * nz + kp, kp == k ? -1 : c * f + kp * nz + k};
+    for (int c = 0; c < 2; ++c)
+      for (int k = 0; k < nz; ++k)
+        for (int kp = 0; kp < nz; ++kp)
+          op.emap_host[4 * op.ntri + c * f + k * nz + kp] = int2{(4 + c) * f + k * nz + kp, (6 + c) * f + kp * nz + k};
   } else {
   // reference entry -> wrapped-diagonal slot (see operator.cuh)
   for (int c = 0; c < 4; ++c)
@@ -627,7 +644,11 @@ int emie_cu_operator_from_spectra(int nx, int ny, int nz, double omega, const do
       const int nent_c = c < 4 ? op.ntri : op.nfull;
       const int off = c < 4 ? c * op.ntri : 4 * op.ntri + (c - 4) * op.nfull;
       for (std::size_t m = 0; m < modes; ++m)
-        for (int s = 0; s < nent_c; ++s) mm[m * op.nentD + op.emap_host[off + s].x] = in[m * nent_c + s];
+        for (int s = 0; s < nent_c; ++s) {
+          const int2 sl = op.emap_host[off + s];
+          mm[m * op.nentD + sl.x] = in[m * nent_c + s];
+          if (sl.y >= 0) mm[m * op.nentD + sl.y] = in[m * nent_c + s];
+        }
       in += modes * nent_c;
     }
     EMIE_CUDA(cudaMemcpy(op.spec, mm.data(), mm.size() * sizeof(cplx), cudaMemcpyHostToDevice));

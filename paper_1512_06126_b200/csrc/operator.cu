@@ -503,6 +503,198 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   else consume(std::integral_constant<int, 2>{});
 }
 
+// ------------------------------ contraction, streamed row blocks (nz 48/64) -----
+// For nz in {48, 64} (config 4: nz = 64) a mode block no longer fits SMEM
+// (265 KB even in triangle form at nz = 64), so the operator is stored as
+// eight dense row-major nz x nz blocks per mode, [xx yy zz xy xz yz xz^T yz^T]
+// (the symmetric components hold both triangles; xz and yz are stored as is
+// and transposed), and the block streams through a ring of K-chunks like a
+// GEMM main loop. Chunk (b, kc) = columns kp in [8kc, 8kc+8) of third b of
+// M = [[xx xy xz] [xy yy yz] [-xz^T -yz^T zz]] for all 3nz rows: one
+// tensor-map box (8 columns x nz rows, 128-byte swizzle) per row third a,
+// since every column slice M_ab(:, kp-range) is a row slice of one stored
+// block (M_ab = M_ba^T for the symmetric parts). 3nz/16 consumer warps own two
+// 8-row output tiles each; the products, the 3-multiply complex form, the
+// octant column groups and the output stores are those of contract_mma_kernel.
+constexpr int kRowsRing = 4;  // K-chunk stages
+template <int NZ>
+constexpr int rows_warps() { return 3 * NZ / 16; }
+__host__ __device__ constexpr int rows_block_id(int a, int b) {
+  // M_ab -> stored block: xx yy zz xy xz yz xzT yzT = 0..7
+  return a == b ? a : (a < 2 && b < 2) ? 3 : b == 2 ? 4 + a : 6 + b;
+}
+
+template <int NZ, bool OCT>
+__global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
+    contract_rows_kernel(const __grid_constant__ CUtensorMap tm, cplx* S, int ex, int ey, int qx, int q0, int q1,
+                         int qbase, int nrhs, const int* __restrict__ octl, int noct) {
+  constexpr int np = 3 * NZ, ldu = np + 4;
+  constexpr int W = rows_warps<NZ>();
+  constexpr int NC = ct_cols<OCT>();
+  constexpr int NT = NZ / 8;           // row tiles (and K-chunks) per third
+  constexpr int NCH = 3 * NT;          // K-chunks per mode
+  constexpr uint32_t kBox = NZ * 128;  // one box: nz rows x 8 complex
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* rempty = rfull + kRowsRing;
+  uint64_t* ufull = rempty + kRowsRing;
+  uint64_t* uempty = ufull + kUStages;
+  long long* colbase = reinterpret_cast<long long*>(smraw + 128);
+  unsigned char* ring = smraw + 1024;  // 1024-aligned boxes (swizzle atoms)
+  cplx* ubuf = reinterpret_cast<cplx*>(ring + kRowsRing * 3 * kBox);
+  const size_t E = static_cast<size_t>(ex) * ey;
+  constexpr uint32_t colbytes = np * sizeof(cplx);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRowsRing; ++i) {
+      mbar_init(rfull + i, 1);
+      mbar_init(rempty + i, W);
+    }
+    for (int i = 0; i < kUStages; ++i) {
+      mbar_init(ufull + i, 1);
+      mbar_init(uempty + i, W);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kUStages * NC * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
+  __syncthreads();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const int G = gridDim.x;
+  const int nwork = OCT ? noct : q1 - q0;
+
+  if (warp == W) {  // ---- producer warp
+    int j = 0;
+    for (int t = blockIdx.x; t < nwork; t += G, ++j) {
+      const int qm = OCT ? __ldg(octl + t) : q0 + t;
+      const int us = j % kUStages;
+      if (j >= kUStages) mbar_wait(uempty + us, static_cast<uint32_t>((j / kUStages - 1) & 1));
+      const int ncol = mirror_count(qm, qx, ex, ey) * nrhs;
+      const int qmy = qm / qx, qmx = qm - qmy * qx;
+      const int ncol2 = OCT && qmx != qmy ? ncol : 0;
+      const int t0 = ncol + ncol2 <= 8 ? ncol : 8;
+      const bool tr = OCT && lane >= t0 && lane < t0 + ncol2;
+      const int c = tr ? lane - t0 : lane;
+      const int mi = c / nrhs, r = c - mi * nrhs;
+      long long base = -1LL;
+      if (lane < ncol)
+        base = (static_cast<long long>(r) * E + mirror_mode(qm, mi, qx, ex, ey)) * np;
+      else if (tr)
+        base = (static_cast<long long>(r) * E + mirror_mode(qmx * qx + qmy, mi, qx, ex, ey)) * np;
+      if (lane < NC) colbase[us * NC + lane] = base < 0 ? -1LL : (tr ? base | kSwapCol : base);
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(ufull + us, (ncol + ncol2) * colbytes);
+      __syncwarp();
+      if (base >= 0) bulk_g2s(ubuf + (us * NC + lane) * ldu, S + base, colbytes, ufull + us);
+      // the block's K-chunks through the ring
+      if (lane == 0) {
+        const int mode = qm - qbase;
+        for (int ch = 0; ch < NCH; ++ch) {
+          const long long gc = static_cast<long long>(j) * NCH + ch;
+          const int st = static_cast<int>(gc % kRowsRing);
+          if (gc >= kRowsRing) mbar_wait(rempty + st, static_cast<uint32_t>((gc / kRowsRing - 1) & 1));
+          const int b = ch / NT, kc = ch - b * NT;
+          mbar_expect_tx(rfull + st, 3 * kBox);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            tma_load_4d(ring + (st * 3 + a) * kBox, &tm, 16 * kc, 0, rows_block_id(a, b), mode, rfull + st);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---- consumers: tiles warp and warp + W (row tile ti: third a = ti / NT, rows 8 (ti % NT) ..)
+  const int fr = lane >> 2, fc = lane & 3;
+  int ta[2], trow[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int ti = warp + i * W;
+    ta[i] = ti / NT;
+    trow[i] = (ti - ta[i] * NT) * 8 + fr;  // this lane's A row inside third ta[i]
+  }
+  auto run = [&](auto NGC, int us, long long gc0) {
+    constexpr int NG = decltype(NGC)::value;
+    const cplx* U = ubuf + us * NC * ldu + fr * ldu + fc;
+    long long cbl = 0;
+    if (OCT && NG == 1) cbl = colbase[us * NC + fr];
+    const bool swp = OCT && NG == 1 && cbl >= 0 && (cbl & kSwapCol);
+    double p1[2][NG][2], p2[2][NG][2], p3[2][NG][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) p1[i][g][0] = p1[i][g][1] = p2[i][g][0] = p2[i][g][1] = p3[i][g][0] = p3[i][g][1] = 0.0;
+#pragma unroll 1
+    for (int b = 0; b < 3; ++b) {
+      const int bsw = b == 2 ? 2 : 1 - b;  // third of a transposed-mode column
+#pragma unroll 1
+      for (int kc = 0; kc < NT; ++kc) {
+        const long long gc = gc0 + b * NT + kc;
+        const int st = static_cast<int>(gc % kRowsRing);
+        mbar_wait(rfull + st, static_cast<uint32_t>((gc / kRowsRing) & 1));
+        const unsigned char* box = ring + st * 3 * kBox;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int col = 4 * ks + fc;  // complex column inside the chunk
+          cplx bu[NG];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            const int third = (g == 1 || swp) ? bsw : b;
+            bu[g] = U[g * 8 * ldu + third * NZ + 8 * kc + 4 * ks];
+          }
+          double bsum[NG];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) bsum[g] = bu[g].re + bu[g].im;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int row = trow[i];
+            const cplx mv = *reinterpret_cast<const cplx*>(box + ta[i] * kBox + row * 128 + ((col ^ (row & 7)) << 4));
+            const bool neg = ta[i] == 2 && b < 2;  // -xz^T, -yz^T
+            const double sg = neg ? -1.0 : 1.0;
+            const double ar = sg * mv.re, ai = sg * mv.im;
+            const double as = ar + ai;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) dmma(p1[i][g][0], p1[i][g][1], ar, bu[g].re);
+#pragma unroll
+            for (int g = 0; g < NG; ++g) dmma(p2[i][g][0], p2[i][g][1], ai, bu[g].im);
+#pragma unroll
+            for (int g = 0; g < NG; ++g) dmma(p3[i][g][0], p3[i][g][1], as, bsum[g]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(rempty + st);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int a = ta[i];
+      const int rowc = trow[i];  // C row fr of the tile = the lane's A row
+      const int plane = a * NZ + rowc;
+      const int asw = a == 2 ? 2 : 1 - a;
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
+          if (cb >= 0) {
+            const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? asw * NZ + rowc : plane);
+            S[o] = cplx{p1[i][g][h] - p2[i][g][h], p3[i][g][h] - p1[i][g][h] - p2[i][g][h]};
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(uempty + us);
+  };
+  int j = 0;
+  for (int t = blockIdx.x; t < nwork; t += G, ++j) {
+    const int us = j % kUStages;
+    mbar_wait(ufull + us, static_cast<uint32_t>((j / kUStages) & 1));
+    const long long gc0 = static_cast<long long>(j) * NCH;
+    if (OCT && colbase[us * NC + 8] >= 0) run(std::integral_constant<int, 2>{}, us, gc0);
+    else run(std::integral_constant<int, 1>{}, us, gc0);
+  }
+}
+
 // exact x <-> y symmetry of the compressed blocks (the property the octant
 // contraction relies on): block(oj, oi) == block(oi, oj) with xx <-> yy and
 // xz <-> yz, bit for bit, for every offset pair including oi == oj
@@ -601,6 +793,35 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
   for (int r0 = 0; r0 < nrhs; r0 += 2) {
     const int g = std::min(2, nrhs - r0);
     cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
+    if (op.rows) {
+      const bool oct = use_octant(op, q0, q1);
+      const int nc = oct ? ct_cols<true>() : ct_cols<false>();
+      const size_t smem = 1024 + static_cast<size_t>(kRowsRing) * 3 * op.nz * 128 +
+                          kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+      // the stored modes as {2nz doubles, nz rows, 8 blocks, modes}; box = 8 complex x nz rows
+      CUtensorMap tm;
+      const uint64_t dims[4] = {2ull * op.nz, static_cast<uint64_t>(op.nz), 8ull, static_cast<uint64_t>(op.qcount)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(op.nz) * 16, static_cast<uint64_t>(op.nz) * op.nz * 16,
+                                   8ull * op.nz * op.nz * 16};
+      const uint32_t box[4] = {16, static_cast<uint32_t>(op.nz), 1, 1};
+      encode_tensor_map_f64(&tm, op.spec, 4, dims, strides, box);
+      const int nwork = oct ? op.noct : nmodes;
+      auto launch = [&](auto kern, int warps) {
+        const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
+        const int grid = std::max(1, std::min(sms * per_sm, nwork));
+        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
+                                                   op.noct);
+      };
+      if (op.nz == 48) {
+        if (oct) launch(contract_rows_kernel<48, true>, rows_warps<48>());
+        else launch(contract_rows_kernel<48, false>, rows_warps<48>());
+      } else {
+        if (oct) launch(contract_rows_kernel<64, true>, rows_warps<64>());
+        else launch(contract_rows_kernel<64, false>, rows_warps<64>());
+      }
+      check_launch("contract_rows_kernel");
+      continue;
+    }
     if (op.mma) {
       const bool oct = use_octant(op, q0, q1);
       const int nc = oct ? ct_cols<true>() : ct_cols<false>();

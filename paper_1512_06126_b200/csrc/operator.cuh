@@ -45,6 +45,9 @@ struct Operator {
   // kp rotated to bank f. With the tile rows {4m..4m+3} u {4m+nz/2..} every
   // quarter-warp of a fragment load touches 8 distinct banks.
   bool mma = false;
+  // ROWS layout (nz in {48, 64}, streamed contraction, operator.cu): per mode
+  // eight dense row-major nz x nz blocks [xx yy zz xy xz yz xz^T yz^T]
+  bool rows = false;
   int ntriP = 0;
   uint32_t* ctab = nullptr;  // [a][b][k][kp] -> slot of M_ab(k,kp), bit 31: negated
   cplx* blocks = nullptr;    // optional compressed blocks, (ny*nx)*nent

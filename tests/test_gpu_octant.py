@@ -41,7 +41,7 @@ def _symmetric_blocks(n, nz, seed):
 
 
 @pytest.mark.parametrize("n,nz", [(16, 8), (12, 16), (8, 32), (20, 32), (3, 8), (1, 16),
-                                  (6, 5), (9, 12), (4, 48), (5, 64)])  # the last four: DFMA contraction
+                                  (6, 5), (9, 12), (4, 48), (5, 64)])  # DFMA (nz 5, 12), streamed rows (48, 64)
 def test_octant_apply_matches_oracle(torch_cuda, n, nz):
     blocks = _symmetric_blocks(n, nz, 31 * n + nz)
     dims, comp = orc.transform_operator(blocks, n, n, nz)

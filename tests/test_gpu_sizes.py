@@ -1,7 +1,8 @@
 """GPU parity across the kernel variants the benchmark grids do not reach:
 every power-of-two embedding length of the streaming FFT path (32 .. 2048),
 the mixed-radix path, every nz of the FP64 tensor-core contraction (8, 16,
-32) and the DFMA contraction (other nz, up to config 4's 64), single and
+32), the streamed row-block contraction (nz 48 and config 4's 64) and the
+DFMA contraction (other nz), single and
 batched right-hand sides,
 operator and system applies. The check is the numpy restatement of
 apply(SpectralOperator) / apply(SystemOperator) (oracle/emie_oracle.py,
@@ -26,8 +27,9 @@ CASES = [
     (512, 1, 2),    # ex 1024
     (1024, 1, 1),   # ex 2048
     (10, 6, 4),     # 20 x 12, mixed radix only
-    (4, 3, 64),     # DFMA nz 64 (config 4's depth)
-    (3, 2, 48),     # DFMA nz 48
+    (4, 3, 64),     # streamed row blocks nz 64 (config 4's depth)
+    (3, 2, 48),     # streamed row blocks nz 48
+    (3, 3, 40),     # DFMA nz 40
 ]
 
 
