@@ -406,14 +406,18 @@ def run_ours(args):
     # of a square grid (hx == hy) only the octant qmx <= qmy (operator.cu)
     octant = emie.xy_symmetric(sop)
     blocks_read = sop.qx * (sop.qx + 1) // 2 if octant else modes
-    bytes_ct = blocks_read * nent * 16 + 2 * NRHS * E * 3 * nz * 16
+    # stored entries per block: the reference's 2nz(2nz+1), or for nz 48/64 the
+    # eight dense nz x nz blocks the streamed contraction reads (operator.cuh)
+    nent_read = 8 * nz * nz if nz in (48, 64) else nent
+    bytes_ct = blocks_read * nent_read * 16 + 2 * NRHS * E * 3 * nz * 16
     flops_ct = NRHS * 72.0 * nz * nz * E
     ct_ms = ms5[2] / max(1, cnt5[2])
     hbm, hbm_kind = peaks()
     fp64 = ctypes.c_double(0.0)
     emie._check(L.emie_cu_probe_fp64(ctypes.byref(fp64), sp))
     achieved = bytes_ct / (ct_ms * 1e-3) / 1e9
-    ct_kernel = ("contract_mma_kernel<%d, %d>" % (nz, int(octant))) if nz in (8, 16, 32) else "contract_kernel"
+    ct_kernel = (("contract_mma_kernel<%d, %d>" % (nz, int(octant))) if nz in (8, 16, 32) else
+                 ("contract_rows_kernel<%d, %d>" % (nz, int(octant))) if nz in (48, 64) else "contract_kernel")
     traffic = None  # dram read + write per launch, from the committed ncu --set full capture
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
@@ -431,7 +435,7 @@ def run_ours(args):
                  "peak_source": "emie_cu_probe_fp64 (max of a DFMA and a DMMA m8n8k4 loop, this GPU)",
                  "flops_per_launch": flops_ct,
                  "flops": "8 per complex multiply-add of the (3nz)^2 mode matrices, all ex*ey modes",
-                 "issued_dmma_frac": (0.75 * tflops / fp64.value) if (fp64.value and nz in (8, 16, 32)) else None}
+                 "issued_dmma_frac": (0.75 * tflops / fp64.value) if (fp64.value and nz in (8, 16, 32, 48, 64)) else None}
     tensor_bound = fp64.value and flops_ct / (fp64.value * 1e12) > bytes_ct / (hbm * 1e9)
     roofline = dict(bound="tensor" if tensor_bound else "hbm", kernel=ct_kernel,
                     **(fp64_view if tensor_bound else hbm_view),
