@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kStreamThreads, P::kStageBytes <= 16384 ? (NST
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const int jj = j + r * M;
-        v[r] = jj < p.nin ? p.pre(ops, t, r, jj, p.staged(stage[st], t, jj)) : cplx{0.0, 0.0};
+        v[r] = jj < p.nin ? p.pre(ops, t, r, jj, p.template staged<N>(stage[st], t, jj)) : cplx{0.0, 0.0};
       }
       butterfly<16>(v, s);
 #pragma unroll
@@ -599,7 +599,7 @@ struct Half {
 // x forward: tile = RT rows iy0.. of plane pr (nrhs*np planes); r2 on load
 struct FxStream {
   static constexpr bool kInverse = false, kTFast = true;
-  static constexpr int kRowBytes = 8 * 128 * 16;     // N = 256: 8 rows of <= 128 points
+  static constexpr int kRowBytes = 8 * 128 * 16;     // 8 rows of <= 128 points (N = 256) or 4 of <= 256 (N = 512)
   static constexpr int kStageBytes = 2 * kRowBytes;  // u rows, then the matching r2 rows
   const cplx* u;
   const cplx* r2;
@@ -660,6 +660,7 @@ struct FxStream {
       bulk_g2s(stg + kRowBytes / sizeof(cplx), r2 + (static_cast<size_t>(iz) * ny + iy0) * nx, bytes, bar);
     }
   }
+  template <int N>
   __device__ cplx staged(const cplx* stg, int t, int jj) const {
     const cplx x = stg[t * nx + jj];
     return r2 ? stg[kRowBytes / sizeof(cplx) + t * nx + jj] * x : x;
@@ -674,7 +675,7 @@ struct FxStream {
 // y forward: tile = PC planes p0.. at column mx of rhs r; mirror signs on store
 struct FyStream {
   static constexpr bool kInverse = false, kTFast = true;
-  static constexpr int kStageBytes = 8 * 128 * 16;  // N = 256: 8 planes of <= 128 points
+  static constexpr int kStageBytes = 8 * 128 * 16;  // 8 planes of <= 128 points (N = 256) or 4 of <= 256
   const cplx* T;
   cplx* S;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
@@ -721,6 +722,7 @@ struct FyStream {
     mbar_expect_tx(bar, bytes);
     bulk_g2s(stg, T + ((static_cast<size_t>(r) * ex + mx) * np + p0) * ny, bytes, bar);
   }
+  template <int N>
   __device__ cplx staged(const cplx* stg, int t, int jj) const { return stg[t * ny + jj]; }
   // S[r][mx][my][plane] with the mirror signs: lanes t (= plane) fastest
   template <int N>
@@ -732,11 +734,22 @@ struct FyStream {
   }
 };
 
+// byte offset of 16-byte chunk t of staged row jj: N = 256 rows of 128 B with
+// the 128-byte swizzle (chunk ^ row mod 8), N = 512 rows of 64 B with the
+// 64-byte swizzle (chunk ^ (row / 2) mod 4)
+template <int N>
+__device__ __forceinline__ int stage_off(int t, int jj) {
+  if constexpr (N == 256) return jj * 128 + ((t ^ (jj & 7)) << 4);
+  else return jj * 64 + ((t ^ ((jj >> 1) & 3)) << 4);
+}
+
 // y inverse: tile = PC planes p0.. at column mx; mirror signs undone on load
 struct IyStream {
   static constexpr bool kInverse = true, kTFast = false;
-  static constexpr int kStageBytes = 256 * 128;  // N = 256: [my][8 planes], 128-byte swizzle
-  CUtensorMap tm;  // S as {2 np doubles, ey, nrhs ex}, box {16, 256, 1}
+  // N = 256: [my][8 planes] (128-byte rows, 128-byte swizzle); N = 512:
+  // [my][4 planes] (64-byte rows, 64-byte swizzle), two boxes of 256 my
+  static constexpr int kStageBytes = 256 * 128;
+  CUtensorMap tm;  // S as {2 np doubles, ey, nrhs ex}, box {16, 256, 1} (N = 512: {8, 256, 1})
   const cplx* S;
   cplx* T;
   int ny, ex, ey, nz, np, gpc, nrhs, nin;
@@ -784,12 +797,15 @@ struct IyStream {
     int r, mx, p0;
     coords<N>(tile, r, mx, p0);
     mbar_expect_tx(bar, kStageBytes);
-    tma_load_3d(stg, &tm, 2 * p0, 0, r * ex + mx, bar);
+#pragma unroll
+    for (int h = 0; h < N / 256; ++h)
+      tma_load_3d(reinterpret_cast<unsigned char*>(stg) + h * (kStageBytes * 256 / N), &tm, 2 * p0, 256 * h,
+                  r * ex + mx, bar);
   }
   // element jj (my) of transform t (plane): 16-byte chunk t of row jj, swizzled
+  template <int N>
   __device__ cplx staged(const cplx* stg, int t, int jj) const {
-    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + jj * 128 +
-                                          ((t ^ (jj & 7)) << 4));
+    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + stage_off<N>(t, jj));
   }
   // T[r][mx][plane][iy], iy < ny: lanes j (= iy) fastest
   template <int N>
@@ -803,8 +819,9 @@ struct IyStream {
 // the thread's kept outputs (slot b*R/2 + r, r < R/2: ix < N/2)
 struct IxStream {
   static constexpr bool kInverse = true, kTFast = false;
-  static constexpr int kStageBytes = 256 * 128;  // N = 256: [mx][8 rows], 128-byte swizzle
-  CUtensorMap tm;  // T as {2 ny doubles, np, ex, nrhs}, box {16, 1, 256, 1}
+  // N = 256: [mx][8 rows], 128-byte swizzle; N = 512: [mx][4 rows], 64-byte swizzle, two boxes
+  static constexpr int kStageBytes = 256 * 128;
+  CUtensorMap tm;  // T as {2 ny doubles, np, ex, nrhs}, box {16, 1, 256, 1} (N = 512: {8, 1, 256, 1})
   const cplx* T;
   const cplx* u;
   cplx* out;
@@ -864,11 +881,14 @@ struct IxStream {
     const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
     const int r = pr / np, plane = pr - r * np;
     mbar_expect_tx(bar, kStageBytes);
-    tma_load_4d(stg, &tm, 2 * iy0, plane, 0, r, bar);
+#pragma unroll
+    for (int h = 0; h < N / 256; ++h)
+      tma_load_4d(reinterpret_cast<unsigned char*>(stg) + h * (kStageBytes * 256 / N), &tm, 2 * iy0, plane, 256 * h,
+                  r, bar);
   }
+  template <int N>
   __device__ cplx staged(const cplx* stg, int t, int jj) const {
-    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + jj * 128 +
-                                          ((t ^ (jj & 7)) << 4));
+    return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + stage_off<N>(t, jj));
   }
   // out[pr][iy][ix], ix < nx: lanes j (= ix) fastest
   template <int N>
@@ -915,9 +935,8 @@ void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
 #ifndef EMIE_TMA_NST_FWD
 #define EMIE_TMA_NST_FWD 1
 #endif
-template <class P, int NST>
+template <int N, class P, int NST>
 void launch_tma(const P& p, int ntiles, const cplx* tw, cudaStream_t st, const char* what) {
-  constexpr int N = 256;
   const size_t smem = NST * static_cast<size_t>(P::kStageBytes) +
                       (static_cast<size_t>(Geo<N>::tile) + N) * sizeof(cplx) + NST * sizeof(uint64_t);
   const int per_sm =
@@ -946,7 +965,7 @@ void launch_stream(const P& p, int ntiles, const cplx* tw, int n, cudaStream_t s
 
 // ------------------------------------------------------------------ host --
 void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
-                           const uint64_t* strides_bytes, const uint32_t* box) {
+                           const uint64_t* strides_bytes, const uint32_t* box, int swizzle) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -963,7 +982,8 @@ void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const ui
     if (i + 1 < rank) sb[i] = strides_bytes[i];
   }
   const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), d, sb, b, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(EMIE_CU_RUNTIME_ERROR, "cuTensorMapEncodeTiled failed");
 }
@@ -1019,8 +1039,9 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.u = d_in; p.r2 = r2; p.T = T;
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
-    p.r2_staged = op.ex == 256;
-    if (op.ex == 256) launch_tma<FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    p.r2_staged = op.ex == 256 || op.ex == 512;
+    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    else if (op.ex == 512) launch_tma<512, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
     else launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_fx");
   } else {
     const bool p2 = op.p2x;
@@ -1044,7 +1065,8 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.T = T; p.S = S;
     p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
     p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ny;
-    if (op.ey == 256) launch_tma<FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
+    if (op.ey == 256) launch_tma<256, FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
+    else if (op.ey == 512) launch_tma<512, FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
     else launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_fy");
   } else {
     const bool p2 = op.p2y;
@@ -1073,12 +1095,14 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
     p.S = S; p.T = T;
     p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
     p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ey;
-    if (op.ey == 256) {
-      const uint64_t dims[3] = {2ull * np, 256ull, static_cast<uint64_t>(nrhs) * op.ex};
-      const uint64_t strides[2] = {static_cast<uint64_t>(np) * 16, 256ull * np * 16};
-      const uint32_t box[3] = {16, 256, 1};
-      encode_tensor_map_f64(&p.tm, S, 3, dims, strides, box);
-      launch_tma<IyStream, EMIE_TMA_NST_INV>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_iy");
+    if (op.ey == 256 || op.ey == 512) {
+      const bool w = op.ey == 512;
+      const uint64_t dims[3] = {2ull * np, static_cast<uint64_t>(op.ey), static_cast<uint64_t>(nrhs) * op.ex};
+      const uint64_t strides[2] = {static_cast<uint64_t>(np) * 16, static_cast<uint64_t>(op.ey) * np * 16};
+      const uint32_t box[3] = {w ? 8u : 16u, 256, 1};
+      encode_tensor_map_f64(&p.tm, S, 3, dims, strides, box, w ? 64 : 128);
+      if (w) launch_tma<512, IyStream, EMIE_TMA_NST_INV>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_iy");
+      else launch_tma<256, IyStream, EMIE_TMA_NST_INV>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_iy");
     } else {
       launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_iy");
     }
@@ -1105,13 +1129,16 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.ex;
     p.inv = 1.0 / static_cast<double>(op.lateral());
-    if (op.ex == 256) {
-      const uint64_t dims[4] = {2ull * op.ny, static_cast<uint64_t>(np), 256ull, static_cast<uint64_t>(nrhs)};
+    if (op.ex == 256 || op.ex == 512) {
+      const bool w = op.ex == 512;
+      const uint64_t dims[4] = {2ull * op.ny, static_cast<uint64_t>(np), static_cast<uint64_t>(op.ex),
+                                static_cast<uint64_t>(nrhs)};
       const uint64_t strides[3] = {static_cast<uint64_t>(op.ny) * 16, static_cast<uint64_t>(np) * op.ny * 16,
-                                   256ull * np * op.ny * 16};
-      const uint32_t box[4] = {16, 1, 256, 1};
-      encode_tensor_map_f64(&p.tm, T, 4, dims, strides, box);
-      launch_tma<IxStream, EMIE_TMA_NST_INV>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_ix");
+                                   static_cast<uint64_t>(op.ex) * np * op.ny * 16};
+      const uint32_t box[4] = {w ? 8u : 16u, 1, 256, 1};
+      encode_tensor_map_f64(&p.tm, T, 4, dims, strides, box, w ? 64 : 128);
+      if (w) launch_tma<512, IxStream, EMIE_TMA_NST_INV>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_ix");
+      else launch_tma<256, IxStream, EMIE_TMA_NST_INV>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_ix");
     } else {
       launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_ix");
     }

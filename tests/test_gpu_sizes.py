@@ -23,7 +23,9 @@ CASES = [
     (16, 16, 32),   # 32 x 32, both axes streaming
     (128, 2, 5),    # ex 256; DFMA nz 5
     (2, 128, 12),   # ey 256; DFMA nz 12
-    (256, 1, 3),    # ex 512
+    (256, 1, 3),    # ex 512 (TMA x passes)
+    (2, 256, 8),    # ey 512 (TMA y passes)
+    (256, 256, 2),  # 512 x 512 (config 4's embedding), all four TMA passes
     (512, 1, 2),    # ex 1024
     (1024, 1, 1),   # ex 2048
     (10, 6, 4),     # 20 x 12, mixed radix only
