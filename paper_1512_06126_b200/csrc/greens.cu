@@ -717,17 +717,20 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     PHASE_MARK(4);
     // phase 1b: prefix products of theta per (lambda, gamma) as
     // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l.
-    // nz <= 64: eight lanes per (lambda, gamma), four tasks per warp at once;
+    // nz <= 64: eight (nz > 32: sixteen) lanes per (lambda, gamma), several tasks per warp at once;
     // a lane owns ceil(nz/8) consecutive intervals: local products, a 3-step
     // shuffle scan over the eight lanes, the lane's exclusive prefix
     // multiplied in. Mantissas (max component in [1, 2), modulus < 2^1.5) are
     // not renormalised inside: a product of <= 64 stays below 2^96.
     if (nz <= 64) {
-      const int lane = threadIdx.x & 31, sub = lane & 7;
-      const int per = (nz + 7) >> 3;
+      // lanes per task: 8 (nz <= 32) or 16 (deeper grids: half the serial
+      // per-lane work; lc * 2 * 16 still fits one pass of the CTA at LC = 8)
+      const int TW = nz > 32 ? 16 : 8, tpw = 32 / TW;
+      const int lane = threadIdx.x & 31, sub = lane & (TW - 1);
+      const int per = (nz + TW - 1) / TW;
       const int ntask = lc * 2;
-      for (int task0 = (threadIdx.x >> 5) * 4; task0 < ntask; task0 += (blockDim.x >> 5) * 4) {
-        const int task = task0 + (lane >> 3);
+      for (int task0 = (threadIdx.x >> 5) * tpw; task0 < ntask; task0 += (blockDim.x >> 5) * tpw) {
+        const int task = task0 + lane / TW;
         const bool live = task < ntask;
         const int li = live ? task >> 1 : 0, gm = task & 1;
         const int fT = gm ? fPic : fPiu;
@@ -758,15 +761,15 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
           le += eq;
           lz += zq;
         }
-        // inclusive scan of the lane totals over the eight lanes of the task
+        // inclusive scan of the lane totals over the TW lanes of the task
         cplx sm_ = lm;
         int se = le, sz = lz;
-#pragma unroll
-        for (int off = 1; off < 8; off <<= 1) {
-          const double mr = __shfl_up_sync(0xffffffffu, sm_.re, off, 8);
-          const double mi = __shfl_up_sync(0xffffffffu, sm_.im, off, 8);
-          const int oe = __shfl_up_sync(0xffffffffu, se, off, 8);
-          const int oz = __shfl_up_sync(0xffffffffu, sz, off, 8);
+#pragma unroll 4
+        for (int off = 1; off < TW; off <<= 1) {
+          const double mr = __shfl_up_sync(0xffffffffu, sm_.re, off, TW);
+          const double mi = __shfl_up_sync(0xffffffffu, sm_.im, off, TW);
+          const int oe = __shfl_up_sync(0xffffffffu, se, off, TW);
+          const int oz = __shfl_up_sync(0xffffffffu, sz, off, TW);
           if (sub >= off) {
             sm_ = cplx{mr, mi} * sm_;
             se += oe;
@@ -774,8 +777,8 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
           }
         }
         // exclusive lane prefix
-        cplx pm = {__shfl_up_sync(0xffffffffu, sm_.re, 1, 8), __shfl_up_sync(0xffffffffu, sm_.im, 1, 8)};
-        int pe = __shfl_up_sync(0xffffffffu, se, 1, 8), pz = __shfl_up_sync(0xffffffffu, sz, 1, 8);
+        cplx pm = {__shfl_up_sync(0xffffffffu, sm_.re, 1, TW), __shfl_up_sync(0xffffffffu, sm_.im, 1, TW)};
+        int pe = __shfl_up_sync(0xffffffffu, se, 1, TW), pz = __shfl_up_sync(0xffffffffu, sz, 1, TW);
         if (sub == 0) {
           pm = {1.0, 0.0};
           pe = 0;
