@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-solve", action="store_true", help="skip the FGMRES solve timing")
     p.add_argument("--strong", action="store_true",
                    help="strong scaling of one grid: depth-slab / mode-shard apply over the N ranks")
+    p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                   help="--strong: column transposes as peer stores (IPC buffers, flag barriers) or NCCL all-to-all")
     return p.parse_args()
 
 
@@ -575,7 +577,15 @@ def run_strong(args):
     n = 3 * cfg.cells()
     U = rng.uniform(-1, 1, (NRHS, n)) + 1j * rng.uniform(-1, 1, (NRHS, n))
     slab = torch.from_numpy(D.slab_of(U, plan, rank, NRHS)).cuda()
-    if world > 1:
+    # column transposes: peer stores over NVLink into the owners' IPC-mapped
+    # buffers (default) or NCCL all-to-all with pack / unpack copies
+    if args.exchange == "peer":
+        if world > 1:
+            px = D.peer_exchange_torch(shard)
+        else:
+            (px,), _ = D.peer_loopback([shard])
+        step = lambda: px.apply(slab)  # noqa: E731
+    elif world > 1:
         sysd = D.DistributedSystem(shard)
         step = lambda: sysd.apply(slab)  # noqa: E731
     else:
@@ -608,8 +618,11 @@ def run_strong(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        out = (sysd.apply(hin.cuda(non_blocking=True)) if world > 1
-               else D.loopback_apply([shard], [hin.cuda(non_blocking=True)])[0])
+        dev_in = hin.cuda(non_blocking=True)
+        if args.exchange == "peer":
+            out = px.apply(dev_in)
+        else:
+            out = sysd.apply(dev_in) if world > 1 else D.loopback_apply([shard], [dev_in])[0]
         hout.copy_(out)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
@@ -623,7 +636,9 @@ def run_strong(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded config conductivity field, seeded fields)",
             "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} sharded over {world} rank(s): "
-                                   "depth slabs + quadrant-mode shards, 2 all-to-alls per apply",
+                                   "depth slabs + quadrant-mode shards, 2 column transposes per apply "
+                                   + ("as peer stores into IPC-mapped buffers (flag barriers)"
+                                      if args.exchange == "peer" else "as NCCL all-to-alls"),
                        "nrhs": NRHS, "slabs": plan.z, "mode_shards": plan.q,
                        "greens_build": "sharded by offset, summed block arrays, per-rank mode-shard spectra"},
             "greens_build_s": greens_s,

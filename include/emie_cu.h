@@ -286,6 +286,29 @@ int emie_cu_move_planes(const double* d_src, double* d_dst, int nrhs, int nidx, 
                         long long modes_total, const int src_desc[4], const int dst_desc[4], int nzh,
                         void* stream);
 
+/* ---------------------------------------------------------------------
+ * Peer-memory exchange of the sharded apply (replaces the
+ * pack / all-to-all / unpack of the column transposes: a rank's
+ * emie_cu_move_planes writes straight into the destination rank's buffer
+ * over NVLink). No reference equivalent (the reference is single-node CPU).
+ * ------------------------------------------------------------------- */
+
+/* exchange buffer shareable through CUDA IPC (plain cudaMalloc, zeroed) */
+int emie_cu_peer_alloc(size_t bytes, void** d_ptr);
+int emie_cu_peer_free(void* d_ptr);
+/* 64-byte IPC handle of a peer buffer / map a peer's buffer into this
+ * process (peer access enabled lazily) / unmap it */
+int emie_cu_ipc_handle(const void* d_ptr, void* h_handle);
+int emie_cu_ipc_open(const void* h_handle, void** d_ptr);
+int emie_cu_ipc_close(void* d_ptr);
+/* after this stream's moves into the G ranks' buffers: release-store epoch
+ * into slot `me` of each rank's flag array (h_flag_ptrs: G device pointers,
+ * peers' flag arrays mapped into this process) */
+int emie_cu_peer_signal(int* const* h_flag_ptrs, int G, int me, int epoch, void* stream);
+/* before this stream reads its buffer: wait until all G slots of d_flags
+ * reach epoch (bounded: traps the context if a peer never signals) */
+int emie_cu_peer_wait(const int* d_flags, int G, int epoch, void* stream);
+
 /* kernel launches issued by this library on the calling thread since the
  * last reset (evidence for bench.py's gpu_launches) */
 long long emie_cu_launch_count(void);

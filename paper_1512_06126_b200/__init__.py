@@ -139,6 +139,14 @@ def lib():
         "emie_cu_contract_modes": [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_move_planes": [vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_longlong, ip, ip,
                                 ctypes.c_int, vp],
+        # peer-memory exchange (distributed.PeerExchange)
+        "emie_cu_peer_alloc": [ctypes.c_size_t, ctypes.POINTER(vp)],
+        "emie_cu_peer_free": [vp],
+        "emie_cu_ipc_handle": [vp, vp],
+        "emie_cu_ipc_open": [vp, ctypes.POINTER(vp)],
+        "emie_cu_ipc_close": [vp],
+        "emie_cu_peer_signal": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
+        "emie_cu_peer_wait": [vp, ctypes.c_int, ctypes.c_int, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)

@@ -768,6 +768,54 @@ int emie_cu_move_planes(const double* d_src, double* d_dst, int nrhs, int nidx, 
   });
 }
 
+int emie_cu_peer_alloc(size_t bytes, void** d_ptr) {
+  return guarded([&] {
+    if (!d_ptr || bytes == 0) fail(EMIE_CU_INVALID_ARGUMENT, "peer_alloc: bad arguments");
+    void* p = nullptr;
+    EMIE_CUDA(cudaMalloc(&p, bytes));  // not the stream-ordered pool: IPC needs the allocation base
+    EMIE_CUDA(cudaMemset(p, 0, bytes));
+    *d_ptr = p;
+  });
+}
+
+int emie_cu_peer_free(void* d_ptr) {
+  return guarded([&] {
+    if (d_ptr) EMIE_CUDA(cudaFree(d_ptr));
+  });
+}
+
+int emie_cu_ipc_handle(const void* d_ptr, void* h_handle) {
+  return guarded([&] {
+    if (!d_ptr || !h_handle) fail(EMIE_CU_INVALID_ARGUMENT, "ipc_handle: null pointer");
+    cudaIpcMemHandle_t hd;
+    EMIE_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(d_ptr)));
+    std::memcpy(h_handle, &hd, sizeof hd);
+  });
+}
+
+int emie_cu_ipc_open(const void* h_handle, void** d_ptr) {
+  return guarded([&] {
+    if (!h_handle || !d_ptr) fail(EMIE_CU_INVALID_ARGUMENT, "ipc_open: null pointer");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, h_handle, sizeof hd);
+    EMIE_CUDA(cudaIpcOpenMemHandle(d_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int emie_cu_ipc_close(void* d_ptr) {
+  return guarded([&] {
+    if (d_ptr) EMIE_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  });
+}
+
+int emie_cu_peer_signal(int* const* h_flag_ptrs, int G, int me, int epoch, void* stream) {
+  return guarded([&] { peer_signal(h_flag_ptrs, G, me, epoch, as_stream(stream)); });
+}
+
+int emie_cu_peer_wait(const int* d_flags, int G, int epoch, void* stream) {
+  return guarded([&] { peer_wait(d_flags, G, epoch, as_stream(stream)); });
+}
+
 int emie_cu_apply_spectral(emie_cu_operator h, const double* d_in, double* d_out, int nrhs,
                            void* stream) {
   return guarded([&] {

@@ -111,6 +111,11 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
 void move_planes(const cplx* src, cplx* dst, int nrhs, int nidx, const int* idx, long long modes_total,
                  const int src_desc[4], const int dst_desc[4], int nzh, cudaStream_t st);
 
+// peer-memory exchange flags (peer.cu): release-store `epoch` into slot `me`
+// of every rank's flag array / wait until all G slots of `flags` reach it
+void peer_signal(int* const* flag_ptrs, int G, int me, int epoch, cudaStream_t st);
+void peer_wait(const int* flags, int G, int epoch, cudaStream_t st);
+
 // Green's build (greens.cu)
 struct FilterParams {
   double step = 0.2, shift = 0.0964;

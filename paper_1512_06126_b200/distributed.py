@@ -197,6 +197,186 @@ class DistributedSystem:
         return sh.stage_inverse(r2)
 
 
+# ------------------------------------------------- peer-memory exchange ----
+class _Buf:
+    """A device buffer by address (exchange buffers live outside torch's
+    allocator: CUDA IPC maps whole cudaMalloc allocations)."""
+
+    def __init__(self, ptr: int):
+        self.ptr = int(ptr)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class PeerExchange:
+    """The sharded apply with the two column transposes done as peer stores
+    (SURVEY.md §8(e).3 over NVLink / NVSwitch; csrc/peer.cu): every rank owns
+    two exchange buffers -- its slab spectrum S_loc[r][m][3 nzl] and the
+    full-depth spectrum S_full[r][m][3 nz] of its quadrant modes -- plus a
+    flag array of G ints, all mapped into every rank through CUDA IPC. A rank
+    moves its slab's columns straight into each owner's S_full (one
+    move_planes pass per destination, the stores cross NVLink), signals the
+    owners, waits for its own G flags, contracts in place, moves the results
+    straight into each slab owner's S_loc, signals, waits, and inverse
+    transforms. No pack / all-to-all / unpack copies and no NCCL call on the
+    data path; the two flag barriers per apply order the buffers' reuse.
+
+    `peers` gives, per rank g, (S_loc, S_full, flags) device addresses as
+    seen from this process: the rank's own allocations for itself, IPC
+    mappings of the others' (PeerExchange.open_ipc) or, for G virtual ranks
+    in one process, the other shards' own buffers (loopback)."""
+
+    def __init__(self, shard: "ShardedApply", peers, own):
+        self.sh, self.peers, self.own = shard, peers, own
+        self.epoch = 0
+        # flag arrays: device addresses (None: a host backend, no device flags)
+        self._flag_ptrs = (None if own[2] is None else
+                           (ctypes.c_void_p * shard.plan.G)(*[p[2] for p in peers]))
+
+    @staticmethod
+    def allocate(shard: "ShardedApply"):
+        """This rank's exchange buffers: (S_loc, S_full, flags) addresses."""
+        from . import lib, _check
+        L, P = lib(), shard.plan
+        sizes = [shard.nrhs * P.E * 3 * shard.nzl * 16, shard.nrhs * P.E * 3 * P.nz * 16, 4 * P.G]
+        out = []
+        for b in sizes:
+            p = ctypes.c_void_p()
+            _check(L.emie_cu_peer_alloc(b, ctypes.byref(p)))
+            out.append(p.value)
+        return (_Buf(out[0]), _Buf(out[1]), out[2])
+
+    @staticmethod
+    def allocate_host(shard: "ShardedApply"):
+        """Host tensors for a NumPy-backend shard (CPU tests of the exchange
+        plan: same moves and stage order, no device flags)."""
+        P, be = shard.plan, shard.be
+        return (be.zeros((shard.nrhs, P.E, 3 * shard.nzl)), be.zeros((shard.nrhs, P.E, 3 * P.nz)), None)
+
+    @staticmethod
+    def _addrs(own):
+        return [own[0].data_ptr(), own[1].data_ptr(), own[2]]
+
+    @staticmethod
+    def free(own):
+        from . import lib
+        for p in PeerExchange._addrs(own):
+            lib().emie_cu_peer_free(ctypes.c_void_p(p))
+
+    @staticmethod
+    def ipc_handles(own) -> List[bytes]:
+        from . import lib, _check
+        out = []
+        for p in PeerExchange._addrs(own):
+            h = ctypes.create_string_buffer(64)
+            _check(lib().emie_cu_ipc_handle(ctypes.c_void_p(p), h))
+            out.append(h.raw)
+        return out
+
+    @staticmethod
+    def open_ipc(handles: List[bytes]):
+        from . import lib, _check
+        out = []
+        for h in handles:
+            p = ctypes.c_void_p()
+            _check(lib().emie_cu_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+            out.append(p.value)
+        return (_Buf(out[0]), _Buf(out[1]), out[2])
+
+    def _stream(self):
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def signal(self):
+        """After this rank's pushes (stream order): epoch += 1 into every rank's flag slot."""
+        from . import lib, _check
+        self.epoch += 1
+        if self._flag_ptrs is None:
+            return
+        P = self.sh.plan
+        _check(lib().emie_cu_peer_signal(self._flag_ptrs, P.G, self.sh.rank, self.epoch, self._stream()))
+
+    def wait(self):
+        """Before reading this rank's buffer: all G ranks reached the epoch."""
+        from . import lib, _check
+        if self._flag_ptrs is None:
+            return
+        _check(lib().emie_cu_peer_wait(ctypes.c_void_p(self.own[2]), self.sh.plan.G, self.epoch, self._stream()))
+
+    # stages (loopback runs each over all virtual ranks before the next)
+    def push_forward(self, U):
+        sh, P, be = self.sh, self.sh.plan, self.sh.be
+        self._U = U
+        S_loc = self.own[0]
+        be.lateral_forward_into(U, S_loc, sh.nrhs)
+        for g in range(P.G):  # my slab's columns of g's modes -> g's full-depth spectrum
+            be.move(S_loc, self.peers[g][1], sh.nrhs, g, P.E, sh._slab_desc(True),
+                    (1, 3 * P.nz, P.nz, P.z[sh.rank]), sh.nzl)
+
+    def push_contracted(self):
+        sh, P, be = self.sh, self.sh.plan, self.sh.be
+        S_full = self.own[1]
+        be.contract(S_full, sh.nrhs, sh.q0, sh.q1)
+        for h in range(P.G):  # my modes' columns of h's planes -> h's slab spectrum
+            nzh = P.nzl(h)
+            be.move(S_full, self.peers[h][0], sh.nrhs, sh.rank, P.E, (1, 3 * P.nz, P.nz, P.z[h]),
+                    (1, 3 * nzh, nzh, 0), nzh)
+
+    def finish(self):
+        out = self.sh.be.lateral_inverse(self.own[0], self._U, self.sh.nrhs)
+        self._U = None
+        return out
+
+    def apply(self, U):
+        """One rank per process (all ranks call it with their slabs)."""
+        self.push_forward(U)
+        self.signal()
+        self.wait()
+        self.push_contracted()
+        self.signal()
+        self.wait()
+        return self.finish()
+
+
+def peer_loopback(shards: Sequence["ShardedApply"], host: bool = False):
+    """G virtual ranks in one process (one GPU, or host tensors with the
+    NumPy backend): every rank's exchange buffers allocated here, the 'peer'
+    buffers are the other shards' own."""
+    owns = [PeerExchange.allocate_host(sh) if host else PeerExchange.allocate(sh) for sh in shards]
+    return [PeerExchange(sh, owns, owns[g]) for g, sh in enumerate(shards)], owns
+
+
+def peer_loopback_apply(xs: Sequence[PeerExchange], slabs):
+    """Stage by stage over the virtual ranks on one stream: every rank's
+    pushes and signals precede every wait (a wait ahead of another virtual
+    rank's signal would block the stream that signal is queued on)."""
+    for x, u in zip(xs, slabs):
+        x.push_forward(u)
+        x.signal()
+    for x in xs:
+        x.wait()
+    for x in xs:
+        x.push_contracted()
+        x.signal()
+    for x in xs:
+        x.wait()
+    return [x.finish() for x in xs]
+
+
+def peer_exchange_torch(shard: "ShardedApply", group=None) -> PeerExchange:
+    """One rank per process: allocate, swap IPC handles over torch.distributed
+    (all_gather_object), map the peers' buffers."""
+    import torch.distributed as dist
+    G, me = shard.plan.G, shard.rank
+    own = PeerExchange.allocate(shard)
+    hs = [None] * G
+    dist.all_gather_object(hs, PeerExchange.ipc_handles(own), group=group)
+    peers = [own if g == me else PeerExchange.open_ipc(hs[g]) for g in range(G)]
+    dist.barrier(group=group)
+    return PeerExchange(shard, peers, own)
+
+
 # -------------------------------------------------------------- backends ----
 class CudaBackend:
     """Stages on the device through the C ABI; tensors are torch complex128
@@ -248,6 +428,11 @@ class CudaBackend:
                                                    ctypes.c_void_p(self.r2.data_ptr()),
                                                    ctypes.c_void_p(S.data_ptr()), nrhs, self._st()))
         return S
+
+    def lateral_forward_into(self, U, S, nrhs):
+        self._check(self.L.emie_cu_lateral_forward(self.geom, ctypes.c_void_p(U.data_ptr()),
+                                                   ctypes.c_void_p(self.r2.data_ptr()),
+                                                   ctypes.c_void_p(S.data_ptr()), nrhs, self._st()))
 
     def contract(self, S, nrhs, q0, q1):
         self._check(self.L.emie_cu_contract_modes(self.op.handle, ctypes.c_void_p(S.data_ptr()), nrhs, q0, q1,
@@ -309,6 +494,9 @@ class NumpyBackend:
         F = np.fft.fft2(pad, axes=(2, 3))  # [r][plane][my][mx]
         S = np.ascontiguousarray(F.transpose(0, 3, 2, 1)).reshape(nrhs, P.E, 3 * nzl)  # m = mx*ey + my
         return self.torch.from_numpy(S)
+
+    def lateral_forward_into(self, U, S, nrhs):
+        S.copy_(self.lateral_forward(U, nrhs))
 
     def contract(self, S, nrhs, q0, q1):
         P = self.plan

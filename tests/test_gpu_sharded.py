@@ -51,6 +51,37 @@ def test_sharded_apply_loopback_bit_identical(torch_cuda, cfg_id, G):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("cfg_id,G", [(1, 1), (1, 2), (1, 3), (1, 8), (2, 4)])
+def test_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G):
+    """the transposes as peer stores (distributed.PeerExchange, csrc/peer.cu:
+    IPC-shareable exchange buffers, move_planes straight into the owner's
+    buffer, release/acquire flag barriers) over G virtual ranks on one GPU,
+    two applies back to back (buffer and epoch reuse): bit-identical to the
+    single-GPU apply"""
+    torch = torch_cuda
+    cfg, grid, sop, sysop = _system(cfg_id)
+    nrhs = 2
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G)
+    emie.xy_symmetric(sop, disable=True)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    xs, owns = D.peer_loopback(shards)
+    try:
+        for rep in range(2):
+            rng = np.random.default_rng(70 + G + rep)
+            n = 3 * cfg.cells()
+            U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+            want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+            slabs = [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)]
+            outs = D.peer_loopback_apply(xs, slabs)
+            got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+            assert np.array_equal(got, want), rep
+        assert all(x.epoch == 4 for x in xs)
+    finally:
+        torch.cuda.synchronize()
+        for o in owns:
+            D.PeerExchange.free(o)
+
+
 def test_mode_shard_rejects_foreign_modes(torch_cuda):
     cfg, grid, sop, _ = _system(1)
     shard = emie.restrict_modes(sop, 10, 20)

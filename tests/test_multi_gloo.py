@@ -157,6 +157,33 @@ def test_sharded_apply_loopback_numpy(G):
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_peer_exchange_loopback_numpy(G):
+    """The peer-store exchange plan (distributed.PeerExchange: each rank moves
+    its columns straight into the owners' buffers, no pack / unpack) over G
+    virtual ranks with host buffers and the NumPy stages, twice in a row
+    (buffer reuse), against the oracle's full apply."""
+    import sys
+    from pathlib import Path
+    import torch
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    from paper_1512_06126_b200 import distributed as D
+    nx, ny, nz, nrhs = 6, 5, 4, 2
+    dims, comp, diag, U, want = _sharded_case(nx, ny, nz, nrhs)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G)
+    shards = []
+    for g in range(G):
+        z0, z1 = plan.z[g], plan.z[g + 1]
+        dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
+        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+    xs, _ = D.peer_loopback(shards, host=True)
+    for _ in range(2):
+        outs = D.peer_loopback_apply(xs, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)) for g in range(G)])
+        got = D.join_slabs([o.numpy() for o in outs], plan, nrhs)
+        assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+    assert all(x.epoch == 4 for x in xs)
+
+
 # ---- FGMRES on depth-sharded vectors (SURVEY.md §8(e).3) -------------------
 def _solve_case(nx=6, ny=5, nz=4, nrhs=2, seed=21):
     import emie_oracle as O
