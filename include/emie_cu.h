@@ -301,6 +301,13 @@ int emie_cu_peer_free(void* d_ptr);
 int emie_cu_ipc_handle(const void* d_ptr, void* h_handle);
 int emie_cu_ipc_open(const void* h_handle, void** d_ptr);
 int emie_cu_ipc_close(void* d_ptr);
+/* emie_cu_contract_modes with the results stored straight into the slab
+ * owners' spectra (fused contraction + return transpose; MMA layout, nz in
+ * {8, 16, 32}): the contracted plane a*nz + k of mode m goes to rank h with
+ * h_z[h] <= k < h_z[h+1], at h_dst[h][(r*E + m)*3nzh + a*nzh + k - h_z[h]]
+ * (nzh = h_z[h+1] - h_z[h]); d_S is read only */
+int emie_cu_contract_modes_peer(emie_cu_operator op, const double* d_S, int nrhs, int q0, int q1,
+                                double* const* h_dst, const int* h_z, int G, void* stream);
 /* after this stream's moves into the G ranks' buffers: release-store epoch
  * into slot `me` of each rank's flag array (h_flag_ptrs: G device pointers,
  * peers' flag arrays mapped into this process) */

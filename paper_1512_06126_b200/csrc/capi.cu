@@ -756,6 +756,25 @@ int emie_cu_contract_modes(emie_cu_operator h, double* d_S, int nrhs, int q0, in
   });
 }
 
+int emie_cu_contract_modes_peer(emie_cu_operator h, const double* d_S, int nrhs, int q0, int q1,
+                                double* const* h_dst, const int* h_z, int G, void* stream) {
+  return guarded([&] {
+    if (!h || !d_S || !h_dst || !h_z) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: nrhs < 1");
+    if (G < 1 || G > kMaxPeerRanks) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: bad rank count");
+    PeerOut po;
+    po.G = G;
+    for (int g = 0; g < G; ++g) {
+      if (!h_dst[g]) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: null destination");
+      po.dst[g] = reinterpret_cast<cplx*>(h_dst[g]);
+    }
+    for (int g = 0; g <= G; ++g) po.z[g] = h_z[g];
+    for (int g = 0; g < G; ++g)
+      if (!(po.z[g] < po.z[g + 1])) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: empty depth slab");
+    contract_modes_peer(h->op, reinterpret_cast<const cplx*>(d_S), nrhs, q0, q1, po, as_stream(stream));
+  });
+}
+
 int emie_cu_move_planes(const double* d_src, double* d_dst, int nrhs, int nidx, const int* d_idx,
                         long long modes_total, const int src_desc[4], const int dst_desc[4], int nzh,
                         void* stream) {

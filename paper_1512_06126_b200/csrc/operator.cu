@@ -308,11 +308,13 @@ constexpr int ct_blk_stages() { return OCT ? kBlkStagesOct : kBlkStages; }
 // exchanged and stored back exchanged: M(qmx, qmy) = P M(qmy, qmx) P with P
 // the x <-> y permutation, so one block read serves both modes and the MMA's
 // A fragment feeds two n8 products.
-template <int NZ, bool OCT>
+// PEER (sharded apply, quadrant modes only): the results go to the slab
+// owners' spectra through po (peer memory over NVLink) instead of back into S
+template <int NZ, bool OCT, bool PEER = false>
 __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
                         int ex, int ey, int qx, int q0, int q1, int qbase, int nrhs, int nentD,
-                        const int* __restrict__ octl, int noct) {
+                        const int* __restrict__ octl, int noct, const __grid_constant__ PeerOut po) {
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int nk = np / 4;
   constexpr int W = mma_warps<NZ>();
@@ -403,6 +405,15 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   const int fr = lane >> 2, fc = lane & 3;
   const int a_rt = warp / (NZ / 8), m = warp - a_rt * (NZ / 8);
   const int k = 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
+  // PEER: the slab owner of this lane's output row k
+  cplx* pdst = nullptr;
+  int pnz = 0;
+  if constexpr (PEER) {
+    int h = 0;
+    while (h + 1 < po.G && k >= po.z[h + 1]) ++h;
+    pnz = po.z[h + 1] - po.z[h];
+    pdst = po.dst[h] + (k - po.z[h]) + a_rt * pnz;
+  }
   // The warp's component a is a template constant inside consume(): the
   // zx / zy negation (-xz^T, -yz^T: the z tile, b < 2) is then a compile-time
   // operand sign that the DMMA applies for free.
@@ -479,8 +490,13 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         for (int h = 0; h < 2; ++h) {
           const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
           if (cb >= 0) {
-            const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? plane_sw : plane);
-            S[o] = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
+            const cplx v = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
+            if constexpr (PEER) {
+              pdst[(cb / (3 * NZ)) * (3 * pnz)] = v;  // cb = (r E + mode) * np
+            } else {
+              const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? plane_sw : plane);
+              S[o] = v;
+            }
           }
         }
       }
@@ -834,7 +850,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
         kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
-                                                   g, op.nentD, op.octl, op.noct);
+                                                   g, op.nentD, op.octl, op.noct, PeerOut{});
       };
       if (oct) {
         if (op.nz == 8) launch(contract_mma_kernel<8, true>, mma_warps<8>());
@@ -872,6 +888,39 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
                                                        q0, q1, op.qbase, g, pair, octv, noctv);
     }
     check_launch("contract_kernel");
+  }
+}
+
+void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, int q1, const PeerOut& po,
+                         cudaStream_t st) {
+  if (!op.mma) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: needs the MMA layout (nz in {8, 16, 32})");
+  if (q0 < op.qbase || q1 > op.qbase + op.qcount || q0 > q1)
+    fail(EMIE_CU_OUT_OF_RANGE, "contraction: quadrant modes outside the stored range");
+  if (po.G < 1 || po.G > kMaxPeerRanks || po.z[0] != 0 || po.z[po.G] != op.nz)
+    fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: bad depth slabs");
+  if (q0 == q1) return;
+  const int np = 3 * op.nz;
+  const int sms = sm_count();
+  for (int r0 = 0; r0 < nrhs; r0 += 2) {
+    const int g = std::min(2, nrhs - r0);
+    const cplx* Sg = S + static_cast<size_t>(r0) * op.lateral() * np;
+    PeerOut pg = po;  // the group's rhs offset: mode index r*E + m counts from r0
+    for (int h = 0; h < po.G; ++h)
+      pg.dst[h] = po.dst[h] + static_cast<size_t>(r0) * op.lateral() * 3 * (po.z[h + 1] - po.z[h]);
+    const int nc = ct_cols<false>();
+    const size_t smem = 128 + kUStages * nc * sizeof(long long) +
+                        ct_blk_stages<false>() * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                        kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+    auto launch = [&](auto kern, int warps) {
+      const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
+      const int grid = std::max(1, std::min(sms * per_sm, q1 - q0));
+      kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0,
+                                                 q1, op.qbase, g, op.nentD, nullptr, 0, pg);
+    };
+    if (op.nz == 8) launch(contract_mma_kernel<8, false, true>, mma_warps<8>());
+    else if (op.nz == 16) launch(contract_mma_kernel<16, false, true>, mma_warps<16>());
+    else launch(contract_mma_kernel<32, false, true>, mma_warps<32>());
+    check_launch("contract_mma_kernel (peer epilogue)");
   }
 }
 

@@ -106,6 +106,17 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int s
 void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs,
              const System* sys, cudaStream_t st);
 void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaStream_t st);
+// the sharded apply's contraction with its results stored straight into the
+// slab owners' spectra (peer memory): plane a*nz + k goes to rank h with
+// z[h] <= k < z[h+1], at dst[h][(r*E + m)*3nzh + a*nzh + k - z[h]]
+constexpr int kMaxPeerRanks = 64;
+struct PeerOut {
+  int G = 0;
+  cplx* dst[kMaxPeerRanks];
+  int z[kMaxPeerRanks + 1];
+};
+void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, int q1, const PeerOut& po,
+                         cudaStream_t st);
 
 // sharded apply column moves (shard.cu); desc = {mapped, planes per column, component stride, depth offset}
 void move_planes(const cplx* src, cplx* dst, int nrhs, int nidx, const int* idx, long long modes_total,

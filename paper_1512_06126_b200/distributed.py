@@ -227,9 +227,10 @@ class PeerExchange:
     mappings of the others' (PeerExchange.open_ipc) or, for G virtual ranks
     in one process, the other shards' own buffers (loopback)."""
 
-    def __init__(self, shard: "ShardedApply", peers, own):
+    def __init__(self, shard: "ShardedApply", peers, own, fused: bool = True):
         self.sh, self.peers, self.own = shard, peers, own
         self.epoch = 0
+        self.fused = fused  # contraction + return transpose in one kernel where the backend has it
         # flag arrays: device addresses (None: a host backend, no device flags)
         self._flag_ptrs = (None if own[2] is None else
                            (ctypes.c_void_p * shard.plan.G)(*[p[2] for p in peers]))
@@ -317,6 +318,10 @@ class PeerExchange:
     def push_contracted(self):
         sh, P, be = self.sh, self.sh.plan, self.sh.be
         S_full = self.own[1]
+        if getattr(be, "fused_peer_contract", False) and self.fused:
+            # one kernel: the contraction's epilogue stores into the owners' S_loc
+            be.contract_peer(S_full, sh.nrhs, sh.q0, sh.q1, [self.peers[h][0] for h in range(P.G)], P.z)
+            return
         be.contract(S_full, sh.nrhs, sh.q0, sh.q1)
         for h in range(P.G):  # my modes' columns of h's planes -> h's slab spectrum
             nzh = P.nzl(h)
@@ -339,12 +344,12 @@ class PeerExchange:
         return self.finish()
 
 
-def peer_loopback(shards: Sequence["ShardedApply"], host: bool = False):
+def peer_loopback(shards: Sequence["ShardedApply"], host: bool = False, fused: bool = True):
     """G virtual ranks in one process (one GPU, or host tensors with the
     NumPy backend): every rank's exchange buffers allocated here, the 'peer'
     buffers are the other shards' own."""
     owns = [PeerExchange.allocate_host(sh) if host else PeerExchange.allocate(sh) for sh in shards]
-    return [PeerExchange(sh, owns, owns[g]) for g, sh in enumerate(shards)], owns
+    return [PeerExchange(sh, owns, owns[g], fused) for g, sh in enumerate(shards)], owns
 
 
 def peer_loopback_apply(xs: Sequence[PeerExchange], slabs):
@@ -437,6 +442,17 @@ class CudaBackend:
     def contract(self, S, nrhs, q0, q1):
         self._check(self.L.emie_cu_contract_modes(self.op.handle, ctypes.c_void_p(S.data_ptr()), nrhs, q0, q1,
                                                   self._st()))
+
+    @property
+    def fused_peer_contract(self) -> bool:
+        return self.plan.nz in (8, 16, 32)  # the MMA-layout contraction has the peer epilogue
+
+    def contract_peer(self, S, nrhs, q0, q1, dsts, z):
+        G = len(dsts)
+        dp = (ctypes.c_void_p * G)(*[d.data_ptr() for d in dsts])
+        zz = (ctypes.c_int * (G + 1))(*z)
+        self._check(self.L.emie_cu_contract_modes_peer(self.op.handle, ctypes.c_void_p(S.data_ptr()), nrhs, q0, q1,
+                                                       dp, zz, G, self._st()))
 
     def lateral_inverse(self, S, U, nrhs):
         out = self.torch.empty_like(U)

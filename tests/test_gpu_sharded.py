@@ -51,20 +51,22 @@ def test_sharded_apply_loopback_bit_identical(torch_cuda, cfg_id, G):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("cfg_id,G", [(1, 1), (1, 2), (1, 3), (1, 8), (2, 4)])
-def test_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G):
+def test_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G, fused):
     """the transposes as peer stores (distributed.PeerExchange, csrc/peer.cu:
     IPC-shareable exchange buffers, move_planes straight into the owner's
     buffer, release/acquire flag barriers) over G virtual ranks on one GPU,
-    two applies back to back (buffer and epoch reuse): bit-identical to the
-    single-GPU apply"""
+    two applies back to back (buffer and epoch reuse), with the return
+    transpose fused into the contraction's epilogue or as move kernels:
+    bit-identical to the single-GPU apply"""
     torch = torch_cuda
     cfg, grid, sop, sysop = _system(cfg_id)
     nrhs = 2
     plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G)
     emie.xy_symmetric(sop, disable=True)
     shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
-    xs, owns = D.peer_loopback(shards)
+    xs, owns = D.peer_loopback(shards, fused=fused)
     try:
         for rep in range(2):
             rng = np.random.default_rng(70 + G + rep)
