@@ -301,6 +301,15 @@ int emie_cu_peer_free(void* d_ptr);
 int emie_cu_ipc_handle(const void* d_ptr, void* h_handle);
 int emie_cu_ipc_open(const void* h_handle, void** d_ptr);
 int emie_cu_ipc_close(void* d_ptr);
+/* emie_cu_lateral_forward of a depth slab (geometry nz = the slab's) fused
+ * with the forward transpose: mode m's spectrum column goes straight into
+ * the full-depth spectrum of rank d_owner[m] (device table over the ex*ey
+ * modes), at h_dst[owner][(r*E + m)*3nz_full + c*nz_full + z_offset + z];
+ * 256/512-point embeddings (emie_cu_lateral_forward_peer_supported) */
+int emie_cu_lateral_forward_peer(emie_cu_operator geom, const double* d_in, const double* d_r2,
+                                 const int* d_owner, double* const* h_dst, int G, int nz_full, int z_offset,
+                                 int nrhs, void* stream);
+int emie_cu_lateral_forward_peer_supported(emie_cu_operator geom, int* out);
 /* emie_cu_contract_modes with the results stored straight into the slab
  * owners' spectra (fused contraction + return transpose; MMA layout, nz in
  * {8, 16, 32}): the contracted plane a*nz + k of mode m goes to rank h with

@@ -147,6 +147,9 @@ def lib():
         "emie_cu_ipc_close": [vp],
         "emie_cu_peer_signal": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_peer_wait": [vp, ctypes.c_int, ctypes.c_int, vp],
+        "emie_cu_lateral_forward_peer": [vp, vp, vp, vp, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, vp],
+        "emie_cu_lateral_forward_peer_supported": [vp, ip],
         "emie_cu_contract_modes_peer": [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ip,
                                         ctypes.c_int, vp],
     }

@@ -732,6 +732,35 @@ int emie_cu_lateral_forward(emie_cu_operator geom, const double* d_in, const dou
   });
 }
 
+int emie_cu_lateral_forward_peer(emie_cu_operator geom, const double* d_in, const double* d_r2,
+                                 const int* d_owner, double* const* h_dst, int G, int nz_full, int z_offset,
+                                 int nrhs, void* stream) {
+  return guarded([&] {
+    if (!geom || !d_in || !d_owner || !h_dst) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: nrhs < 1");
+    const Operator& op = geom->op;
+    if (z_offset < 0 || z_offset + op.nz > nz_full)
+      fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: slab outside the full depth");
+    std::vector<cplx*> dst(G);
+    for (int g = 0; g < G; ++g) {
+      if (!h_dst[g]) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: null destination");
+      dst[g] = reinterpret_cast<cplx*>(h_dst[g]);
+    }
+    const cudaStream_t st = as_stream(stream);
+    cplx* T = scratch<cplx>(static_cast<std::size_t>(nrhs) * 3 * op.nz * op.ny * op.ex, st);
+    lateral_forward_peer(op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<const cplx*>(d_r2), T, d_owner,
+                         dst.data(), G, nz_full, z_offset, nrhs, st);
+    release(T, st);
+  });
+}
+
+int emie_cu_lateral_forward_peer_supported(emie_cu_operator geom, int* out) {
+  return guarded([&] {
+    if (!geom || !out) fail(EMIE_CU_INVALID_ARGUMENT, "null pointer");
+    *out = lateral_forward_peer_ok(geom->op) ? 1 : 0;
+  });
+}
+
 int emie_cu_lateral_inverse(emie_cu_operator geom, const double* d_S, const double* d_u, double* d_out,
                             const double* d_s, const double* d_r1, int nrhs, void* stream) {
   return guarded([&] {

@@ -734,6 +734,37 @@ struct FyStream {
   }
 };
 
+// y forward of a depth slab in the sharded apply, fused with the forward
+// transpose: the spectrum column of mode m is stored straight into the
+// full-depth spectrum of m's owner rank (peer memory over NVLink) at depth
+// offset zoff, S_g[r][m][c*nzf + zoff + z], instead of the slab's own S
+constexpr int kMaxFyPeers = 64;
+struct FyPeerStream : FyStream {
+  cplx* pdst[kMaxFyPeers];  // owner rank -> its full-depth spectrum
+  const int* owner;         // mode (mx*ey + my) -> owner rank
+  int nzf, zoff;            // full depth, this slab's first interval
+  struct Ops {
+    int r, mx, p0;
+    bool mxflip;
+  };
+  template <int N>
+  __device__ void prefetch(int tile, Ops& o) const {
+    coords<N>(tile, o.r, o.mx, o.p0);
+    o.mxflip = 2 * o.mx > ex;
+  }
+  __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
+  template <int N>
+  __device__ void emit(const Ops& o, int t, int my, int, int, cplx v) const {
+    const int plane = o.p0 + t;
+    if (plane >= np) return;
+    const bool flip = (plane < nz && o.mxflip) || (plane >= nz && plane < 2 * nz && 2 * my > N);
+    const int m = o.mx * N + my;
+    const int c = plane / nz, z = plane - c * nz;
+    cplx* d = pdst[__ldg(owner + m)] + (static_cast<size_t>(o.r) * ex * N + m) * 3 * nzf + c * nzf + zoff + z;
+    gst(d, flip ? -v : v);
+  }
+};
+
 // byte offset of 16-byte chunk t of staged row jj: N = 256 rows of 128 B with
 // the 128-byte swizzle (chunk ^ row mod 8), N = 512 rows of 64 B with the
 // 64-byte swizzle (chunk ^ (row / 2) mod 4)
@@ -1084,6 +1115,35 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     check_launch("apply_fy_kernel");
   }
   profile_mark(1, false, st);
+}
+
+bool lateral_forward_peer_ok(const Operator& op) {
+  return stream_ok(op.p2x, op.ex, op.nx) && stream_ok(op.p2y, op.ey, op.ny) && (op.ey == 256 || op.ey == 512) &&
+         (op.ex == 256 || op.ex == 512);
+}
+
+void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, cplx* T, const int* owner,
+                          cplx* const* dsts, int G, int nzf, int zoff, int nrhs, cudaStream_t st) {
+  if (!lateral_forward_peer_ok(op)) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: needs 256/512-point TMA passes");
+  if (G < 1 || G > kMaxFyPeers) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: bad rank count");
+  const int np = 3 * op.nz;
+  {  // x pass into the local T (TMA path, as lateral_forward)
+    FxStream p{};
+    p.u = d_in; p.r2 = r2; p.T = T;
+    p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
+    p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
+    p.r2_staged = true;
+    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    else launch_tma<512, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+  }
+  FyPeerStream p{};
+  p.T = T; p.S = nullptr;
+  p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
+  p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ny;
+  for (int g = 0; g < G; ++g) p.pdst[g] = dsts[g];
+  p.owner = owner; p.nzf = nzf; p.zoff = zoff;
+  if (op.ey == 256) launch_tma<256, FyPeerStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy_peer");
+  else launch_tma<512, FyPeerStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy_peer");
 }
 
 void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_in, cplx* d_out,

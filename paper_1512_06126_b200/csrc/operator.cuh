@@ -98,6 +98,11 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
                      int nrhs, cudaStream_t st);
 void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_in, cplx* d_out,
                      const cplx* s, const double* r1, int nrhs, cudaStream_t st);
+// the sharded apply's slab forward with the forward transpose fused into the
+// y pass (stores into the owners' full-depth spectra, owner[mode] -> rank)
+bool lateral_forward_peer_ok(const Operator& op);
+void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, cplx* T, const int* owner,
+                          cplx* const* dsts, int G, int nzf, int zoff, int nrhs, cudaStream_t st);
 
 // stages (operator.cu)
 // sym_known: 1 the blocks are x <-> y symmetric by construction, 0 they are

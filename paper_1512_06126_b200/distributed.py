@@ -310,6 +310,10 @@ class PeerExchange:
         sh, P, be = self.sh, self.sh.plan, self.sh.be
         self._U = U
         S_loc = self.own[0]
+        if getattr(be, "fused_peer_forward", False) and self.fused:
+            # one pass: the slab's y transform stores each mode's column into its owner's S_full
+            be.lateral_forward_peer(U, [self.peers[g][1] for g in range(P.G)], sh.nrhs)
+            return
         be.lateral_forward_into(U, S_loc, sh.nrhs)
         for g in range(P.G):  # my slab's columns of g's modes -> g's full-depth spectrum
             be.move(S_loc, self.peers[g][1], sh.nrhs, g, P.E, sh._slab_desc(True),
@@ -442,6 +446,28 @@ class CudaBackend:
     def contract(self, S, nrhs, q0, q1):
         self._check(self.L.emie_cu_contract_modes(self.op.handle, ctypes.c_void_p(S.data_ptr()), nrhs, q0, q1,
                                                   self._st()))
+
+    @property
+    def fused_peer_forward(self) -> bool:
+        if not hasattr(self, "_fpf"):
+            v = ctypes.c_int(0)
+            self._check(self.L.emie_cu_lateral_forward_peer_supported(self.geom, ctypes.byref(v)))
+            self._fpf = bool(v.value)
+            if self._fpf:  # mode -> owner rank
+                own = np.empty(self.plan.E, np.int32)
+                for g, ms in enumerate(self.plan.modes):
+                    own[ms] = g
+                self.owner = self.torch.from_numpy(own).to(self.dev)
+        return self._fpf
+
+    def lateral_forward_peer(self, U, dsts, nrhs):
+        P = self.plan
+        G = len(dsts)
+        dp = (ctypes.c_void_p * G)(*[d.data_ptr() for d in dsts])
+        self._check(self.L.emie_cu_lateral_forward_peer(self.geom, ctypes.c_void_p(U.data_ptr()),
+                                                        ctypes.c_void_p(self.r2.data_ptr()),
+                                                        ctypes.c_void_p(self.owner.data_ptr()), dp, G, P.nz,
+                                                        P.z[self.rank], nrhs, self._st()))
 
     @property
     def fused_peer_contract(self) -> bool:

@@ -52,14 +52,15 @@ def test_sharded_apply_loopback_bit_identical(torch_cuda, cfg_id, G):
 
 
 @pytest.mark.parametrize("fused", [True, False])
-@pytest.mark.parametrize("cfg_id,G", [(1, 1), (1, 2), (1, 3), (1, 8), (2, 4)])
+@pytest.mark.parametrize("cfg_id,G", [(1, 1), (1, 2), (1, 3), (1, 8), (2, 4), (3, 2), (3, 8)])
 def test_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G, fused):
     """the transposes as peer stores (distributed.PeerExchange, csrc/peer.cu:
     IPC-shareable exchange buffers, move_planes straight into the owner's
     buffer, release/acquire flag barriers) over G virtual ranks on one GPU,
     two applies back to back (buffer and epoch reuse), with the return
-    transpose fused into the contraction's epilogue or as move kernels:
-    bit-identical to the single-GPU apply"""
+    transpose fused into the contraction's epilogue and (256-point
+    embeddings: config 3) the forward one into the y pass, or both as move
+    kernels: bit-identical to the single-GPU apply"""
     torch = torch_cuda
     cfg, grid, sop, sysop = _system(cfg_id)
     nrhs = 2
