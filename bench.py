@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-solve", action="store_true", help="skip the FGMRES solve timing")
     p.add_argument("--strong", action="store_true",
                    help="strong scaling of one grid: depth-slab / mode-shard apply over the N ranks")
