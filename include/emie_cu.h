@@ -311,8 +311,8 @@ int emie_cu_lateral_forward_peer(emie_cu_operator geom, const double* d_in, cons
                                  int nrhs, void* stream);
 int emie_cu_lateral_forward_peer_supported(emie_cu_operator geom, int* out);
 /* emie_cu_contract_modes with the results stored straight into the slab
- * owners' spectra (fused contraction + return transpose; MMA layout, nz in
- * {8, 16, 32}): the contracted plane a*nz + k of mode m goes to rank h with
+ * owners' spectra (fused contraction + return transpose; DMMA layouts, nz in
+ * {8, 16, 32, 48, 64}): the contracted plane a*nz + k of mode m goes to rank h with
  * h_z[h] <= k < h_z[h+1], at h_dst[h][(r*E + m)*3nzh + a*nzh + k - h_z[h]]
  * (nzh = h_z[h+1] - h_z[h]); d_S is read only */
 int emie_cu_contract_modes_peer(emie_cu_operator op, const double* d_S, int nrhs, int q0, int q1,

@@ -540,10 +540,11 @@ __host__ __device__ constexpr int rows_block_id(int a, int b) {
   return a == b ? a : (a < 2 && b < 2) ? 3 : b == 2 ? 4 + a : 6 + b;
 }
 
-template <int NZ, bool OCT>
+template <int NZ, bool OCT, bool PEER = false>
 __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
     contract_rows_kernel(const __grid_constant__ CUtensorMap tm, cplx* S, int ex, int ey, int qx, int q0, int q1,
-                         int qbase, int nrhs, const int* __restrict__ octl, int noct) {
+                         int qbase, int nrhs, const int* __restrict__ octl, int noct,
+                         const __grid_constant__ PeerOut po) {
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int W = rows_warps<NZ>();
   constexpr int NC = ct_cols<OCT>();
@@ -687,14 +688,27 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
       const int rowc = trow[i];  // C row fr of the tile = the lane's A row
       const int plane = a * NZ + rowc;
       const int asw = a == 2 ? 2 : 1 - a;
+      cplx* pdst = nullptr;  // PEER: the slab owner of output row rowc
+      int pnz = 0;
+      if constexpr (PEER) {
+        int hh = 0;
+        while (hh + 1 < po.G && rowc >= po.z[hh + 1]) ++hh;
+        pnz = po.z[hh + 1] - po.z[hh];
+        pdst = po.dst[hh] + (rowc - po.z[hh]) + a * pnz;
+      }
 #pragma unroll
       for (int g = 0; g < NG; ++g)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
           if (cb >= 0) {
-            const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? asw * NZ + rowc : plane);
-            S[o] = cplx{p1[i][g][h] - p2[i][g][h], p3[i][g][h] - p1[i][g][h] - p2[i][g][h]};
+            const cplx v = cplx{p1[i][g][h] - p2[i][g][h], p3[i][g][h] - p1[i][g][h] - p2[i][g][h]};
+            if constexpr (PEER) {
+              pdst[(cb / np) * (3 * pnz)] = v;  // cb = (r E + mode) * np
+            } else {
+              const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? asw * NZ + rowc : plane);
+              S[o] = v;
+            }
           }
         }
     }
@@ -826,7 +840,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
         kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
-                                                   op.noct);
+                                                   op.noct, PeerOut{});
       };
       if (op.nz == 48) {
         if (oct) launch(contract_rows_kernel<48, true>, rows_warps<48>());
@@ -893,7 +907,8 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
 
 void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, int q1, const PeerOut& po,
                          cudaStream_t st) {
-  if (!op.mma) fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: needs the MMA layout (nz in {8, 16, 32})");
+  if (!op.mma && !op.rows)
+    fail(EMIE_CU_INVALID_ARGUMENT, "contract_modes_peer: needs the MMA or row-block layout (nz in {8, 16, 32, 48, 64})");
   if (q0 < op.qbase || q1 > op.qbase + op.qcount || q0 > q1)
     fail(EMIE_CU_OUT_OF_RANGE, "contraction: quadrant modes outside the stored range");
   if (po.G < 1 || po.G > kMaxPeerRanks || po.z[0] != 0 || po.z[po.G] != op.nz)
@@ -908,6 +923,26 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
     for (int h = 0; h < po.G; ++h)
       pg.dst[h] = po.dst[h] + static_cast<size_t>(r0) * op.lateral() * 3 * (po.z[h + 1] - po.z[h]);
     const int nc = ct_cols<false>();
+    if (op.rows) {
+      const size_t smem = 1024 + static_cast<size_t>(kRowsRing) * 3 * op.nz * 128 +
+                          kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+      CUtensorMap tm;
+      const uint64_t dims[4] = {2ull * op.nz, static_cast<uint64_t>(op.nz), 8ull, static_cast<uint64_t>(op.qcount)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(op.nz) * 16, static_cast<uint64_t>(op.nz) * op.nz * 16,
+                                   8ull * op.nz * op.nz * 16};
+      const uint32_t box[4] = {16, static_cast<uint32_t>(op.nz), 1, 1};
+      encode_tensor_map_f64(&tm, op.spec, 4, dims, strides, box);
+      auto launch_rows = [&](auto kern, int warps) {
+        const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
+        const int grid = std::max(1, std::min(sms * per_sm, q1 - q0));
+        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1, op.qbase,
+                                                   g, nullptr, 0, pg);
+      };
+      if (op.nz == 48) launch_rows(contract_rows_kernel<48, false, true>, rows_warps<48>());
+      else launch_rows(contract_rows_kernel<64, false, true>, rows_warps<64>());
+      check_launch("contract_rows_kernel (peer epilogue)");
+      continue;
+    }
     const size_t smem = 128 + kUStages * nc * sizeof(long long) +
                         ct_blk_stages<false>() * static_cast<size_t>(op.nentD) * sizeof(cplx) +
                         kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);

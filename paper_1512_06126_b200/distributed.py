@@ -471,7 +471,7 @@ class CudaBackend:
 
     @property
     def fused_peer_contract(self) -> bool:
-        return self.plan.nz in (8, 16, 32)  # the MMA-layout contraction has the peer epilogue
+        return self.plan.nz in (8, 16, 32, 48, 64)  # the DMMA contractions have the peer epilogue
 
     def contract_peer(self, S, nrhs, q0, q1, dsts, z):
         G = len(dsts)

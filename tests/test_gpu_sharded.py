@@ -85,6 +85,39 @@ def test_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G, fused):
             D.PeerExchange.free(o)
 
 
+@pytest.mark.parametrize("nz,G", [(64, 2), (48, 3)])
+def test_peer_exchange_deep_grid_bit_identical(torch_cuda, nz, G):
+    """nz 48/64 (config 4's depth): the row-block contraction with the peer
+    epilogue, G virtual ranks, bit-identical to the single-GPU apply"""
+    torch = torch_cuda
+    tops, sigma = [0.0, 500.0, 2500.0], [0.0, 1e-3, 10 ** -1.5, 1.0]
+    breaks = list(np.linspace(600.0, 600.0 + 50.0 * nz, nz + 1))
+    model = emie.LayeredModel(tops, sigma)
+    nx = ny = 8
+    grid = emie.make_grid(model, breaks, nx, ny, 100.0, 100.0)
+    rng = np.random.default_rng(nz)
+    grid.sigma_a[...] = 10.0 ** rng.uniform(-3, 0, (nz, ny, nx))
+    sop = emie.assemble_operator(grid, model, 2 * np.pi * 0.5)
+    emie.xy_symmetric(sop, disable=True)
+    sysop = emie.build_system(grid, sop)
+    nrhs = 2
+    plan = D.ShardPlan(nx, ny, nz, sop.ex, sop.ey, G)
+    n = 3 * nx * ny * nz
+    U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+    want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    assert shards[0].be.fused_peer_contract
+    xs, owns = D.peer_loopback(shards)
+    try:
+        outs = D.peer_loopback_apply(xs, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
+        got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+        assert np.array_equal(got, want)
+    finally:
+        torch.cuda.synchronize()
+        for o in owns:
+            D.PeerExchange.free(o)
+
+
 def test_mode_shard_rejects_foreign_modes(torch_cuda):
     cfg, grid, sop, _ = _system(1)
     shard = emie.restrict_modes(sop, 10, 20)
