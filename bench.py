@@ -205,12 +205,18 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EMIE_BENCH_BACKEND=gloo: a CPU-side process group (a multi-rank dry run of
+    # this script on fewer GPUs; ranks share devices, their work is independent)
+    backend = os.environ.get("EMIE_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     cfg = configs.config(args.config)
     freqs = configs.config(5).freqs
@@ -551,12 +557,18 @@ def run_strong(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EMIE_BENCH_BACKEND=gloo: a CPU-side process group (a multi-rank dry run of
+    # this script on fewer GPUs; ranks share devices, their work is independent)
+    backend = os.environ.get("EMIE_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = configs.config(args.config)
     model = emie.LayeredModel(cfg.tops, cfg.sigma)
     grid = emie.make_grid(model, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy)
