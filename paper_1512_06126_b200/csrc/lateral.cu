@@ -743,25 +743,31 @@ struct FyPeerStream : FyStream {
   cplx* pdst[kMaxFyPeers];  // owner rank -> its full-depth spectrum
   const int* owner;         // mode (mx*ey + my) -> owner rank
   int nzf, zoff;            // full depth, this slab's first interval
+  // the last pass gives each thread one plane of the tile (t = tid mod 8,
+  // transform index fastest), so its depth offset and sign class are per tile
   struct Ops {
-    int r, mx, p0;
-    bool mxflip;
+    long long rE;  // r * ex * ey
+    int mx, poff;  // poff: c * nzf + zoff + z of the thread's plane, -1 past the slab
+    bool xflip, ycls;
   };
   template <int N>
   __device__ void prefetch(int tile, Ops& o) const {
-    coords<N>(tile, o.r, o.mx, o.p0);
-    o.mxflip = 2 * o.mx > ex;
+    int r, p0;
+    coords<N>(tile, r, o.mx, p0);
+    o.rE = static_cast<long long>(r) * ex * N;
+    const int plane = p0 + static_cast<int>(threadIdx.x) % Geo<N>::ntr;
+    const int c = plane / nz, z = plane - c * nz;
+    o.poff = plane < np ? c * nzf + zoff + z : -1;
+    o.xflip = c == 0 && 2 * o.mx > ex;
+    o.ycls = c == 1;
   }
   __device__ cplx pre(const Ops&, int, int, int, cplx x) const { return x; }
   template <int N>
-  __device__ void emit(const Ops& o, int t, int my, int, int, cplx v) const {
-    const int plane = o.p0 + t;
-    if (plane >= np) return;
-    const bool flip = (plane < nz && o.mxflip) || (plane >= nz && plane < 2 * nz && 2 * my > N);
+  __device__ void emit(const Ops& o, int, int my, int, int, cplx v) const {
+    if (o.poff < 0) return;
+    const bool flip = o.xflip || (o.ycls && 2 * my > N);
     const int m = o.mx * N + my;
-    const int c = plane / nz, z = plane - c * nz;
-    cplx* d = pdst[__ldg(owner + m)] + (static_cast<size_t>(o.r) * ex * N + m) * 3 * nzf + c * nzf + zoff + z;
-    gst(d, flip ? -v : v);
+    gst(pdst[__ldg(owner + m)] + (o.rE + m) * 3 * nzf + o.poff, flip ? -v : v);
   }
 };
 
