@@ -6,10 +6,13 @@
 //
 // The lateral FFT stages live in lateral.cu. Apply data flow for nrhs fields (all complex128):
 //   u [r][plane][iy][ix]            plane = c*nz + iz (GridVector layout)
-//   K_fx : r2-scale, zero-pad, x-FFT        -> T [r][plane][iy][mx]
+//   K_fx : r2-scale, zero-pad, x-FFT        -> T [r][mx][plane][iy]
 //   K_fy : zero-pad, y-FFT, transpose       -> S [r][mx][my][plane]  (mode-major)
-//   K_ct : per quadrant mode, 3nz x 3nz block times 4 mirror modes x nrhs
-//                                            -> S (in place)
+//   K_ct : per quadrant (or octant) mode, 3nz x 3nz block times its mirror
+//          modes x nrhs (and the transposed mode's) -> S (in place):
+//          contract_mma_kernel (nz 8/16/32: whole block by TMA, DMMA),
+//          contract_rows_kernel (nz 48/64: row blocks streamed as K-chunks, DMMA),
+//          contract_kernel (other nz: wrapped diagonals, DFMA)
 //   K_iy : inverse y-FFT, keep iy < ny       -> T
 //   K_ix : inverse x-FFT, keep ix < nx, 1/(ex ey), s*u + r1*(.) epilogue -> out
 // The mode-major spectrum makes every contraction read/write a contiguous
