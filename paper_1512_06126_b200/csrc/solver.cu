@@ -145,11 +145,17 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(cplx* w, const cplx
 //   MODE 0: dots conj(V_l) . w (+ |w|^2)                      (CGS2 pass 1)
 //   MODE 1: w' = w - V h, then conj(V_l) . w'                  (pass-1 update + pass-2 dots)
 //   MODE 2: w'' = w' - V h and |w''|^2                          (pass-2 update + norm)
+// MODE 1 walks the tiles in reverse: its first tiles are those the MODE 0
+// sweep read last, still in L2 (and MODE 2's first those MODE 1 read last).
 // The update keeps update_kernel's arithmetic (sequential in l, same FMAs),
 // so w', w'' are bit-identical to it. Dots: compute warp k owns vectors
 // l = k, k + 8, ..., lanes own elements; per-lane partials live in registers
 // across tiles and are reduced in a fixed order at the end (one CTA per SM,
 // fixed grid: the summation order does not depend on the GPU).
+#ifndef EMIE_CGS_REVERSE
+#define EMIE_CGS_REVERSE 1
+#endif
+constexpr bool kCgsReverse = EMIE_CGS_REVERSE;  // MODE 1 tiles in reverse (A/B switch)
 constexpr int kTE = 128;        // elements per tile
 constexpr int kTileMaxV = 41;   // basis vectors per staged tile (restart <= 40)
 constexpr int kCgsWarps = 8;    // compute warps
@@ -188,7 +194,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
 
   if (warp == kCgsWarps) {  // ---- producer
     int j = 0;
-    for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    for (std::size_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++j) {
+      const std::size_t t = (kCgsReverse && MODE == 1) ? ntiles - 1 - tt : tt;
       const int s = j & 1;
       if (j >= 2) mbar_wait(empty + s, static_cast<uint32_t>(((j >> 1) - 1) & 1));
       const std::size_t e0 = t * kTE;
@@ -208,7 +215,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   for (int i = 0; i < kLPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
   double nacc = 0.0;
   int j = 0;
-  for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+  for (std::size_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++j) {
+    const std::size_t t = (kCgsReverse && MODE == 1) ? ntiles - 1 - tt : tt;  // see the producer
     const int s = j & 1;
     mbar_wait(full + s, static_cast<uint32_t>((j >> 1) & 1));
     const cplx* Vt = stage0 + s * stage_elems;
