@@ -22,9 +22,11 @@
 #include <cstdio>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <vector>
 
 #include "operator.cuh"
+#include "tma.cuh"
 
 namespace emie_cu {
 
@@ -475,16 +477,135 @@ __device__ unsigned long long g_phase_clk[8];
   } while (0)
 #endif
 
+// The lambda-only phases of a chunk (layered.cpp:67-129): 0a layer states,
+// 0b both reflection chains, 0c diag_a, into the chunk plan C, tasks strided
+// over (tid, nth); `sync`: a CTA-cooperative run (barriers between phases).
+// The assemble kernel runs it per chunk, or layer_state_kernel runs it ahead
+// for every chunk of a batch of offsets (one thread per lambda), writing the
+// SMEM image the assemble kernel then loads with one bulk copy.
+__device__ __forceinline__ void chunk_layer_states(const GreenParams& P, const Chunk& C, double R, int t0, int lc,
+                                                   int tid, int nth, bool sync) {
+  const int L = P.L, NL = P.L + 1;
+    // phase 0a: eta, e2l, em1 per (lambda, layer)
+    for (int x = tid; x < lc * NL; x += nth) {
+      const int li = x / NL, m = x - li * NL;
+      const double lam = exp((P.n1 + t0 + li) * P.step + P.shift) / R;
+      const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
+      const cplx eta = csqrt_pos(eta2);
+      C.eta[li * NL + m] = eta;
+      C.ieta[li * NL + m] = crecip(eta);
+      if (m == 0 || m == L) {
+        C.e2l[li * NL + m] = {1.0, 0.0};
+        C.em1[li * NL + m] = {0.0, 0.0};
+      } else {
+        const cplx e = cexpm1((-2.0 * P.thick[m]) * eta);
+        C.e2l[li * NL + m] = cplx{1.0, 0.0} + e;
+        C.em1[li * NL + m] = -e;
+      }
+    }
+    if (sync) __syncthreads();
+    // phase 0b: reflection chains per (lambda, gamma, direction) (layered.cpp:107-122).
+    // Tasks are direction-major so a warp runs one kind of chain (no divergence);
+    // one complex reciprocal per step gives both p = (1+w)/(1-w) and 1+p = 2/(1-w).
+    for (int x = tid; x < lc * 4; x += nth) {
+      const int dir = x / (2 * lc), rem = x - dir * 2 * lc;
+      const int li = rem >> 1, gm = rem & 1;
+      const cplx* e2l = C.e2l + li * NL;
+      const cplx* em1 = C.em1 + li * NL;
+      const cplx* eta = C.eta + li * NL;
+      const cplx* ie = C.ieta + li * NL;
+      const int base = (li * 2 + gm) * NL;
+      // w = -g N / D with g = alpha eta_m / eta_{m+1} (layered.cpp:113-116), so
+      // p = (1 + w) / (1 - w) = (D - g N) / (D + g N) and 1 + p = 2 D / (D + g N):
+      // one complex reciprocal per step
+      if (dir == 0) {
+        cplx* p = C.p + base;
+        cplx* op = C.one_p + base;
+        cplx opm = {1.0, 0.0};
+        p[0] = {0.0, 0.0};
+        op[0] = opm;
+        for (int m = 0; m < L; ++m) {
+          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - opm), D = em1[m] + e2l[m] * opm;
+          const cplx rat = eta[m] * ie[m + 1];
+          const cplx gN = (gm ? P.sig_up[m] * rat : rat) * N;
+          const cplx r = crecip(D + gN);
+          p[m + 1] = (D - gN) * r;
+          opm = 2.0 * (D * r);
+          op[m + 1] = opm;
+        }
+      } else {
+        cplx* q = C.q + base;
+        cplx* oq = C.one_q + base;
+        cplx oqm = {1.0, 0.0};
+        q[L] = {0.0, 0.0};
+        oq[L] = oqm;
+        for (int m = L; m > 0; --m) {
+          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - oqm), D = em1[m] + e2l[m] * oqm;
+          const cplx rat = eta[m] * ie[m - 1];
+          const cplx gN = (gm ? P.sig_dn[m] * rat : rat) * N;
+          const cplx r = crecip(D + gN);
+          q[m - 1] = (D - gN) * r;
+          oqm = 2.0 * (D * r);
+          oq[m - 1] = oqm;
+        }
+      }
+    }
+    if (sync) __syncthreads();
+    // phase 0c: diag_a (layered.cpp:124-126)
+    for (int x = tid; x < lc * 2 * NL; x += nth) {
+      const int li = x / (2 * NL), r = x - li * 2 * NL;
+      const int m = r % NL;
+      const cplx eta = C.eta[li * NL + m], e2l = C.e2l[li * NL + m], em1 = C.em1[li * NL + m];
+      const cplx pq = C.p[li * 2 * NL + r] * C.q[li * 2 * NL + r];
+      C.diag_a[li * 2 * NL + r] = crecip(eta * (em1 + e2l * (cplx{1.0, 0.0} - pq)));
+    }
+}
+
+// chunk_layer_states for every (offset, lambda) of a batch, one thread per
+// lambda, into each chunk's SMEM image LS[b][chunk][14 NL LC] (the head of
+// the assemble kernel's Chunk plan: eta e2l em1 p q one_p one_q diag_a ieta)
+__global__ void __launch_bounds__(128) layer_state_kernel(const GreenParams P, const int* __restrict__ offs, int nb,
+                                                          int nchunk, cplx* __restrict__ LS) {
+  const int NL = P.L + 1, LC = P.LC;
+  const size_t ls_elems = static_cast<size_t>(14) * NL * LC;
+  const long long tot = static_cast<long long>(nb) * nchunk * LC;
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < tot;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int li = static_cast<int>(x % LC);
+    const long long y = x / LC;
+    const int ch = static_cast<int>(y % nchunk), b = static_cast<int>(y / nchunk);
+    const int t = ch * LC + li;
+    if (t >= P.nw) continue;
+    const int off = offs[b];
+    const Geom g = pair_geometry(off / P.nx, off % P.nx, P.hx, P.hy);
+    cplx* img = LS + (static_cast<size_t>(b) * nchunk + ch) * ls_elems;
+    Chunk v;  // the one-lambda view of slot li
+    v.eta = img + li * NL;
+    v.e2l = img + LC * NL + li * NL;
+    v.em1 = img + 2 * LC * NL + li * NL;
+    v.p = img + 3 * LC * NL + li * 2 * NL;
+    v.q = img + 5 * LC * NL + li * 2 * NL;
+    v.one_p = img + 7 * LC * NL + li * 2 * NL;
+    v.one_q = img + 9 * LC * NL + li * 2 * NL;
+    v.diag_a = img + 11 * LC * NL + li * 2 * NL;
+    v.ieta = img + 13 * LC * NL + li * NL;
+    chunk_layer_states(P, v, g.r, t, 1, 0, 1, false);
+  }
+}
+
 #ifndef EMIE_GREEN_MINB
 #define EMIE_GREEN_MINB 1  // CTAs per SM the register budget targets
 #endif
 #ifndef EMIE_GREEN_SMEM_KB
 #define EMIE_GREEN_SMEM_KB 200  // SMEM budget of the lambda chunk buffers
 #endif
+// LSPRE: the layer states of every chunk come precomputed (layer_state_kernel)
+template <bool LSPRE>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
-    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs) {
+    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, const cplx* __restrict__ LS, int nchunk) {
   extern __shared__ cplx sm[];
+  __shared__ uint64_t lsbar;
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
   const int off = offs[blockIdx.x];
   const int oi = off / P.nx, oj = off % P.nx;
@@ -511,6 +632,15 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   }
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
   auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 2 + f) * nz + j]; };
+  // layer-state image of a chunk (eta .. ieta, the head of the SMEM plan)
+  const size_t ls_elems = static_cast<size_t>(14) * NL * LC;
+  const uint32_t ls_bytes = static_cast<uint32_t>(ls_elems * sizeof(cplx));
+  if (LSPRE && threadIdx.x == 0) {
+    mbar_init(&lsbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&lsbar, ls_bytes);
+    bulk_g2s(sm, LS + static_cast<size_t>(blockIdx.x) * nchunk * ls_elems, ls_bytes, &lsbar);
+  }
 
   // Pair assignment (balanced): group pairs [g0, g0 + cnt), cnt <= 3T. Slots
   // 0, 1: pair g0 + i T + tid over the full lambda range. The ntail = cnt - 2T
@@ -565,80 +695,12 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       C.lam[4 * LC + li] = Woff[4 * nw + t] * lam;
       C.lam[5 * LC + li] = Woff[5 * nw + t] * lam;
     }
-    // phase 0a: eta, e2l, em1 per (lambda, layer)
-    for (int x = threadIdx.x; x < lc * NL; x += blockDim.x) {
-      const int li = x / NL, m = x - li * NL;
-      const double lam = exp((P.n1 + t0 + li) * P.step + P.shift) / R;
-      const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
-      const cplx eta = csqrt_pos(eta2);
-      C.eta[li * NL + m] = eta;
-      C.ieta[li * NL + m] = crecip(eta);
-      if (m == 0 || m == L) {
-        C.e2l[li * NL + m] = {1.0, 0.0};
-        C.em1[li * NL + m] = {0.0, 0.0};
-      } else {
-        const cplx e = cexpm1((-2.0 * P.thick[m]) * eta);
-        C.e2l[li * NL + m] = cplx{1.0, 0.0} + e;
-        C.em1[li * NL + m] = -e;
-      }
-    }
-    __syncthreads();
-    PHASE_MARK(1);
-    // phase 0b: reflection chains per (lambda, gamma, direction) (layered.cpp:107-122).
-    // Tasks are direction-major so a warp runs one kind of chain (no divergence);
-    // one complex reciprocal per step gives both p = (1+w)/(1-w) and 1+p = 2/(1-w).
-    for (int x = threadIdx.x; x < lc * 4; x += blockDim.x) {
-      const int dir = x / (2 * lc), rem = x - dir * 2 * lc;
-      const int li = rem >> 1, gm = rem & 1;
-      const cplx* e2l = C.e2l + li * NL;
-      const cplx* em1 = C.em1 + li * NL;
-      const cplx* eta = C.eta + li * NL;
-      const cplx* ie = C.ieta + li * NL;
-      const int base = (li * 2 + gm) * NL;
-      // w = -g N / D with g = alpha eta_m / eta_{m+1} (layered.cpp:113-116), so
-      // p = (1 + w) / (1 - w) = (D - g N) / (D + g N) and 1 + p = 2 D / (D + g N):
-      // one complex reciprocal per step
-      if (dir == 0) {
-        cplx* p = C.p + base;
-        cplx* op = C.one_p + base;
-        cplx opm = {1.0, 0.0};
-        p[0] = {0.0, 0.0};
-        op[0] = opm;
-        for (int m = 0; m < L; ++m) {
-          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - opm), D = em1[m] + e2l[m] * opm;
-          const cplx rat = eta[m] * ie[m + 1];
-          const cplx gN = (gm ? P.sig_up[m] * rat : rat) * N;
-          const cplx r = crecip(D + gN);
-          p[m + 1] = (D - gN) * r;
-          opm = 2.0 * (D * r);
-          op[m + 1] = opm;
-        }
-      } else {
-        cplx* q = C.q + base;
-        cplx* oq = C.one_q + base;
-        cplx oqm = {1.0, 0.0};
-        q[L] = {0.0, 0.0};
-        oq[L] = oqm;
-        for (int m = L; m > 0; --m) {
-          const cplx N = em1[m] + e2l[m] * (cplx{2.0, 0.0} - oqm), D = em1[m] + e2l[m] * oqm;
-          const cplx rat = eta[m] * ie[m - 1];
-          const cplx gN = (gm ? P.sig_dn[m] * rat : rat) * N;
-          const cplx r = crecip(D + gN);
-          q[m - 1] = (D - gN) * r;
-          oqm = 2.0 * (D * r);
-          oq[m - 1] = oqm;
-        }
-      }
-    }
-    __syncthreads();
-    PHASE_MARK(2);
-    // phase 0c: diag_a (layered.cpp:124-126)
-    for (int x = threadIdx.x; x < lc * 2 * NL; x += blockDim.x) {
-      const int li = x / (2 * NL), r = x - li * 2 * NL;
-      const int m = r % NL;
-      const cplx eta = C.eta[li * NL + m], e2l = C.e2l[li * NL + m], em1 = C.em1[li * NL + m];
-      const cplx pq = C.p[li * 2 * NL + r] * C.q[li * 2 * NL + r];
-      C.diag_a[li * 2 * NL + r] = crecip(eta * (em1 + e2l * (cplx{1.0, 0.0} - pq)));
+    if constexpr (LSPRE) {
+      // the chunk's layer states come precomputed (layer_state_kernel): one
+      // bulk copy, issued after the previous chunk's phase 1
+      mbar_wait(&lsbar, static_cast<uint32_t>((t0 / LC) & 1));
+    } else {
+      chunk_layer_states(P, C, R, t0, lc, threadIdx.x, blockDim.x, true);
     }
     __syncthreads();
     PHASE_MARK(3);
@@ -714,6 +776,11 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       }
     }
     __syncthreads();
+    if (LSPRE && threadIdx.x == 0 && t0 + LC < nw) {  // phase 1 was the last reader of the layer states
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&lsbar, ls_bytes);
+      bulk_g2s(sm, LS + (static_cast<size_t>(blockIdx.x) * nchunk + t0 / LC + 1) * ls_elems, ls_bytes, &lsbar);
+    }
     PHASE_MARK(4);
     // phase 1b: prefix products of theta per (lambda, gamma) as
     // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l.
@@ -1236,7 +1303,8 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 11 * NL + kFields * nz)) * sizeof(cplx) +
                       8 * static_cast<size_t>(P.LC) * sizeof(double) +
                       static_cast<size_t>(P.LC) * 2 * nz * sizeof(int);
-  set_smem(reinterpret_cast<const void*>(assemble_kernel), smem);
+  set_smem(reinterpret_cast<const void*>(assemble_kernel<false>), smem);
+  set_smem(reinterpret_cast<const void*>(assemble_kernel<true>), smem);
   const int groups = ceil_div(P.npairs, (kGreenSlots + 1) * kGreenThreads);
   dim3 grid(ncomp, groups);
   profile_mark(5, true, st);
@@ -1246,8 +1314,35 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
     EMIE_CUDA(cudaMemcpyToSymbolAsync(g_phase_clk, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
   }
 #endif
-  assemble_kernel<<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs);
-  check_launch("assemble_kernel");
+  // the lambda-only phases ahead of the assembly (layer_state_kernel, high
+  // occupancy) for batches of offsets
+  // (only when an offset's pairs span several group CTAs, which would each
+  // recompute them: nz > 32; measured slower for one group, config 3)
+  static const int ls_mode = [] {
+    const char* e = std::getenv("EMIE_CU_GREENS_LS");  // 0: inline, 1: precomputed, unset: by group count
+    return e && *e ? std::atoi(e) : -1;
+  }();
+  const bool pre = ls_mode < 0 ? groups > 1 : ls_mode == 1;
+  if (!pre) {
+    assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0);
+    check_launch("assemble_kernel");
+  } else {
+    const int nchunk = ceil_div(P.nw, P.LC);
+    const size_t ls_elems = static_cast<size_t>(14) * NL * P.LC;
+    const int batch = std::min(ncomp, 4096);
+    cplx* LS = scratch<cplx>(static_cast<size_t>(batch) * nchunk * ls_elems, st);
+    for (int b0 = 0; b0 < ncomp; b0 += batch) {
+      const int nb = std::min(batch, ncomp - b0);
+      const long long tot = static_cast<long long>(nb) * nchunk * P.LC;
+      const int lgrid = static_cast<int>(std::min<long long>(ceil_div(tot, 128), 32LL * sm_count()));
+      layer_state_kernel<<<lgrid, 128, 0, st>>>(P, offs + b0, nb, nchunk, LS);
+      check_launch("layer_state_kernel");
+      assemble_kernel<true><<<dim3(nb, groups), kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs + b0, LS,
+                                                                           nchunk);
+      check_launch("assemble_kernel");
+    }
+    release(LS, st);
+  }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {
     unsigned long long h[8];
