@@ -309,7 +309,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
   op.qcount = q1 - q0;
   if (op.qcount > 0) {
     op.spec = dev_alloc<cplx>(static_cast<std::size_t>(op.qcount) * op.nentD);
-    if (op.nentD != op.nent)  // padding slots of the MMA layout are read, never written
+    if (op.mma)  // padding slots of the MMA layout are read, never written (the row-block layout has none)
       EMIE_CUDA(cudaMemset(op.spec, 0, static_cast<std::size_t>(op.qcount) * op.nentD * sizeof(cplx)));
   }
   op.tw_x = upload_twiddles(op.ex);
