@@ -425,8 +425,9 @@ def run_ours(args):
     fp64 = ctypes.c_double(0.0)
     emie._check(L.emie_cu_probe_fp64(ctypes.byref(fp64), sp))
     achieved = bytes_ct / (ct_ms * 1e-3) / 1e9
-    ct_kernel = (("contract_mma_kernel<%d, %d>" % (nz, int(octant))) if nz in (8, 16, 32) else
-                 ("contract_rows_kernel<%d, %d>" % (nz, int(octant))) if nz in (48, 64) else "contract_kernel")
+    # template arguments as ncu names them (the last one: the sharded apply's peer epilogue, off here)
+    ct_kernel = (("contract_mma_kernel<%d, %d, 0>" % (nz, int(octant))) if nz in (8, 16, 32) else
+                 ("contract_rows_kernel<%d, %d, 0>" % (nz, int(octant))) if nz in (48, 64) else "contract_kernel")
     traffic = None  # dram read + write per launch, from the committed ncu --set full capture
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
