@@ -418,7 +418,11 @@ void host_pipelined_apply(const Operator& op, const System* sys, const double* h
                           int nrhs, cudaStream_t st) {
   CopyStreams& cs = copy_streams();
   const std::size_t n1 = 3 * op.cells();
-  const int slots = std::min(nrhs, kHostSlots);
+  static const int slot_cap = [] {
+    const char* e = std::getenv("EMIE_CU_HOST_SLOTS");
+    return e && *e ? std::max(1, std::min(64, std::atoi(e))) : kHostSlots;
+  }();
+  const int slots = std::min(nrhs, slot_cap);
   cplx* din = scratch<cplx>(n1 * slots, st);
   cplx* dout = scratch<cplx>(n1 * slots, st);
   // events: 0 scratch ready; per ring slot s: 1 + 3s uploaded, 2 + 3s applied, 3 + 3s downloaded
@@ -448,7 +452,7 @@ void host_pipelined_apply(const Operator& op, const System* sys, const double* h
                               cudaMemcpyDeviceToHost, cs.down));
     EMIE_CUDA(cudaEventRecord(ev_down(s), cs.down));
   }
-  const cudaEvent_t done = cs.event(1 + 3 * kHostSlots);
+  const cudaEvent_t done = cs.event(1 + 3 * 64);
   EMIE_CUDA(cudaEventRecord(done, cs.down));
   EMIE_CUDA(cudaStreamWaitEvent(st, done, 0));  // buffers go back to the pool after the last copy
   release(din, st);

@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         }
       }
     }
+    if constexpr (LSPRE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // layer-state reads before the refill
     __syncthreads();
     if (LSPRE && threadIdx.x == 0 && t0 + LC < nw) {  // phase 1 was the last reader of the layer states
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(kStreamThreads, P::kStageBytes <= 16384 ? (NST
       butterfly<16>(v, s);
 #pragma unroll
       for (int r = 0; r < 16; ++r) work[G::at(t, 16 * j + r)] = v[r];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reads before its TMA refill
       __syncthreads();  // staging[st] consumed, work filled
     }
     const int next = tile + NST * gridDim.x;

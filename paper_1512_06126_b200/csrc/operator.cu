@@ -485,6 +485,8 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
         for (int g = 0; g < NG; ++g) dmma(p3[g][0], p3[g][1], ms, neg ? -bs[g] : bs[g]);
       }
       // block stage reads are complete (the DMMAs consumed them): release it
+      // (the proxy fence orders these generic reads before the TMA refill)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(bempty + bs);
 #pragma unroll
@@ -503,6 +505,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
           }
         }
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(uempty + us);  // input columns and their table
     };
@@ -682,6 +685,8 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
           }
         }
         __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
+        __syncwarp();
         if (lane == 0) mbar_arrive(rempty + st);
       }
     }
@@ -715,6 +720,8 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
           }
         }
     }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(uempty + us);
   };

@@ -269,6 +269,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       }
     }
     __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
+    __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
     if (MODE == 1) compute_bar();  // xs is rewritten by the next tile
   }
