@@ -78,6 +78,16 @@ int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
                          double omega, const double* filter, int keep_blocks,
                          emie_cu_operator* out, void* stream);
 
+/* assemble_block (include/emie/greens.hpp:129-135, src/greens.cpp:150-221) at
+ * n signed lateral offsets (oi[i], oj[i]), |oi| < ny, |oj| < nx (else
+ * EMIE_CU_OUT_OF_RANGE, greens.cpp:153-154): filter design and lambda
+ * accumulation on the device for exactly these offsets, each evaluated
+ * independently (no mirror). h_blocks: n blocks of 2 nz (2 nz + 1) complex in
+ * GreensBlock order (xx yy zz xy upper triangles, xz yz full). */
+int emie_cu_assemble_blocks(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                            int nx, int ny, double hx, double hy, double omega, const double* filter,
+                            int n, const int* h_oi, const int* h_oj, double* h_blocks);
+
 /* a SpectralOperator given by its six host component arrays (the
  * emie_cu_operator_download_spectra layout): uploaded into the device
  * wrapped-diagonal layout, no transform */
@@ -115,6 +125,16 @@ int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy,
  * design samples it */
 int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int beta,
                           const double* h_s, int n, double* h_out);
+
+/* v_functions (include/emie/layered.hpp:108-114, src/layered.cpp:397-408)
+ * of every interval pair at n given lambdas, as the device Green's build
+ * evaluates them inside its filter sums (the same layer-state, interval-factor,
+ * prefix-product and pair code as the build; greens.cpp:167-191 combinations):
+ * h_out[t][4][nz][nz] complex = V1, V1 + V3, V2 + V5 (upper triangle k <= kp,
+ * lower entries 0) and V4 (every k, kp). Pins the lambda accumulation's inputs
+ * against the reference's moment tables (test_layered.cpp:362-401). */
+int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                       double omega, int n, const double* h_lam, double* h_out);
 
 void emie_cu_operator_destroy(emie_cu_operator op);
 

@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-REF_DIR = HERE / "_ref"
+REF_DIR = HERE / os.environ.get("EMIE_REF_VARIANT", "_ref")  # _ref_fma: FMA-contracted build of the same sources
 CAPI = REF_DIR / "libemie_ref_capi.so"
 TOOL = REF_DIR / "emie_ref_tool"
 
@@ -130,12 +130,27 @@ class RefCase:
 
     def block(self, oi, oj):
         out = np.zeros(self.nent, np.complex128)
-        _check(lib().ref_assemble_block(self.ctx, oi, oj, _dp(out.view(np.float64))))
+        _check(lib().ref_assemble_block(self.ctx, int(oi), int(oj), _dp(out.view(np.float64))))
         return out
+
+    def block_weights(self, oi, oj, w, lam):
+        """assemble_block's accumulation with given filter weights w (6, nw), lam (nw)."""
+        w = np.ascontiguousarray(w, np.float64)
+        lam = np.ascontiguousarray(lam, np.float64)
+        out = np.zeros(self.nent, np.complex128)
+        _check(lib().ref_assemble_block_weights(self.ctx, int(oi), int(oj), _dp(w), _dp(lam), len(lam),
+                                                _dp(out.view(np.float64))))
+        return out
+
+    def vfunctions(self, lam):
+        """v_functions of every (n, m) pair at lam -> (5, nz, nz)."""
+        out = np.zeros(5 * self.nz * self.nz, np.complex128)
+        _check(lib().ref_vfunctions(self.ctx, ctypes.c_double(lam), _dp(out.view(np.float64))))
+        return out.reshape(5, self.nz, self.nz)
 
     def block_full(self, oi, oj):
         out = np.zeros(9 * self.nz * self.nz, np.complex128)
-        _check(lib().ref_assemble_block_full(self.ctx, oi, oj, _dp(out.view(np.float64))))
+        _check(lib().ref_assemble_block_full(self.ctx, int(oi), int(oj), _dp(out.view(np.float64))))
         return out.reshape(9, self.nz, self.nz)
 
 

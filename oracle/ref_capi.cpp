@@ -141,6 +141,79 @@ int ref_assemble_block(void* p, int oi, int oj, double* out) {
   });
 }
 
+// assemble_block's lambda accumulation (greens.cpp:150-221, same loop order
+// and the reference's own MomentMemo tables and v_functions) with
+// caller-supplied filter weights w[6][nw] (greens.cpp:137 order) and
+// abscissae lam[nw]: separates the filter design from the accumulation when
+// a device build is compared with the reference (parity diagnostics only)
+int ref_assemble_block_weights(void* p, int oi, int oj, const double* w, const double* lam, int nw,
+                               double* out) {
+  Ctx* c = static_cast<Ctx*>(p);
+  return guarded([&] {
+    const AnomalyGrid& grid = c->grid;
+    const int nz = grid.nz();
+    const PairGeometry g = pair_geometry(oi, oj, grid.hx, grid.hy);
+    const double R = g.r;
+    const std::size_t ntri = static_cast<std::size_t>(nz) * (nz + 1) / 2, nfull = std::size_t(nz) * nz;
+    std::vector<cdouble> a00(ntri), a20(ntri), a02(ntri), a11(ntri), az(ntri), axz(nfull), ayz(nfull);
+    MomentMemo memo(c->model, grid.part, c->omega);
+    for (int t = 0; t < nw; ++t) {
+      const double lambda = lam[t] / R;
+      const auto tabs = memo.get(lambda);
+      const double w00 = w[t], w20 = w[nw + t], w02 = w[2 * nw + t];
+      const double w11 = w[3 * nw + t], w10 = w[4 * nw + t], w01 = w[5 * nw + t];
+      for (int k = 0; k < nz; ++k)
+        for (int kp = 0; kp < nz; ++kp) {
+          const VFunctions v = v_functions(tabs->first, tabs->second, k, kp, grid.sigma_b[k], c->omega);
+          const cdouble f4 = lambda * v.v4;
+          const std::size_t fi = static_cast<std::size_t>(k) * nz + kp;
+          axz[fi] += w10 * f4;
+          ayz[fi] += w01 * f4;
+          if (k <= kp) {
+            const std::size_t s = GreensBlock::tri(k, kp, nz);
+            const cdouble f2 = (v.v1 + v.v3) / lambda;
+            a00[s] += w00 * (lambda * v.v1);
+            a20[s] += w20 * f2;
+            a02[s] += w02 * f2;
+            a11[s] += w11 * f2;
+            az[s] += w00 * (lambda * (v.v2 + v.v5));
+          }
+        }
+    }
+    const double c3 = R * R * R / (4.0 * pi), c2 = R * R / (4.0 * pi), c1 = R / (4.0 * pi);
+    cdouble* o = reinterpret_cast<cdouble*>(out);
+    for (std::size_t s = 0; s < ntri; ++s) o[s] = c3 * a00[s] + c1 * a20[s];
+    for (std::size_t s = 0; s < ntri; ++s) o[ntri + s] = c3 * a00[s] + c1 * a02[s];
+    for (std::size_t s = 0; s < ntri; ++s) o[2 * ntri + s] = c3 * az[s];
+    for (std::size_t s = 0; s < ntri; ++s) o[3 * ntri + s] = c1 * a11[s];
+    for (std::size_t i = 0; i < nfull; ++i) o[4 * ntri + i] = c2 * axz[i];
+    for (std::size_t i = 0; i < nfull; ++i) o[4 * ntri + nfull + i] = c2 * ayz[i];
+  });
+}
+
+// v_functions (layered.cpp:397-408) of every (n, m) interval pair at one
+// lambda: out[5][nz][nz] = v1..v5 (pins the device's V-function evaluation)
+int ref_vfunctions(void* p, double lambda, double* out) {
+  Ctx* c = static_cast<Ctx*>(p);
+  return guarded([&] {
+    const int nz = c->grid.nz();
+    MomentMemo memo(c->model, c->grid.part, c->omega);
+    const auto tabs = memo.get(lambda);
+    cdouble* o = reinterpret_cast<cdouble*>(out);
+    const std::size_t nz2 = std::size_t(nz) * nz;
+    for (int n = 0; n < nz; ++n)
+      for (int m = 0; m < nz; ++m) {
+        const VFunctions v = v_functions(tabs->first, tabs->second, n, m, c->grid.sigma_b[n], c->omega);
+        const std::size_t i = std::size_t(n) * nz + m;
+        o[i] = v.v1;
+        o[nz2 + i] = v.v2;
+        o[2 * nz2 + i] = v.v3;
+        o[3 * nz2 + i] = v.v4;
+        o[4 * nz2 + i] = v.v5;
+      }
+  });
+}
+
 // nine components q[3a+b], each nz x nz
 int ref_assemble_block_full(void* p, int oi, int oj, double* out) {
   Ctx* c = static_cast<Ctx*>(p);

@@ -128,6 +128,9 @@ def lib():
         "emie_cu_fgmres": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                            ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
         "emie_cu_device_count": [ip],
+        "emie_cu_assemble_blocks": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, ctypes.c_int, vp, vp, vp],
+        "emie_cu_vfunctions": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_double, ctypes.c_int, vp, vp],
         "emie_cu_kernel_output": [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp],
         # sharded apply (distributed.py)
@@ -402,6 +405,30 @@ def assemble_operator(grid: AnomalyGrid, model: LayeredModel, omega: float,
     return SpectralOperator(h)
 
 
+def assemble_block(grid: AnomalyGrid, model: LayeredModel, omega: float, offset_i, offset_j,
+                   params: Optional[FilterParams] = None) -> np.ndarray:
+    """assemble_block (greens.hpp:129-135) at one or more signed offsets, on
+    the device -> (n, 2nz(2nz+1)) blocks in GreensBlock order (xx yy zz xy
+    triangles, xz yz full); OutOfRange outside the grid (greens.cpp:153-154)."""
+    model.validate()
+    grid.validate(model)
+    oi = np.ascontiguousarray(np.atleast_1d(offset_i), dtype=np.int32)
+    oj = np.ascontiguousarray(np.atleast_1d(offset_j), dtype=np.int32)
+    if oi.shape != oj.shape:
+        raise InvalidArgument("assemble_block: offset arrays differ in length")
+    tops = np.ascontiguousarray(model.tops, dtype=np.float64)
+    sig = _c128(model.sigma)
+    br = np.ascontiguousarray(grid.breaks, dtype=np.float64)
+    fp = (params or FilterParams()).as_array()
+    nz = grid.nz
+    out = np.zeros((oi.size, 2 * nz * (2 * nz + 1)), np.complex128)
+    _check(lib().emie_cu_assemble_blocks(len(tops), _ptr(tops), _ptr(sig), nz, _ptr(br), grid.nx, grid.ny,
+                                         grid.hx, grid.hy, float(omega), _ptr(fp), oi.size,
+                                         oi.ctypes.data_as(ctypes.c_void_p), oj.ctypes.data_as(ctypes.c_void_p),
+                                         _ptr(out)))
+    return out
+
+
 def greens_offsets(nx: int, ny: int, hx: float, hy: float) -> np.ndarray:
     """Offsets oi*nx + oj the Green's build computes (the rest are x <-> y
     mirrors on square grids with hx == hy); the sharded build splits these."""
@@ -490,6 +517,22 @@ def design_offset_filters(oi: int, oj: int, hx: float, hy: float,
     _check(lib().emie_cu_design_offset_filters(int(oi), int(oj), float(hx), float(hy), _ptr(fp),
                                                _ptr(w), _ptr(lam)))
     return w, lam
+
+
+def vfunctions(model: LayeredModel, breaks, omega: float, lam) -> np.ndarray:
+    """V-functions of every interval pair at the given lambdas as the device
+    build evaluates them (layered.cpp:397-408) -> (n, 4, nz, nz) complex:
+    V1, V1 + V3, V2 + V5 (upper triangle), V4 (full)."""
+    model.validate()
+    tops = np.ascontiguousarray(model.tops, dtype=np.float64)
+    sig = _c128(model.sigma)
+    br = np.ascontiguousarray(breaks, dtype=np.float64)
+    lam = np.ascontiguousarray(np.atleast_1d(lam), dtype=np.float64)
+    nz = len(br) - 1
+    out = np.zeros((lam.size, 4, nz, nz), np.complex128)
+    _check(lib().emie_cu_vfunctions(len(tops), _ptr(tops), _ptr(sig), nz, _ptr(br), float(omega), lam.size,
+                                    _ptr(lam), _ptr(out)))
+    return out
 
 
 def kernel_output(oi: int, oj: int, hx: float, hy: float, alpha: int, beta: int, s) -> np.ndarray:

@@ -504,21 +504,42 @@ int emie_cu_operator_from_blocks(int nx, int ny, int nz, double omega, const dou
   });
 }
 
+namespace {
+// FilterParams (hankel.hpp:20-26) from the ABI's {step, shift, half, n1, n2},
+// NULL = defaults; validated as FilterDesigner's constructor does (hankel.cpp:205-208)
+FilterParams filter_params_of(const double* filter) {
+  FilterParams fp;
+  if (filter) {
+    fp.step = filter[0];
+    fp.shift = filter[1];
+    fp.half = static_cast<int>(filter[2]);
+    fp.n1 = static_cast<int>(filter[3]);
+    fp.n2 = static_cast<int>(filter[4]);
+  }
+  check_filter_params(fp);
+  return fp;
+}
+}  // namespace
+
+int emie_cu_assemble_blocks(int L, const double* tops, const double* sigma, int nz, const double* breaks, int nx,
+                            int ny, double hx, double hy, double omega, const double* filter, int n,
+                            const int* h_oi, const int* h_oj, double* h_blocks) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || (n > 0 && (!h_oi || !h_oj || !h_blocks)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "assemble_blocks: null pointer");
+    const FilterParams fp = filter_params_of(filter);
+    assemble_signed_host(nx, ny, nz, omega, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, fp, n,
+                         h_oi, h_oj, reinterpret_cast<cplx*>(h_blocks));
+  });
+}
+
 int emie_cu_greens_build(int L, const double* tops, const double* sigma, int nz,
                          const double* breaks, int nx, int ny, double hx, double hy, double omega,
                          const double* filter, int keep_blocks, emie_cu_operator* out,
                          void* stream) {
   return guarded([&] {
     if (!out || !tops || !sigma || !breaks) fail(EMIE_CU_INVALID_ARGUMENT, "greens_build: null pointer");
-    FilterParams fp;
-    if (filter) {
-      fp.step = filter[0];
-      fp.shift = filter[1];
-      fp.half = static_cast<int>(filter[2]);
-      fp.n1 = static_cast<int>(filter[3]);
-      fp.n2 = static_cast<int>(filter[4]);
-    }
-    check_filter_params(fp);
+    const FilterParams fp = filter_params_of(filter);
     auto h = std::make_unique<emie_cu_operator_s>();
     init_operator_geometry(h->op, nx, ny, nz, omega);
     const cudaStream_t st = as_stream(stream);
@@ -544,15 +565,7 @@ int emie_cu_greens_blocks(int L, const double* tops, const double* sigma, int nz
                           double* d_blocks, void* stream) {
   return guarded([&] {
     if (!tops || !sigma || !breaks || !d_blocks) fail(EMIE_CU_INVALID_ARGUMENT, "greens_blocks: null pointer");
-    FilterParams fp;
-    if (filter) {
-      fp.step = filter[0];
-      fp.shift = filter[1];
-      fp.half = static_cast<int>(filter[2]);
-      fp.n1 = static_cast<int>(filter[3]);
-      fp.n2 = static_cast<int>(filter[4]);
-    }
-    check_filter_params(fp);
+    const FilterParams fp = filter_params_of(filter);
     Operator geom;
     init_operator_geometry(geom, nx, ny, nz, omega, 0, 0);
     greens_blocks(geom, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, fp, c0, c1,
@@ -580,15 +593,7 @@ int emie_cu_operator_from_greens_blocks(int nx, int ny, int nz, double omega, do
 int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy, const double* filter,
                                   double* h_w, double* h_lam) {
   return guarded([&] {
-    FilterParams fp;
-    if (filter) {
-      fp.step = filter[0];
-      fp.shift = filter[1];
-      fp.half = static_cast<int>(filter[2]);
-      fp.n1 = static_cast<int>(filter[3]);
-      fp.n2 = static_cast<int>(filter[4]);
-    }
-    check_filter_params(fp);
+    const FilterParams fp = filter_params_of(filter);
     design_offset_filters_host(oi, oj, hx, hy, fp, h_w, h_lam);
   });
 }
@@ -1076,6 +1081,16 @@ extern "C" int emie_cu_probe_fp64(double* tflops, void* stream) {
     cudaEventDestroy(b);
     release(out, st);
     tflops[0] = std::max(f1 / (t1 * 1e-3), f2 / (t2 * 1e-3)) / 1e12;
+  });
+}
+
+extern "C" int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                                  double omega, int n, const double* h_lam, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || (n > 0 && (!h_lam || !h_out)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "vfunctions: null pointer");
+    vfunctions_host(L, tops, reinterpret_cast<const cplx*>(sigma), nz, breaks, omega, n, h_lam,
+                    reinterpret_cast<cplx*>(h_out));
   });
 }
 

@@ -184,6 +184,18 @@ __host__ __device__ inline Geom pair_geometry(int oi, int oj, double hx, double 
   return g;
 }
 
+// Offsets travel as integer codes: code = (oi + bias_i) * span + (oj + bias_j).
+// A full build uses span = nx, no bias (code = the offset-major slot oi*nx + oj
+// of the stored sector); a signed-offset request (assemble_block at negative
+// offsets, emie_cu_assemble_blocks) uses span = 2nx - 1, bias (ny-1, nx-1) and
+// stores its blocks compactly in request order.
+struct OffsetCode {
+  int span = 1, bias_i = 0, bias_j = 0, compact = 0;
+  __host__ __device__ int oi(int c) const { return c / span - bias_i; }
+  __host__ __device__ int oj(int c) const { return c % span - bias_j; }
+  __host__ __device__ int slot(int c, int pos) const { return compact ? pos : c; }
+};
+
 __device__ double kernel_output(const Geom& g, int alpha, int beta, double s) {  // hankel.cpp:101-113
   const double r = exp(s);
   const double hx = g.p * r, hy = g.q * r;
@@ -247,16 +259,17 @@ __global__ void filter_den_kernel(cplx* den, double* floor_out, const cplx* __re
 __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
                                      const double* __restrict__ den_floor,
                                      const cplx* __restrict__ tw, FftPlan pl, int half, double step,
-                                     double shift, int n1, int n2, int nx, double hx, double hy,
+                                     double shift, int n1, int n2, OffsetCode oc, double hx, double hy,
                                      int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs) {
   extern __shared__ cplx sm[];
   const int n = pl.n, ld = n | 1;
   cplx* a = sm;
   cplx* b = a + ld;
   cplx* t = b + ld;
-  const int off = offs ? offs[blockIdx.x] : static_cast<int>(blockIdx.x), kern = blockIdx.y;
-  const int oi = fixed_oi != INT32_MIN ? fixed_oi : off / nx;
-  const int oj = fixed_oi != INT32_MIN ? fixed_oj : off % nx;
+  const int code = offs ? offs[blockIdx.x] : static_cast<int>(blockIdx.x), kern = blockIdx.y;
+  const int off = oc.slot(code, blockIdx.x);
+  const int oi = fixed_oi != INT32_MIN ? fixed_oi : oc.oi(code);
+  const int oj = fixed_oi != INT32_MIN ? fixed_oj : oc.oj(code);
   const Geom g = pair_geometry(oi, oj, hx, hy);
   const int alpha = kAlpha[kern], beta = kBeta[kern];
   load_twiddles(t, tw, n);
@@ -321,6 +334,7 @@ struct GreenParams {
   int LC;          // lambdas per chunk
   int npairs;      // nz(nz+1)/2
   int nent;
+  OffsetCode oc;   // offset codes of this build
   // model (host-filled)
   double thick[kMaxLayers];
   cplx sig[kMaxLayers];  // floored conductivities
@@ -484,12 +498,14 @@ __device__ unsigned long long g_phase_clk[8];
 // for every chunk of a batch of offsets (one thread per lambda), writing the
 // SMEM image the assemble kernel then loads with one bulk copy.
 __device__ __forceinline__ void chunk_layer_states(const GreenParams& P, const Chunk& C, double R, int t0, int lc,
-                                                   int tid, int nth, bool sync) {
+                                                   int tid, int nth, bool sync, const double* lam_in = nullptr) {
   const int L = P.L, NL = P.L + 1;
     // phase 0a: eta, e2l, em1 per (lambda, layer)
     for (int x = tid; x < lc * NL; x += nth) {
       const int li = x / NL, m = x - li * NL;
-      const double lam = exp((P.n1 + t0 + li) * P.step + P.shift) / R;
+      // lambda_t = lam_t / R on the filter lattice (greens.cpp:166); the
+      // V-function probe passes its lambdas explicitly
+      const double lam = lam_in ? lam_in[t0 + li] : exp((P.n1 + t0 + li) * P.step + P.shift) / R;
       const cplx eta2 = cplx{lam * lam, 0.0} - cplx{0.0, P.omega * kMu0} * P.sig[m];
       const cplx eta = csqrt_pos(eta2);
       C.eta[li * NL + m] = eta;
@@ -576,8 +592,8 @@ __global__ void __launch_bounds__(128) layer_state_kernel(const GreenParams P, c
     const int ch = static_cast<int>(y % nchunk), b = static_cast<int>(y / nchunk);
     const int t = ch * LC + li;
     if (t >= P.nw) continue;
-    const int off = offs[b];
-    const Geom g = pair_geometry(off / P.nx, off % P.nx, P.hx, P.hy);
+    const int code = offs[b];
+    const Geom g = pair_geometry(P.oc.oi(code), P.oc.oj(code), P.hx, P.hy);
     cplx* img = LS + (static_cast<size_t>(b) * nchunk + ch) * ls_elems;
     Chunk v;  // the one-lambda view of slot li
     v.eta = img + li * NL;
@@ -593,6 +609,276 @@ __global__ void __launch_bounds__(128) layer_state_kernel(const GreenParams P, c
   }
 }
 
+// Chunk field accessors: F(li, f, j) interval field f of interval j at chunk
+// lambda li; Ei(li, gamma, j) packed prefix exponent of that medium
+__device__ __forceinline__ cplx& chunk_field(const Chunk& C, int nz, int li, int f, int j) {
+  return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j];
+}
+
+// phase 1 of a chunk: interval pack (shared by both gammas) and the per-interval
+// factors of both media (layered.cpp:222-317), strided over (tid, nth)
+__device__ __forceinline__ void chunk_factors(const GreenParams& P, const Chunk& C, const Interval* __restrict__ iv,
+                                              int lc, double wmu, int tid, int nth) {
+  const int NL = P.L + 1, nz = P.nz;
+  auto F = [&](int li, int f, int j) -> cplx& { return chunk_field(C, nz, li, f, j); };
+  // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317)
+  for (int x = tid; x < lc * nz; x += nth) {
+    const int li = x / nz, j = x - li * nz;
+    const Interval I = iv[j];
+    const cplx eta = C.eta[li * NL + I.layer];
+    const cplx ie = C.ieta[li * NL + I.layer];  // 1/eta, 1/eta^2: the divisions below become products
+    const cplx ie2 = ie * ie;
+    const cplx ehm1 = cexpm1(-I.h * eta);
+    const cplx eh = cplx{1.0, 0.0} + ehm1;
+    const cplx el2 = C.e2l[li * NL + I.layer];
+    cplx epa = {1.0, 0.0}, epa2m1 = {0.0, 0.0}, epabm1 = {0.0, 0.0}, epb2m1 = {0.0, 0.0};
+    cplx eqb = {1.0, 0.0}, eqabm1 = {0.0, 0.0};
+    if (I.has_p) {
+      const cplx epam1 = cexpm1(-(I.a - I.d) * eta);
+      const cplx epbm1 = epam1 + ehm1 + epam1 * ehm1;
+      epa = cplx{1.0, 0.0} + epam1;
+      epa2m1 = 2.0 * epam1 + epam1 * epam1;
+      epabm1 = epam1 + epbm1 + epam1 * epbm1;
+      epb2m1 = 2.0 * epbm1 + epbm1 * epbm1;
+    }
+    if (I.has_q) {
+      const cplx eqbm1 = cexpm1(-(I.dp - I.b) * eta);
+      const cplx eqam1 = eqbm1 + ehm1 + eqbm1 * ehm1;
+      eqb = cplx{1.0, 0.0} + eqbm1;
+      eqabm1 = eqam1 + eqbm1 + eqam1 * eqbm1;
+    }
+    const cplx elh = (I.has_p && I.has_q) ? cexp((-(2.0 * I.l - I.h)) * eta) : cplx{0.0, 0.0};
+    const cplx u = -ehm1;
+    const cplx eta2 = eta * eta;
+    const cplx isk = I.inv_sig;
+    for (int gm = 0; gm < 2; ++gm) {
+      const int r = li * 2 * NL + gm * NL + I.layer;
+      const cplx p = C.p[r], q = C.q[r], A = C.diag_a[r];
+      const cplx one_p = C.one_p[r], one_q = C.one_q[r];
+      const cplx Sa = one_p + p * epa2m1;
+      const cplx Sab = one_p + p * epabm1;
+      const cplx Mab = (cplx{2.0, 0.0} - one_p) - p * epabm1;
+      const cplx Dp = one_p + p * epb2m1;
+      const cplx Tq = one_q + q * eqabm1;
+      const cplx TMq = (cplx{2.0, 0.0} - one_q) - q * eqabm1;
+      const cplx iDp = crecip(Dp);
+      const cplx theta = (eh * Sa) * iDp;
+      const cplx H0 = ((u * Sab) * ie) * iDp;
+      const cplx J0 = (A * u * Sa * Tq) * ie;
+      const cplx Ip = (epa * u) * ie;
+      const cplx Iq = (eqb * u) * ie;
+      const cplx Sp = p * Ip * Ip, Sq = q * Iq * Iq;
+      const cplx M0 = (2.0 * (I.h * eta + ehm1)) * ie2;
+      const cplx P0 = 2.0 * ((elh * u) * ie2 - (I.h * el2) * ie);
+      const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
+      if (gm == 0) {
+        F(li, fLU, j) = cplx{-wmu * H0.im, wmu * H0.re};
+        F(li, fRU, j) = J0;
+        F(li, fD1, j) = cplx{-wmu * W00d.im, wmu * W00d.re};
+        F(li, fPiu, j) = theta;
+      } else {
+        const cplx H1 = (u * Mab) * iDp;
+        F(li, fL0v, j) = (cplx{0.0, wmu} + eta2 * isk) * H0;
+        F(li, fL0s, j) = H0 * isk;
+        F(li, fL1s, j) = H1 * isk;
+        F(li, fR0, j) = J0;
+        F(li, fR1, j) = -(A * u * Sa * TMq);
+        const cplx W11d = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) - cplx{2.0 * I.h, 0.0};
+        const cplx W20d = eta2 * W00d - cplx{2.0 * I.h, 0.0};
+        F(li, fD25, j) = cplx{-wmu * W00d.im, wmu * W00d.re} + W20d * isk;
+        F(li, fD3, j) = -(W11d * isk);
+        F(li, fD4, j) = (A * eta * (Sq - Sp)) * isk;
+        F(li, fPic, j) = theta;
+      }
+    }
+  }
+}
+
+// phase 1b: prefix products of theta per (lambda, gamma) (CTA-wide, warp tasks)
+__device__ __forceinline__ void chunk_prefix(const GreenParams& P, const Chunk& C, int lc) {
+  const int nz = P.nz;
+  auto F = [&](int li, int f, int j) -> cplx& { return chunk_field(C, nz, li, f, j); };
+  auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 2 + f) * nz + j]; };
+  // phase 1b: prefix products of theta per (lambda, gamma) as
+  // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l.
+  // nz <= 64: eight (nz > 32: sixteen) lanes per (lambda, gamma), several tasks per warp at once;
+  // a lane owns ceil(nz/8) consecutive intervals: local products, a 3-step
+  // shuffle scan over the eight lanes, the lane's exclusive prefix
+  // multiplied in. Mantissas (max component in [1, 2), modulus < 2^1.5) are
+  // not renormalised inside: a product of <= 64 stays below 2^96.
+  if (nz <= 64) {
+    // lanes per task: 8 (nz <= 32) or 16 (deeper grids: half the serial
+    // per-lane work; lc * 2 * 16 still fits one pass of the CTA at LC = 8)
+    const int TW = nz > 32 ? 16 : 8, tpw = 32 / TW;
+    const int lane = threadIdx.x & 31, sub = lane & (TW - 1);
+    const int per = (nz + TW - 1) / TW;
+    const int ntask = lc * 2;
+    for (int task0 = (threadIdx.x >> 5) * tpw; task0 < ntask; task0 += (blockDim.x >> 5) * tpw) {
+      const int task = task0 + lane / TW;
+      const bool live = task < ntask;
+      const int li = live ? task >> 1 : 0, gm = task & 1;
+      const int fT = gm ? fPic : fPiu;
+      cplx m[8];
+      int e[8], z[8];
+      cplx lm = {1.0, 0.0};  // running local product (inclusive)
+      int le = 0, lz = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = sub * per + q;
+        cplx mq = {1.0, 0.0};
+        int eq = 0, zq = 0;
+        if (q < per && j < nz && live) {
+          const cplx th = F(li, fT, j);
+          if (th.re == 0.0 && th.im == 0.0) {
+            zq = 1;
+          } else {
+            const int sh = ilog2(fmax(fabs(th.re), fabs(th.im)));
+            mq = scal2(th, -sh);
+            eq = sh;
+          }
+        }
+        // exclusive local prefix of element q, then include it
+        m[q] = lm;
+        e[q] = le;
+        z[q] = lz;
+        lm = lm * mq;
+        le += eq;
+        lz += zq;
+      }
+      // inclusive scan of the lane totals over the TW lanes of the task
+      cplx sm_ = lm;
+      int se = le, sz = lz;
+#pragma unroll 4
+      for (int off = 1; off < TW; off <<= 1) {
+        const double mr = __shfl_up_sync(0xffffffffu, sm_.re, off, TW);
+        const double mi = __shfl_up_sync(0xffffffffu, sm_.im, off, TW);
+        const int oe = __shfl_up_sync(0xffffffffu, se, off, TW);
+        const int oz = __shfl_up_sync(0xffffffffu, sz, off, TW);
+        if (sub >= off) {
+          sm_ = cplx{mr, mi} * sm_;
+          se += oe;
+          sz += oz;
+        }
+      }
+      // exclusive lane prefix
+      cplx pm = {__shfl_up_sync(0xffffffffu, sm_.re, 1, TW), __shfl_up_sync(0xffffffffu, sm_.im, 1, TW)};
+      int pe = __shfl_up_sync(0xffffffffu, se, 1, TW), pz = __shfl_up_sync(0xffffffffu, sz, 1, TW);
+      if (sub == 0) {
+        pm = {1.0, 0.0};
+        pe = 0;
+        pz = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = sub * per + q;
+        if (q < per && j < nz && live) {
+          cplx v = pm * m[q];
+          const int sh = ilog2(fmax(fabs(v.re), fabs(v.im)));
+          v = scal2(v, -sh);
+          // right factors P(j) J(j); theta(j) (read above by this lane only) -> 1/P(j)
+          if (gm) {
+            F(li, fR0, j) = v * F(li, fR0, j);
+            F(li, fR1, j) = v * F(li, fR1, j);
+          } else {
+            F(li, fRU, j) = v * F(li, fRU, j);
+          }
+          F(li, fT, j) = crecip(v);
+          Ei(li, gm, j) = ez_pack(pe + e[q] + sh, pz + z[q]);
+        }
+      }
+    }
+  } else {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int task = warp; task < lc * 2; task += nwarps) {
+      const int li = task >> 1, gm = task & 1;
+      const int fT = gm ? fPic : fPiu;
+      cplx cm = {1.0, 0.0};  // carry: product of the previous segments
+      int ce = 0, cz = 0;
+      for (int j0 = 0; j0 < nz; j0 += 32) {
+        const int j = j0 + lane;
+        // this lane's factor, normalised
+        cplx m = {1.0, 0.0};
+        int e = 0, z = 0;
+        if (j < nz) {
+          const cplx th = F(li, fT, j);
+          if (th.re == 0.0 && th.im == 0.0) {
+            z = 1;
+          } else {
+            const int s = ilog2(fmax(fabs(th.re), fabs(th.im)));
+            m = scal2(th, -s);
+            e = s;
+          }
+        }
+        // inclusive scan (lane order = interval order). Mantissas with max
+        // component in [1, 2) have modulus in [1, 2^1.5), so a product of
+        // <= 32 stays in [1, 2^48]: no renormalisation inside the scan, and
+        // since power-of-two scalings are exact, the final normalised
+        // mantissas equal a step-by-step renormalised scan bit for bit
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const double mr = __shfl_up_sync(0xffffffffu, m.re, off);
+          const double mi = __shfl_up_sync(0xffffffffu, m.im, off);
+          const int oe = __shfl_up_sync(0xffffffffu, e, off);
+          const int oz = __shfl_up_sync(0xffffffffu, z, off);
+          if (lane >= off) {
+            m = cplx{mr, mi} * m;
+            e += oe;
+            z += oz;
+          }
+        }
+        // exclusive prefix = carry x inclusive of the previous lane
+        cplx pm = {__shfl_up_sync(0xffffffffu, m.re, 1), __shfl_up_sync(0xffffffffu, m.im, 1)};
+        int pe = __shfl_up_sync(0xffffffffu, e, 1), pz = __shfl_up_sync(0xffffffffu, z, 1);
+        if (lane == 0) {
+          pm = {1.0, 0.0};
+          pe = 0;
+          pz = 0;
+        }
+        pm = cm * pm;
+        {
+          const int s = ilog2(fmax(fabs(pm.re), fabs(pm.im)));
+          pm = scal2(pm, -s);
+          pe += ce + s;
+        }
+        pz += cz;
+        if (j < nz) {
+          if (gm) {
+            F(li, fR0, j) = pm * F(li, fR0, j);
+            F(li, fR1, j) = pm * F(li, fR1, j);
+          } else {
+            F(li, fRU, j) = pm * F(li, fRU, j);
+          }
+          F(li, fT, j) = crecip(pm);
+          Ei(li, gm, j) = ez_pack(pe, pz);
+        }
+        // new carry: carry x inclusive of lane 31
+        const cplx lm = {__shfl_sync(0xffffffffu, m.re, 31), __shfl_sync(0xffffffffu, m.im, 31)};
+        const int le = __shfl_sync(0xffffffffu, e, 31), lz = __shfl_sync(0xffffffffu, z, 31);
+        cm = cm * lm;
+        const int s = ilog2(fmax(fabs(cm.re), fabs(cm.im)));
+        cm = scal2(cm, -s);
+        ce += le + s;
+        cz += lz;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void chunk_left(const GreenParams& P, const Chunk& C, int lc, int tid, int nth) {
+  const int nz = P.nz;
+  auto F = [&](int li, int f, int j) -> cplx& { return chunk_field(C, nz, li, f, j); };
+  // phase 1c: left factors of rows k < nz - 1 divided by P(k+1) of their medium
+  for (int x = tid; x < lc * (nz - 1); x += nth) {
+    const int li = x / (nz - 1), j = x - li * (nz - 1);
+    const cplx pu = F(li, fPiu, j + 1), pcn = F(li, fPic, j + 1);
+    F(li, fLU, j) = F(li, fLU, j) * pu;
+    F(li, fL0v, j) = F(li, fL0v, j) * pcn;
+    F(li, fL1s, j) = F(li, fL1s, j) * pcn;
+    F(li, fL0s, j) = F(li, fL0s, j) * pcn;
+  }
+}
+
 #ifndef EMIE_GREEN_MINB
 #define EMIE_GREEN_MINB 1  // CTAs per SM the register budget targets
 #endif
@@ -603,12 +889,14 @@ __global__ void __launch_bounds__(128) layer_state_kernel(const GreenParams P, c
 template <bool LSPRE>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
-    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, const cplx* __restrict__ LS, int nchunk) {
+    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, const cplx* __restrict__ LS, int nchunk,
+    int pos0) {
   extern __shared__ cplx sm[];
   __shared__ uint64_t lsbar;
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
-  const int off = offs[blockIdx.x];
-  const int oi = off / P.nx, oj = off % P.nx;
+  const int code = offs[blockIdx.x];
+  const int off = P.oc.slot(code, pos0 + blockIdx.x);  // block / weight slot
+  const int oi = P.oc.oi(code), oj = P.oc.oj(code);
   const Geom g = pair_geometry(oi, oj, P.hx, P.hy);
   const double R = g.r;
   const double* Woff = W + static_cast<size_t>(off) * 6 * P.nw;
@@ -704,77 +992,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     }
     __syncthreads();
     PHASE_MARK(3);
-    // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317)
-    for (int x = threadIdx.x; x < lc * nz; x += blockDim.x) {
-      const int li = x / nz, j = x - li * nz;
-      const Interval I = iv[j];
-      const cplx eta = C.eta[li * NL + I.layer];
-      const cplx ie = C.ieta[li * NL + I.layer];  // 1/eta, 1/eta^2: the divisions below become products
-      const cplx ie2 = ie * ie;
-      const cplx ehm1 = cexpm1(-I.h * eta);
-      const cplx eh = cplx{1.0, 0.0} + ehm1;
-      const cplx el2 = C.e2l[li * NL + I.layer];
-      cplx epa = {1.0, 0.0}, epa2m1 = {0.0, 0.0}, epabm1 = {0.0, 0.0}, epb2m1 = {0.0, 0.0};
-      cplx eqb = {1.0, 0.0}, eqabm1 = {0.0, 0.0};
-      if (I.has_p) {
-        const cplx epam1 = cexpm1(-(I.a - I.d) * eta);
-        const cplx epbm1 = epam1 + ehm1 + epam1 * ehm1;
-        epa = cplx{1.0, 0.0} + epam1;
-        epa2m1 = 2.0 * epam1 + epam1 * epam1;
-        epabm1 = epam1 + epbm1 + epam1 * epbm1;
-        epb2m1 = 2.0 * epbm1 + epbm1 * epbm1;
-      }
-      if (I.has_q) {
-        const cplx eqbm1 = cexpm1(-(I.dp - I.b) * eta);
-        const cplx eqam1 = eqbm1 + ehm1 + eqbm1 * ehm1;
-        eqb = cplx{1.0, 0.0} + eqbm1;
-        eqabm1 = eqam1 + eqbm1 + eqam1 * eqbm1;
-      }
-      const cplx elh = (I.has_p && I.has_q) ? cexp((-(2.0 * I.l - I.h)) * eta) : cplx{0.0, 0.0};
-      const cplx u = -ehm1;
-      const cplx eta2 = eta * eta;
-      const cplx isk = I.inv_sig;
-      for (int gm = 0; gm < 2; ++gm) {
-        const int r = li * 2 * NL + gm * NL + I.layer;
-        const cplx p = C.p[r], q = C.q[r], A = C.diag_a[r];
-        const cplx one_p = C.one_p[r], one_q = C.one_q[r];
-        const cplx Sa = one_p + p * epa2m1;
-        const cplx Sab = one_p + p * epabm1;
-        const cplx Mab = (cplx{2.0, 0.0} - one_p) - p * epabm1;
-        const cplx Dp = one_p + p * epb2m1;
-        const cplx Tq = one_q + q * eqabm1;
-        const cplx TMq = (cplx{2.0, 0.0} - one_q) - q * eqabm1;
-        const cplx iDp = crecip(Dp);
-        const cplx theta = (eh * Sa) * iDp;
-        const cplx H0 = ((u * Sab) * ie) * iDp;
-        const cplx J0 = (A * u * Sa * Tq) * ie;
-        const cplx Ip = (epa * u) * ie;
-        const cplx Iq = (eqb * u) * ie;
-        const cplx Sp = p * Ip * Ip, Sq = q * Iq * Iq;
-        const cplx M0 = (2.0 * (I.h * eta + ehm1)) * ie2;
-        const cplx P0 = 2.0 * ((elh * u) * ie2 - (I.h * el2) * ie);
-        const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
-        if (gm == 0) {
-          F(li, fLU, j) = cplx{-wmu * H0.im, wmu * H0.re};
-          F(li, fRU, j) = J0;
-          F(li, fD1, j) = cplx{-wmu * W00d.im, wmu * W00d.re};
-          F(li, fPiu, j) = theta;
-        } else {
-          const cplx H1 = (u * Mab) * iDp;
-          F(li, fL0v, j) = (cplx{0.0, wmu} + eta2 * isk) * H0;
-          F(li, fL0s, j) = H0 * isk;
-          F(li, fL1s, j) = H1 * isk;
-          F(li, fR0, j) = J0;
-          F(li, fR1, j) = -(A * u * Sa * TMq);
-          const cplx W11d = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) - cplx{2.0 * I.h, 0.0};
-          const cplx W20d = eta2 * W00d - cplx{2.0 * I.h, 0.0};
-          F(li, fD25, j) = cplx{-wmu * W00d.im, wmu * W00d.re} + W20d * isk;
-          F(li, fD3, j) = -(W11d * isk);
-          F(li, fD4, j) = (A * eta * (Sq - Sp)) * isk;
-          F(li, fPic, j) = theta;
-        }
-      }
-    }
+    chunk_factors(P, C, iv, lc, wmu, threadIdx.x, blockDim.x);
     if constexpr (LSPRE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // layer-state reads before the refill
     __syncthreads();
     if (LSPRE && threadIdx.x == 0 && t0 + LC < nw) {  // phase 1 was the last reader of the layer states
@@ -783,180 +1001,9 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       bulk_g2s(sm, LS + (static_cast<size_t>(blockIdx.x) * nchunk + t0 / LC + 1) * ls_elems, ls_bytes, &lsbar);
     }
     PHASE_MARK(4);
-    // phase 1b: prefix products of theta per (lambda, gamma) as
-    // (mantissa, exponent, zero count); P_j = prod_{l<j} theta_l.
-    // nz <= 64: eight (nz > 32: sixteen) lanes per (lambda, gamma), several tasks per warp at once;
-    // a lane owns ceil(nz/8) consecutive intervals: local products, a 3-step
-    // shuffle scan over the eight lanes, the lane's exclusive prefix
-    // multiplied in. Mantissas (max component in [1, 2), modulus < 2^1.5) are
-    // not renormalised inside: a product of <= 64 stays below 2^96.
-    if (nz <= 64) {
-      // lanes per task: 8 (nz <= 32) or 16 (deeper grids: half the serial
-      // per-lane work; lc * 2 * 16 still fits one pass of the CTA at LC = 8)
-      const int TW = nz > 32 ? 16 : 8, tpw = 32 / TW;
-      const int lane = threadIdx.x & 31, sub = lane & (TW - 1);
-      const int per = (nz + TW - 1) / TW;
-      const int ntask = lc * 2;
-      for (int task0 = (threadIdx.x >> 5) * tpw; task0 < ntask; task0 += (blockDim.x >> 5) * tpw) {
-        const int task = task0 + lane / TW;
-        const bool live = task < ntask;
-        const int li = live ? task >> 1 : 0, gm = task & 1;
-        const int fT = gm ? fPic : fPiu;
-        cplx m[8];
-        int e[8], z[8];
-        cplx lm = {1.0, 0.0};  // running local product (inclusive)
-        int le = 0, lz = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int j = sub * per + q;
-          cplx mq = {1.0, 0.0};
-          int eq = 0, zq = 0;
-          if (q < per && j < nz && live) {
-            const cplx th = F(li, fT, j);
-            if (th.re == 0.0 && th.im == 0.0) {
-              zq = 1;
-            } else {
-              const int sh = ilog2(fmax(fabs(th.re), fabs(th.im)));
-              mq = scal2(th, -sh);
-              eq = sh;
-            }
-          }
-          // exclusive local prefix of element q, then include it
-          m[q] = lm;
-          e[q] = le;
-          z[q] = lz;
-          lm = lm * mq;
-          le += eq;
-          lz += zq;
-        }
-        // inclusive scan of the lane totals over the TW lanes of the task
-        cplx sm_ = lm;
-        int se = le, sz = lz;
-#pragma unroll 4
-        for (int off = 1; off < TW; off <<= 1) {
-          const double mr = __shfl_up_sync(0xffffffffu, sm_.re, off, TW);
-          const double mi = __shfl_up_sync(0xffffffffu, sm_.im, off, TW);
-          const int oe = __shfl_up_sync(0xffffffffu, se, off, TW);
-          const int oz = __shfl_up_sync(0xffffffffu, sz, off, TW);
-          if (sub >= off) {
-            sm_ = cplx{mr, mi} * sm_;
-            se += oe;
-            sz += oz;
-          }
-        }
-        // exclusive lane prefix
-        cplx pm = {__shfl_up_sync(0xffffffffu, sm_.re, 1, TW), __shfl_up_sync(0xffffffffu, sm_.im, 1, TW)};
-        int pe = __shfl_up_sync(0xffffffffu, se, 1, TW), pz = __shfl_up_sync(0xffffffffu, sz, 1, TW);
-        if (sub == 0) {
-          pm = {1.0, 0.0};
-          pe = 0;
-          pz = 0;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int j = sub * per + q;
-          if (q < per && j < nz && live) {
-            cplx v = pm * m[q];
-            const int sh = ilog2(fmax(fabs(v.re), fabs(v.im)));
-            v = scal2(v, -sh);
-            // right factors P(j) J(j); theta(j) (read above by this lane only) -> 1/P(j)
-            if (gm) {
-              F(li, fR0, j) = v * F(li, fR0, j);
-              F(li, fR1, j) = v * F(li, fR1, j);
-            } else {
-              F(li, fRU, j) = v * F(li, fRU, j);
-            }
-            F(li, fT, j) = crecip(v);
-            Ei(li, gm, j) = ez_pack(pe + e[q] + sh, pz + z[q]);
-          }
-        }
-      }
-    } else {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      const int nwarps = blockDim.x >> 5;
-      for (int task = warp; task < lc * 2; task += nwarps) {
-        const int li = task >> 1, gm = task & 1;
-        const int fT = gm ? fPic : fPiu;
-        cplx cm = {1.0, 0.0};  // carry: product of the previous segments
-        int ce = 0, cz = 0;
-        for (int j0 = 0; j0 < nz; j0 += 32) {
-          const int j = j0 + lane;
-          // this lane's factor, normalised
-          cplx m = {1.0, 0.0};
-          int e = 0, z = 0;
-          if (j < nz) {
-            const cplx th = F(li, fT, j);
-            if (th.re == 0.0 && th.im == 0.0) {
-              z = 1;
-            } else {
-              const int s = ilog2(fmax(fabs(th.re), fabs(th.im)));
-              m = scal2(th, -s);
-              e = s;
-            }
-          }
-          // inclusive scan (lane order = interval order). Mantissas with max
-          // component in [1, 2) have modulus in [1, 2^1.5), so a product of
-          // <= 32 stays in [1, 2^48]: no renormalisation inside the scan, and
-          // since power-of-two scalings are exact, the final normalised
-          // mantissas equal a step-by-step renormalised scan bit for bit
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const double mr = __shfl_up_sync(0xffffffffu, m.re, off);
-            const double mi = __shfl_up_sync(0xffffffffu, m.im, off);
-            const int oe = __shfl_up_sync(0xffffffffu, e, off);
-            const int oz = __shfl_up_sync(0xffffffffu, z, off);
-            if (lane >= off) {
-              m = cplx{mr, mi} * m;
-              e += oe;
-              z += oz;
-            }
-          }
-          // exclusive prefix = carry x inclusive of the previous lane
-          cplx pm = {__shfl_up_sync(0xffffffffu, m.re, 1), __shfl_up_sync(0xffffffffu, m.im, 1)};
-          int pe = __shfl_up_sync(0xffffffffu, e, 1), pz = __shfl_up_sync(0xffffffffu, z, 1);
-          if (lane == 0) {
-            pm = {1.0, 0.0};
-            pe = 0;
-            pz = 0;
-          }
-          pm = cm * pm;
-          {
-            const int s = ilog2(fmax(fabs(pm.re), fabs(pm.im)));
-            pm = scal2(pm, -s);
-            pe += ce + s;
-          }
-          pz += cz;
-          if (j < nz) {
-            if (gm) {
-              F(li, fR0, j) = pm * F(li, fR0, j);
-              F(li, fR1, j) = pm * F(li, fR1, j);
-            } else {
-              F(li, fRU, j) = pm * F(li, fRU, j);
-            }
-            F(li, fT, j) = crecip(pm);
-            Ei(li, gm, j) = ez_pack(pe, pz);
-          }
-          // new carry: carry x inclusive of lane 31
-          const cplx lm = {__shfl_sync(0xffffffffu, m.re, 31), __shfl_sync(0xffffffffu, m.im, 31)};
-          const int le = __shfl_sync(0xffffffffu, e, 31), lz = __shfl_sync(0xffffffffu, z, 31);
-          cm = cm * lm;
-          const int s = ilog2(fmax(fabs(cm.re), fabs(cm.im)));
-          cm = scal2(cm, -s);
-          ce += le + s;
-          cz += lz;
-        }
-      }
-    }
+    chunk_prefix(P, C, lc);
     __syncthreads();
-    // phase 1c: left factors of rows k < nz - 1 divided by P(k+1) of their medium
-    for (int x = threadIdx.x; x < lc * (nz - 1); x += blockDim.x) {
-      const int li = x / (nz - 1), j = x - li * (nz - 1);
-      const cplx pu = F(li, fPiu, j + 1), pcn = F(li, fPic, j + 1);
-      F(li, fLU, j) = F(li, fLU, j) * pu;
-      F(li, fL0v, j) = F(li, fL0v, j) * pcn;
-      F(li, fL1s, j) = F(li, fL1s, j) * pcn;
-      F(li, fL0s, j) = F(li, fL0s, j) * pcn;
-    }
+    chunk_left(P, C, lc, threadIdx.x, blockDim.x);
     __syncthreads();
     PHASE_MARK(5);
     // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
@@ -1036,6 +1083,65 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     }
   }
   if (bad) atomicOr(err, 4);
+}
+
+
+// V-function probe (test entry, emie_cu_vfunctions): the assemble kernel's own
+// lambda-only phases, interval factors, prefix products and pair evaluation
+// (chunk_layer_states, chunk_factors, chunk_prefix, chunk_left, pair_lambda)
+// at caller-given lambdas, unit weights: per lambda the pair quantities the
+// filter sums accumulate (v_functions, layered.cpp:397-408):
+//   out[t][0][k][kp] V1, [1] V1 + V3, [2] V2 + V5 (k <= kp), [3] V4 (all k, kp)
+__global__ void __launch_bounds__(kGreenThreads) vfunc_probe_kernel(const GreenParams P, const Interval* __restrict__ iv,
+                                                                   const double* __restrict__ lam, int n,
+                                                                   cplx* __restrict__ out) {
+  extern __shared__ cplx sm[];
+  const int NL = P.L + 1, nz = P.nz, LC = P.LC;
+  Chunk C;
+  {
+    cplx* s = sm;
+    C.eta = s; s += LC * NL;
+    C.e2l = s; s += LC * NL;
+    C.em1 = s; s += LC * NL;
+    C.p = s; s += LC * 2 * NL;
+    C.q = s; s += LC * 2 * NL;
+    C.one_p = s; s += LC * 2 * NL;
+    C.one_q = s; s += LC * 2 * NL;
+    C.diag_a = s; s += LC * 2 * NL;
+    C.ieta = s; s += LC * NL;
+    C.F = s; s += static_cast<size_t>(LC) * kFields * nz;
+    C.lam = reinterpret_cast<double*>(s);
+    C.E = reinterpret_cast<int*>(C.lam + 8 * LC);
+  }
+  const int t0 = blockIdx.x * LC, lc = min(LC, n - t0);
+  chunk_layer_states(P, C, 1.0, t0, lc, threadIdx.x, blockDim.x, true, lam);
+  __syncthreads();
+  chunk_factors(P, C, iv, lc, P.omega * kMu0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  chunk_prefix(P, C, lc);
+  __syncthreads();
+  chunk_left(P, C, lc, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const double wl[6] = {1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
+  const size_t nz2 = static_cast<size_t>(nz) * nz;
+  for (int x = threadIdx.x; x < lc * P.npairs; x += blockDim.x) {
+    const int li = x / P.npairs, s = x - li * P.npairs;
+    PairC pc;
+    pair_of(s, nz, pc.k, pc.kp);
+    pc.kn = min(pc.k + 1, nz - 1);
+    pc.kind = pc.kp == pc.k ? 0 : 1;
+    cplx a[9];
+#pragma unroll
+    for (int f = 0; f < 9; ++f) a[f] = {0.0, 0.0};
+    pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 2 * nz, nz, pc, wl, a);
+    cplx* o = out + static_cast<size_t>(t0 + li) * 4 * nz2;
+    const size_t up = static_cast<size_t>(pc.k) * nz + pc.kp, lo = static_cast<size_t>(pc.kp) * nz + pc.k;
+    o[up] = a[0];
+    o[nz2 + up] = a[1];
+    o[2 * nz2 + up] = a[4];
+    o[3 * nz2 + up] = a[5];
+    if (pc.k != pc.kp) o[3 * nz2 + lo] = a[7];
+  }
 }
 
 // x <-> y mirror of a square grid with hx == hy: the block of offset (oj, oi)
@@ -1121,7 +1227,7 @@ void free_filter_bank(FilterBank& fb, cudaStream_t st) {
   cudaFree(fb.tw);
 }
 
-void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, int nx, double hx,
+void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, OffsetCode oc, double hx,
                     double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
                     int fixed_oj = 0, const int* offs = nullptr) {
   const int n = 2 * fp.half;
@@ -1129,7 +1235,7 @@ void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, int 
   set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
   dim3 grid(noff, 6);
   filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
-                                                fp.step, fp.shift, fp.n1, fp.n2, nx, hx, hy, err,
+                                                fp.step, fp.shift, fp.n1, fp.n2, oc, hx, hy, err,
                                                 fixed_oi, fixed_oj, offs);
   check_launch("filter_design_kernel");
 }
@@ -1176,7 +1282,7 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
   double* dW = scratch<double>(6 * nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, 1, 1, hx, hy, dW, err, st, oi, oj);
+  design_filters(fb, fp, 1, OffsetCode{}, hx, hy, dW, err, st, oi, oj);
   int e = 0;
   EMIE_CUDA(cudaMemcpyAsync(w, dW, 6 * nw * sizeof(double), cudaMemcpyDeviceToHost, st));
   EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1185,6 +1291,39 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
   free_filter_bank(fb, st);
   raise_filter_errors(e);
   for (int m = fp.n1; m <= fp.n2; ++m) lam[m - fp.n1] = std::exp(m * fp.step + fp.shift);
+}
+
+void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                 const double* breaks, double hx, double hy, const FilterParams& fp, GreenParams& P,
+                 std::vector<Interval>& ivh);
+
+void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
+                     int n, const double* lam, cplx* out) {
+  if (nz < 1) fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition needs at least one interval");
+  if (n <= 0) return;
+  GreenParams P;
+  std::vector<Interval> ivh;
+  green_setup(1, 1, nz, omega, L, tops, sigma, breaks, 1.0, 1.0, FilterParams{}, P, ivh);
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  Interval* div = scratch<Interval>(nz, st);
+  double* dl = scratch<double>(n, st);
+  cplx* dout = scratch<cplx>(static_cast<size_t>(n) * 4 * nz * nz, st);
+  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemcpyAsync(dl, lam, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemsetAsync(dout, 0, static_cast<size_t>(n) * 4 * nz * nz * sizeof(cplx), st));
+  const int NL = L + 1;
+  const size_t smem = (static_cast<size_t>(P.LC) * (3 * NL + 11 * NL + kFields * nz)) * sizeof(cplx) +
+                      8 * static_cast<size_t>(P.LC) * sizeof(double) + static_cast<size_t>(P.LC) * 2 * nz * sizeof(int);
+  set_smem(reinterpret_cast<const void*>(vfunc_probe_kernel), smem);
+  vfunc_probe_kernel<<<ceil_div(n, P.LC), kGreenThreads, smem, st>>>(P, div, dl, n, dout);
+  check_launch("vfunc_probe_kernel");
+  EMIE_CUDA(cudaMemcpyAsync(out, dout, static_cast<size_t>(n) * 4 * nz * nz * sizeof(cplx), cudaMemcpyDeviceToHost,
+                            st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  release(div, st);
+  release(dl, st);
+  release(dout, st);
 }
 
 // The computed offsets of a build: all, or on a square grid with hx == hy only
@@ -1201,10 +1340,12 @@ std::vector<int> computed_offsets(int nx, int ny, double hx, double hy) {
 // Blocks of computed offsets [c0, c1) (positions in computed_offsets) into
 // `blocks` (nx*ny*nent complex, offset-major; other offsets untouched):
 // filter design (K6) and the lambda accumulation (K5).
-void greens_blocks(const Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
-                   double hx, double hy, const FilterParams& fp, int c0, int c1, cplx* blocks, cudaStream_t st) {
-  // ---- host validation: LayeredModel::validate, VerticalPartition::create,
-  // AnomalyGrid::validate (layered.cpp:53-65, 191-208; greens.cpp:18-35)
+// Host side of a build: model, partition and grid validation (LayeredModel::
+// validate, VerticalPartition::create, AnomalyGrid::validate: layered.cpp:53-65,
+// 191-208; greens.cpp:18-35), the kernel parameters and the interval table
+void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                 const double* breaks, double hx, double hy, const FilterParams& fp, GreenParams& P,
+                 std::vector<Interval>& ivh) {
   if (L < 1) fail(EMIE_CU_INVALID_ARGUMENT, "layered model needs at least one interface");
   if (L + 1 > kMaxLayers) fail(EMIE_CU_INVALID_ARGUMENT, "layered model: too many layers for the device build");
   for (int i = 0; i + 1 < L; ++i)
@@ -1215,26 +1356,25 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
     if (!std::isfinite(sigma[i].re) || !std::isfinite(sigma[i].im))
       fail(EMIE_CU_INVALID_ARGUMENT, "layered model: non-finite conductivity");
   if (!(hx > 0.0) || !(hy > 0.0)) fail(EMIE_CU_INVALID_ARGUMENT, "grid: cell sizes must be positive");
-  const int nz = op.nz;
   auto layer_of = [&](double z) {  // points on an interface belong below
     return static_cast<int>(std::upper_bound(tops, tops + L, z) - tops);
   };
   auto top_of = [&](int m) { return m == 0 ? tops[0] : tops[m - 1]; };
   auto bottom_of = [&](int m) { return m == L ? tops[L - 1] : tops[m]; };
-  GreenParams P{};
+  P = GreenParams{};
   P.L = L;
   P.nz = nz;
-  P.nx = op.nx;
-  P.ny = op.ny;
+  P.nx = nx;
+  P.ny = ny;
   P.hx = hx;
   P.hy = hy;
-  P.omega = op.omega;
+  P.omega = omega;
   P.nw = fp.n2 - fp.n1 + 1;
   P.step = fp.step;
   P.shift = fp.shift;
   P.n1 = fp.n1;
-  P.npairs = op.ntri;
-  P.nent = op.nent;
+  P.npairs = nz * (nz + 1) / 2;
+  P.nent = 2 * nz * (2 * nz + 1);
   for (int m = 0; m <= L; ++m) {
     P.thick[m] = bottom_of(m) - top_of(m);
     cplx s = sigma[m];
@@ -1248,7 +1388,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
     P.sig_up[m] = {up.real(), up.imag()};
     P.sig_dn[m] = {dn.real(), dn.imag()};
   }
-  std::vector<Interval> ivh(nz);
+  ivh.assign(nz, Interval{});
   for (int i = 0; i < nz; ++i) {
     if (!(breaks[i] < breaks[i + 1])) fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition: breaks must increase");
     const int m = layer_of(breaks[i]);
@@ -1281,22 +1421,23 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
     if (lcm >= 8) lcm &= ~7;  // multiples of 8: the per-chunk phases split evenly over the warps
     P.LC = lcm;
   }
+}
 
+// Filter design (K6) and lambda accumulation (K5) of the offsets offs_h
+// (codes of P.oc) into `blocks` (slot P.oc.slot(code, position) of nslots)
+void assemble_codes(const GreenParams& P, const std::vector<Interval>& ivh, const FilterParams& fp,
+                    const std::vector<int>& offs_h, int nslots, cplx* blocks, cudaStream_t st) {
   keep_pool_warm();
-  const int noff = op.nx * op.ny;
-  const std::vector<int> all = computed_offsets(op.nx, op.ny, hx, hy);
-  const int cb = std::max(0, std::min(c0, static_cast<int>(all.size())));
-  const int ce = c1 < 0 ? static_cast<int>(all.size()) : std::max(cb, std::min(c1, static_cast<int>(all.size())));
-  if (ce == cb) return;
-  const std::vector<int> offs_h(all.begin() + cb, all.begin() + ce);
+  const int nz = P.nz, L = P.L;
   const int ncomp = static_cast<int>(offs_h.size());
+  if (ncomp == 0) return;
   int* offs = scratch<int>(offs_h.size(), st);
   EMIE_CUDA(cudaMemcpyAsync(offs, offs_h.data(), offs_h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   FilterBank fb = make_filter_bank(fp, st);
-  double* W = scratch<double>(static_cast<size_t>(noff) * 6 * P.nw, st);
+  double* W = scratch<double>(static_cast<size_t>(nslots) * 6 * P.nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, ncomp, op.nx, hx, hy, W, err, st, INT32_MIN, 0, offs);
+  design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs);
 
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
@@ -1325,7 +1466,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   }();
   const bool pre = ls_mode < 0 ? groups > 1 : ls_mode == 1;
   if (!pre) {
-    assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0);
+    assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
     check_launch("assemble_kernel");
   } else {
     const int nchunk = ceil_div(P.nw, P.LC);
@@ -1339,7 +1480,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
       layer_state_kernel<<<lgrid, 128, 0, st>>>(P, offs + b0, nb, nchunk, LS);
       check_launch("layer_state_kernel");
       assemble_kernel<true><<<dim3(nb, groups), kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs + b0, LS,
-                                                                           nchunk);
+                                                                           nchunk, b0);
       check_launch("assemble_kernel");
     }
     release(LS, st);
@@ -1370,6 +1511,52 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
     raise_filter_errors(e);
     fail(EMIE_CU_DOMAIN_ERROR, "assemble_block: non-finite block entry");
   }
+}
+
+
+void greens_blocks(const Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
+                   double hx, double hy, const FilterParams& fp, int c0, int c1, cplx* blocks, cudaStream_t st) {
+  GreenParams P;
+  std::vector<Interval> ivh;
+  green_setup(op.nx, op.ny, op.nz, op.omega, L, tops, sigma, breaks, hx, hy, fp, P, ivh);
+  P.oc = OffsetCode{op.nx, 0, 0, 0};
+  const std::vector<int> all = computed_offsets(op.nx, op.ny, hx, hy);
+  const int cb = std::max(0, std::min(c0, static_cast<int>(all.size())));
+  const int ce = c1 < 0 ? static_cast<int>(all.size()) : std::max(cb, std::min(c1, static_cast<int>(all.size())));
+  if (ce == cb) return;
+  assemble_codes(P, ivh, fp, std::vector<int>(all.begin() + cb, all.begin() + ce), op.nx * op.ny, blocks, st);
+}
+
+// assemble_block (greens.hpp:129-135, greens.cpp:150-221) at n signed offsets
+// (|oi| < ny, |oj| < nx; out_of_range otherwise, greens.cpp:153-154) into host
+// blocks in request order, GreensBlock layout; no mirror or symmetrisation
+// (the reference evaluates every requested offset independently)
+void assemble_signed_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                          const double* breaks, double hx, double hy, const FilterParams& fp, int n, const int* oi,
+                          const int* oj, cplx* h_out) {
+  if (nx < 1 || ny < 1 || nz < 1) fail(EMIE_CU_INVALID_ARGUMENT, "grid: empty dimensions");
+  GreenParams P;
+  std::vector<Interval> ivh;
+  green_setup(nx, ny, nz, omega, L, tops, sigma, breaks, hx, hy, fp, P, ivh);
+  for (int i = 0; i < n; ++i)
+    if (std::abs(oi[i]) >= ny || std::abs(oj[i]) >= nx)
+      fail(EMIE_CU_OUT_OF_RANGE, "assemble_block: offset outside the grid");
+  if (n <= 0) return;
+  P.oc = OffsetCode{2 * nx - 1, ny - 1, nx - 1, 1};
+  std::vector<int> codes(n);
+  for (int i = 0; i < n; ++i) codes[i] = (oi[i] + ny - 1) * (2 * nx - 1) + (oj[i] + nx - 1);
+  cudaStream_t st = nullptr;
+  const size_t bytes = static_cast<size_t>(n) * P.nent * sizeof(cplx);
+  cplx* d = scratch<cplx>(static_cast<size_t>(n) * P.nent, st);
+  try {
+    assemble_codes(P, ivh, fp, codes, n, d, st);
+  } catch (...) {
+    release(d, st);
+    throw;
+  }
+  EMIE_CUDA(cudaMemcpyAsync(h_out, d, bytes, cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  release(d, st);
 }
 
 // The rest of the build once every computed offset's block is in `blocks`:

@@ -151,6 +151,11 @@ void kernel_output_host(int oi, int oj, double hx, double hy, int alpha, int bet
                         const double* s, int n, double* out);
 void design_offset_filters_host(int oi, int oj, double hx, double hy, const FilterParams& fp,
                                 double* w, double* lam);
+void assemble_signed_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                          const double* breaks, double hx, double hy, const FilterParams& fp, int n, const int* oi,
+                          const int* oj, cplx* h_out);
+void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
+                     int n, const double* lam, cplx* out);
 
 // launch configuration cached per (device, kernel, threads, dynamic SMEM)
 // (capi.cu): sets the SMEM opt-in once and returns the resident CTAs per SM;
