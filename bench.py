@@ -64,6 +64,51 @@ def parse():
     return p.parse_args()
 
 
+def host_cpu():
+    """Host cores for the CPU baselines (physical cores and the
+    lscpu model name): logical CPUs, physical cores, model."""
+    info = {"logical_cpus": os.cpu_count(), "physical_cores": None, "model": None}
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        cores = {tuple(r.split(",")) for r in out.splitlines() if r and not r.startswith("#")}
+        info["physical_cores"] = len(cores) or None
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.lower().startswith("model name"):
+                info["model"] = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    info["threads_used"] = info["physical_cores"] or info["logical_cpus"]
+    return info
+
+
+def config_of(args, cfg, freq=None):
+    """The workload dict both arms print (same keys and values)."""
+    return {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} (5-layer background), "
+                        "apply(SystemOperator) on both MT polarisations per step (nrhs=2)",
+            "nrhs": NRHS, "frequency_hz": cfg.freqs[0] if freq is None else freq,
+            "grid": [cfg.nx, cfg.ny, cfg.nz], "cell_m": [cfg.hx, cfg.hy],
+            "l2": f"inputs larger than L2 (the {spectra_gb(cfg):.2f} GB operator spectra are read every step)"}
+
+
+def spectra_gb(cfg):
+    """Size of the reference's spectral operator (toeplitz.cpp:86-90): quadrant
+    modes x 2nz(2nz+1) complex128."""
+    q = lambda n: smooth_embedding(2 * n - 1) // 2 + 1  # noqa: E731
+    return q(cfg.nx) * q(cfg.ny) * 2 * cfg.nz * (2 * cfg.nz + 1) * 16 / 1e9
+
+
+def smooth_embedding(n):  # toeplitz.cpp:18-26 (2,3,5-smooth), for the label only
+    m = max(1, n)
+    while True:
+        k = m
+        for f in (2, 3, 5):
+            while k % f == 0:
+                k //= f
+        if k == 1:
+            return m
+        m += 1
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -165,7 +210,8 @@ def run_reference(args):
         return 0
     from paper_1512_06126_b200 import configs
     cfg = configs.config(args.config)
-    threads = os.cpu_count()
+    cpu = host_cpu()
+    threads = cpu["threads_used"]
     d = reference_apply_rate(cfg, args.warmup + args.steps, threads=threads)
     times = d["times"][args.warmup:]
     tot = float(np.sum(times))
@@ -174,12 +220,14 @@ def run_reference(args):
         "impl": "reference", "metric": metric_for(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
-        "data": "synthetic (seeded config-3 conductivity; operator values synthetic, same shape)",
-        "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz}, apply(SystemOperator), 2 polarisations",
-                   "nrhs": NRHS, "threads": d["threads"]},
+        "data": "synthetic (seeded config conductivity field, seeded fields; the reference applies a "
+                "synthetic operator of the same shape -- its apply cost does not depend on the values)",
+        "config": config_of(args, cfg),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": d["threads"], "kind": "reference",
-                         "sample": f"{len(times)} steps x {NRHS} applies at cfg3 (reference apply, "
-                                   "OpenMP, FFTW-API shim)"},
+                         "host": cpu,
+                         "sample": f"{len(times)} steps x {NRHS} applies at cfg{args.config} (reference "
+                                   "apply(SystemOperator), OpenMP on the physical cores, FFTW-API shim: "
+                                   "no libfftw3 on the host)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     try:
@@ -442,10 +490,13 @@ def run_ours(args):
                 "peak_source": hbm_kind, "bytes_per_launch": bytes_ct}
     fp64_view = {"achieved": tflops, "peak": fp64.value, "unit": "TFLOP/s",
                  "frac": tflops / fp64.value if fp64.value else None,
-                 "peak_source": "emie_cu_probe_fp64 (max of a DFMA and a DMMA m8n8k4 loop, this GPU)",
+                 "peak_source": "emie_cu_probe_fp64 on this GPU (max of a DFMA and a DMMA m8n8k4 loop): "
+                                "MEASURED_PEAKS.json carries no FP64 figure",
                  "flops_per_launch": flops_ct,
                  "flops": "8 per complex multiply-add of the (3nz)^2 mode matrices, all ex*ey modes",
-                 "issued_dmma_frac": (0.75 * tflops / fp64.value) if (fp64.value and nz in (8, 16, 32, 48, 64)) else None}
+                 "issued_dmma_frac": (0.75 * tflops / fp64.value) if (fp64.value and nz in (8, 16, 32, 48, 64)) else None,
+                 "issued_dmma_frac_how": "derived: the 3-multiply complex form issues 6 of the 8 algorithmic "
+                                         "flops per complex MAC (ncu sm__pipe_fp64 active is in profiles/)"}
     tensor_bound = fp64.value and flops_ct / (fp64.value * 1e12) > bytes_ct / (hbm * 1e9)
     roofline = dict(bound="tensor" if tensor_bound else "hbm", kernel=ct_kernel,
                     **(fp64_view if tensor_bound else hbm_view),
@@ -459,19 +510,21 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            d = reference_apply_rate(cfg, 4, threads=os.cpu_count())
+            hc = host_cpu()
+            d = reference_apply_rate(cfg, 4, threads=hc["threads_used"])
             times = d["times"][1:]
             cpu = {"value": NRHS * len(times) / float(np.sum(times)), "unit": UNIT,
-                   "cores": d["threads"], "kind": "reference",
+                   "cores": d["threads"], "kind": "reference", "host": hc,
                    "sample": f"{len(times)} steps x {NRHS} applies of the reference apply(SystemOperator) "
-                             "at cfg3 shape (oracle/_ref, OpenMP, FFTW-API shim)"}
+                             f"at cfg{args.config} shape (oracle/_ref, OpenMP on the physical cores, "
+                             "FFTW-API shim: no libfftw3 on the host)"}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
     greens_cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            g = reference_greens_seconds(cfg, 16, threads=os.cpu_count())
+            g = reference_greens_seconds(cfg, 16, threads=host_cpu()["threads_used"])
             greens_cpu = {"value_s": g["extrapolated_s"], "cores": g["threads"], "kind": "reference",
                           "sample": f"assemble_block over every {g['stride']}th offset ({g['offsets']} of "
                                     f"{g['total_offsets']}, {g['seconds']:.2f} s), extrapolated linearly"}
@@ -484,13 +537,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded config-3 conductivity field, seeded fields)",
-            "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} (5-layer background), "
-                                   "apply(SystemOperator) on both "
-                                   "MT polarisations per step (nrhs=2)",
-                       "nrhs": NRHS, "frequency_hz": freq if world == 1 else "one config-5 frequency per rank",
-                       "operator": operator_src,
-                       "l2": f"inputs larger than L2 ({blocks_read * nent * 16 / 1e9:.2f} GB operator "
-                             "streamed per step)",
+            "config": config_of(args, cfg, freq if world == 1 else "one config-5 frequency per rank"),
+            "operator": operator_src,
+            "layout": {"operator_streamed_gb_per_step": round(blocks_read * nent_read * 16 / 1e9, 3),
                        "embedding": [sop.ex, sop.ey], "quadrant_modes": modes,
                        "contraction_blocks_read": blocks_read, "octant": octant},
             "solve": solve,
@@ -505,12 +554,17 @@ def run_ours(args):
             "stage_ms": stages,
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": NRHS * n * 16,
+            "e2e": {"value": e2e_call_value, "unit": UNIT, "h2d_bytes_per_step": NRHS * n * 16,
                     "d2h_bytes_per_step": NRHS * n * 16, "pcie_gbs": pcie,
-                    "how": f"emie_cu_apply_system_host over {K} steps x {NRHS} fields in one call "
-                           "(pinned host buffers; each field uploaded, applied, downloaded in the "
-                           "timed region; consecutive fields overlap on the copy engines)",
-                    "one_call_per_step": e2e_call_value},
+                    "how": f"one emie_cu_apply_system_host call per step ({K} steps): the step's {NRHS} "
+                           "polarisation fields uploaded from pinned host memory, applied, downloaded, "
+                           "all inside the timed region (FGMRES applies depend on each other, so steps "
+                           "do not overlap)",
+                    "streamed_independent_fields": {
+                        "value": e2e_value,
+                        "how": f"{K} steps x {NRHS} independent fields through one call, consecutive "
+                               "fields overlapping on the copy engines (throughput for independent "
+                               "sources, e.g. many right-hand sides; not a solve's dependent applies)"}},
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -666,10 +720,33 @@ def run_strong(args):
     return 0
 
 
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: launch the N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1; N above the visible
+    device count is an error (EMIE_BENCH_BACKEND=gloo allows a dry run of the
+    multi-rank path on fewer GPUs)."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if args.gpus > have and os.environ.get("EMIE_BENCH_BACKEND", "nccl") == "nccl":
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.strong:
         return run_strong(args)
     return run_ours(args)

@@ -136,6 +136,12 @@ int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int b
 int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, const double* breaks,
                        double omega, int n, const double* h_lam, double* h_out);
 
+/* dense_reference_apply (include/emie/toeplitz.hpp:47, src/toeplitz.cpp:285-312):
+ * the O(N^2) direct block-Toeplitz apply of host compressed blocks (the
+ * emie_cu_operator_from_blocks layout) to one host field, on the device, in a
+ * fixed summation order; the oracle the reference tests the FFT apply against */
+int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_blocks, const double* h_in, double* h_out);
+
 void emie_cu_operator_destroy(emie_cu_operator op);
 
 /* apply(const SpectralOperator&, const GridVector&) (toeplitz.hpp:43,
@@ -205,6 +211,36 @@ int emie_cu_profile_collect(double* ms, long long* count, int n);
  * (mma.sync m8n8k4 f64) kernel on the device, TFLOP/s (denominator of the
  * FP64 roofline, which MEASURED_PEAKS.json does not carry) */
 int emie_cu_probe_fp64(double* tflops, void* stream);
+
+/* live iteration hook (SolverConfig::on_iteration, cie.hpp:52, 58): called
+ * with the right-hand side index, the iteration count and the residual
+ * estimate exactly where the reference calls it (cie.cpp:178-185, 199-201) */
+typedef void (*emie_cu_iter_fn)(void* ctx, int rhs, int iteration, double residual);
+
+/* a linear map or preconditioner for emie_cu_fgmres_map: out = A(in), n complex
+ * entries; returns 0 or a nonzero status code (the solve stops with that status) */
+typedef int (*emie_cu_map_fn)(void* ctx, const double* in, double* out, long long n, void* stream);
+
+/* emie_cu_fgmres / emie_cu_fgmres_host with the live iteration hook (hook may be NULL) */
+int emie_cu_fgmres_ex(emie_cu_system sys, const double* d_rhs, double* d_x, int nrhs, double tol,
+                      int restart, int max_iters, emie_cu_report* reports, double* h_history,
+                      int hist_cap, emie_cu_iter_fn hook, void* hook_ctx, void* stream);
+int emie_cu_fgmres_host_ex(emie_cu_system sys, const double* h_rhs, double* h_x, int nrhs, double tol,
+                           int restart, int max_iters, emie_cu_report* reports, double* h_history,
+                           int hist_cap, emie_cu_iter_fn hook, void* hook_ctx, void* stream);
+
+/* fgmres(const LinearMap&, rhs, SolverConfig) (cie.hpp:71-72, cie.cpp:117-238)
+ * over a caller-supplied map: the Krylov basis, the CGS2 orthogonalisation and
+ * every vector operation stay on the device, the map (and the optional
+ * flexible right preconditioner, SolverConfig::right_precond) is called once
+ * per step. host_vectors != 0: rhs, x and the callbacks' vectors are host
+ * memory (the library stages them); else device memory, the callbacks run
+ * stream-ordered on `stream`. One right-hand side; report/history as
+ * emie_cu_fgmres. */
+int emie_cu_fgmres_map(long long n, int host_vectors, emie_cu_map_fn apply, void* apply_ctx,
+                       emie_cu_map_fn precond, void* precond_ctx, emie_cu_iter_fn hook, void* hook_ctx,
+                       const double* rhs, double* x, double tol, int restart, int max_iters,
+                       emie_cu_report* report, double* h_history, int hist_cap, void* stream);
 
 /* same with host right-hand sides and solutions */
 int emie_cu_fgmres_host(emie_cu_system sys, const double* h_rhs, double* h_x, int nrhs,
@@ -342,8 +378,13 @@ int emie_cu_contract_modes_peer(emie_cu_operator op, const double* d_S, int nrhs
  * peers' flag arrays mapped into this process) */
 int emie_cu_peer_signal(int* const* h_flag_ptrs, int G, int me, int epoch, void* stream);
 /* before this stream reads its buffer: wait until all G slots of d_flags
- * reach epoch (bounded: traps the context if a peer never signals) */
+ * reach epoch (bounded: after ~30 s without a peer's signal the wait gives
+ * up and sets a sticky timeout flag; later waits return at once) */
 int emie_cu_peer_wait(const int* d_flags, int G, int epoch, void* stream);
+/* synchronise the device, then report (*timed_out = 1) and clear the sticky
+ * timeout flag of the peer waits: a sharded apply whose exchange timed out
+ * produced no valid result */
+int emie_cu_peer_status(int* timed_out);
 
 /* kernel launches issued by this library on the calling thread since the
  * last reset (evidence for bench.py's gpu_launches) */

@@ -83,6 +83,51 @@ def reference_blocks(tops, sigma, breaks, nx, ny, hx, hy, omega, offs) -> dict:
     return {"ref": a["base"], "hx+": a["hx+"], "hy+": a["hy+"], "fma": b["base"]}
 
 
+def _chain_here(case: dict) -> dict:
+    """The reference pipeline of one case: assemble_operator +
+    transform_operator + build_system (ref_build), then solve_cie for each
+    right-hand side (cie.cpp:240-249)."""
+    sys.path.insert(0, str(HERE))
+    import ref_binding as R
+    c = R.RefCase(case["tops"], case["sigma"], case["breaks"], int(case["nx"]), int(case["ny"]), float(case["hx"]),
+                  float(case["hy"]), float(case["omega"]), case["sigma_a"])
+    blocks, _, _ = c.build()
+    xs, its = [], []
+    for b in case["rhs"]:
+        x, rep = c.solve(b, float(case["tol"]), int(case["restart"]), int(case["max_iters"]))
+        xs.append(x)
+        its.append(rep["iterations"])
+    out = {"x": np.stack(xs), "iters": np.array(its)}
+    if int(case["want_blocks"]):
+        out["blocks"] = blocks
+    return out
+
+
+def reference_chain(tops, sigma, breaks, nx, ny, hx, hy, omega, sigma_a, rhs, tol, restart=40, max_iters=500,
+                    variants=("_ref", "_ref_fma"), want_blocks=False) -> dict:
+    """{variant: {"x": solutions (nrhs, n), "iters": (nrhs,)[, "blocks"]}} of
+    the reference's own build + solve, one child process per variant."""
+    with tempfile.TemporaryDirectory() as d:
+        cpath = Path(d) / "case.npz"
+        np.savez(cpath, tops=np.asarray(tops, np.float64), sigma=np.asarray(sigma, np.complex128),
+                 breaks=np.asarray(breaks, np.float64), nx=nx, ny=ny, hx=hx, hy=hy, omega=omega,
+                 sigma_a=np.asarray(sigma_a, np.complex128).reshape(-1), rhs=np.asarray(rhs, np.complex128),
+                 tol=tol, restart=restart, max_iters=max_iters, want_blocks=int(want_blocks))
+        procs = []
+        for v in variants:
+            env = dict(os.environ, EMIE_REF_VARIANT=v)
+            procs.append((v, subprocess.Popen([sys.executable, str(Path(__file__)), str(cpath),
+                                               str(Path(d) / f"{v}.npz"), "chain"], env=env,
+                                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+        res = {}
+        for v, p in procs:
+            out, _ = p.communicate(timeout=7200)
+            if p.returncode != 0:
+                raise RuntimeError(f"reference variant {v} failed:\n{out.decode()}")
+            res[v] = dict(np.load(Path(d) / f"{v}.npz"))
+    return res
+
+
 def envelope(blocks: dict) -> np.ndarray:
     """Per-block envelope: the largest move of the reference under the
     variants, relative to the block's max modulus."""
@@ -94,5 +139,5 @@ def envelope(blocks: dict) -> np.ndarray:
 
 if __name__ == "__main__":
     case = dict(np.load(sys.argv[1]))
-    res = _blocks_here(case, sys.argv[3])
+    res = _chain_here(case) if sys.argv[3] == "chain" else _blocks_here(case, sys.argv[3])
     np.savez(sys.argv[2], **res)

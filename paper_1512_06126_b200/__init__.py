@@ -128,6 +128,11 @@ def lib():
         "emie_cu_fgmres": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                            ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
         "emie_cu_device_count": [ip],
+        "emie_cu_fgmres_ex": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                              ctypes.POINTER(_Report), vp, ctypes.c_int, vp, vp, vp],
+        "emie_cu_fgmres_map": [ctypes.c_longlong, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_double,
+                               ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
+        "emie_cu_dense_apply": [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp],
         "emie_cu_assemble_blocks": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, ctypes.c_int, vp, vp, vp],
         "emie_cu_vfunctions": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_double, ctypes.c_int, vp, vp],
@@ -150,6 +155,7 @@ def lib():
         "emie_cu_ipc_close": [vp],
         "emie_cu_peer_signal": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_peer_wait": [vp, ctypes.c_int, ctypes.c_int, vp],
+        "emie_cu_peer_status": [ip],
         "emie_cu_lateral_forward_peer": [vp, vp, vp, vp, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_lateral_forward_peer_supported": [vp, ip],
@@ -619,6 +625,11 @@ def apply(op, v, out=None):
             raise InvalidArgument("apply: device fields must be contiguous complex128 CUDA tensors")
         if out is None:
             out = torch.empty_like(v)
+        elif (not _is_torch(out) or out.dtype != torch.complex128 or not out.is_cuda or not out.is_contiguous()
+              or out.numel() != v.numel() or out.device != v.device):
+            raise InvalidArgument("apply: out must be a contiguous complex128 CUDA tensor shaped like the field")
+        if out.data_ptr() == v.data_ptr():
+            raise InvalidArgument("apply: out may not alias the input field")
         fn = L.emie_cu_apply_system if isinstance(op, SystemOperator) else L.emie_cu_apply_spectral
         _check(fn(op.handle, ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(out.data_ptr()), nrhs,
                   _stream_of()))
@@ -639,6 +650,9 @@ def apply_host(sys: SystemOperator, v: np.ndarray, out: Optional[np.ndarray] = N
     nrhs = _field_shape_check(x, sys.b.nx * sys.b.ny * sys.b.nz, "system")
     if out is None:
         out = np.empty_like(x)
+    elif (not isinstance(out, np.ndarray) or out.dtype != np.complex128 or not out.flags.c_contiguous
+          or out.size != x.size):
+        raise InvalidArgument("apply_host: out must be a C-contiguous complex128 array of the field's size")
     _check(lib().emie_cu_apply_system_host(sys.handle, _ptr(x), _ptr(out), nrhs, _stream_of()))
     return out
 
@@ -646,10 +660,15 @@ def apply_host(sys: SystemOperator, v: np.ndarray, out: Optional[np.ndarray] = N
 # ----------------------------------------------------------------- solve ---
 @dataclass
 class SolverConfig:
-    """include/emie/cie.hpp:53-59 (the device path has no preconditioner hook)."""
+    """include/emie/cie.hpp:53-59. right_precond: optional flexible right
+    preconditioner, a callable numpy field -> numpy field (the solve then
+    runs over host callbacks); on_iteration(iteration, residual): called live
+    where the reference calls it (cie.cpp:178-185, 199-201)."""
     tol: float = 1e-8
     restart: int = 40
     max_iters: int = 500
+    right_precond: Optional[Callable] = None
+    on_iteration: Optional[Callable] = None
 
 
 @dataclass
@@ -676,10 +695,13 @@ def fgmres_system(sys: SystemOperator, rhs, config: SolverConfig = SolverConfig(
     reps = (_Report * nrhs)()
     cap = max(1, config.max_iters + 1)
     hist = np.zeros((nrhs, cap), np.float64)
-    _check(lib().emie_cu_fgmres(sys.handle, ctypes.c_void_p(d_rhs.data_ptr()),
-                                ctypes.c_void_p(d_x.data_ptr()), nrhs, float(config.tol),
-                                int(config.restart), int(config.max_iters), reps, _ptr(hist), cap,
-                                _stream_of()))
+    hook, errs = _iteration_hook(config.on_iteration, per_rhs=nrhs > 1)
+    rc = lib().emie_cu_fgmres_ex(sys.handle, ctypes.c_void_p(d_rhs.data_ptr()), ctypes.c_void_p(d_x.data_ptr()),
+                                 nrhs, float(config.tol), int(config.restart), int(config.max_iters), reps,
+                                 _ptr(hist), cap, hook, None, _stream_of())
+    if errs:
+        raise errs[0]
+    _check(rc)
     out = []
     for i in range(nrhs):
         r = reps[i]
@@ -689,9 +711,78 @@ def fgmres_system(sys: SystemOperator, rhs, config: SolverConfig = SolverConfig(
     return x, out
 
 
+_ITER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double)
+_MAP_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                           ctypes.c_void_p)
+
+
+def _iteration_hook(fn, per_rhs=False):
+    """C callback for SolverConfig.on_iteration; exceptions are kept and
+    re-raised after the call (no exception crosses the ABI)."""
+    errs = []
+    if fn is None:
+        return None, errs
+
+    def cb(_ctx, rhs, it, res):
+        if errs:
+            return
+        try:
+            fn(rhs, it, res) if per_rhs else fn(it, res)
+        except BaseException as e:  # noqa: BLE001 - re-raised by the caller
+            errs.append(e)
+    return _ITER_FN(cb), errs
+
+
+def _host_map(fn, shape, errs):
+    def cb(_ctx, src, dst, n, _stream):
+        try:
+            x = np.ctypeslib.as_array(ctypes.cast(src, ctypes.POINTER(ctypes.c_double)), (2 * n,))
+            y = np.asarray(fn(x.view(np.complex128).reshape(shape).copy()), dtype=np.complex128)
+            if y.size != n:
+                raise InvalidArgument("fgmres: linear map changed the field size")
+            ctypes.memmove(dst, np.ascontiguousarray(y).ctypes.data, 16 * n)
+            return 0
+        except BaseException as e:  # noqa: BLE001 - re-raised by the caller
+            errs.append(e)
+            return 4
+    return _MAP_FN(cb)
+
+
+def fgmres(apply_a: Callable, rhs, config: SolverConfig = SolverConfig()):
+    """fgmres(const LinearMap&, rhs, SolverConfig) (cie.hpp:71-72,
+    cie.cpp:117-238) over a Python callable numpy field -> numpy field: the
+    Krylov iteration runs on the device (emie_cu_fgmres_map), the map and the
+    optional right preconditioner are called once per step on host copies.
+    -> (x, SolveReport)."""
+    x0 = _c128(rhs)
+    n = x0.size
+    if n == 0:
+        raise InvalidArgument("fgmres: empty right-hand side")
+    errs = []
+    amap = _host_map(apply_a, x0.shape, errs)
+    pmap = _host_map(config.right_precond, x0.shape, errs) if config.right_precond else None
+    hook, herrs = _iteration_hook(config.on_iteration)
+    x = np.zeros_like(x0)
+    rep = _Report()
+    cap = max(1, config.max_iters + 1)
+    hist = np.zeros(cap, np.float64)
+    rc = lib().emie_cu_fgmres_map(n, 1, amap, None, pmap, None, hook, None, _ptr(x0), _ptr(x), float(config.tol),
+                                  int(config.restart), int(config.max_iters), ctypes.byref(rep), _ptr(hist), cap,
+                                  None)
+    for e in errs + herrs:
+        raise e
+    _check(rc)
+    return x, SolveReport(_STATUS.get(rep.status, "?"), rep.iterations, rep.residual,
+                          list(hist[:min(rep.history_len, cap)]))
+
+
 def solve_cie(grid: AnomalyGrid, model: LayeredModel, op: SpectralOperator, rhs,
               config: SolverConfig = SolverConfig()):
-    """include/emie/cie.hpp:77-80 (src/cie.cpp:240-249) -> (U, [SolveReport])."""
+    """include/emie/cie.hpp:77-80 (src/cie.cpp:240-249) -> (U, [SolveReport]).
+    With config.right_precond the solve runs over host callbacks (fgmres)."""
     grid.validate(model)
     sys = build_system(grid, op)
+    if config.right_precond is not None:
+        x, rep = fgmres(lambda u: apply_host(sys, u), rhs, config)
+        return x, [rep]
     return fgmres_system(sys, rhs, config)

@@ -6,13 +6,16 @@
 //
 // Host-side code here is the API glue the reference also does on the host:
 // argument validation with the reference's exception types, layout
-// conversions, the EMG1 snapshot I/O (greens.cpp:373-446), and two test
-// helpers the reference itself ships as oracles (dense_reference_apply,
-// toeplitz.cpp:285-312; fetch_block, greens.cpp:295-330).
+// conversions, the signed-offset reconstruction fetch_block (greens.cpp:
+// 295-330) and the EMG1 snapshot I/O (greens.cpp:373-446). Everything that
+// computes — the Green's build, spectra, applies, the dense oracle apply and
+// FGMRES (also over caller-supplied maps) — runs on the device.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <functional>
 #include <fstream>
 #include <mutex>
 #include <stdexcept>
@@ -172,29 +175,45 @@ CompressedGreensOperator compress(int nx, int ny, std::vector<GreensBlock> block
   return op;
 }
 
+// Signed-offset reconstruction (greens.hpp:83-99; Lemma 2 of the paper): each
+// of the nine components is a stored component, possibly transposed in the
+// interval indices, times +-1 from the offset signs. Table row q = 3a + b:
+// source component, parity in the x offset, parity in the y offset, and
+// whether it is the negative transpose of a stored full component.
+namespace {
+struct ComponentRule {
+  int src;   // 0 xx, 1 yy, 2 zz, 3 xy (triangles), 4 xz, 5 yz (full)
+  int px, py;
+  bool neg_transpose;
+};
+constexpr ComponentRule kRules[9] = {
+    {0, 0, 0, false}, {3, 1, 1, false}, {4, 1, 0, false},  // xx xy xz
+    {3, 1, 1, false}, {1, 0, 0, false}, {5, 0, 1, false},  // yx yy yz
+    {4, 1, 0, true},  {5, 0, 1, true},  {2, 0, 0, false},  // zx zy zz
+};
+}  // namespace
+
 FullBlock fetch_block(const CompressedGreensOperator& op, int oi, int oj) {
   if (std::abs(oi) >= op.ny || std::abs(oj) >= op.nx) throw std::out_of_range("fetch_block: offset out of range");
   const GreensBlock& b = op.stored(std::abs(oi), std::abs(oj));
   const int nz = op.nz;
-  const double sx = oj < 0 ? -1.0 : 1.0, sy = oi < 0 ? -1.0 : 1.0;
+  const std::vector<cdouble>* comps[6] = {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz};
   FullBlock f;
   f.nz = nz;
-  for (auto& q : f.q) q.assign(std::size_t(nz) * nz, cdouble(0.0));
-  for (int k = 0; k < nz; ++k)
-    for (int kp = 0; kp < nz; ++kp) {
-      const std::size_t i = std::size_t(k) * nz + kp, t = GreensBlock::tri(std::min(k, kp), std::max(k, kp), nz);
-      f.q[0][i] = b.xx[t];
-      f.q[4][i] = b.yy[t];
-      f.q[8][i] = b.zz[t];
-      f.q[1][i] = f.q[3][i] = sx * sy * b.xy[t];
-      f.q[2][i] = sx * b.xz[i];
-      f.q[5][i] = sy * b.yz[i];
-    }
-  for (int k = 0; k < nz; ++k)
-    for (int kp = 0; kp < nz; ++kp) {
-      f.q[6][std::size_t(k) * nz + kp] = -f.q[2][std::size_t(kp) * nz + k];
-      f.q[7][std::size_t(k) * nz + kp] = -f.q[5][std::size_t(kp) * nz + k];
-    }
+  for (int q = 0; q < 9; ++q) {
+    const ComponentRule& r = kRules[q];
+    const double sign = ((r.px && oj < 0) != (r.py && oi < 0) ? -1.0 : 1.0) * (r.neg_transpose ? -1.0 : 1.0);
+    const std::vector<cdouble>& src = *comps[r.src];
+    std::vector<cdouble>& dst = f.q[q];
+    dst.resize(std::size_t(nz) * nz);
+    for (int k = 0; k < nz; ++k)
+      for (int kp = 0; kp < nz; ++kp) {
+        std::size_t i;
+        if (r.src < 4) i = GreensBlock::tri(std::min(k, kp), std::max(k, kp), nz);
+        else i = r.neg_transpose ? std::size_t(kp) * nz + k : std::size_t(k) * nz + kp;
+        dst[std::size_t(k) * nz + kp] = sign * src[i];
+      }
+  }
   return f;
 }
 
@@ -355,26 +374,15 @@ GridVector apply(const SpectralOperator& sop, const GridVector& v) {
 }
 
 GridVector dense_reference_apply(const CompressedGreensOperator& op, const GridVector& v) {
-  // O(N^2) oracle, guarded to 4096 cells as in the reference
-  const int nx = op.nx, ny = op.ny, nz = op.nz;
-  const std::size_t cells = std::size_t(nx) * ny * nz;
+  // the O(N^2) oracle (toeplitz.cpp:285-312) runs on the device
+  // (emie_cu_dense_apply); same 4096-cell guard and errors
+  const std::size_t cells = std::size_t(op.nx) * op.ny * op.nz;
   if (cells > 4096) throw std::invalid_argument("dense_reference_apply: grid too large");
-  if (v.nx != nx || v.ny != ny || v.nz != nz || v.size() != 3 * cells)
+  if (v.nx != op.nx || v.ny != op.ny || v.nz != op.nz || v.size() != 3 * cells)
     throw std::invalid_argument("dense_reference_apply: field shape");
-  GridVector out(nx, ny, nz);
-  for (int oi = -(ny - 1); oi < ny; ++oi)
-    for (int oj = -(nx - 1); oj < nx; ++oj) {
-      const FullBlock f = fetch_block(op, oi, oj);
-      for (int iy = std::max(0, oi); iy < std::min(ny, ny + oi); ++iy)
-        for (int ix = std::max(0, oj); ix < std::min(nx, nx + oj); ++ix)
-          for (int a = 0; a < 3; ++a)
-            for (int k = 0; k < nz; ++k) {
-              cdouble acc = 0.0;
-              for (int b = 0; b < 3; ++b)
-                for (int kp = 0; kp < nz; ++kp) acc += f.at(a, b, k, kp) * v.at(b, kp, iy - oi, ix - oj);
-              out.at(a, k, iy, ix) += acc;
-            }
-    }
+  const std::vector<cdouble> packed = pack_blocks(op);
+  GridVector out(op.nx, op.ny, op.nz);
+  check(emie_cu_dense_apply(op.nx, op.ny, op.nz, dbl(packed.data()), dbl(v.a.data()), dbl(out.a.data())));
   return out;
 }
 
@@ -414,154 +422,99 @@ GridVector apply(const SystemOperator& sys, const GridVector& u) {
   return out;
 }
 
-// Flexible restarted GMRES for a caller-supplied host map (cie.cpp:117-238
-// interface). The operator work happens in the map; for the CIE system use
-// solve_cie, which runs the whole iteration on the device.
+// fgmres over a caller-supplied host LinearMap (cie.hpp:71-72): the solver
+// itself (Krylov basis, CGS2 orthogonalisation, Givens least squares, restarts)
+// is the device FGMRES of emie_cu_fgmres_map; the library stages each basis
+// vector to the host, calls the map (and SolverConfig::right_precond, the
+// flexible preconditioner) and uploads the result. on_iteration is called
+// live from the solver. An exception thrown by a callback stops the solve and
+// is rethrown here unchanged.
+namespace {
+struct HostMapCtx {
+  const std::function<GridVector(const GridVector&)>* f;
+  int nx, ny, nz;
+  std::exception_ptr err;
+};
+int host_map_trampoline(void* ctx, const double* in, double* out, long long n, void*) {
+  auto* c = static_cast<HostMapCtx*>(ctx);
+  try {
+    GridVector v(c->nx, c->ny, c->nz);
+    std::memcpy(v.a.data(), in, std::size_t(n) * sizeof(cdouble));
+    const GridVector w = (*c->f)(v);
+    if (w.a.size() != std::size_t(n)) throw std::invalid_argument("fgmres: linear map changed the field size");
+    std::memcpy(out, w.a.data(), std::size_t(n) * sizeof(cdouble));
+    return 0;
+  } catch (...) {
+    c->err = std::current_exception();
+    return EMIE_CU_RUNTIME_ERROR;
+  }
+}
+struct HookCtx {
+  const IterationHook* f;
+  std::exception_ptr err;
+};
+void hook_trampoline(void* ctx, int, int iteration, double residual) {
+  auto* c = static_cast<HookCtx*>(ctx);
+  if (c->err) return;
+  try {
+    (*c->f)(iteration, residual);
+  } catch (...) {
+    c->err = std::current_exception();
+  }
+}
+void fill_report(SolveReport& rep, const emie_cu_report& r, const std::vector<double>& hist) {
+  rep.status = static_cast<SolveStatus>(r.status);
+  rep.iterations = r.iterations;
+  rep.residual = r.residual;
+  rep.history.assign(hist.begin(), hist.begin() + std::min<int>(r.history_len, int(hist.size())));
+}
+}  // namespace
+
 FgmresResult fgmres(const LinearMap& A, const GridVector& rhs, const SolverConfig& cfg) {
   if (!(cfg.tol > 0.0) || cfg.restart < 1 || cfg.max_iters < 1)
     throw std::invalid_argument("fgmres: bad solver configuration");
-  auto dot = [](const GridVector& u, const GridVector& v) {
-    cdouble s = 0.0;
-    for (std::size_t i = 0; i < u.a.size(); ++i) s += std::conj(u.a[i]) * v.a[i];
-    return s;
-  };
-  auto nrm = [](const GridVector& u) {
-    double s = 0.0;
-    for (const auto& c : u.a) s += std::norm(c);
-    return std::sqrt(s);
-  };
   FgmresResult res;
   res.x = GridVector(rhs.nx, rhs.ny, rhs.nz);
-  const double bnorm = nrm(rhs);
-  if (bnorm == 0.0) {
-    res.report.status = SolveStatus::converged;
-    return res;
-  }
-  const int m = cfg.restart;
-  GridVector r = rhs;
-  double rnorm = bnorm;
-  int iter = 0;
-  bool broke = false;
-  while (iter < cfg.max_iters) {
-    std::vector<GridVector> V, Z;
-    V.push_back(r);
-    for (auto& c : V[0].a) c *= 1.0 / rnorm;
-    std::vector<cdouble> h(std::size_t(m + 1) * m), g(m + 1), sn(m);
-    std::vector<double> cs(m);
-    g[0] = rnorm;
-    int cols = 0;
-    for (int j = 0; j < m && iter < cfg.max_iters; ++j) {
-      ++iter;
-      cdouble* hj = h.data() + std::size_t(j) * (m + 1);
-      GridVector w;
-      if (cfg.right_precond) {
-        Z.push_back(cfg.right_precond(V[j]));
-        w = A(Z.back());
-      } else {
-        w = A(V[j]);
-      }
-      const double wn0 = nrm(w);
-      for (int pass = 0; pass < 2; ++pass)
-        for (int i = 0; i <= j; ++i) {
-          const cdouble hc = dot(V[i], w);
-          for (std::size_t e = 0; e < w.a.size(); ++e) w.a[e] -= hc * V[i].a[e];
-          hj[i] += hc;
-        }
-      const double hnext = nrm(w);
-      for (int i = 0; i < j; ++i) {
-        const cdouble t = cs[i] * hj[i] + sn[i] * hj[i + 1];
-        hj[i + 1] = -std::conj(sn[i]) * hj[i] + cs[i] * hj[i + 1];
-        hj[i] = t;
-      }
-      if (hnext <= 1e-13 * std::max(wn0, 1e-300)) {
-        double colmax = hnext;
-        for (int i = 0; i <= j; ++i) colmax = std::max(colmax, std::abs(hj[i]));
-        if (std::abs(hj[j]) > 1e-13 * std::max(colmax, 1e-300)) {
-          cols = j + 1;
-        } else {
-          cols = j;
-          broke = true;
-          res.report.history.push_back(rnorm / bnorm);
-          if (cfg.on_iteration) cfg.on_iteration(iter, rnorm / bnorm);
-        }
-        break;
-      }
-      hj[j + 1] = hnext;
-      V.push_back(w);
-      for (auto& c : V.back().a) c *= 1.0 / hnext;
-      const cdouble f = hj[j];
-      if (f == 0.0) {
-        cs[j] = 0.0;
-        sn[j] = 1.0;
-      } else {
-        const double t = std::sqrt(std::norm(f) + hnext * hnext);
-        cs[j] = std::abs(f) / t;
-        sn[j] = f / std::abs(f) * hnext / t;
-      }
-      hj[j] = cs[j] * hj[j] + sn[j] * hj[j + 1];
-      hj[j + 1] = 0.0;
-      g[j + 1] = -std::conj(sn[j]) * g[j];
-      g[j] = cs[j] * g[j];
-      cols = j + 1;
-      const double est = std::abs(g[j + 1]) / bnorm;
-      res.report.history.push_back(est);
-      if (cfg.on_iteration) cfg.on_iteration(iter, est);
-      if (est <= cfg.tol) break;
-    }
-    std::vector<cdouble> y(cols);
-    for (int k = cols - 1; k >= 0; --k) {
-      cdouble acc = g[k];
-      for (int l = k + 1; l < cols; ++l) acc -= h[std::size_t(l) * (m + 1) + k] * y[l];
-      y[k] = acc / h[std::size_t(k) * (m + 1) + k];
-    }
-    for (int k = 0; k < cols; ++k) {
-      const GridVector& d = cfg.right_precond ? Z[k] : V[k];
-      for (std::size_t e = 0; e < d.a.size(); ++e) res.x.a[e] += y[k] * d.a[e];
-    }
-    GridVector rt = A(res.x);
-    for (std::size_t e = 0; e < rt.a.size(); ++e) rt.a[e] = rhs.a[e] - rt.a[e];
-    rnorm = nrm(rt);
-    r = std::move(rt);
-    if (rnorm / bnorm <= cfg.tol) {
-      res.report.status = SolveStatus::converged;
-      break;
-    }
-    if (broke) {
-      res.report.status = SolveStatus::breakdown;
-      break;
-    }
-  }
-  if (broke && rnorm / bnorm <= cfg.tol) res.report.status = SolveStatus::converged;
-  res.report.iterations = iter;
-  res.report.residual = rnorm / bnorm;
+  HostMapCtx actx{&A, rhs.nx, rhs.ny, rhs.nz, nullptr};
+  HostMapCtx pctx{&cfg.right_precond, rhs.nx, rhs.ny, rhs.nz, nullptr};
+  HookCtx hctx{&cfg.on_iteration, nullptr};
+  emie_cu_report rep{};
+  std::vector<double> hist(std::size_t(cfg.max_iters) + 1);
+  const int rc = emie_cu_fgmres_map(static_cast<long long>(rhs.size()), 1, host_map_trampoline, &actx,
+                                    cfg.right_precond ? host_map_trampoline : nullptr, &pctx,
+                                    cfg.on_iteration ? hook_trampoline : nullptr, &hctx, dbl(rhs.a.data()),
+                                    dbl(res.x.a.data()), cfg.tol, cfg.restart, cfg.max_iters, &rep, hist.data(),
+                                    static_cast<int>(hist.size()), nullptr);
+  for (const std::exception_ptr& e : {actx.err, pctx.err, hctx.err})
+    if (e) std::rethrow_exception(e);
+  check(rc);
+  fill_report(res.report, rep, hist);
   return res;
 }
 
 GridVector solve_cie(const AnomalyGrid& grid, const LayeredModel& model, const SpectralOperator& op,
                      const GridVector& rhs, const SolverConfig& cfg, SolveReport* report) {
   grid.validate(model);
-  if (cfg.right_precond) {  // flexible preconditioning needs the host-callback solver
-    const SystemOperator sys = build_system(grid, op);
+  const SystemOperator sys = build_system(grid, op);
+  if (cfg.right_precond) {  // a host preconditioner: the map solver with apply(sys, .) as the operator
     FgmresResult r = fgmres([&](const GridVector& u) { return apply(sys, u); }, rhs, cfg);
     if (report) *report = std::move(r.report);
     return std::move(r.x);
   }
   if (!(cfg.tol > 0.0) || cfg.restart < 1 || cfg.max_iters < 1)
     throw std::invalid_argument("fgmres: bad solver configuration");
-  const SystemOperator sys = build_system(grid, op);
+  if (rhs.nx != op.nx || rhs.ny != op.ny || rhs.nz != op.nz)
+    throw std::invalid_argument("apply: field shape does not match system");
   GridVector x(rhs.nx, rhs.ny, rhs.nz);
   emie_cu_report rep{};
   std::vector<double> hist(std::size_t(cfg.max_iters) + 1);
-  check(emie_cu_fgmres_host(sys.device->h, dbl(rhs.a.data()), dbl(x.a.data()), 1, cfg.tol, cfg.restart,
-                            cfg.max_iters, &rep, hist.data(), static_cast<int>(hist.size()), nullptr));
-  if (report) {
-    report->status = static_cast<SolveStatus>(rep.status);
-    report->iterations = rep.iterations;
-    report->residual = rep.residual;
-    report->history.assign(hist.begin(), hist.begin() + std::min<int>(rep.history_len, int(hist.size())));
-    if (cfg.on_iteration)
-      for (std::size_t i = 0; i < report->history.size(); ++i) cfg.on_iteration(int(i) + 1, report->history[i]);
-  }
+  HookCtx hctx{&cfg.on_iteration, nullptr};
+  const int rc = emie_cu_fgmres_host_ex(sys.device->h, dbl(rhs.a.data()), dbl(x.a.data()), 1, cfg.tol, cfg.restart,
+                                        cfg.max_iters, &rep, hist.data(), static_cast<int>(hist.size()),
+                                        cfg.on_iteration ? hook_trampoline : nullptr, &hctx, nullptr);
+  if (hctx.err) std::rethrow_exception(hctx.err);
+  check(rc);
+  if (report) fill_report(*report, rep, hist);
   return x;
 }
 

@@ -869,6 +869,13 @@ int emie_cu_peer_signal(int* const* h_flag_ptrs, int G, int me, int epoch, void*
   return guarded([&] { peer_signal(h_flag_ptrs, G, me, epoch, as_stream(stream)); });
 }
 
+extern "C" int emie_cu_peer_status(int* timed_out) {
+  return guarded([&] {
+    if (!timed_out) fail(EMIE_CU_INVALID_ARGUMENT, "peer_status: null pointer");
+    *timed_out = peer_status();
+  });
+}
+
 int emie_cu_peer_wait(const int* d_flags, int G, int epoch, void* stream) {
   return guarded([&] { peer_wait(d_flags, G, epoch, as_stream(stream)); });
 }
@@ -957,15 +964,27 @@ int emie_cu_apply_system_host(emie_cu_system h, const double* h_in, double* h_ou
 
 }  // extern "C"
 
-extern "C" int emie_cu_fgmres(emie_cu_system h, const double* d_rhs, double* d_x, int nrhs,
-                              double tol, int restart, int max_iters, emie_cu_report* reports,
-                              double* h_history, int hist_cap, void* stream) {
+extern "C" int emie_cu_fgmres_ex(emie_cu_system h, const double* d_rhs, double* d_x, int nrhs, double tol,
+                                 int restart, int max_iters, emie_cu_report* reports, double* h_history,
+                                 int hist_cap, emie_cu_iter_fn hook, void* hook_ctx, void* stream) {
   return guarded([&] {
     if (!h || !d_rhs || !d_x) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: null pointer");
     if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: nrhs < 1");
-    fgmres_device(h->sys, reinterpret_cast<const cplx*>(d_rhs), reinterpret_cast<cplx*>(d_x),
-                  nrhs, tol, restart, max_iters, reports, h_history, hist_cap, as_stream(stream));
+    const System& sys = h->sys;
+    KrylovMap A;
+    A.n = 3 * sys.op->cells();
+    A.apply = [&sys](const cplx* in, cplx* out, int nb, cudaStream_t s) { apply_b(*sys.op, in, out, nb, &sys, s); };
+    if (hook) A.on_iteration = [&](int r, int it, double res) { hook(hook_ctx, r, it, res); };
+    fgmres_map(A, reinterpret_cast<const cplx*>(d_rhs), reinterpret_cast<cplx*>(d_x), nrhs, tol, restart,
+               max_iters, reports, h_history, hist_cap, as_stream(stream));
   });
+}
+
+extern "C" int emie_cu_fgmres(emie_cu_system h, const double* d_rhs, double* d_x, int nrhs,
+                              double tol, int restart, int max_iters, emie_cu_report* reports,
+                              double* h_history, int hist_cap, void* stream) {
+  return emie_cu_fgmres_ex(h, d_rhs, d_x, nrhs, tol, restart, max_iters, reports, h_history, hist_cap, nullptr,
+                           nullptr, stream);
 }
 
 // ---- slab vector operations (sharded FGMRES) ----
@@ -1084,6 +1103,15 @@ extern "C" int emie_cu_probe_fp64(double* tflops, void* stream) {
   });
 }
 
+extern "C" int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_blocks, const double* h_in,
+                                   double* h_out) {
+  return guarded([&] {
+    if (!h_blocks || !h_in || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "dense_reference_apply: null pointer");
+    dense_apply_host(nx, ny, nz, reinterpret_cast<const cplx*>(h_blocks), reinterpret_cast<const cplx*>(h_in),
+                     reinterpret_cast<cplx*>(h_out));
+  });
+}
+
 extern "C" int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, const double* breaks,
                                   double omega, int n, const double* h_lam, double* h_out) {
   return guarded([&] {
@@ -1108,9 +1136,9 @@ extern "C" int emie_cu_apply_spectral_host(emie_cu_operator h, const double* h_i
   });
 }
 
-extern "C" int emie_cu_fgmres_host(emie_cu_system h, const double* h_rhs, double* h_x, int nrhs,
-                                   double tol, int restart, int max_iters, emie_cu_report* reports,
-                                   double* h_history, int hist_cap, void* stream) {
+extern "C" int emie_cu_fgmres_host_ex(emie_cu_system h, const double* h_rhs, double* h_x, int nrhs, double tol,
+                                      int restart, int max_iters, emie_cu_report* reports, double* h_history,
+                                      int hist_cap, emie_cu_iter_fn hook, void* hook_ctx, void* stream) {
   return guarded([&] {
     if (!h || !h_rhs || !h_x) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: null pointer");
     if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: nrhs < 1");
@@ -1119,8 +1147,73 @@ extern "C" int emie_cu_fgmres_host(emie_cu_system h, const double* h_rhs, double
     cplx* drhs = scratch<cplx>(n, st);
     cplx* dx = scratch<cplx>(n, st);
     EMIE_CUDA(cudaMemcpyAsync(drhs, h_rhs, n * sizeof(cplx), cudaMemcpyHostToDevice, st));
-    fgmres_device(h->sys, drhs, dx, nrhs, tol, restart, max_iters, reports, h_history, hist_cap, st);
+    const System& sys = h->sys;
+    KrylovMap A;
+    A.n = 3 * sys.op->cells();
+    A.apply = [&sys](const cplx* in, cplx* out, int nb, cudaStream_t s) { apply_b(*sys.op, in, out, nb, &sys, s); };
+    if (hook) A.on_iteration = [&](int r, int it, double res) { hook(hook_ctx, r, it, res); };
+    fgmres_map(A, drhs, dx, nrhs, tol, restart, max_iters, reports, h_history, hist_cap, st);
     EMIE_CUDA(cudaMemcpyAsync(h_x, dx, n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    release(drhs, st);
+    release(dx, st);
+    EMIE_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int emie_cu_fgmres_host(emie_cu_system h, const double* h_rhs, double* h_x, int nrhs,
+                                   double tol, int restart, int max_iters, emie_cu_report* reports,
+                                   double* h_history, int hist_cap, void* stream) {
+  return emie_cu_fgmres_host_ex(h, h_rhs, h_x, nrhs, tol, restart, max_iters, reports, h_history, hist_cap,
+                                nullptr, nullptr, stream);
+}
+
+extern "C" int emie_cu_fgmres_map(long long n, int host_vectors, emie_cu_map_fn apply, void* apply_ctx,
+                                  emie_cu_map_fn precond, void* precond_ctx, emie_cu_iter_fn hook, void* hook_ctx,
+                                  const double* rhs, double* x, double tol, int restart, int max_iters,
+                                  emie_cu_report* report, double* h_history, int hist_cap, void* stream) {
+  return guarded([&] {
+    if (!apply || !rhs || !x || n < 1) fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: null map or vectors");
+    const cudaStream_t st = as_stream(stream);
+    const std::size_t N = static_cast<std::size_t>(n);
+    cplx* drhs = scratch<cplx>(N, st);
+    cplx* dx = scratch<cplx>(N, st);
+    // host callbacks see host vectors: staged through two pinned buffers
+    struct Pinned {
+      cplx* p = nullptr;
+      ~Pinned() { cudaFreeHost(p); }
+    } stage;
+    if (host_vectors) EMIE_CUDA(cudaMallocHost(&stage.p, 2 * N * sizeof(cplx)));
+    auto call = [&](emie_cu_map_fn f, void* ctx, const cplx* in, cplx* out, cudaStream_t s, const char* what) {
+      int rc;
+      if (host_vectors) {
+        EMIE_CUDA(cudaMemcpyAsync(stage.p, in, N * sizeof(cplx), cudaMemcpyDeviceToHost, s));
+        EMIE_CUDA(cudaStreamSynchronize(s));
+        rc = f(ctx, reinterpret_cast<const double*>(stage.p), reinterpret_cast<double*>(stage.p + N), n, s);
+        if (rc == 0) EMIE_CUDA(cudaMemcpyAsync(out, stage.p + N, N * sizeof(cplx), cudaMemcpyHostToDevice, s));
+      } else {
+        rc = f(ctx, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out), n, s);
+      }
+      if (rc != 0) fail(rc, std::string("fgmres: the ") + what + " callback failed");
+    };
+    KrylovMap A;
+    A.n = N;
+    A.speculate = false;  // every callback invocation is observable by the caller
+    A.apply = [&](const cplx* in, cplx* out, int nb, cudaStream_t s) {
+      for (int r = 0; r < nb; ++r) call(apply, apply_ctx, in + r * N, out + r * N, s, "operator");
+    };
+    if (precond)
+      A.precond = [&](const cplx* in, cplx* out, cudaStream_t s) { call(precond, precond_ctx, in, out, s, "preconditioner"); };
+    if (hook) A.on_iteration = [&](int r, int it, double res) { hook(hook_ctx, r, it, res); };
+    EMIE_CUDA(cudaMemcpyAsync(drhs, rhs, N * sizeof(cplx), host_vectors ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    try {
+      fgmres_map(A, drhs, dx, 1, tol, restart, max_iters, report, h_history, hist_cap, st);
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      release(drhs, st);
+      release(dx, st);
+      throw;
+    }
+    EMIE_CUDA(cudaMemcpyAsync(x, dx, N * sizeof(cplx), host_vectors ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
     release(drhs, st);
     release(dx, st);
     EMIE_CUDA(cudaStreamSynchronize(st));

@@ -347,8 +347,10 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   }
   // columns past a mode's ncol are multiplied but never stored: keep them finite
   for (int i = threadIdx.x; i < kUStages * NC * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
-  __syncthreads();
+  // every writing thread orders its generic zero stores before the producer's
+  // later TMA writes into ubuf (write, fence, barrier, then bulk copy)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
   const int G = gridDim.x;
   const int nwork = OCT ? noct : q1 - q0;
 
@@ -580,8 +582,10 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < kUStages * NC * ldu; i += blockDim.x) ubuf[i] = cplx{0.0, 0.0};
-  __syncthreads();
+  // every writing thread orders its generic zero stores before the producer's
+  // later TMA writes into ubuf (write, fence, barrier, then bulk copy)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
   const int G = gridDim.x;
   const int nwork = OCT ? noct : q1 - q0;
 

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "../../include/emie_cu.h"
@@ -130,6 +131,7 @@ void move_planes(const cplx* src, cplx* dst, int nrhs, int nidx, const int* idx,
 // peer-memory exchange flags (peer.cu): release-store `epoch` into slot `me`
 // of every rank's flag array / wait until all G slots of `flags` reach it
 void peer_signal(int* const* flag_ptrs, int G, int me, int epoch, cudaStream_t st);
+int peer_status();
 void peer_wait(const int* flags, int G, int epoch, cudaStream_t st);
 
 // Green's build (greens.cu)
@@ -154,6 +156,7 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
 void assemble_signed_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
                           const double* breaks, double hx, double hy, const FilterParams& fp, int n, const int* oi,
                           const int* oj, cplx* h_out);
+void dense_apply_host(int nx, int ny, int nz, const cplx* h_blocks, const cplx* h_in, cplx* h_out);
 void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
                      int n, const double* lam, cplx* out);
 
@@ -193,5 +196,21 @@ void vec_residual(cplx* r, const cplx* b, const cplx* t, std::size_t n, double* 
 void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, double tol,
                    int m, int max_iters, emie_cu_report* reports, double* h_history,
                    int hist_cap, cudaStream_t st);
+// The same device FGMRES over any linear map: A applies nrhs device vectors
+// of n complex entries (in -> out, stream ordered); precond, when set, is the
+// flexible right preconditioner (cie.hpp:57, cie.cpp:151-156: z_j = M v_j,
+// x += sum y_j z_j); on_iteration(rhs, iteration, residual estimate) is
+// called live, where the reference calls SolverConfig::on_iteration
+// (cie.cpp:178-185, 199-201). speculate = false when A or M has side effects
+// the caller can observe (host callbacks): no speculative next-step apply.
+struct KrylovMap {
+  std::size_t n = 0;
+  std::function<void(const cplx* in, cplx* out, int nrhs, cudaStream_t st)> apply;
+  std::function<void(const cplx* in, cplx* out, cudaStream_t st)> precond;
+  std::function<void(int rhs, int iteration, double residual)> on_iteration;
+  bool speculate = true;
+};
+void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, double tol, int m, int max_iters,
+                emie_cu_report* reports, double* h_history, int hist_cap, cudaStream_t st);
 
 }  // namespace emie_cu

@@ -8,8 +8,9 @@
 // destination's memory: the source's signal kernel release-stores the
 // exchange epoch there (system scope) after its move kernels in stream
 // order; the destination's wait kernel acquire-loads its G flags before the
-// next stage reads the buffer (bounded spin: a peer that never arrives traps
-// the context instead of hanging the GPU).
+// next stage reads the buffer (bounded spin: a peer that never arrives sets a
+// sticky timeout flag, which emie_cu_peer_status reports, and the waits
+// return instead of hanging the GPU; the context stays usable).
 #include "operator.cuh"
 
 namespace emie_cu {
@@ -21,7 +22,13 @@ struct PeerFlags {
   int* p[kMaxPeers];
 };
 
+__device__ int g_peer_timeout = 0;  // sticky: a wait gave up on a peer
+
 __global__ void peer_signal_kernel(PeerFlags f, int G, int me, int epoch) {
+  // the earlier kernels' remote NVLink stores (moves, fused transposes) are
+  // ordered before the flag by the kernel boundary; the system-scope fence
+  // makes that ordering explicit for the peers that acquire the flag
+  asm volatile("fence.sc.sys;" ::: "memory");
   const int g = threadIdx.x;
   if (g < G) {
     int* a = f.p[g] + me;
@@ -37,8 +44,12 @@ __global__ void peer_wait_kernel(const int* flags, int G, int epoch) {
     while (true) {
       asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + g) : "memory");
       if (v - epoch >= 0) break;  // epochs only grow (wrap-safe difference)
+      if (*reinterpret_cast<volatile int*>(&g_peer_timeout)) break;  // an earlier wait already gave up
       __nanosleep(200);
-      if (++spins > (1LL << 27)) __trap();  // ~30 s: a peer is gone; fail loudly, never hang
+      if (++spins > (1LL << 27)) {  // ~30 s: a peer is gone; report it, never hang
+        atomicExch(&g_peer_timeout, 1);
+        break;
+      }
     }
   }
   __syncthreads();
@@ -47,6 +58,18 @@ __global__ void peer_wait_kernel(const int* flags, int G, int epoch) {
 }
 
 }  // namespace
+
+// reads and clears the sticky timeout flag (synchronises the device)
+int peer_status() {
+  int v = 0;
+  EMIE_CUDA(cudaDeviceSynchronize());
+  EMIE_CUDA(cudaMemcpyFromSymbol(&v, g_peer_timeout, sizeof(int)));
+  if (v) {
+    const int z = 0;
+    EMIE_CUDA(cudaMemcpyToSymbol(g_peer_timeout, &z, sizeof(int)));
+  }
+  return v;
+}
 
 void peer_signal(int* const* flag_ptrs, int G, int me, int epoch, cudaStream_t st) {
   if (!flag_ptrs || G < 1 || G > kMaxPeers || me < 0 || me >= G)

@@ -443,6 +443,7 @@ struct Rhs {
   cplx* r = nullptr;    // residual (device)
   cplx* V = nullptr;    // basis (m+1) vectors (device)
   cplx* w = nullptr;    // apply output (device)
+  cplx* Z = nullptr;    // preconditioned directions m vectors (device; flexible FGMRES only)
   double bnorm = 0, rnorm = 0;
   int iter = 0, j = 0, cols = 0;
   bool broke = false;
@@ -460,10 +461,17 @@ struct Rhs {
 void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, double tol,
                    int m, int max_iters, emie_cu_report* reports, double* h_history,
                    int hist_cap, cudaStream_t st) {
+  KrylovMap A;
+  A.n = 3 * sys.op->cells();
+  A.apply = [&sys](const cplx* in, cplx* out, int nb, cudaStream_t s) { apply_b(*sys.op, in, out, nb, &sys, s); };
+  fgmres_map(A, d_rhs, d_x, nrhs, tol, m, max_iters, reports, h_history, hist_cap, st);
+}
+
+void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, double tol, int m, int max_iters,
+                emie_cu_report* reports, double* h_history, int hist_cap, cudaStream_t st) {
   if (!(tol > 0.0) || m < 1 || max_iters < 1)
     fail(EMIE_CU_INVALID_ARGUMENT, "fgmres: bad solver configuration");
-  const Operator& op = *sys.op;
-  const std::size_t n = 3 * op.cells();
+  const std::size_t n = A.n;
   Workspace ws(st, n, m + 1);
   const int T = 256;
   const int GB = red_blocks(n);
@@ -474,6 +482,8 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
   cplx* Wall = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
   cplx* Bin = scratch<cplx>(static_cast<std::size_t>(nrhs) * n, st);
   double* ycoef = scratch<double>(2 * (m + 1), st);
+  // flexible right preconditioning: the directions z_j = M v_j (cie.cpp:151-153)
+  cplx* Zall = A.precond ? scratch<cplx>(static_cast<std::size_t>(nrhs) * m * n, st) : nullptr;
 
   std::vector<Rhs> rs(nrhs);
   const int ps = ws.pstride;
@@ -501,6 +511,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
     R.r = Rall + i * n;
     R.V = Vall + static_cast<std::size_t>(i) * (m + 1) * n;
     R.w = Wall + i * n;
+    if (Zall) R.Z = Zall + static_cast<std::size_t>(i) * m * n;
     EMIE_CUDA(cudaMemsetAsync(R.x, 0, n * sizeof(cplx), st));
     R.bnorm = ws.norm_of(R.b);
     if (R.bnorm == 0.0) {  // cie.cpp:124-128
@@ -547,7 +558,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
         y[k] = acc / R.h[static_cast<std::size_t>(k) * (m + 1) + k];
       }
       EMIE_CUDA(cudaMemcpyAsync(ycoef, y.data(), R.cols * sizeof(cd), cudaMemcpyHostToDevice, st));
-      combine_kernel<<<GB, T, 0, st>>>(R.x, R.V, n, R.cols, ycoef, n);
+      combine_kernel<<<GB, T, 0, st>>>(R.x, R.Z ? R.Z : R.V, n, R.cols, ycoef, n);
       check_launch("combine_kernel");
       EMIE_CUDA(cudaStreamSynchronize(st));  // ycoef is reused by the next rhs
     }
@@ -569,9 +580,14 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
     for (std::size_t q = 0; q < es.size(); ++q) {
       const Rhs& R = *es[q].R;  // es[q].slot == q
       const cplx* src = es[q].inner ? R.V + static_cast<std::size_t>(es[q].j) * n : R.x;
+      if (es[q].inner && R.Z) {  // z_j = M v_j, then A z_j (cie.cpp:151-153)
+        cplx* z = R.Z + static_cast<std::size_t>(es[q].j) * n;
+        A.precond(src, z, st);
+        src = z;
+      }
       EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     }
-    apply_b(op, Bin, Wall, static_cast<int>(es.size()), &sys, st);
+    A.apply(Bin, Wall, static_cast<int>(es.size()), st);
     for (std::size_t q = 0; q < es.size(); ++q) {
       Rhs& R = *es[q].R;
       cplx* w = Wall + q * n;
@@ -671,6 +687,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
         R.cols = j;
         R.broke = true;
         R.history.push_back(R.rnorm / R.bnorm);
+        if (A.on_iteration) A.on_iteration(R.idx, R.iter, R.rnorm / R.bnorm);
       }
       end_inner = true;
     } else {
@@ -688,6 +705,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       R.cols = j + 1;
       const double est = std::abs(R.g[j + 1]) / R.bnorm;
       R.history.push_back(est);
+      if (A.on_iteration) A.on_iteration(R.idx, R.iter, est);
       if (est <= tol) end_inner = true;
     }
     if (!end_inner) {
@@ -719,7 +737,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
       if (pending.empty()) break;
       enqueue_round(pending, par);
     }
-    bool spec = !drain;
+    bool spec = !drain && A.speculate;
     for (const Entry& e : pending)
       if (!e.inner || !(e.j + 1 < m && e.R->iter + 1 < max_iters)) spec = false;
     std::vector<Entry> next;
@@ -770,6 +788,7 @@ void fgmres_device(const System& sys, const cplx* d_rhs, cplx* d_x, int nrhs, do
   release(Bin, st);
   release(ycoef, st);
   release(dv_all, st);
+  if (Zall) release(Zall, st);
   EMIE_CUDA(cudaStreamSynchronize(st));
 }
 

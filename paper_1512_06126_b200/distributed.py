@@ -18,7 +18,7 @@ The per-rank stages are separate methods so the same code runs under NCCL
 (one process per GPU), gloo on CPU (tests, NumPy backend) or a loopback that
 runs G virtual ranks in one process (one-GPU parity tests). Backends: CUDA
 (the C ABI of libemie_cu.so on torch tensors) and NumPy (the restatement of
-oracle/emie_oracle.py, test infrastructure only).
+tests/numpy_backend.py, test infrastructure only).
 """
 from __future__ import annotations
 
@@ -289,10 +289,16 @@ class PeerExchange:
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
+    host_barrier = None  # callable: host-side exchange barrier instead of the flag kernels
+
     def signal(self):
         """After this rank's pushes (stream order): epoch += 1 into every rank's flag slot."""
         from . import lib, _check
         self.epoch += 1
+        if self.host_barrier is not None:  # pushes complete before the host barrier
+            import torch
+            torch.cuda.current_stream().synchronize()
+            return
         if self._flag_ptrs is None:
             return
         P = self.sh.plan
@@ -301,6 +307,9 @@ class PeerExchange:
     def wait(self):
         """Before reading this rank's buffer: all G ranks reached the epoch."""
         from . import lib, _check
+        if self.host_barrier is not None:
+            self.host_barrier()
+            return
         if self._flag_ptrs is None:
             return
         _check(lib().emie_cu_peer_wait(ctypes.c_void_p(self.own[2]), self.sh.plan.G, self.epoch, self._stream()))
@@ -336,6 +345,15 @@ class PeerExchange:
         out = self.sh.be.lateral_inverse(self.own[0], self._U, self.sh.nrhs)
         self._U = None
         return out
+
+    def check(self):
+        """Raise if a flag wait of this process gave up on a peer (the sticky
+        timeout of emie_cu_peer_wait; synchronises the device)."""
+        from . import lib, _check
+        t = ctypes.c_int(0)
+        _check(lib().emie_cu_peer_status(ctypes.byref(t)))
+        if t.value:
+            raise RuntimeError("peer exchange: a rank never signalled (flag wait timed out); results are invalid")
 
     def apply(self, U):
         """One rank per process (all ranks call it with their slabs)."""
@@ -501,76 +519,6 @@ class CudaBackend:
             self.L.emie_cu_operator_destroy(self.geom)
         except Exception:  # noqa: BLE001 -- interpreter teardown
             pass
-
-
-class NumpyBackend:
-    """The same stages restated with numpy (oracle/emie_oracle.py): test
-    infrastructure for the gloo CPU tests of the exchange logic."""
-
-    def __init__(self, plan: ShardPlan, rank: int, comp, dims, diag_slab, xp=None):
-        import torch
-        self.torch = torch
-        self.plan, self.rank, self.comp, self.dims = plan, rank, comp, dims
-        self.s, self.r1, self.r2 = (np.asarray(d) for d in diag_slab)
-        self._orc = None
-
-    def _oracle(self):
-        if self._orc is None:
-            import emie_oracle  # tests put oracle/ on sys.path
-            self._orc = emie_oracle
-        return self._orc
-
-    def empty(self, shape):
-        return self.torch.empty(shape, dtype=self.torch.complex128)
-
-    def zeros(self, shape):
-        return self.torch.zeros(shape, dtype=self.torch.complex128)
-
-    def lateral_forward(self, U, nrhs):
-        P = self.plan
-        nzl = P.nzl(self.rank)
-        u = U.numpy().reshape(nrhs, 3, nzl * P.ny * P.nx) * self.r2[None, None, :]
-        u = u.reshape(nrhs, 3 * nzl, P.ny, P.nx)
-        pad = np.zeros((nrhs, 3 * nzl, P.ey, P.ex), np.complex128)
-        pad[:, :, :P.ny, :P.nx] = u
-        F = np.fft.fft2(pad, axes=(2, 3))  # [r][plane][my][mx]
-        S = np.ascontiguousarray(F.transpose(0, 3, 2, 1)).reshape(nrhs, P.E, 3 * nzl)  # m = mx*ey + my
-        return self.torch.from_numpy(S)
-
-    def lateral_forward_into(self, U, S, nrhs):
-        S.copy_(self.lateral_forward(U, nrhs))
-
-    def contract(self, S, nrhs, q0, q1):
-        P = self.plan
-        O = self._oracle()
-        Sn = S.numpy()
-        for qm in range(q0, q1):
-            for m in mirror_modes(qm, P.qx, P.ex, P.ey):
-                mx, my = divmod(m, P.ey)
-                M = O._mode_matrix(self.comp, self.dims, P.nz, my, mx)
-                for r in range(nrhs):
-                    Sn[r, m] = M @ Sn[r, m]
-
-    def lateral_inverse(self, S, U, nrhs):
-        P = self.plan
-        nzl = P.nzl(self.rank)
-        F = S.numpy().reshape(nrhs, P.ex, P.ey, 3 * nzl).transpose(0, 3, 2, 1)
-        b = np.fft.ifft2(F, axes=(2, 3))[:, :, :P.ny, :P.nx].reshape(nrhs, 3, -1)
-        u = U.numpy().reshape(nrhs, 3, -1)
-        out = self.s[None, None, :] * u + self.r1[None, None, :] * b
-        return self.torch.from_numpy(np.ascontiguousarray(out).reshape(U.shape))
-
-    def move(self, src, dst, nrhs, g, E, sdesc, ddesc, nzh):
-        idx = self.plan.modes[g]
-        s_arr, d_arr = src.numpy().reshape(-1), dst.numpy().reshape(-1)
-        ni = len(idx)
-        r = np.arange(nrhs)[:, None, None, None]
-        i = np.arange(ni)[None, :, None, None]
-        c = np.arange(3)[None, None, :, None]
-        z = np.arange(nzh)[None, None, None, :]
-        ms = r * E + idx[i] if sdesc[0] else r * ni + i
-        md = r * E + idx[i] if ddesc[0] else r * ni + i
-        d_arr[md * ddesc[1] + c * ddesc[2] + ddesc[3] + z] = s_arr[ms * sdesc[1] + c * sdesc[2] + sdesc[3] + z]
 
 
 def greens_offset_ranges(n_offsets: int, G: int) -> List[tuple]:

@@ -85,6 +85,33 @@ def field_at(prof, z):
     raise ValueError("depth above the surface")
 
 
+def derivative_at(prof, z):
+    """dE/dz of the profile at depth z (z >= 0; on an interface, the layer below)."""
+    for zt, l, D, r, e in prof:
+        if z >= zt and (z < zt + l or np.isinf(l)):
+            if np.isinf(l):
+                return -e * D * cmath.exp(-e * (z - zt))
+            return e * D * (-cmath.exp(-e * (z - zt)) + r * cmath.exp(-e * l) * cmath.exp(-e * (zt + l - z)))
+    raise ValueError("depth above the surface")
+
+
+def magnetic_at(prof, z, omega):
+    """Tangential H^N of the profile (Faraday, fields ~ e^{-i omega t}):
+    H_y = (dE_x/dz) / (i omega mu0) for an x-polarised E (and H_x = -(dE_y/dz) /
+    (i omega mu0) for a y-polarised one)."""
+    return derivative_at(prof, z) / (1j * omega * MU0)
+
+
+def surface_impedance(tops, sigma, omega):
+    """Z = E_x / H_y at z = 0+ (earth side, SPEC.md DESIGN DECISIONS) of the
+    1-D background -> (Z, rho_a = |Z|^2 / (omega mu0), phase in degrees). The
+    phase is reported in the e^{+i omega t} MT convention, arg(conj Z), so a
+    uniform halfspace gives +45 degrees (SPEC.md normal_field_profile)."""
+    prof = profile(tops, sigma, omega)
+    z = 1.0 / magnetic_at(prof, 0.0, omega)  # E(0) = 1
+    return z, abs(z) ** 2 / (omega * MU0), float(np.degrees(np.angle(np.conj(z))))
+
+
 def interval_average(prof, a, b):
     """(1/(b-a)) * integral of E over [a, b] inside one layer."""
     h = b - a

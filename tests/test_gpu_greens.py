@@ -134,8 +134,10 @@ np.save(sys.argv[1], op.blocks())
         outs.append(np.load(f))
     assert np.all(np.isfinite(outs[0]))
     # same formulas compiled in two contexts (FMA contraction may differ in
-    # the last bit); the blocks amplify such differences, so the
-    # bar is the Green's parity bar's conditioning floor, per block
+    # the last bit); the filter sums amplify such differences by up to 1e13
+    # (V1 + V3 at small lambda, tests/test_gpu_vfunctions.py), which is why the
+    # reference's own FMA build moves its blocks by 1e-6..1e-4 of the block max
+    # (oracle/ref_envelope.py). Two device contexts stay two decades inside that.
     a, b = outs
     err = np.max(np.abs(a - b), axis=-1) / np.max(np.abs(a), axis=-1)
-    assert np.max(err) <= 1e-8, np.max(err)
+    assert np.max(err) <= 1e-7, np.max(err)

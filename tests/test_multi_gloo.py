@@ -8,6 +8,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from numpy_backend import NumpyBackend
 from paper_1512_06126_b200.sharding import max_over_ranks, run_sweep, shard_indices
 
 
@@ -104,7 +105,7 @@ def _sharded_worker(rank, world, port, q):
     plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], world)
     z0, z1 = plan.z[rank], plan.z[rank + 1]
     dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
-    be = D.NumpyBackend(plan, rank, comp, dims, dslab)
+    be = NumpyBackend(plan, rank, comp, dims, dslab)
     sysd = D.DistributedSystem(D.ShardedApply(plan, rank, be, nrhs))
     out = sysd.apply(torch.from_numpy(D.slab_of(U, plan, rank, nrhs)))
     parts = [None] * world
@@ -151,7 +152,7 @@ def test_sharded_apply_loopback_numpy(G):
     for g in range(G):
         z0, z1 = plan.z[g], plan.z[g + 1]
         dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
-        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+        shards.append(D.ShardedApply(plan, g, NumpyBackend(plan, g, comp, dims, dslab), nrhs))
     outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)) for g in range(G)])
     got = D.join_slabs([o.numpy() for o in outs], plan, nrhs)
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
@@ -175,7 +176,7 @@ def test_peer_exchange_loopback_numpy(G):
     for g in range(G):
         z0, z1 = plan.z[g], plan.z[g + 1]
         dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
-        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+        shards.append(D.ShardedApply(plan, g, NumpyBackend(plan, g, comp, dims, dslab), nrhs))
     xs, _ = D.peer_loopback(shards, host=True)
     for _ in range(2):
         outs = D.peer_loopback_apply(xs, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)) for g in range(G)])
@@ -212,7 +213,7 @@ def _numpy_sharded_solve(G, ranks, dims, comp, diag, B, reduce, dist_apply=None)
     for g in ranks:
         z0, z1 = plan.z[g], plan.z[g + 1]
         dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
-        shards.append(D.ShardedApply(plan, g, D.NumpyBackend(plan, g, comp, dims, dslab), nrhs))
+        shards.append(D.ShardedApply(plan, g, NumpyBackend(plan, g, comp, dims, dslab), nrhs))
         ops.append(DS.NumpySlabOps())
         rhs.append(torch.from_numpy(D.slab_of(B, plan, g, nrhs).reshape(nrhs, -1)))
     if dist_apply is None:
