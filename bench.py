@@ -61,6 +61,11 @@ def parse():
                    help="strong scaling of one grid: depth-slab / mode-shard apply over the N ranks")
     p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                    help="--strong: column transposes as peer stores (IPC buffers, flag barriers) or NCCL all-to-all")
+    p.add_argument("--peer-sync", default="flags", choices=["flags", "host"],
+                   help="--strong --exchange peer: device flag barriers, or stream sync + a host barrier (ranks "
+                        "sharing one GPU: no kernel may spin on another process's flag)")
+    p.add_argument("--check", action="store_true",
+                   help="--strong: compare the sharded apply with the unsharded device apply (gathered on rank 0)")
     return p.parse_args()
 
 
@@ -649,6 +654,8 @@ def run_strong(args):
     if args.exchange == "peer":
         if world > 1:
             px = D.peer_exchange_torch(shard)
+            if args.peer_sync == "host":
+                px.host_barrier = dist.barrier
         else:
             (px,), _ = D.peer_loopback([shard])
         step = lambda: px.apply(slab)  # noqa: E731
@@ -695,6 +702,23 @@ def run_strong(args):
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
     if dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    check = None
+    if args.exchange == "peer":
+        px.check()  # a flag wait that gave up invalidates the run
+    if args.check:
+        out = step()
+        torch.cuda.synchronize()
+        parts = [None] * world
+        if dist:
+            dist.all_gather_object(parts, out.cpu().numpy())
+        else:
+            parts = [out.cpu().numpy()]
+        if rank == 0:
+            full_op = emie.assemble_operator(grid, model, cfg.omega)
+            want = emie.apply(emie.build_system(grid, full_op), U.reshape(-1)).reshape(NRHS, -1)
+            got = D.join_slabs(parts, plan, NRHS).reshape(NRHS, -1)
+            check = {"max_rel_err_vs_unsharded_apply": float(np.max(np.abs(got - want)) / np.max(np.abs(want))),
+                     "processes": world, "exchange": args.exchange, "peer_sync": args.peer_sync}
     if rank == 0:
         slab_bytes = hin.numel() * 16
         line = {
@@ -713,6 +737,7 @@ def run_strong(args):
                     "h2d_bytes_per_step": slab_bytes * world, "d2h_bytes_per_step": slab_bytes * world},
             "gpu_launches": None,
             "clocks": clk,
+            "check": check,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -142,6 +142,35 @@ int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, c
  * fixed summation order; the oracle the reference tests the FFT apply against */
 int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_blocks, const double* h_in, double* h_out);
 
+/* ---- layered-medium API on the device (include/emie/layered.hpp), the
+ * building blocks of the Green's build evaluated at caller-given lambdas
+ * and depths. A spectral state is 9 arrays of L+1 complex, in the order
+ * sig eta p q one_p one_q e2l em1_2l diag_a (SpectralLayerState,
+ * layered.hpp:41-58); gamma 0 = Gamma::unit, 1 = Gamma::cond. */
+
+/* build_spectral_state (layered.hpp:56-57, layered.cpp:67-129) at n lambdas,
+ * both gammas: h_out[t][gamma][9][L+1] complex */
+int emie_cu_spectral_states(int L, const double* tops, const double* sigma, double omega, int n,
+                            const double* h_lam, double* h_out);
+
+/* vertical_moment_tables (layered.hpp:97-103, layered.cpp:222-395) for the
+ * partition breaks[nz+1] at n lambdas: h_out[t][gamma][6][nz][nz] complex, pair
+ * order (0,0) (1,0) (0,1) (1,1) (2,0) (0,2), row-major (VerticalMomentTable::w) */
+int emie_cu_moment_tables(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                          double omega, int n, const double* h_lam, double* h_out);
+
+/* fundamental_value (layered.hpp:60-66, layered.cpp:140-189) of one spectral
+ * state at n point pairs: h_ord[4i..4i+3] = dz, dzs, layer_z, layer_zs
+ * (-1: layer of the point) */
+int emie_cu_fundamental_values(int L, const double* tops, const double* h_state, int gamma, int n,
+                               const double* h_z, const double* h_zs, const int* h_ord, double* h_out);
+
+/* point_moments (layered.hpp:116-126, layered.cpp:450-542) at n observation
+ * depths for the partition breaks[nz+1] with interval layers layer[nz]:
+ * h_out[t][2][nz] complex (m[0], m[1]) */
+int emie_cu_point_moments(int L, const double* tops, const double* h_state, int gamma, int nz,
+                          const double* breaks, const int* layer, int n, const double* h_zobs, double* h_out);
+
 void emie_cu_operator_destroy(emie_cu_operator op);
 
 /* apply(const SpectralOperator&, const GridVector&) (toeplitz.hpp:43,

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libemie_cu.so"
 CPPLIB = PKG / "libemie_b200.so"  # C++ drop-in of the reference emie:: API over the C ABI
-SOURCES = ["capi.cu", "operator.cu", "lateral.cu", "solver.cu", "greens.cu", "shard.cu", "peer.cu", "dense.cu"]
+SOURCES = ["capi.cu", "operator.cu", "lateral.cu", "solver.cu", "greens.cu", "shard.cu", "peer.cu", "dense.cu", "layered.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

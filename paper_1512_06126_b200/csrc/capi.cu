@@ -1112,6 +1112,50 @@ extern "C" int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_block
   });
 }
 
+extern "C" int emie_cu_spectral_states(int L, const double* tops, const double* sigma, double omega, int n,
+                                       const double* h_lam, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || (n > 0 && (!h_lam || !h_out))) fail(EMIE_CU_INVALID_ARGUMENT, "spectral_states: null pointer");
+    layered_probe_host(0, L, tops, reinterpret_cast<const cplx*>(sigma), 0, nullptr, omega, n, h_lam,
+                       reinterpret_cast<cplx*>(h_out));
+  });
+}
+
+extern "C" int emie_cu_moment_tables(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                                     double omega, int n, const double* h_lam, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || (n > 0 && (!h_lam || !h_out)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "moment_tables: null pointer");
+    if (nz < 1) fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition needs at least one interval");
+    layered_probe_host(1, L, tops, reinterpret_cast<const cplx*>(sigma), nz, breaks, omega, n, h_lam,
+                       reinterpret_cast<cplx*>(h_out));
+  });
+}
+
+extern "C" int emie_cu_fundamental_values(int L, const double* tops, const double* h_state, int gamma, int n,
+                                          const double* h_z, const double* h_zs, const int* h_ord, double* h_out) {
+  return guarded([&] {
+    if (!tops || !h_state || (n > 0 && (!h_z || !h_zs || !h_ord || !h_out)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "fundamental_values: null pointer");
+    for (int i = 0; i < n; ++i)
+      if (h_ord[4 * i] < 0 || h_ord[4 * i] > 2 || h_ord[4 * i + 1] < 0 || h_ord[4 * i + 1] > 2)
+        fail(EMIE_CU_INVALID_ARGUMENT, "fundamental_value: derivative orders must be 0..2");
+    fundamental_values_host(L, tops, reinterpret_cast<const cplx*>(h_state), gamma, n, h_z, h_zs, h_ord,
+                            reinterpret_cast<cplx*>(h_out));
+  });
+}
+
+extern "C" int emie_cu_point_moments(int L, const double* tops, const double* h_state, int gamma, int nz,
+                                     const double* breaks, const int* layer, int n, const double* h_zobs,
+                                     double* h_out) {
+  return guarded([&] {
+    if (!tops || !h_state || !breaks || !layer || (n > 0 && (!h_zobs || !h_out)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "point_moments: null pointer");
+    point_moments_host(L, tops, reinterpret_cast<const cplx*>(h_state), gamma, nz, breaks, layer, n, h_zobs,
+                       reinterpret_cast<cplx*>(h_out));
+  });
+}
+
 extern "C" int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, const double* breaks,
                                   double omega, int n, const double* h_lam, double* h_out) {
   return guarded([&] {

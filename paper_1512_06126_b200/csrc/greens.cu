@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "layered.cuh"
 #include "operator.cuh"
 #include "tma.cuh"
 
@@ -48,92 +49,6 @@ constexpr int kGreenSlots = EMIE_GREEN_SLOTS;
 #define EMIE_GREEN_PAIR_UNROLL 2
 #endif
 constexpr int kPairUnroll = EMIE_GREEN_PAIR_UNROLL;  // lambdas per pair-phase loop body  // full-lambda-range pairs per thread (+ a lambda-split tail)
-
-// ------------------------------------------------------ complex helpers ----
-// Smith's algorithm: the exact-path fallback of cdiv (zero or non-finite divisor)
-__device__ __noinline__ cplx cdiv_smith(cplx a, cplx b) {
-  if (fabs(b.re) >= fabs(b.im)) {
-    const double r = b.im / b.re, d = b.re + b.im * r;
-    return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
-  }
-  const double r = b.re / b.im, d = b.re * r + b.im;
-  return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
-}
-
-__device__ __forceinline__ cplx csqrt_pos(cplx z) {
-  // principal square root, then the Re > 0 branch (layered.cpp:87-89)
-  const double m = hypot(z.re, z.im);
-  cplx r;
-  if (m == 0.0) return {0.0, 0.0};
-  const double t = sqrt(0.5 * (fabs(z.re) + m));
-  if (z.re >= 0.0) r = {t, z.im / (2.0 * t)};
-  else r = {fabs(z.im) / (2.0 * t), copysign(t, z.im)};
-  if (r.re < 0.0) r = -r;
-  return r;
-}
-// exp(x) - 1 without cancellation (layered.cpp:19-25)
-__device__ __forceinline__ cplx cexpm1(cplx x) {
-  const double em = expm1(x.re);
-  double sh, ch;
-  sincos(0.5 * x.im, &sh, &ch);
-  // one sincos: cos x = 1 - 2 sin^2(x/2), sin x = 2 sin(x/2) cos(x/2)
-  const double s = 2.0 * sh * ch, cm1 = -2.0 * sh * sh;
-  return {em * (1.0 + cm1) + cm1, (em + 1.0) * s};
-}
-__device__ __forceinline__ cplx cexp(cplx x) {
-  const double e = exp(x.re);
-  double s, c;
-  sincos(x.im, &s, &c);
-  return {e * c, e * s};
-}
-// 2^e as a double for e in [-1022, 1023] (exponent bits built directly)
-__device__ __forceinline__ double pow2i(int e) {
-  return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-}
-// a * 2^e without the software scalbn: one multiply in the normal range, two
-// half-steps outside it (exact unless the result itself under/overflows)
-__device__ __forceinline__ cplx scal2(cplx a, int e) {
-  if (e >= -1022 && e <= 1023) {
-    const double f = pow2i(e);
-    return {a.re * f, a.im * f};
-  }
-  e = max(-2200, min(2200, e));
-  const int e1 = e / 2, e2 = e - e1;
-  const double f1 = (e1 < -1022) ? 0.0 : pow2i(min(e1, 1023));
-  const double f2 = (e2 < -1022) ? 0.0 : pow2i(min(e2, 1023));
-  return {a.re * f1 * f2, a.im * f1 * f2};
-}
-// floor(log2 |x|) for finite x != 0 (ilogb without the library call)
-__device__ __forceinline__ int ilog2(double x) {
-  const long long b = __double_as_longlong(x);
-  const int ex = static_cast<int>((b >> 52) & 0x7ff);
-  if (ex != 0) return ex - 1023;
-  return ilogb(x);  // subnormal: rare
-}
-
-// 1/d for d in [1, 8) to ~1 ulp: hardware reciprocal estimate + two Newton steps
-__device__ __forceinline__ double rcp_unit(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
-}
-// a / b without FP64 divisions (nvcc emits each as an out-of-line call): b is
-// scaled by the power of two of its larger component, so |b'|^2 is in [1, 2]
-// and neither overflows nor underflows; a / b = a conj(b') / |b'|^2 * 2^-e.
-__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
-  const double m = fmax(fabs(b.re), fabs(b.im));
-  if (!(m > 0.0) || !(m <= 1.0e300) || m < 1.0e-300) return cdiv_smith(a, b);
-  const int e = ilog2(m);
-  const double sc = pow2i(-e);
-  const double br = b.re * sc, bi = b.im * sc;
-  const double r = rcp_unit(br * br + bi * bi);
-  const cplx q = {(a.re * br + a.im * bi) * r, (a.im * br - a.re * bi) * r};
-  return scal2(q, -e);
-}
-__device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
 
 // ------------------------------------------------------ hankel helpers ----
 __device__ __forceinline__ double ediff(double a, double b) {  // hankel.cpp:22-26
@@ -342,13 +257,6 @@ struct GreenParams {
   cplx sig_dn[kMaxLayers];  // sig[m-1] / sig[m]
 };
 
-// per-interval geometry (device arrays): a, b, h, d (top), dp (bottom), l
-struct Interval {
-  double a, b, h, d, dp, l;
-  int layer;
-  int has_p, has_q;
-  cplx inv_sig;  // 1 / sigma_b of the interval
-};
 
 // SMEM plan for one chunk of LC lambdas
 struct Chunk {
@@ -621,74 +529,31 @@ __device__ __forceinline__ void chunk_factors(const GreenParams& P, const Chunk&
                                               int lc, double wmu, int tid, int nth) {
   const int NL = P.L + 1, nz = P.nz;
   auto F = [&](int li, int f, int j) -> cplx& { return chunk_field(C, nz, li, f, j); };
-  // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317)
+  // phase 1: interval pack (shared by both gammas) and factors (layered.cpp:237-317),
+  // folded into the left / right / diagonal fields of the pair evaluation
   for (int x = tid; x < lc * nz; x += nth) {
     const int li = x / nz, j = x - li * nz;
     const Interval I = iv[j];
-    const cplx eta = C.eta[li * NL + I.layer];
-    const cplx ie = C.ieta[li * NL + I.layer];  // 1/eta, 1/eta^2: the divisions below become products
-    const cplx ie2 = ie * ie;
-    const cplx ehm1 = cexpm1(-I.h * eta);
-    const cplx eh = cplx{1.0, 0.0} + ehm1;
-    const cplx el2 = C.e2l[li * NL + I.layer];
-    cplx epa = {1.0, 0.0}, epa2m1 = {0.0, 0.0}, epabm1 = {0.0, 0.0}, epb2m1 = {0.0, 0.0};
-    cplx eqb = {1.0, 0.0}, eqabm1 = {0.0, 0.0};
-    if (I.has_p) {
-      const cplx epam1 = cexpm1(-(I.a - I.d) * eta);
-      const cplx epbm1 = epam1 + ehm1 + epam1 * ehm1;
-      epa = cplx{1.0, 0.0} + epam1;
-      epa2m1 = 2.0 * epam1 + epam1 * epam1;
-      epabm1 = epam1 + epbm1 + epam1 * epbm1;
-      epb2m1 = 2.0 * epbm1 + epbm1 * epbm1;
-    }
-    if (I.has_q) {
-      const cplx eqbm1 = cexpm1(-(I.dp - I.b) * eta);
-      const cplx eqam1 = eqbm1 + ehm1 + eqbm1 * ehm1;
-      eqb = cplx{1.0, 0.0} + eqbm1;
-      eqabm1 = eqam1 + eqbm1 + eqam1 * eqbm1;
-    }
-    const cplx elh = (I.has_p && I.has_q) ? cexp((-(2.0 * I.l - I.h)) * eta) : cplx{0.0, 0.0};
-    const cplx u = -ehm1;
-    const cplx eta2 = eta * eta;
+    const IvPack k = iv_pack(I, C.eta[li * NL + I.layer], C.ieta[li * NL + I.layer], C.e2l[li * NL + I.layer]);
     const cplx isk = I.inv_sig;
     for (int gm = 0; gm < 2; ++gm) {
       const int r = li * 2 * NL + gm * NL + I.layer;
-      const cplx p = C.p[r], q = C.q[r], A = C.diag_a[r];
-      const cplx one_p = C.one_p[r], one_q = C.one_q[r];
-      const cplx Sa = one_p + p * epa2m1;
-      const cplx Sab = one_p + p * epabm1;
-      const cplx Mab = (cplx{2.0, 0.0} - one_p) - p * epabm1;
-      const cplx Dp = one_p + p * epb2m1;
-      const cplx Tq = one_q + q * eqabm1;
-      const cplx TMq = (cplx{2.0, 0.0} - one_q) - q * eqabm1;
-      const cplx iDp = crecip(Dp);
-      const cplx theta = (eh * Sa) * iDp;
-      const cplx H0 = ((u * Sab) * ie) * iDp;
-      const cplx J0 = (A * u * Sa * Tq) * ie;
-      const cplx Ip = (epa * u) * ie;
-      const cplx Iq = (eqb * u) * ie;
-      const cplx Sp = p * Ip * Ip, Sq = q * Iq * Iq;
-      const cplx M0 = (2.0 * (I.h * eta + ehm1)) * ie2;
-      const cplx P0 = 2.0 * ((elh * u) * ie2 - (I.h * el2) * ie);
-      const cplx W00d = A * (Sp + Sq + M0 + p * q * P0);
+      const IvFac f = iv_factors(I, k, C.p[r], C.q[r], C.diag_a[r], C.one_p[r], C.one_q[r]);
       if (gm == 0) {
-        F(li, fLU, j) = cplx{-wmu * H0.im, wmu * H0.re};
-        F(li, fRU, j) = J0;
-        F(li, fD1, j) = cplx{-wmu * W00d.im, wmu * W00d.re};
-        F(li, fPiu, j) = theta;
+        F(li, fLU, j) = cplx{-wmu * f.H0.im, wmu * f.H0.re};
+        F(li, fRU, j) = f.J0;
+        F(li, fD1, j) = cplx{-wmu * f.W00d.im, wmu * f.W00d.re};
+        F(li, fPiu, j) = f.theta;
       } else {
-        const cplx H1 = (u * Mab) * iDp;
-        F(li, fL0v, j) = (cplx{0.0, wmu} + eta2 * isk) * H0;
-        F(li, fL0s, j) = H0 * isk;
-        F(li, fL1s, j) = H1 * isk;
-        F(li, fR0, j) = J0;
-        F(li, fR1, j) = -(A * u * Sa * TMq);
-        const cplx W11d = A * (eta2 * (Sp + Sq) + 2.0 * u - 2.0 * p * q * elh * u) - cplx{2.0 * I.h, 0.0};
-        const cplx W20d = eta2 * W00d - cplx{2.0 * I.h, 0.0};
-        F(li, fD25, j) = cplx{-wmu * W00d.im, wmu * W00d.re} + W20d * isk;
-        F(li, fD3, j) = -(W11d * isk);
-        F(li, fD4, j) = (A * eta * (Sq - Sp)) * isk;
-        F(li, fPic, j) = theta;
+        F(li, fL0v, j) = (cplx{0.0, wmu} + k.eta2 * isk) * f.H0;
+        F(li, fL0s, j) = f.H0 * isk;
+        F(li, fL1s, j) = f.H1 * isk;
+        F(li, fR0, j) = f.J0;
+        F(li, fR1, j) = f.J1;
+        F(li, fD25, j) = cplx{-wmu * f.W00d.im, wmu * f.W00d.re} + f.W20d * isk;
+        F(li, fD3, j) = -(f.W11d * isk);
+        F(li, fD4, j) = f.W10d * isk;
+        F(li, fPic, j) = f.theta;
       }
     }
   }
@@ -1144,6 +1009,120 @@ __global__ void __launch_bounds__(kGreenThreads) vfunc_probe_kernel(const GreenP
   }
 }
 
+
+// Layered-model API probes (emie_cu_spectral_states / emie_cu_moment_tables):
+// the Green's build's own device code at caller-given lambdas, one CTA per
+// lambda, for the drop-in's build_spectral_state and vertical_moment_tables
+// (layered.hpp:56-57, 97-103).
+__device__ __forceinline__ Chunk probe_chunk(cplx* s, int NL, int nz) {
+  Chunk C;  // the assemble kernel's SMEM plan for one lambda (lc = 1)
+  C.eta = s; s += NL;
+  C.e2l = s; s += NL;
+  C.em1 = s; s += NL;
+  C.p = s; s += 2 * NL;
+  C.q = s; s += 2 * NL;
+  C.one_p = s; s += 2 * NL;
+  C.one_q = s; s += 2 * NL;
+  C.diag_a = s; s += 2 * NL;
+  C.ieta = s; s += NL;
+  C.F = s; s += static_cast<size_t>(kFields) * nz;
+  C.lam = reinterpret_cast<double*>(s);
+  C.E = reinterpret_cast<int*>(C.lam + 8);
+  return C;
+}
+constexpr int kProbeSmemPerNL = 14;  // complex per layer of probe_chunk
+
+// out[t][gamma][9][NL] = sig eta p q one_p one_q e2l em1_2l diag_a
+// (SpectralLayerState, layered.hpp:41-58; gamma 0 unit, 1 cond)
+__global__ void state_probe_kernel(const GreenParams P, const double* __restrict__ lam, cplx* __restrict__ out) {
+  extern __shared__ cplx sm[];
+  const int NL = P.L + 1;
+  const Chunk C = probe_chunk(sm, NL, P.nz);
+  chunk_layer_states(P, C, 1.0, blockIdx.x, 1, threadIdx.x, blockDim.x, true, lam);
+  __syncthreads();
+  cplx* o = out + static_cast<size_t>(blockIdx.x) * 2 * 9 * NL;
+  for (int x = threadIdx.x; x < 2 * NL; x += blockDim.x) {
+    const int g = x / NL, m = x - g * NL, r = g * NL + m;
+    cplx* og = o + g * 9 * NL;
+    og[m] = P.sig[m];
+    og[NL + m] = C.eta[m];
+    og[2 * NL + m] = C.p[r];
+    og[3 * NL + m] = C.q[r];
+    og[4 * NL + m] = C.one_p[r];
+    og[5 * NL + m] = C.one_q[r];
+    og[6 * NL + m] = C.e2l[m];
+    og[7 * NL + m] = C.em1[m];
+    og[8 * NL + m] = C.diag_a[r];
+  }
+}
+
+// out[t][gamma][6][nz][nz]: the vertical moment tables of both gammas in the
+// pair order (0,0) (1,0) (0,1) (1,1) (2,0) (0,2) (VerticalMomentTable,
+// layered.hpp:83-103). Diagonal entries from the interval factors; an upper
+// entry (i < j) is row factor x chain of the intervening thetas x column
+// factor; lower entries by reciprocity, weighted by sigma_i / sigma_j for
+// the conductive gamma (layered.cpp:363-376).
+__global__ void table_probe_kernel(const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ lam,
+                                   cplx* __restrict__ out) {
+  extern __shared__ cplx sm[];
+  const int NL = P.L + 1, nz = P.nz;
+  const Chunk C = probe_chunk(sm, NL, nz);
+  IvFac* fac = reinterpret_cast<IvFac*>(sm + kProbeSmemPerNL * NL + static_cast<size_t>(kFields) * nz + 8);
+  cplx* eta2 = reinterpret_cast<cplx*>(fac + 2 * nz);
+  chunk_layer_states(P, C, 1.0, blockIdx.x, 1, threadIdx.x, blockDim.x, true, lam);
+  __syncthreads();
+  for (int x = threadIdx.x; x < 2 * nz; x += blockDim.x) {
+    const int g = x / nz, j = x - g * nz;
+    const Interval I = iv[j];
+    const IvPack k = iv_pack(I, C.eta[I.layer], C.ieta[I.layer], C.e2l[I.layer]);
+    const int r = g * NL + I.layer;
+    fac[x] = iv_factors(I, k, C.p[r], C.q[r], C.diag_a[r], C.one_p[r], C.one_q[r]);
+    if (g == 0) eta2[j] = k.eta2;
+  }
+  __syncthreads();
+  const size_t nz2 = static_cast<size_t>(nz) * nz;
+  cplx* o = out + static_cast<size_t>(blockIdx.x) * 12 * nz2;
+  // upper triangle and diagonal: one thread per (gamma, row)
+  for (int x = threadIdx.x; x < 2 * nz; x += blockDim.x) {
+    const int g = x / nz, i = x - g * nz;
+    const IvFac* f = fac + g * nz;
+    cplx* w = o + static_cast<size_t>(g) * 6 * nz2;
+    const size_t d = static_cast<size_t>(i) * nz + i;
+    w[d] = f[i].W00d;
+    w[nz2 + d] = f[i].W10d;
+    w[2 * nz2 + d] = f[i].W10d;
+    w[3 * nz2 + d] = f[i].W11d;
+    w[4 * nz2 + d] = f[i].W20d;
+    w[5 * nz2 + d] = f[i].W20d;
+    cplx chain = {1.0, 0.0};
+    for (int j = i + 1; j < nz; ++j) {
+      const size_t e = static_cast<size_t>(i) * nz + j;
+      const cplx b0 = f[i].H0 * chain, b1 = f[i].H1 * chain;
+      const cplx w00 = b0 * f[j].J0;
+      w[e] = w00;
+      w[nz2 + e] = b1 * f[j].J0;
+      w[2 * nz2 + e] = b0 * f[j].J1;
+      w[3 * nz2 + e] = b1 * f[j].J1;
+      w[4 * nz2 + e] = eta2[i] * w00;
+      w[5 * nz2 + e] = eta2[j] * w00;
+      chain = chain * f[j].theta;
+    }
+  }
+  __syncthreads();
+  // lower triangle: reciprocity, derivative roles swapped (10 <-> 01, 20 <-> 02)
+  constexpr int kSwap[6] = {0, 2, 1, 3, 5, 4};
+  for (size_t x = threadIdx.x; x < 2 * nz2; x += blockDim.x) {
+    const int g = static_cast<int>(x / nz2);
+    const int rem = static_cast<int>(x - g * nz2), i = rem / nz, j = rem - i * nz;
+    if (i <= j) continue;
+    cplx ratio = {1.0, 0.0};
+    if (g == 1) ratio = cdiv(P.sig[iv[i].layer], P.sig[iv[j].layer]);
+    cplx* w = o + static_cast<size_t>(g) * 6 * nz2;
+    for (int q = 0; q < 6; ++q)
+      w[q * nz2 + static_cast<size_t>(i) * nz + j] = ratio * w[kSwap[q] * nz2 + static_cast<size_t>(j) * nz + i];
+  }
+}
+
 // x <-> y mirror of a square grid with hx == hy: the block of offset (oj, oi)
 // is the block of (oi, oj) with xx <-> yy and xz <-> yz exchanged (zz and xy
 // unchanged) -- the horizontal isotropy of the layered medium; measured on the
@@ -1295,7 +1274,7 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
 
 void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
                  const double* breaks, double hx, double hy, const FilterParams& fp, GreenParams& P,
-                 std::vector<Interval>& ivh);
+                 std::vector<Interval>& ivh, bool grid_checks = true);
 
 void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
                      int n, const double* lam, cplx* out) {
@@ -1326,6 +1305,47 @@ void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const
   release(dout, st);
 }
 
+// build_spectral_state / vertical_moment_tables at n lambdas (the drop-in's
+// layered API): what = 0 states [n][2][9][L+1], 1 tables [n][2][6][nz][nz]
+void layered_probe_host(int what, int L, const double* tops, const cplx* sigma, int nz, const double* breaks,
+                        double omega, int n, const double* lam, cplx* out) {
+  if (n <= 0) return;
+  GreenParams P;
+  std::vector<Interval> ivh;
+  if (what == 0 && nz < 1) {  // states need no partition: a one-interval stand-in inside layer 1
+    const double top = tops[0], bot = L > 1 ? tops[1] : tops[0] + 1.0;
+    const double br[2] = {top, std::min(bot, top + 1.0)};
+    green_setup(1, 1, 1, omega, L, tops, sigma, br, 1.0, 1.0, FilterParams{}, P, ivh, false);
+  } else {
+    green_setup(1, 1, nz, omega, L, tops, sigma, breaks, 1.0, 1.0, FilterParams{}, P, ivh, false);
+  }
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  const int NL = L + 1;
+  const size_t per = what == 0 ? 18 * static_cast<size_t>(NL) : 12 * static_cast<size_t>(nz) * nz;
+  Interval* div = scratch<Interval>(ivh.size(), st);
+  double* dl = scratch<double>(n, st);
+  cplx* dout = scratch<cplx>(static_cast<size_t>(n) * per, st);
+  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), ivh.size() * sizeof(Interval), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemcpyAsync(dl, lam, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  const size_t smem = (kProbeSmemPerNL * static_cast<size_t>(NL) + kFields * static_cast<size_t>(P.nz) + 8) *
+                          sizeof(cplx) + 2 * static_cast<size_t>(P.nz) * (sizeof(IvFac) + sizeof(cplx));
+  if (what == 0) {
+    set_smem(reinterpret_cast<const void*>(state_probe_kernel), smem);
+    state_probe_kernel<<<n, 64, smem, st>>>(P, dl, dout);
+    check_launch("state_probe_kernel");
+  } else {
+    set_smem(reinterpret_cast<const void*>(table_probe_kernel), smem);
+    table_probe_kernel<<<n, 128, smem, st>>>(P, div, dl, dout);
+    check_launch("table_probe_kernel");
+  }
+  EMIE_CUDA(cudaMemcpyAsync(out, dout, static_cast<size_t>(n) * per * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  release(div, st);
+  release(dl, st);
+  release(dout, st);
+}
+
 // The computed offsets of a build: all, or on a square grid with hx == hy only
 // oi <= oj (the rest by the x <-> y mirror, mirror_blocks_kernel)
 std::vector<int> computed_offsets(int nx, int ny, double hx, double hy) {
@@ -1345,7 +1365,7 @@ std::vector<int> computed_offsets(int nx, int ny, double hx, double hy) {
 // 191-208; greens.cpp:18-35), the kernel parameters and the interval table
 void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
                  const double* breaks, double hx, double hy, const FilterParams& fp, GreenParams& P,
-                 std::vector<Interval>& ivh) {
+                 std::vector<Interval>& ivh, bool grid_checks) {
   if (L < 1) fail(EMIE_CU_INVALID_ARGUMENT, "layered model needs at least one interface");
   if (L + 1 > kMaxLayers) fail(EMIE_CU_INVALID_ARGUMENT, "layered model: too many layers for the device build");
   for (int i = 0; i + 1 < L; ++i)
@@ -1395,7 +1415,7 @@ void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops
     const double slack = 1e-7 * (1.0 + std::fabs(breaks[i + 1]));
     if (m < L && breaks[i + 1] > bottom_of(m) + slack)
       fail(EMIE_CU_INVALID_ARGUMENT, "vertical partition: interval straddles a layer interface");
-    if (!(sigma[m].re > 0.0))
+    if (grid_checks && !(sigma[m].re > 0.0))
       fail(EMIE_CU_INVALID_ARGUMENT,
            "grid: interval in a non-conducting layer; the anomaly must be buried in the conductive section");
     Interval& I = ivh[i];

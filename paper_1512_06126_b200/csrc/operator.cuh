@@ -157,6 +157,12 @@ void assemble_signed_host(int nx, int ny, int nz, double omega, int L, const dou
                           const double* breaks, double hx, double hy, const FilterParams& fp, int n, const int* oi,
                           const int* oj, cplx* h_out);
 void dense_apply_host(int nx, int ny, int nz, const cplx* h_blocks, const cplx* h_in, cplx* h_out);
+void layered_probe_host(int what, int L, const double* tops, const cplx* sigma, int nz, const double* breaks,
+                        double omega, int n, const double* lam, cplx* out);
+void fundamental_values_host(int L, const double* tops, const cplx* st9, int gamma, int n, const double* z,
+                             const double* zs, const int* ord, cplx* out);
+void point_moments_host(int L, const double* tops, const cplx* st9, int gamma, int nz, const double* breaks,
+                        const int* layer, int n, const double* zobs, cplx* out);
 void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
                      int n, const double* lam, cplx* out);
 

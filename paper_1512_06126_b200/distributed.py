@@ -162,6 +162,9 @@ def torch_all_to_all(group=None):
 
     def a2a(sends, recv_shapes):
         ins = [torch.view_as_real(s.contiguous()).reshape(-1) for s in sends]
+        dev = ins[0].device
+        if use_p2p and dev.type != "cpu":  # gloo point-to-point moves host tensors only
+            ins = [t.cpu() for t in ins]
         outs = [torch.empty(int(np.prod(sh)) * 2, dtype=torch.float64, device=ins[0].device) for sh in recv_shapes]
         if use_p2p:
             me = dist.get_rank(group)
@@ -176,6 +179,8 @@ def torch_all_to_all(group=None):
                 r.wait()
         else:
             dist.all_to_all(outs, ins, group=group)
+        if outs[0].device != dev:
+            outs = [o.to(dev) for o in outs]
         return [torch.view_as_complex(o.view(-1, 2)).view(sh) for o, sh in zip(outs, recv_shapes)]
     return a2a
 
@@ -528,6 +533,25 @@ def greens_offset_ranges(n_offsets: int, G: int) -> List[tuple]:
     return [(s[g], s[g + 1]) for g in range(G)]
 
 
+def sharded_block_arrays(nx, ny, nz, offsets, G: int, ranks: Sequence[int], compute, zeros, reduce_blocks):
+    """The offset-sharded half of the Green's build: the
+    build's computed offsets are split into G contiguous ranges; each listed
+    rank computes its range into a zeroed (ny, nx, 2nz(2nz+1)) block array
+    (compute(c0, c1, buf)), and reduce_blocks sums the arrays over all ranks --
+    every offset is written by exactly one rank, so the sum is exact -- and
+    returns each listed rank's copy. compute / zeros / reduce_blocks are the
+    device build, torch CUDA tensors and NCCL in production; the CPU tests
+    plug in the numpy oracle, host tensors and gloo."""
+    rng = greens_offset_ranges(len(offsets), G)
+    nent = 2 * nz * (2 * nz + 1)
+    bufs = []
+    for g in ranks:
+        b = zeros((ny, nx, nent))
+        compute(rng[g][0], rng[g][1], b)
+        bufs.append(b)
+    return reduce_blocks(bufs)
+
+
 def sharded_greens_build(grid, model, omega: float, plan: ShardPlan, ranks: Sequence[int], reduce_blocks,
                          params=None):
     """The Green's build sharded by offset: each listed
@@ -539,14 +563,10 @@ def sharded_greens_build(grid, model, omega: float, plan: ShardPlan, ranks: Sequ
     import torch
     from . import greens_offsets, greens_blocks, operator_from_greens_blocks
     offs = greens_offsets(grid.nx, grid.ny, grid.hx, grid.hy)
-    rng = greens_offset_ranges(len(offs), plan.G)
-    nent = 2 * grid.nz * (2 * grid.nz + 1)
-    bufs = []
-    for g in ranks:
-        b = torch.zeros((grid.ny, grid.nx, nent), dtype=torch.complex128, device="cuda")
-        greens_blocks(grid, model, omega, rng[g][0], rng[g][1], b, params)
-        bufs.append(b)
-    full = reduce_blocks(bufs)
+    full = sharded_block_arrays(
+        grid.nx, grid.ny, grid.nz, offs, plan.G, ranks,
+        lambda c0, c1, b: greens_blocks(grid, model, omega, c0, c1, b, params),
+        lambda shape: torch.zeros(shape, dtype=torch.complex128, device="cuda"), reduce_blocks)
     return [operator_from_greens_blocks(grid, omega, full[i], plan.q[g], plan.q[g + 1])
             for i, g in enumerate(ranks)]
 
