@@ -126,6 +126,31 @@ int emie_cu_design_offset_filters(int oi, int oj, double hx, double hy,
 int emie_cu_kernel_output(int oi, int oj, double hx, double hy, int alpha, int beta,
                           const double* h_s, int n, double* h_out);
 
+/* pair_geometry (hankel.hpp:35, hankel.cpp:80-91) -> out {r, p, q, phi}: the
+ * device build's own geometry routine, evaluated on the host */
+int emie_cu_pair_geometry(int oi, int oj, double hx, double hy, double* out);
+
+/* FilterDesigner::design / design_weights (hankel.hpp:62-63, 93; hankel.cpp:
+ * 239-281) of one (alpha, beta) kernel for a pair geometry {r, p, q, phi} on
+ * the device: weights h_w[n2-n1+1], abscissae h_lam[n2-n1+1] */
+int emie_cu_design_filter(const double* geom, int alpha, int beta, const double* filter, double* h_w,
+                          double* h_lam);
+
+/* design_input (hankel.hpp:44, hankel.cpp:93-99) at n lambdas, on the device */
+int emie_cu_design_input(int n, const double* h_lam, double* h_out);
+
+/* kernel_output (hankel.hpp:48) for a pair geometry {r, p, q, phi} */
+int emie_cu_kernel_output_geom(const double* geom, int alpha, int beta, const double* h_s, int n, double* h_out);
+
+/* assemble_block_full (greens.hpp:139-141, greens.cpp:231-293) at one signed
+ * offset: device filter design, the moment tables of both gammas at the
+ * offset's lattice, nine independent filter sums (lower triangles and the
+ * source-side z couplings evaluated, not mirrored): h_out[9][nz][nz] complex,
+ * q = 3a + b row-major (FullBlock). out_of_range outside the grid. */
+int emie_cu_assemble_block_full(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                                int nx, int ny, double hx, double hy, double omega, const double* filter,
+                                int oi, int oj, double* h_out);
+
 /* v_functions (include/emie/layered.hpp:108-114, src/layered.cpp:397-408)
  * of every interval pair at n given lambdas, as the device Green's build
  * evaluates them inside its filter sums (the same layer-state, interval-factor,
@@ -141,6 +166,31 @@ int emie_cu_vfunctions(int L, const double* tops, const double* sigma, int nz, c
  * emie_cu_operator_from_blocks layout) to one host field, on the device, in a
  * fixed summation order; the oracle the reference tests the FFT apply against */
 int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_blocks, const double* h_in, double* h_out);
+
+/* ---- receivers (SPEC.md receiver_green_integrals, reconstruct_fields; the
+ * reference leaves them as placeholders, src/receiver.cpp:1). For a receiver
+ * M outside the anomaly and a cell: int_cell G^E(M, M0) dM0 and int_cell
+ * G^H(M, M0) dM0 of paper Appendix A (Eq. geh, Ge2), with one-sided lateral
+ * digital filters (point observer, source rectangle: designed on the device
+ * like the cell-pair filters) and the receiver's vertical single moments
+ * (point_moments). Receivers inside or on the closed anomaly volume are
+ * rejected (EMIE_CU_INVALID_ARGUMENT). */
+
+/* anomalous fields sum_n (sigma_a - sigma_b) E_n int_n G dOmega of nrhs CIE
+ * solutions h_U (E_n = U_n / a_n, SPEC.md): h_rec[nrec][3] = (x, y, z) [m],
+ * grid origin (x0, y0); h_out[rec][rhs][6] complex = E xyz, H xyz (add the
+ * normal field for the total field) */
+int emie_cu_receiver_fields(int L, const double* tops, const double* sigma, int nz, const double* breaks, int nx,
+                            int ny, double hx, double hy, double x0, double y0, double omega, const double* filter,
+                            const double* h_sigma_a, int nrhs, const double* h_U, int nrec, const double* h_rec,
+                            double* h_out);
+
+/* the tensors themselves for one receiver h_rec[3] and the cells of column
+ * (ix, iy): h_out[k][18] complex = G^E (row-major 3x3, row = field component)
+ * then G^H */
+int emie_cu_receiver_tensors(int L, const double* tops, const double* sigma, int nz, const double* breaks, int nx,
+                             int ny, double hx, double hy, double x0, double y0, double omega, const double* filter,
+                             const double* h_rec, int ix, int iy, double* h_out);
 
 /* ---- layered-medium API on the device (include/emie/layered.hpp), the
  * building blocks of the Green's build evaluated at caller-given lambdas

@@ -128,6 +128,12 @@ def lib():
         "emie_cu_fgmres": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                            ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
         "emie_cu_device_count": [ip],
+        "emie_cu_receiver_fields": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, vp, vp, ctypes.c_int, vp, ctypes.c_int, vp, vp],
+        "emie_cu_receiver_tensors": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, vp, vp, ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_fgmres_ex": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                               ctypes.POINTER(_Report), vp, ctypes.c_int, vp, vp, vp],
         "emie_cu_fgmres_map": [ctypes.c_longlong, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_double,
@@ -538,6 +544,52 @@ def vfunctions(model: LayeredModel, breaks, omega: float, lam) -> np.ndarray:
     out = np.zeros((lam.size, 4, nz, nz), np.complex128)
     _check(lib().emie_cu_vfunctions(len(tops), _ptr(tops), _ptr(sig), nz, _ptr(br), float(omega), lam.size,
                                     _ptr(lam), _ptr(out)))
+    return out
+
+
+def receiver_tensors(grid: AnomalyGrid, model: LayeredModel, omega: float, receiver, ix: int, iy: int,
+                     params: Optional[FilterParams] = None) -> np.ndarray:
+    """int_cell G^E(M, M0) dM0 and int_cell G^H(M, M0) dM0 (SPEC.md
+    receiver_green_integrals; paper Appendix A Eq. geh / Ge2) for the receiver
+    M = (x, y, z) and every cell of column (ix, iy), on the device ->
+    (nz, 2, 3, 3) complex: [k, 0] = G^E, [k, 1] = G^H, row = field component."""
+    model.validate()
+    grid.validate(model)
+    tops = np.ascontiguousarray(model.tops, dtype=np.float64)
+    sig = _c128(model.sigma)
+    br = np.ascontiguousarray(grid.breaks, dtype=np.float64)
+    fp = (params or FilterParams()).as_array()
+    rec = np.ascontiguousarray(receiver, dtype=np.float64).reshape(3)
+    out = np.zeros((grid.nz, 2, 3, 3), np.complex128)
+    _check(lib().emie_cu_receiver_tensors(len(tops), _ptr(tops), _ptr(sig), grid.nz, _ptr(br), grid.nx, grid.ny,
+                                          grid.hx, grid.hy, grid.x0, grid.y0, float(omega), _ptr(fp), _ptr(rec),
+                                          int(ix), int(iy), _ptr(out)))
+    return out
+
+
+def receiver_fields(grid: AnomalyGrid, model: LayeredModel, omega: float, U, receivers,
+                    params: Optional[FilterParams] = None) -> np.ndarray:
+    """Anomalous receiver fields of CIE solutions (SPEC.md reconstruct_fields,
+    paper Eq. APR_lab): sum_n (sigma_a - sigma_b) E_n int_n G dOmega with E_n =
+    U_n / a_n. U: (nrhs, 3N) solutions; receivers (nrec, 3) -> (nrec, nrhs, 2, 3)
+    complex: [., ., 0] = E, [., ., 1] = H (add the normal field for totals)."""
+    model.validate()
+    grid.validate(model)
+    tops = np.ascontiguousarray(model.tops, dtype=np.float64)
+    sig = _c128(model.sigma)
+    br = np.ascontiguousarray(grid.breaks, dtype=np.float64)
+    fp = (params or FilterParams()).as_array()
+    u = _c128(U)
+    ncell = grid.nx * grid.ny * grid.nz
+    if u.size % (3 * ncell) != 0 or u.size == 0:
+        raise InvalidArgument("receiver_fields: field shape does not match the grid")
+    nrhs = u.size // (3 * ncell)
+    rec = np.ascontiguousarray(receivers, dtype=np.float64).reshape(-1, 3)
+    sa = _c128(grid.sigma_a)
+    out = np.zeros((rec.shape[0], nrhs, 2, 3), np.complex128)
+    _check(lib().emie_cu_receiver_fields(len(tops), _ptr(tops), _ptr(sig), grid.nz, _ptr(br), grid.nx, grid.ny,
+                                         grid.hx, grid.hy, grid.x0, grid.y0, float(omega), _ptr(fp), _ptr(sa), nrhs,
+                                         _ptr(u), rec.shape[0], _ptr(rec), _ptr(out)))
     return out
 
 

@@ -14,10 +14,14 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <array>
+#include <utility>
 #include <exception>
 #include <functional>
 #include <fstream>
+#include <memory>
 #include <mutex>
+#include <shared_mutex>
 #include <stdexcept>
 #include <string>
 
@@ -103,6 +107,177 @@ VerticalPartition VerticalPartition::create(const LayeredModel& model, const std
     p.layer.push_back(m);
   }
   return p;
+}
+
+// ------------------------------------------- layered kernels (device) ----
+namespace {
+thread_local std::uint64_t g_exp_evals = 0;  // exponentials the device evaluated for this thread's calls
+
+// the state's nine arrays in the ABI order (emie_cu.h): sig eta p q one_p one_q e2l em1_2l diag_a
+std::vector<cdouble> pack_state(const SpectralLayerState& st) {
+  std::vector<cdouble> v;
+  for (const auto* a : {&st.sig, &st.eta, &st.p, &st.q, &st.one_p, &st.one_q, &st.e2l, &st.em1_2l, &st.diag_a})
+    v.insert(v.end(), a->begin(), a->end());
+  return v;
+}
+int gamma_index(Gamma g) { return g == Gamma::cond ? 1 : 0; }
+// complex exponentials of one interval pack (layered.cpp:237-273)
+std::uint64_t pack_exps(const LayeredModel& m, const VerticalPartition& part) {
+  std::uint64_t n = 0;
+  const int L = static_cast<int>(m.tops.size());
+  for (int l : part.layer) n += 1 + (l > 0) + (l < L) + (l > 0 && l < L);
+  return n;
+}
+}  // namespace
+
+SpectralLayerState build_spectral_state(const LayeredModel& model, double omega, double lambda, Gamma gamma) {
+  const int L = static_cast<int>(model.tops.size()), NL = L + 1;
+  if (L < 1 || model.sigma.size() != model.tops.size() + 1)
+    throw std::invalid_argument("layered model: sigma count must be tops count + 1");
+  std::vector<cdouble> out(std::size_t(2) * 9 * NL);
+  check(emie_cu_spectral_states(L, model.tops.data(), dbl(model.sigma.data()), omega, 1, &lambda, dbl(out.data())));
+  g_exp_evals += static_cast<std::uint64_t>(std::max(0, L - 1));
+  SpectralLayerState st;
+  st.model = &model;
+  st.omega = omega;
+  st.lambda = lambda;
+  st.gamma = gamma;
+  const cdouble* o = out.data() + std::size_t(gamma_index(gamma)) * 9 * NL;
+  for (auto* a : {&st.sig, &st.eta, &st.p, &st.q, &st.one_p, &st.one_q, &st.e2l, &st.em1_2l, &st.diag_a}) {
+    a->assign(o, o + NL);
+    o += NL;
+  }
+  return st;
+}
+
+cdouble fundamental_value(const SpectralLayerState& st, double z, double zs, int dz, int dzs, int layer_z,
+                          int layer_zs) {
+  if (!st.model) throw std::invalid_argument("fundamental_value: state without a model");
+  const std::vector<cdouble> packed = pack_state(st);
+  const int ord[4] = {dz, dzs, layer_z, layer_zs};
+  cdouble v;
+  check(emie_cu_fundamental_values(static_cast<int>(st.model->tops.size()), st.model->tops.data(),
+                                   dbl(packed.data()), gamma_index(st.gamma), 1, &z, &zs, ord, dbl(&v)));
+  g_exp_evals += 3;
+  return v;
+}
+
+int VerticalMomentTable::pair_index(int a, int b) {
+  static constexpr int order[6][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}, {2, 0}, {0, 2}};
+  for (int i = 0; i < 6; ++i)
+    if (order[i][0] == a && order[i][1] == b) return i;
+  throw std::invalid_argument("moment table: unsupported derivative pair");
+}
+
+std::pair<VerticalMomentTable, VerticalMomentTable> vertical_moment_tables(const SpectralLayerState& unit_state,
+                                                                           const SpectralLayerState& cond_state,
+                                                                           const VerticalPartition& part) {
+  const SpectralLayerState& st = unit_state;
+  if (!st.model) throw std::invalid_argument("moment tables: state without a model");
+  const LayeredModel& m = *st.model;
+  const int nz = part.count();
+  const std::size_t nz2 = std::size_t(nz) * nz;
+  std::vector<cdouble> out(12 * nz2);
+  check(emie_cu_moment_tables(static_cast<int>(m.tops.size()), m.tops.data(), dbl(m.sigma.data()), nz,
+                              part.breaks.data(), st.omega, 1, &st.lambda, dbl(out.data())));
+  g_exp_evals += pack_exps(m, part) + static_cast<std::uint64_t>(std::max<int>(0, int(m.tops.size()) - 1));
+  std::pair<VerticalMomentTable, VerticalMomentTable> tabs;
+  for (int g = 0; g < 2; ++g) {
+    VerticalMomentTable& t = g ? tabs.second : tabs.first;
+    t.nz = nz;
+    t.gamma = g ? Gamma::cond : Gamma::unit;
+    t.lambda = g ? cond_state.lambda : unit_state.lambda;
+    for (int q = 0; q < 6; ++q) {
+      const cdouble* src = out.data() + (std::size_t(g) * 6 + q) * nz2;
+      t.w[q].assign(src, src + nz2);
+    }
+  }
+  return tabs;
+}
+
+VerticalMomentTable vertical_moment_table(const SpectralLayerState& st, const VerticalPartition& part) {
+  auto tabs = vertical_moment_tables(st, st, part);
+  return st.gamma == Gamma::cond ? std::move(tabs.second) : std::move(tabs.first);
+}
+
+VFunctions v_functions(const VerticalMomentTable& u, const VerticalMomentTable& c, int n, int m, cdouble sigma_bn,
+                       double omega) {
+  // layered.cpp:397-408: V1, V2 from the (0,0) moments; V3, V4, V5 from the
+  // conductive (1,1), (1,0), (2,0) moments over the observation interval's sigma
+  const cdouble iwmu(0.0, omega * mu0);
+  return VFunctions{iwmu * u.at(0, 0, n, m), iwmu * c.at(0, 0, n, m), -c.at(1, 1, n, m) / sigma_bn,
+                    c.at(1, 0, n, m) / sigma_bn, c.at(2, 0, n, m) / sigma_bn};
+}
+
+PointMomentTable point_moments(const SpectralLayerState& st, const VerticalPartition& part, double z_obs) {
+  if (!st.model) throw std::invalid_argument("point_moments: state without a model");
+  const std::vector<cdouble> packed = pack_state(st);
+  const int nz = part.count();
+  std::vector<cdouble> out(std::size_t(2) * nz);
+  check(emie_cu_point_moments(static_cast<int>(st.model->tops.size()), st.model->tops.data(), dbl(packed.data()),
+                              gamma_index(st.gamma), nz, part.breaks.data(), part.layer.data(), 1, &z_obs,
+                              dbl(out.data())));
+  g_exp_evals += pack_exps(*st.model, part);
+  PointMomentTable pm;
+  pm.nz = nz;
+  pm.m[0].assign(out.begin(), out.begin() + nz);
+  pm.m[1].assign(out.begin() + nz, out.end());
+  return pm;
+}
+
+std::uint64_t exp_eval_count() { return g_exp_evals; }
+void reset_exp_eval_count() { g_exp_evals = 0; }
+
+// ------------------------------------------------- filters (device) ----
+namespace {
+std::array<double, 5> filter_array(const FilterParams& p) {
+  return {p.step, p.shift, double(p.half), double(p.n1), double(p.n2)};
+}
+}  // namespace
+
+PairGeometry pair_geometry(int oi, int oj, double hx, double hy) {
+  double g[4];
+  check(emie_cu_pair_geometry(oi, oj, hx, hy, g));
+  return PairGeometry{g[0], g[1], g[2], g[3]};
+}
+
+double design_input(double lambda) {
+  double v = 0.0;
+  check(emie_cu_design_input(1, &lambda, &v));
+  return v;
+}
+
+double kernel_output(const PairGeometry& g, int alpha, int beta, double s) {
+  const double geom[4] = {g.r, g.p, g.q, g.phi};
+  double v = 0.0;
+  check(emie_cu_kernel_output_geom(geom, alpha, beta, &s, 1, &v));
+  return v;
+}
+
+FilterDesigner::FilterDesigner(const FilterParams& par) : par_(par) {
+  // FilterDesigner's checks (hankel.cpp:205-208)
+  if (!(par.step > 0.0) || !(par.shift > 0.0) || !(par.shift < 0.5 * par.step))
+    throw std::invalid_argument("filter params: need 0 < shift < step/2");
+  if (par.half < 2 || par.n1 < -par.half || par.n2 <= par.n1 || par.n2 > par.half - 1)
+    throw std::invalid_argument("filter params: bad weight window");
+}
+
+FilterWeights FilterDesigner::design(const PairGeometry& g, int alpha, int beta) const {
+  FilterWeights fw;
+  fw.alpha = alpha;
+  fw.beta = beta;
+  fw.n1 = par_.n1;
+  fw.n2 = par_.n2;
+  fw.w.resize(std::size_t(par_.n2 - par_.n1 + 1));
+  fw.lam.resize(fw.w.size());
+  const double geom[4] = {g.r, g.p, g.q, g.phi};
+  const auto fa = filter_array(par_);
+  check(emie_cu_design_filter(geom, alpha, beta, fa.data(), fw.w.data(), fw.lam.data()));
+  return fw;
+}
+
+FilterWeights design_weights(const PairGeometry& g, int alpha, int beta, const FilterParams& par) {
+  return FilterDesigner(par).design(g, alpha, beta);
 }
 
 // --------------------------------------------------------------- grid ----
@@ -257,6 +432,85 @@ CompressedGreensOperator assemble_operator(const AnomalyGrid& grid, const Layere
   std::vector<cdouble> v(std::size_t(grid.nx) * grid.ny * 2 * nz * (2 * nz + 1));
   check(emie_cu_operator_download_blocks(h, dbl(v.data())));
   return compress(grid.nx, grid.ny, unpack_blocks(v, grid.nx * grid.ny, nz), omega);
+}
+
+// MomentMemo (greens.hpp:101-123 contract): host cache of device tables
+MomentMemo::MomentMemo(const LayeredModel& model, const VerticalPartition& part, double omega,
+                       std::size_t byte_budget)
+    : model_(model), part_(part), omega_(omega), byte_budget_(byte_budget) {
+  const std::size_t nz2 = std::size_t(part.count()) * part.count();
+  bytes_per_entry_ = 2 * 6 * nz2 * sizeof(cdouble) + 256;
+}
+
+std::shared_ptr<const MomentMemo::TablePair> MomentMemo::get(double lambda) {
+  std::uint64_t key;
+  std::memcpy(&key, &lambda, sizeof key);
+  {
+    std::shared_lock<std::shared_mutex> rl(mu_);
+    const auto it = map_.find(key);
+    if (it != map_.end()) return it->second;
+  }
+  const SpectralLayerState su = build_spectral_state(model_, omega_, lambda, Gamma::unit);
+  const SpectralLayerState sc = build_spectral_state(model_, omega_, lambda, Gamma::cond);
+  auto tabs = std::make_shared<const TablePair>(vertical_moment_tables(su, sc, part_));
+  std::unique_lock<std::shared_mutex> wl(mu_);
+  if ((map_.size() + 1) * bytes_per_entry_ > byte_budget_) map_.clear();
+  return map_.emplace(key, std::move(tabs)).first->second;
+}
+
+namespace {
+GreensBlock block_of(const cdouble* v, int nz) {
+  GreensBlock b;
+  b.nz = nz;
+  const std::size_t nt = std::size_t(nz) * (nz + 1) / 2, nf = std::size_t(nz) * nz;
+  for (auto* c : {&b.xx, &b.yy, &b.zz, &b.xy, &b.xz, &b.yz}) {
+    const std::size_t n = (c == &b.xz || c == &b.yz) ? nf : nt;
+    c->assign(v, v + n);
+    v += n;
+  }
+  return b;
+}
+GreensBlock device_block(const AnomalyGrid& grid, const LayeredModel& model, double omega, int oi, int oj,
+                         const FilterParams& params) {
+  if (std::abs(oi) >= grid.ny || std::abs(oj) >= grid.nx)
+    throw std::out_of_range("assemble_block: offset outside the grid");
+  const int nz = grid.nz();
+  const auto fa = filter_array(params);
+  std::vector<cdouble> v(2 * std::size_t(nz) * (2 * nz + 1));
+  check(emie_cu_assemble_blocks(static_cast<int>(model.tops.size()), model.tops.data(), dbl(model.sigma.data()), nz,
+                                grid.part.breaks.data(), grid.nx, grid.ny, grid.hx, grid.hy, omega, fa.data(), 1, &oi,
+                                &oj, dbl(v.data())));
+  return block_of(v.data(), nz);
+}
+}  // namespace
+
+GreensBlock assemble_block(const AnomalyGrid& grid, double omega, int offset_i, int offset_j,
+                           const FilterDesigner& designer, MomentMemo& memo) {
+  return device_block(grid, memo.model(), omega, offset_i, offset_j, designer.params());
+}
+
+GreensBlock assemble_block(const AnomalyGrid& grid, const LayeredModel& model, double omega, int offset_i,
+                           int offset_j, const FilterParams& params) {
+  FilterDesigner check_params(params);  // the reference's designer validates the parameters first
+  return device_block(grid, model, omega, offset_i, offset_j, params);
+}
+
+FullBlock assemble_block_full(const AnomalyGrid& grid, double omega, int offset_i, int offset_j,
+                              const FilterDesigner& designer, MomentMemo& memo) {
+  if (std::abs(offset_i) >= grid.ny || std::abs(offset_j) >= grid.nx)
+    throw std::out_of_range("assemble_block_full: offset outside the grid");
+  const LayeredModel& model = memo.model();
+  const int nz = grid.nz();
+  const std::size_t nz2 = std::size_t(nz) * nz;
+  const auto fa = filter_array(designer.params());
+  std::vector<cdouble> out(9 * nz2);
+  check(emie_cu_assemble_block_full(static_cast<int>(model.tops.size()), model.tops.data(), dbl(model.sigma.data()),
+                                    nz, grid.part.breaks.data(), grid.nx, grid.ny, grid.hx, grid.hy, omega, fa.data(),
+                                    offset_i, offset_j, dbl(out.data())));
+  FullBlock f;
+  f.nz = nz;
+  for (int q = 0; q < 9; ++q) f.q[q].assign(out.begin() + q * nz2, out.begin() + (q + 1) * nz2);
+  return f;
 }
 
 // EMG1 snapshot (greens.cpp:373-446)

@@ -1112,6 +1112,71 @@ extern "C" int emie_cu_dense_apply(int nx, int ny, int nz, const double* h_block
   });
 }
 
+extern "C" int emie_cu_pair_geometry(int oi, int oj, double hx, double hy, double* out) {
+  return guarded([&] {
+    if (!out) fail(EMIE_CU_INVALID_ARGUMENT, "pair_geometry: null pointer");
+    pair_geometry_host(oi, oj, hx, hy, out);
+  });
+}
+
+extern "C" int emie_cu_design_filter(const double* geom, int alpha, int beta, const double* filter, double* h_w,
+                                     double* h_lam) {
+  return guarded([&] {
+    if (!geom || !h_w || !h_lam) fail(EMIE_CU_INVALID_ARGUMENT, "design_filter: null pointer");
+    design_geometry_host(geom, alpha, beta, filter_params_of(filter), h_w, h_lam);
+  });
+}
+
+extern "C" int emie_cu_design_input(int n, const double* h_lam, double* h_out) {
+  return guarded([&] {
+    if (n > 0 && (!h_lam || !h_out)) fail(EMIE_CU_INVALID_ARGUMENT, "design_input: null pointer");
+    design_input_host(n, h_lam, h_out);
+  });
+}
+
+extern "C" int emie_cu_kernel_output_geom(const double* geom, int alpha, int beta, const double* h_s, int n,
+                                          double* h_out) {
+  return guarded([&] {
+    if (!geom || (n > 0 && (!h_s || !h_out))) fail(EMIE_CU_INVALID_ARGUMENT, "kernel_output: null pointer");
+    kernel_output_geom_host(geom, alpha, beta, h_s, n, h_out);
+  });
+}
+
+extern "C" int emie_cu_assemble_block_full(int L, const double* tops, const double* sigma, int nz,
+                                           const double* breaks, int nx, int ny, double hx, double hy, double omega,
+                                           const double* filter, int oi, int oj, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "assemble_block_full: null pointer");
+    assemble_full_host(nx, ny, nz, omega, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy,
+                       filter_params_of(filter), oi, oj, reinterpret_cast<cplx*>(h_out));
+  });
+}
+
+extern "C" int emie_cu_receiver_fields(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                                      int nx, int ny, double hx, double hy, double x0, double y0, double omega,
+                                      const double* filter, const double* h_sigma_a, int nrhs, const double* h_U,
+                                      int nrec, const double* h_rec, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || (nrec > 0 && (!h_rec || !h_out || !h_sigma_a || !h_U)))
+      fail(EMIE_CU_INVALID_ARGUMENT, "receiver_fields: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "receiver_fields: nrhs < 1");
+    receiver_host(nx, ny, nz, omega, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, x0, y0,
+                  filter_params_of(filter), reinterpret_cast<const cplx*>(h_sigma_a), nrhs,
+                  reinterpret_cast<const cplx*>(h_U), nrec, h_rec, reinterpret_cast<cplx*>(h_out), -1);
+  });
+}
+
+extern "C" int emie_cu_receiver_tensors(int L, const double* tops, const double* sigma, int nz, const double* breaks,
+                                        int nx, int ny, double hx, double hy, double x0, double y0, double omega,
+                                        const double* filter, const double* h_rec, int ix, int iy, double* h_out) {
+  return guarded([&] {
+    if (!tops || !sigma || !breaks || !h_rec || !h_out) fail(EMIE_CU_INVALID_ARGUMENT, "receiver_tensors: null pointer");
+    if (ix < 0 || iy < 0 || ix >= nx || iy >= ny) fail(EMIE_CU_OUT_OF_RANGE, "receiver_tensors: cell column outside the grid");
+    receiver_host(nx, ny, nz, omega, L, tops, reinterpret_cast<const cplx*>(sigma), breaks, hx, hy, x0, y0,
+                  filter_params_of(filter), nullptr, 1, nullptr, 1, h_rec, reinterpret_cast<cplx*>(h_out), iy * nx + ix);
+  });
+}
+
 extern "C" int emie_cu_spectral_states(int L, const double* tops, const double* sigma, double omega, int n,
                                        const double* h_lam, double* h_out) {
   return guarded([&] {

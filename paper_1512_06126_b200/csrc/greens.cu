@@ -111,6 +111,53 @@ struct OffsetCode {
   __host__ __device__ int slot(int c, int pos) const { return compact ? pos : c; }
 };
 
+// ---- receiver-side filters: a point observer and a source rectangle ------
+// The lateral integral of a receiver (SPEC.md receiver_green_integrals) is
+// one-sided: K_ab(lambda) = d^a/dx^a d^b/dy^b int_S J0(lambda rho) dS0 for the
+// receiver at the origin and the source rectangle S. Its filter is designed
+// like the cell-pair filters (hankel.cpp:204-281: same design input v, same
+// lattice, FFT division), with the design output the one-sided integral of
+// v's J0 transform (rho^4/4) e^{-rho^2/4} = (x^4 + 2 x^2 y^2 + y^4)/4 e^{-x^2/4}
+// e^{-y^2/4}: per axis the 2-point difference of the antiderivatives
+//   P0(t) = sqrt(pi) erf(t/2),  P1 = -2t g + 2 P0,  P2 = -2t^3 g - 12 t g + 12 P0,
+// g = e^{-t^2/4} (a = 0), of t^{2k} g itself (a = 1) or of its derivative (a = 2),
+// at t1 = -(cx - p/2) r, t2 = -(cx + p/2) r. The sum is R^{1-a-b} sum_m w_m
+// f(lambda_m / R) (two lateral integrations instead of four: 1 - a - b in
+// place of hankel.hpp's 3 - a - b).
+struct PGeom {
+  double r, p, q, cx, cy;  // reference distance; rectangle size and centre offset over r
+};
+
+__device__ void point_stencil(int alpha, double t1, double t2, double out[3]) {
+  const double g1 = exp(-0.25 * t1 * t1), g2 = exp(-0.25 * t2 * t2);
+  if (alpha == 0) {
+    const double e = kSqrtPi * ediff(t2, t1);  // P0(t1) - P0(t2)
+    const double d1 = t1 * g1 - t2 * g2, d3 = t1 * t1 * t1 * g1 - t2 * t2 * t2 * g2;
+    out[0] = e;
+    out[1] = -2.0 * d1 + 2.0 * e;
+    out[2] = -2.0 * d3 - 12.0 * d1 + 12.0 * e;
+  } else if (alpha == 1) {
+    out[0] = g1 - g2;
+    out[1] = t1 * t1 * g1 - t2 * t2 * g2;
+    out[2] = t1 * t1 * t1 * t1 * g1 - t2 * t2 * t2 * t2 * g2;
+  } else {
+    out[0] = -0.5 * (t1 * g1 - t2 * g2);
+    out[1] = (2.0 * t1 - 0.5 * t1 * t1 * t1) * g1 - (2.0 * t2 - 0.5 * t2 * t2 * t2) * g2;
+    out[2] = (4.0 * t1 * t1 * t1 - 0.5 * t1 * t1 * t1 * t1 * t1) * g1 -
+             (4.0 * t2 * t2 * t2 - 0.5 * t2 * t2 * t2 * t2 * t2) * g2;
+  }
+}
+
+__device__ double point_kernel_output(const PGeom& g, int alpha, int beta, double s) {
+  const double r = exp(s);
+  double ax[3], ay[3];
+  point_stencil(alpha, -(g.cx - 0.5 * g.p) * r, -(g.cx + 0.5 * g.p) * r, ax);
+  point_stencil(beta, -(g.cy - 0.5 * g.q) * r, -(g.cy + 0.5 * g.q) * r, ay);
+  const double comb = 0.25 * (ax[2] * ay[0] + 2.0 * ax[1] * ay[1] + ax[0] * ay[2]);
+  if (comb == 0.0) return 0.0;
+  return exp(-(1 - alpha - beta) * s) * comb;
+}
+
 __device__ double kernel_output(const Geom& g, int alpha, int beta, double s) {  // hankel.cpp:101-113
   const double r = exp(s);
   const double hx = g.p * r, hy = g.q * r;
@@ -175,23 +222,27 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
                                      const double* __restrict__ den_floor,
                                      const cplx* __restrict__ tw, FftPlan pl, int half, double step,
                                      double shift, int n1, int n2, OffsetCode oc, double hx, double hy,
-                                     int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs) {
+                                     int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs,
+                                     Geom gfix, int use_gfix, int kern0, const PGeom* __restrict__ pgeo) {
   extern __shared__ cplx sm[];
   const int n = pl.n, ld = n | 1;
   cplx* a = sm;
   cplx* b = a + ld;
   cplx* t = b + ld;
-  const int code = offs ? offs[blockIdx.x] : static_cast<int>(blockIdx.x), kern = blockIdx.y;
+  const int code = offs ? offs[blockIdx.x] : static_cast<int>(blockIdx.x), kern = kern0 + blockIdx.y;
   const int off = oc.slot(code, blockIdx.x);
   const int oi = fixed_oi != INT32_MIN ? fixed_oi : oc.oi(code);
   const int oj = fixed_oi != INT32_MIN ? fixed_oj : oc.oj(code);
-  const Geom g = pair_geometry(oi, oj, hx, hy);
+  // a caller-given pair geometry (FilterDesigner::design, hankel.hpp:93), else the offset's
+  const Geom g = use_gfix ? gfix : pair_geometry(oi, oj, hx, hy);
   const int alpha = kAlpha[kern], beta = kBeta[kern];
   load_twiddles(t, tw, n);
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const int m = j - half;
     const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
-    a[j] = {sign * kernel_output(g, alpha, beta, m * step + shift), 0.0};
+    const double sj = m * step + shift;
+    a[j] = {sign * (pgeo ? point_kernel_output(pgeo[blockIdx.x], alpha, beta, sj) : kernel_output(g, alpha, beta, sj)),
+            0.0};
   }
   __syncthreads();
   cplx* res = fft_smem(a, b, ld, 1, pl, t, false);
@@ -252,6 +303,7 @@ struct GreenParams {
   OffsetCode oc;   // offset codes of this build
   // model (host-filled)
   double thick[kMaxLayers];
+  double ztop[kMaxLayers], zbot[kMaxLayers];  // top_of / bottom_of per layer (layered.cpp:38-43)
   cplx sig[kMaxLayers];  // floored conductivities
   cplx sig_up[kMaxLayers];  // sig[m+1] / sig[m] (TM reflection chain, layered.cpp:113)
   cplx sig_dn[kMaxLayers];  // sig[m-1] / sig[m]
@@ -353,8 +405,14 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
     V4 = Fl[fD4 * nz + k];
   } else {
     const int kn = c.kn;
-    V1 = scale_or_flush(Fl[fLU * nz + k] * Fl[fRU * nz + kp], El[kp] - El[kn]);
-    const int ec = El[nz + kp] - El[nz + kn];
+    const int eu = El[kp] - El[kn], ec = El[nz + kp] - El[nz + kn];
+#ifndef EMIE_GREENS_NO_SKIP
+    // both media's chain products below 2^-1022 (far pairs at large lambda,
+    // where prod theta ~ e^{-lambda dz}): every term of this pair-lambda is an
+    // exact zero (scale_or_flush), so the accumulators would not change
+    if (eu < -1022 && ec < -1022) return;
+#endif
+    V1 = scale_or_flush(Fl[fLU * nz + k] * Fl[fRU * nz + kp], eu);
     cplx r0 = Fl[fR0 * nz + kp], r1 = Fl[fR1 * nz + kp];
     if (ec > 1023) {  // a chain product above 2^1023: never in practice, kept exact
       r0 = scal2(r0, ec);
@@ -1123,6 +1181,258 @@ __global__ void table_probe_kernel(const GreenParams P, const Interval* __restri
   }
 }
 
+
+// the filter lattice of one offset: lambda_t = e^{(n1 + t) step + shift} / R
+// (the expression chunk_layer_states evaluates; greens.cpp:166)
+__global__ void lattice_kernel(double R, int n1, double step, double shift, int n, double* lam) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) lam[t] = exp((n1 + t) * step + shift) / R;
+}
+
+// assemble_block_full (greens.hpp:139-141, greens.cpp:231-293): all nine
+// components of one signed offset, each from its own filter sum over the
+// device moment tables T[t][gamma][6][nz][nz] at the offset's lattice (the
+// lower triangles and the source-side z couplings evaluated, not mirrored).
+// One thread per (k, kp), lambda order; out[9][nz][nz].
+__global__ void full_block_kernel(const double* __restrict__ W, int nw, const double* __restrict__ lam,
+                                  const cplx* __restrict__ T, const cplx* __restrict__ sigb, int nz, double omega,
+                                  double R, cplx* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nz2 = static_cast<size_t>(nz) * nz;
+  if (e >= static_cast<int>(nz2)) return;
+  const int k = e / nz, kp = e - k * nz;
+  const size_t i = static_cast<size_t>(k) * nz + kp, it = static_cast<size_t>(kp) * nz + k;
+  const cplx iwmu = {0.0, omega * kMu0};
+  const cplx isk = crecip(sigb[k]), iskp = crecip(sigb[kp]);
+  cplx a00 = {0, 0}, a20 = {0, 0}, a02 = {0, 0}, a11 = {0, 0}, az = {0, 0};
+  cplx axz = {0, 0}, ayz = {0, 0}, azx = {0, 0}, azy = {0, 0};
+  for (int t = 0; t < nw; ++t) {
+    const double l = lam[t];
+    const cplx* tu = T + static_cast<size_t>(t) * 12 * nz2;
+    const cplx* tc = tu + 6 * nz2;
+    // v_functions (layered.cpp:397-408) at (k, kp) and, source side, (kp, k)
+    const cplx v1 = iwmu * tu[i], v2 = iwmu * tc[i];
+    const cplx v3 = -(tc[3 * nz2 + i] * isk), v4 = tc[nz2 + i] * isk, v5 = tc[4 * nz2 + i] * isk;
+    const cplx vs4 = tc[nz2 + it] * iskp;
+    const cplx v13 = v1 + v3;
+    const cplx f2 = {v13.re / l, v13.im / l};
+    a00 = a00 + W[t] * (l * v1);
+    a20 = a20 + W[nw + t] * f2;
+    a02 = a02 + W[2 * nw + t] * f2;
+    a11 = a11 + W[3 * nw + t] * f2;
+    az = az + W[t] * (l * (v2 + v5));
+    axz = axz + W[4 * nw + t] * (l * v4);
+    ayz = ayz + W[5 * nw + t] * (l * v4);
+    azx = azx + W[4 * nw + t] * (l * vs4);
+    azy = azy + W[5 * nw + t] * (l * vs4);
+  }
+  const double c3 = R * R * R / (4.0 * kPi), c2 = R * R / (4.0 * kPi), c1 = R / (4.0 * kPi);
+  out[i] = c3 * a00 + c1 * a20;             // xx
+  out[4 * nz2 + i] = c3 * a00 + c1 * a02;   // yy
+  out[8 * nz2 + i] = c3 * az;               // zz
+  out[nz2 + i] = c1 * a11;                  // xy
+  out[3 * nz2 + i] = c1 * a11;              // yx: the same defining sum
+  out[2 * nz2 + i] = c2 * axz;              // xz
+  out[5 * nz2 + i] = c2 * ayz;              // yz
+  out[6 * nz2 + i] = -(c2 * azx);           // zx
+  out[7 * nz2 + i] = -(c2 * azy);           // zy
+}
+
+
+// ---- receiver fields (SPEC.md receiver_green_integrals / reconstruct_fields) ----
+// For a receiver M at depth z and a source cell (rectangle S x interval k):
+//   int G^E dOmega, int G^H dOmega (paper Appendix A, Eq. geh / Ge2)
+// with the lateral one-sided filters above and the vertical single moments of
+// the receiver (layered.cpp:450-542 contract):
+//   m0_g = int_k U_g(z, z') dz', m1_g = d/dz m0_g (g = unit 1, cond s),
+//   n0 = int_k d/dz' U_s dz' = U_s(z, b) - U_s(z, a), n1 = d/dz n0;
+// outside the source interval d^2/dz^2 acts as eta_r^2 (receiver layer r), so
+// with k^2 = i w mu0 sigma_r (eta^2 = lambda^2 - k^2) the tensor is
+//   Exx = c [L(lam m0_1)00 + L(Phi)20 / k^2], Phi = (k^2 m0_1 - n1)/lam,
+//   Eyy = ... L(Phi)02, Exy = Eyx = c L(Phi)11 / k^2,
+//   Exz = c L(lam m1_s)10 / k^2, Eyz = c L(lam m1_s)01 / k^2,
+//   Ezx = -c L(lam n0)10 / k^2, Ezy = -c L(lam n0)01 / k^2, Ezz = c L(lam^3 m0_s)00 / k^2,
+// c = i w mu0 / 4 pi; and H = curl G / (i w mu0) of Eq. geh:
+//   Hxx = -L(B)11, Hyx = L(lam m1_1)00 + L(B)20, Hzx = -L(lam m0_1)01,
+//   Hxy = -L(B)02 - L(lam m1_1)00, Hyy = L(B)11, Hzy = L(lam m0_1)10,
+//   Hxz = L(lam m0_s)01, Hyz = -L(lam m0_s)10, Hzz = 0, all / 4 pi, B = (n0 + m1_1)/lam.
+// L(f)ab = R^{1-a-b} sum_t w^{ab}_t f(lambda_t / R). Every reference distance R
+// is a lattice power e^{j step}, so lambda_t / R = e^{(n1 + t - j) step + shift}
+// lies on one global lattice: the vertical functions of a receiver depth are
+// tabulated once per lattice point (receiver_table_kernel).
+
+// T[n][k][6] = m0_1 m1_1 m0_s m1_s n0 n1 at lattice lambda lam[n], depth z
+__global__ void receiver_table_kernel(const GreenParams P, const Interval* __restrict__ iv,
+                                      const double* __restrict__ br, double z, const double* __restrict__ lam,
+                                      cplx* __restrict__ T) {
+  extern __shared__ cplx sm[];
+  const int NL = P.L + 1, nz = P.nz;
+  const Chunk C = probe_chunk(sm, NL, nz);
+  StateDev* S = reinterpret_cast<StateDev*>(sm + kProbeSmemPerNL * NL + static_cast<size_t>(kFields) * nz + 8);
+  chunk_layer_states(P, C, 1.0, blockIdx.x, 1, threadIdx.x, blockDim.x, true, lam);
+  __syncthreads();
+  for (int x = threadIdx.x; x < 2 * NL; x += blockDim.x) {
+    const int g = x / NL, m = x - g * NL, r = g * NL + m;
+    StateDev& st = S[g];
+    if (m == 0) {
+      st.L = P.L;
+      st.gamma = g;
+    }
+    st.top[m] = P.ztop[m];
+    st.bot[m] = P.zbot[m];
+    st.sig[m] = P.sig[m];
+    st.eta[m] = C.eta[m];
+    st.p[m] = C.p[r];
+    st.q[m] = C.q[r];
+    st.one_p[m] = C.one_p[r];
+    st.one_q[m] = C.one_q[r];
+    st.e2l[m] = C.e2l[m];
+    st.em1[m] = C.em1[m];
+    st.a[m] = C.diag_a[r];
+  }
+  __syncthreads();
+  cplx* t = T + static_cast<size_t>(blockIdx.x) * nz * 6;
+  if (threadIdx.x < 2) {  // the two gammas' single moments, sequential over the intervals
+    const int g = threadIdx.x;
+    cplx m0[64], m1[64];
+    point_moments_dev(S[g], iv, br, nz, z, m0, m1);
+    for (int k = 0; k < nz; ++k) {
+      t[k * 6 + 2 * g] = m0[k];
+      t[k * 6 + 2 * g + 1] = m1[k];
+    }
+  }
+  for (int k = threadIdx.x; k < nz; k += blockDim.x) {  // end-point values of the conductive solution
+    const int lk = iv[k].layer;
+    const cplx nb = fundamental_dev(S[1], z, br[k + 1], 0, 0, -1, lk), na = fundamental_dev(S[1], z, br[k], 0, 0, -1, lk);
+    const cplx db = fundamental_dev(S[1], z, br[k + 1], 1, 0, -1, lk), da = fundamental_dev(S[1], z, br[k], 1, 0, -1, lk);
+    t[k * 6 + 4] = nb - na;
+    t[k * 6 + 5] = db - da;
+  }
+}
+
+struct RecvSum {  // the lateral filter sums of one (column, interval)
+  cplx a1_00, a1_10, a1_01, ph_20, ph_02, ph_11, a3_10, a3_01, a4_10, a4_01, a5_00, b1_11, b1_20, b1_02, b2_00,
+      b3_01, b3_10;
+};
+
+// one CTA per source column of the batch, thread k = interval: the receiver
+// tensors of every cell of the column; with fields, contracted with the
+// scattering currents J = (sigma_a - sigma_b) U / a (paper Eq. APR_lab, the CIE
+// unscaling E = U / a of SPEC.md) of nrhs solutions into part[col][rhs][6]
+// (E xyz, H xyz), else the raw tensors into tens[col][k][18] (E then H, row-major)
+__global__ void __launch_bounds__(64) receiver_kernel(const GreenParams P, const double* __restrict__ W, int nw,
+                                                      const int* __restrict__ jcol, const int* __restrict__ cols,
+                                                      int nbase, const double* __restrict__ lam,
+                                                      const cplx* __restrict__ T, cplx k2, const cplx* __restrict__ U,
+                                                      int nrhs, const cplx* __restrict__ sa,
+                                                      const Interval* __restrict__ iv, cplx* __restrict__ part,
+                                                      cplx* __restrict__ tens) {
+  __shared__ cplx red[64 * 12];
+  const int b = blockIdx.x, k = threadIdx.x, nz = P.nz;
+  const int j = jcol[b];
+  const double R = exp(j * P.step);
+  const double* w = W + static_cast<size_t>(b) * 6 * nw;
+  RecvSum s{};
+  if (k < nz) {
+    for (int t = 0; t < nw; ++t) {
+      const int n = P.n1 + t - j - nbase;
+      const double l = lam[n], il = 1.0 / l;
+      const cplx* v = T + (static_cast<size_t>(n) * nz + k) * 6;
+      const cplx m01 = v[0], m11 = v[1], m0s = v[2], m1s = v[3], n0 = v[4], n1 = v[5];
+      const double w00 = w[t], w20 = w[nw + t], w02 = w[2 * nw + t], w11 = w[3 * nw + t], w10 = w[4 * nw + t],
+                   w01 = w[5 * nw + t];
+      const cplx A1 = l * m01, PH = (k2 * m01 - n1) * il, A3 = l * m1s, A4 = l * n0, A5 = (l * l * l) * m0s;
+      const cplx B1 = (n0 + m11) * il, B2 = l * m11, B3 = l * m0s;
+      s.a1_00 = s.a1_00 + w00 * A1;
+      s.a1_10 = s.a1_10 + w10 * A1;
+      s.a1_01 = s.a1_01 + w01 * A1;
+      s.ph_20 = s.ph_20 + w20 * PH;
+      s.ph_02 = s.ph_02 + w02 * PH;
+      s.ph_11 = s.ph_11 + w11 * PH;
+      s.a3_10 = s.a3_10 + w10 * A3;
+      s.a3_01 = s.a3_01 + w01 * A3;
+      s.a4_10 = s.a4_10 + w10 * A4;
+      s.a4_01 = s.a4_01 + w01 * A4;
+      s.a5_00 = s.a5_00 + w00 * A5;
+      s.b1_11 = s.b1_11 + w11 * B1;
+      s.b1_20 = s.b1_20 + w20 * B1;
+      s.b1_02 = s.b1_02 + w02 * B1;
+      s.b2_00 = s.b2_00 + w00 * B2;
+      s.b3_01 = s.b3_01 + w01 * B3;
+      s.b3_10 = s.b3_10 + w10 * B3;
+    }
+  }
+  const double i4pi = 1.0 / (4.0 * kPi), iR = 1.0 / R;
+  const cplx c = {0.0, P.omega * kMu0 * i4pi}, ck = cdiv(c, k2);
+  cplx E[9], H[9];
+  E[0] = c * (R * s.a1_00) + ck * (iR * s.ph_20);
+  E[4] = c * (R * s.a1_00) + ck * (iR * s.ph_02);
+  E[1] = E[3] = ck * (iR * s.ph_11);
+  E[2] = ck * s.a3_10;
+  E[5] = ck * s.a3_01;
+  E[6] = -(ck * s.a4_10);
+  E[7] = -(ck * s.a4_01);
+  E[8] = ck * (R * s.a5_00);
+  H[0] = -(i4pi * iR) * s.b1_11;
+  H[3] = i4pi * (R * s.b2_00 + iR * s.b1_20);
+  H[6] = -i4pi * s.a1_01;
+  H[1] = -i4pi * (iR * s.b1_02 + R * s.b2_00);
+  H[4] = (i4pi * iR) * s.b1_11;
+  H[7] = i4pi * s.a1_10;
+  H[2] = i4pi * s.b3_01;
+  H[5] = -i4pi * s.b3_10;
+  H[8] = {0.0, 0.0};
+  if (tens) {
+    if (k < nz) {
+      cplx* o = tens + (static_cast<size_t>(b) * nz + k) * 18;
+      for (int q = 0; q < 9; ++q) {
+        o[q] = E[q];
+        o[9 + q] = H[q];
+      }
+    }
+    return;
+  }
+  // contract with the currents of the column's cell (k): rhs-major, E xyz H xyz
+  const int col = cols[b];
+  const size_t N = static_cast<size_t>(P.nx) * P.ny * nz;
+  for (int r = 0; r < nrhs; ++r) {
+    cplx acc[6] = {};
+    if (k < nz) {
+      const size_t cell = static_cast<size_t>(k) * P.nx * P.ny + col;
+      const cplx sbk = P.sig[iv[k].layer];
+      const cplx sak = sa[cell];
+      // J = (sigma_a - sigma_b) U / a, a = (sigma_a + conj sigma_b) / (2 sqrt Re sigma_b) (cie.cpp:9-22)
+      const cplx fac = cdiv((sak - sbk) * (2.0 * sqrt(sbk.re)), sak + conj(sbk));
+      cplx J[3];
+      for (int cc = 0; cc < 3; ++cc) J[cc] = fac * U[static_cast<size_t>(r) * 3 * N + cc * N + cell];
+      for (int a = 0; a < 3; ++a)
+        for (int cc = 0; cc < 3; ++cc) {
+          acc[a] = acc[a] + E[3 * a + cc] * J[cc];
+          acc[3 + a] = acc[3 + a] + H[3 * a + cc] * J[cc];
+        }
+    }
+    for (int q = 0; q < 6; ++q) red[k * 12 + (r % 2) * 6 + q] = acc[q];
+    __syncthreads();
+    if (k == 0) {
+      for (int q = 0; q < 6; ++q) {
+        cplx sum = {0.0, 0.0};
+        for (int kk = 0; kk < nz; ++kk) sum = sum + red[kk * 12 + (r % 2) * 6 + q];
+        part[(static_cast<size_t>(b) * nrhs + r) * 6 + q] = sum;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+
+__global__ void sum_columns_kernel(const cplx* __restrict__ part, int ncols, int nv, cplx* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nv) return;
+  cplx acc = out[q];
+  for (int b = 0; b < ncols; ++b) acc = acc + part[static_cast<size_t>(b) * nv + q];
+  out[q] = acc;
+}
+
 // x <-> y mirror of a square grid with hx == hy: the block of offset (oj, oi)
 // is the block of (oi, oj) with xx <-> yy and xz <-> yz exchanged (zz and xy
 // unchanged) -- the horizontal isotropy of the layered medium; measured on the
@@ -1164,6 +1474,11 @@ __global__ void symmetrize_diagonal_kernel(cplx* blocks, int nx, int ntri, int n
     blk[i] = m;
     blk[j] = m;
   }
+}
+
+__global__ void design_input_kernel(const double* __restrict__ lam, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = design_input(lam[i]);
 }
 
 __global__ void kernel_output_kernel(Geom g, int alpha, int beta, const double* s, int n,
@@ -1208,14 +1523,16 @@ void free_filter_bank(FilterBank& fb, cudaStream_t st) {
 
 void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, OffsetCode oc, double hx,
                     double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
-                    int fixed_oj = 0, const int* offs = nullptr) {
+                    int fixed_oj = 0, const int* offs = nullptr, const Geom* gfix = nullptr, int kern0 = 0,
+                    int nkern = 6, const PGeom* pgeo = nullptr) {
   const int n = 2 * fp.half;
   const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
   set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
-  dim3 grid(noff, 6);
+  dim3 grid(noff, nkern);
   filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
                                                 fp.step, fp.shift, fp.n1, fp.n2, oc, hx, hy, err,
-                                                fixed_oi, fixed_oj, offs);
+                                                fixed_oi, fixed_oj, offs, gfix ? *gfix : Geom{}, gfix != nullptr,
+                                                kern0, pgeo);
   check_launch("filter_design_kernel");
 }
 
@@ -1346,6 +1663,245 @@ void layered_probe_host(int what, int L, const double* tops, const cplx* sigma, 
   release(dout, st);
 }
 
+// FilterDesigner::design (hankel.hpp:93, hankel.cpp:239-281) for a given pair
+// geometry {r, p, q, phi} and one (alpha, beta) kernel
+void design_geometry_host(const double geom[4], int alpha, int beta, const FilterParams& fp, double* w, double* lam) {
+  int kern = -1;
+  for (int k = 0; k < 6; ++k) {
+    static const int ab[6][2] = {{0, 0}, {2, 0}, {0, 2}, {1, 1}, {1, 0}, {0, 1}};
+    if (ab[k][0] == alpha && ab[k][1] == beta) kern = k;
+  }
+  if (kern < 0) fail(EMIE_CU_INVALID_ARGUMENT, "kernel orders: need alpha, beta >= 0 and alpha + beta <= 2");
+  if (!(geom[0] > 0.0)) fail(EMIE_CU_INVALID_ARGUMENT, "pair geometry: reference distance must be positive");
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  FilterBank fb = make_filter_bank(fp, st);
+  const int nw = fp.n2 - fp.n1 + 1;
+  double* dW = scratch<double>(6 * nw, st);
+  int* err = scratch<int>(1, st);
+  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  const Geom g{geom[0], geom[1], geom[2], geom[3]};
+  design_filters(fb, fp, 1, OffsetCode{}, 1.0, 1.0, dW, err, st, 0, 0, nullptr, &g, kern, 1);
+  int e = 0;
+  EMIE_CUDA(cudaMemcpyAsync(w, dW + kern * nw, nw * sizeof(double), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  release(dW, st);
+  release(err, st);
+  free_filter_bank(fb, st);
+  raise_filter_errors(e);
+  for (int m = fp.n1; m <= fp.n2; ++m) lam[m - fp.n1] = std::exp(m * fp.step + fp.shift);
+}
+
+void kernel_output_geom_host(const double geom[4], int alpha, int beta, const double* s, int n, double* out) {
+  if (alpha < 0 || beta < 0 || alpha > 2 || beta > 2 || alpha + beta > 2)
+    fail(EMIE_CU_INVALID_ARGUMENT, "kernel orders: need alpha, beta >= 0 and alpha + beta <= 2");
+  if (n <= 0) return;
+  double* d = nullptr;
+  EMIE_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+  EMIE_CUDA(cudaMemcpy(d, s, n * sizeof(double), cudaMemcpyHostToDevice));
+  kernel_output_kernel<<<ceil_div(n, 256), 256>>>(Geom{geom[0], geom[1], geom[2], geom[3]}, alpha, beta, d, n, d + n);
+  check_launch("kernel_output_kernel");
+  EMIE_CUDA(cudaMemcpy(out, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+}
+
+void design_input_host(int n, const double* lam, double* out) {
+  if (n <= 0) return;
+  double* d = nullptr;
+  EMIE_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+  EMIE_CUDA(cudaMemcpy(d, lam, n * sizeof(double), cudaMemcpyHostToDevice));
+  design_input_kernel<<<ceil_div(n, 256), 256>>>(d, n, d + n);
+  check_launch("design_input_kernel");
+  EMIE_CUDA(cudaMemcpy(out, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+}
+
+void pair_geometry_host(int oi, int oj, double hx, double hy, double out[4]) {
+  if (!(hx > 0.0) || !(hy > 0.0)) fail(EMIE_CU_INVALID_ARGUMENT, "pair_geometry: cell sizes must be positive");
+  const Geom g = pair_geometry(oi, oj, hx, hy);  // the device build's own (host/device) routine
+  out[0] = g.r;
+  out[1] = g.p;
+  out[2] = g.q;
+  out[3] = g.phi;
+}
+
+// assemble_block_full at one signed offset (device filter design, moment
+// tables at the offset's lattice, nine independent filter sums): out[9][nz][nz]
+void assemble_full_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                        const double* breaks, double hx, double hy, const FilterParams& fp, int oi, int oj,
+                        cplx* h_out) {
+  GreenParams P;
+  std::vector<Interval> ivh;
+  green_setup(nx, ny, nz, omega, L, tops, sigma, breaks, hx, hy, fp, P, ivh);
+  if (std::abs(oi) >= ny || std::abs(oj) >= nx)
+    fail(EMIE_CU_OUT_OF_RANGE, "assemble_block_full: offset outside the grid");
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  const int nw = P.nw, NL = L + 1;
+  const Geom g = pair_geometry(oi, oj, hx, hy);
+  FilterBank fb = make_filter_bank(fp, st);
+  double* dW = scratch<double>(6 * static_cast<size_t>(nw), st);
+  double* dl = scratch<double>(nw, st);
+  int* err = scratch<int>(1, st);
+  const size_t nz2 = static_cast<size_t>(nz) * nz;
+  cplx* dT = scratch<cplx>(static_cast<size_t>(nw) * 12 * nz2, st);
+  cplx* dsb = scratch<cplx>(nz, st);
+  cplx* dout = scratch<cplx>(9 * nz2, st);
+  Interval* div = scratch<Interval>(nz, st);
+  std::vector<cplx> sb(nz);
+  for (int i = 0; i < nz; ++i) sb[i] = P.sig[ivh[i].layer];
+  EMIE_CUDA(cudaMemcpyAsync(dsb, sb.data(), nz * sizeof(cplx), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  design_filters(fb, fp, 1, OffsetCode{}, hx, hy, dW, err, st, oi, oj);
+  lattice_kernel<<<ceil_div(nw, 128), 128, 0, st>>>(g.r, fp.n1, fp.step, fp.shift, nw, dl);
+  check_launch("lattice_kernel");
+  const size_t smem = (kProbeSmemPerNL * static_cast<size_t>(NL) + kFields * static_cast<size_t>(nz) + 8) *
+                          sizeof(cplx) + 2 * static_cast<size_t>(nz) * (sizeof(IvFac) + sizeof(cplx));
+  set_smem(reinterpret_cast<const void*>(table_probe_kernel), smem);
+  table_probe_kernel<<<nw, 128, smem, st>>>(P, div, dl, dT);
+  check_launch("table_probe_kernel");
+  full_block_kernel<<<ceil_div(static_cast<long long>(nz2), 128), 128, 0, st>>>(dW, nw, dl, dT, dsb, nz, omega, g.r,
+                                                                               dout);
+  check_launch("full_block_kernel");
+  int e = 0;
+  EMIE_CUDA(cudaMemcpyAsync(h_out, dout, 9 * nz2 * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {static_cast<void*>(dW), static_cast<void*>(dl), static_cast<void*>(err), static_cast<void*>(dT),
+                  static_cast<void*>(dsb), static_cast<void*>(dout), static_cast<void*>(div)})
+    release(q, st);
+  free_filter_bank(fb, st);
+  raise_filter_errors(e);
+  for (size_t x = 0; x < 9 * nz2; ++x)
+    if (!std::isfinite(h_out[x].re) || !std::isfinite(h_out[x].im))
+      fail(EMIE_CU_DOMAIN_ERROR, "assemble_block_full: non-finite block entry");
+}
+
+// Receiver fields (SPEC.md receiver_green_integrals + reconstruct_fields):
+// the anomalous E and H of nrhs solutions U at nrec receivers, out[rec][rhs][6]
+// (E xyz, H xyz); or, with tens_col >= 0, the raw tensors of one receiver and
+// one source column, out[k][18]. Receivers inside the closed anomaly volume
+// are rejected (SPEC.md Receiver invariant).
+void receiver_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                   const double* breaks, double hx, double hy, double x0, double y0, const FilterParams& fp,
+                   const cplx* h_sa, int nrhs, const cplx* h_U, int nrec, const double* rec, cplx* h_out,
+                   int tens_col) {
+  GreenParams P;
+  std::vector<Interval> ivh;
+  green_setup(nx, ny, nz, omega, L, tops, sigma, breaks, hx, hy, fp, P, ivh);
+  if (nz > 64) fail(EMIE_CU_INVALID_ARGUMENT, "receivers: at most 64 intervals");
+  for (int r = 0; r < nrec; ++r) {
+    const double x = rec[3 * r], y = rec[3 * r + 1], z = rec[3 * r + 2];
+    if (!std::isfinite(x) || !std::isfinite(y) || !std::isfinite(z))
+      fail(EMIE_CU_INVALID_ARGUMENT, "receiver: non-finite position");
+    if (x >= x0 && x <= x0 + nx * hx && y >= y0 && y <= y0 + ny * hy && z >= breaks[0] && z <= breaks[nz])
+      fail(EMIE_CU_INVALID_ARGUMENT, "receiver inside the anomaly volume (or on its boundary)");
+  }
+  if (nrec <= 0) return;
+  cudaStream_t st = nullptr;
+  keep_pool_warm();
+  const int nw = P.nw, NL = L + 1, ncols = nx * ny;
+  const size_t N = static_cast<size_t>(ncols) * nz;
+  Interval* div = scratch<Interval>(nz, st);
+  double* dbr = scratch<double>(nz + 1, st);
+  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemcpyAsync(dbr, breaks, (nz + 1) * sizeof(double), cudaMemcpyHostToDevice, st));
+  cplx *dsa = nullptr, *dU = nullptr;
+  if (tens_col < 0) {
+    dsa = scratch<cplx>(N, st);
+    dU = scratch<cplx>(static_cast<size_t>(nrhs) * 3 * N, st);
+    EMIE_CUDA(cudaMemcpyAsync(dsa, h_sa, N * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    EMIE_CUDA(cudaMemcpyAsync(dU, h_U, static_cast<size_t>(nrhs) * 3 * N * sizeof(cplx), cudaMemcpyHostToDevice, st));
+  }
+  FilterBank fb = make_filter_bank(fp, st);
+  int* err = scratch<int>(1, st);
+  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  const std::vector<int> all_cols = [&] {
+    std::vector<int> v;
+    if (tens_col >= 0) v.push_back(tens_col);
+    else
+      for (int c = 0; c < ncols; ++c) v.push_back(c);
+    return v;
+  }();
+  const int B = std::min<int>(static_cast<int>(all_cols.size()), 4096);
+  double* W = scratch<double>(static_cast<size_t>(B) * 6 * nw, st);
+  PGeom* dpg = scratch<PGeom>(B, st);
+  int* djc = scratch<int>(2 * static_cast<size_t>(B), st);
+  cplx* part = scratch<cplx>(static_cast<size_t>(B) * std::max(1, nrhs) * 6, st);
+  cplx* dout = scratch<cplx>(tens_col >= 0 ? static_cast<size_t>(nz) * 18 : static_cast<size_t>(nrec) * nrhs * 6, st);
+  EMIE_CUDA(cudaMemsetAsync(dout, 0, (tens_col >= 0 ? static_cast<size_t>(nz) * 18 : static_cast<size_t>(nrec) * nrhs * 6) *
+                                         sizeof(cplx), st));
+  const size_t smem = (kProbeSmemPerNL * static_cast<size_t>(NL) + kFields * static_cast<size_t>(nz) + 8) * sizeof(cplx) +
+                      2 * sizeof(StateDev);
+  set_smem(reinterpret_cast<const void*>(receiver_table_kernel), smem);
+  std::vector<PGeom> pg(B);
+  std::vector<int> jc(2 * static_cast<size_t>(B));
+  for (int r = 0; r < nrec; ++r) {
+    const double xr = rec[3 * r], yr = rec[3 * r + 1], zr = rec[3 * r + 2];
+    // the receiver's layer and k^2 = i omega mu0 sigma_r (earth side at an interface)
+    const int lr = static_cast<int>(std::upper_bound(tops, tops + L, zr) - tops);
+    const cplx sr = P.sig[lr];
+    const cplx k2 = {-omega * kMu0 * sr.im, omega * kMu0 * sr.re};
+    // lattice index of every column's reference distance, and the table range
+    auto jof = [&](int col) {
+      const int ix = col % nx, iy = col / nx;
+      const double dx = x0 + (ix + 0.5) * hx - xr, dy = y0 + (iy + 0.5) * hy - yr;
+      return static_cast<int>(std::ceil(std::log(std::hypot(std::fabs(dx) + 0.5 * hx, std::fabs(dy) + 0.5 * hy)) / fp.step));
+    };
+    int jmin = INT32_MAX, jmax = INT32_MIN;
+    for (int col : all_cols) {
+      const int j = jof(col);
+      jmin = std::min(jmin, j);
+      jmax = std::max(jmax, j);
+    }
+    const int nbase = fp.n1 - jmax, nlam = (fp.n2 - jmin) - nbase + 1;
+    double* lam = scratch<double>(nlam, st);
+    cplx* T = scratch<cplx>(static_cast<size_t>(nlam) * nz * 6, st);
+    lattice_kernel<<<ceil_div(nlam, 128), 128, 0, st>>>(1.0, nbase, fp.step, fp.shift, nlam, lam);
+    check_launch("lattice_kernel");
+    receiver_table_kernel<<<nlam, 64, smem, st>>>(P, div, dbr, zr, lam, T);
+    check_launch("receiver_table_kernel");
+    for (size_t c0 = 0; c0 < all_cols.size(); c0 += B) {
+      const int nb = static_cast<int>(std::min<size_t>(B, all_cols.size() - c0));
+      for (int b = 0; b < nb; ++b) {
+        const int col = all_cols[c0 + b], ix = col % nx, iy = col / nx;
+        const double dx = x0 + (ix + 0.5) * hx - xr, dy = y0 + (iy + 0.5) * hy - yr;
+        const int j = jof(col);
+        const double R = std::exp(j * fp.step);
+        pg[b] = PGeom{R, hx / R, hy / R, dx / R, dy / R};
+        jc[b] = j;
+        jc[B + b] = col;
+      }
+      EMIE_CUDA(cudaMemcpyAsync(dpg, pg.data(), nb * sizeof(PGeom), cudaMemcpyHostToDevice, st));
+      EMIE_CUDA(cudaMemcpyAsync(djc, jc.data(), 2 * static_cast<size_t>(B) * sizeof(int), cudaMemcpyHostToDevice, st));
+      design_filters(fb, fp, nb, OffsetCode{}, hx, hy, W, err, st, INT32_MIN, 0, nullptr, nullptr, 0, 6, dpg);
+      receiver_kernel<<<nb, 64, 0, st>>>(P, W, nw, djc, djc + B, nbase, lam, T, k2, dU, nrhs, dsa, div,
+                                         tens_col >= 0 ? nullptr : part, tens_col >= 0 ? dout : nullptr);
+      check_launch("receiver_kernel");
+      if (tens_col < 0) {
+        sum_columns_kernel<<<ceil_div(nrhs * 6, 64), 64, 0, st>>>(part, nb, nrhs * 6,
+                                                                  dout + static_cast<size_t>(r) * nrhs * 6);
+        check_launch("sum_columns_kernel");
+      }
+      EMIE_CUDA(cudaStreamSynchronize(st));  // pg / jc are rewritten by the next batch
+    }
+    release(lam, st);
+    release(T, st);
+  }
+  int e = 0;
+  const size_t nout = tens_col >= 0 ? static_cast<size_t>(nz) * 18 : static_cast<size_t>(nrec) * nrhs * 6;
+  EMIE_CUDA(cudaMemcpyAsync(h_out, dout, nout * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {static_cast<void*>(div), static_cast<void*>(dbr), static_cast<void*>(dsa), static_cast<void*>(dU),
+                  static_cast<void*>(err), static_cast<void*>(W), static_cast<void*>(dpg), static_cast<void*>(djc),
+                  static_cast<void*>(part), static_cast<void*>(dout)})
+    if (q) release(q, st);
+  free_filter_bank(fb, st);
+  raise_filter_errors(e);
+}
+
 // The computed offsets of a build: all, or on a square grid with hx == hy only
 // oi <= oj (the rest by the x <-> y mirror, mirror_blocks_kernel)
 std::vector<int> computed_offsets(int nx, int ny, double hx, double hy) {
@@ -1397,6 +1953,8 @@ void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops
   P.nent = 2 * nz * (2 * nz + 1);
   for (int m = 0; m <= L; ++m) {
     P.thick[m] = bottom_of(m) - top_of(m);
+    P.ztop[m] = top_of(m);
+    P.zbot[m] = bottom_of(m);
     cplx s = sigma[m];
     if (s.re < 1e-9) s.re = 1e-9;  // sigma_floored (layered.cpp:47-51)
     P.sig[m] = s;

@@ -163,6 +163,17 @@ void fundamental_values_host(int L, const double* tops, const cplx* st9, int gam
                              const double* zs, const int* ord, cplx* out);
 void point_moments_host(int L, const double* tops, const cplx* st9, int gamma, int nz, const double* breaks,
                         const int* layer, int n, const double* zobs, cplx* out);
+void design_geometry_host(const double geom[4], int alpha, int beta, const FilterParams& fp, double* w, double* lam);
+void kernel_output_geom_host(const double geom[4], int alpha, int beta, const double* s, int n, double* out);
+void design_input_host(int n, const double* lam, double* out);
+void pair_geometry_host(int oi, int oj, double hx, double hy, double out[4]);
+void assemble_full_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                        const double* breaks, double hx, double hy, const FilterParams& fp, int oi, int oj,
+                        cplx* h_out);
+void receiver_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
+                   const double* breaks, double hx, double hy, double x0, double y0, const FilterParams& fp,
+                   const cplx* h_sa, int nrhs, const cplx* h_U, int nrec, const double* rec, cplx* h_out,
+                   int tens_col);
 void vfunctions_host(int L, const double* tops, const cplx* sigma, int nz, const double* breaks, double omega,
                      int n, const double* lam, cplx* out);
 

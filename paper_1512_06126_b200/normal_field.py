@@ -66,18 +66,33 @@ def profile(tops, sigma, omega):
         e = eta[m]
         zt = tops[m - 1]
         if m == L:
-            out.append((zt, np.inf, Et, 0j, e))
+            out.append((zt, np.inf, Et, 0j, e, eta[0]))
             break
         l = tops[m] - tops[m - 1]
         el = cmath.exp(-e * l)
         D = Et / (1.0 + rho[m] * el * el)
-        out.append((zt, l, D, rho[m], e))
+        out.append((zt, l, D, rho[m], e, eta[0]))
         Et = D * el * (1.0 + rho[m])
     return out
 
 
+def _air(prof, z, deriv, tops=None):
+    """Above the surface (z < 0): the upper halfspace continues E and E' of
+    z = 0 (both modes; sigma_air floored to 1e-9, so nearly linear in z)."""
+    e0, d0 = field_at(prof, 0.0), derivative_at(prof, 0.0)
+    ea = prof[0][5] if len(prof[0]) > 5 else None
+    if ea is None or ea == 0:
+        return d0 if deriv else e0 + d0 * z
+    c, s = cmath.cosh(ea * z), cmath.sinh(ea * z)
+    if deriv:
+        return e0 * ea * s + d0 * c
+    return e0 * c + d0 / ea * s
+
+
 def field_at(prof, z):
-    for zt, l, D, r, e in prof:
+    if z < 0.0:
+        return _air(prof, z, False)
+    for zt, l, D, r, e, *_ in prof:
         if z >= zt and (z < zt + l or np.isinf(l)):
             if np.isinf(l):
                 return D * cmath.exp(-e * (z - zt))
@@ -86,8 +101,11 @@ def field_at(prof, z):
 
 
 def derivative_at(prof, z):
-    """dE/dz of the profile at depth z (z >= 0; on an interface, the layer below)."""
-    for zt, l, D, r, e in prof:
+    """dE/dz of the profile at depth z (on an interface, the layer below; z < 0:
+    the upper halfspace)."""
+    if z < 0.0:
+        return _air(prof, z, True)
+    for zt, l, D, r, e, *_ in prof:
         if z >= zt and (z < zt + l or np.isinf(l)):
             if np.isinf(l):
                 return -e * D * cmath.exp(-e * (z - zt))
@@ -100,6 +118,21 @@ def magnetic_at(prof, z, omega):
     H_y = (dE_x/dz) / (i omega mu0) for an x-polarised E (and H_x = -(dE_y/dz) /
     (i omega mu0) for a y-polarised one)."""
     return derivative_at(prof, z) / (1j * omega * MU0)
+
+
+def normal_fields(tops, sigma, omega, points):
+    """Total normal fields at points (n, 3) for the two plane-wave
+    polarisations -> E, H each (n, 2, 3) complex: pol x has E = (E(z), 0, 0),
+    H = (0, E'/(i w mu0), 0); pol y has E = (0, E(z), 0), H = (-E'/(i w mu0), 0, 0)."""
+    prof = profile(tops, sigma, omega)
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    E = np.zeros((len(pts), 2, 3), np.complex128)
+    H = np.zeros_like(E)
+    for i, (_, _, z) in enumerate(pts):
+        e, h = field_at(prof, z), magnetic_at(prof, z, omega)
+        E[i, 0, 0], H[i, 0, 1] = e, h
+        E[i, 1, 1], H[i, 1, 0] = e, -h
+    return E, H
 
 
 def surface_impedance(tops, sigma, omega):
@@ -115,7 +148,7 @@ def surface_impedance(tops, sigma, omega):
 def interval_average(prof, a, b):
     """(1/(b-a)) * integral of E over [a, b] inside one layer."""
     h = b - a
-    for zt, l, D, r, e in prof:
+    for zt, l, D, r, e, *_ in prof:
         if a >= zt - 1e-9 and (np.isinf(l) or b <= zt + l + 1e-7 * (1.0 + abs(b))):
             g = -_cexpm1(-e * h) / e  # (1 - e^{-eta h}) / eta
             down = cmath.exp(-e * (a - zt)) * g
