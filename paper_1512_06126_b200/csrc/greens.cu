@@ -385,6 +385,7 @@ __device__ __forceinline__ cplx scale_or_flush(cplx v, int e) {
 struct PairC {
   int k, kp, kn;  // kn = min(k + 1, nz - 1)
   int kind;       // 0 diagonal, 1 off-diagonal
+  int same;       // both intervals in one layer (FULL mode)
 };
 
 // one lambda of one interval pair into its nine accumulators (greens.cpp:167-191,
@@ -392,7 +393,7 @@ struct PairC {
 // w11 / lambda, w10 lambda, w01 lambda. KIND < 0: the pair's kind at run time;
 // 0 / 1: known at compile time (branch-free body, so two off-diagonal pairs of
 // a thread interleave: phase 2)
-template <int KIND = -1>
+template <int KIND = -1, bool FULL = false>
 __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const int* __restrict__ El, int nz,
                                             const PairC& c, const double* wl, cplx* a) {
   const int k = c.k, kp = c.kp;
@@ -406,12 +407,6 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
   } else {
     const int kn = c.kn;
     const int eu = El[kp] - El[kn], ec = El[nz + kp] - El[nz + kn];
-#ifndef EMIE_GREENS_NO_SKIP
-    // both media's chain products below 2^-1022 (far pairs at large lambda,
-    // where prod theta ~ e^{-lambda dz}): every term of this pair-lambda is an
-    // exact zero (scale_or_flush), so the accumulators would not change
-    if (eu < -1022 && ec < -1022) return;
-#endif
     V1 = scale_or_flush(Fl[fLU * nz + k] * Fl[fRU * nz + kp], eu);
     cplx r0 = Fl[fR0 * nz + kp], r1 = Fl[fR1 * nz + kp];
     if (ec > 1023) {  // a chain product above 2^1023: never in practice, kept exact
@@ -431,6 +426,14 @@ __device__ __forceinline__ void pair_lambda(const cplx* __restrict__ Fl, const i
     const cplx lo = Fl[fL0s * nz + k] * r1;
     a[7] = a[7] + wl[4] * lo;
     a[8] = a[8] + wl[5] * lo;
+    if constexpr (FULL) {
+      // zz at (kp, k) (assemble_block_full, greens.cpp:262-265): V2 + V5 of the
+      // lower entry, by reciprocity lambda^2 W00c(k, kp) / sigma(k)
+      // (i w mu0 sigma(kp) + eta(kp)^2 = lambda^2); inside one layer it is the
+      // upper entry's own V2 + V5, bit for bit as the reference's tables give it
+      const cplx xl = c.same ? X25 : wl[6] * (Fl[fL0s * nz + k] * r0);
+      a[9] = a[9] + wl[0] * xl;
+    }
   }
   a[0] = a[0] + wl[0] * V1;
   a[1] = a[1] + wl[1] * V13;
@@ -809,7 +812,7 @@ __device__ __forceinline__ void chunk_left(const GreenParams& P, const Chunk& C,
 #define EMIE_GREEN_SMEM_KB 200  // SMEM budget of the lambda chunk buffers
 #endif
 // LSPRE: the layer states of every chunk come precomputed (layer_state_kernel)
-template <bool LSPRE>
+template <bool LSPRE, bool FULL = false>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
     cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, const cplx* __restrict__ LS, int nchunk,
@@ -876,13 +879,15 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     pc[i].kp = kp;
     pc[i].kn = min(k + 1, nz - 1);
     pc[i].kind = kp == k ? 0 : 1;
+    pc[i].same = iv[k].layer == iv[kp].layer;
   }
-  // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k)
-  cplx acc[NS + 1][9];
+  // accumulators: a00 a20 a02 a11 az (upper) axz ayz (k,kp) axz ayz (kp,k) [az (kp,k): FULL]
+  constexpr int NA = FULL ? 10 : 9, NWL = FULL ? 7 : 6;
+  cplx acc[NS + 1][NA];
 #pragma unroll
   for (int i = 0; i <= NS; ++i)
 #pragma unroll
-    for (int f = 0; f < 9; ++f) acc[i][f] = {0.0, 0.0};
+    for (int f = 0; f < NA; ++f) acc[i][f] = {0.0, 0.0};
 
   const int nw = P.nw;
   const bool general2 =
@@ -905,6 +910,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       C.lam[3 * LC + li] = Woff[3 * nw + t] * ilam;
       C.lam[4 * LC + li] = Woff[4 * nw + t] * lam;
       C.lam[5 * LC + li] = Woff[5 * nw + t] * lam;
+      C.lam[6 * LC + li] = lam * lam;
     }
     if constexpr (LSPRE) {
       // the chunk's layer states come precomputed (layer_state_kernel): one
@@ -932,27 +938,28 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
 #pragma unroll kPairUnroll
     for (int li = 0; li < lc; ++li) {
-      double wl[6];
+      double wl[NWL];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
+      for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
       const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
       const int* El = C.E + li * 2 * nz;
       if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
-        pair_lambda<1>(Fl, El, nz, pc[0], wl, acc[0]);
-        pair_lambda<1>(Fl, El, nz, pc[1], wl, acc[1]);
+        pair_lambda<1, FULL>(Fl, El, nz, pc[0], wl, acc[0]);
+        pair_lambda<1, FULL>(Fl, El, nz, pc[1], wl, acc[1]);
       } else {
 #pragma unroll
         for (int i = 0; i < NS; ++i)
-          if (pv[i]) pair_lambda(Fl, El, nz, pc[i], wl, acc[i]);
+          if (pv[i]) pair_lambda<-1, FULL>(Fl, El, nz, pc[i], wl, acc[i]);
       }
     }
     if (pv[NS]) {
       for (int u = threadIdx.x; u < ntail * lc; u += teff) {
         const int li = u / ntail;
-        double wl[6];
+        double wl[NWL];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 2 * nz, nz, pc[NS], wl, acc[NS]);
+        for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
+        pair_lambda<-1, FULL>(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 2 * nz, nz, pc[NS], wl,
+                              acc[NS]);
       }
     }
   }
@@ -962,11 +969,11 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   if (ntail > 0) {
     cplx* part = sm;  // the chunk buffers are free now: [9][T]
 #pragma unroll
-    for (int f = 0; f < 9; ++f) part[f * T + threadIdx.x] = acc[NS][f];
+    for (int f = 0; f < NA; ++f) part[f * T + threadIdx.x] = acc[NS][f];
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < ntail) {
 #pragma unroll
-      for (int f = 0; f < 9; ++f) {
+      for (int f = 0; f < NA; ++f) {
         cplx sum = part[f * T + threadIdx.x];
         for (int r = threadIdx.x + ntail; r < teff; r += ntail) sum = sum + part[f * T + r];
         acc[NS][f] = sum;
@@ -994,6 +1001,30 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     v[6] = c2 * acc[i][7];
     v[7] = c2 * acc[i][8];
     for (int c = 0; c < 8; ++c) bad |= !isfinite(v[c].re) || !isfinite(v[c].im);
+    if constexpr (FULL) {  // FullBlock q[3a+b][k][kp] (greens.cpp:276-291)
+      const size_t n2 = static_cast<size_t>(nfull), up = static_cast<size_t>(k) * nz + kp,
+                   lo = static_cast<size_t>(kp) * nz + k;
+      const cplx zl = k == kp ? v[2] : c3 * acc[i][9];
+      bad |= !isfinite(zl.re) || !isfinite(zl.im);
+      blk[up] = blk[lo] = v[0];                    // xx
+      blk[4 * n2 + up] = blk[4 * n2 + lo] = v[1];  // yy
+      blk[8 * n2 + up] = v[2];                     // zz
+      blk[8 * n2 + lo] = zl;
+      blk[n2 + up] = blk[n2 + lo] = v[3];          // xy
+      blk[3 * n2 + up] = blk[3 * n2 + lo] = v[3];  // yx: the same defining sum
+      blk[2 * n2 + up] = v[4];                     // xz
+      blk[5 * n2 + up] = v[5];                     // yz
+      // zx(k, kp): the source-side sum, -xz(kp, k) (on the diagonal -xz(k, k))
+      blk[6 * n2 + up] = k == kp ? -v[4] : -v[6];
+      blk[7 * n2 + up] = k == kp ? -v[5] : -v[7];
+      if (k != kp) {
+        blk[2 * n2 + lo] = v[6];
+        blk[5 * n2 + lo] = v[7];
+        blk[6 * n2 + lo] = -v[4];
+        blk[7 * n2 + lo] = -v[5];
+      }
+      continue;
+    }
     blk[s] = v[0];
     blk[ntri + s] = v[1];
     blk[2 * ntri + s] = v[2];
@@ -1189,54 +1220,6 @@ __global__ void lattice_kernel(double R, int n1, double step, double shift, int 
   if (t < n) lam[t] = exp((n1 + t) * step + shift) / R;
 }
 
-// assemble_block_full (greens.hpp:139-141, greens.cpp:231-293): all nine
-// components of one signed offset, each from its own filter sum over the
-// device moment tables T[t][gamma][6][nz][nz] at the offset's lattice (the
-// lower triangles and the source-side z couplings evaluated, not mirrored).
-// One thread per (k, kp), lambda order; out[9][nz][nz].
-__global__ void full_block_kernel(const double* __restrict__ W, int nw, const double* __restrict__ lam,
-                                  const cplx* __restrict__ T, const cplx* __restrict__ sigb, int nz, double omega,
-                                  double R, cplx* __restrict__ out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t nz2 = static_cast<size_t>(nz) * nz;
-  if (e >= static_cast<int>(nz2)) return;
-  const int k = e / nz, kp = e - k * nz;
-  const size_t i = static_cast<size_t>(k) * nz + kp, it = static_cast<size_t>(kp) * nz + k;
-  const cplx iwmu = {0.0, omega * kMu0};
-  const cplx isk = crecip(sigb[k]), iskp = crecip(sigb[kp]);
-  cplx a00 = {0, 0}, a20 = {0, 0}, a02 = {0, 0}, a11 = {0, 0}, az = {0, 0};
-  cplx axz = {0, 0}, ayz = {0, 0}, azx = {0, 0}, azy = {0, 0};
-  for (int t = 0; t < nw; ++t) {
-    const double l = lam[t];
-    const cplx* tu = T + static_cast<size_t>(t) * 12 * nz2;
-    const cplx* tc = tu + 6 * nz2;
-    // v_functions (layered.cpp:397-408) at (k, kp) and, source side, (kp, k)
-    const cplx v1 = iwmu * tu[i], v2 = iwmu * tc[i];
-    const cplx v3 = -(tc[3 * nz2 + i] * isk), v4 = tc[nz2 + i] * isk, v5 = tc[4 * nz2 + i] * isk;
-    const cplx vs4 = tc[nz2 + it] * iskp;
-    const cplx v13 = v1 + v3;
-    const cplx f2 = {v13.re / l, v13.im / l};
-    a00 = a00 + W[t] * (l * v1);
-    a20 = a20 + W[nw + t] * f2;
-    a02 = a02 + W[2 * nw + t] * f2;
-    a11 = a11 + W[3 * nw + t] * f2;
-    az = az + W[t] * (l * (v2 + v5));
-    axz = axz + W[4 * nw + t] * (l * v4);
-    ayz = ayz + W[5 * nw + t] * (l * v4);
-    azx = azx + W[4 * nw + t] * (l * vs4);
-    azy = azy + W[5 * nw + t] * (l * vs4);
-  }
-  const double c3 = R * R * R / (4.0 * kPi), c2 = R * R / (4.0 * kPi), c1 = R / (4.0 * kPi);
-  out[i] = c3 * a00 + c1 * a20;             // xx
-  out[4 * nz2 + i] = c3 * a00 + c1 * a02;   // yy
-  out[8 * nz2 + i] = c3 * az;               // zz
-  out[nz2 + i] = c1 * a11;                  // xy
-  out[3 * nz2 + i] = c1 * a11;              // yx: the same defining sum
-  out[2 * nz2 + i] = c2 * axz;              // xz
-  out[5 * nz2 + i] = c2 * ayz;              // yz
-  out[6 * nz2 + i] = -(c2 * azx);           // zx
-  out[7 * nz2 + i] = -(c2 * azy);           // zy
-}
 
 
 // ---- receiver fields (SPEC.md receiver_green_integrals / reconstruct_fields) ----
@@ -1325,14 +1308,31 @@ __global__ void __launch_bounds__(64) receiver_kernel(const GreenParams P, const
                                                       int nbase, const double* __restrict__ lam,
                                                       const cplx* __restrict__ T, cplx k2, const cplx* __restrict__ U,
                                                       int nrhs, const cplx* __restrict__ sa,
-                                                      const Interval* __restrict__ iv, cplx* __restrict__ part,
-                                                      cplx* __restrict__ tens) {
+                                                      const Interval* __restrict__ iv,
+                                                      const double* __restrict__ br, double zr,
+                                                      cplx* __restrict__ part, cplx* __restrict__ tens) {
   __shared__ cplx red[64 * 12];
   const int b = blockIdx.x, k = threadIdx.x, nz = P.nz;
   const int j = jcol[b];
   const double R = exp(j * P.step);
   const double* w = W + static_cast<size_t>(b) * 6 * nw;
   RecvSum s{};
+  // a receiver within the z-range of interval k (laterally outside the cell):
+  // d^2/dz^2 int_k U dz' = eta^2 m0 - 2 (the kink of U at z' = z) adds +2 to
+  // Phi's numerator and -2 lambda to the E_zz integrand, which keeps both
+  // integrands decaying in lambda; on a face plane the one-sided limits of
+  // the two forms average (E_zz: -lambda); fundamental_value's coincident
+  // derivative is the one from above (outside at the top face, inside at the bottom)
+  double cA = 0.0, cP = 0.0;
+  if (k < nz) {
+    const double za = br[k], zb = br[k + 1], z = zr;
+    if (z > za && z < zb) cA = cP = 2.0;
+    else if (z == za) cA = 1.0;
+    else if (z == zb) {
+      cA = 1.0;
+      cP = 2.0;
+    }
+  }
   if (k < nz) {
     for (int t = 0; t < nw; ++t) {
       const int n = P.n1 + t - j - nbase;
@@ -1341,7 +1341,8 @@ __global__ void __launch_bounds__(64) receiver_kernel(const GreenParams P, const
       const cplx m01 = v[0], m11 = v[1], m0s = v[2], m1s = v[3], n0 = v[4], n1 = v[5];
       const double w00 = w[t], w20 = w[nw + t], w02 = w[2 * nw + t], w11 = w[3 * nw + t], w10 = w[4 * nw + t],
                    w01 = w[5 * nw + t];
-      const cplx A1 = l * m01, PH = (k2 * m01 - n1) * il, A3 = l * m1s, A4 = l * n0, A5 = (l * l * l) * m0s;
+      const cplx A1 = l * m01, PH = (k2 * m01 - n1 + cplx{cP, 0.0}) * il, A3 = l * m1s, A4 = l * n0;
+      const cplx A5 = (l * l * l) * m0s - cplx{cA * l, 0.0};
       const cplx B1 = (n0 + m11) * il, B2 = l * m11, B3 = l * m0s;
       s.a1_00 = s.a1_00 + w00 * A1;
       s.a1_10 = s.a1_10 + w10 * A1;
@@ -1725,8 +1726,13 @@ void pair_geometry_host(int oi, int oj, double hx, double hy, double out[4]) {
   out[3] = g.phi;
 }
 
-// assemble_block_full at one signed offset (device filter design, moment
-// tables at the offset's lattice, nine independent filter sums): out[9][nz][nz]
+void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, const FilterParams& fp,
+                    const std::vector<int>& offs_h, int nslots, cplx* blocks, cudaStream_t st, bool full);
+
+// assemble_block_full at one signed offset: the build's own kernel in its
+// FULL mode (nine components; lower triangles and source-side z couplings
+// from their own sums over the same per-lambda quantities the compressed
+// blocks are summed from, greens.cpp:231-293): out[9][nz][nz]
 void assemble_full_host(int nx, int ny, int nz, double omega, int L, const double* tops, const cplx* sigma,
                         const double* breaks, double hx, double hy, const FilterParams& fp, int oi, int oj,
                         cplx* h_out) {
@@ -1735,47 +1741,20 @@ void assemble_full_host(int nx, int ny, int nz, double omega, int L, const doubl
   green_setup(nx, ny, nz, omega, L, tops, sigma, breaks, hx, hy, fp, P, ivh);
   if (std::abs(oi) >= ny || std::abs(oj) >= nx)
     fail(EMIE_CU_OUT_OF_RANGE, "assemble_block_full: offset outside the grid");
+  P.oc = OffsetCode{2 * nx - 1, ny - 1, nx - 1, 1};
+  const std::vector<int> codes{(oi + ny - 1) * (2 * nx - 1) + (oj + nx - 1)};
   cudaStream_t st = nullptr;
-  keep_pool_warm();
-  const int nw = P.nw, NL = L + 1;
-  const Geom g = pair_geometry(oi, oj, hx, hy);
-  FilterBank fb = make_filter_bank(fp, st);
-  double* dW = scratch<double>(6 * static_cast<size_t>(nw), st);
-  double* dl = scratch<double>(nw, st);
-  int* err = scratch<int>(1, st);
-  const size_t nz2 = static_cast<size_t>(nz) * nz;
-  cplx* dT = scratch<cplx>(static_cast<size_t>(nw) * 12 * nz2, st);
-  cplx* dsb = scratch<cplx>(nz, st);
-  cplx* dout = scratch<cplx>(9 * nz2, st);
-  Interval* div = scratch<Interval>(nz, st);
-  std::vector<cplx> sb(nz);
-  for (int i = 0; i < nz; ++i) sb[i] = P.sig[ivh[i].layer];
-  EMIE_CUDA(cudaMemcpyAsync(dsb, sb.data(), nz * sizeof(cplx), cudaMemcpyHostToDevice, st));
-  EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
-  EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, 1, OffsetCode{}, hx, hy, dW, err, st, oi, oj);
-  lattice_kernel<<<ceil_div(nw, 128), 128, 0, st>>>(g.r, fp.n1, fp.step, fp.shift, nw, dl);
-  check_launch("lattice_kernel");
-  const size_t smem = (kProbeSmemPerNL * static_cast<size_t>(NL) + kFields * static_cast<size_t>(nz) + 8) *
-                          sizeof(cplx) + 2 * static_cast<size_t>(nz) * (sizeof(IvFac) + sizeof(cplx));
-  set_smem(reinterpret_cast<const void*>(table_probe_kernel), smem);
-  table_probe_kernel<<<nw, 128, smem, st>>>(P, div, dl, dT);
-  check_launch("table_probe_kernel");
-  full_block_kernel<<<ceil_div(static_cast<long long>(nz2), 128), 128, 0, st>>>(dW, nw, dl, dT, dsb, nz, omega, g.r,
-                                                                               dout);
-  check_launch("full_block_kernel");
-  int e = 0;
-  EMIE_CUDA(cudaMemcpyAsync(h_out, dout, 9 * nz2 * sizeof(cplx), cudaMemcpyDeviceToHost, st));
-  EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  const size_t n9 = 9 * static_cast<size_t>(nz) * nz;
+  cplx* d = scratch<cplx>(n9, st);
+  try {
+    assemble_codes(P, ivh, fp, codes, 1, d, st, true);
+  } catch (...) {
+    release(d, st);
+    throw;
+  }
+  EMIE_CUDA(cudaMemcpyAsync(h_out, d, n9 * sizeof(cplx), cudaMemcpyDeviceToHost, st));
   EMIE_CUDA(cudaStreamSynchronize(st));
-  for (void* q : {static_cast<void*>(dW), static_cast<void*>(dl), static_cast<void*>(err), static_cast<void*>(dT),
-                  static_cast<void*>(dsb), static_cast<void*>(dout), static_cast<void*>(div)})
-    release(q, st);
-  free_filter_bank(fb, st);
-  raise_filter_errors(e);
-  for (size_t x = 0; x < 9 * nz2; ++x)
-    if (!std::isfinite(h_out[x].re) || !std::isfinite(h_out[x].im))
-      fail(EMIE_CU_DOMAIN_ERROR, "assemble_block_full: non-finite block entry");
+  release(d, st);
 }
 
 // Receiver fields (SPEC.md receiver_green_integrals + reconstruct_fields):
@@ -1876,7 +1855,7 @@ void receiver_host(int nx, int ny, int nz, double omega, int L, const double* to
       EMIE_CUDA(cudaMemcpyAsync(dpg, pg.data(), nb * sizeof(PGeom), cudaMemcpyHostToDevice, st));
       EMIE_CUDA(cudaMemcpyAsync(djc, jc.data(), 2 * static_cast<size_t>(B) * sizeof(int), cudaMemcpyHostToDevice, st));
       design_filters(fb, fp, nb, OffsetCode{}, hx, hy, W, err, st, INT32_MIN, 0, nullptr, nullptr, 0, 6, dpg);
-      receiver_kernel<<<nb, 64, 0, st>>>(P, W, nw, djc, djc + B, nbase, lam, T, k2, dU, nrhs, dsa, div,
+      receiver_kernel<<<nb, 64, 0, st>>>(P, W, nw, djc, djc + B, nbase, lam, T, k2, dU, nrhs, dsa, div, dbr, zr,
                                          tens_col >= 0 ? nullptr : part, tens_col >= 0 ? dout : nullptr);
       check_launch("receiver_kernel");
       if (tens_col < 0) {
@@ -2003,8 +1982,10 @@ void green_setup(int nx, int ny, int nz, double omega, int L, const double* tops
 
 // Filter design (K6) and lambda accumulation (K5) of the offsets offs_h
 // (codes of P.oc) into `blocks` (slot P.oc.slot(code, position) of nslots)
-void assemble_codes(const GreenParams& P, const std::vector<Interval>& ivh, const FilterParams& fp,
-                    const std::vector<int>& offs_h, int nslots, cplx* blocks, cudaStream_t st) {
+void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, const FilterParams& fp,
+                    const std::vector<int>& offs_h, int nslots, cplx* blocks, cudaStream_t st, bool full) {
+  GreenParams P = P0;
+  if (full) P.nent = 9 * P.nz * P.nz;  // FullBlock slots
   keep_pool_warm();
   const int nz = P.nz, L = P.L;
   const int ncomp = static_cast<int>(offs_h.size());
@@ -2025,6 +2006,7 @@ void assemble_codes(const GreenParams& P, const std::vector<Interval>& ivh, cons
                       static_cast<size_t>(P.LC) * 2 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel<false>), smem);
   set_smem(reinterpret_cast<const void*>(assemble_kernel<true>), smem);
+  set_smem(reinterpret_cast<const void*>(assemble_kernel<false, true>), smem);
   const int groups = ceil_div(P.npairs, (kGreenSlots + 1) * kGreenThreads);
   dim3 grid(ncomp, groups);
   profile_mark(5, true, st);
@@ -2042,9 +2024,12 @@ void assemble_codes(const GreenParams& P, const std::vector<Interval>& ivh, cons
     const char* e = std::getenv("EMIE_CU_GREENS_LS");  // 0: inline, 1: precomputed, unset: by group count
     return e && *e ? std::atoi(e) : -1;
   }();
-  const bool pre = ls_mode < 0 ? groups > 1 : ls_mode == 1;
+  const bool pre = !full && (ls_mode < 0 ? groups > 1 : ls_mode == 1);
   if (!pre) {
-    assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
+    if (full)
+      assemble_kernel<false, true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
+    else
+      assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
     check_launch("assemble_kernel");
   } else {
     const int nchunk = ceil_div(P.nw, P.LC);
@@ -2102,7 +2087,7 @@ void greens_blocks(const Operator& op, int L, const double* tops, const cplx* si
   const int cb = std::max(0, std::min(c0, static_cast<int>(all.size())));
   const int ce = c1 < 0 ? static_cast<int>(all.size()) : std::max(cb, std::min(c1, static_cast<int>(all.size())));
   if (ce == cb) return;
-  assemble_codes(P, ivh, fp, std::vector<int>(all.begin() + cb, all.begin() + ce), op.nx * op.ny, blocks, st);
+  assemble_codes(P, ivh, fp, std::vector<int>(all.begin() + cb, all.begin() + ce), op.nx * op.ny, blocks, st, false);
 }
 
 // assemble_block (greens.hpp:129-135, greens.cpp:150-221) at n signed offsets
@@ -2127,7 +2112,7 @@ void assemble_signed_host(int nx, int ny, int nz, double omega, int L, const dou
   const size_t bytes = static_cast<size_t>(n) * P.nent * sizeof(cplx);
   cplx* d = scratch<cplx>(static_cast<size_t>(n) * P.nent, st);
   try {
-    assemble_codes(P, ivh, fp, codes, n, d, st);
+    assemble_codes(P, ivh, fp, codes, n, d, st, false);
   } catch (...) {
     release(d, st);
     throw;

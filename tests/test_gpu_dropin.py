@@ -31,3 +31,28 @@ def test_dropin_fgmres_map_preconditioner_and_hook(torch_cuda):
     r = subprocess.run([str(b)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "dropin_fgmres ok" in r.stdout
+
+
+def _cases(name):
+    import re
+    src = ROOT / "tools" / f"dropin_cases_{name}.txt"
+    return [l for l in src.read_text().splitlines() if l.strip()]
+
+
+# the reference's own greens and layered suites (tests/test_greens.cpp,
+# tests/test_layered.cpp), unchanged, compiled against the drop-in: every
+# case but the brute-force spectral-integration oracle of test_greens.cpp:109
+# (~13 min through per-point device calls; run by tools/run_dropin_suites.sh,
+# result in profiles/r02_dropin_suites.log)
+SLOW = {"cross couplings match direct spectral integration"}
+
+
+@pytest.mark.parametrize("suite,case", [("greens", c) for c in _cases("greens") if c not in SLOW] +
+                         [("layered", c) for c in _cases("layered")])
+def test_reference_suites_against_dropin(torch_cuda, suite, case):
+    b = ROOT / "oracle" / "_ref" / f"dropin_test_{suite}"
+    if not b.exists():
+        pytest.fail(f"{b} missing: run __graft_entry__.build() (make -C oracle dropin)")
+    r = subprocess.run([str(b), f"-tc={case}"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "1 passed" in r.stdout, r.stdout

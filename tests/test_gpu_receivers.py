@@ -4,7 +4,9 @@ so parity rests on the SPEC's own checks and on the device Green's blocks):
 
 * homogeneous whole space: int_cell G^E and int_cell G^H against brute
   Gauss cubature of the analytic whole-space dyadic (1 + grad grad / k^2)
-  i w mu0 e^{-kappa r} / (4 pi r) and its curl, <= 1e-5 (SPEC's bar);
+  i w mu0 e^{-kappa r} / (4 pi r) and its curl, <= 1e-5 (SPEC's bar), for
+  receivers above, below, beside the cells at their depths and on their
+  face planes;
 * layered medium: the receiver tensor averaged over an observation cell
   reproduces the Galerkin block B_n^m of the device Green's build for that
   pair of cells (paper Eq. slae_matricies: B = int_n int_m G^E), at the
@@ -60,7 +62,8 @@ def wholespace_tensors(rec, box, sigma, omega, n=24, split=2):
 
 
 @pytest.mark.parametrize("rec", [(-350.0, 80.0, -30.0), (520.0, -260.0, 0.0), (50.0, 40.0, -220.0),
-                                 (800.0, 700.0, 450.0)])
+                                 (800.0, 700.0, 450.0), (520.0, -260.0, 50.0), (520.0, -260.0, 100.0),
+                                 (520.0, -260.0, 400.0), (-20.0, 300.0, 175.0)])
 def test_wholespace_receiver_integrals(torch_cuda, rec):
     sigma, omega = 0.02, 2 * np.pi * 3.0
     model = emie.LayeredModel([0.0], [sigma, sigma])  # the same conductivity above and below: a whole space
