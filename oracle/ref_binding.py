@@ -133,13 +133,14 @@ class RefCase:
         _check(lib().ref_assemble_block(self.ctx, int(oi), int(oj), _dp(out.view(np.float64))))
         return out
 
-    def block_weights(self, oi, oj, w, lam):
-        """assemble_block's accumulation with given filter weights w (6, nw), lam (nw)."""
+    def block_weights(self, oi, oj, w, lam, r=0.0):
+        """assemble_block's accumulation with given filter weights w (6, nw), lam (nw)
+        (r > 0: that reference distance instead of pair_geometry's)."""
         w = np.ascontiguousarray(w, np.float64)
         lam = np.ascontiguousarray(lam, np.float64)
         out = np.zeros(self.nent, np.complex128)
         _check(lib().ref_assemble_block_weights(self.ctx, int(oi), int(oj), _dp(w), _dp(lam), len(lam),
-                                                _dp(out.view(np.float64))))
+                                                _dp(out.view(np.float64)), ctypes.c_double(r)))
         return out
 
     def vfunctions(self, lam):

@@ -147,13 +147,13 @@ int ref_assemble_block(void* p, int oi, int oj, double* out) {
 // abscissae lam[nw]: separates the filter design from the accumulation when
 // a device build is compared with the reference (parity diagnostics only)
 int ref_assemble_block_weights(void* p, int oi, int oj, const double* w, const double* lam, int nw,
-                               double* out) {
+                               double* out, double r_override) {
   Ctx* c = static_cast<Ctx*>(p);
   return guarded([&] {
     const AnomalyGrid& grid = c->grid;
     const int nz = grid.nz();
     const PairGeometry g = pair_geometry(oi, oj, grid.hx, grid.hy);
-    const double R = g.r;
+    const double R = r_override > 0.0 ? r_override : g.r;  // another reference distance (filter studies)
     const std::size_t ntri = static_cast<std::size_t>(nz) * (nz + 1) / 2, nfull = std::size_t(nz) * nz;
     std::vector<cdouble> a00(ntri), a20(ntri), a02(ntri), a11(ntri), az(ntri), axz(nfull), ayz(nfull);
     MomentMemo memo(c->model, grid.part, c->omega);
