@@ -509,6 +509,26 @@ def run_ours(args):
                     traffic_source="profiles/traffic.json (ncu --set full, dram__bytes_read.sum + "
                                    "dram__bytes_write.sum, one launch)",
                     hbm=hbm_view, fp64=fp64_view)
+    # Green's build roofline (FP64-pipe bound; the ncu-measured
+    # FP64 work is authoritative): executed FP64 flops of one cfg3 assemble
+    # launch from the committed ncu capture over this run's assemble time
+    greens_roofline = None
+    gpath = ROOT / "profiles" / "r02_greens_fp64.json"
+    if greens_stage and gpath.exists() and args.config == 3 and fp64.value:
+        gj = json.loads(gpath.read_text())
+        t_as = greens_stage["assemble_kernel_ms"] * 1e-3
+        p_alg = cfg.nx * cfg.ny * 451 * cfg.nz ** 2  # pair-lambda evaluations of all offsets
+        ach = gj["fp64_flops_executed"] / t_as / 1e12
+        greens_roofline = {
+            "bound": "fp64", "kernel": gj["kernel"], "achieved": ach, "peak": fp64.value, "unit": "TFLOP/s",
+            "frac": ach / fp64.value, "fp64_pipe_active_pct_ncu": gj["fp64_pipe_active_pct"],
+            "flops_per_launch": gj["fp64_flops_executed"],
+            "flops_how": "executed FP64 flops (2 DFMA + DADD + DMUL thread instructions, ncu) of one launch",
+            "algorithmic": {"pair_lambda": p_alg, "flops": 140.0 * p_alg, "tflops": 140.0 * p_alg / t_as / 1e12,
+                            "note": "SURVEY.md §8(d) estimate of the reference algorithm over all nx*ny offsets; "
+                                    "the build computes the offsets oi <= oj (x<->y mirror) with five complex "
+                                    "products per pair-lambda instead of fifteen"},
+            "source": "profiles/r02_greens_fp64.json (ncu --set full)"}
     stage_names = ["fwd_x_fft", "fwd_y_fft", "contraction", "inv_y_fft", "inv_x_fft_epilogue"]
     stages = {nm: round(float(ms5[i] / max(1, cnt5[i])), 4) for i, nm in enumerate(stage_names)}
 
@@ -555,6 +575,7 @@ def run_ours(args):
             "library_init_s": init_s,
             "greens_build_warm_s": greens_warm_s,
             "greens_stage_ms": greens_stage,
+            "greens_roofline": greens_roofline,
             "greens_cpu_baseline": greens_cpu,
             "stage_ms": stages,
             "roofline": roofline,
