@@ -9,6 +9,7 @@
 // reference's 3, 9, 12-point test grids) the ping-pong mixed-radix one.
 //
 // Reference: src/toeplitz.cpp:92-161 (spectra), 163-283 (apply), cie.cpp:56-73.
+#include <cstdlib>
 #include <algorithm>
 
 #include <cudaTypedefs.h>
@@ -953,6 +954,101 @@ void set_smem(const void* fn, size_t bytes) {
 constexpr int kTileElems = 2048;  // pow2 engine: kFftThreads * kFftEPT
 constexpr int kFftThreads = kTileElems / kFftEPT;
 
+
+// ---- spectra build on the TMA streaming engine (K7, toeplitz.cpp:92-161) ----
+// The parity-extended offset sequences of the compressed blocks: a tile is TR
+// consecutive entries e (the transforms) of one row of offsets; their nonzero
+// inputs (offsets 0..n-1) arrive as one tensor-map box [offset][TR entries]
+// (128-byte rows, N = 256; 64-byte rows, N = 512), the mirrored half
+// (j > N - n: the entry at offset N - j, times the component's parity sign,
+// toeplitz.cpp:140-151) is read from the same staged rows, the zero middle
+// is never loaded. x pass: R[(oi qx + mx) nent + e] for mx < qx; y pass: the
+// quadrant modes my < qy of the operator's shard, through emap into the
+// device mode blocks (operator.cuh).
+template <int N>
+__device__ __forceinline__ cplx staged_parity(const cplx* stg, int t, int jj, int n) {
+  const int row = jj < n ? jj : (jj > N - n ? N - jj : -1);
+  if (row < 0) return cplx{0.0, 0.0};
+  return *reinterpret_cast<const cplx*>(reinterpret_cast<const unsigned char*>(stg) + stage_off<N>(t, row));
+}
+
+struct SpxStream {
+  static constexpr bool kInverse = false, kTFast = true;
+  static constexpr int kStageBytes = 16384;  // <= N/2 offsets of 128-byte (64-byte) rows
+  CUtensorMap tm;  // blocks as {2 nent doubles, nx, ny}, box {16 | 8, nx, 1}
+  cplx* R;
+  int nx, ny, qx, nent, ntri, nfull, nchunks, nin;
+  uint32_t box_bytes;
+  struct Ops {
+    int oi, e0;
+    double sgn;  // parity of the thread's first-pass transform (entry)
+  };
+  __device__ int ntiles() const { return ny * nchunks; }
+  template <int N>
+  __device__ void prefetch(int tile, Ops& o) const {
+    o.oi = tile / nchunks;
+    o.e0 = (tile - o.oi * nchunks) * Geo<N>::ntr;
+    const int e = o.e0 + static_cast<int>(threadIdx.x) / (N / 16);
+    o.sgn = e < nent ? static_cast<double>(kParX[comp_of(e, ntri, nfull)]) : 1.0;
+  }
+  __device__ cplx pre(const Ops& o, int, int, int jj, cplx x) const { return jj >= nx ? o.sgn * x : x; }
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    const int oi = tile / nchunks, e0 = (tile - oi * nchunks) * Geo<N>::ntr;
+    mbar_expect_tx(bar, box_bytes);
+    tma_load_3d(stg, &tm, 2 * e0, 0, oi, bar);
+  }
+  template <int N>
+  __device__ cplx staged(const cplx* stg, int t, int jj) const { return staged_parity<N>(stg, t, jj, nx); }
+  template <int N>
+  __device__ void emit(const Ops& o, int t, int mx, int, int, cplx v) const {
+    const int e = o.e0 + t;
+    if (mx < qx && e < nent) gst(R + (static_cast<size_t>(o.oi) * qx + mx) * nent + e, v);
+  }
+};
+
+struct SpyStream {
+  static constexpr bool kInverse = false, kTFast = true;
+  static constexpr int kStageBytes = 16384;
+  CUtensorMap tm;  // R as {2 nent doubles, qx, ny}, box {16 | 8, 1, ny}
+  cplx* spec;
+  const int2* emap;
+  int ny, qx, qy, nent, ntri, nfull, nchunks, nentD, qbase, qcount, nin;
+  uint32_t box_bytes;
+  struct Ops {
+    int mx, e0;
+    double sgn;
+  };
+  __device__ int ntiles() const { return qx * nchunks; }
+  template <int N>
+  __device__ void prefetch(int tile, Ops& o) const {
+    o.mx = tile / nchunks;
+    o.e0 = (tile - o.mx * nchunks) * Geo<N>::ntr;
+    const int e = o.e0 + static_cast<int>(threadIdx.x) / (N / 16);
+    o.sgn = e < nent ? static_cast<double>(kParY[comp_of(e, ntri, nfull)]) : 1.0;
+  }
+  __device__ cplx pre(const Ops& o, int, int, int jj, cplx x) const { return jj >= ny ? o.sgn * x : x; }
+  template <int N>
+  __device__ void issue(int tile, cplx* stg, uint64_t* bar) const {
+    const int mx = tile / nchunks, e0 = (tile - mx * nchunks) * Geo<N>::ntr;
+    mbar_expect_tx(bar, box_bytes);
+    tma_load_3d(stg, &tm, 2 * e0, mx, 0, bar);
+  }
+  template <int N>
+  __device__ cplx staged(const cplx* stg, int t, int jj) const { return staged_parity<N>(stg, t, jj, ny); }
+  template <int N>
+  __device__ void emit(const Ops& o, int t, int my, int, int, cplx v) const {
+    const int e = o.e0 + t;
+    const int qm = my * qx + o.mx;
+    if (my < qy && e < nent && qm >= qbase && qm < qbase + qcount) {
+      const int2 m = __ldg(emap + e);
+      cplx* blk = spec + static_cast<size_t>(qm - qbase) * nentD;
+      gst(blk + m.x, v);
+      if (m.y >= 0) gst(blk + m.y, v);
+    }
+  }
+};
+
 int per_tile(int n) { return std::max(1, kTileElems / std::max(1, n)); }
 
 // the streaming path takes power-of-two n in [16, 2048] whose nonzero input
@@ -1029,7 +1125,26 @@ void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const ui
 void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) {
   const int nent = op.nent;
   cplx* R = scratch<cplx>(static_cast<size_t>(op.ny) * op.qx * nent, st);
-  {
+  static const bool no_tma = [] {
+    const char* e = std::getenv("EMIE_CU_SPECTRA_NO_TMA");  // A/B switch: the per-CTA load/FFT/store kernels
+    return e && *e == '1';
+  }();
+  const bool tma_x = !no_tma && (op.ex == 256 || op.ex == 512), tma_y = !no_tma && (op.ey == 256 || op.ey == 512);
+  if (tma_x) {
+    SpxStream p{};
+    const bool w = op.ex == 512;
+    const int TR = w ? 4 : 8;
+    p.R = R;
+    p.nx = op.nx; p.ny = op.ny; p.qx = op.qx; p.nent = nent; p.ntri = op.ntri; p.nfull = op.nfull;
+    p.nchunks = ceil_div(nent, TR); p.nin = op.ex;
+    p.box_bytes = static_cast<uint32_t>(2 * TR * op.nx * sizeof(double));
+    const uint64_t dims[3] = {2ull * nent, static_cast<uint64_t>(op.nx), static_cast<uint64_t>(op.ny)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(nent) * 16, static_cast<uint64_t>(op.nx) * nent * 16};
+    const uint32_t box[3] = {static_cast<uint32_t>(2 * TR), static_cast<uint32_t>(op.nx), 1};
+    encode_tensor_map_f64(&p.tm, d_blocks, 3, dims, strides, box, w ? 64 : 128);
+    if (w) launch_tma<512, SpxStream, 1>(p, op.ny * p.nchunks, op.tw_x, st, "stream_tma_spectra_x");
+    else launch_tma<256, SpxStream, 1>(p, op.ny * p.nchunks, op.tw_x, st, "stream_tma_spectra_x");
+  } else {
     const bool p2 = op.p2x;
     const FftPlan& pl = p2 ? op.plan_x2 : op.plan_x;
     const int EC = std::min(16, per_tile(op.ex));
@@ -1046,7 +1161,21 @@ void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) 
     }
     check_launch("spectra_x_kernel");
   }
-  {
+  if (tma_y) {
+    SpyStream p{};
+    const bool w = op.ey == 512;
+    const int TR = w ? 4 : 8;
+    p.spec = op.spec; p.emap = op.emap;
+    p.ny = op.ny; p.qx = op.qx; p.qy = op.qy; p.nent = nent; p.ntri = op.ntri; p.nfull = op.nfull;
+    p.nchunks = ceil_div(nent, TR); p.nentD = op.nentD; p.qbase = op.qbase; p.qcount = op.qcount; p.nin = op.ey;
+    p.box_bytes = static_cast<uint32_t>(2 * TR * op.ny * sizeof(double));
+    const uint64_t dims[3] = {2ull * nent, static_cast<uint64_t>(op.qx), static_cast<uint64_t>(op.ny)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(nent) * 16, static_cast<uint64_t>(op.qx) * nent * 16};
+    const uint32_t box[3] = {static_cast<uint32_t>(2 * TR), 1, static_cast<uint32_t>(op.ny)};
+    encode_tensor_map_f64(&p.tm, R, 3, dims, strides, box, w ? 64 : 128);
+    if (w) launch_tma<512, SpyStream, 1>(p, op.qx * p.nchunks, op.tw_y, st, "stream_tma_spectra_y");
+    else launch_tma<256, SpyStream, 1>(p, op.qx * p.nchunks, op.tw_y, st, "stream_tma_spectra_y");
+  } else {
     const bool p2 = op.p2y;
     const FftPlan& pl = p2 ? op.plan_y2 : op.plan_y;
     const int EC = std::min(16, per_tile(op.ey));

@@ -118,13 +118,13 @@ def test_fgmres_over_python_map_hook_and_preconditioner(torch_cuda):
     assert [i for i, _ in seen] == list(range(1, rep.iterations + 1))
     assert [r for _, r in seen] == rep.history
     assert calls[0] == rep.iterations + -(-rep.iterations // 12)  # + one residual per cycle, no speculation
-    s, _, _ = sysop.diagonals()
-    ncell = s.size
-    xp, rp = emie.fgmres(A, b, emie.SolverConfig(tol=1e-8, restart=40, max_iters=500,
-                                                 right_precond=lambda v: v / np.tile(s, v.size // ncell)))
-    assert rp.status == "converged", (rp.iterations, rp.residual)
+    # flexible right preconditioning (z_j = M v_j, x += sum y_j z_j): with M a
+    # scaling the Krylov space is unchanged, so the iterates match the plain solve
+    xp, rp = emie.fgmres(A, b, emie.SolverConfig(tol=1e-10, restart=12, right_precond=lambda v: 0.5 * v))
+    assert rp.status == "converged" and rp.iterations == rep.iterations, (rp.iterations, rp.residual)
+    assert np.max(np.abs(xp - xs)) <= 1e-9 * np.max(np.abs(xs))
     r = b - emie.apply_host(sysop, xp)
-    assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b)
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b)
 
     def boom(u):
         raise KeyError("map failed")
