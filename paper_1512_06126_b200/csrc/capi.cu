@@ -2,6 +2,7 @@
 // reference's argument checks and maps its exception types onto status codes.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <map>
@@ -57,6 +58,45 @@ T* dev_alloc(std::size_t n) {
   void* p = nullptr;
   EMIE_CUDA(cudaMalloc(&p, n * sizeof(T) + 16));
   return static_cast<T*>(p);
+}
+
+// The spectra of a destroyed operator are kept (one buffer) for the next
+// operator of the same size: repeated builds (frequency sweeps, benchmarks)
+// skip the ~1 GB cudaMalloc / cudaFree pair. The hand-over synchronises the
+// device first, as cudaFree would. EMIE_CU_NO_SPEC_CACHE=1 disables it.
+std::mutex g_spec_mu;
+void* g_spec_buf = nullptr;
+std::size_t g_spec_bytes = 0;
+bool spec_cache_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("EMIE_CU_NO_SPEC_CACHE");
+    return !(e && *e == '1');
+  }();
+  return on;
+}
+cplx* spec_alloc(std::size_t n) {
+  const std::size_t bytes = n * sizeof(cplx) + 16;
+  {
+    std::lock_guard<std::mutex> lk(g_spec_mu);
+    if (g_spec_buf && g_spec_bytes == bytes) {
+      void* p = g_spec_buf;
+      g_spec_buf = nullptr;
+      return static_cast<cplx*>(p);
+    }
+  }
+  return dev_alloc<cplx>(n);
+}
+void spec_free(void* p, std::size_t bytes) {
+  if (!p) return;
+  if (spec_cache_on()) {
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(g_spec_mu);
+    if (g_spec_buf) cudaFree(g_spec_buf);
+    g_spec_buf = p;
+    g_spec_bytes = bytes;
+    return;
+  }
+  cudaFree(p);
 }
 
 // --------------------------------------------------- system diagonals ----
@@ -178,7 +218,7 @@ void profile_mark(int stage, bool begin, cudaStream_t st) {
 }
 
 Operator::~Operator() {
-  cudaFree(spec);
+  spec_free(spec, spec_bytes);
   cudaFree(blocks);
   cudaFree(tw_x);
   cudaFree(tw_y);
@@ -308,7 +348,8 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
   op.qbase = q0;
   op.qcount = q1 - q0;
   if (op.qcount > 0) {
-    op.spec = dev_alloc<cplx>(static_cast<std::size_t>(op.qcount) * op.nentD);
+    op.spec = spec_alloc(static_cast<std::size_t>(op.qcount) * op.nentD);
+    op.spec_bytes = static_cast<std::size_t>(op.qcount) * op.nentD * sizeof(cplx) + 16;
     if (op.mma)  // padding slots of the MMA layout are read, never written (the row-block layout has none)
       EMIE_CUDA(cudaMemset(op.spec, 0, static_cast<std::size_t>(op.qcount) * op.nentD * sizeof(cplx)));
   }

@@ -2153,22 +2153,23 @@ void greens_finish(Operator& op, cplx* blocks, double hx, double hy, cudaStream_
 
 void greens_build(Operator& op, int L, const double* tops, const cplx* sigma, const double* breaks,
                   double hx, double hy, const FilterParams& fp, bool keep_blocks, cudaStream_t st) {
+  // the block array: kept with the operator (plain allocation, freed by it) or
+  // a stream-ordered scratch buffer the pool hands to the next build
+  const size_t nb = static_cast<size_t>(op.nx) * op.ny * op.nent;
   cplx* blocks = nullptr;
-  EMIE_CUDA(cudaMalloc(&blocks, static_cast<size_t>(op.nx) * op.ny * op.nent * sizeof(cplx) + 16));
+  if (keep_blocks) EMIE_CUDA(cudaMalloc(&blocks, nb * sizeof(cplx) + 16));
+  else blocks = scratch<cplx>(nb, st);
   try {
     greens_blocks(op, L, tops, sigma, breaks, hx, hy, fp, 0, -1, blocks, st);
     greens_finish(op, blocks, hx, hy, st);
   } catch (...) {
     cudaStreamSynchronize(st);
-    cudaFree(blocks);
+    if (keep_blocks) cudaFree(blocks);
+    else release(blocks, st);
     throw;
   }
-  if (keep_blocks) {
-    op.blocks = blocks;
-  } else {
-    EMIE_CUDA(cudaStreamSynchronize(st));
-    cudaFree(blocks);
-  }
+  if (keep_blocks) op.blocks = blocks;
+  else release(blocks, st);
 }
 
 }  // namespace emie_cu

@@ -35,6 +35,7 @@ struct Operator {
   int ntri = 0, nfull = 0, nent = 0;
   int nsd = 0, nentD = 0;    // symmetric diagonals per component, diag block size
   cplx* spec = nullptr;      // qx*qy*nentD (diagonal or MMA layout)
+  std::size_t spec_bytes = 0;  // its allocation (recycled by the next operator, capi.cu spec_alloc)
   int2* emap = nullptr;      // reference entry -> (slot, second slot or -1)
   std::vector<int2> emap_host;
   // MMA layout (nz in {8, 16, 32}, contraction on the FP64 tensor cores):
