@@ -463,9 +463,7 @@ __device__ unsigned long long g_phase_clk[8];
 // The lambda-only phases of a chunk (layered.cpp:67-129): 0a layer states,
 // 0b both reflection chains, 0c diag_a, into the chunk plan C, tasks strided
 // over (tid, nth); `sync`: a CTA-cooperative run (barriers between phases).
-// The assemble kernel runs it per chunk, or layer_state_kernel runs it ahead
-// for every chunk of a batch of offsets (one thread per lambda), writing the
-// SMEM image the assemble kernel then loads with one bulk copy.
+// The assemble kernel runs it per chunk, chunk_image_kernel per (offset, chunk).
 __device__ __forceinline__ void chunk_layer_states(const GreenParams& P, const Chunk& C, double R, int t0, int lc,
                                                    int tid, int nth, bool sync, const double* lam_in = nullptr) {
   const int L = P.L, NL = P.L + 1;
@@ -544,38 +542,6 @@ __device__ __forceinline__ void chunk_layer_states(const GreenParams& P, const C
       const cplx pq = C.p[li * 2 * NL + r] * C.q[li * 2 * NL + r];
       C.diag_a[li * 2 * NL + r] = crecip(eta * (em1 + e2l * (cplx{1.0, 0.0} - pq)));
     }
-}
-
-// chunk_layer_states for every (offset, lambda) of a batch, one thread per
-// lambda, into each chunk's SMEM image LS[b][chunk][14 NL LC] (the head of
-// the assemble kernel's Chunk plan: eta e2l em1 p q one_p one_q diag_a ieta)
-__global__ void __launch_bounds__(128) layer_state_kernel(const GreenParams P, const int* __restrict__ offs, int nb,
-                                                          int nchunk, cplx* __restrict__ LS) {
-  const int NL = P.L + 1, LC = P.LC;
-  const size_t ls_elems = static_cast<size_t>(14) * NL * LC;
-  const long long tot = static_cast<long long>(nb) * nchunk * LC;
-  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < tot;
-       x += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int li = static_cast<int>(x % LC);
-    const long long y = x / LC;
-    const int ch = static_cast<int>(y % nchunk), b = static_cast<int>(y / nchunk);
-    const int t = ch * LC + li;
-    if (t >= P.nw) continue;
-    const int code = offs[b];
-    const Geom g = pair_geometry(P.oc.oi(code), P.oc.oj(code), P.hx, P.hy);
-    cplx* img = LS + (static_cast<size_t>(b) * nchunk + ch) * ls_elems;
-    Chunk v;  // the one-lambda view of slot li
-    v.eta = img + li * NL;
-    v.e2l = img + LC * NL + li * NL;
-    v.em1 = img + 2 * LC * NL + li * NL;
-    v.p = img + 3 * LC * NL + li * 2 * NL;
-    v.q = img + 5 * LC * NL + li * 2 * NL;
-    v.one_p = img + 7 * LC * NL + li * 2 * NL;
-    v.one_q = img + 9 * LC * NL + li * 2 * NL;
-    v.diag_a = img + 11 * LC * NL + li * 2 * NL;
-    v.ieta = img + 13 * LC * NL + li * NL;
-    chunk_layer_states(P, v, g.r, t, 1, 0, 1, false);
-  }
 }
 
 // Chunk field accessors: F(li, f, j) interval field f of interval j at chunk
@@ -805,20 +771,85 @@ __device__ __forceinline__ void chunk_left(const GreenParams& P, const Chunk& C,
   }
 }
 
+// Fields of a chunk the pair phase reads (fPiu, fPic are consumed by chunk_left)
+constexpr int kImgFields = fPiu;
+#ifndef EMIE_GREEN_IMG_THREADS
+#define EMIE_GREEN_IMG_THREADS 128
+#endif
+#ifndef EMIE_GREEN_IMG_MINB
+#define EMIE_GREEN_IMG_MINB 4
+#endif
+constexpr int kImgThreads = EMIE_GREEN_IMG_THREADS;
+#ifndef EMIE_GREEN_IMG_LAMBDAS
+#define EMIE_GREEN_IMG_LAMBDAS 4
+#endif
+constexpr int kImgLambdas = EMIE_GREEN_IMG_LAMBDAS;  // lambdas per chunk_image_kernel CTA
+constexpr size_t kImgBudget = size_t{4} << 30;       // bytes of chunk images per batch
+
+// Per-lambda phases 0-1c of the accumulation (layer states, interval factors,
+// prefix products, left factors: everything of a chunk but the pair sums) for
+// one (offset, lambda chunk of LA) per CTA, at several CTAs per SM -- these
+// phases are latency-bound chains the single 256-thread CTA per SM of the pair
+// kernel hides poorly. Output: the chunk image IF[b][t][kImgFields][nz] and
+// IE[b][t][2][nz] (offset stride estride ints) the pair kernel streams in.
+__global__ void __launch_bounds__(kImgThreads, EMIE_GREEN_IMG_MINB) chunk_image_kernel(
+    const GreenParams P, const Interval* __restrict__ iv, const int* __restrict__ offs, int LA,
+    cplx* __restrict__ IF, int* __restrict__ IE, size_t estride) {
+  extern __shared__ cplx sm[];
+  const int NL = P.L + 1, nz = P.nz;
+  const int b = blockIdx.y, t0 = blockIdx.x * LA;
+  const int lc = min(LA, P.nw - t0);
+  const int code = offs[b];
+  const Geom g = pair_geometry(P.oc.oi(code), P.oc.oj(code), P.hx, P.hy);
+  Chunk C;
+  {
+    cplx* s = sm;
+    C.eta = s; s += LA * NL;
+    C.e2l = s; s += LA * NL;
+    C.em1 = s; s += LA * NL;
+    C.p = s; s += LA * 2 * NL;
+    C.q = s; s += LA * 2 * NL;
+    C.one_p = s; s += LA * 2 * NL;
+    C.one_q = s; s += LA * 2 * NL;
+    C.diag_a = s; s += LA * 2 * NL;
+    C.ieta = s; s += LA * NL;
+    C.F = s; s += static_cast<size_t>(LA) * kFields * nz;
+    C.lam = nullptr;
+    C.E = reinterpret_cast<int*>(s);
+  }
+  chunk_layer_states(P, C, g.r, t0, lc, threadIdx.x, blockDim.x, true);
+  __syncthreads();
+  chunk_factors(P, C, iv, lc, P.omega * kMu0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  chunk_prefix(P, C, lc);
+  __syncthreads();
+  chunk_left(P, C, lc, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int per = kImgFields * nz;
+  cplx* dst = IF + (static_cast<size_t>(b) * P.nw + t0) * per;
+  for (int x = threadIdx.x; x < lc * per; x += blockDim.x) {
+    const int li = x / per;
+    dst[x] = C.F[static_cast<size_t>(li) * kFields * nz + (x - li * per)];
+  }
+  int* de = IE + b * estride + static_cast<size_t>(t0) * 2 * nz;
+  for (int x = threadIdx.x; x < lc * 2 * nz; x += blockDim.x) de[x] = C.E[x];
+}
+
 #ifndef EMIE_GREEN_MINB
 #define EMIE_GREEN_MINB 1  // CTAs per SM the register budget targets
 #endif
 #ifndef EMIE_GREEN_SMEM_KB
 #define EMIE_GREEN_SMEM_KB 200  // SMEM budget of the lambda chunk buffers
 #endif
-// LSPRE: the layer states of every chunk come precomputed (layer_state_kernel)
-template <bool LSPRE, bool FULL = false>
+// IMG: phases 0-1c come as chunk images (chunk_image_kernel) streamed in by
+// bulk copies into two SMEM buffers; the CTA runs only the pair phase
+template <bool FULL = false, bool IMG = false>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
-    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, const cplx* __restrict__ LS, int nchunk,
-    int pos0) {
+    cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, int pos0, const cplx* __restrict__ IF,
+    const int* __restrict__ IE, size_t estride) {
   extern __shared__ cplx sm[];
-  __shared__ uint64_t lsbar;
+  __shared__ uint64_t ibar[2];
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
   const int code = offs[blockIdx.x];
   const int off = P.oc.slot(code, pos0 + blockIdx.x);  // block / weight slot
@@ -829,7 +860,28 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   const double wmu = P.omega * kMu0;  // V1 = i wmu W00 (layered.cpp:400)
 
   Chunk C;
-  {
+  // IMG: two buffers {F [LC][kImgFields][nz], E [LC][2][nz] (16-byte padded)}, then lam
+  const size_t ibufF = static_cast<size_t>(LC) * kImgFields * nz;
+  const size_t ibufE = (static_cast<size_t>(LC) * 2 * nz + 3) / 4 * 2;  // in cplx units
+  cplx* ibuf[2] = {sm, sm + ibufF + ibufE};
+  auto img_issue = [&](int c) {  // one thread: chunk c's image into buffer c & 1
+    const int s0 = c * LC, n = min(LC, P.nw - s0);
+    const uint32_t fb = static_cast<uint32_t>(n) * kImgFields * nz * sizeof(cplx);
+    const uint32_t eb = (static_cast<uint32_t>(n) * 2 * nz * sizeof(int) + 15u) & ~15u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&ibar[c & 1], fb + eb);
+    bulk_g2s(ibuf[c & 1], IF + (static_cast<size_t>(blockIdx.x) * P.nw + s0) * kImgFields * nz, fb, &ibar[c & 1]);
+    bulk_g2s(ibuf[c & 1] + ibufF, IE + blockIdx.x * estride + static_cast<size_t>(s0) * 2 * nz, eb, &ibar[c & 1]);
+  };
+  if constexpr (IMG) {
+    C.lam = reinterpret_cast<double*>(sm + 2 * (ibufF + ibufE));
+    if (threadIdx.x == 0) {
+      mbar_init(&ibar[0], 1);
+      mbar_init(&ibar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      img_issue(0);
+    }
+  } else {
     cplx* s = sm;
     C.eta = s; s += LC * NL;
     C.e2l = s; s += LC * NL;
@@ -846,16 +898,6 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   }
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
   auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 2 + f) * nz + j]; };
-  // layer-state image of a chunk (eta .. ieta, the head of the SMEM plan)
-  const size_t ls_elems = static_cast<size_t>(14) * NL * LC;
-  const uint32_t ls_bytes = static_cast<uint32_t>(ls_elems * sizeof(cplx));
-  if (LSPRE && threadIdx.x == 0) {
-    mbar_init(&lsbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&lsbar, ls_bytes);
-    bulk_g2s(sm, LS + static_cast<size_t>(blockIdx.x) * nchunk * ls_elems, ls_bytes, &lsbar);
-  }
-
   // Pair assignment (balanced): group pairs [g0, g0 + cnt), cnt <= 3T. Slots
   // 0, 1: pair g0 + i T + tid over the full lambda range. The ntail = cnt - 2T
   // remaining pairs are split over lambda: thread tid < Teff = (T / ntail) ntail
@@ -895,10 +937,12 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   long long clk = clock64();
 #endif
+  const int fstride = (IMG ? kImgFields : kFields) * nz;  // complex per lambda of C.F
   for (int t0 = 0; t0 < nw; t0 += LC) {
     const int lc = min(LC, nw - t0);
     __syncthreads();  // previous chunk consumed
     PHASE_MARK(0);
+    if (IMG && threadIdx.x == 0 && t0 + LC < nw) img_issue(t0 / LC + 1);  // into the buffer just freed
     // per-lambda scalars of the chunk
     for (int li = threadIdx.x; li < lc; li += blockDim.x) {
       const int t = t0 + li;
@@ -912,28 +956,25 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       C.lam[5 * LC + li] = Woff[5 * nw + t] * lam;
       C.lam[6 * LC + li] = lam * lam;
     }
-    if constexpr (LSPRE) {
-      // the chunk's layer states come precomputed (layer_state_kernel): one
-      // bulk copy, issued after the previous chunk's phase 1
-      mbar_wait(&lsbar, static_cast<uint32_t>((t0 / LC) & 1));
+    if constexpr (IMG) {
+      const int c = t0 / LC;
+      C.F = ibuf[c & 1];
+      C.E = reinterpret_cast<int*>(ibuf[c & 1] + ibufF);
+      mbar_wait(&ibar[c & 1], static_cast<uint32_t>((c >> 1) & 1));
     } else {
       chunk_layer_states(P, C, R, t0, lc, threadIdx.x, blockDim.x, true);
     }
     __syncthreads();
     PHASE_MARK(3);
+    if constexpr (!IMG) {
     chunk_factors(P, C, iv, lc, wmu, threadIdx.x, blockDim.x);
-    if constexpr (LSPRE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // layer-state reads before the refill
     __syncthreads();
-    if (LSPRE && threadIdx.x == 0 && t0 + LC < nw) {  // phase 1 was the last reader of the layer states
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&lsbar, ls_bytes);
-      bulk_g2s(sm, LS + (static_cast<size_t>(blockIdx.x) * nchunk + t0 / LC + 1) * ls_elems, ls_bytes, &lsbar);
-    }
     PHASE_MARK(4);
     chunk_prefix(P, C, lc);
     __syncthreads();
     chunk_left(P, C, lc, threadIdx.x, blockDim.x);
     __syncthreads();
+    }
     PHASE_MARK(5);
     // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
 #pragma unroll kPairUnroll
@@ -941,7 +982,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
       double wl[NWL];
 #pragma unroll
       for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
-      const cplx* Fl = C.F + static_cast<size_t>(li) * kFields * nz;
+      const cplx* Fl = C.F + static_cast<size_t>(li) * fstride;
       const int* El = C.E + li * 2 * nz;
       if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
         pair_lambda<1, FULL>(Fl, El, nz, pc[0], wl, acc[0]);
@@ -958,7 +999,7 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
         double wl[NWL];
 #pragma unroll
         for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda<-1, FULL>(C.F + static_cast<size_t>(li) * kFields * nz, C.E + li * 2 * nz, nz, pc[NS], wl,
+        pair_lambda<-1, FULL>(C.F + static_cast<size_t>(li) * fstride, C.E + li * 2 * nz, nz, pc[NS], wl,
                               acc[NS]);
       }
     }
@@ -2006,7 +2047,6 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
                       static_cast<size_t>(P.LC) * 2 * nz * sizeof(int);
   set_smem(reinterpret_cast<const void*>(assemble_kernel<false>), smem);
   set_smem(reinterpret_cast<const void*>(assemble_kernel<true>), smem);
-  set_smem(reinterpret_cast<const void*>(assemble_kernel<false, true>), smem);
   const int groups = ceil_div(P.npairs, (kGreenSlots + 1) * kGreenThreads);
   dim3 grid(ncomp, groups);
   profile_mark(5, true, st);
@@ -2016,37 +2056,55 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     EMIE_CUDA(cudaMemcpyToSymbolAsync(g_phase_clk, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
   }
 #endif
-  // the lambda-only phases ahead of the assembly (layer_state_kernel, high
-  // occupancy) for batches of offsets
-  // (only when an offset's pairs span several group CTAs, which would each
-  // recompute them: nz > 32; measured slower for one group, config 3)
-  static const int ls_mode = [] {
-    const char* e = std::getenv("EMIE_CU_GREENS_LS");  // 0: inline, 1: precomputed, unset: by group count
+  // Split (chunk_image_kernel + the pair kernel on streamed images) when an
+  // offset's pairs span several group CTAs, each of which would recompute the
+  // per-lambda phases (nz > 32: config 4 620 -> 455 ms); with one group the
+  // fused kernel is faster (config 3 33 vs 39 ms: the phases are issue-bound,
+  // more CTAs per SM do not speed them up, and the images cost HBM traffic).
+  static const int img_mode = [] {
+    const char* e = std::getenv("EMIE_CU_GREENS_IMG");  // 0: fused, 1: split, unset: by group count
     return e && *e ? std::atoi(e) : -1;
   }();
-  const bool pre = !full && (ls_mode < 0 ? groups > 1 : ls_mode == 1);
-  if (!pre) {
-    if (full)
-      assemble_kernel<false, true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
-    else
-      assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, nullptr, 0, 0);
-    check_launch("assemble_kernel");
-  } else {
-    const int nchunk = ceil_div(P.nw, P.LC);
-    const size_t ls_elems = static_cast<size_t>(14) * NL * P.LC;
-    const int batch = std::min(ncomp, 4096);
-    cplx* LS = scratch<cplx>(static_cast<size_t>(batch) * nchunk * ls_elems, st);
+  if (!full && (img_mode < 0 ? groups > 1 : img_mode == 1)) {
+    const int LA = kImgLambdas;
+    const size_t smemA = static_cast<size_t>(LA) * (14 * NL + kFields * nz) * sizeof(cplx) +
+                         static_cast<size_t>(LA) * 2 * nz * sizeof(int);
+    set_smem(reinterpret_cast<const void*>(chunk_image_kernel), smemA);
+    GreenParams PB = P;
+    {
+      const size_t per_lambda = 2 * (kImgFields * static_cast<size_t>(nz) * sizeof(cplx) + 2 * nz * sizeof(int)) +
+                                8 * sizeof(double);
+      int lcb = static_cast<int>(std::max<size_t>(2, std::min<size_t>(32, (size_t{EMIE_GREEN_SMEM_KB} << 10) / per_lambda)));
+      PB.LC = lcb & ~1;  // even: every chunk's exponent image starts 16-byte aligned
+    }
+    const size_t ibufF = static_cast<size_t>(PB.LC) * kImgFields * nz;
+    const size_t ibufE = (static_cast<size_t>(PB.LC) * 2 * nz + 3) / 4 * 2;
+    const size_t smemB = (2 * (ibufF + ibufE)) * sizeof(cplx) + 8 * static_cast<size_t>(PB.LC) * sizeof(double);
+    set_smem(reinterpret_cast<const void*>(assemble_kernel<false, true>), smemB);
+    const size_t fper = static_cast<size_t>(P.nw) * kImgFields * nz;  // complex per offset
+    const size_t estride = (static_cast<size_t>(P.nw) * 2 * nz + 3) & ~size_t{3};
+    const size_t per_off = fper * sizeof(cplx) + estride * sizeof(int);
+    const int maxb = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, kImgBudget / per_off)));
+    const int nbatch = ceil_div(ncomp, maxb), batch = ceil_div(ncomp, nbatch);
+    cplx* IF = scratch<cplx>(static_cast<size_t>(batch) * fper, st);
+    int* IE = scratch<int>(static_cast<size_t>(batch) * estride, st);
     for (int b0 = 0; b0 < ncomp; b0 += batch) {
       const int nb = std::min(batch, ncomp - b0);
-      const long long tot = static_cast<long long>(nb) * nchunk * P.LC;
-      const int lgrid = static_cast<int>(std::min<long long>(ceil_div(tot, 128), 32LL * sm_count()));
-      layer_state_kernel<<<lgrid, 128, 0, st>>>(P, offs + b0, nb, nchunk, LS);
-      check_launch("layer_state_kernel");
-      assemble_kernel<true><<<dim3(nb, groups), kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs + b0, LS,
-                                                                           nchunk, b0);
+      chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), nb), kImgThreads, smemA, st>>>(P, div, offs + b0, LA, IF, IE,
+                                                                                     estride);
+      check_launch("chunk_image_kernel");
+      assemble_kernel<false, true><<<dim3(nb, groups), kGreenThreads, smemB, st>>>(
+          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride);
       check_launch("assemble_kernel");
     }
-    release(LS, st);
+    release(IF, st);
+    release(IE, st);
+  } else {
+    if (full)
+      assemble_kernel<true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0);
+    else
+      assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0);
+    check_launch("assemble_kernel");
   }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
   {

@@ -107,11 +107,12 @@ def test_greens_errors(torch_cuda):
 
 
 @pytest.mark.parametrize("nz", [8, 48])
-def test_precomputed_layer_states_bit_identical(torch_cuda, nz):
-    """the lambda-only phases (layer states, reflection chains, diag_a) run
-    ahead in layer_state_kernel and reach the assembly by bulk copy (the
-    default when an offset's pairs span several CTAs, nz > 32) or inline in
-    the assemble kernel: the blocks agree to rounding"""
+def test_split_chunk_images_match_fused(torch_cuda, nz):
+    """the per-lambda phases (layer states, interval factors, prefix products,
+    left factors) run ahead in chunk_image_kernel and reach the pair kernel as
+    streamed chunk images (the default when an offset's pairs span several
+    CTAs, nz > 32) or inline in the fused assemble kernel: the blocks agree to
+    rounding"""
     import os
     import subprocess
     import sys
@@ -128,8 +129,8 @@ np.save(sys.argv[1], op.blocks())
 """
     outs = []
     for flag in ("0", "1"):
-        env = dict(os.environ, EMIE_CU_GREENS_LS=flag)
-        f = Path(f"/tmp/emie_ls_{nz}_{flag}.npy")
+        env = dict(os.environ, EMIE_CU_GREENS_IMG=flag)
+        f = Path(f"/tmp/emie_img_{nz}_{flag}.npy")
         subprocess.run([sys.executable, "-c", code, str(f)], env=env, check=True)
         outs.append(np.load(f))
     assert np.all(np.isfinite(outs[0]))
