@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--peer-sync", default="flags", choices=["flags", "host"],
                    help="--strong --exchange peer: device flag barriers, or stream sync + a host barrier (ranks "
                         "sharing one GPU: no kernel may spin on another process's flag)")
+    p.add_argument("--shard-layout", default="auto", choices=["auto", "octant", "quadrant"],
+                   help="--strong: octant rows per rank (square grids with hx == hy: each stored block read once "
+                        "for a mode and its transpose) or quadrant-mode ranges; auto = octant where possible")
     p.add_argument("--check", action="store_true",
                    help="--strong: compare the sharded apply with the unsharded device apply (gathered on rank 0)")
     return p.parse_args()
@@ -629,8 +632,9 @@ def pcie_bandwidth(hin, hout, din, dout):
 # ------------------------------------------------- strong-scaling arm ----
 def run_strong(args):
     """One grid sharded over the N ranks: each rank owns a
-    depth slab and a quadrant-mode shard of the spectra; two all-to-alls per
-    apply (NCCL; N = 1 runs the same stages through the loopback)."""
+    depth slab and a mode shard of the spectra (octant rows on square grids,
+    else a quadrant-mode range); two column transposes per apply (peer stores
+    or NCCL; N = 1 runs the same stages through the loopback)."""
     import torch
     import paper_1512_06126_b200 as emie
     from paper_1512_06126_b200 import configs
@@ -657,7 +661,11 @@ def run_strong(args):
     # the Green's build sharded by offset (summed block arrays), each rank
     # keeping only the spectra of its quadrant-mode shard
     ex, ey = emie.smooth_embedding_size(2 * cfg.nx - 1), emie.smooth_embedding_size(2 * cfg.ny - 1)
-    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, ex, ey, world)
+    square = cfg.nx == cfg.ny and cfg.hx == cfg.hy and ex == ey
+    if args.shard_layout == "octant" and not square:
+        raise SystemExit("--shard-layout octant needs a square grid with hx == hy")
+    octant = square and args.shard_layout != "quadrant"
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, ex, ey, world, octant=octant)
     torch.cuda.synchronize()
     tg0 = time.perf_counter()
     red = D.torch_block_sum() if world > 1 else D.loopback_block_sum
@@ -748,10 +756,12 @@ def run_strong(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded config conductivity field, seeded fields)",
             "config": {"workload": f"cfg{args.config} {cfg.nx}x{cfg.ny}x{cfg.nz} sharded over {world} rank(s): "
-                                   "depth slabs + quadrant-mode shards, 2 column transposes per apply "
+                                   "depth slabs + " + ("octant-row mode shards" if octant else "quadrant-mode shards")
+                                   + ", 2 column transposes per apply "
                                    + ("as peer stores into IPC-mapped buffers (flag barriers)"
                                       if args.exchange == "peer" else "as NCCL all-to-alls"),
                        "nrhs": NRHS, "slabs": plan.z, "mode_shards": plan.q,
+                       "shard_layout": "octant" if octant else "quadrant",
                        "greens_build": "sharded by offset, summed block arrays, per-rank mode-shard spectra"},
             "greens_build_s": greens_s,
             "e2e": {"value": NRHS * args.e2e_steps / float(e2e_s.item()), "unit": UNIT,

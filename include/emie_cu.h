@@ -341,6 +341,19 @@ int emie_cu_geometry_create(int nx, int ny, int nz, emie_cu_operator* out);
 /* a copy of op holding only quadrant modes [q0, q1) (a mode shard) */
 int emie_cu_operator_restrict_modes(emie_cu_operator op, int q0, int q1, emie_cu_operator* out);
 
+/* octant work for a mode shard (no reference counterpart: the reference has
+ * one process, toeplitz.cpp:197-258 reads every quadrant mode). For an
+ * x <-> y symmetric operator (emie_cu_operator_xy_symmetry) whose shard is
+ * whole rows of quadrant modes (q0, q1 multiples of qx), enable = 1 makes
+ * emie_cu_contract_modes / emie_cu_contract_modes_peer over the shard's range
+ * contract its octant rows: each block (qmy, qmx <= qmy) is read once and
+ * applied to that mode's columns and to the transposed mode's (qmx, qmy),
+ * so the caller's spectrum must hold the columns of every quadrant mode
+ * whose larger index is one of the shard's rows (distributed.ShardPlan with
+ * octant=True). Errors: INVALID_ARGUMENT when the operator is not symmetric
+ * or the shard not row-aligned. *out (optional) = the resulting state. */
+int emie_cu_operator_shard_octant(emie_cu_operator op, int enable, int* out);
+
 /* the full modes m = mx*ey + my of quadrant modes [q0, q1) in contraction
  * order (each quadrant mode's 1-4 mirrors); *count = total, at most cap written */
 int emie_cu_mode_list(emie_cu_operator op, int q0, int q1, int* h_modes, int cap, int* count);
@@ -445,6 +458,15 @@ int emie_cu_lateral_forward_peer(emie_cu_operator geom, const double* d_in, cons
                                  const int* d_owner, double* const* h_dst, int G, int nz_full, int z_offset,
                                  int nrhs, void* stream);
 int emie_cu_lateral_forward_peer_supported(emie_cu_operator geom, int* out);
+/* emie_cu_lateral_forward_peer with the owners given by the shard plan's
+ * G + 1 splits (host ints) instead of a per-mode table: octant = 1, rank g
+ * owns the quadrant modes whose larger index lies in rows [split[g],
+ * split[g+1]) (split[G] = qy); octant = 0, quadrant modes [split[g],
+ * split[g+1]) (split[G] = qx qy). The owner is then computed on the store
+ * path, no table load per element. */
+int emie_cu_lateral_forward_peer_split(emie_cu_operator geom, const double* d_in, const double* d_r2,
+                                       const int* h_split, int octant, double* const* h_dst, int G, int nz_full,
+                                       int z_offset, int nrhs, void* stream);
 /* emie_cu_contract_modes with the results stored straight into the slab
  * owners' spectra (fused contraction + return transpose; DMMA layouts, nz in
  * {8, 16, 32, 48, 64}): the contracted plane a*nz + k of mode m goes to rank h with

@@ -148,6 +148,7 @@ def lib():
         "emie_cu_geometry_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
         "emie_cu_operator_restrict_modes": [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
         "emie_cu_mode_list": [vp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_int, ip],
+        "emie_cu_operator_shard_octant": [vp, ctypes.c_int, ip],
         "emie_cu_lateral_forward": [vp, vp, vp, vp, ctypes.c_int, vp],
         "emie_cu_lateral_inverse": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp],
         "emie_cu_contract_modes": [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
@@ -165,6 +166,8 @@ def lib():
         "emie_cu_lateral_forward_peer": [vp, vp, vp, vp, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_lateral_forward_peer_supported": [vp, ip],
+        "emie_cu_lateral_forward_peer_split": [vp, vp, vp, ip, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
         "emie_cu_contract_modes_peer": [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ip,
                                         ctypes.c_int, vp],
     }

@@ -740,7 +740,22 @@ int emie_cu_operator_restrict_modes(emie_cu_operator h, int q0, int q1, emie_cu_
     if (q1 > q0)
       EMIE_CUDA(cudaMemcpy(r->op.spec, src.spec + static_cast<std::size_t>(q0 - src.qbase) * src.nentD,
                            static_cast<std::size_t>(q1 - q0) * src.nentD * sizeof(cplx), cudaMemcpyDeviceToDevice));
+    // the x <-> y symmetry carries over to a row-aligned shard (its octant lists)
+    r->op.xysym = src.xysym;
+    set_octant_lists(r->op, nullptr);
     *out = r.release();
+  });
+}
+
+int emie_cu_operator_shard_octant(emie_cu_operator h, int enable, int* out) {
+  return guarded([&] {
+    if (!h) fail(EMIE_CU_INVALID_ARGUMENT, "shard_octant: null operator");
+    Operator& op = h->op;
+    if (enable && !(op.xysym && op.noct > 0))
+      fail(EMIE_CU_INVALID_ARGUMENT,
+           "shard_octant: the operator is not x <-> y symmetric or its shard is not whole rows of quadrant modes");
+    op.shard_octant = enable != 0;
+    if (out) *out = op.shard_octant ? 1 : 0;
   });
 }
 
@@ -799,7 +814,37 @@ int emie_cu_lateral_forward_peer(emie_cu_operator geom, const double* d_in, cons
     const cudaStream_t st = as_stream(stream);
     cplx* T = scratch<cplx>(static_cast<std::size_t>(nrhs) * 3 * op.nz * op.ny * op.ex, st);
     lateral_forward_peer(op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<const cplx*>(d_r2), T, d_owner,
-                         dst.data(), G, nz_full, z_offset, nrhs, st);
+                         nullptr, 0, dst.data(), G, nz_full, z_offset, nrhs, st);
+    release(T, st);
+  });
+}
+
+int emie_cu_lateral_forward_peer_split(emie_cu_operator geom, const double* d_in, const double* d_r2,
+                                       const int* h_split, int octant, double* const* h_dst, int G, int nz_full,
+                                       int z_offset, int nrhs, void* stream) {
+  return guarded([&] {
+    if (!geom || !d_in || !h_split || !h_dst)
+      fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: null pointer");
+    if (nrhs < 1) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: nrhs < 1");
+    const Operator& op = geom->op;
+    if (z_offset < 0 || z_offset + op.nz > nz_full)
+      fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: slab outside the full depth");
+    if (G < 1) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: bad rank count");
+    if (octant && op.ex != op.ey) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: octant needs ex == ey");
+    const int end = octant ? op.qy : op.qx * op.qy;
+    if (h_split[0] != 0 || h_split[G] != end)
+      fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: splits must run from 0 to the row / mode count");
+    for (int g = 0; g < G; ++g)
+      if (h_split[g + 1] < h_split[g]) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: splits decrease");
+    std::vector<cplx*> dst(G);
+    for (int g = 0; g < G; ++g) {
+      if (!h_dst[g]) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer_split: null destination");
+      dst[g] = reinterpret_cast<cplx*>(h_dst[g]);
+    }
+    const cudaStream_t st = as_stream(stream);
+    cplx* T = scratch<cplx>(static_cast<std::size_t>(nrhs) * 3 * op.nz * op.ny * op.ex, st);
+    lateral_forward_peer(op, reinterpret_cast<const cplx*>(d_in), reinterpret_cast<const cplx*>(d_r2), T, nullptr,
+                         h_split, octant ? 1 : 0, dst.data(), G, nz_full, z_offset, nrhs, st);
     release(T, st);
   });
 }

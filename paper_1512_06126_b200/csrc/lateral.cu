@@ -741,21 +741,34 @@ struct FyStream {
 // full-depth spectrum of m's owner rank (peer memory over NVLink) at depth
 // offset zoff, S_g[r][m][c*nzf + zoff + z], instead of the slab's own S
 constexpr int kMaxFyPeers = 64;
+// The owner of mode (mx, my) comes from the plan -- no global-memory load on
+// the store path (a per-mode owner table in HBM cost the pass 2x: 113 vs 58 us
+// for one rank at config 3) -- or, for any other plan, from that table:
+//   octant plans: the rank whose rows [split_g, split_g+1) hold max(qmx, qmy),
+//     one byte of a row -> rank table in the kernel parameters;
+//   quadrant plans: the rank whose range holds qm = qmy qx + qmx (split scan),
+// with (qmx, qmy) the quadrant mode of (mx, my) (folds mx -> ex - mx past ex/2).
+constexpr int kMaxFyRows = 260;  // quadrant rows of a 512-point embedding (257), padded
 struct FyPeerStream : FyStream {
-  cplx* pdst[kMaxFyPeers];  // owner rank -> its full-depth spectrum
-  const int* owner;         // mode (mx*ey + my) -> owner rank
-  int nzf, zoff;            // full depth, this slab's first interval
+  cplx* pdst[kMaxFyPeers];     // owner rank -> its full-depth spectrum
+  const int* owner;            // mode (mx*ey + my) -> owner rank, or nullptr: the splits
+  int split[kMaxFyPeers + 1];  // split[g] .. split[g+1]: rank g's rows (oct) or quadrant modes
+  int G, oct, qx;
+  unsigned char row_owner[kMaxFyRows];  // oct: quadrant row -> owner rank
+  int nzf, zoff;               // full depth, this slab's first interval
   // the last pass gives each thread one plane of the tile (t = tid mod 8,
   // transform index fastest), so its depth offset and sign class are per tile
   struct Ops {
     long long rE;  // r * ex * ey
     int mx, poff;  // poff: c * nzf + zoff + z of the thread's plane, -1 past the slab
+    int qmx;       // quadrant column of mx
     bool xflip, ycls;
   };
   template <int N>
   __device__ void prefetch(int tile, Ops& o) const {
     int r, p0;
     coords<N>(tile, r, o.mx, p0);
+    o.qmx = 2 * o.mx > ex ? ex - o.mx : o.mx;
     o.rE = static_cast<long long>(r) * ex * N;
     const int plane = p0 + static_cast<int>(threadIdx.x) % Geo<N>::ntr;
     const int c = plane / nz, z = plane - c * nz;
@@ -769,7 +782,19 @@ struct FyPeerStream : FyStream {
     if (o.poff < 0) return;
     const bool flip = o.xflip || (o.ycls && 2 * my > N);
     const int m = o.mx * N + my;
-    gst(pdst[__ldg(owner + m)] + (o.rE + m) * 3 * nzf + o.poff, flip ? -v : v);
+    int g = 0;
+    if (owner) {
+      g = __ldg(owner + m);
+    } else if (oct) {  // one indexed constant-bank byte
+      g = row_owner[max(o.qmx, 2 * my > N ? N - my : my)];
+    } else {
+      const int qmy = 2 * my > N ? N - my : my;
+      const int key = qmy * qx + o.qmx;
+      for (int i = 1; i < G; ++i) g += key >= split[i] ? 1 : 0;
+    }
+    // indexed constant-bank load (measured: a 7-deep register select chain
+    // over the destinations is slower, 103 vs 58 us for one rank at config 3)
+    gst(pdst[g] + (o.rE + m) * 3 * nzf + o.poff, flip ? -v : v);
   }
 };
 
@@ -1259,7 +1284,8 @@ bool lateral_forward_peer_ok(const Operator& op) {
 }
 
 void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, cplx* T, const int* owner,
-                          cplx* const* dsts, int G, int nzf, int zoff, int nrhs, cudaStream_t st) {
+                          const int* split, int oct, cplx* const* dsts, int G, int nzf, int zoff, int nrhs,
+                          cudaStream_t st) {
   if (!lateral_forward_peer_ok(op)) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: needs 256/512-point TMA passes");
   if (G < 1 || G > kMaxFyPeers) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: bad rank count");
   const int np = 3 * op.nz;
@@ -1278,6 +1304,15 @@ void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, 
   p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ny;
   for (int g = 0; g < G; ++g) p.pdst[g] = dsts[g];
   p.owner = owner; p.nzf = nzf; p.zoff = zoff;
+  p.G = G; p.oct = oct; p.qx = op.qx;
+  if (!owner) {
+    for (int g = 0; g <= G; ++g) p.split[g] = split[g];
+    if (oct) {
+      if (op.qy > kMaxFyRows || G > 255) fail(EMIE_CU_INVALID_ARGUMENT, "lateral_forward_peer: embedding too large");
+      for (int g = 0; g < G; ++g)
+        for (int r = split[g]; r < split[g + 1]; ++r) p.row_owner[r] = static_cast<unsigned char>(g);
+    }
+  }
   if (op.ey == 256) launch_tma<256, FyPeerStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy_peer");
   else launch_tma<512, FyPeerStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy_peer");
 }

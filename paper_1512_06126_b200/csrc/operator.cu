@@ -311,8 +311,9 @@ constexpr int ct_blk_stages() { return OCT ? kBlkStagesOct : kBlkStages; }
 // exchanged and stored back exchanged: M(qmx, qmy) = P M(qmy, qmx) P with P
 // the x <-> y permutation, so one block read serves both modes and the MMA's
 // A fragment feeds two n8 products.
-// PEER (sharded apply, quadrant modes only): the results go to the slab
-// owners' spectra through po (peer memory over NVLink) instead of back into S
+// PEER (sharded apply): the results go to the slab owners' spectra through po
+// (peer memory over NVLink) instead of back into S; with OCT the rank's octant
+// items are its rows of the octant (Operator::shard_octant)
 template <int NZ, bool OCT, bool PEER = false>
 __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
@@ -499,7 +500,10 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
           if (cb >= 0) {
             const cplx v = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
             if constexpr (PEER) {
-              pdst[(cb / (3 * NZ)) * (3 * pnz)] = v;  // cb = (r E + mode) * np
+              // cb = (r E + mode) * np; a transposed-mode column's row is in the exchanged third
+              const bool sw = OCT && (cb & kSwapCol);
+              constexpr int asw = a == 2 ? 2 : 1 - a;
+              pdst[((cb & ~kSwapCol) / (3 * NZ)) * (3 * pnz) + (sw ? (asw - a) * pnz : 0)] = v;
             } else {
               const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? plane_sw : plane);
               S[o] = v;
@@ -716,7 +720,9 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
           if (cb >= 0) {
             const cplx v = cplx{p1[i][g][h] - p2[i][g][h], p3[i][g][h] - p1[i][g][h] - p2[i][g][h]};
             if constexpr (PEER) {
-              pdst[(cb / np) * (3 * pnz)] = v;  // cb = (r E + mode) * np
+              // cb = (r E + mode) * np; a transposed-mode column's row is in the exchanged third
+              const bool sw = OCT && (cb & kSwapCol);
+              pdst[((cb & ~kSwapCol) / np) * (3 * pnz) + (sw ? (asw - a) * pnz : 0)] = v;
             } else {
               const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? asw * NZ + rowc : plane);
               S[o] = v;
@@ -772,8 +778,10 @@ void set_smem(const void* fn, size_t bytes) {
 void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int sym_known) {
   lateral_spectra(op, d_blocks, st);
   bool sym = false;
-  const bool full = op.qbase == 0 && op.qcount == static_cast<int>(op.modes());
-  if (full && op.nx == op.ny && op.ex == op.ey && sym_known != 0) {
+  // whole rows of quadrant modes (a full operator or a row-aligned mode shard):
+  // the octant lists cover them (set_octant_lists)
+  const bool rows = op.qx > 0 && op.qcount > 0 && op.qbase % op.qx == 0 && op.qcount % op.qx == 0;
+  if (rows && op.nx == op.ny && op.ex == op.ey && sym_known != 0) {
     sym = true;
     if (sym_known < 0) {
       int* bad = scratch<int>(1, st);
@@ -790,29 +798,39 @@ void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int s
     }
   }
   op.xysym = sym;
+  set_octant_lists(op, st);
+}
+
+// The octant work lists of op's stored rows (qbase and qcount whole rows of
+// qx quadrant modes; every row of a full operator): octant modes qmx <= qmy
+// with qmy in those rows -- off-diagonal (two modes per block) first, the
+// diagonal (one mode) last, so the lighter items fill the tail -- then the
+// DFMA contraction's item codes. None unless op.xysym.
+void set_octant_lists(Operator& op, cudaStream_t st) {
   cudaFree(op.octl);
   op.octl = nullptr;
   op.noct = op.noctv = 0;
-  if (sym) {
-    // octant modes qmx <= qmy: off-diagonal (two modes per block) first, the
-    // diagonal (one mode) last, so the lighter items fill the tail
-    std::vector<int> l;
-    for (int qmy = 0; qmy < op.qy; ++qmy)
-      for (int qmx = 0; qmx < qmy; ++qmx) l.push_back(qmy * op.qx + qmx);
-    for (int q = 0; q < op.qx; ++q) l.push_back(q * op.qx + q);
-    // the DFMA contraction's items: 2 qm (+ 2 qm + 1 for the transposed mode)
-    std::vector<int> v;
-    for (int qm : l) {
-      v.push_back(2 * qm);
-      if (qm / op.qx != qm % op.qx) v.push_back(2 * qm + 1);
-    }
-    EMIE_CUDA(cudaMalloc(&op.octl, (l.size() + v.size()) * sizeof(int)));
-    EMIE_CUDA(cudaMemcpyAsync(op.octl, l.data(), l.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    EMIE_CUDA(cudaMemcpyAsync(op.octl + l.size(), v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    EMIE_CUDA(cudaStreamSynchronize(st));
-    op.noct = static_cast<int>(l.size());
-    op.noctv = static_cast<int>(v.size());
+  if (!op.xysym || op.qx == 0 || op.qbase % op.qx != 0 || op.qcount % op.qx != 0 || op.qcount == 0) {
+    op.xysym = false;
+    return;
   }
+  const int y0 = op.qbase / op.qx, y1 = (op.qbase + op.qcount) / op.qx;
+  std::vector<int> l;
+  for (int qmy = y0; qmy < y1; ++qmy)
+    for (int qmx = 0; qmx < qmy; ++qmx) l.push_back(qmy * op.qx + qmx);
+  for (int q = y0; q < y1; ++q) l.push_back(q * op.qx + q);
+  // the DFMA contraction's items: 2 qm (+ 2 qm + 1 for the transposed mode)
+  std::vector<int> v;
+  for (int qm : l) {
+    v.push_back(2 * qm);
+    if (qm / op.qx != qm % op.qx) v.push_back(2 * qm + 1);
+  }
+  EMIE_CUDA(cudaMalloc(&op.octl, (l.size() + v.size()) * sizeof(int)));
+  EMIE_CUDA(cudaMemcpyAsync(op.octl, l.data(), l.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaMemcpyAsync(op.octl + l.size(), v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  EMIE_CUDA(cudaStreamSynchronize(st));
+  op.noct = static_cast<int>(l.size());
+  op.noctv = static_cast<int>(v.size());
 }
 
 // octant contraction in use (EMIE_CU_NO_OCTANT=1 turns it off, for A/B runs)
@@ -821,8 +839,11 @@ static bool use_octant(const Operator& op, int q0, int q1) {
     const char* e = std::getenv("EMIE_CU_NO_OCTANT");
     return e && e[0] == '1';
   }();
-  return !off && op.xysym && op.noct > 0 && op.qbase == 0 && q0 == 0 &&
-         q1 == static_cast<int>(op.modes()) && op.qcount == q1;
+  // a mode shard contracts its octant rows only when the sharded apply's plan
+  // delivers the transposed modes' columns too (Operator::shard_octant)
+  const bool full = op.qbase == 0 && op.qcount == static_cast<int>(op.modes());
+  return !off && op.xysym && op.noct > 0 && q0 == op.qbase && q1 == op.qbase + op.qcount &&
+         (full || op.shard_octant);
 }
 
 // K_ct over quadrant modes [q0, q1) (all stored in op: qbase <= q0, q1 <= qbase + qcount):
@@ -936,7 +957,9 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
     PeerOut pg = po;  // the group's rhs offset: mode index r*E + m counts from r0
     for (int h = 0; h < po.G; ++h)
       pg.dst[h] = po.dst[h] + static_cast<size_t>(r0) * op.lateral() * 3 * (po.z[h + 1] - po.z[h]);
-    const int nc = ct_cols<false>();
+    const bool oct = use_octant(op, q0, q1);
+    const int nc = oct ? ct_cols<true>() : ct_cols<false>();
+    const int nwork = oct ? op.noct : q1 - q0;
     if (op.rows) {
       const size_t smem = 1024 + static_cast<size_t>(kRowsRing) * 3 * op.nz * 128 +
                           kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
@@ -948,27 +971,39 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
       encode_tensor_map_f64(&tm, op.spec, 4, dims, strides, box);
       auto launch_rows = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
-        const int grid = std::max(1, std::min(sms * per_sm, q1 - q0));
+        const int grid = std::max(1, std::min(sms * per_sm, nwork));
         kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1, op.qbase,
-                                                   g, nullptr, 0, pg);
+                                                   g, op.octl, op.noct, pg);
       };
-      if (op.nz == 48) launch_rows(contract_rows_kernel<48, false, true>, rows_warps<48>());
-      else launch_rows(contract_rows_kernel<64, false, true>, rows_warps<64>());
+      if (op.nz == 48) {
+        if (oct) launch_rows(contract_rows_kernel<48, true, true>, rows_warps<48>());
+        else launch_rows(contract_rows_kernel<48, false, true>, rows_warps<48>());
+      } else {
+        if (oct) launch_rows(contract_rows_kernel<64, true, true>, rows_warps<64>());
+        else launch_rows(contract_rows_kernel<64, false, true>, rows_warps<64>());
+      }
       check_launch("contract_rows_kernel (peer epilogue)");
       continue;
     }
+    const int bst = oct ? ct_blk_stages<true>() : ct_blk_stages<false>();
     const size_t smem = 128 + kUStages * nc * sizeof(long long) +
-                        ct_blk_stages<false>() * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                        bst * static_cast<size_t>(op.nentD) * sizeof(cplx) +
                         kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
     auto launch = [&](auto kern, int warps) {
       const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
-      const int grid = std::max(1, std::min(sms * per_sm, q1 - q0));
+      const int grid = std::max(1, std::min(sms * per_sm, nwork));
       kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0,
-                                                 q1, op.qbase, g, op.nentD, nullptr, 0, pg);
+                                                 q1, op.qbase, g, op.nentD, op.octl, op.noct, pg);
     };
-    if (op.nz == 8) launch(contract_mma_kernel<8, false, true>, mma_warps<8>());
-    else if (op.nz == 16) launch(contract_mma_kernel<16, false, true>, mma_warps<16>());
-    else launch(contract_mma_kernel<32, false, true>, mma_warps<32>());
+    if (oct) {
+      if (op.nz == 8) launch(contract_mma_kernel<8, true, true>, mma_warps<8>());
+      else if (op.nz == 16) launch(contract_mma_kernel<16, true, true>, mma_warps<16>());
+      else launch(contract_mma_kernel<32, true, true>, mma_warps<32>());
+    } else {
+      if (op.nz == 8) launch(contract_mma_kernel<8, false, true>, mma_warps<8>());
+      else if (op.nz == 16) launch(contract_mma_kernel<16, false, true>, mma_warps<16>());
+      else launch(contract_mma_kernel<32, false, true>, mma_warps<32>());
+    }
     check_launch("contract_mma_kernel (peer epilogue)");
   }
 }

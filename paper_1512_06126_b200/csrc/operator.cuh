@@ -72,6 +72,12 @@ struct Operator {
   bool xysym = false;
   int* octl = nullptr;  // noct octant modes, then the DFMA kernel's noctv item codes
   int noct = 0, noctv = 0;
+  // a row-aligned mode shard (qbase, qcount whole rows) of an xysym operator
+  // contracts its octant rows -- the modes (qmy, qmx <= qmy) of its rows and
+  // their transposes, i.e. every quadrant mode whose larger index is one of
+  // its rows -- instead of its quadrant modes; set by the sharded apply whose
+  // plan gives the rank those modes (emie_cu_operator_shard_octant)
+  bool shard_octant = false;
 
   std::size_t modes() const { return static_cast<std::size_t>(qx) * qy; }
   std::size_t lateral() const { return static_cast<std::size_t>(ex) * ey; }
@@ -103,13 +109,16 @@ void lateral_inverse(const Operator& op, const cplx* S, cplx* T, const cplx* d_i
 // the sharded apply's slab forward with the forward transpose fused into the
 // y pass (stores into the owners' full-depth spectra, owner[mode] -> rank)
 bool lateral_forward_peer_ok(const Operator& op);
+// owner: mode -> rank table, or nullptr and the plan's splits (rows when oct, else quadrant modes)
 void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, cplx* T, const int* owner,
-                          cplx* const* dsts, int G, int nzf, int zoff, int nrhs, cudaStream_t st);
+                          const int* split, int oct, cplx* const* dsts, int G, int nzf, int zoff, int nrhs,
+                          cudaStream_t st);
 
 // stages (operator.cu)
 // sym_known: 1 the blocks are x <-> y symmetric by construction, 0 they are
 // not, -1 check on the device (bitwise)
 void transform_blocks(Operator& op, const cplx* d_blocks, cudaStream_t st, int sym_known = -1);
+void set_octant_lists(Operator& op, cudaStream_t st);
 void apply_b(const Operator& op, const cplx* d_in, cplx* d_out, int nrhs,
              const System* sys, cudaStream_t st);
 void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaStream_t st);

@@ -10,7 +10,9 @@ split at its contraction:
      mirrors of g's quadrant modes, in contraction order) for its planes; g
      scatters them into the full-depth spectrum S[r][m][c*nz + z];
   3. rank g contracts its quadrant modes [q0, q1) with its shard of the
-     spectra (1/G of the operator in HBM);
+     spectra (1/G of the operator in HBM) -- or, with ShardPlan(octant=True)
+     on an x <-> y symmetric operator, the octant items of its rows of
+     quadrant modes, reading each block once for a mode and its transpose;
   4. all-to-all #2 returns the columns to the slab owners;
   5. every rank inverse-transforms its slab with the system epilogue.
 
@@ -50,15 +52,38 @@ def mirror_modes(qm: int, qx: int, ex: int, ey: int) -> List[int]:
     return out
 
 
+def octant_row_splits(qy: int, G: int) -> List[int]:
+    """Row boundaries of G octant shards: rank g owns rows [b_g, b_g+1) of
+    quadrant modes, i.e. the octant items (qmy, qmx <= qmy) of those rows --
+    2 qmy + 1 quadrant modes per row, r^2 over rows [0, r) -- balanced by
+    that count (b_g ~ qy sqrt(g / G)), at least one row each."""
+    if not 1 <= G <= qy:
+        raise ValueError("octant shard plan: need 1 <= G <= qy")
+    b = [0] + [int(round(qy * np.sqrt(g / G))) for g in range(1, G)] + [qy]
+    for g in range(1, G + 1):  # strictly increasing, room for the ranks after g
+        b[g] = min(max(b[g], b[g - 1] + 1), qy - (G - g))
+    return b
+
+
 @dataclass
 class ShardPlan:
-    """Depth slabs and quadrant-mode shards of G ranks for one grid."""
+    """Depth slabs and mode shards of G ranks for one grid.
+
+    octant=False: rank g owns quadrant modes [q_g, q_g+1) and contracts them.
+    octant=True (x <-> y symmetric operators, ex == ey): rank g owns whole
+    rows [b_g, b_g+1) of quadrant modes (its operator shard, q_g = b_g qx)
+    and contracts their octant items: each stored block (qmy, qmx <= qmy) is
+    read once and serves that mode and its transpose (qmx, qmy), so the rank's
+    modes are every quadrant mode whose larger index is one of its rows (an
+    L-shaped set) and its operator reads halve (csrc/operator.cu
+    contract_mma_kernel OCT, Operator::shard_octant)."""
     nx: int
     ny: int
     nz: int
     ex: int
     ey: int
     G: int
+    octant: bool = False
 
     def __post_init__(self):
         if not 1 <= self.G <= self.nz:
@@ -66,8 +91,18 @@ class ShardPlan:
         self.qx, self.qy = self.ex // 2 + 1, self.ey // 2 + 1
         self.E = self.ex * self.ey
         self.z = _splits(self.nz, self.G)
-        self.q = _splits(self.qx * self.qy, self.G)
-        self.modes = [np.array([m for qm in range(self.q[g], self.q[g + 1])
+        if self.octant:
+            if self.ex != self.ey:
+                raise ValueError("octant shard plan: needs a square embedding (ex == ey)")
+            self.rows = octant_row_splits(self.qy, self.G)
+            self.q = [r * self.qx for r in self.rows]
+            self.qmodes = [[qm for r in range(self.rows[g], self.rows[g + 1])
+                            for qm in [r * self.qx + c for c in range(r + 1)] + [c * self.qx + r for c in range(r)]]
+                           for g in range(self.G)]
+        else:
+            self.q = _splits(self.qx * self.qy, self.G)
+            self.qmodes = [list(range(self.q[g], self.q[g + 1])) for g in range(self.G)]
+        self.modes = [np.array([m for qm in self.qmodes[g]
                                 for m in mirror_modes(qm, self.qx, self.ex, self.ey)], dtype=np.int32)
                       for g in range(self.G)]
 
@@ -425,6 +460,8 @@ class CudaBackend:
         _check(L.emie_cu_geometry_create(plan.nx, plan.ny, nzl, ctypes.byref(g)))
         self.geom = g
         self.op = op_shard  # SpectralOperator holding quadrant modes [q0, q1)
+        if plan.octant:  # contract the shard's octant rows (the plan delivers the transposed modes)
+            _check(L.emie_cu_operator_shard_octant(op_shard.handle, 1, None))
         # local system diagonals (cie.cpp:24-54) of the slab's cells
         sysh = ctypes.c_void_p()
         sa = np.ascontiguousarray(sigma_slab, dtype=np.complex128)
@@ -476,21 +513,19 @@ class CudaBackend:
             v = ctypes.c_int(0)
             self._check(self.L.emie_cu_lateral_forward_peer_supported(self.geom, ctypes.byref(v)))
             self._fpf = bool(v.value)
-            if self._fpf:  # mode -> owner rank
-                own = np.empty(self.plan.E, np.int32)
-                for g, ms in enumerate(self.plan.modes):
-                    own[ms] = g
-                self.owner = self.torch.from_numpy(own).to(self.dev)
+            if self._fpf:  # the owners as the plan's splits (rows of the octant, or quadrant-mode ranges)
+                P = self.plan
+                self.splits = (ctypes.c_int * (P.G + 1))(*(P.rows if P.octant else P.q))
         return self._fpf
 
     def lateral_forward_peer(self, U, dsts, nrhs):
         P = self.plan
         G = len(dsts)
         dp = (ctypes.c_void_p * G)(*[d.data_ptr() for d in dsts])
-        self._check(self.L.emie_cu_lateral_forward_peer(self.geom, ctypes.c_void_p(U.data_ptr()),
-                                                        ctypes.c_void_p(self.r2.data_ptr()),
-                                                        ctypes.c_void_p(self.owner.data_ptr()), dp, G, P.nz,
-                                                        P.z[self.rank], nrhs, self._st()))
+        self._check(self.L.emie_cu_lateral_forward_peer_split(self.geom, ctypes.c_void_p(U.data_ptr()),
+                                                              ctypes.c_void_p(self.r2.data_ptr()), self.splits,
+                                                              1 if P.octant else 0, dp, G, P.nz, P.z[self.rank],
+                                                              nrhs, self._st()))
 
     @property
     def fused_peer_contract(self) -> bool:

@@ -51,7 +51,9 @@ class NumpyBackend:
         P = self.plan
         O = self._oracle()
         Sn = S.numpy()
-        for qm in range(q0, q1):
+        # the rank's quadrant modes (octant plans: its rows' modes and their transposes)
+        qms = P.qmodes[self.rank] if (q0, q1) == (P.q[self.rank], P.q[self.rank + 1]) else range(q0, q1)
+        for qm in qms:
             for m in mirror_modes(qm, P.qx, P.ex, P.ey):
                 mx, my = divmod(m, P.ey)
                 M = O._mode_matrix(self.comp, self.dims, P.nz, my, mx)

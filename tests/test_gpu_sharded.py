@@ -193,3 +193,164 @@ def test_sharded_greens_build_bit_identical(torch_cuda, cfg_id, G):
     outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
     got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
     assert np.array_equal(got, want)
+
+
+# ---- octant shards (ShardPlan(octant=True), Operator::shard_octant) --------
+@pytest.mark.parametrize("cfg_id,G", [(1, 1), (1, 2), (1, 3), (2, 4)])
+def test_octant_sharded_apply_loopback_bit_identical(torch_cuda, cfg_id, G):
+    """row-aligned mode shards of an x <-> y symmetric operator contracting
+    their octant rows (each block read once for a mode and its transpose):
+    bit-identical to the single-GPU octant apply -- every output column is the
+    same block times the same column in the same order"""
+    torch = torch_cuda
+    cfg, grid, sop, sysop = _system(cfg_id)
+    assert emie.xy_symmetric(sop)
+    nrhs = 2
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G, octant=True)
+    rng = np.random.default_rng(17 + G)
+    n = 3 * cfg.cells()
+    U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+    want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
+    got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("cfg_id,G", [(1, 2), (1, 3), (3, 2), (3, 8)])
+def test_octant_peer_exchange_loopback_bit_identical(torch_cuda, cfg_id, G, fused):
+    """the peer-store exchange over octant shards (the forward y pass storing
+    each mode's column into the owner of its L-shaped set; the contraction's
+    peer epilogue storing the transposed modes' rows into the exchanged
+    component): bit-identical to the single-GPU octant apply, twice in a row"""
+    torch = torch_cuda
+    cfg, grid, sop, sysop = _system(cfg_id)
+    nrhs = 2
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G, octant=True)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    xs, owns = D.peer_loopback(shards, fused=fused)
+    try:
+        for rep in range(2):
+            rng = np.random.default_rng(90 + G + rep)
+            n = 3 * cfg.cells()
+            U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+            want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+            outs = D.peer_loopback_apply(xs, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
+            got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+            assert np.array_equal(got, want), rep
+    finally:
+        torch.cuda.synchronize()
+        for o in owns:
+            D.PeerExchange.free(o)
+
+
+@pytest.mark.parametrize("nz,G", [(64, 2), (48, 3)])
+def test_octant_peer_exchange_deep_grid_bit_identical(torch_cuda, nz, G):
+    """nz 48/64: the row-block contraction, octant rows with the peer epilogue"""
+    torch = torch_cuda
+    tops, sigma = [0.0, 500.0, 2500.0], [0.0, 1e-3, 10 ** -1.5, 1.0]
+    breaks = list(np.linspace(600.0, 600.0 + 50.0 * nz, nz + 1))
+    model = emie.LayeredModel(tops, sigma)
+    nx = ny = 8
+    grid = emie.make_grid(model, breaks, nx, ny, 100.0, 100.0)
+    rng = np.random.default_rng(nz + 1)
+    grid.sigma_a[...] = 10.0 ** rng.uniform(-3, 0, (nz, ny, nx))
+    sop = emie.assemble_operator(grid, model, 2 * np.pi * 0.5)
+    assert emie.xy_symmetric(sop)
+    sysop = emie.build_system(grid, sop)
+    nrhs = 2
+    plan = D.ShardPlan(nx, ny, nz, sop.ex, sop.ey, G, octant=True)
+    n = 3 * nx * ny * nz
+    U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+    want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+    shards = [D.cuda_shard(grid, sop, plan, g, nrhs) for g in range(G)]
+    xs, owns = D.peer_loopback(shards)
+    try:
+        outs = D.peer_loopback_apply(xs, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
+        got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+        assert np.array_equal(got, want)
+    finally:
+        torch.cuda.synchronize()
+        for o in owns:
+            D.PeerExchange.free(o)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_octant_sharded_greens_build_bit_identical(torch_cuda, G):
+    """the offset-sharded Green's build feeding octant shards: each rank's
+    shard operator checks the x <-> y symmetry on the summed blocks and
+    contracts its octant rows; equal to the single-GPU build + octant apply"""
+    torch = torch_cuda
+    cfg = configs.config(1)
+    model = emie.LayeredModel(cfg.tops, cfg.sigma)
+    grid = emie.make_grid(model, cfg.breaks, cfg.nx, cfg.ny, cfg.hx, cfg.hy)
+    grid.sigma_a[...] = cfg.sigma_a
+    sop = emie.assemble_operator(grid, model, cfg.omega)
+    sysop = emie.build_system(grid, sop)
+    nrhs = 2
+    plan = D.ShardPlan(grid.nx, grid.ny, grid.nz, sop.ex, sop.ey, G, octant=True)
+    shards_op = D.sharded_greens_build(grid, model, cfg.omega, plan, list(range(G)), D.loopback_block_sum)
+    assert all(emie.xy_symmetric(o) for o in shards_op)
+    shards = [D.cuda_shard(grid, None, plan, g, nrhs, op_shard=shards_op[g]) for g in range(G)]
+    rng = np.random.default_rng(19)
+    n = 3 * grid.nx * grid.ny * grid.nz
+    U = rng.uniform(-1, 1, (nrhs, n)) + 1j * rng.uniform(-1, 1, (nrhs, n))
+    want = emie.apply(sysop, torch.from_numpy(U.reshape(-1)).cuda()).cpu().numpy().reshape(nrhs, n)
+    outs = D.loopback_apply(shards, [torch.from_numpy(D.slab_of(U, plan, g, nrhs)).cuda() for g in range(G)])
+    got = D.join_slabs([o.cpu().numpy() for o in outs], plan, nrhs)
+    assert np.array_equal(got, want)
+
+
+def test_shard_octant_rejects_unsymmetric_or_ragged_shards(torch_cuda):
+    cfg, grid, sop, _ = _system(1)
+    L = emie.lib()
+    ragged = emie.restrict_modes(sop, 10, 20)  # not whole rows of quadrant modes
+    assert L.emie_cu_operator_shard_octant(ragged.handle, 1, None) != 0
+    rows = emie.restrict_modes(sop, 0, 3 * sop.qx)
+    assert L.emie_cu_operator_shard_octant(rows.handle, 1, None) == 0
+    emie.xy_symmetric(sop, disable=True)
+    rows2 = emie.restrict_modes(sop, 0, 3 * sop.qx)
+    assert L.emie_cu_operator_shard_octant(rows2.handle, 1, None) != 0
+
+
+@pytest.mark.parametrize("octant", [True, False])
+def test_forward_peer_split_owner_matches_table(torch_cuda, octant):
+    """the fused forward y pass with the owners computed from the plan's
+    splits (emie_cu_lateral_forward_peer_split, the sharded apply's path)
+    stores exactly what the per-mode owner table variant stores"""
+    import ctypes
+    torch = torch_cuda
+    cfg, grid, sop, _ = _system(3)
+    G, nrhs = 3, 2
+    plan = D.ShardPlan(cfg.nx, cfg.ny, cfg.nz, sop.ex, sop.ey, G, octant=octant)
+    sh = D.cuda_shard(grid, sop, plan, 1, nrhs)
+    be = sh.be
+    assert be.fused_peer_forward
+    rng = np.random.default_rng(5)
+    U = torch.from_numpy(D.slab_of(rng.uniform(-1, 1, (nrhs, 3 * cfg.cells())) + 0j, plan, 1, nrhs)).cuda()
+    own = np.empty(plan.E, np.int32)
+    for g, ms in enumerate(plan.modes):
+        own[ms] = g
+    owner = torch.from_numpy(own).cuda()
+    outs = []
+    for use_table in (True, False):
+        dsts = [torch.zeros((nrhs, plan.E, 3 * plan.nz), dtype=torch.complex128, device="cuda") for _ in range(G)]
+        dp = (ctypes.c_void_p * G)(*[d.data_ptr() for d in dsts])
+        if use_table:
+            rc = be.L.emie_cu_lateral_forward_peer(be.geom, ctypes.c_void_p(U.data_ptr()),
+                                                   ctypes.c_void_p(be.r2.data_ptr()),
+                                                   ctypes.c_void_p(owner.data_ptr()), dp, G, plan.nz,
+                                                   plan.z[1], nrhs, be._st())
+        else:
+            be.lateral_forward_peer(U, dsts, nrhs)
+            rc = 0
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append([d.cpu().numpy() for d in dsts])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    # each destination holds exactly its own modes' columns of this slab
+    for g in range(G):
+        nz0 = np.abs(outs[1][g]).sum(axis=(0, 2)) > 0
+        assert set(np.nonzero(nz0)[0]) <= set(plan.modes[g].tolist())

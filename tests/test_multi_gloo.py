@@ -95,14 +95,14 @@ def _sharded_case(nx=6, ny=5, nz=4, nrhs=2, seed=11):
     return dims, comp, diag, U, want
 
 
-def _sharded_worker(rank, world, port, q):
+def _sharded_worker(rank, world, port, q, octant=False):
     import torch
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1512_06126_b200 import distributed as D
-    nx, ny, nz, nrhs = 6, 5, 4, 2
+    nx, ny, nz, nrhs = (6, 6, 4, 2) if octant else (6, 5, 4, 2)
     dims, comp, diag, U, _ = _sharded_case(nx, ny, nz, nrhs)
-    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], world)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], world, octant=octant)
     z0, z1 = plan.z[rank], plan.z[rank + 1]
     dslab = [np.asarray(d).reshape(nz, ny, nx)[z0:z1].reshape(-1) for d in diag]
     be = NumpyBackend(plan, rank, comp, dims, dslab)
@@ -116,35 +116,63 @@ def _sharded_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_sharded_apply_gloo_matches_full_apply():
+@pytest.mark.parametrize("octant", [False, True])
+def test_sharded_apply_gloo_matches_full_apply(octant):
+    """two processes over gloo; octant: the row-sharded octant plan (each
+    rank owns the L-shaped set of quadrant modes of its octant rows)"""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, octant)) for r in range(2)]
     for p in procs:
         p.start()
     got = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    *_, want = _sharded_case()
+    *_, want = _sharded_case(6, 6 if octant else 5)
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("qy,G", [(7, 1), (7, 2), (7, 3), (129, 8), (257, 8), (5, 5)])
+def test_octant_row_splits_partition_the_modes(qy, G):
+    """every quadrant mode (and so every full mode) belongs to exactly one
+    rank's L-shaped set; ranks hold whole rows; the sets are balanced"""
+    from paper_1512_06126_b200 import distributed as D
+    ex = 2 * (qy - 1)
+    plan = D.ShardPlan(4, 4, 8, ex, ex, G, octant=True)
+    assert plan.q == [r * plan.qx for r in plan.rows] and plan.rows[0] == 0 and plan.rows[-1] == qy
+    assert all(plan.rows[g] < plan.rows[g + 1] for g in range(G))
+    allq = np.sort(np.concatenate([np.asarray(qm, dtype=np.int64) for qm in plan.qmodes]))
+    assert np.array_equal(allq, np.arange(plan.qx * plan.qy))
+    allm = np.sort(np.concatenate(plan.modes))
+    assert np.array_equal(allm, np.arange(plan.E))
+    for g in range(G):  # the L-shape: larger index in the rank's rows
+        for qm in plan.qmodes[g]:
+            a, b = divmod(qm, plan.qx)
+            assert plan.rows[g] <= max(a, b) < plan.rows[g + 1]
+    if qy >= 8 * G:
+        sizes = [len(qm) for qm in plan.qmodes]
+        assert max(sizes) <= 1.2 * min(sizes)
+    with pytest.raises(ValueError):
+        D.ShardPlan(4, 4, 8, ex, ex + 2, G, octant=True)
+
+
+@pytest.mark.parametrize("octant", [False, True])
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
-def test_sharded_apply_loopback_numpy(G):
+def test_sharded_apply_loopback_numpy(G, octant):
     """G virtual ranks in one process (the list-transpose all-to-all)."""
     import sys
     from pathlib import Path
     import torch
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
     from paper_1512_06126_b200 import distributed as D
-    nx, ny, nz, nrhs = 6, 5, 4, 2
+    nx, ny, nz, nrhs = (6, 6, 4, 2) if octant else (6, 5, 4, 2)
     dims, comp, diag, U, want = _sharded_case(nx, ny, nz, nrhs)
-    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G, octant=octant)
     # every full mode belongs to exactly one rank's list
     allm = np.sort(np.concatenate(plan.modes))
     assert np.array_equal(allm, np.arange(plan.E))
@@ -158,8 +186,9 @@ def test_sharded_apply_loopback_numpy(G):
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("octant", [False, True])
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
-def test_peer_exchange_loopback_numpy(G):
+def test_peer_exchange_loopback_numpy(G, octant):
     """The peer-store exchange plan (distributed.PeerExchange: each rank moves
     its columns straight into the owners' buffers, no pack / unpack) over G
     virtual ranks with host buffers and the NumPy stages, twice in a row
@@ -169,9 +198,9 @@ def test_peer_exchange_loopback_numpy(G):
     import torch
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
     from paper_1512_06126_b200 import distributed as D
-    nx, ny, nz, nrhs = 6, 5, 4, 2
+    nx, ny, nz, nrhs = (6, 6, 4, 2) if octant else (6, 5, 4, 2)
     dims, comp, diag, U, want = _sharded_case(nx, ny, nz, nrhs)
-    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G)
+    plan = D.ShardPlan(nx, ny, nz, dims[0], dims[1], G, octant=octant)
     shards = []
     for g in range(G):
         z0, z1 = plan.z[g], plan.z[g + 1]

@@ -7,3 +7,5 @@ python bench.py --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 --no-solve 
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv \
     python bench.py --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 --no-solve > gpurun_out/ncu_launch.log 2>&1
 tail -2 gpurun_out/smoke.log; tail -3 gpurun_out/gputests_full.log; tail -c 300 gpurun_out/bench_r02.json; tail -c 300 gpurun_out/bench_r02_reference.json
+python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline --no-solve > gpurun_out/bench_r02_cfg4.json 2> gpurun_out/bench_r02_cfg4.err
+tail -c 300 gpurun_out/bench_r02_cfg4.json
