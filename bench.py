@@ -472,8 +472,8 @@ def run_ours(args):
     octant = emie.xy_symmetric(sop)
     blocks_read = sop.qx * (sop.qx + 1) // 2 if octant else modes
     # stored entries per block: the reference's 2nz(2nz+1), or for nz 48/64 the
-    # eight dense nz x nz blocks the streamed contraction reads (operator.cuh)
-    nent_read = 8 * nz * nz if nz in (48, 64) else nent
+    # six dense nz x nz blocks the streamed contraction reads (operator.cuh)
+    nent_read = 6 * nz * nz if nz in (48, 64) else nent
     bytes_ct = blocks_read * nent_read * 16 + 2 * NRHS * E * 3 * nz * 16
     flops_ct = NRHS * 72.0 * nz * nz * E
     ct_ms = ms5[2] / max(1, cnt5[2])

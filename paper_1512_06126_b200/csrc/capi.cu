@@ -332,7 +332,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
     op.nentD = 4 * op.ntriP + 2 * op.nfull;
   } else if (op.rows) {
     op.ntriP = op.ntri;
-    op.nentD = 8 * op.nfull;  // eight dense blocks (operator.cuh)
+    op.nentD = kRowsBlocks * op.nfull;  // six dense blocks (operator.cuh)
   } else {
     op.ntriP = op.ntri;
     op.nentD = op.nent;  // compact wrapped-diagonal layout (operator.cuh)
@@ -387,7 +387,8 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
     EMIE_CUDA(cudaMemcpy(op.ctab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
   } else if (op.rows) {
     // symmetric entry (k, kp) -> both triangles of its dense block; xz / yz
-    // (k, kp) -> (k, kp) of the block and (kp, k) of its transpose
+    // (k, kp) -> (k, kp) of its block (the contraction reads -xz^T, -yz^T as
+    // transposed boxes of these)
     const int f = op.nfull;
     for (int c = 0; c < 4; ++c)
       for (int k = 0; k < nz; ++k)
@@ -397,7 +398,7 @@ void init_operator_geometry(Operator& op, int nx, int ny, int nz, double omega, 
     for (int c = 0; c < 2; ++c)
       for (int k = 0; k < nz; ++k)
         for (int kp = 0; kp < nz; ++kp)
-          op.emap_host[4 * op.ntri + c * f + k * nz + kp] = int2{(4 + c) * f + k * nz + kp, (6 + c) * f + kp * nz + k};
+          op.emap_host[4 * op.ntri + c * f + k * nz + kp] = int2{(4 + c) * f + k * nz + kp, -1};
   } else {
   // reference entry -> wrapped-diagonal slot (see operator.cuh)
   for (int c = 0; c < 4; ++c)

@@ -1142,7 +1142,9 @@ void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const ui
   }
   const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), d, sb, b, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            swizzle == 0    ? CU_TENSOR_MAP_SWIZZLE_NONE
+                            : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(EMIE_CU_RUNTIME_ERROR, "cuTensorMapEncodeTiled failed");
 }

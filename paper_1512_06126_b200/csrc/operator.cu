@@ -534,27 +534,31 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
 // ------------------------------ contraction, streamed row blocks (nz 48/64) -----
 // For nz in {48, 64} (config 4: nz = 64) a mode block no longer fits SMEM
 // (265 KB even in triangle form at nz = 64), so the operator is stored as
-// eight dense row-major nz x nz blocks per mode, [xx yy zz xy xz yz xz^T yz^T]
-// (the symmetric components hold both triangles; xz and yz are stored as is
-// and transposed), and the block streams through a ring of K-chunks like a
-// GEMM main loop. Chunk (b, kc) = columns kp in [8kc, 8kc+8) of third b of
-// M = [[xx xy xz] [xy yy yz] [-xz^T -yz^T zz]] for all 3nz rows: one
-// tensor-map box (8 columns x nz rows, 128-byte swizzle) per row third a,
-// since every column slice M_ab(:, kp-range) is a row slice of one stored
-// block (M_ab = M_ba^T for the symmetric parts). 3nz/16 consumer warps own two
+// six dense row-major nz x nz blocks per mode, [xx yy zz xy xz yz] (the
+// symmetric components hold both triangles), and the block streams through a
+// ring of K-chunks like a GEMM main loop. Chunk (b, kc) = columns kp in
+// [8kc, 8kc+8) of third b of M = [[xx xy xz] [xy yy yz] [-xz^T -yz^T zz]] for
+// all 3nz rows: one tensor-map box per row third a -- a column slice of the
+// stored block (8 columns x nz rows, 128-byte swizzle; M_ab = M_ba^T for the
+// symmetric parts), or for -xz^T, -yz^T a row slice of xz / yz (8 rows x nz
+// columns, unswizzled, read transposed by the consumers: 16-byte lanes along
+// a row, so a warp's load still spans four 128-byte runs). The transposed
+// copies xz^T, yz^T the layout once stored were 2 of 8 blocks of HBM traffic. 3nz/16 consumer warps own two
 // 8-row output tiles each; the products, the 3-multiply complex form, the
 // octant column groups and the output stores are those of contract_mma_kernel.
 constexpr int kRowsRing = 4;  // K-chunk stages
 template <int NZ>
 constexpr int rows_warps() { return 3 * NZ / 16; }
 __host__ __device__ constexpr int rows_block_id(int a, int b) {
-  // M_ab -> stored block: xx yy zz xy xz yz xzT yzT = 0..7
-  return a == b ? a : (a < 2 && b < 2) ? 3 : b == 2 ? 4 + a : 6 + b;
+  // M_ab -> stored block: xx yy zz xy xz yz = 0..5 (a = 2, b < 2: block 4 + b, transposed)
+  return a == b ? a : (a < 2 && b < 2) ? 3 : b == 2 ? 4 + a : 4 + b;
 }
+__host__ __device__ constexpr bool rows_transposed(int a, int b) { return a == 2 && b < 2; }
 
 template <int NZ, bool OCT, bool PEER = false>
 __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
-    contract_rows_kernel(const __grid_constant__ CUtensorMap tm, cplx* S, int ex, int ey, int qx, int q0, int q1,
+    contract_rows_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmT, cplx* S,
+                         int ex, int ey, int qx, int q0, int q1,
                          int qbase, int nrhs, const int* __restrict__ octl, int noct,
                          const __grid_constant__ PeerOut po) {
   constexpr int np = 3 * NZ, ldu = np + 4;
@@ -626,8 +630,12 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
           const int b = ch / NT, kc = ch - b * NT;
           mbar_expect_tx(rfull + st, 3 * kBox);
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
-            tma_load_4d(ring + (st * 3 + a) * kBox, &tm, 16 * kc, 0, rows_block_id(a, b), mode, rfull + st);
+          for (int a = 0; a < 3; ++a) {
+            if (rows_transposed(a, b))  // rows 8kc.. of xz / yz, all columns
+              tma_load_4d(ring + (st * 3 + a) * kBox, &tmT, 0, 8 * kc, rows_block_id(a, b), mode, rfull + st);
+            else
+              tma_load_4d(ring + (st * 3 + a) * kBox, &tm, 16 * kc, 0, rows_block_id(a, b), mode, rfull + st);
+          }
         }
       }
       __syncwarp();
@@ -679,8 +687,9 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int row = trow[i];
-            const cplx mv = *reinterpret_cast<const cplx*>(box + ta[i] * kBox + row * 128 + ((col ^ (row & 7)) << 4));
-            const bool neg = ta[i] == 2 && b < 2;  // -xz^T, -yz^T
+            const bool neg = rows_transposed(ta[i], b);  // -xz^T, -yz^T: a transposed row-slice box
+            const cplx mv = *reinterpret_cast<const cplx*>(
+                box + ta[i] * kBox + (neg ? col * (NZ * 16) + row * 16 : row * 128 + ((col ^ (row & 7)) << 4)));
             const double sg = neg ? -1.0 : 1.0;
             const double ar = sg * mv.re, ai = sg * mv.im;
             const double as = ar + ai;
@@ -833,6 +842,20 @@ void set_octant_lists(Operator& op, cudaStream_t st) {
   op.noctv = static_cast<int>(v.size());
 }
 
+// the ROWS layout's stored modes as {2nz doubles, nz rows, 6 blocks, modes}:
+// column-slice boxes (8 complex x nz rows, 128-byte swizzle) and row-slice
+// boxes (nz complex x 8 rows, unswizzled) for the transposed thirds
+static void rows_tensor_maps(const Operator& op, CUtensorMap* tm, CUtensorMap* tmT) {
+  const uint64_t dims[4] = {2ull * op.nz, static_cast<uint64_t>(op.nz), static_cast<uint64_t>(kRowsBlocks),
+                            static_cast<uint64_t>(op.qcount)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(op.nz) * 16, static_cast<uint64_t>(op.nz) * op.nz * 16,
+                               static_cast<uint64_t>(kRowsBlocks) * op.nz * op.nz * 16};
+  const uint32_t box[4] = {16, static_cast<uint32_t>(op.nz), 1, 1};
+  encode_tensor_map_f64(tm, op.spec, 4, dims, strides, box);
+  const uint32_t boxT[4] = {2u * static_cast<uint32_t>(op.nz), 8, 1, 1};
+  encode_tensor_map_f64(tmT, op.spec, 4, dims, strides, boxT, 0);
+}
+
 // octant contraction in use (EMIE_CU_NO_OCTANT=1 turns it off, for A/B runs)
 static bool use_octant(const Operator& op, int q0, int q1) {
   static const bool off = [] {
@@ -864,17 +887,13 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
       const size_t smem = 1024 + static_cast<size_t>(kRowsRing) * 3 * op.nz * 128 +
                           kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
       // the stored modes as {2nz doubles, nz rows, 8 blocks, modes}; box = 8 complex x nz rows
-      CUtensorMap tm;
-      const uint64_t dims[4] = {2ull * op.nz, static_cast<uint64_t>(op.nz), 8ull, static_cast<uint64_t>(op.qcount)};
-      const uint64_t strides[3] = {static_cast<uint64_t>(op.nz) * 16, static_cast<uint64_t>(op.nz) * op.nz * 16,
-                                   8ull * op.nz * op.nz * 16};
-      const uint32_t box[4] = {16, static_cast<uint32_t>(op.nz), 1, 1};
-      encode_tensor_map_f64(&tm, op.spec, 4, dims, strides, box);
+      CUtensorMap tm, tmT;
+      rows_tensor_maps(op, &tm, &tmT);
       const int nwork = oct ? op.noct : nmodes;
       auto launch = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
-        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
+        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, tmT, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
                                                    op.noct, PeerOut{});
       };
       if (op.nz == 48) {
@@ -963,17 +982,13 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
     if (op.rows) {
       const size_t smem = 1024 + static_cast<size_t>(kRowsRing) * 3 * op.nz * 128 +
                           kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
-      CUtensorMap tm;
-      const uint64_t dims[4] = {2ull * op.nz, static_cast<uint64_t>(op.nz), 8ull, static_cast<uint64_t>(op.qcount)};
-      const uint64_t strides[3] = {static_cast<uint64_t>(op.nz) * 16, static_cast<uint64_t>(op.nz) * op.nz * 16,
-                                   8ull * op.nz * op.nz * 16};
-      const uint32_t box[4] = {16, static_cast<uint32_t>(op.nz), 1, 1};
-      encode_tensor_map_f64(&tm, op.spec, 4, dims, strides, box);
+      CUtensorMap tm, tmT;
+      rows_tensor_maps(op, &tm, &tmT);
       auto launch_rows = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
-        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1, op.qbase,
-                                                   g, op.octl, op.noct, pg);
+        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, tmT, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1,
+                                                   op.qbase, g, op.octl, op.noct, pg);
       };
       if (op.nz == 48) {
         if (oct) launch_rows(contract_rows_kernel<48, true, true>, rows_warps<48>());

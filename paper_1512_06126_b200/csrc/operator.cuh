@@ -48,7 +48,8 @@ struct Operator {
   // quarter-warp of a fragment load touches 8 distinct banks.
   bool mma = false;
   // ROWS layout (nz in {48, 64}, streamed contraction, operator.cu): per mode
-  // eight dense row-major nz x nz blocks [xx yy zz xy xz yz xz^T yz^T]
+  // six dense row-major nz x nz blocks [xx yy zz xy xz yz] (the symmetric
+  // ones with both triangles; -xz^T / -yz^T are read as row slices of xz / yz)
   bool rows = false;
   int ntriP = 0;
   uint32_t* ctab = nullptr;  // [a][b][k][kp] -> slot of M_ab(k,kp), bit 31: negated
@@ -126,6 +127,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
 // slab owners' spectra (peer memory): plane a*nz + k goes to rank h with
 // z[h] <= k < z[h+1], at dst[h][(r*E + m)*3nzh + a*nzh + k - z[h]]
 constexpr int kMaxPeerRanks = 64;
+constexpr int kRowsBlocks = 6;  // dense blocks per mode of the ROWS layout
 struct PeerOut {
   int G = 0;
   cplx* dst[kMaxPeerRanks];

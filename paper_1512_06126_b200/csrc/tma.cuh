@@ -60,6 +60,6 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
 
 // host: tiled FLOAT64 tensor map with 128-byte (or 64-byte) swizzle (cuTensorMapEncodeTiled)
 void encode_tensor_map_f64(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
-                           const uint64_t* strides_bytes, const uint32_t* box, int swizzle = 128);
+                           const uint64_t* strides_bytes, const uint32_t* box, int swizzle = 128);  // 0, 64 or 128 bytes
 
 }  // namespace emie_cu
