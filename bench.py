@@ -449,17 +449,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         iters = max(r.iterations for r in reps)
-        # CGS2 traffic per iteration, 16 B x 3N per vector: three
-        # tiled sweeps over the j+1 basis vectors (dots; update + dots; update +
-        # norm: solver.cu) reading w each and writing it in the last two;
-        # j averages (restart-1)/2 over full cycles
+        # orthogonalisation traffic per iteration, 16 B x 3N per
+        # vector; j averages (restart-1)/2 over full cycles. DCGS2 (default,
+        # solver.cu): two tiled sweeps over the j+1 basis vectors (dots of w and
+        # of v_j's delayed reorthogonalisation; v_j corrected + w projected +
+        # norm) reading w in both, writing w and v_j in the second. CGS2
+        # (EMIE_CU_DCGS2=0): three sweeps, w read 3x and written 2x.
         jbar = (min(40, iters) - 1) / 2.0
-        cgs2_bytes = NRHS * (3 * (jbar + 1) + 5) * 16 * n
+        dcgs2 = os.environ.get("EMIE_CU_DCGS2", "1") != "0"
+        ortho_bytes = NRHS * ((2 * (jbar + 1) + 4) if dcgs2 else (3 * (jbar + 1) + 5)) * 16 * n
         solve = {"seconds": secs, "iterations": [r.iterations for r in reps],
                  "status": [r.status for r in reps], "residual": [r.residual for r in reps],
                  "tol": 1e-6, "restart": 40, "max_iters": 2000,
                  "ms_per_iteration": 1e3 * secs / max(1, iters),
-                 "cgs2_bytes_per_iteration": cgs2_bytes,
+                 "orthogonalisation": "DCGS2 (delayed reorthogonalisation: 2 sweeps per step)" if dcgs2
+                 else "CGS2 (3 sweeps per step)",
+                 "ortho_bytes_per_iteration": ortho_bytes,
                  "rhs": "x- and y-polarised plane-wave normal field (normal_field.py), both in lockstep"}
 
     # roofline of the dominant kernel (the per-mode contraction)

@@ -167,10 +167,19 @@ __device__ __forceinline__ void compute_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kCgsWarps * 32) : "memory");
 }
 
+// DCGS2 (delayed classical Gram-Schmidt with reorthogonalisation, one
+// projection sweep fewer per Arnoldi step than CGS2): the last basis vector
+// v_j = V[nv-1] arrives projected once; MODE 3 reads the basis and w once for
+// both dot sets, V[<nv-1]^H v_j (v_j's delayed second projection) and
+// V^H w (+ |w|^2, |v_j|^2); dcgs_coef_kernel turns them into v_j's
+// correction a, its norm alpha and w's coefficients against the corrected
+// basis; MODE 4 corrects v_j in place, v_j <- (v_j - V a) / alpha, and
+// projects w once, w <- w - V h, with |w|^2 (h: [h 2nv][a 2(nv-1)][1/alpha]).
 template <int MODE>
 __global__ void __launch_bounds__(kCgsThreads, 1)
     cgs_tile_kernel(cplx* w, const cplx* __restrict__ V, std::size_t vstride, int nv,
-                    const double* __restrict__ h, std::size_t n, double* partial, int pstride, int with_norm) {
+                    const double* __restrict__ h, std::size_t n, double* partial, int pstride, int with_norm,
+                    cplx* Vlast = nullptr) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 2;
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   cplx* stage0 = reinterpret_cast<cplx*>(sm + 128);
   cplx* xs = stage0 + 2 * stage_elems;
   double* hs = reinterpret_cast<double*>(xs + kTE);
-  double* red = hs + 2 * kTileMaxV;  // kCgsWarps
+  double* red = hs + 4 * kTileMaxV + 2;  // kCgsWarps
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -187,8 +196,10 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (MODE != 0)
+  if (MODE == 1 || MODE == 2)
     for (int i = tid; i < 2 * nv; i += blockDim.x) hs[i] = h[i];
+  if (MODE == 4)
+    for (int i = tid; i < 4 * nv - 1; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
   const std::size_t ntiles = (n + kTE - 1) / kTE;
 
@@ -211,9 +222,12 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
 
   // ---- compute warps
   double acc[kLPerWarp][2];
+  double accv[MODE == 3 ? kLPerWarp : 1][2];  // MODE 3: dots with v_j = V[nv-1]
 #pragma unroll
   for (int i = 0; i < kLPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
-  double nacc = 0.0;
+#pragma unroll
+  for (int i = 0; i < (MODE == 3 ? kLPerWarp : 1); ++i) accv[i][0] = accv[i][1] = 0.0;
+  double nacc = 0.0, vacc = 0.0;
   int j = 0;
   for (std::size_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++j) {
     const std::size_t t = (kCgsReverse && MODE == 1) ? ntiles - 1 - tt : tt;  // see the producer
@@ -224,7 +238,31 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const std::size_t e0 = t * kTE;
     const int cnt = static_cast<int>(min(static_cast<std::size_t>(kTE), n - e0));
     const cplx* x_src = wt;
-    if (MODE != 0) {
+    if (MODE == 4) {
+      // v_j <- (v_j - sum_l a_l V_l) / alpha; w <- w - sum_l h_l V_l - h_{nv-1} v_j (l < nv - 1)
+      if (tid < cnt) {
+        const int jv = nv - 1;
+        const double* ha = hs + 2 * nv;
+        cplx x = wt[tid], vf = Vt[jv * kTE + tid];
+        for (int l = 0; l < jv; ++l) {
+          const cplx v = Vt[l * kTE + tid];
+          const double hr = hs[2 * l], hi = hs[2 * l + 1], ar = ha[2 * l], ai = ha[2 * l + 1];
+          x.re = fma(-hr, v.re, fma(hi, v.im, x.re));
+          x.im = fma(-hr, v.im, fma(-hi, v.re, x.im));
+          vf.re = fma(-ar, v.re, fma(ai, v.im, vf.re));
+          vf.im = fma(-ar, v.im, fma(-ai, v.re, vf.im));
+        }
+        const double ia = ha[2 * jv];
+        vf.re *= ia;
+        vf.im *= ia;
+        const double hr = hs[2 * jv], hi = hs[2 * jv + 1];
+        x.re = fma(-hr, vf.re, fma(hi, vf.im, x.re));
+        x.im = fma(-hr, vf.im, fma(-hi, vf.re, x.im));
+        w[e0 + tid] = x;
+        Vlast[e0 + tid] = vf;
+        nacc = fma(x.re, x.re, fma(x.im, x.im, nacc));
+      }
+    } else if (MODE != 0 && MODE != 3) {
       // update: thread e < kTE owns element e (update_kernel's arithmetic)
       if (tid < cnt) {
         cplx x = wt[tid];
@@ -241,16 +279,28 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       if (MODE == 1) compute_bar();
       x_src = xs;
     }
-    if (MODE != 2) {
+    if (MODE == 0 || MODE == 1 || MODE == 3) {
       cplx wv[kTE / 32];
 #pragma unroll
       for (int k = 0; k < kTE / 32; ++k) {
         const int e = lane + 32 * k;
         wv[k] = e < cnt ? x_src[e] : cplx{0.0, 0.0};
       }
-      if (MODE == 0 && with_norm && warp == 0) {
+      if ((MODE == 3 || (MODE == 0 && with_norm)) && warp == 0) {
 #pragma unroll
         for (int k = 0; k < kTE / 32; ++k) nacc = fma(wv[k].re, wv[k].re, fma(wv[k].im, wv[k].im, nacc));
+      }
+      cplx vj[MODE == 3 ? kTE / 32 : 1];
+      if constexpr (MODE == 3) {
+#pragma unroll
+        for (int k = 0; k < kTE / 32; ++k) {
+          const int e = lane + 32 * k;
+          vj[k] = e < cnt ? Vt[(nv - 1) * kTE + e] : cplx{0.0, 0.0};
+        }
+        if (warp == 1) {
+#pragma unroll
+          for (int k = 0; k < kTE / 32; ++k) vacc = fma(vj[k].re, vj[k].re, fma(vj[k].im, vj[k].im, vacc));
+        }
       }
 #pragma unroll
       for (int i = 0; i < kLPerWarp; ++i) {
@@ -263,6 +313,12 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
               const cplx v = Vt[l * kTE + e];
               acc[i][0] = fma(v.re, wv[k].re, fma(v.im, wv[k].im, acc[i][0]));
               acc[i][1] = fma(v.re, wv[k].im, fma(-v.im, wv[k].re, acc[i][1]));
+              if constexpr (MODE == 3) {
+                if (l < nv - 1) {
+                  accv[i][0] = fma(v.re, vj[k].re, fma(v.im, vj[k].im, accv[i][0]));
+                  accv[i][1] = fma(v.re, vj[k].im, fma(-v.im, vj[k].re, accv[i][1]));
+                }
+              }
             }
           }
         }
@@ -274,8 +330,27 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
     if (MODE == 1) compute_bar();  // xs is rewritten by the next tile
   }
-  // ---- fixed-order reductions
-  if (MODE != 2) {
+  // ---- fixed-order reductions (MODE 3 layout: [2nv w-dots][|w|^2][2(nv-1) v_j-dots][|v_j|^2])
+  if (MODE == 3) {
+#pragma unroll
+    for (int i = 0; i < kLPerWarp; ++i) {
+      const int l = warp + kCgsWarps * i;
+      double r = accv[i][0], im = accv[i][1];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_down_sync(0xffffffffu, r, o);
+        im += __shfl_down_sync(0xffffffffu, im, o);
+      }
+      if (lane == 0 && l < nv - 1) {
+        partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * nv + 1 + 2 * l] = r;
+        partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * nv + 2 + 2 * l] = im;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vacc += __shfl_down_sync(0xffffffffu, vacc, o);
+    if (warp == 1 && lane == 0) partial[static_cast<std::size_t>(blockIdx.x) * pstride + 4 * nv - 1] = vacc;
+  }
+  if (MODE == 0 || MODE == 1 || MODE == 3) {
 #pragma unroll
     for (int i = 0; i < kLPerWarp; ++i) {
       const int l = warp + kCgsWarps * i;
@@ -291,7 +366,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       }
     }
   }
-  if (MODE == 2 || (MODE == 0 && with_norm)) {
+  if (MODE == 2 || MODE == 4 || MODE == 3 || (MODE == 0 && with_norm)) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
     if (lane == 0) red[warp] = nacc;
@@ -299,15 +374,48 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     if (tid == 0) {
       double sum = 0.0;
       for (int k = 0; k < kCgsWarps; ++k) sum += red[k];
-      if (MODE == 2) partial[blockIdx.x] = sum;
+      if (MODE == 2 || MODE == 4) partial[blockIdx.x] = sum;
       else partial[static_cast<std::size_t>(blockIdx.x) * pstride + 2 * nv] = sum;
     }
   }
 }
 
+// DCGS2 coefficients from the finalized MODE 3 sums s (one thread, fixed
+// order): a = V[<nv-1]^H v_j, alpha = sqrt(|v_j|^2 - |a|^2) (the corrected
+// v_j's norm, V orthonormal), h_l = V_l^H w (l < nv-1) and
+// h_{nv-1} = (v_j^H w - a^H h_{<nv-1}) / alpha (w against the corrected v_j).
+// coef = [h 2nv][a 2(nv-1)][1/alpha] for MODE 4; host slots: s0 = [h][|w|^2],
+// s1 = [a][alpha]
+__global__ void dcgs_coef_kernel(const double* __restrict__ s, int nv, double* coef, double* s0, double* s1) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int jv = nv - 1;
+  const double* a = s + 2 * nv + 1;
+  double an = 0.0, cr = 0.0, ci = 0.0;
+  for (int l = 0; l < jv; ++l) {
+    const double ar = a[2 * l], ai = a[2 * l + 1], br = s[2 * l], bi = s[2 * l + 1];
+    an = fma(ar, ar, fma(ai, ai, an));
+    cr = fma(ar, br, fma(ai, bi, cr));  // conj(a_l) b_l
+    ci = fma(ar, bi, fma(-ai, br, ci));
+  }
+  const double a2 = s[4 * nv - 1] - an;
+  const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+  const double ia = alpha > 0.0 ? 1.0 / alpha : 0.0;
+  for (int l = 0; l < jv; ++l) {
+    coef[2 * l] = s0[2 * l] = s[2 * l];
+    coef[2 * l + 1] = s0[2 * l + 1] = s[2 * l + 1];
+    coef[2 * nv + 2 * l] = s1[2 * l] = a[2 * l];
+    coef[2 * nv + 2 * l + 1] = s1[2 * l + 1] = a[2 * l + 1];
+  }
+  coef[2 * jv] = s0[2 * jv] = (s[2 * jv] - cr) * ia;
+  coef[2 * jv + 1] = s0[2 * jv + 1] = (s[2 * jv + 1] - ci) * ia;
+  coef[4 * nv - 2] = ia;
+  s0[2 * nv] = s[2 * nv];
+  s1[2 * jv] = alpha;
+}
+
 std::size_t cgs_smem(int nv) {
   return 128 + 2 * static_cast<std::size_t>(nv + 1) * kTE * sizeof(cplx) + kTE * sizeof(cplx) +
-         (2 * kTileMaxV + kCgsWarps) * sizeof(double);
+         (4 * kTileMaxV + 2 + kCgsWarps) * sizeof(double);
 }
 
 // y[e] = a * x[e] (real a)
@@ -374,13 +482,13 @@ void make_rotation(cd f, cd g, double& c, cd& s) {
 // tiled sweep launch: grid = kCgsBlocks (or fewer tiles), one CTA per SM
 template <int MODE>
 int cgs_launch(cplx* w, const cplx* V, std::size_t vstride, int nv, const double* h, std::size_t n,
-               double* partial, int pstride, int with_norm, cudaStream_t st) {
+               double* partial, int pstride, int with_norm, cudaStream_t st, cplx* Vlast = nullptr) {
   const std::size_t smem = cgs_smem(kTileMaxV);
   (void)resident_ctas(reinterpret_cast<const void*>(cgs_tile_kernel<MODE>), kCgsThreads, smem);
   const int G = static_cast<int>(std::max<std::size_t>(
       1, std::min<std::size_t>(kCgsBlocks, (n + kTE - 1) / kTE)));
   cgs_tile_kernel<MODE><<<G, kCgsThreads, cgs_smem(nv), st>>>(w, V, vstride, nv, h, n, partial, pstride,
-                                                              with_norm);
+                                                              with_norm, Vlast);
   check_launch("cgs_tile_kernel");
   return G;
 }
@@ -396,7 +504,7 @@ struct Workspace {
 
   Workspace(cudaStream_t s, std::size_t n_, int maxv) : st(s), n(n_) {
     G = red_blocks(n);
-    pstride = 2 * maxv + 2;
+    pstride = 4 * maxv + 4;  // DCGS2 dots: 4 nv values per block
     // rows for the reduction kernels' blocks and the tiled sweeps' (cgs_launch)
     partial = scratch<double>(static_cast<std::size_t>(std::max(G, kCgsBlocks)) * pstride, st);
     dvals = scratch<double>(pstride, st);
@@ -449,6 +557,10 @@ struct Rhs {
   bool broke = false;
   std::vector<cd> h, g, rot_s;
   std::vector<double> rot_c, history;
+  // DCGS2: unrotated Hessenberg columns, g before each rotation, the norms
+  // rho_j of the once-projected w_j, v_j's correction a_j and alpha_j
+  std::vector<cd> hraw, gpre, acoef;
+  std::vector<double> rho, alpha;
   emie_cu_report rep{1, 0, 0.0, 0};
   // finalized reductions of the current step (device) and their pinned host
   // mirror: [0] pass-1 dots + |w|^2, [1] pass-2 dots, [2] the new norm
@@ -487,6 +599,15 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
 
   std::vector<Rhs> rs(nrhs);
   const int ps = ws.pstride;
+  // orthogonalisation: DCGS2 (two sweeps per step) unless EMIE_CU_DCGS2=0 or
+  // the restart exceeds the tiled sweeps' basis cap (CGS2, three sweeps)
+  static const bool dcgs2_env = [] {
+    const char* e = std::getenv("EMIE_CU_DCGS2");
+    return !(e && e[0] == '0');
+  }();
+  const bool dcgs2 = dcgs2_env && m + 1 <= kTileMaxV;
+  double* dsum = scratch<double>(4 * static_cast<std::size_t>(m + 1) + 4, st);
+  double* dcoef = scratch<double>(4 * static_cast<std::size_t>(m + 1) + 4, st);
   // finalized reductions per rhs, two rounds deep (parity): [par][3][ps]
   double* dv_all = scratch<double>(static_cast<std::size_t>(nrhs) * 6 * ps, st);
   struct Pinned {  // freed on every exit path
@@ -534,6 +655,13 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
     R.rot_c.assign(m, 0.0);
     R.rot_s.assign(m, cd(0.0));
     R.g.assign(m + 1, cd(0.0));
+    if (dcgs2) {
+      R.hraw.assign(static_cast<std::size_t>(m + 1) * m, cd(0.0));
+      R.gpre.assign(m + 1, cd(0.0));
+      R.acoef.assign(static_cast<std::size_t>(m + 1) * (m + 1), cd(0.0));
+      R.rho.assign(m + 1, 0.0);
+      R.alpha.assign(m + 1, 1.0);
+    }
     R.g[0] = R.rnorm;
     R.cols = 0;
     R.j = 0;
@@ -556,6 +684,17 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
         for (int l = k + 1; l < R.cols; ++l)
           acc -= R.h[static_cast<std::size_t>(l) * (m + 1) + k] * y[l];
         y[k] = acc / R.h[static_cast<std::size_t>(k) * (m + 1) + k];
+      }
+      if (dcgs2 && !R.Z) {
+        // the applies saw v_j before its delayed correction: v_j(applied) =
+        // alpha_j v_j + sum_{i<j} a_{j,i} v_i in the corrected basis V
+        std::vector<cd> yc(R.cols);
+        for (int i = 0; i < R.cols; ++i) {
+          cd acc = R.alpha[i] * y[i];
+          for (int jj = i + 1; jj < R.cols; ++jj) acc += R.acoef[static_cast<std::size_t>(jj) * (m + 1) + i] * y[jj];
+          yc[i] = acc;
+        }
+        y.swap(yc);
       }
       EMIE_CUDA(cudaMemcpyAsync(ycoef, y.data(), R.cols * sizeof(cd), cudaMemcpyHostToDevice, st));
       combine_kernel<<<GB, T, 0, st>>>(R.x, R.Z ? R.Z : R.V, n, R.cols, ycoef, n);
@@ -606,6 +745,24 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
         continue;
       }
       const int j = es[q].j;
+      if (dcgs2) {
+        // one dots sweep (v_j's delayed reorthogonalisation and w's
+        // projection), the coefficients, one update sweep (v_j corrected in
+        // place, w projected) with the new |w|^2
+        const int nv = j + 1;
+        int g = cgs_launch<3>(w, R.V, n, nv, nullptr, n, ws.partial, ps, 0, st);
+        finalize_kernel<<<4 * nv, kFinThreads, 0, st>>>(ws.partial, g, ps, 4 * nv, dsum);
+        check_launch("finalize_kernel");
+        dcgs_coef_kernel<<<1, 32, 0, st>>>(dsum, nv, dcoef, dv, dv + ps);
+        check_launch("dcgs_coef_kernel");
+        to_host(0, 2 * nv + 1);
+        to_host(1, 2 * nv - 1);
+        g = cgs_launch<4>(w, R.V, n, nv, dcoef, n, ws.partial, 1, 0, st, R.V + static_cast<std::size_t>(j) * n);
+        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, g, 1, 1, dv + 2 * ps);
+        check_launch("finalize_kernel");
+        to_host(2, 1);
+        continue;
+      }
       // CGS2 pass 1: dots against v_0..v_j plus |w|^2, then w -= V h
       if (j + 1 <= kTileMaxV) {
         int g = cgs_launch<0>(w, R.V, n, j + 1, nullptr, n, ws.partial, ps, 1, st);
@@ -669,9 +826,41 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
     const int j = R.j;
     cd* hj = R.h.data() + static_cast<std::size_t>(j) * (m + 1);
     const double wn0 = std::sqrt(hp[2 * (j + 1)]);
-    for (int i = 0; i <= j; ++i) hj[i] += cd(hp[2 * i], hp[2 * i + 1]);
-    for (int i = 0; i <= j; ++i) hj[i] += cd(hp[ps + 2 * i], hp[ps + 2 * i + 1]);
     const double hnext = std::sqrt(hp[2 * ps]);
+    if (dcgs2) {
+      // v_j was applied before its second projection: v_j(applied) =
+      // alpha v_j + V a, so column j - 1 gains rho_{j-1} a and its subdiagonal
+      // becomes rho_{j-1} alpha; it is re-rotated from its raw entries
+      const double alpha = hp[ps + 2 * j];
+      R.alpha[j] = alpha;
+      for (int i = 0; i < j; ++i)
+        R.acoef[static_cast<std::size_t>(j) * (m + 1) + i] = cd(hp[ps + 2 * i], hp[ps + 2 * i + 1]);
+      if (j >= 1) {
+        cd* hr = R.hraw.data() + static_cast<std::size_t>(j - 1) * (m + 1);
+        for (int i = 0; i < j; ++i) hr[i] += R.rho[j - 1] * R.acoef[static_cast<std::size_t>(j) * (m + 1) + i];
+        hr[j] = R.rho[j - 1] * alpha;
+        cd* hc = R.h.data() + static_cast<std::size_t>(j - 1) * (m + 1);
+        for (int i = 0; i <= j; ++i) hc[i] = hr[i];
+        for (int i = 0; i < j - 1; ++i) {
+          const cd t = R.rot_c[i] * hc[i] + R.rot_s[i] * hc[i + 1];
+          hc[i + 1] = -std::conj(R.rot_s[i]) * hc[i] + R.rot_c[i] * hc[i + 1];
+          hc[i] = t;
+        }
+        make_rotation(hc[j - 1], hc[j], R.rot_c[j - 1], R.rot_s[j - 1]);
+        const cd t = R.rot_c[j - 1] * hc[j - 1] + R.rot_s[j - 1] * hc[j];
+        hc[j] = 0.0;
+        hc[j - 1] = t;
+        R.g[j] = -std::conj(R.rot_s[j - 1]) * R.gpre[j - 1];
+        R.g[j - 1] = R.rot_c[j - 1] * R.gpre[j - 1];
+      }
+      cd* hr = R.hraw.data() + static_cast<std::size_t>(j) * (m + 1);
+      for (int i = 0; i <= j; ++i) hj[i] = hr[i] = cd(hp[2 * i], hp[2 * i + 1]);
+      hr[j + 1] = hnext;
+      R.rho[j] = hnext;
+    } else {
+      for (int i = 0; i <= j; ++i) hj[i] += cd(hp[2 * i], hp[2 * i + 1]);
+      for (int i = 0; i <= j; ++i) hj[i] += cd(hp[ps + 2 * i], hp[ps + 2 * i + 1]);
+    }
     for (int i = 0; i < j; ++i) {
       const cd t = R.rot_c[i] * hj[i] + R.rot_s[i] * hj[i + 1];
       hj[i + 1] = -std::conj(R.rot_s[i]) * hj[i] + R.rot_c[i] * hj[i + 1];
@@ -700,6 +889,7 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
       const cd t = R.rot_c[j] * hj[j] + R.rot_s[j] * hj[j + 1];
       hj[j + 1] = 0.0;
       hj[j] = t;
+      if (dcgs2) R.gpre[j] = R.g[j];
       R.g[j + 1] = -std::conj(R.rot_s[j]) * R.g[j];
       R.g[j] = R.rot_c[j] * R.g[j];
       R.cols = j + 1;
@@ -787,6 +977,8 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
   release(Wall, st);
   release(Bin, st);
   release(ycoef, st);
+  release(dsum, st);
+  release(dcoef, st);
   release(dv_all, st);
   if (Zall) release(Zall, st);
   EMIE_CUDA(cudaStreamSynchronize(st));

@@ -135,3 +135,56 @@ def test_fgmres_over_python_map_hook_and_preconditioner(torch_cuda):
     _, reps2 = emie.fgmres_system(sysop, g["rhs"], emie.SolverConfig(tol=1e-6, on_iteration=lambda k, i, r: seen2.append((k, i, r))))
     for k in range(2):
         assert [r for kk, _, r in seen2 if kk == k] == reps2[k].history
+
+
+def _solve_in_subprocess(dcgs2, restart, max_iters, tol, precond=False):
+    """the library reads EMIE_CU_DCGS2 once per process"""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {str(root)!r}); sys.path.insert(0, {str(root / 'tests')!r})
+import paper_1512_06126_b200 as emie
+from test_gpu_solve import _odd_system
+sop, sysop, b = _odd_system(7, 4, 8, 0.2, 31)
+cfg = emie.SolverConfig(tol={tol}, restart={restart}, max_iters={max_iters})
+if {precond}:  # flexible right preconditioning over host callbacks, one rhs per solve
+    cfg.right_precond = lambda v: 0.5 * v
+    out = [emie.fgmres(lambda u: emie.apply_host(sysop, u), b[i], cfg) for i in range(2)]
+    x, reps = np.stack([o[0] for o in out]), [o[1] for o in out]
+else:
+    x, reps = emie.fgmres_system(sysop, b, cfg)
+res = [np.linalg.norm(emie.apply(sysop, x[i]) - b[i]) / np.linalg.norm(b[i]) for i in range(2)]
+np.savez(sys.argv[1], x=x, it=[r.iterations for r in reps], est=[r.residual for r in reps], res=res,
+         h=np.array(reps[0].history))
+"""
+    with tempfile.NamedTemporaryFile(suffix=".npz", delete=False) as f:
+        out = f.name
+    env = dict(os.environ, EMIE_CU_DCGS2="1" if dcgs2 else "0")
+    subprocess.run([sys.executable, "-c", code, out], env=env, check=True)
+    return dict(np.load(out))
+
+
+@pytest.mark.parametrize("restart,max_iters,tol,precond",
+                         [(40, 400, 1e-10, False), (7, 300, 1e-9, False), (12, 200, 1e-9, True), (40, 23, 1e-14, False)])
+def test_dcgs2_matches_cgs2(torch_cuda, restart, max_iters, tol, precond):
+    """DCGS2 (one dots sweep and one update sweep per step; v_j's second
+    projection delayed into the next step, the Hessenberg column corrected
+    and re-rotated on the host, the solution's coefficients mapped back to
+    the corrected basis) against CGS2: the same Krylov iterates in exact
+    arithmetic, so equal iteration counts (+-1), solutions to the solve's
+    tolerance, and a residual estimate that tracks the true residual -- also
+    when the solve stops inside a cycle (max_iters 23) and with a flexible
+    right preconditioner (the Z basis)"""
+    a = _solve_in_subprocess(True, restart, max_iters, tol, precond)
+    b = _solve_in_subprocess(False, restart, max_iters, tol, precond)
+    for i in range(2):
+        assert abs(int(a["it"][i]) - int(b["it"][i])) <= 1
+        assert np.linalg.norm(a["x"][i] - b["x"][i]) <= 1e3 * tol * np.linalg.norm(b["x"][i])
+        assert abs(a["res"][i] - a["est"][i]) <= 1e-9 + 1e-3 * a["res"][i]
+        if max_iters > 100:
+            assert a["res"][i] <= 2 * tol
