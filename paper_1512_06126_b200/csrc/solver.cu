@@ -380,37 +380,44 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   }
 }
 
-// DCGS2 coefficients from the finalized MODE 3 sums s (one thread, fixed
-// order): a = V[<nv-1]^H v_j, alpha = sqrt(|v_j|^2 - |a|^2) (the corrected
-// v_j's norm, V orthonormal), h_l = V_l^H w (l < nv-1) and
+// DCGS2 coefficients from the finalized MODE 3 sums s (one warp, fixed-order
+// butterfly sums): a = V[<nv-1]^H v_j, alpha = sqrt(|v_j|^2 - |a|^2) (the
+// corrected v_j's norm, V orthonormal), h_l = V_l^H w (l < nv-1) and
 // h_{nv-1} = (v_j^H w - a^H h_{<nv-1}) / alpha (w against the corrected v_j).
 // coef = [h 2nv][a 2(nv-1)][1/alpha] for MODE 4; host slots: s0 = [h][|w|^2],
 // s1 = [a][alpha]
-__global__ void dcgs_coef_kernel(const double* __restrict__ s, int nv, double* coef, double* s0, double* s1) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(32) dcgs_coef_kernel(const double* __restrict__ s, int nv, double* coef,
+                                                       double* s0, double* s1) {
+  const int lane = threadIdx.x;
   const int jv = nv - 1;
   const double* a = s + 2 * nv + 1;
   double an = 0.0, cr = 0.0, ci = 0.0;
-  for (int l = 0; l < jv; ++l) {
+  for (int l = lane; l < jv; l += 32) {
     const double ar = a[2 * l], ai = a[2 * l + 1], br = s[2 * l], bi = s[2 * l + 1];
     an = fma(ar, ar, fma(ai, ai, an));
     cr = fma(ar, br, fma(ai, bi, cr));  // conj(a_l) b_l
     ci = fma(ar, bi, fma(-ai, br, ci));
+    coef[2 * l] = s0[2 * l] = br;
+    coef[2 * l + 1] = s0[2 * l + 1] = bi;
+    coef[2 * nv + 2 * l] = s1[2 * l] = ar;
+    coef[2 * nv + 2 * l + 1] = s1[2 * l + 1] = ai;
   }
-  const double a2 = s[4 * nv - 1] - an;
-  const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
-  const double ia = alpha > 0.0 ? 1.0 / alpha : 0.0;
-  for (int l = 0; l < jv; ++l) {
-    coef[2 * l] = s0[2 * l] = s[2 * l];
-    coef[2 * l + 1] = s0[2 * l + 1] = s[2 * l + 1];
-    coef[2 * nv + 2 * l] = s1[2 * l] = a[2 * l];
-    coef[2 * nv + 2 * l + 1] = s1[2 * l + 1] = a[2 * l + 1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    an += __shfl_xor_sync(0xffffffffu, an, o);
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+    ci += __shfl_xor_sync(0xffffffffu, ci, o);
   }
-  coef[2 * jv] = s0[2 * jv] = (s[2 * jv] - cr) * ia;
-  coef[2 * jv + 1] = s0[2 * jv + 1] = (s[2 * jv + 1] - ci) * ia;
-  coef[4 * nv - 2] = ia;
-  s0[2 * nv] = s[2 * nv];
-  s1[2 * jv] = alpha;
+  if (lane == 0) {
+    const double a2 = s[4 * nv - 1] - an;
+    const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+    const double ia = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    coef[2 * jv] = s0[2 * jv] = (s[2 * jv] - cr) * ia;
+    coef[2 * jv + 1] = s0[2 * jv + 1] = (s[2 * jv + 1] - ci) * ia;
+    coef[4 * nv - 2] = ia;
+    s0[2 * nv] = s[2 * nv];
+    s1[2 * jv] = alpha;
+  }
 }
 
 std::size_t cgs_smem(int nv) {
