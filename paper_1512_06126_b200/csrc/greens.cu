@@ -2084,7 +2084,11 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     const size_t fper = static_cast<size_t>(P.nw) * kImgFields * nz;  // complex per offset
     const size_t estride = (static_cast<size_t>(P.nw) * 2 * nz + 3) & ~size_t{3};
     const size_t per_off = fper * sizeof(cplx) + estride * sizeof(int);
-    const int maxb = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, kImgBudget / per_off)));
+    // batch: at most kImgBudget of images, and at most a quarter of the free memory
+    size_t free_b = 0, total_b = 0;
+    size_t budget = kImgBudget;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, free_b / 4);
+    const int maxb = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
     const int nbatch = ceil_div(ncomp, maxb), batch = ceil_div(ncomp, nbatch);
     cplx* IF = scratch<cplx>(static_cast<size_t>(batch) * fper, st);
     int* IE = scratch<int>(static_cast<size_t>(batch) * estride, st);
