@@ -466,6 +466,16 @@ def run_ours(args):
                  else "CGS2 (3 sweeps per step)",
                  "ortho_bytes_per_iteration": ortho_bytes,
                  "rhs": "x- and y-polarised plane-wave normal field (normal_field.py), both in lockstep"}
+        # effective bandwidth of everything but the apply: the orthogonalisation
+        # bytes over the iteration time left after the device apply step
+        ortho_ms = solve["ms_per_iteration"] - ms_max / args.steps
+        hbm_pk, hbm_src = peaks()
+        if ortho_ms > 0:
+            gbs = ortho_bytes / (ortho_ms * 1e-3) / 1e9
+            solve["ortho_effective"] = {"gb_s": round(gbs, 1), "hbm_peak_gb_s": hbm_pk, "peak_source": hbm_src,
+                                        "frac": round(gbs / hbm_pk, 3),
+                                        "how": "ortho bytes / (solve ms per iteration - device apply ms per "
+                                               "2-rhs step): the sweeps plus the small per-step kernels and gaps"}
 
     # roofline of the dominant kernel (the per-mode contraction)
     nz = cfg.nz
