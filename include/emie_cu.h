@@ -414,6 +414,18 @@ int emie_cu_vec_dots(const double* d_V, long long vstride, int nv, const double*
 int emie_cu_vec_update(double* d_w, const double* d_V, long long vstride, int nv, const double* d_h,
                        long long n, double* d_dots_out, double* d_norm_out, void* stream);
 
+/* DCGS2 step on the slab (the single-GPU solver's sweeps): dots sweep,
+ * d_out (4nv doubles) = [conj(V_l) . w, l < nv][|w|^2][conj(V_l) . V_{nv-1},
+ * l < nv-1][|V_{nv-1}|^2]; 1 <= nv <= 41 */
+int emie_cu_vec_dcgs_dots(const double* d_V, long long vstride, int nv, const double* d_w, long long n,
+                          double* d_out, void* stream);
+/* DCGS2 update sweep from the caller's global coefficients d_coef =
+ * [h (nv complex)][a (nv-1 complex)][1/alpha]: V_{nv-1} <- (V_{nv-1} -
+ * sum a_l V_l) / alpha in place, w <- w - sum_{l<nv-1} h_l V_l - h_{nv-1}
+ * V_{nv-1}(new); d_norm_out[0] = |w_new|^2 (local) */
+int emie_cu_vec_dcgs_update(double* d_w, double* d_V, long long vstride, int nv, const double* d_coef, long long n,
+                            double* d_norm_out, void* stream);
+
 /* x += sum_l y_l V_l in l order (cie.cpp:213-214), d_y: nv complex */
 int emie_cu_vec_combine(double* d_x, const double* d_V, long long vstride, int nv, const double* d_y,
                         long long n, void* stream);

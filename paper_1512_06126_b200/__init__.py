@@ -112,6 +112,8 @@ def lib():
                                                 ctypes.POINTER(vp), vp],
         "emie_cu_vec_dots": [vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, ctypes.c_int, vp, vp],
         "emie_cu_vec_update": [vp, vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp, vp, vp],
+        "emie_cu_vec_dcgs_dots": [vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp, vp],
+        "emie_cu_vec_dcgs_update": [vp, vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp, vp],
         "emie_cu_vec_combine": [vp, vp, ctypes.c_longlong, ctypes.c_int, vp, ctypes.c_longlong, vp],
         "emie_cu_vec_scale": [vp, vp, ctypes.c_double, ctypes.c_longlong, vp],
         "emie_cu_vec_residual": [vp, vp, vp, ctypes.c_longlong, vp, vp],

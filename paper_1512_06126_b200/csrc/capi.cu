@@ -1096,6 +1096,25 @@ extern "C" int emie_cu_vec_update(double* d_w, const double* d_V, long long vstr
   });
 }
 
+extern "C" int emie_cu_vec_dcgs_dots(const double* d_V, long long vstride, int nv, const double* d_w, long long n,
+                                     double* d_out, void* stream) {
+  return guarded([&] {
+    if (!d_V || !d_w || !d_out || n < 1 || vstride < 0) fail(EMIE_CU_INVALID_ARGUMENT, "vec_dcgs_dots: bad arguments");
+    vec_dcgs_dots(reinterpret_cast<const cplx*>(d_V), static_cast<std::size_t>(vstride), nv,
+                  reinterpret_cast<const cplx*>(d_w), static_cast<std::size_t>(n), d_out, as_stream(stream));
+  });
+}
+
+extern "C" int emie_cu_vec_dcgs_update(double* d_w, double* d_V, long long vstride, int nv, const double* d_coef,
+                                       long long n, double* d_norm_out, void* stream) {
+  return guarded([&] {
+    if (!d_w || !d_V || !d_coef || !d_norm_out || n < 1 || vstride < 0)
+      fail(EMIE_CU_INVALID_ARGUMENT, "vec_dcgs_update: bad arguments");
+    vec_dcgs_update(reinterpret_cast<cplx*>(d_w), reinterpret_cast<cplx*>(d_V), static_cast<std::size_t>(vstride), nv,
+                    d_coef, static_cast<std::size_t>(n), d_norm_out, as_stream(stream));
+  });
+}
+
 extern "C" int emie_cu_vec_combine(double* d_x, const double* d_V, long long vstride, int nv, const double* d_y,
                                    long long n, void* stream) {
   return guarded([&] {

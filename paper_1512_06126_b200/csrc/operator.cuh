@@ -217,6 +217,10 @@ void vec_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::si
               double* out, cudaStream_t st);
 void vec_update(cplx* w, const cplx* V, std::size_t vstride, int nv, const double* h, std::size_t n,
                 double* dots_out, double* norm_out, cudaStream_t st);
+void vec_dcgs_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::size_t n, double* out,
+                   cudaStream_t st);
+void vec_dcgs_update(cplx* w, cplx* V, std::size_t vstride, int nv, const double* coef, std::size_t n,
+                     double* norm_out, cudaStream_t st);
 void vec_combine(cplx* x, const cplx* V, std::size_t vstride, int nv, const double* y, std::size_t n,
                  cudaStream_t st);
 void vec_scale(cplx* y, const cplx* x, double a, std::size_t n, cudaStream_t st);

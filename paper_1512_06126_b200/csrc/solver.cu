@@ -177,7 +177,7 @@ __device__ __forceinline__ void compute_bar() {
 // projects w once, w <- w - V h, with |w|^2 (h: [h 2nv][a 2(nv-1)][1/alpha]).
 template <int MODE>
 __global__ void __launch_bounds__(kCgsThreads, 1)
-    cgs_tile_kernel(cplx* w, const cplx* __restrict__ V, std::size_t vstride, int nv,
+    cgs_tile_kernel(cplx* w, const cplx* V, std::size_t vstride, int nv,  // V: TMA source only (MODE 4 writes V[nv-1])
                     const double* __restrict__ h, std::size_t n, double* partial, int pstride, int with_norm,
                     cplx* Vlast = nullptr) {
   extern __shared__ __align__(128) unsigned char sm[];
@@ -1011,6 +1011,27 @@ void vec_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::si
     finalize_kernel<<<nvals, kFinThreads, 0, st>>>(partial, g, ps, nvals, out);
     check_launch("finalize_kernel");
   }
+  release(partial, st);
+}
+
+void vec_dcgs_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::size_t n, double* out,
+                   cudaStream_t st) {
+  if (nv < 1 || nv > kTileMaxV) fail(EMIE_CU_INVALID_ARGUMENT, "vec_dcgs_dots: nv outside [1, 41]");
+  const int ps = 4 * nv + 4;
+  double* partial = scratch<double>(static_cast<std::size_t>(kCgsBlocks) * ps, st);
+  const int g = cgs_launch<3>(const_cast<cplx*>(w), V, vstride, nv, nullptr, n, partial, ps, 0, st);
+  finalize_kernel<<<4 * nv, kFinThreads, 0, st>>>(partial, g, ps, 4 * nv, out);
+  check_launch("finalize_kernel");
+  release(partial, st);
+}
+
+void vec_dcgs_update(cplx* w, cplx* V, std::size_t vstride, int nv, const double* coef, std::size_t n,
+                     double* norm_out, cudaStream_t st) {
+  if (nv < 1 || nv > kTileMaxV) fail(EMIE_CU_INVALID_ARGUMENT, "vec_dcgs_update: nv outside [1, 41]");
+  double* partial = scratch<double>(kCgsBlocks, st);
+  const int g = cgs_launch<4>(w, V, vstride, nv, coef, n, partial, 1, 0, st, V + (nv - 1) * vstride);
+  finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+  check_launch("finalize_kernel");
   release(partial, st);
 }
 

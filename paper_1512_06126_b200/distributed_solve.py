@@ -4,10 +4,12 @@ The reference's restarted FGMRES (src/cie.cpp:117-238) with the operator
 apply sharded as in distributed.py: every rank holds the depth slab of every
 Krylov vector, runs the vector kernels on it and all-reduces the local sums
 (2(j+1)+1 doubles per CGS2 pass, one norm per step), so all ranks carry the
-same Hessenberg matrix, rotations and decisions. The orthogonalisation is the
-CGS2 of the single-GPU solver (solver.cu: dots; update fused with the second
-pass's dots; update with the new norm), the host arithmetic is
-fgmres_device's, step for step.
+same Hessenberg matrix, rotations and decisions. The orthogonalisation is
+the single-GPU solver's (solver.cu): DCGS2 by default -- one dots sweep
+giving both V^H w and v_j's delayed reorthogonalisation dots, one update
+sweep correcting v_j in place and projecting w, so two all-reduces per step
+(4nv + 1 doubles) -- or CGS2 (three sweeps, three all-reduces); the host
+arithmetic is fgmres_device's, step for step.
 
 Plumbing only: the vector kernels are the library's (emie_cu_vec_*, the tiled
 CGS2 sweeps) on this rank's slab; the reductions are torch.distributed
@@ -61,6 +63,19 @@ class CudaSlabOps:
         q = self._p(out) if want == "norm" else None
         self._check(self.L.emie_cu_vec_update(self._p(w), self._p(V), ctypes.c_longlong(V.shape[1]), nv,
                                               self._p(h), ctypes.c_longlong(w.numel()), d, q, self._st()))
+        return out
+
+    def dcgs_dots(self, V, nv, w):
+        out = self.reals(4 * nv)
+        self._check(self.L.emie_cu_vec_dcgs_dots(self._p(V), ctypes.c_longlong(V.shape[1]), nv, self._p(w),
+                                                 ctypes.c_longlong(w.numel()), self._p(out), self._st()))
+        return out
+
+    def dcgs_update(self, w, V, nv, coef):
+        out = self.reals(1)
+        self._check(self.L.emie_cu_vec_dcgs_update(self._p(w), self._p(V), ctypes.c_longlong(V.shape[1]), nv,
+                                                   self._p(coef), ctypes.c_longlong(w.numel()), self._p(out),
+                                                   self._st()))
         return out
 
     def combine(self, x, V, nv, y):
@@ -118,6 +133,32 @@ class NumpySlabOps:
             out = np.array([np.vdot(wn, wn).real])
         return self.torch.from_numpy(out)
 
+    def dcgs_dots(self, V, nv, w):
+        Vn, wn = V.numpy()[:nv], w.numpy().reshape(-1)
+        out = np.zeros(4 * nv)
+        d = np.conj(Vn) @ wn
+        out[0:2 * nv:2], out[1:2 * nv:2] = d.real, d.imag
+        out[2 * nv] = np.vdot(wn, wn).real
+        a = np.conj(Vn[:nv - 1]) @ Vn[nv - 1]
+        out[2 * nv + 1:4 * nv - 1:2], out[2 * nv + 2:4 * nv - 1:2] = a.real, a.imag
+        out[4 * nv - 1] = np.vdot(Vn[nv - 1], Vn[nv - 1]).real
+        return self.torch.from_numpy(out)
+
+    def dcgs_update(self, w, V, nv, coef):
+        c = coef.numpy()
+        h = c[0:2 * nv:2] + 1j * c[1:2 * nv:2]
+        a = c[2 * nv:4 * nv - 2:2] + 1j * c[2 * nv + 1:4 * nv - 2:2]
+        Vn, wn = V.numpy(), w.numpy().reshape(-1)
+        vj = Vn[nv - 1].copy()
+        for l in range(nv - 1):
+            vj -= a[l] * Vn[l]
+        vj *= c[4 * nv - 2]
+        Vn[nv - 1] = vj
+        for l in range(nv - 1):
+            wn -= h[l] * Vn[l]
+        wn -= h[nv - 1] * vj
+        return self.torch.from_numpy(np.array([np.vdot(wn, wn).real]))
+
     def combine(self, x, V, nv, y):
         yn = y.numpy()
         xn = x.numpy().reshape(-1)
@@ -174,14 +215,36 @@ def _rotation(f: complex, g: complex):
     return abs(f) / t, f / abs(f) * np.conj(g) / t
 
 
+def dcgs_coefficients(d: np.ndarray, nv: int):
+    """DCGS2 step coefficients from the global dcgs_dots sums d (4nv values,
+    the layout of solver.cu's MODE 3 / dcgs_coef_kernel): v_j's correction a
+    (nv-1 complex), alpha = sqrt(|v_j|^2 - |a|^2), w's coefficients h against
+    the corrected basis -> (coef [h][a][1/alpha] as float64, h, a, alpha)."""
+    b = d[0:2 * nv:2] + 1j * d[1:2 * nv:2]
+    a = d[2 * nv + 1:4 * nv - 1:2] + 1j * d[2 * nv + 2:4 * nv - 1:2]
+    a2 = d[4 * nv - 1] - float(np.sum(a.real ** 2 + a.imag ** 2))
+    alpha = math.sqrt(a2) if a2 > 0.0 else 0.0
+    ia = 1.0 / alpha if alpha > 0.0 else 0.0
+    h = b.copy()
+    h[nv - 1] = (b[nv - 1] - np.sum(np.conj(a) * b[:nv - 1])) * ia
+    coef = np.zeros(4 * nv - 1)
+    coef[0:2 * nv:2], coef[1:2 * nv:2] = h.real, h.imag
+    coef[2 * nv:4 * nv - 2:2], coef[2 * nv + 1:4 * nv - 2:2] = a.real, a.imag
+    coef[4 * nv - 2] = ia
+    return coef, h, a, alpha
+
+
 def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callable, rhs: Sequence,
-                   tol: float = 1e-8, restart: int = 40, max_iters: int = 500):
+                   tol: float = 1e-8, restart: int = 40, max_iters: int = 500, ortho: str = "dcgs2"):
     """FGMRES (cie.cpp:117-238) for nrhs right-hand sides in lockstep.
 
     apply(list of per-rank U (nrhs, n_local)) -> list of per-rank A U;
     ops: per-rank slab vector backends (CudaSlabOps / NumpySlabOps);
     reduce(list of per-rank local sums) -> the global sums (host numpy);
-    rhs: per-rank (nrhs, n_local) slabs. Returns (per-rank x slabs, reports)."""
+    rhs: per-rank (nrhs, n_local) slabs. Returns (per-rank x slabs, reports).
+    ortho: "dcgs2" (the single-GPU solver's default: one dots sweep and one
+    update sweep per step, two all-reduces) or "cgs2" (three sweeps, three
+    all-reduces); restarts above 40 use CGS2."""
     from . import SolveReport
     if not (tol > 0.0) or restart < 1 or max_iters < 1:
         from . import InvalidArgument
@@ -189,6 +252,7 @@ def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callabl
     G = len(ops)
     nrhs, n = rhs[0].shape[0], [b.shape[1] for b in rhs]
     m = restart
+    dcgs = ortho == "dcgs2" and m + 1 <= 41
     V = [[ops[g].zeros((m + 1, n[g])) for g in range(G)] for _ in range(nrhs)]
     x = [ops[g].zeros((nrhs, n[g])) for g in range(G)]
     r = [ops[g].zeros((nrhs, n[g])) for g in range(G)]
@@ -216,7 +280,9 @@ def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callabl
         for g in range(G):
             ops[g].scale(V[i][g][0], r[g][i], 1.0 / s["rnorm"])
         s.update(h=np.zeros((m, m + 1), np.complex128), c=np.zeros(m), sn=np.zeros(m, np.complex128),
-                 gv=np.zeros(m + 1, np.complex128), cols=0, j=0, phase="inner")
+                 gv=np.zeros(m + 1, np.complex128), cols=0, j=0, phase="inner",
+                 hraw=np.zeros((m, m + 1), np.complex128), gpre=np.zeros(m + 1, np.complex128),
+                 acoef=np.zeros((m + 1, m + 1), np.complex128), rho=np.zeros(m + 1), alpha=np.ones(m + 1))
         s["gv"][0] = s["rnorm"]
         return True
 
@@ -234,6 +300,9 @@ def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callabl
                 for l in range(k + 1, cols):
                     acc -= s["h"][l, k] * y[l]
                 y[k] = acc / s["h"][k, k]
+            if dcgs:  # the applies saw v_j before its correction: v_j(applied) = alpha_j v_j + V a_j
+                y = np.array([s["alpha"][k] * y[k] + np.sum(s["acoef"][k + 1:cols, k] * y[k + 1:cols])
+                              for k in range(cols)])
             yv = np.zeros(2 * cols)
             yv[0::2], yv[1::2] = y.real, y.imag
             for g in range(G):
@@ -265,15 +334,46 @@ def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callabl
                 continue
             j = s["j"]
             nv = j + 1
-            d1, h1 = red(lambda g: ops[g].dots(V[i][g], nv, w[g], True))
-            d2, h2 = red(lambda g: ops[g].update(w[g], V[i][g], nv, h1[g], "dots"))
-            nn, _ = red(lambda g: ops[g].update(w[g], V[i][g], nv, h2[g], "norm"))
-            s["iter"] += 1
             hj = s["h"][j]
-            wn0 = math.sqrt(d1[2 * nv])
-            hj[:nv] += d1[0:2 * nv:2] + 1j * d1[1:2 * nv:2]
-            hj[:nv] += d2[0::2] + 1j * d2[1::2]
-            hnext = math.sqrt(nn[0])
+            if dcgs:
+                d, _ = red(lambda g: ops[g].dcgs_dots(V[i][g], nv, w[g]))
+                coef, hc, acol, alpha = dcgs_coefficients(d, nv)
+                nn, _ = red(lambda g: ops[g].dcgs_update(w[g], V[i][g], nv, ops[g].upload(coef)))
+                s["iter"] += 1
+                wn0 = math.sqrt(d[2 * nv])
+                hnext = math.sqrt(nn[0])
+                s["alpha"][j] = alpha
+                s["acoef"][j, :j] = acol
+                if j >= 1:  # column j-1 gains rho_{j-1} a, subdiagonal rho_{j-1} alpha; re-rotated
+                    hr = s["hraw"][j - 1]
+                    hr[:j] += s["rho"][j - 1] * acol
+                    hr[j] = s["rho"][j - 1] * alpha
+                    hc1 = s["h"][j - 1]
+                    hc1[:j + 1] = hr[:j + 1]
+                    for k in range(j - 1):
+                        t = s["c"][k] * hc1[k] + s["sn"][k] * hc1[k + 1]
+                        hc1[k + 1] = -np.conj(s["sn"][k]) * hc1[k] + s["c"][k] * hc1[k + 1]
+                        hc1[k] = t
+                    c1, sn1 = _rotation(hc1[j - 1], hc1[j])
+                    s["c"][j - 1], s["sn"][j - 1] = c1, sn1
+                    t = c1 * hc1[j - 1] + sn1 * hc1[j]
+                    hc1[j] = 0.0
+                    hc1[j - 1] = t
+                    s["gv"][j] = -np.conj(sn1) * s["gpre"][j - 1]
+                    s["gv"][j - 1] = c1 * s["gpre"][j - 1]
+                s["hraw"][j, :nv] = hc
+                s["hraw"][j, nv] = hnext
+                s["rho"][j] = hnext
+                hj[:nv] = hc
+            else:
+                d1, h1 = red(lambda g: ops[g].dots(V[i][g], nv, w[g], True))
+                d2, h2 = red(lambda g: ops[g].update(w[g], V[i][g], nv, h1[g], "dots"))
+                nn, _ = red(lambda g: ops[g].update(w[g], V[i][g], nv, h2[g], "norm"))
+                s["iter"] += 1
+                wn0 = math.sqrt(d1[2 * nv])
+                hj[:nv] += d1[0:2 * nv:2] + 1j * d1[1:2 * nv:2]
+                hj[:nv] += d2[0::2] + 1j * d2[1::2]
+                hnext = math.sqrt(nn[0])
             for k in range(j):
                 t = s["c"][k] * hj[k] + s["sn"][k] * hj[k + 1]
                 hj[k + 1] = -np.conj(s["sn"][k]) * hj[k] + s["c"][k] * hj[k + 1]
@@ -297,6 +397,7 @@ def fgmres_sharded(apply: Callable[[List], List], ops: Sequence, reduce: Callabl
                 t = c * hj[j] + sn * hj[j + 1]
                 hj[j + 1] = 0.0
                 hj[j] = t
+                s["gpre"][j] = s["gv"][j]
                 s["gv"][j + 1] = -np.conj(sn) * s["gv"][j]
                 s["gv"][j] = c * s["gv"][j]
                 s["cols"] = nv

@@ -232,7 +232,7 @@ def _solve_case(nx=6, ny=5, nz=4, nrhs=2, seed=21):
     return dims, comp, diag, B, want
 
 
-def _numpy_sharded_solve(G, ranks, dims, comp, diag, B, reduce, dist_apply=None):
+def _numpy_sharded_solve(G, ranks, dims, comp, diag, B, reduce, dist_apply=None, ortho="dcgs2"):
     import torch
     from paper_1512_06126_b200 import distributed as D
     from paper_1512_06126_b200 import distributed_solve as DS
@@ -254,7 +254,7 @@ def _numpy_sharded_solve(G, ranks, dims, comp, diag, B, reduce, dist_apply=None)
 
         def apply(U):
             return [sysd.apply(U[0].reshape(-1)).reshape(nrhs, -1)]
-    x, reps = DS.fgmres_sharded(apply, ops, reduce, rhs, tol=1e-10, restart=8, max_iters=200)
+    x, reps = DS.fgmres_sharded(apply, ops, reduce, rhs, tol=1e-10, restart=8, max_iters=200, ortho=ortho)
     return plan, x, reps
 
 
@@ -266,14 +266,18 @@ def _check_solve(x_full, reps, want):
 
 
 @pytest.mark.parametrize("G", [1, 2, 3])
-def test_sharded_solve_loopback_numpy(G):
+@pytest.mark.parametrize("ortho", ["dcgs2", "cgs2"])
+def test_sharded_solve_loopback_numpy(G, ortho):
+    """both orthogonalisations (DCGS2: v_j's second projection delayed one
+    step, Hessenberg column re-rotated, solution coefficients mapped back)
+    against the oracle's FGMRES (MGS2, cie.cpp:117-238)"""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
     from paper_1512_06126_b200 import distributed as D
     from paper_1512_06126_b200 import distributed_solve as DS
     dims, comp, diag, B, want = _solve_case()
-    plan, x, reps = _numpy_sharded_solve(G, list(range(G)), dims, comp, diag, B, DS.LoopbackReducer())
+    plan, x, reps = _numpy_sharded_solve(G, list(range(G)), dims, comp, diag, B, DS.LoopbackReducer(), ortho=ortho)
     _check_solve(D.join_slabs([t.numpy() for t in x], plan, B.shape[0]), reps, want)
 
 
