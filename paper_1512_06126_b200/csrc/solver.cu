@@ -434,12 +434,17 @@ __global__ void scale_kernel(cplx* y, const cplx* __restrict__ x, double a, std:
 
 // y[e] = x[e] / sqrt(*nrm2): the next basis vector normalised on the device
 // (same IEEE sqrt and division as the host path, so bit-identical to it)
-__global__ void scale_by_norm_kernel(cplx* y, const cplx* __restrict__ x, const double* nrm2, std::size_t n) {
+// y2 (optional): a second copy, the next round's apply batch slot
+__global__ void scale_by_norm_kernel(cplx* y, const cplx* __restrict__ x, const double* nrm2, std::size_t n,
+                                     cplx* y2 = nullptr) {
   const double s = *nrm2;
   const double a = s > 0.0 ? 1.0 / std::sqrt(s) : 0.0;
   for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<std::size_t>(gridDim.x) * blockDim.x)
-    y[e] = a * ldg(x + e);
+       e += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const cplx v = a * ldg(x + e);
+    y[e] = v;
+    if (y2) y2[e] = v;
+  }
 }
 
 // x[e] += sum_k y[k] V_k[e] in k order (cie.cpp:213-214)
@@ -720,7 +725,8 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
     Rhs* R;
     bool inner;
     int j;
-    int slot;  // position in its round's batch (Bin / Wall slot)
+    int slot;             // position in its round's batch (Bin / Wall slot)
+    bool staged = false;  // v_j already written into its Bin slot (speculative normalisation)
   };
   auto enqueue_round = [&](const std::vector<Entry>& es, int par) {
     for (std::size_t q = 0; q < es.size(); ++q) {
@@ -731,7 +737,8 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
         A.precond(src, z, st);
         src = z;
       }
-      EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      if (!es[q].staged)
+        EMIE_CUDA(cudaMemcpyAsync(Bin + q * n, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     }
     A.apply(Bin, Wall, static_cast<int>(es.size()), st);
     for (std::size_t q = 0; q < es.size(); ++q) {
@@ -942,11 +949,15 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
       for (std::size_t q = 0; q < pending.size(); ++q) {
         const Entry& e = pending[q];
         const Rhs& R = *e.R;
+        // the normalised v_{j+1} also lands in its slot of the next round's
+        // apply batch (no preconditioner: the batch holds v itself)
+        const bool stage = !R.Z;
         scale_by_norm_kernel<<<GB, T, 0, st>>>(R.V + static_cast<std::size_t>(e.j + 1) * n,
                                                Wall + static_cast<std::size_t>(e.slot) * n,
-                                               R.dv + par * 3 * ps + 2 * ps, n);
+                                               R.dv + par * 3 * ps + 2 * ps, n,
+                                               stage ? Bin + q * n : nullptr);
         check_launch("scale_by_norm_kernel");
-        next.push_back({e.R, true, e.j + 1, static_cast<int>(q)});
+        next.push_back({e.R, true, e.j + 1, static_cast<int>(q), stage});
       }
       enqueue_round(next, par ^ 1);
     }
