@@ -863,15 +863,18 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   // IMG: two buffers {F [LC][kImgFields][nz], E [LC][2][nz] (16-byte padded)}, then lam
   const size_t ibufF = static_cast<size_t>(LC) * kImgFields * nz;
   const size_t ibufE = (static_cast<size_t>(LC) * 2 * nz + 3) / 4 * 2;  // in cplx units
-  cplx* ibuf[2] = {sm, sm + ibufF + ibufE};
+  // buffer b at sm + b * (ibufF + ibufE): pointer arithmetic on sm keeps the
+  // pair loop's loads in the shared window (LDS; a pointer picked from an
+  // array loses that and compiles to generic LD + 64-bit address math)
+  auto ibuf = [&](int b) { return sm + static_cast<size_t>(b) * (ibufF + ibufE); };
   auto img_issue = [&](int c) {  // one thread: chunk c's image into buffer c & 1
     const int s0 = c * LC, n = min(LC, P.nw - s0);
     const uint32_t fb = static_cast<uint32_t>(n) * kImgFields * nz * sizeof(cplx);
     const uint32_t eb = (static_cast<uint32_t>(n) * 2 * nz * sizeof(int) + 15u) & ~15u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&ibar[c & 1], fb + eb);
-    bulk_g2s(ibuf[c & 1], IF + (static_cast<size_t>(blockIdx.x) * P.nw + s0) * kImgFields * nz, fb, &ibar[c & 1]);
-    bulk_g2s(ibuf[c & 1] + ibufF, IE + blockIdx.x * estride + static_cast<size_t>(s0) * 2 * nz, eb, &ibar[c & 1]);
+    bulk_g2s(ibuf(c & 1), IF + (static_cast<size_t>(blockIdx.x) * P.nw + s0) * kImgFields * nz, fb, &ibar[c & 1]);
+    bulk_g2s(ibuf(c & 1) + ibufF, IE + blockIdx.x * estride + static_cast<size_t>(s0) * 2 * nz, eb, &ibar[c & 1]);
   };
   if constexpr (IMG) {
     C.lam = reinterpret_cast<double*>(sm + 2 * (ibufF + ibufE));
@@ -958,8 +961,8 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     }
     if constexpr (IMG) {
       const int c = t0 / LC;
-      C.F = ibuf[c & 1];
-      C.E = reinterpret_cast<int*>(ibuf[c & 1] + ibufF);
+      C.F = ibuf(c & 1);
+      C.E = reinterpret_cast<int*>(ibuf(c & 1) + ibufF);
       mbar_wait(&ibar[c & 1], static_cast<uint32_t>((c >> 1) & 1));
     } else {
       chunk_layer_states(P, C, R, t0, lc, threadIdx.x, blockDim.x, true);
@@ -2084,10 +2087,13 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     const size_t fper = static_cast<size_t>(P.nw) * kImgFields * nz;  // complex per offset
     const size_t estride = (static_cast<size_t>(P.nw) * 2 * nz + 3) & ~size_t{3};
     const size_t per_off = fper * sizeof(cplx) + estride * sizeof(int);
-    // batch: at most kImgBudget of images, and at most a quarter of the free memory
-    size_t free_b = 0, total_b = 0;
-    size_t budget = kImgBudget;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, free_b / 4);
+    // batch: at most kImgBudget of images, and at most a quarter of the memory
+    // free at the first split build (queried once: cudaMemGetInfo stalls the
+    // host behind the device's queued work)
+    static const size_t budget = [] {
+      size_t free_b = 0, total_b = 0;
+      return cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? std::min(kImgBudget, free_b / 4) : kImgBudget;
+    }();
     const int maxb = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
     const int nbatch = ceil_div(ncomp, maxb), batch = ceil_div(ncomp, nbatch);
     cplx* IF = scratch<cplx>(static_cast<size_t>(batch) * fper, st);
