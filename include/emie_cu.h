@@ -45,6 +45,10 @@ typedef struct emie_cu_system_s* emie_cu_system;     /* device SystemOperator */
 const char* emie_cu_last_error(void);
 const char* emie_cu_version(void);
 int emie_cu_device_count(int* count);
+/* grow the library's stream-ordered memory pool by `bytes` once (allocated
+ * and freed; the pool keeps it reserved), so the first large build or solve
+ * does not pay the device's first-touch allocation cost */
+int emie_cu_pool_reserve(unsigned long long bytes);
 
 /* smooth_embedding_size (include/emie/toeplitz.hpp:13, src/toeplitz.cpp:18-26) */
 int emie_cu_smooth_embedding_size(int n, int* out);

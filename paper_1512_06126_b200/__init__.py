@@ -130,6 +130,7 @@ def lib():
         "emie_cu_fgmres": [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                            ctypes.POINTER(_Report), vp, ctypes.c_int, vp],
         "emie_cu_device_count": [ip],
+        "emie_cu_pool_reserve": [ctypes.c_ulonglong],
         "emie_cu_receiver_fields": [ctypes.c_int, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, vp, vp, ctypes.c_int, vp, ctypes.c_int, vp, vp],
@@ -484,11 +485,14 @@ def operator_from_greens_blocks(grid: AnomalyGrid, omega: float, d_blocks, q0: i
     return SpectralOperator(h)
 
 
-def warmup() -> None:
+def warmup(reserve_bytes: int = 0) -> None:
     """Library initialisation: one tiny Green's build (16 x 16 x 2) and system
     apply, so the device code of the build and the first allocations of the
     stream-ordered pool are in place before a timed build (CUDA loads kernels
-    lazily, on first launch)."""
+    lazily, on first launch); reserve_bytes > 0 also grows the library's
+    memory pool by that much (emie_cu_pool_reserve)."""
+    if reserve_bytes > 0:
+        _check(lib().emie_cu_pool_reserve(ctypes.c_ulonglong(int(reserve_bytes))))
     model = LayeredModel([0.0, 1000.0], [0.0, 0.01, 0.1])
     grid = make_grid(model, [1100.0, 1200.0, 1300.0], 16, 16, 100.0, 100.0)
     op = assemble_operator(grid, model, 2.0 * np.pi)

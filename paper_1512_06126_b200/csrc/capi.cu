@@ -518,6 +518,17 @@ extern "C" {
 const char* emie_cu_last_error(void) { return g_err.c_str(); }
 const char* emie_cu_version(void) { return "emie-b200 0.1 (sm_100a)"; }
 
+int emie_cu_pool_reserve(unsigned long long bytes) {
+  return guarded([&] {
+    keep_pool_warm();
+    if (bytes == 0) return;
+    void* p = nullptr;
+    EMIE_CUDA(cudaMallocAsync(&p, static_cast<std::size_t>(bytes), nullptr));
+    EMIE_CUDA(cudaFreeAsync(p, nullptr));
+    EMIE_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
 int emie_cu_device_count(int* count) {
   return guarded([&] { EMIE_CUDA(cudaGetDeviceCount(count)); });
 }

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "layered.cuh"
@@ -784,7 +785,21 @@ constexpr int kImgThreads = EMIE_GREEN_IMG_THREADS;
 #define EMIE_GREEN_IMG_LAMBDAS 4
 #endif
 constexpr int kImgLambdas = EMIE_GREEN_IMG_LAMBDAS;  // lambdas per chunk_image_kernel CTA
-constexpr size_t kImgBudget = size_t{4} << 30;       // bytes of chunk images per batch
+constexpr size_t kImgBudget = size_t{2} << 30;       // bytes of chunk images per batch (cfg3: 1 / 2 / 4 GB -> 31.6 / 30.1 / 29.7 ms)
+// chunk images shared by offsets at equal R (EMIE_CU_GREENS_RSHARE=0: one per offset, A/B)
+inline bool img_share_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EMIE_CU_GREENS_RSHARE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// R of each offset code, as every kernel of the build computes it
+__global__ void r_of_codes_kernel(const GreenParams P, const int* __restrict__ offs, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = pair_geometry(P.oc.oi(offs[i]), P.oc.oj(offs[i]), P.hx, P.hy).r;
+}
 
 // Per-lambda phases 0-1c of the accumulation (layer states, interval factors,
 // prefix products, left factors: everything of a chunk but the pair sums) for
@@ -847,7 +862,7 @@ template <bool FULL = false, bool IMG = false>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
     cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, int pos0, const cplx* __restrict__ IF,
-    const int* __restrict__ IE, size_t estride) {
+    const int* __restrict__ IE, size_t estride, const int* __restrict__ img_of = nullptr, int img_base = 0) {
   extern __shared__ cplx sm[];
   __shared__ uint64_t ibar[2];
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
@@ -867,14 +882,17 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   // pair loop's loads in the shared window (LDS; a pointer picked from an
   // array loses that and compiles to generic LD + 64-bit address math)
   auto ibuf = [&](int b) { return sm + static_cast<size_t>(b) * (ibufF + ibufE); };
+  // the offset's chunk image: its own, or the one of its R group (offsets at
+  // the same distance R share every per-lambda phase)
+  const int img = img_of ? img_of[blockIdx.x] - img_base : static_cast<int>(blockIdx.x);
   auto img_issue = [&](int c) {  // one thread: chunk c's image into buffer c & 1
     const int s0 = c * LC, n = min(LC, P.nw - s0);
     const uint32_t fb = static_cast<uint32_t>(n) * kImgFields * nz * sizeof(cplx);
     const uint32_t eb = (static_cast<uint32_t>(n) * 2 * nz * sizeof(int) + 15u) & ~15u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&ibar[c & 1], fb + eb);
-    bulk_g2s(ibuf(c & 1), IF + (static_cast<size_t>(blockIdx.x) * P.nw + s0) * kImgFields * nz, fb, &ibar[c & 1]);
-    bulk_g2s(ibuf(c & 1) + ibufF, IE + blockIdx.x * estride + static_cast<size_t>(s0) * 2 * nz, eb, &ibar[c & 1]);
+    bulk_g2s(ibuf(c & 1), IF + (static_cast<size_t>(img) * P.nw + s0) * kImgFields * nz, fb, &ibar[c & 1]);
+    bulk_g2s(ibuf(c & 1) + ibufF, IE + img * estride + static_cast<size_t>(s0) * 2 * nz, eb, &ibar[c & 1]);
   };
   if constexpr (IMG) {
     C.lam = reinterpret_cast<double*>(sm + 2 * (ibufF + ibufE));
@@ -2059,16 +2077,19 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     EMIE_CUDA(cudaMemcpyToSymbolAsync(g_phase_clk, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
   }
 #endif
-  // Split (chunk_image_kernel + the pair kernel on streamed images) when an
-  // offset's pairs span several group CTAs, each of which would recompute the
-  // per-lambda phases (nz > 32: config 4 620 -> 455 ms); with one group the
-  // fused kernel is faster (config 3 33 vs 39 ms: the phases are issue-bound,
-  // more CTAs per SM do not speed them up, and the images cost HBM traffic).
+  // Split (chunk_image_kernel + the pair kernel on streamed images) or the
+  // fused kernel: the split saves the per-lambda phases of every pair-group
+  // CTA after the first (nz > 32) and of every offset sharing another's R.
   static const int img_mode = [] {
     const char* e = std::getenv("EMIE_CU_GREENS_IMG");  // 0: fused, 1: split, unset: by group count
     return e && *e ? std::atoi(e) : -1;
   }();
-  if (!full && (img_mode < 0 ? groups > 1 : img_mode == 1)) {
+  // default: split when an offset spans several pair groups (nz > 32), or
+  // for large builds, where the images shared by offsets at equal R outweigh
+  // the images' HBM round trip (config 3: 29.6 vs 33.2 ms fused; config 2's
+  // 2,080 offsets: 5.3 vs 5.1 ms, and the split's host-side grouping costs more)
+  const bool split_default = groups > 1 || (!P.oc.compact && img_share_enabled() && ncomp >= 4096);
+  if (!full && (img_mode < 0 ? split_default : img_mode == 1)) {
     const int LA = kImgLambdas;
     const size_t smemA = static_cast<size_t>(LA) * (14 * NL + kFields * nz) * sizeof(cplx) +
                          static_cast<size_t>(LA) * 2 * nz * sizeof(int);
@@ -2091,24 +2112,69 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     // free at the first split build (queried once: cudaMemGetInfo stalls the
     // host behind the device's queued work)
     static const size_t budget = [] {
+      size_t cap = kImgBudget;
+      if (const char* e = std::getenv("EMIE_CU_GREENS_IMG_MB"))  // A/B of the batch size
+        if (*e) cap = static_cast<size_t>(std::max(16, std::atoi(e))) << 20;
       size_t free_b = 0, total_b = 0;
-      return cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? std::min(kImgBudget, free_b / 4) : kImgBudget;
+      return cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? std::min(cap, free_b / 4) : cap;
     }();
-    const int maxb = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
-    const int nbatch = ceil_div(ncomp, maxb), batch = ceil_div(ncomp, nbatch);
-    cplx* IF = scratch<cplx>(static_cast<size_t>(batch) * fper, st);
-    int* IE = scratch<int>(static_cast<size_t>(batch) * estride, st);
-    for (int b0 = 0; b0 < ncomp; b0 += batch) {
-      const int nb = std::min(batch, ncomp - b0);
-      chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), nb), kImgThreads, smemA, st>>>(P, div, offs + b0, LA, IF, IE,
-                                                                                     estride);
+    // Offsets at the same distance R (bit for bit, as the kernels compute it)
+    // share one chunk image: the per-lambda phases depend on the offset only
+    // through lambda = lambda_m / R (5,384 distinct R among config 3's 8,256
+    // computed offsets). Slots come from the codes (full builds), so the
+    // offsets are reordered by R; signed-offset requests (slot = request
+    // position) keep one image per offset.
+    std::vector<int> img_h(ncomp), reps;
+    if (!P.oc.compact && img_share_enabled()) {
+      double* dR = scratch<double>(ncomp, st);
+      r_of_codes_kernel<<<ceil_div(ncomp, 256), 256, 0, st>>>(P, offs, ncomp, dR);
+      check_launch("r_of_codes_kernel");
+      std::vector<double> Rh(ncomp);
+      EMIE_CUDA(cudaMemcpyAsync(Rh.data(), dR, ncomp * sizeof(double), cudaMemcpyDeviceToHost, st));
+      EMIE_CUDA(cudaStreamSynchronize(st));
+      release(dR, st);
+      std::vector<uint64_t> key(ncomp);
+      std::memcpy(key.data(), Rh.data(), ncomp * sizeof(double));
+      std::vector<int> idx(ncomp);
+      for (int i = 0; i < ncomp; ++i) idx[i] = i;
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] < key[b]; });
+      std::vector<int> sorted(ncomp);
+      for (int b = 0; b < ncomp; ++b) {
+        sorted[b] = offs_h[idx[b]];
+        if (b == 0 || key[idx[b]] != key[idx[b - 1]]) reps.push_back(sorted[b]);
+        img_h[b] = static_cast<int>(reps.size()) - 1;
+      }
+      EMIE_CUDA(cudaMemcpyAsync(offs, sorted.data(), ncomp * sizeof(int), cudaMemcpyHostToDevice, st));
+    } else {
+      reps = offs_h;
+      for (int b = 0; b < ncomp; ++b) img_h[b] = b;
+    }
+    const int nu = static_cast<int>(reps.size());
+    int* dreps = scratch<int>(nu, st);
+    int* dimg = scratch<int>(ncomp, st);
+    EMIE_CUDA(cudaMemcpyAsync(dreps, reps.data(), nu * sizeof(int), cudaMemcpyHostToDevice, st));
+    EMIE_CUDA(cudaMemcpyAsync(dimg, img_h.data(), ncomp * sizeof(int), cudaMemcpyHostToDevice, st));
+    const int maxu = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
+    const int nbatch = ceil_div(nu, maxu), ubatch = ceil_div(nu, nbatch);
+    cplx* IF = scratch<cplx>(static_cast<size_t>(ubatch) * fper, st);
+    int* IE = scratch<int>(static_cast<size_t>(ubatch) * estride, st);
+    int b0 = 0;
+    for (int u0 = 0; u0 < nu; u0 += ubatch) {
+      const int u1 = std::min(nu, u0 + ubatch);
+      int b1 = b0;
+      while (b1 < ncomp && img_h[b1] < u1) ++b1;  // the offsets of images [u0, u1)
+      chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), u1 - u0), kImgThreads, smemA, st>>>(P, div, dreps + u0, LA, IF,
+                                                                                          IE, estride);
       check_launch("chunk_image_kernel");
-      assemble_kernel<false, true><<<dim3(nb, groups), kGreenThreads, smemB, st>>>(
-          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride);
+      assemble_kernel<false, true><<<dim3(b1 - b0, groups), kGreenThreads, smemB, st>>>(
+          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride, dimg + b0, u0);
       check_launch("assemble_kernel");
+      b0 = b1;
     }
     release(IF, st);
     release(IE, st);
+    release(dreps, st);
+    release(dimg, st);
   } else {
     if (full)
       assemble_kernel<true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0);

@@ -80,4 +80,11 @@ def test_blocks_within_reference_envelope(torch_cuda, k):
         sel = [(i, (a, b)) for i, (a, b) in enumerate(offs) if 0 <= a < b]
         full = np.stack([allb[a, b] for _, (a, b) in sel])
         idx = [i for i, _ in sel]
-        assert np.array_equal(full, dev[idx]), "full build and assemble_block disagree"
+        # the full build runs the fused kernel or (large builds) the split
+        # chunk-image kernels with images shared by offsets at equal R: the
+        # same formulas in another kernel, so rounding-level agreement with
+        # assemble_block, and the same bar against the reference
+        d = np.max(np.abs(full - dev[idx]), axis=1) / scale[idx]
+        assert d.max() <= 1e-7, f"full build vs assemble_block: {d.max():.2e}"
+        rf = np.max(np.abs(full - ref["ref"][idx]), axis=1) / scale[idx] / env[idx]
+        assert np.all(rf <= ENV_FACTOR), f"cfg{k} full build: envelope ratio {rf.max():.2f}"
