@@ -347,27 +347,21 @@ enum {
   fLU, fL0v, fL1s, fL0s, fRU, fR0, fR1, fD1, fD3, fD4, fD25, fPiu, fPic, kFields
 };
 
-// Pair order inside a group: diagonals (k, k) for s < nz, then neighbours
-// (k, k+1), then kp >= k + 2 row by row -- so a warp mostly holds one kind of
-// pair and the kind branches of the pair evaluation stay warp-uniform.
+// Pair order: by distance d = kp - k, then by k -- the diagonals (k, k) for
+// s < nz, then the neighbours (k, k+1), then d = 2, ... -- so a warp mostly
+// holds one kind of pair (the kind branches of the pair evaluation stay
+// warp-uniform) and pairs of one distance, whose chains underflow together:
+// at large lambda only the short-distance pairs contribute (the chain of
+// d - 1 thetas falls below 2^-1022), and a warp whose pairs all flush skips
+// the lambda (pair_flushed).
 __device__ __forceinline__ void pair_of(int s, int nz, int& k, int& kp) {
-  if (s < nz) {
-    k = kp = s;
-    return;
+  int d = 0;
+  while (s >= nz - d) {
+    s -= nz - d;
+    ++d;
   }
-  s -= nz;
-  if (s < nz - 1) {
-    k = s;
-    kp = s + 1;
-    return;
-  }
-  s -= nz - 1;
-  k = 0;
-  while (s >= nz - 2 - k) {
-    s -= nz - 2 - k;
-    ++k;
-  }
-  kp = k + 2 + s;
+  k = s;
+  kp = s + d;
 }
 
 // Prefix exponent e and zero count z of a chain packed as e - z 2^24: the
@@ -388,6 +382,15 @@ struct PairC {
   int kind;       // 0 diagonal, 1 off-diagonal
   int same;       // both intervals in one layer (FULL mode)
 };
+
+// true when every contribution of an off-diagonal pair at this lambda is
+// (signed) zero: both media's chain scalings 2^(E(kp) - E(k+1)) flush
+// (pow2_or_zero) or a zero theta lies on both chains, so V1, r0 and r1 of
+// pair_lambda are all multiplied by 0 (the reference's running products
+// underflow to the same zeros, layered.cpp:340-360)
+__device__ __forceinline__ bool pair_flushed(const int* __restrict__ El, int nz, const PairC& c) {
+  return c.kind != 0 && El[c.kp] - El[c.kn] < -1022 && El[nz + c.kp] - El[nz + c.kn] < -1022;
+}
 
 // one lambda of one interval pair into its nine accumulators (greens.cpp:167-191,
 // v_functions layered.cpp:397-408); wl = w00 lambda, w20 / lambda, w02 / lambda,
@@ -919,23 +922,29 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
   }
   auto F = [&](int li, int f, int j) -> cplx& { return C.F[(static_cast<size_t>(li) * kFields + f) * nz + j]; };
   auto Ei = [&](int li, int f, int j) -> int& { return C.E[(li * 2 + f) * nz + j]; };
-  // Pair assignment (balanced): group pairs [g0, g0 + cnt), cnt <= 3T. Slots
-  // 0, 1: pair g0 + i T + tid over the full lambda range. The ntail = cnt - 2T
-  // remaining pairs are split over lambda: thread tid < Teff = (T / ntail) ntail
-  // keeps tail pair tid % ntail for every Teff-th (pair, lambda) item of a
-  // chunk; the T / ntail partial sums per tail pair are added in a fixed order
-  // at the end, so every thread evaluates ~2.06 pairs per lambda, not 3.
+  // Pair assignment (balanced): group pairs [g0, g0 + cnt) in distance order
+  // (pair_of), cnt <= 3T. Even slots take pairs from the front of the group
+  // (short distances: active at every lambda), odd slots from the back (long
+  // distances: flushed at large lambda), so every thread holds about the same
+  // number of live (pair, lambda) items. The ntail = cnt - F - B pairs in the
+  // middle are split over lambda: thread tid < Teff = (T / ntail) ntail keeps
+  // tail pair tid % ntail for every Teff-th (pair, lambda) item of a chunk;
+  // the T / ntail partial sums per tail pair are added in a fixed order at
+  // the end, so every thread evaluates ~2.06 pairs per lambda, not 3.
   constexpr int T = kGreenThreads, NS = kGreenSlots;
   const int g0 = blockIdx.y * (NS + 1) * T;
   const int cnt = min((NS + 1) * T, P.npairs - g0);
-  const int ntail = max(0, cnt - NS * T);
+  const int nfront = min(cnt, ((NS + 1) / 2) * T), nback = min(cnt - nfront, (NS / 2) * T);
+  const int ntail = cnt - nfront - nback;
   const int teff = ntail > 0 ? (T / ntail) * ntail : 0;
   PairC pc[NS + 1];
   bool pv[NS + 1];
 #pragma unroll
   for (int i = 0; i <= NS; ++i) {
-    const int sl = i < NS ? i * T + threadIdx.x : NS * T + (ntail > 0 ? threadIdx.x % ntail : 0);
-    pv[i] = i < NS ? sl < cnt : static_cast<int>(threadIdx.x) < teff;
+    const int r = (i / 2) * T + static_cast<int>(threadIdx.x);  // rank within the front / back run
+    const int sl = i == NS ? nfront + (ntail > 0 ? static_cast<int>(threadIdx.x) % ntail : 0)
+                           : (i % 2 == 0 ? r : cnt - 1 - r);
+    pv[i] = i < NS ? r < (i % 2 == 0 ? nfront : nback) : static_cast<int>(threadIdx.x) < teff;
     int k = 0, kp = 0;
     if (pv[i]) pair_of(g0 + sl, nz, k, kp);
     pc[i].k = k;
@@ -997,31 +1006,67 @@ __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kerne
     __syncthreads();
     }
     PHASE_MARK(5);
-    // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair
-#pragma unroll kPairUnroll
-    for (int li = 0; li < lc; ++li) {
-      double wl[NWL];
+    // phase 2: pairs x lambdas (greens.cpp:167-191), lambda order per pair.
+    // Live lambda range of each slot in this chunk: [0, hi) ends after the
+    // last lambda at which any pair of the warp's slot is not flushed
+    // (pair_flushed; scanned from the chunk end, so a live chunk costs one
+    // vote). Lambdas past hi add exact zeros and are skipped; flushed lanes
+    // inside the range add exact zeros too. Large lambdas flush every chain
+    // of d >= 2 intervals, so the long-distance slots end early.
+    int hi[NS + 1] = {};
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      int h = lc;
+      while (h > 0 && __all_sync(0xffffffffu, !pv[i] || pair_flushed(C.E + (h - 1) * 2 * nz, nz, pc[i]))) --h;
+      hi[i] = h;
+    }
+    auto lam_w = [&](int li, double* wl) {
 #pragma unroll
       for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
-      const cplx* Fl = C.F + static_cast<size_t>(li) * fstride;
-      const int* El = C.E + li * 2 * nz;
-      if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
+    };
+    if (general2) {  // warp-uniform: both slots off-diagonal pairs, one branch-free block
+      const int h01 = min(hi[0], hi[NS > 1 ? 1 : 0]);
+#pragma unroll kPairUnroll
+      for (int li = 0; li < h01; ++li) {
+        double wl[NWL];
+        lam_w(li, wl);
+        const cplx* Fl = C.F + static_cast<size_t>(li) * fstride;
+        const int* El = C.E + li * 2 * nz;
         pair_lambda<1, FULL>(Fl, El, nz, pc[0], wl, acc[0]);
-        pair_lambda<1, FULL>(Fl, El, nz, pc[1], wl, acc[1]);
-      } else {
+        pair_lambda<1, FULL>(Fl, El, nz, pc[NS > 1 ? 1 : 0], wl, acc[NS > 1 ? 1 : 0]);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        for (int li = h01; li < hi[i]; ++li) {
+          double wl[NWL];
+          lam_w(li, wl);
+          pair_lambda<1, FULL>(C.F + static_cast<size_t>(li) * fstride, C.E + li * 2 * nz, nz, pc[i], wl, acc[i]);
+        }
+      }
+    } else {
+      int hmax = 0;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) hmax = max(hmax, hi[i]);
+#pragma unroll kPairUnroll
+      for (int li = 0; li < hmax; ++li) {
+        double wl[NWL];
+        lam_w(li, wl);
+        const cplx* Fl = C.F + static_cast<size_t>(li) * fstride;
+        const int* El = C.E + li * 2 * nz;
 #pragma unroll
         for (int i = 0; i < NS; ++i)
-          if (pv[i]) pair_lambda<-1, FULL>(Fl, El, nz, pc[i], wl, acc[i]);
+          if (pv[i] && li < hi[i]) pair_lambda<-1, FULL>(Fl, El, nz, pc[i], wl, acc[i]);
       }
     }
     if (pv[NS]) {
       for (int u = threadIdx.x; u < ntail * lc; u += teff) {
         const int li = u / ntail;
+        const int* El = C.E + li * 2 * nz;
+        if (pair_flushed(El, nz, pc[NS])) continue;
         double wl[NWL];
 #pragma unroll
         for (int q = 0; q < NWL; ++q) wl[q] = C.lam[q * LC + li];
-        pair_lambda<-1, FULL>(C.F + static_cast<size_t>(li) * fstride, C.E + li * 2 * nz, nz, pc[NS], wl,
-                              acc[NS]);
+        pair_lambda<-1, FULL>(C.F + static_cast<size_t>(li) * fstride, El, nz, pc[NS], wl, acc[NS]);
       }
     }
   }
