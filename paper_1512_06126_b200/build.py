@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 def build_cpp() -> Path:
     """libemie_b200.so: include/emie/*.hpp implemented over libemie_cu.so."""
     cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", str(ROOT / "include"),
-           str(PKG / "cpp" / "emie_dropin.cpp"), "-L", str(PKG), "-lemie_cu",
+           str(PKG / "cpp" / "emie_dropin.cpp"), str(PKG / "cpp" / "emie_quad.cpp"), "-L", str(PKG), "-lemie_cu",
            "-Wl,-rpath,$ORIGIN", "-o", str(CPPLIB)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

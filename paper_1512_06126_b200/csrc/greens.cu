@@ -58,36 +58,48 @@ __device__ __forceinline__ double ediff(double a, double b) {  // hankel.cpp:22-
   return erf(0.5 * b) - erf(0.5 * a);
 }
 
+// The stencils are evaluated product by product with explicit rounding (no
+// fused multiply-adds), as the reference's host build evaluates them: on a
+// symmetric axis (d = 0) the odd terms cancel to an exact zero
+// (test_hankel.cpp:88-95), which a contracted a*b + c*d would leave as the
+// rounding residue of one product.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
 __device__ void axis_stencil(int alpha, double d, double h, double out[3]) {  // hankel.cpp:35-71
-  const double wp = d + h, w0 = d, wm = d - h;
-  const double gp = exp(-0.25 * wp * wp);
-  const double g0 = exp(-0.25 * w0 * w0);
-  const double gm = exp(-0.25 * wm * wm);
-  const double gs = gp - 2.0 * g0 + gm;
+  const double wp = add(d, h), w0 = d, wm = sub(d, h);
+  const double gp = exp(mul(mul(-0.25, wp), wp));
+  const double g0 = exp(mul(mul(-0.25, w0), w0));
+  const double gm = exp(mul(mul(-0.25, wm), wm));
+  const double gs = add(sub(gp, mul(2.0, g0)), gm);
   const double ep = ediff(w0, wp);
   const double em = ediff(wm, w0);
+  // a_p x_p - 2 a_0 x_0 + a_m x_m with a = w^k
+  auto st3 = [&](double ap, double a0, double am) { return add(sub(mul(ap, gp), mul(mul(2.0, a0), g0)), mul(am, gm)); };
   if (alpha == 0) {
-    const double lin = wp * ep - wm * em;
-    const double w2s = wp * wp * gp - 2.0 * w0 * w0 * g0 + wm * wm * gm;
-    out[0] = kSqrtPi * lin + 2.0 * gs;
-    out[1] = 2.0 * kSqrtPi * lin + 8.0 * gs;
-    out[2] = 12.0 * kSqrtPi * lin + 4.0 * w2s + 64.0 * gs;
+    const double lin = sub(mul(wp, ep), mul(wm, em));
+    const double w2s = st3(mul(wp, wp), mul(w0, w0), mul(wm, wm));
+    out[0] = add(mul(kSqrtPi, lin), mul(2.0, gs));
+    out[1] = add(mul(mul(2.0, kSqrtPi), lin), mul(8.0, gs));
+    out[2] = add(add(mul(mul(12.0, kSqrtPi), lin), mul(4.0, w2s)), mul(64.0, gs));
   } else if (alpha == 1) {
-    const double es = ep - em;
-    const double wg = wp * gp - 2.0 * w0 * g0 + wm * gm;
-    const double w3g = wp * wp * wp * gp - 2.0 * w0 * w0 * w0 * g0 + wm * wm * wm * gm;
-    out[0] = kSqrtPi * es;
-    out[1] = 2.0 * kSqrtPi * es - 2.0 * wg;
-    out[2] = 12.0 * kSqrtPi * es - 2.0 * w3g - 12.0 * wg;
+    const double es = sub(ep, em);
+    const double wg = st3(wp, w0, wm);
+    const double w3g = st3(mul(mul(wp, wp), wp), mul(mul(w0, w0), w0), mul(mul(wm, wm), wm));
+    out[0] = mul(kSqrtPi, es);
+    out[1] = sub(mul(mul(2.0, kSqrtPi), es), mul(2.0, wg));
+    out[2] = sub(sub(mul(mul(12.0, kSqrtPi), es), mul(2.0, w3g)), mul(12.0, wg));
   } else {
     out[0] = gs;
-    out[1] = wp * wp * gp - 2.0 * w0 * w0 * g0 + wm * wm * gm;
-    out[2] = wp * wp * wp * wp * gp - 2.0 * w0 * w0 * w0 * w0 * g0 + wm * wm * wm * wm * gm;
+    out[1] = st3(mul(wp, wp), mul(w0, w0), mul(wm, wm));
+    out[2] = st3(mul(mul(mul(wp, wp), wp), wp), mul(mul(mul(w0, w0), w0), w0), mul(mul(mul(wm, wm), wm), wm));
   }
 }
 
 struct Geom {
   double r, p, q, phi;
+  double cs, sn;  // cos(phi), sin(phi): on the host from the C library, as the reference evaluates them
 };
 __host__ __device__ inline Geom pair_geometry(int oi, int oj, double hx, double hy) {  // hankel.cpp:80-91
   const double ax = oj * hx - 0.5 * hx;
@@ -97,7 +109,17 @@ __host__ __device__ inline Geom pair_geometry(int oi, int oj, double hx, double 
   g.p = hx / g.r;
   g.q = hy / g.r;
   g.phi = atan2(ay, ax);
+#ifdef __CUDA_ARCH__
+  sincos(g.phi, &g.sn, &g.cs);
+#else
+  g.cs = std::cos(g.phi);
+  g.sn = std::sin(g.phi);
+#endif
   return g;
+}
+// a caller's PairGeometry (r, p, q, phi) as the device routines take it
+inline Geom geom_of(const double* geom) {
+  return Geom{geom[0], geom[1], geom[2], geom[3], std::cos(geom[3]), std::sin(geom[3])};
 }
 
 // Offsets travel as integer codes: code = (oi + bias_i) * span + (oj + bias_j).
@@ -162,22 +184,26 @@ __device__ double point_kernel_output(const PGeom& g, int alpha, int beta, doubl
 __device__ double kernel_output(const Geom& g, int alpha, int beta, double s) {  // hankel.cpp:101-113
   const double r = exp(s);
   const double hx = g.p * r, hy = g.q * r;
-  double sn, cs;
-  sincos(g.phi, &sn, &cs);
-  const double dx = r * cs + 0.5 * hx;
-  const double dy = r * sn + 0.5 * hy;
+  const double sn = g.sn, cs = g.cs;
+  // products rounded before the sum, as the reference evaluates them: on an
+  // axis through the pair's symmetry (e.g. oi = 0) r sin(phi) rounds to
+  // exactly -hy / 2, so dy = 0 and the one-derivative kernel across it is an
+  // exact zero (test_hankel.cpp:88-95); a fused multiply-add would keep the
+  // product's rounding residue instead
+  const double dx = __dadd_rn(__dmul_rn(r, cs), 0.5 * hx);
+  const double dy = __dadd_rn(__dmul_rn(r, sn), 0.5 * hy);
   double ax[3], ay[3];
   axis_stencil(alpha, dx, hx, ax);
   axis_stencil(beta, dy, hy, ay);
-  const double comb = 0.25 * (ax[2] * ay[0] + 2.0 * ax[1] * ay[1] + ax[0] * ay[2]);
+  const double comb = mul(0.25, add(add(mul(ax[2], ay[0]), mul(mul(2.0, ax[1]), ay[1])), mul(ax[0], ay[2])));
   if (comb == 0.0) return 0.0;
-  return exp(-(3 - alpha - beta) * s) * comb;
+  return mul(exp(-(3 - alpha - beta) * s), comb);
 }
 
 __device__ __forceinline__ double design_input(double lambda) {  // hankel.cpp:93-99
   if (lambda > 38.0) return 0.0;
-  const double l2 = lambda * lambda;
-  return 8.0 * exp(-l2) * lambda * ((l2 - 4.0) * l2 + 2.0);
+  const double l2 = mul(lambda, lambda);
+  return mul(mul(mul(8.0, exp(-l2)), lambda), add(mul(sub(l2, 4.0), l2), 2.0));
 }
 
 __constant__ int kAlpha[6] = {0, 2, 0, 1, 1, 0};  // greens.cpp:137
@@ -224,7 +250,8 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
                                      const cplx* __restrict__ tw, FftPlan pl, int half, double step,
                                      double shift, int n1, int n2, OffsetCode oc, double hx, double hy,
                                      int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs,
-                                     Geom gfix, int use_gfix, int kern0, const PGeom* __restrict__ pgeo) {
+                                     Geom gfix, int use_gfix, int kern0, const PGeom* __restrict__ pgeo,
+                                     const Geom* __restrict__ gtab) {
   extern __shared__ cplx sm[];
   const int n = pl.n, ld = n | 1;
   cplx* a = sm;
@@ -234,8 +261,10 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
   const int off = oc.slot(code, blockIdx.x);
   const int oi = fixed_oi != INT32_MIN ? fixed_oi : oc.oi(code);
   const int oj = fixed_oi != INT32_MIN ? fixed_oj : oc.oj(code);
-  // a caller-given pair geometry (FilterDesigner::design, hankel.hpp:93), else the offset's
-  const Geom g = use_gfix ? gfix : pair_geometry(oi, oj, hx, hy);
+  // a caller-given pair geometry (FilterDesigner::design, hankel.hpp:93), else
+  // the offset's, from the host's table (the reference's own C-library
+  // hypot / atan2 / sin / cos: bit-identical design inputs) when given
+  const Geom g = use_gfix ? gfix : gtab ? gtab[blockIdx.x] : pair_geometry(oi, oj, hx, hy);
   const int alpha = kAlpha[kern], beta = kBeta[kern];
   load_twiddles(t, tw, n);
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -798,12 +827,6 @@ inline bool img_share_enabled() {
   return on;
 }
 
-// R of each offset code, as every kernel of the build computes it
-__global__ void r_of_codes_kernel(const GreenParams P, const int* __restrict__ offs, int n, double* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = pair_geometry(P.oc.oi(offs[i]), P.oc.oj(offs[i]), P.hx, P.hy).r;
-}
-
 // Per-lambda phases 0-1c of the accumulation (layer states, interval factors,
 // prefix products, left factors: everything of a chunk but the pair sums) for
 // one (offset, lambda chunk of LA) per CTA, at several CTAs per SM -- these
@@ -812,13 +835,13 @@ __global__ void r_of_codes_kernel(const GreenParams P, const int* __restrict__ o
 // IE[b][t][2][nz] (offset stride estride ints) the pair kernel streams in.
 __global__ void __launch_bounds__(kImgThreads, EMIE_GREEN_IMG_MINB) chunk_image_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const int* __restrict__ offs, int LA,
-    cplx* __restrict__ IF, int* __restrict__ IE, size_t estride) {
+    cplx* __restrict__ IF, int* __restrict__ IE, size_t estride, const double* __restrict__ Rrep) {
   extern __shared__ cplx sm[];
   const int NL = P.L + 1, nz = P.nz;
   const int b = blockIdx.y, t0 = blockIdx.x * LA;
   const int lc = min(LA, P.nw - t0);
   const int code = offs[b];
-  const Geom g = pair_geometry(P.oc.oi(code), P.oc.oj(code), P.hx, P.hy);
+  const double R = Rrep ? Rrep[b] : pair_geometry(P.oc.oi(code), P.oc.oj(code), P.hx, P.hy).r;
   Chunk C;
   {
     cplx* s = sm;
@@ -835,7 +858,7 @@ __global__ void __launch_bounds__(kImgThreads, EMIE_GREEN_IMG_MINB) chunk_image_
     C.lam = nullptr;
     C.E = reinterpret_cast<int*>(s);
   }
-  chunk_layer_states(P, C, g.r, t0, lc, threadIdx.x, blockDim.x, true);
+  chunk_layer_states(P, C, R, t0, lc, threadIdx.x, blockDim.x, true);
   __syncthreads();
   chunk_factors(P, C, iv, lc, P.omega * kMu0, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -865,15 +888,16 @@ template <bool FULL = false, bool IMG = false>
 __global__ void __launch_bounds__(kGreenThreads, EMIE_GREEN_MINB) assemble_kernel(
     const GreenParams P, const Interval* __restrict__ iv, const double* __restrict__ W,
     cplx* __restrict__ blocks, int* err, const int* __restrict__ offs, int pos0, const cplx* __restrict__ IF,
-    const int* __restrict__ IE, size_t estride, const int* __restrict__ img_of = nullptr, int img_base = 0) {
+    const int* __restrict__ IE, size_t estride, const int* __restrict__ img_of = nullptr, int img_base = 0,
+    const double* __restrict__ Roff = nullptr) {
   extern __shared__ cplx sm[];
   __shared__ uint64_t ibar[2];
   const int L = P.L, NL = P.L + 1, nz = P.nz, LC = P.LC;
   const int code = offs[blockIdx.x];
   const int off = P.oc.slot(code, pos0 + blockIdx.x);  // block / weight slot
   const int oi = P.oc.oi(code), oj = P.oc.oj(code);
-  const Geom g = pair_geometry(oi, oj, P.hx, P.hy);
-  const double R = g.r;
+  // the offset's distance R: the host's (hankel.cpp:80-91 in the C library) when given
+  const double R = Roff ? Roff[blockIdx.x] : pair_geometry(oi, oj, P.hx, P.hy).r;
   const double* Woff = W + static_cast<size_t>(off) * 6 * P.nw;
   const double wmu = P.omega * kMu0;  // V1 = i wmu W00 (layered.cpp:400)
 
@@ -1632,7 +1656,7 @@ void free_filter_bank(FilterBank& fb, cudaStream_t st) {
 void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, OffsetCode oc, double hx,
                     double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
                     int fixed_oj = 0, const int* offs = nullptr, const Geom* gfix = nullptr, int kern0 = 0,
-                    int nkern = 6, const PGeom* pgeo = nullptr) {
+                    int nkern = 6, const PGeom* pgeo = nullptr, const Geom* gtab = nullptr) {
   const int n = 2 * fp.half;
   const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
   set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
@@ -1640,7 +1664,7 @@ void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, Offs
   filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
                                                 fp.step, fp.shift, fp.n1, fp.n2, oc, hx, hy, err,
                                                 fixed_oi, fixed_oj, offs, gfix ? *gfix : Geom{}, gfix != nullptr,
-                                                kern0, pgeo);
+                                                kern0, pgeo, gtab);
   check_launch("filter_design_kernel");
 }
 
@@ -1686,7 +1710,8 @@ void design_offset_filters_host(int oi, int oj, double hx, double hy, const Filt
   double* dW = scratch<double>(6 * nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, 1, OffsetCode{}, hx, hy, dW, err, st, oi, oj);
+  const Geom gh = pair_geometry(oi, oj, hx, hy);  // host C library, as the reference
+  design_filters(fb, fp, 1, OffsetCode{}, hx, hy, dW, err, st, oi, oj, nullptr, &gh);
   int e = 0;
   EMIE_CUDA(cudaMemcpyAsync(w, dW, 6 * nw * sizeof(double), cudaMemcpyDeviceToHost, st));
   EMIE_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1788,7 +1813,7 @@ void design_geometry_host(const double geom[4], int alpha, int beta, const Filte
   double* dW = scratch<double>(6 * nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  const Geom g{geom[0], geom[1], geom[2], geom[3]};
+  const Geom g = geom_of(geom);
   design_filters(fb, fp, 1, OffsetCode{}, 1.0, 1.0, dW, err, st, 0, 0, nullptr, &g, kern, 1);
   int e = 0;
   EMIE_CUDA(cudaMemcpyAsync(w, dW + kern * nw, nw * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1807,7 +1832,7 @@ void kernel_output_geom_host(const double geom[4], int alpha, int beta, const do
   double* d = nullptr;
   EMIE_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
   EMIE_CUDA(cudaMemcpy(d, s, n * sizeof(double), cudaMemcpyHostToDevice));
-  kernel_output_kernel<<<ceil_div(n, 256), 256>>>(Geom{geom[0], geom[1], geom[2], geom[3]}, alpha, beta, d, n, d + n);
+  kernel_output_kernel<<<ceil_div(n, 256), 256>>>(geom_of(geom), alpha, beta, d, n, d + n);
   check_launch("kernel_output_kernel");
   EMIE_CUDA(cudaMemcpy(out, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
   cudaFree(d);
@@ -2103,7 +2128,23 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
   double* W = scratch<double>(static_cast<size_t>(nslots) * 6 * P.nw, st);
   int* err = scratch<int>(1, st);
   EMIE_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-  design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs);
+  // the offsets' pair geometries from the host's C library, as the reference
+  // computes them (hankel.cpp:80-91 and the sin / cos of kernel_output): the
+  // filter designs and the lambda lattices lambda_m / R start from identical inputs
+  std::vector<Geom> gh(ncomp);
+  std::vector<double> Rh(ncomp);
+  for (int i = 0; i < ncomp; ++i) {
+    gh[i] = pair_geometry(P.oc.oi(offs_h[i]), P.oc.oj(offs_h[i]), P.hx, P.hy);
+    Rh[i] = gh[i].r;
+  }
+  double* dRoff = scratch<double>(ncomp, st);
+  EMIE_CUDA(cudaMemcpyAsync(dRoff, Rh.data(), ncomp * sizeof(double), cudaMemcpyHostToDevice, st));
+  {
+    Geom* gtab = scratch<Geom>(ncomp, st);
+    EMIE_CUDA(cudaMemcpyAsync(gtab, gh.data(), ncomp * sizeof(Geom), cudaMemcpyHostToDevice, st));
+    design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs, nullptr, 0, 6, nullptr, gtab);
+    release(gtab, st);
+  }
 
   Interval* div = scratch<Interval>(nz, st);
   EMIE_CUDA(cudaMemcpyAsync(div, ivh.data(), nz * sizeof(Interval), cudaMemcpyHostToDevice, st));
@@ -2170,33 +2211,36 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     // offsets are reordered by R; signed-offset requests (slot = request
     // position) keep one image per offset.
     std::vector<int> img_h(ncomp), reps;
+    std::vector<double> Rrep;
     if (!P.oc.compact && img_share_enabled()) {
-      double* dR = scratch<double>(ncomp, st);
-      r_of_codes_kernel<<<ceil_div(ncomp, 256), 256, 0, st>>>(P, offs, ncomp, dR);
-      check_launch("r_of_codes_kernel");
-      std::vector<double> Rh(ncomp);
-      EMIE_CUDA(cudaMemcpyAsync(Rh.data(), dR, ncomp * sizeof(double), cudaMemcpyDeviceToHost, st));
-      EMIE_CUDA(cudaStreamSynchronize(st));
-      release(dR, st);
       std::vector<uint64_t> key(ncomp);
       std::memcpy(key.data(), Rh.data(), ncomp * sizeof(double));
       std::vector<int> idx(ncomp);
       for (int i = 0; i < ncomp; ++i) idx[i] = i;
       std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] < key[b]; });
       std::vector<int> sorted(ncomp);
+      std::vector<double> Rs(ncomp);
       for (int b = 0; b < ncomp; ++b) {
         sorted[b] = offs_h[idx[b]];
-        if (b == 0 || key[idx[b]] != key[idx[b - 1]]) reps.push_back(sorted[b]);
+        Rs[b] = Rh[idx[b]];
+        if (b == 0 || key[idx[b]] != key[idx[b - 1]]) {
+          reps.push_back(sorted[b]);
+          Rrep.push_back(Rs[b]);
+        }
         img_h[b] = static_cast<int>(reps.size()) - 1;
       }
       EMIE_CUDA(cudaMemcpyAsync(offs, sorted.data(), ncomp * sizeof(int), cudaMemcpyHostToDevice, st));
+      EMIE_CUDA(cudaMemcpyAsync(dRoff, Rs.data(), ncomp * sizeof(double), cudaMemcpyHostToDevice, st));
     } else {
       reps = offs_h;
+      Rrep = Rh;
       for (int b = 0; b < ncomp; ++b) img_h[b] = b;
     }
     const int nu = static_cast<int>(reps.size());
     int* dreps = scratch<int>(nu, st);
     int* dimg = scratch<int>(ncomp, st);
+    double* dRrep = scratch<double>(nu, st);
+    EMIE_CUDA(cudaMemcpyAsync(dRrep, Rrep.data(), nu * sizeof(double), cudaMemcpyHostToDevice, st));
     EMIE_CUDA(cudaMemcpyAsync(dreps, reps.data(), nu * sizeof(int), cudaMemcpyHostToDevice, st));
     EMIE_CUDA(cudaMemcpyAsync(dimg, img_h.data(), ncomp * sizeof(int), cudaMemcpyHostToDevice, st));
     const int maxu = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
@@ -2209,10 +2253,10 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
       int b1 = b0;
       while (b1 < ncomp && img_h[b1] < u1) ++b1;  // the offsets of images [u0, u1)
       chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), u1 - u0), kImgThreads, smemA, st>>>(P, div, dreps + u0, LA, IF,
-                                                                                          IE, estride);
+                                                                                          IE, estride, dRrep + u0);
       check_launch("chunk_image_kernel");
       assemble_kernel<false, true><<<dim3(b1 - b0, groups), kGreenThreads, smemB, st>>>(
-          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride, dimg + b0, u0);
+          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride, dimg + b0, u0, dRoff + b0);
       check_launch("assemble_kernel");
       b0 = b1;
     }
@@ -2220,11 +2264,14 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     release(IE, st);
     release(dreps, st);
     release(dimg, st);
+    release(dRrep, st);
   } else {
     if (full)
-      assemble_kernel<true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0);
+      assemble_kernel<true><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0,
+                                                               nullptr, 0, dRoff);
     else
-      assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0);
+      assemble_kernel<false><<<grid, kGreenThreads, smem, st>>>(P, div, W, blocks, err, offs, 0, nullptr, nullptr, 0,
+                                                                nullptr, 0, dRoff);
     check_launch("assemble_kernel");
   }
 #ifdef EMIE_GREENS_PHASE_CLOCKS
@@ -2248,6 +2295,7 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
   release(err, st);
   release(div, st);
   release(offs, st);
+  release(dRoff, st);
   free_filter_bank(fb, st);
   if (e) {
     raise_filter_errors(e);

@@ -39,8 +39,10 @@ def _cases(name):
     return [l for l in src.read_text().splitlines() if l.strip()]
 
 
-# the reference's own greens and layered suites (tests/test_greens.cpp,
-# tests/test_layered.cpp), unchanged, compiled against the drop-in: every
+# the reference's own greens, layered and hankel suites (tests/test_greens.cpp,
+# tests/test_layered.cpp, tests/test_hankel.cpp), unchanged, compiled against
+# the drop-in (hankel: the filter design on the device, the closed forms gated
+# by the drop-in's kernel_output_oracle): every
 # case but the brute-force spectral-integration oracle of test_greens.cpp:109
 # (~13 min through per-point device calls; run by tools/run_dropin_suites.sh,
 # result in profiles/r02_dropin_suites.log)
@@ -48,7 +50,8 @@ SLOW = {"cross couplings match direct spectral integration"}
 
 
 @pytest.mark.parametrize("suite,case", [("greens", c) for c in _cases("greens") if c not in SLOW] +
-                         [("layered", c) for c in _cases("layered")])
+                         [("layered", c) for c in _cases("layered")] +
+                         [("hankel", c) for c in _cases("hankel")])
 def test_reference_suites_against_dropin(torch_cuda, suite, case):
     b = ROOT / "oracle" / "_ref" / f"dropin_test_{suite}"
     if not b.exists():
