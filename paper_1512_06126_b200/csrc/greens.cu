@@ -816,7 +816,7 @@ constexpr int kImgThreads = EMIE_GREEN_IMG_THREADS;
 #ifndef EMIE_GREEN_IMG_LAMBDAS
 #define EMIE_GREEN_IMG_LAMBDAS 4
 #endif
-constexpr int kImgLambdas = EMIE_GREEN_IMG_LAMBDAS;  // lambdas per chunk_image_kernel CTA
+constexpr int kImgLambdas = EMIE_GREEN_IMG_LAMBDAS;  // lambdas per chunk_image_kernel CTA (nz > 32)
 constexpr size_t kImgBudget = size_t{2} << 30;       // bytes of chunk images per batch (cfg3: 1 / 2 / 4 GB -> 31.6 / 30.1 / 29.7 ms)
 // chunk images shared by offsets at equal R (EMIE_CU_GREENS_RSHARE=0: one per offset, A/B)
 inline bool img_share_enabled() {
@@ -2176,7 +2176,10 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
   // 2,080 offsets: 5.3 vs 5.1 ms, and the split's host-side grouping costs more)
   const bool split_default = groups > 1 || (!P.oc.compact && img_share_enabled() && ncomp >= 4096);
   if (!full && (img_mode < 0 ? split_default : img_mode == 1)) {
-    const int LA = kImgLambdas;
+    // lambdas per image CTA: 6 at nz <= 32 (config 3: 27.7 -> 26.2 ms; the
+    // serial chain phase runs 24 tasks instead of 16), else kImgLambdas (its
+    // SMEM would cost CTAs per SM at nz = 64: 340 -> 360 ms with 6)
+    const int LA = nz <= 32 ? 6 : kImgLambdas;
     const size_t smemA = static_cast<size_t>(LA) * (14 * NL + kFields * nz) * sizeof(cplx) +
                          static_cast<size_t>(LA) * 2 * nz * sizeof(int);
     set_smem(reinterpret_cast<const void*>(chunk_image_kernel), smemA);
