@@ -97,6 +97,34 @@ __device__ void axis_stencil(int alpha, double d, double h, double out[3]) {  //
   }
 }
 
+// axis_stencil for alpha = 0, 1, 2 at once: the exponentials and error-function
+// differences are shared, every output is formed by exactly axis_stencil's
+// operations (the same bits)
+__device__ void axis_stencil_all(double d, double h, double out[3][3]) {
+  const double wp = add(d, h), w0 = d, wm = sub(d, h);
+  const double gp = exp(mul(mul(-0.25, wp), wp));
+  const double g0 = exp(mul(mul(-0.25, w0), w0));
+  const double gm = exp(mul(mul(-0.25, wm), wm));
+  const double gs = add(sub(gp, mul(2.0, g0)), gm);
+  const double ep = ediff(w0, wp);
+  const double em = ediff(wm, w0);
+  auto st3 = [&](double ap, double a0, double am) { return add(sub(mul(ap, gp), mul(mul(2.0, a0), g0)), mul(am, gm)); };
+  const double lin = sub(mul(wp, ep), mul(wm, em));
+  const double w2s = st3(mul(wp, wp), mul(w0, w0), mul(wm, wm));
+  out[0][0] = add(mul(kSqrtPi, lin), mul(2.0, gs));
+  out[0][1] = add(mul(mul(2.0, kSqrtPi), lin), mul(8.0, gs));
+  out[0][2] = add(add(mul(mul(12.0, kSqrtPi), lin), mul(4.0, w2s)), mul(64.0, gs));
+  const double es = sub(ep, em);
+  const double wg = st3(wp, w0, wm);
+  const double w3g = st3(mul(mul(wp, wp), wp), mul(mul(w0, w0), w0), mul(mul(wm, wm), wm));
+  out[1][0] = mul(kSqrtPi, es);
+  out[1][1] = sub(mul(mul(2.0, kSqrtPi), es), mul(2.0, wg));
+  out[1][2] = sub(sub(mul(mul(12.0, kSqrtPi), es), mul(2.0, w3g)), mul(12.0, wg));
+  out[2][0] = gs;
+  out[2][1] = w2s;  // st3 of the squares, as axis_stencil's alpha = 2 out[1]
+  out[2][2] = st3(mul(mul(mul(wp, wp), wp), wp), mul(mul(mul(w0, w0), w0), w0), mul(mul(mul(wm, wm), wm), wm));
+}
+
 struct Geom {
   double r, p, q, phi;
   double cs, sn;  // cos(phi), sin(phi): on the host from the C library, as the reference evaluates them
@@ -242,6 +270,40 @@ __global__ void filter_den_kernel(cplx* den, double* floor_out, const cplx* __re
   }
 }
 
+// The design samples of all six kernels of an offset (greens.cpp:137 order)
+// at once: per sample the two axes' stencils of every derivative order share
+// their exponentials and error functions (axis_stencil_all), so a full build
+// evaluates the transcendentals once per (offset, sample) instead of once per
+// (offset, kernel, sample); each value is kernel_output's, bit for bit.
+// S[i][kern][j] = (-1)^(j + half) u(m step + shift), m = j - half.
+__global__ void filter_samples_kernel(const Geom* __restrict__ gtab, int noff, int n, int half, double step,
+                                      double shift, double* __restrict__ S) {
+  const long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (x >= static_cast<long long>(noff) * n) return;
+  const int i = static_cast<int>(x / n), j = static_cast<int>(x - static_cast<long long>(i) * n);
+  const Geom g = gtab[i];
+  const int m = j - half;
+  const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
+  const double sj = m * step + shift;
+  // kernel_output (hankel.cpp:101-113) with the stencils shared
+  const double r = exp(sj);
+  const double hx = g.p * r, hy = g.q * r;
+  const double dx = __dadd_rn(__dmul_rn(r, g.cs), 0.5 * hx);
+  const double dy = __dadd_rn(__dmul_rn(r, g.sn), 0.5 * hy);
+  double ax[3][3], ay[3][3];
+  axis_stencil_all(dx, hx, ax);
+  axis_stencil_all(dy, hy, ay);
+  double* o = S + static_cast<size_t>(i) * 6 * n + j;
+#pragma unroll
+  for (int kern = 0; kern < 6; ++kern) {
+    const int alpha = kAlpha[kern], beta = kBeta[kern];
+    const double comb = mul(0.25, add(add(mul(ax[alpha][2], ay[beta][0]), mul(mul(2.0, ax[alpha][1]), ay[beta][1])),
+                                      mul(ax[alpha][0], ay[beta][2])));
+    const double u = comb == 0.0 ? 0.0 : mul(exp(-(3 - alpha - beta) * sj), comb);
+    o[static_cast<size_t>(kern) * n] = sign * u;
+  }
+}
+
 // FilterDesigner::design (hankel.cpp:239-281) for offset blockIdx.x (oi, oj
 // >= 0 row-major over ny x nx) and kernel blockIdx.y; err bits: 1 vanishing
 // input spectrum, 2 non-real residue
@@ -251,7 +313,7 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
                                      double shift, int n1, int n2, OffsetCode oc, double hx, double hy,
                                      int* err, int fixed_oi, int fixed_oj, const int* __restrict__ offs,
                                      Geom gfix, int use_gfix, int kern0, const PGeom* __restrict__ pgeo,
-                                     const Geom* __restrict__ gtab) {
+                                     const Geom* __restrict__ gtab, const double* __restrict__ samp) {
   extern __shared__ cplx sm[];
   const int n = pl.n, ld = n | 1;
   cplx* a = sm;
@@ -267,12 +329,17 @@ __global__ void filter_design_kernel(double* W, const cplx* __restrict__ den,
   const Geom g = use_gfix ? gfix : gtab ? gtab[blockIdx.x] : pair_geometry(oi, oj, hx, hy);
   const int alpha = kAlpha[kern], beta = kBeta[kern];
   load_twiddles(t, tw, n);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const int m = j - half;
-    const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
-    const double sj = m * step + shift;
-    a[j] = {sign * (pgeo ? point_kernel_output(pgeo[blockIdx.x], alpha, beta, sj) : kernel_output(g, alpha, beta, sj)),
-            0.0};
+  if (samp) {  // precomputed by filter_samples_kernel (full builds)
+    const double* sv = samp + (static_cast<size_t>(blockIdx.x) * 6 + kern) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) a[j] = {sv[j], 0.0};
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const int m = j - half;
+      const double sign = ((j + half) % 2 == 0) ? 1.0 : -1.0;
+      const double sj = m * step + shift;
+      a[j] = {sign * (pgeo ? point_kernel_output(pgeo[blockIdx.x], alpha, beta, sj) : kernel_output(g, alpha, beta, sj)),
+              0.0};
+    }
   }
   __syncthreads();
   cplx* res = fft_smem(a, b, ld, 1, pl, t, false);
@@ -1656,7 +1723,8 @@ void free_filter_bank(FilterBank& fb, cudaStream_t st) {
 void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, OffsetCode oc, double hx,
                     double hy, double* W, int* err, cudaStream_t st, int fixed_oi = INT32_MIN,
                     int fixed_oj = 0, const int* offs = nullptr, const Geom* gfix = nullptr, int kern0 = 0,
-                    int nkern = 6, const PGeom* pgeo = nullptr, const Geom* gtab = nullptr) {
+                    int nkern = 6, const PGeom* pgeo = nullptr, const Geom* gtab = nullptr,
+                    const double* samp = nullptr) {
   const int n = 2 * fp.half;
   const size_t smem = (2 * static_cast<size_t>(n | 1) + n) * sizeof(cplx);
   set_smem(reinterpret_cast<const void*>(filter_design_kernel), smem);
@@ -1664,7 +1732,7 @@ void design_filters(const FilterBank& fb, const FilterParams& fp, int noff, Offs
   filter_design_kernel<<<grid, 256, smem, st>>>(W, fb.den, fb.floor, fb.tw, fb.pl, fp.half,
                                                 fp.step, fp.shift, fp.n1, fp.n2, oc, hx, hy, err,
                                                 fixed_oi, fixed_oj, offs, gfix ? *gfix : Geom{}, gfix != nullptr,
-                                                kern0, pgeo, gtab);
+                                                kern0, pgeo, gtab, samp);
   check_launch("filter_design_kernel");
 }
 
@@ -2142,7 +2210,28 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
   {
     Geom* gtab = scratch<Geom>(ncomp, st);
     EMIE_CUDA(cudaMemcpyAsync(gtab, gh.data(), ncomp * sizeof(Geom), cudaMemcpyHostToDevice, st));
-    design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs, nullptr, 0, 6, nullptr, gtab);
+    // the six kernels' design samples of every offset, transcendentals shared
+    // (filter_samples_kernel), in batches of at most 2^16 offsets
+    // (EMIE_CU_GREENS_SHARED_SAMPLES=0: kernel_output per kernel, A/B and the
+    // bit-identity test)
+    static const bool shared_samples = [] {
+      const char* e = std::getenv("EMIE_CU_GREENS_SHARED_SAMPLES");
+      return !(e && e[0] == '0');
+    }();
+    const int n = 2 * fp.half;
+    const int bmax = P.oc.compact ? ncomp : std::min(ncomp, 1 << 16);  // compact slots are positions: one batch
+    double* samp = shared_samples ? scratch<double>(static_cast<size_t>(bmax) * 6 * n, st) : nullptr;
+    for (int i0 = 0; i0 < ncomp && !shared_samples; i0 += ncomp)
+      design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs, nullptr, 0, 6, nullptr, gtab);
+    for (int i0 = 0; i0 < ncomp && shared_samples; i0 += bmax) {
+      const int nb = std::min(bmax, ncomp - i0);
+      filter_samples_kernel<<<ceil_div(static_cast<long long>(nb) * n, 256), 256, 0, st>>>(gtab + i0, nb, n, fp.half,
+                                                                                          fp.step, fp.shift, samp);
+      check_launch("filter_samples_kernel");
+      design_filters(fb, fp, nb, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs + i0, nullptr, 0, 6, nullptr,
+                     nullptr, samp);
+    }
+    if (samp) release(samp, st);
     release(gtab, st);
   }
 

@@ -175,3 +175,30 @@ np.save(sys.argv[1], op.blocks())
     a, b = outs["shared"], outs["fused"]
     err = np.max(np.abs(a - b), axis=-1) / np.max(np.abs(b), axis=-1)
     assert np.max(err) <= 1e-7, np.max(err)
+
+
+def test_shared_sample_designs_bit_identical(torch_cuda):
+    """the build designs its filters from samples whose transcendentals are
+    shared by the six kernels of an offset (filter_samples_kernel); the same
+    operations as kernel_output per kernel give the same bits, so the blocks
+    equal those of the per-kernel samples (EMIE_CU_GREENS_SHARED_SAMPLES=0)"""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {str(Path(__file__).resolve().parent.parent)!r})
+import paper_1512_06126_b200 as emie
+m = emie.LayeredModel([0.0, 500.0, 2500.0], [0.0, 1e-3, 10 ** -1.5, 1.0])
+grid = emie.make_grid(m, list(np.linspace(600.0, 1000.0, 9)), 6, 5, 100.0, 130.0)
+op = emie.assemble_operator(grid, m, 2 * np.pi * 0.5, keep_blocks=True)
+np.save(sys.argv[1], op.blocks())
+"""
+    outs = []
+    for flag in ("1", "0"):
+        f = Path(f"/tmp/emie_samples_{flag}.npy")
+        subprocess.run([sys.executable, "-c", code, str(f)], env=dict(os.environ, EMIE_CU_GREENS_SHARED_SAMPLES=flag),
+                       check=True)
+        outs.append(np.load(f))
+    assert np.all(np.isfinite(outs[0]))
+    assert np.array_equal(outs[0], outs[1])
