@@ -531,8 +531,9 @@ def run_ours(args):
                                    "dram__bytes_write.sum, one launch)",
                     hbm=hbm_view, fp64=fp64_view)
     # Green's build roofline (FP64-pipe bound; the ncu-measured
-    # FP64 work is authoritative): executed FP64 flops of one cfg3 assemble
-    # launch from the committed ncu capture over this run's assemble time
+    # FP64 work is authoritative): executed FP64 flops of one cfg3 build's
+    # assemble stage (every launch) from the committed ncu capture over this
+    # run's assemble time
     greens_roofline = None
     gpath = ROOT / "profiles" / "r02_greens_fp64.json"
     if greens_stage and gpath.exists() and args.config == 3 and fp64.value:
@@ -544,7 +545,8 @@ def run_ours(args):
             "bound": "fp64", "kernel": gj["kernel"], "achieved": ach, "peak": fp64.value, "unit": "TFLOP/s",
             "frac": ach / fp64.value, "fp64_pipe_active_pct_ncu": gj["fp64_pipe_active_pct"],
             "flops_per_launch": gj["fp64_flops_executed"],
-            "flops_how": "executed FP64 flops (2 DFMA + DADD + DMUL thread instructions, ncu) of one launch",
+            "flops_how": "executed FP64 flops (2 DFMA + DADD + DMUL thread instructions, ncu) of one build's "
+                         "assemble stage, all launches",
             "algorithmic": {"pair_lambda": p_alg, "flops": 140.0 * p_alg, "tflops": 140.0 * p_alg / t_as / 1e12,
                             "note": "SURVEY.md §8(d) estimate of the reference algorithm over all nx*ny offsets; "
                                     "the build computes the offsets oi <= oj (x<->y mirror) with five complex "
