@@ -28,6 +28,11 @@ a = ap.parse_args()
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+# library init as the bench does it, with the pool grown once up front: the
+# builds' image batches (2 GB), the Krylov bases (2 GB at restart 40) and the
+# operators otherwise make the stream-ordered pool map new memory mid-sweep
+# (up to ~0.9 s for one build)
+emie.warmup(reserve_bytes=8 << 30)
 dist = None
 if world > 1:
     import torch.distributed as dist
