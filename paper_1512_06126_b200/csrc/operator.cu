@@ -265,10 +265,58 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
 // (component b, kp) in steps of 4. Complex products use three real MMAs
 // (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi); re = P1 - P2, im = P3 - P1 - P2).
 // The zx / zy blocks (-xz^T, -yz^T) flip the sign bit of the B fragment.
+constexpr long long kSwapColPeer = 1LL << 60;  // = kSwapCol (below)
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// ---- staged peer epilogue (sharded apply): a mode's output columns are
+// assembled in its input-column stage -- free once every consumer warp has
+// finished the mode's MMAs -- in owner-major order (owner h's rows of the
+// three components, 3 (z[h+1] - z[h]) values, contiguous), then each
+// (column, owner) segment goes to the owner's spectrum in one bulk copy
+// shared -> global over NVLink instead of a 16-byte store per lane.
+__device__ __forceinline__ void consumers_sync(int nthreads) {  // named barrier 1: the consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// the owner of output row k: index h, first row z[h], rows pnz
+__device__ __forceinline__ void peer_owner(const PeerOut& po, int k, int& h, int& zh, int& pnz) {
+  h = 0;
+  while (h + 1 < po.G && k >= po.z[h + 1]) ++h;
+  zh = po.z[h];
+  pnz = po.z[h + 1] - zh;
+}
+// issue the staged columns of one mode (lane c < NC of one consumer warp: its
+// column's owner segments); with a stage shared with the input columns, wait
+// until the copies have read it (the producer refills it next), else the wait
+// comes before the stage's next use
+template <int NC, int np, int ldu>
+__device__ __forceinline__ void peer_push(const PeerOut& po, const long long* colbase, const cplx* stage, int lane,
+                                          bool wait_read) {
+  if (lane < NC) {
+    const long long cb = colbase[lane];
+    if (cb >= 0) {
+      const long long col = (cb & ~kSwapColPeer) / np;  // r E + mode
+      const cplx* src = stage + static_cast<size_t>(lane) * ldu;
+      for (int h = 0; h < po.G; ++h) {
+        const int zh = po.z[h], pnz = po.z[h + 1] - zh;
+        if (pnz > 0)
+          bulk_s2g(po.dst[h] + col * 3 * pnz, src + 3 * zh, static_cast<uint32_t>(3 * pnz * sizeof(cplx)));
+      }
+      bulk_commit();
+      if (wait_read) bulk_wait_read_all();
+    }
+  }
 }
 
 // mirror mi (0 .. nmir-1) of quadrant mode qm, in mode_cols order
@@ -298,7 +346,7 @@ constexpr int kBlkStagesOct = EMIE_CT_OCT_BST;  // 16-column stages leave SMEM f
 #endif
 constexpr int kL2Ahead = EMIE_CT_L2AHEAD;  // modes past the SMEM stages prefetched to L2
 // column-table flag: the column belongs to the transposed mode (x <-> y exchanged)
-constexpr long long kSwapCol = 1LL << 60;
+constexpr long long kSwapCol = kSwapColPeer;
 
 template <bool OCT>
 constexpr int ct_cols() { return OCT ? 16 : 8; }
@@ -412,13 +460,10 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   const int a_rt = warp / (NZ / 8), m = warp - a_rt * (NZ / 8);
   const int k = 4 * m + (fr >> 1) + (fr & 1) * (NZ / 2);
   // PEER: the slab owner of this lane's output row k
-  cplx* pdst = nullptr;
-  int pnz = 0;
+  int pzh = 0, pnz = 0;
   if constexpr (PEER) {
-    int h = 0;
-    while (h + 1 < po.G && k >= po.z[h + 1]) ++h;
-    pnz = po.z[h + 1] - po.z[h];
-    pdst = po.dst[h] + (k - po.z[h]) + a_rt * pnz;
+    int h;
+    peer_owner(po, k, h, pzh, pnz);
   }
   // The warp's component a is a template constant inside consume(): the
   // zx / zy negation (-xz^T, -yz^T: the z tile, b < 2) is then a compile-time
@@ -492,19 +537,54 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(bempty + bs);
+      if (PEER && po.G == 1) {
+        // one rank: the owner is this rank's own spectrum; 16-byte stores
+        // (staging only costs barriers here: 4,038 vs 3,694 applies/s)
+        constexpr int asw = a == 2 ? 2 : 1 - a;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
+        for (int g = 0; g < NG; ++g)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
-          if (cb >= 0) {
-            const cplx v = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
-            if constexpr (PEER) {
-              // cb = (r E + mode) * np; a transposed-mode column's row is in the exchanged third
-              const bool sw = OCT && (cb & kSwapCol);
-              constexpr int asw = a == 2 ? 2 : 1 - a;
-              pdst[((cb & ~kSwapCol) / (3 * NZ)) * (3 * pnz) + (sw ? (asw - a) * pnz : 0)] = v;
-            } else {
+          for (int h = 0; h < 2; ++h) {
+            const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
+            if (cb >= 0) {
+              const int ap = (OCT && (cb & kSwapCol)) ? asw : a;
+              po.dst[0][((cb & ~kSwapCol) / np) * np + ap * NZ + k] =
+                  cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
+            }
+          }
+      } else if constexpr (PEER) {
+        // several owners: the mode's outputs staged in SMEM (barrier: every
+        // consumer warp has finished the mode), then one bulk copy per
+        // (column, owner) over NVLink instead of a 16-byte store per lane; a
+        // transposed-mode column's row goes to the exchanged third.
+        // own stage (po.sep): the previous mode's copies must have read it
+        cplx* stage = ubuf + static_cast<size_t>(po.sep ? kUStages : us) * NC * ldu;
+        if (po.sep && warp == 0) bulk_wait_read_all();
+        consumers_sync(W * 32);
+        constexpr int asw = a == 2 ? 2 : 1 - a;
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = 8 * g + 2 * fc + h;
+            const long long cb = colbase[us * NC + c];
+            if (cb >= 0) {
+              const int ap = (OCT && (cb & kSwapCol)) ? asw : a;
+              stage[c * ldu + 3 * pzh + ap * pnz + (k - pzh)] =
+                  cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
+            }
+          }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the bulk reads
+        consumers_sync(W * 32);
+        if (warp == 0) peer_push<NC, np, ldu>(po, colbase + us * NC, stage, lane, !po.sep);
+      } else {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
+            if (cb >= 0) {
+              const cplx v = cplx{p1[g][h] - p2[g][h], p3[g][h] - p1[g][h] - p2[g][h]};
               const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? plane_sw : plane);
               S[o] = v;
             }
@@ -529,6 +609,9 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   if (a_rt == 0) consume(std::integral_constant<int, 0>{});
   else if (a_rt == 1) consume(std::integral_constant<int, 1>{});
   else consume(std::integral_constant<int, 2>{});
+  if constexpr (PEER) {
+    if (warp == 0) bulk_wait_all();  // the staged columns have landed in the owners' spectra
+  }
 }
 
 // ------------------------------ contraction, streamed row blocks (nz 48/64) -----
@@ -707,37 +790,47 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
         if (lane == 0) mbar_arrive(rempty + st);
       }
     }
+    // PEER: the input-column stage us becomes the output stage once every
+    // consumer warp has finished its K-chunks (barrier); rows in owner-major
+    // order, one bulk copy per (column, owner) (peer_push)
+    cplx* stage = ubuf + static_cast<size_t>(us) * NC * ldu;
+    const bool staged = PEER && po.G > 1;  // one rank: direct 16-byte stores into its own spectrum
+    if (staged) consumers_sync(W * 32);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int a = ta[i];
       const int rowc = trow[i];  // C row fr of the tile = the lane's A row
       const int plane = a * NZ + rowc;
       const int asw = a == 2 ? 2 : 1 - a;
-      cplx* pdst = nullptr;  // PEER: the slab owner of output row rowc
-      int pnz = 0;
+      int pzh = 0, pnz = 0;  // PEER: the slab owner of output row rowc
       if constexpr (PEER) {
-        int hh = 0;
-        while (hh + 1 < po.G && rowc >= po.z[hh + 1]) ++hh;
-        pnz = po.z[hh + 1] - po.z[hh];
-        pdst = po.dst[hh] + (rowc - po.z[hh]) + a * pnz;
+        int hh;
+        peer_owner(po, rowc, hh, pzh, pnz);
       }
 #pragma unroll
       for (int g = 0; g < NG; ++g)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const long long cb = colbase[us * NC + 8 * g + 2 * fc + h];
+          const int c = 8 * g + 2 * fc + h;
+          const long long cb = colbase[us * NC + c];
           if (cb >= 0) {
             const cplx v = cplx{p1[i][g][h] - p2[i][g][h], p3[i][g][h] - p1[i][g][h] - p2[i][g][h]};
             if constexpr (PEER) {
-              // cb = (r E + mode) * np; a transposed-mode column's row is in the exchanged third
-              const bool sw = OCT && (cb & kSwapCol);
-              pdst[((cb & ~kSwapCol) / np) * (3 * pnz) + (sw ? (asw - a) * pnz : 0)] = v;
+              // a transposed-mode column's row goes to the exchanged third
+              const int ap = (OCT && (cb & kSwapCol)) ? asw : a;
+              if (staged) stage[c * ldu + 3 * pzh + ap * pnz + (rowc - pzh)] = v;
+              else po.dst[0][((cb & ~kSwapCol) / np) * np + ap * NZ + rowc] = v;
             } else {
               const long long o = (cb & ~kSwapCol) + ((cb & kSwapCol) ? asw * NZ + rowc : plane);
               S[o] = v;
             }
           }
         }
+    }
+    if (staged) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the bulk reads
+      consumers_sync(W * 32);
+      if (warp == 0) peer_push<NC, np, ldu>(po, colbase + us * NC, stage, lane, true);
     }
     __syncwarp();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -751,6 +844,9 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
     const long long gc0 = static_cast<long long>(j) * NCH;
     if (OCT && colbase[us * NC + 8] >= 0) run(std::integral_constant<int, 2>{}, us, gc0);
     else run(std::integral_constant<int, 1>{}, us, gc0);
+  }
+  if constexpr (PEER) {
+    if (warp == 0) bulk_wait_all();  // the staged columns have landed in the owners' spectra
   }
 }
 
@@ -1001,9 +1097,21 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
       continue;
     }
     const int bst = oct ? ct_blk_stages<true>() : ct_blk_stages<false>();
-    const size_t smem = 128 + kUStages * nc * sizeof(long long) +
-                        bst * static_cast<size_t>(op.nentD) * sizeof(cplx) +
-                        kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+    size_t smem = 128 + kUStages * nc * sizeof(long long) + bst * static_cast<size_t>(op.nentD) * sizeof(cplx) +
+                  kUStages * nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+    // the staged epilogue's own output stage where SMEM allows (octant, nz <=
+    // 32: 209 KB), else it reuses the input-column stage
+    {
+      static const int optin = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        return v;
+      }();
+      const size_t extra = nc * static_cast<size_t>(np + 4) * sizeof(cplx);
+      pg.sep = smem + extra <= static_cast<size_t>(optin) ? 1 : 0;
+      if (pg.sep) smem += extra;
+    }
     auto launch = [&](auto kern, int warps) {
       const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
       const int grid = std::max(1, std::min(sms * per_sm, nwork));

@@ -132,6 +132,7 @@ struct PeerOut {
   int G = 0;
   cplx* dst[kMaxPeerRanks];
   int z[kMaxPeerRanks + 1];
+  int sep = 0;  // launcher-set: the staged epilogue has its own SMEM stage (else it reuses the input-column stage)
 };
 void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, int q1, const PeerOut& po,
                          cudaStream_t st);
