@@ -2211,7 +2211,7 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     Geom* gtab = scratch<Geom>(ncomp, st);
     EMIE_CUDA(cudaMemcpyAsync(gtab, gh.data(), ncomp * sizeof(Geom), cudaMemcpyHostToDevice, st));
     // the six kernels' design samples of every offset, transcendentals shared
-    // (filter_samples_kernel), in batches of at most 2^16 offsets
+    // (filter_samples_kernel), in batches
     // (EMIE_CU_GREENS_SHARED_SAMPLES=0: kernel_output per kernel, A/B and the
     // bit-identity test)
     static const bool shared_samples = [] {
@@ -2219,7 +2219,8 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
       return !(e && e[0] == '0');
     }();
     const int n = 2 * fp.half;
-    const int bmax = P.oc.compact ? ncomp : std::min(ncomp, 1 << 16);  // compact slots are positions: one batch
+    // batches of 4,096 offsets (200 MB of samples); compact slots are positions: one batch
+    const int bmax = P.oc.compact ? ncomp : std::min(ncomp, 4096);
     double* samp = shared_samples ? scratch<double>(static_cast<size_t>(bmax) * 6 * n, st) : nullptr;
     for (int i0 = 0; i0 < ncomp && !shared_samples; i0 += ncomp)
       design_filters(fb, fp, ncomp, P.oc, P.hx, P.hy, W, err, st, INT32_MIN, 0, offs, nullptr, 0, 6, nullptr, gtab);
