@@ -526,6 +526,7 @@ __global__ void __launch_bounds__(kStreamThreads, P::kStageBytes <= 16384 ? (NST
     stream_tma_kernel(const __grid_constant__ P p, const cplx* __restrict__ tw) {
   using G = Geo<N>;
   extern __shared__ __align__(1024) unsigned char smraw[];
+  pdl_trigger();
   cplx* stage[NST];
 #pragma unroll
   for (int b = 0; b < NST; ++b) stage[b] = reinterpret_cast<cplx*>(smraw + b * P::kStageBytes);
@@ -539,6 +540,7 @@ __global__ void __launch_bounds__(kStreamThreads, P::kStageBytes <= 16384 ? (NST
   }
   load_twiddles(tws, tw, N);
   __syncthreads();
+  pdl_wait();  // the previous kernel's outputs (this pass's input) are complete
   const int ntiles = p.ntiles();
   int tile = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -1101,7 +1103,7 @@ void launch_tma(const P& p, int ntiles, const cplx* tw, cudaStream_t st, const c
   const int per_sm =
       resident_ctas(reinterpret_cast<const void*>(stream_tma_kernel<N, P, NST>), kStreamThreads, smem);
   const int grid = std::max(1, std::min(ntiles, sm_count() * per_sm));
-  stream_tma_kernel<N, P, NST><<<grid, kStreamThreads, smem, st>>>(p, tw);
+  launch_pdl(stream_tma_kernel<N, P, NST>, grid, kStreamThreads, smem, st, p, tw);
   check_launch(what);
 }
 

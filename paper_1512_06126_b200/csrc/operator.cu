@@ -367,6 +367,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
     contract_mma_kernel(const cplx* __restrict__ op, const uint32_t* __restrict__ ctab, cplx* S,
                         int ex, int ey, int qx, int q0, int q1, int qbase, int nrhs, int nentD,
                         const int* __restrict__ octl, int noct, const __grid_constant__ PeerOut po) {
+  pdl_trigger();
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int nk = np / 4;
   constexpr int W = mma_warps<NZ>();
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__((mma_warps<NZ>() + 1) * 32, 1)
   // later TMA writes into ubuf (write, fence, barrier, then bulk copy)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  pdl_wait();  // the spectra S of the y pass are complete
   const int G = gridDim.x;
   const int nwork = OCT ? noct : q1 - q0;
 
@@ -644,6 +646,7 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
                          int ex, int ey, int qx, int q0, int q1,
                          int qbase, int nrhs, const int* __restrict__ octl, int noct,
                          const __grid_constant__ PeerOut po) {
+  pdl_trigger();
   constexpr int np = 3 * NZ, ldu = np + 4;
   constexpr int W = rows_warps<NZ>();
   constexpr int NC = ct_cols<OCT>();
@@ -677,6 +680,7 @@ __global__ void __launch_bounds__((rows_warps<NZ>() + 1) * 32, 1)
   // later TMA writes into ubuf (write, fence, barrier, then bulk copy)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  pdl_wait();  // the spectra S of the y pass are complete
   const int G = gridDim.x;
   const int nwork = OCT ? noct : q1 - q0;
 
@@ -989,7 +993,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
       auto launch = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
-        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, tmT, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
+        launch_pdl(kern, grid, (warps + 1) * 32, smem, st, tm, tmT, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase, g, op.octl,
                                                    op.noct, PeerOut{});
       };
       if (op.nz == 48) {
@@ -1013,7 +1017,7 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
       auto launch = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
-        kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
+        launch_pdl(kern, grid, (warps + 1) * 32, smem, st, op.spec, op.ctab, Sg, op.ex, op.ey, op.qx, q0, q1, op.qbase,
                                                    g, op.nentD, op.octl, op.noct, PeerOut{});
       };
       if (oct) {
@@ -1083,7 +1087,7 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
       auto launch_rows = [&](auto kern, int warps) {
         const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
         const int grid = std::max(1, std::min(sms * per_sm, nwork));
-        kern<<<grid, (warps + 1) * 32, smem, st>>>(tm, tmT, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1,
+        launch_pdl(kern, grid, (warps + 1) * 32, smem, st, tm, tmT, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0, q1,
                                                    op.qbase, g, op.octl, op.noct, pg);
       };
       if (op.nz == 48) {
@@ -1115,7 +1119,7 @@ void contract_modes_peer(const Operator& op, const cplx* S, int nrhs, int q0, in
     auto launch = [&](auto kern, int warps) {
       const int per_sm = resident_ctas(reinterpret_cast<const void*>(kern), (warps + 1) * 32, smem);
       const int grid = std::max(1, std::min(sms * per_sm, nwork));
-      kern<<<grid, (warps + 1) * 32, smem, st>>>(op.spec, op.ctab, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0,
+      launch_pdl(kern, grid, (warps + 1) * 32, smem, st, op.spec, op.ctab, const_cast<cplx*>(Sg), op.ex, op.ey, op.qx, q0,
                                                  q1, op.qbase, g, op.nentD, op.octl, op.noct, pg);
     };
     if (oct) {

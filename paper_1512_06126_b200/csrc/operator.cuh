@@ -1,6 +1,9 @@
 // Device-resident operator objects behind the C ABI (include/emie_cu.h).
 #pragma once
 
+#include <cstdlib>
+#include <utility>
+
 #include <algorithm>
 #include <cstddef>
 #include <cstdint>
@@ -128,6 +131,31 @@ void contract_modes(const Operator& op, cplx* S, int nrhs, int q0, int q1, cudaS
 // z[h] <= k < z[h+1], at dst[h][(r*E + m)*3nzh + a*nzh + k - z[h]]
 constexpr int kMaxPeerRanks = 64;
 constexpr int kRowsBlocks = 6;  // dense blocks per mode of the ROWS layout
+// launch with programmatic stream serialisation (the kernel calls
+// pdl_trigger / pdl_wait): it may start while the previous kernel of the
+// stream drains. EMIE_CU_PDL=0 launches plainly (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EMIE_CU_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 struct PeerOut {
   int G = 0;
   cplx* dst[kMaxPeerRanks];

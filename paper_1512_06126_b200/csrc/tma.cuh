@@ -8,6 +8,13 @@
 
 namespace emie_cu {
 
+// programmatic dependent launch: a kernel lets the next one in its stream
+// launch early (its CTAs take SMs as this kernel's CTAs retire and run their
+// prologue) and waits for the previous kernel's completion and memory before
+// touching global data that kernel may produce or read
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
