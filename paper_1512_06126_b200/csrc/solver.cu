@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kRedThreads) dots_kernel(const cplx* __restric
 constexpr int kFinThreads = 256;
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* partial, int nblocks, int pstride,
                                                                int nvals, double* out) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   if (i >= nvals) return;
   double s = 0.0;
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     cgs_tile_kernel(cplx* w, const cplx* V, std::size_t vstride, int nv,  // V: TMA source only (MODE 4 writes V[nv-1])
                     const double* __restrict__ h, std::size_t n, double* partial, int pstride, int with_norm,
                     cplx* Vlast = nullptr) {
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 2;
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // h and the vectors come from the previous kernels
   if (MODE == 1 || MODE == 2)
     for (int i = tid; i < 2 * nv; i += blockDim.x) hs[i] = h[i];
   if (MODE == 4)
@@ -388,6 +392,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
 // s1 = [a][alpha]
 __global__ void __launch_bounds__(32) dcgs_coef_kernel(const double* __restrict__ s, int nv, double* coef,
                                                        double* s0, double* s1) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x;
   const int jv = nv - 1;
   const double* a = s + 2 * nv + 1;
@@ -437,6 +443,8 @@ __global__ void scale_kernel(cplx* y, const cplx* __restrict__ x, double a, std:
 // y2 (optional): a second copy, the next round's apply batch slot
 __global__ void scale_by_norm_kernel(cplx* y, const cplx* __restrict__ x, const double* nrm2, std::size_t n,
                                      cplx* y2 = nullptr) {
+  pdl_trigger();
+  pdl_wait();
   const double s = *nrm2;
   const double a = s > 0.0 ? 1.0 / std::sqrt(s) : 0.0;
   for (std::size_t e = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
@@ -499,8 +507,8 @@ int cgs_launch(cplx* w, const cplx* V, std::size_t vstride, int nv, const double
   (void)resident_ctas(reinterpret_cast<const void*>(cgs_tile_kernel<MODE>), kCgsThreads, smem);
   const int G = static_cast<int>(std::max<std::size_t>(
       1, std::min<std::size_t>(kCgsBlocks, (n + kTE - 1) / kTE)));
-  cgs_tile_kernel<MODE><<<G, kCgsThreads, cgs_smem(nv), st>>>(w, V, vstride, nv, h, n, partial, pstride,
-                                                              with_norm, Vlast);
+  launch_pdl(cgs_tile_kernel<MODE>, G, kCgsThreads, cgs_smem(nv), st, w, V, vstride, nv, h, n, partial, pstride,
+             with_norm, Vlast);
   check_launch("cgs_tile_kernel");
   return G;
 }
@@ -536,13 +544,13 @@ struct Workspace {
   }
   // finalize partial sums; when norm_slot_src >= 0 the |w|^2 lives at 2*nv
   void finalize(int nvals, int) {
-    finalize_kernel<<<nvals, kFinThreads, 0, st>>>(partial, G, pstride, nvals, dvals);
+    launch_pdl(finalize_kernel, nvals, kFinThreads, 0, st, partial, G, pstride, nvals, dvals);
     check_launch("finalize_kernel");
   }
   double norm_of(const cplx* w) {
     dots_kernel<<<G, kRedThreads, 0, st>>>(w, 0, 0, w, n, partial, pstride, 1);
     check_launch("dots_kernel");
-    finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, G, pstride, 1, dvals);
+    launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, partial, G, pstride, 1, dvals);
     check_launch("finalize_kernel");
     fetch(1);
     return std::sqrt(hpin[0]);
@@ -753,7 +761,7 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
       if (!es[q].inner) {  // cie.cpp:217-229
         residual_kernel<<<ws.G, kRedThreads, 0, st>>>(R.r, R.b, w, n, ws.partial);
         check_launch("residual_kernel");
-        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, dv + 2 * ps);
+        launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, ws.partial, ws.G, 1, 1, dv + 2 * ps);
         check_launch("finalize_kernel");
         to_host(2, 1);
         continue;
@@ -765,14 +773,14 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
         // place, w projected) with the new |w|^2
         const int nv = j + 1;
         int g = cgs_launch<3>(w, R.V, n, nv, nullptr, n, ws.partial, ps, 0, st);
-        finalize_kernel<<<4 * nv, kFinThreads, 0, st>>>(ws.partial, g, ps, 4 * nv, dsum);
+        launch_pdl(finalize_kernel, 4 * nv, kFinThreads, 0, st, ws.partial, g, ps, 4 * nv, dsum);
         check_launch("finalize_kernel");
-        dcgs_coef_kernel<<<1, 32, 0, st>>>(dsum, nv, dcoef, dv, dv + ps);
+        launch_pdl(dcgs_coef_kernel, 1, 32, 0, st, dsum, nv, dcoef, dv, dv + ps);
         check_launch("dcgs_coef_kernel");
         to_host(0, 2 * nv + 1);
         to_host(1, 2 * nv - 1);
         g = cgs_launch<4>(w, R.V, n, nv, dcoef, n, ws.partial, 1, 0, st, R.V + static_cast<std::size_t>(j) * n);
-        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, g, 1, 1, dv + 2 * ps);
+        launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, ws.partial, g, 1, 1, dv + 2 * ps);
         check_launch("finalize_kernel");
         to_host(2, 1);
         continue;
@@ -780,23 +788,23 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
       // CGS2 pass 1: dots against v_0..v_j plus |w|^2, then w -= V h
       if (j + 1 <= kTileMaxV) {
         int g = cgs_launch<0>(w, R.V, n, j + 1, nullptr, n, ws.partial, ps, 1, st);
-        finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, g, ps, 2 * (j + 1) + 1, dv);
+        launch_pdl(finalize_kernel, 2 * (j + 1) + 1, kFinThreads, 0, st, ws.partial, g, ps, 2 * (j + 1) + 1, dv);
         check_launch("finalize_kernel");
         to_host(0, 2 * (j + 1) + 1);
         // w -= V h1 fused with the pass-2 dots, then w -= V h2 with the new norm
         g = cgs_launch<1>(w, R.V, n, j + 1, dv, n, ws.partial, ps, 0, st);
-        finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, g, ps, 2 * (j + 1), dv + ps);
+        launch_pdl(finalize_kernel, 2 * (j + 1), kFinThreads, 0, st, ws.partial, g, ps, 2 * (j + 1), dv + ps);
         check_launch("finalize_kernel");
         to_host(1, 2 * (j + 1));
         g = cgs_launch<2>(w, R.V, n, j + 1, dv + ps, n, ws.partial, 1, 0, st);
-        finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, g, 1, 1, dv + 2 * ps);
+        launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, ws.partial, g, 1, 1, dv + 2 * ps);
         check_launch("finalize_kernel");
         to_host(2, 1);
         continue;
       }
       dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 1);
       check_launch("dots_kernel");
-      finalize_kernel<<<2 * (j + 1) + 1, kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1) + 1, dv);
+      launch_pdl(finalize_kernel, 2 * (j + 1) + 1, kFinThreads, 0, st, ws.partial, ws.G, ps, 2 * (j + 1) + 1, dv);
       check_launch("finalize_kernel");
       to_host(0, 2 * (j + 1) + 1);
       update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv, n, nullptr);
@@ -804,12 +812,12 @@ void fgmres_map(const KrylovMap& A, const cplx* d_rhs, cplx* d_x, int nrhs, doub
       // pass 2, with the new |w|^2
       dots_kernel<<<ws.G, kRedThreads, 0, st>>>(R.V, n, j + 1, w, n, ws.partial, ps, 0);
       check_launch("dots_kernel");
-      finalize_kernel<<<2 * (j + 1), kFinThreads, 0, st>>>(ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
+      launch_pdl(finalize_kernel, 2 * (j + 1), kFinThreads, 0, st, ws.partial, ws.G, ps, 2 * (j + 1), dv + ps);
       check_launch("finalize_kernel");
       to_host(1, 2 * (j + 1));
       update_kernel<<<ws.G, kRedThreads, 0, st>>>(w, R.V, n, j + 1, dv + ps, n, ws.partial);
       check_launch("update_kernel");
-      finalize_kernel<<<1, kFinThreads, 0, st>>>(ws.partial, ws.G, 1, 1, dv + 2 * ps);
+      launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, ws.partial, ws.G, 1, 1, dv + 2 * ps);
       check_launch("finalize_kernel");
       to_host(2, 1);
     }
@@ -1019,7 +1027,7 @@ void vec_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, std::si
     check_launch("dots_kernel");
   }
   if (nvals > 0) {
-    finalize_kernel<<<nvals, kFinThreads, 0, st>>>(partial, g, ps, nvals, out);
+    launch_pdl(finalize_kernel, nvals, kFinThreads, 0, st, partial, g, ps, nvals, out);
     check_launch("finalize_kernel");
   }
   release(partial, st);
@@ -1031,7 +1039,7 @@ void vec_dcgs_dots(const cplx* V, std::size_t vstride, int nv, const cplx* w, st
   const int ps = 4 * nv + 4;
   double* partial = scratch<double>(static_cast<std::size_t>(kCgsBlocks) * ps, st);
   const int g = cgs_launch<3>(const_cast<cplx*>(w), V, vstride, nv, nullptr, n, partial, ps, 0, st);
-  finalize_kernel<<<4 * nv, kFinThreads, 0, st>>>(partial, g, ps, 4 * nv, out);
+  launch_pdl(finalize_kernel, 4 * nv, kFinThreads, 0, st, partial, g, ps, 4 * nv, out);
   check_launch("finalize_kernel");
   release(partial, st);
 }
@@ -1041,7 +1049,7 @@ void vec_dcgs_update(cplx* w, cplx* V, std::size_t vstride, int nv, const double
   if (nv < 1 || nv > kTileMaxV) fail(EMIE_CU_INVALID_ARGUMENT, "vec_dcgs_update: nv outside [1, 41]");
   double* partial = scratch<double>(kCgsBlocks, st);
   const int g = cgs_launch<4>(w, V, vstride, nv, coef, n, partial, 1, 0, st, V + (nv - 1) * vstride);
-  finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+  launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, partial, g, 1, 1, norm_out);
   check_launch("finalize_kernel");
   release(partial, st);
 }
@@ -1053,12 +1061,12 @@ void vec_update(cplx* w, const cplx* V, std::size_t vstride, int nv, const doubl
   const bool tiled = nv >= 1 && nv <= kTileMaxV;
   if (tiled && dots_out && !norm_out) {
     const int g = cgs_launch<1>(w, V, vstride, nv, h, n, partial, ps, 0, st);
-    finalize_kernel<<<2 * nv, kFinThreads, 0, st>>>(partial, g, ps, 2 * nv, dots_out);
+    launch_pdl(finalize_kernel, 2 * nv, kFinThreads, 0, st, partial, g, ps, 2 * nv, dots_out);
     check_launch("finalize_kernel");
   } else if (tiled && !dots_out) {
     const int g = cgs_launch<2>(w, V, vstride, nv, h, n, partial, 1, 0, st);
     if (norm_out) {
-      finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+      launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, partial, g, 1, 1, norm_out);
       check_launch("finalize_kernel");
     }
   } else {
@@ -1072,13 +1080,13 @@ void vec_update(cplx* w, const cplx* V, std::size_t vstride, int nv, const doubl
         dots_kernel<<<g, kRedThreads, 0, st>>>(w, 0, 0, w, n, partial, 1, 1);
         check_launch("dots_kernel");
       }
-      finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+      launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, partial, g, 1, 1, norm_out);
       check_launch("finalize_kernel");
     }
     if (dots_out && nv > 0) {
       dots_kernel<<<g, kRedThreads, 0, st>>>(V, vstride, nv, w, n, partial, ps, 0);
       check_launch("dots_kernel");
-      finalize_kernel<<<2 * nv, kFinThreads, 0, st>>>(partial, g, ps, 2 * nv, dots_out);
+      launch_pdl(finalize_kernel, 2 * nv, kFinThreads, 0, st, partial, g, ps, 2 * nv, dots_out);
       check_launch("finalize_kernel");
     }
   }
@@ -1102,7 +1110,7 @@ void vec_residual(cplx* r, const cplx* b, const cplx* t, std::size_t n, double* 
   double* partial = scratch<double>(static_cast<std::size_t>(g), st);
   residual_kernel<<<g, kRedThreads, 0, st>>>(r, b, t, n, partial);
   check_launch("residual_kernel");
-  finalize_kernel<<<1, kFinThreads, 0, st>>>(partial, g, 1, 1, norm_out);
+  launch_pdl(finalize_kernel, 1, kFinThreads, 0, st, partial, g, 1, 1, norm_out);
   check_launch("finalize_kernel");
   release(partial, st);
 }
