@@ -1041,6 +1041,7 @@ struct SpyStream {
   cplx* spec;
   const int2* emap;
   int ny, qx, qy, nent, ntri, nfull, nchunks, nentD, qbase, qcount, nin;
+  int mirror;  // store the second slot of a symmetric entry here (else mirror_fill_kernel does, coalesced)
   uint32_t box_bytes;
   struct Ops {
     int mx, e0;
@@ -1071,10 +1072,31 @@ struct SpyStream {
       const int2 m = __ldg(emap + e);
       cplx* blk = spec + static_cast<size_t>(qm - qbase) * nentD;
       gst(blk + m.x, v);
-      if (m.y >= 0) gst(blk + m.y, v);
+      if (mirror && m.y >= 0) gst(blk + m.y, v);
     }
   }
 };
+
+// Row-block layout (nz 48 / 64): the lower triangles of the symmetric dense
+// blocks (xx yy zz xy) of every stored mode, from their upper triangles --
+// one (mode, component) block per CTA through SMEM, so the y pass writes
+// only the upper triangles row by row and the transposed copies leave here
+// in whole rows instead of one 16-byte store per entry a row apart (the
+// scattered stores cost config 4's y pass 38 ms for 26 GB)
+__global__ void __launch_bounds__(256) mirror_fill_kernel(cplx* spec, int nz, int nentD) {
+  extern __shared__ cplx tile[];  // nz x (nz + 1)
+  cplx* blk = spec + static_cast<size_t>(blockIdx.x >> 2) * nentD + static_cast<size_t>(blockIdx.x & 3) * nz * nz;
+  const int n2 = nz * nz, ld = nz + 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const int k = i / nz, kp = i - k * nz;
+    if (kp > k) tile[k * ld + kp] = blk[i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const int r = i / nz, c = i - r * nz;  // lower entry (r, c), c < r, = upper (c, r)
+    if (c < r) blk[i] = tile[c * ld + r];
+  }
+}
 
 int per_tile(int n) { return std::max(1, kTileElems / std::max(1, n)); }
 
@@ -1197,6 +1219,7 @@ void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) 
     p.spec = op.spec; p.emap = op.emap;
     p.ny = op.ny; p.qx = op.qx; p.qy = op.qy; p.nent = nent; p.ntri = op.ntri; p.nfull = op.nfull;
     p.nchunks = ceil_div(nent, TR); p.nentD = op.nentD; p.qbase = op.qbase; p.qcount = op.qcount; p.nin = op.ey;
+    p.mirror = op.rows ? 0 : 1;
     p.box_bytes = static_cast<uint32_t>(2 * TR * op.ny * sizeof(double));
     const uint64_t dims[3] = {2ull * nent, static_cast<uint64_t>(op.qx), static_cast<uint64_t>(op.ny)};
     const uint64_t strides[2] = {static_cast<uint64_t>(nent) * 16, static_cast<uint64_t>(op.qx) * nent * 16};
@@ -1204,6 +1227,12 @@ void lateral_spectra(const Operator& op, const cplx* d_blocks, cudaStream_t st) 
     encode_tensor_map_f64(&p.tm, R, 3, dims, strides, box, w ? 64 : 128);
     if (w) launch_tma<512, SpyStream, 1>(p, op.qx * p.nchunks, op.tw_y, st, "stream_tma_spectra_y");
     else launch_tma<256, SpyStream, 1>(p, op.qx * p.nchunks, op.tw_y, st, "stream_tma_spectra_y");
+    if (op.rows && op.qcount > 0) {
+      const size_t smem = static_cast<size_t>(op.nz) * (op.nz + 1) * sizeof(cplx);
+      set_smem(reinterpret_cast<const void*>(mirror_fill_kernel), smem);
+      mirror_fill_kernel<<<op.qcount * 4, 256, smem, st>>>(op.spec, op.nz, op.nentD);
+      check_launch("mirror_fill_kernel");
+    }
   } else {
     const bool p2 = op.p2y;
     const FftPlan& pl = p2 ? op.plan_y2 : op.plan_y;
