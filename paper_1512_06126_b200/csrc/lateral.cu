@@ -1087,9 +1087,20 @@ __global__ void __launch_bounds__(256) mirror_fill_kernel(cplx* spec, int nz, in
   extern __shared__ cplx tile[];  // nz x (nz + 1)
   cplx* blk = spec + static_cast<size_t>(blockIdx.x >> 2) * nentD + static_cast<size_t>(blockIdx.x & 3) * nz * nz;
   const int n2 = nz * nz, ld = nz + 1;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+  // all of a thread's upper-triangle loads in flight at once (nz <= 64: 16 per thread)
+  constexpr int kPer = 16;
+  cplx v[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int i = threadIdx.x + q * 256;
     const int k = i / nz, kp = i - k * nz;
-    if (kp > k) tile[k * ld + kp] = blk[i];
+    if (i < n2 && kp > k) v[q] = blk[i];
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int i = threadIdx.x + q * 256;
+    const int k = i / nz, kp = i - k * nz;
+    if (i < n2 && kp > k) tile[k * ld + kp] = v[q];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
