@@ -604,7 +604,11 @@ struct Half {
 struct FxStream {
   static constexpr bool kInverse = false, kTFast = true;
   static constexpr int kRowBytes = 8 * 128 * 16;     // 8 rows of <= 128 points (N = 256) or 4 of <= 256 (N = 512)
-  static constexpr int kStageBytes = 2 * kRowBytes;  // u rows, then the matching r2 rows
+#ifndef EMIE_FX_STAGE_R2
+#define EMIE_FX_STAGE_R2 1  // 0: r2 by per-thread loads, 16 KB stages (two per CTA at three CTAs per SM)
+#endif
+  static constexpr bool kStageR2 = EMIE_FX_STAGE_R2;
+  static constexpr int kStageBytes = (kStageR2 ? 2 : 1) * kRowBytes;  // u rows, then the matching r2 rows
   const cplx* u;
   const cplx* r2;
   cplx* T;
@@ -657,9 +661,9 @@ struct FxStream {
     constexpr int RT = Geo<N>::ntr;
     const int pr = tile / tpp, iy0 = (tile - pr * tpp) * RT;
     const uint32_t bytes = static_cast<uint32_t>(min(RT, ny - iy0) * nx) * sizeof(cplx);
-    mbar_expect_tx(bar, r2 ? 2 * bytes : bytes);
+    mbar_expect_tx(bar, r2 && r2_staged ? 2 * bytes : bytes);
     bulk_g2s(stg, u + (static_cast<size_t>(pr) * ny + iy0) * nx, bytes, bar);
-    if (r2) {
+    if (r2 && r2_staged) {
       const int iz = (pr % np) % nz;
       bulk_g2s(stg + kRowBytes / sizeof(cplx), r2 + (static_cast<size_t>(iz) * ny + iy0) * nx, bytes, bar);
     }
@@ -667,7 +671,7 @@ struct FxStream {
   template <int N>
   __device__ cplx staged(const cplx* stg, int t, int jj) const {
     const cplx x = stg[t * nx + jj];
-    return r2 ? stg[kRowBytes / sizeof(cplx) + t * nx + jj] * x : x;
+    return r2 && r2_staged ? stg[kRowBytes / sizeof(cplx) + t * nx + jj] * x : x;
   }
   // T[r][mx][plane][iy]: lanes t (= iy) fastest, 128 B runs per mx
   template <int N>
@@ -1129,6 +1133,12 @@ void launch_stream_n(const P& p, int ntiles, const cplx* tw, cudaStream_t st) {
 #ifndef EMIE_TMA_NST_FWD
 #define EMIE_TMA_NST_FWD 1
 #endif
+#ifndef EMIE_TMA_NST_FX
+#define EMIE_TMA_NST_FX EMIE_TMA_NST_FWD
+#endif
+#ifndef EMIE_TMA_NST_FY
+#define EMIE_TMA_NST_FY EMIE_TMA_NST_FWD
+#endif
 template <int N, class P, int NST>
 void launch_tma(const P& p, int ntiles, const cplx* tw, cudaStream_t st, const char* what) {
   const size_t smem = NST * static_cast<size_t>(P::kStageBytes) +
@@ -1275,9 +1285,9 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.u = d_in; p.r2 = r2; p.T = T;
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
-    p.r2_staged = op.ex == 256 || op.ex == 512;
-    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
-    else if (op.ex == 512) launch_tma<512, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    p.r2_staged = FxStream::kStageR2 && (op.ex == 256 || op.ex == 512);
+    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FX>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    else if (op.ex == 512) launch_tma<512, FxStream, EMIE_TMA_NST_FX>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
     else launch_stream(p, p.nplanes * p.tpp, op.tw_x, op.ex, st, "stream_fx");
   } else {
     const bool p2 = op.p2x;
@@ -1301,8 +1311,8 @@ void lateral_forward(const Operator& op, const cplx* d_in, const cplx* r2, cplx*
     p.T = T; p.S = S;
     p.ny = op.ny; p.ex = op.ex; p.ey = op.ey; p.nz = op.nz; p.np = np;
     p.gpc = ceil_div(np, kStreamElems / op.ey); p.nrhs = nrhs; p.nin = op.ny;
-    if (op.ey == 256) launch_tma<256, FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
-    else if (op.ey == 512) launch_tma<512, FyStream, EMIE_TMA_NST_FWD>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
+    if (op.ey == 256) launch_tma<256, FyStream, EMIE_TMA_NST_FY>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
+    else if (op.ey == 512) launch_tma<512, FyStream, EMIE_TMA_NST_FY>(p, nrhs * op.ex * p.gpc, op.tw_y, st, "stream_tma_fy");
     else launch_stream(p, nrhs * op.ex * p.gpc, op.tw_y, op.ey, st, "stream_fy");
   } else {
     const bool p2 = op.p2y;
@@ -1338,9 +1348,9 @@ void lateral_forward_peer(const Operator& op, const cplx* d_in, const cplx* r2, 
     p.u = d_in; p.r2 = r2; p.T = T;
     p.nx = op.nx; p.ny = op.ny; p.nz = op.nz; p.np = np; p.ex = op.ex;
     p.tpp = ceil_div(op.ny, kStreamElems / op.ex); p.nplanes = nrhs * np; p.nin = op.nx;
-    p.r2_staged = true;
-    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
-    else launch_tma<512, FxStream, EMIE_TMA_NST_FWD>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    p.r2_staged = FxStream::kStageR2;
+    if (op.ex == 256) launch_tma<256, FxStream, EMIE_TMA_NST_FX>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
+    else launch_tma<512, FxStream, EMIE_TMA_NST_FX>(p, p.nplanes * p.tpp, op.tw_x, st, "stream_tma_fx");
   }
   FyPeerStream p{};
   p.T = T; p.S = nullptr;
