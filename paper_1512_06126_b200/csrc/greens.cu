@@ -24,6 +24,7 @@
 #include <complex>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "layered.cuh"
@@ -885,6 +886,32 @@ constexpr int kImgThreads = EMIE_GREEN_IMG_THREADS;
 #endif
 constexpr int kImgLambdas = EMIE_GREEN_IMG_LAMBDAS;  // lambdas per chunk_image_kernel CTA (nz > 32)
 constexpr size_t kImgBudget = size_t{2} << 30;       // bytes of chunk images per batch (cfg3: 1 / 2 / 4 GB -> 31.6 / 30.1 / 29.7 ms)
+// image kernel of batch i + 1 overlapped with the pair kernel of batch i on a
+// second stream (EMIE_CU_GREENS_OVERLAP=0: serial, A/B)
+inline bool greens_overlap_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EMIE_CU_GREENS_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// the pair kernels' stream and its events, per build (builds may run on
+// several host threads and devices); destroying them right after the build
+// is enqueued is safe: the runtime releases them once their work completes
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[4] = {};
+  AuxStream() {
+    EMIE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto& e : ev) EMIE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~AuxStream() {
+    for (auto& e : ev) (void)cudaEventDestroy(e);
+    (void)cudaStreamDestroy(s);
+  }
+  AuxStream(const AuxStream&) = delete;
+  AuxStream& operator=(const AuxStream&) = delete;
+};
 // chunk images shared by offsets at equal R (EMIE_CU_GREENS_RSHARE=0: one per offset, A/B)
 inline bool img_share_enabled() {
   static const bool on = [] {
@@ -2336,25 +2363,56 @@ void assemble_codes(const GreenParams& P0, const std::vector<Interval>& ivh, con
     EMIE_CUDA(cudaMemcpyAsync(dRrep, Rrep.data(), nu * sizeof(double), cudaMemcpyHostToDevice, st));
     EMIE_CUDA(cudaMemcpyAsync(dreps, reps.data(), nu * sizeof(int), cudaMemcpyHostToDevice, st));
     EMIE_CUDA(cudaMemcpyAsync(dimg, img_h.data(), ncomp * sizeof(int), cudaMemcpyHostToDevice, st));
-    const int maxu = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / per_off)));
+    // Two image buffers (each half the budget): the image kernel of batch
+    // i + 1 runs on st while the pair kernel of batch i runs on a second
+    // stream, so neither kernel's tail drains the GPU between batches
+    // (EMIE_CU_GREENS_OVERLAP=0: one buffer, one stream, A/B)
+    const int nbuf = greens_overlap_enabled() ? 2 : 1;
+    const int maxu = static_cast<int>(std::min<size_t>(65535, std::max<size_t>(1, budget / nbuf / per_off)));
     const int nbatch = ceil_div(nu, maxu), ubatch = ceil_div(nu, nbatch);
-    cplx* IF = scratch<cplx>(static_cast<size_t>(ubatch) * fper, st);
-    int* IE = scratch<int>(static_cast<size_t>(ubatch) * estride, st);
+    cplx* IF[2] = {nullptr, nullptr};
+    int* IE[2] = {nullptr, nullptr};
+    for (int k = 0; k < std::min(nbuf, nbatch); ++k) {
+      IF[k] = scratch<cplx>(static_cast<size_t>(ubatch) * fper, st);
+      IE[k] = scratch<int>(static_cast<size_t>(ubatch) * estride, st);
+    }
+    cudaStream_t pst = st;
+    std::unique_ptr<AuxStream> aux;
+    auto aux_event = [&](int e) { return aux->ev[e]; };
+    if (nbuf == 2 && nbatch > 1) {
+      aux = std::make_unique<AuxStream>();
+      pst = aux->s;
+      EMIE_CUDA(cudaEventRecord(aux_event(2), st));  // the pair stream starts behind everything queued on st
+      EMIE_CUDA(cudaStreamWaitEvent(pst, aux_event(2), 0));
+    }
     int b0 = 0;
-    for (int u0 = 0; u0 < nu; u0 += ubatch) {
+    for (int u0 = 0, i = 0; u0 < nu; u0 += ubatch, ++i) {
       const int u1 = std::min(nu, u0 + ubatch);
+      const int k = pst == st ? 0 : i & 1;
       int b1 = b0;
       while (b1 < ncomp && img_h[b1] < u1) ++b1;  // the offsets of images [u0, u1)
-      chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), u1 - u0), kImgThreads, smemA, st>>>(P, div, dreps + u0, LA, IF,
-                                                                                          IE, estride, dRrep + u0);
+      if (pst != st && i >= 2) EMIE_CUDA(cudaStreamWaitEvent(st, aux_event(k), 0));  // pair kernel i - 2 read buffer k
+      chunk_image_kernel<<<dim3(ceil_div(P.nw, LA), u1 - u0), kImgThreads, smemA, st>>>(P, div, dreps + u0, LA, IF[k],
+                                                                                          IE[k], estride, dRrep + u0);
       check_launch("chunk_image_kernel");
-      assemble_kernel<false, true><<<dim3(b1 - b0, groups), kGreenThreads, smemB, st>>>(
-          PB, div, W, blocks, err, offs + b0, b0, IF, IE, estride, dimg + b0, u0, dRoff + b0);
+      if (pst != st) {
+        EMIE_CUDA(cudaEventRecord(aux_event(3), st));
+        EMIE_CUDA(cudaStreamWaitEvent(pst, aux_event(3), 0));
+      }
+      assemble_kernel<false, true><<<dim3(b1 - b0, groups), kGreenThreads, smemB, pst>>>(
+          PB, div, W, blocks, err, offs + b0, b0, IF[k], IE[k], estride, dimg + b0, u0, dRoff + b0);
       check_launch("assemble_kernel");
+      if (pst != st) EMIE_CUDA(cudaEventRecord(aux_event(k), pst));
       b0 = b1;
     }
-    release(IF, st);
-    release(IE, st);
+    if (pst != st) {  // join: st resumes behind the last pair kernel
+      EMIE_CUDA(cudaEventRecord(aux_event(2), pst));
+      EMIE_CUDA(cudaStreamWaitEvent(st, aux_event(2), 0));
+    }
+    for (int k = 0; k < 2; ++k) {
+      release(IF[k], st);
+      release(IE[k], st);
+    }
     release(dreps, st);
     release(dimg, st);
     release(dRrep, st);
